@@ -1,0 +1,327 @@
+"""ctypes binding of the CPU oracle (oracle/tango_oracle.c).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference leg may import this module.  The product path
+(paper_2308_00890_b200) never imports it.
+
+``build()`` compiles liboracle.so with gcc (-O2 -ffp-contract=off
+-fno-fast-math -fopenmp) next to the C source.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "tango_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fno-finite-math-only",
+          "-fopenmp", "-fPIC", "-shared", "-Wall", "-Wno-unknown-pragmas"]
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class Graph(C.Structure):
+    _fields_ = [("n", C.c_int64), ("e", C.c_int64), ("in_ptr", C.c_void_p), ("in_src", C.c_void_p),
+                ("chunk", C.c_int32)]
+
+
+class QRef(C.Structure):
+    _fields_ = [("q", C.c_void_p), ("v", C.c_void_p), ("s", C.c_float)]
+
+
+class Cfg(C.Structure):
+    _fields_ = [("F", C.c_int32), ("H", C.c_int32), ("D", C.c_int32), ("slope", C.c_float),
+                ("bits", C.c_int32), ("seed", C.c_uint64), ("step", C.c_uint32), ("layer_id", C.c_uint32)]
+
+
+_P = C.c_void_p
+_FWD_FIELDS = ["qH", "sH", "qW", "sW", "maxacc", "Hp", "S", "Dd", "qHp", "sHp", "qS", "sS", "qD", "sD",
+               "e_pre", "alpha", "m", "den", "Hout", "amax_out"]
+_BWD_FIELDS = ["qG", "sG", "dalpha", "P", "dE", "dE_pre", "dD", "dS", "dHp_agg", "dHp", "da_src", "da_dst",
+               "da_src_abs", "da_dst_abs", "qdHp", "sdHp", "dH", "dW"]
+_GCN_FWD_FIELDS = ["qX", "sX", "qW", "sW", "Ys", "qYs", "sYs", "ia", "out"]
+_GCN_BWD_FIELDS = ["Gs", "qGs", "sGs", "ib", "dY", "qdY", "sdY", "dX", "dW"]
+
+
+class FwdOut(C.Structure):
+    _fields_ = [(f, _P) for f in _FWD_FIELDS]
+
+
+class BwdOut(C.Structure):
+    _fields_ = [(f, _P) for f in _BWD_FIELDS]
+
+
+class GcnFwdOut(C.Structure):
+    _fields_ = [(f, _P) for f in _GCN_FWD_FIELDS]
+
+
+class GcnBwdOut(C.Structure):
+    _fields_ = [(f, _P) for f in _GCN_BWD_FIELDS]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        L = _lib
+        L.orc_philox4x32_10.argtypes = [_P, _P, _P]
+        L.orc_sr_uniform.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64]
+        L.orc_sr_uniform.restype = C.c_float
+        L.orc_quantize.argtypes = [_P, C.c_int64, C.c_int, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int64, _P,
+                                   _P, _P, _P]
+        L.orc_exp_p.argtypes = [C.c_float]
+        L.orc_exp_p.restype = C.c_float
+        L.orc_sddmm_add.argtypes = [C.POINTER(Graph), C.c_int, QRef, QRef, C.c_float, _P, _P]
+        L.orc_edge_softmax.argtypes = [C.POINTER(Graph), C.c_int, _P, _P, _P, _P]
+        L.orc_spmm_alpha.argtypes = [C.POINTER(Graph), C.c_int, C.c_int, C.c_int, _P, QRef, _P]
+        L.orc_sddmm_dot.argtypes = [C.POINTER(Graph), C.c_int, C.c_int, QRef, QRef, _P]
+        L.orc_softmax_bwd.argtypes = [C.POINTER(Graph), C.c_int, _P, _P, _P, C.c_float, _P, _P, _P]
+        L.orc_edge_sum.argtypes = [C.POINTER(Graph), C.c_int, C.c_int, _P, _P]
+        L.orc_spmm_sum.argtypes = [C.POINTER(Graph), C.c_int, C.c_int, QRef, _P, _P]
+        L.orc_gemm.argtypes = [C.c_int64, C.c_int64, C.c_int64, QRef, C.c_int64, C.c_int, QRef, C.c_int64, C.c_int,
+                               _P, _P]
+        L.orc_gat_fwd.argtypes = [C.POINTER(Graph), C.POINTER(Cfg), _P, _P, _P, _P, C.POINTER(FwdOut)]
+        L.orc_gat_bwd.argtypes = [C.POINTER(Graph), C.POINTER(Cfg), _P, _P, _P, C.POINTER(FwdOut), _P, _P,
+                                  C.POINTER(BwdOut)]
+        L.orc_gcn_fwd.argtypes = [C.POINTER(Graph), C.POINTER(Cfg), _P, _P, C.POINTER(GcnFwdOut)]
+        L.orc_gcn_bwd.argtypes = [C.POINTER(Graph), C.POINTER(Cfg), _P, _P, C.POINTER(GcnFwdOut), _P,
+                                  C.POINTER(GcnBwdOut)]
+        L.orc_num_threads.restype = C.c_int
+        L.orc_set_threads.argtypes = [C.c_int]
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _check(st):
+    if st != 0:
+        raise OracleError(f"oracle status {st}")
+
+
+def set_threads(t: int):
+    lib().orc_set_threads(int(t))
+
+
+def num_threads() -> int:
+    return lib().orc_num_threads()
+
+
+# ------------------------------------------------------------------ primitives
+def philox(ctr, key):
+    c = _c(ctr, np.uint32)
+    k = _c(key, np.uint32)
+    out = np.zeros(4, np.uint32)
+    lib().orc_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def sr_uniform(seed, step, tag, g) -> float:
+    return float(lib().orc_sr_uniform(seed, step, tag, g))
+
+
+def quantize(x, bits=8, seed=0, step=0, tag=0, g0=0, amax=None):
+    x = _c(x, np.float32)
+    q = np.zeros(x.shape, np.int8)
+    s = np.zeros(1, np.float32)
+    am = np.zeros(1, np.float32)
+    amin = None if amax is None else np.array([amax], np.float32)
+    st = lib().orc_quantize(_p(x), x.size, bits, seed, step, tag, g0, _p(amin), _p(q), _p(s), _p(am))
+    _check(st)
+    return q, np.float32(s[0]), np.float32(am[0])
+
+
+def exp_p(x: float) -> np.float32:
+    return np.float32(lib().orc_exp_p(float(np.float32(x))))
+
+
+def graph_struct(g, chunk=256):
+    in_ptr = _c(g.in_ptr, np.int64)
+    in_src = _c(g.in_src, np.int32)
+    gs = Graph(g.n, in_src.shape[0], in_ptr.ctypes.data, in_src.ctypes.data, chunk)
+    gs._keep = (in_ptr, in_src)
+    return gs
+
+
+def qref(q=None, v=None, s=1.0):
+    """Codes q (int8) with scale s, or bypass fp32 values v (s = 1)."""
+    if q is not None:
+        q = _c(q, np.int8)
+        r = QRef(q.ctypes.data, None, float(s))
+        r._keep = q
+    else:
+        v = _c(v, np.float32)
+        r = QRef(None, v.ctypes.data, float(s))
+        r._keep = v
+    return r
+
+
+def sddmm_add(g, heads, S: QRef, D: QRef, slope, chunk=256):
+    gs = graph_struct(g, chunk)
+    e_pre = np.zeros((g.e, heads), np.float32)
+    el = np.zeros((g.e, heads), np.float32)
+    lib().orc_sddmm_add(C.byref(gs), heads, S, D, slope, _p(e_pre), _p(el))
+    return e_pre, el
+
+
+def edge_softmax(g, heads, el, chunk=256):
+    gs = graph_struct(g, chunk)
+    el = _c(el, np.float32)
+    m = np.zeros((g.n, heads), np.float32)
+    den = np.zeros((g.n, heads), np.float32)
+    alpha = np.zeros((g.e, heads), np.float32)
+    lib().orc_edge_softmax(C.byref(gs), heads, _p(el), _p(m), _p(den), _p(alpha))
+    return m, den, alpha
+
+
+def spmm_alpha(g, direction, heads, cols, alpha, X: QRef, chunk=256):
+    gs = graph_struct(g, chunk)
+    alpha = _c(alpha, np.float32)
+    out = np.zeros((g.n, cols), np.float32)
+    _check(lib().orc_spmm_alpha(C.byref(gs), direction, heads, cols, _p(alpha), X, _p(out)))
+    return out
+
+
+def sddmm_dot(g, heads, cols, A: QRef, B: QRef, chunk=256):
+    gs = graph_struct(g, chunk)
+    out = np.zeros((g.e, heads), np.float32)
+    lib().orc_sddmm_dot(C.byref(gs), heads, cols, A, B, _p(out))
+    return out
+
+
+def softmax_bwd(g, heads, alpha, dalpha, e_pre, slope, chunk=256):
+    gs = graph_struct(g, chunk)
+    alpha, dalpha, e_pre = (_c(a, np.float32) for a in (alpha, dalpha, e_pre))
+    P = np.zeros((g.n, heads), np.float32)
+    dE = np.zeros((g.e, heads), np.float32)
+    dEp = np.zeros((g.e, heads), np.float32)
+    lib().orc_softmax_bwd(C.byref(gs), heads, _p(alpha), _p(dalpha), _p(e_pre), slope, _p(P), _p(dE), _p(dEp))
+    return P, dE, dEp
+
+
+def edge_sum(g, direction, heads, x, chunk=256):
+    gs = graph_struct(g, chunk)
+    x = _c(x, np.float32)
+    out = np.zeros((g.n, heads), np.float32)
+    _check(lib().orc_edge_sum(C.byref(gs), direction, heads, _p(x), _p(out)))
+    return out
+
+
+def spmm_sum(g, direction, cols, X: QRef, chunk=256):
+    gs = graph_struct(g, chunk)
+    oi = np.zeros((g.n, cols), np.int32)
+    of = np.zeros((g.n, cols), np.float32)
+    _check(lib().orc_spmm_sum(C.byref(gs), direction, cols, X, _p(oi), _p(of)))
+    return oi, of
+
+
+def gemm(A: QRef, B: QRef, M, N, K, lda, ldb, transA=False, transB=False):
+    acc64 = np.zeros((M, N), np.int64)
+    accf = np.zeros((M, N), np.float32)
+    lib().orc_gemm(M, N, K, A, lda, int(transA), B, ldb, int(transB), _p(acc64), _p(accf))
+    return acc64, accf
+
+
+# ------------------------------------------------------------------ layers
+def _cfg(F, H, D, slope, bits, seed, step, layer_id):
+    return Cfg(F, H, D, slope, bits, seed, step, layer_id)
+
+
+def gat_fwd(g, H, W, a_src, a_dst, heads, head_dim, slope=0.2, bits=8, seed=0x7A4E60, step=0, layer_id=0,
+            chunk=256):
+    n, F = H.shape
+    HD = heads * head_dim
+    E = g.e
+    gs = graph_struct(g, chunk)
+    cfg = _cfg(F, heads, head_dim, slope, bits, seed, step, layer_id)
+    H, W, a_src, a_dst = (_c(a, np.float32) for a in (H, W, a_src, a_dst))
+    o = dict(qH=np.zeros((n, F), np.int8), sH=np.zeros(1, np.float32), qW=np.zeros((F, HD), np.int8),
+             sW=np.zeros(1, np.float32), maxacc=np.zeros(1, np.int32), Hp=np.zeros((n, HD), np.float32),
+             S=np.zeros((n, heads), np.float32), Dd=np.zeros((n, heads), np.float32),
+             qHp=np.zeros((n, HD), np.int8), sHp=np.zeros(1, np.float32), qS=np.zeros((n, heads), np.int8),
+             sS=np.zeros(1, np.float32), qD=np.zeros((n, heads), np.int8), sD=np.zeros(1, np.float32),
+             e_pre=np.zeros((E, heads), np.float32), alpha=np.zeros((E, heads), np.float32),
+             m=np.zeros((n, heads), np.float32), den=np.zeros((n, heads), np.float32),
+             Hout=np.zeros((n, HD), np.float32), amax_out=np.zeros(1, np.float32))
+    st = FwdOut(*[_p(o[f]) for f in _FWD_FIELDS])
+    _check(lib().orc_gat_fwd(C.byref(gs), C.byref(cfg), _p(H), _p(W), _p(a_src), _p(a_dst), C.byref(st)))
+    o["_struct"] = st
+    o["_cfg"] = dict(F=F, heads=heads, head_dim=head_dim, slope=slope, bits=bits, seed=seed, step=step,
+                     layer_id=layer_id, chunk=chunk)
+    return o
+
+
+def gat_bwd(g, fwd, H, W, a_src, a_dst, dHout):
+    c = fwd["_cfg"]
+    n, F = H.shape
+    heads, hd = c["heads"], c["head_dim"]
+    HD = heads * hd
+    E = g.e
+    gs = graph_struct(g, c["chunk"])
+    cfg = _cfg(F, heads, hd, c["slope"], c["bits"], c["seed"], c["step"], c["layer_id"])
+    H, W, a_src, a_dst, dHout = (_c(a, np.float32) for a in (H, W, a_src, a_dst, dHout))
+    o = dict(qG=np.zeros((n, HD), np.int8), sG=np.zeros(1, np.float32), dalpha=np.zeros((E, heads), np.float32),
+             P=np.zeros((n, heads), np.float32), dE=np.zeros((E, heads), np.float32),
+             dE_pre=np.zeros((E, heads), np.float32), dD=np.zeros((n, heads), np.float32),
+             dS=np.zeros((n, heads), np.float32), dHp_agg=np.zeros((n, HD), np.float32),
+             dHp=np.zeros((n, HD), np.float32), da_src=np.zeros(HD, np.float32), da_dst=np.zeros(HD, np.float32),
+             da_src_abs=np.zeros(HD, np.float32), da_dst_abs=np.zeros(HD, np.float32),
+             qdHp=np.zeros((n, HD), np.int8), sdHp=np.zeros(1, np.float32), dH=np.zeros((n, F), np.float32),
+             dW=np.zeros((F, HD), np.float32))
+    st = BwdOut(*[_p(o[f]) for f in _BWD_FIELDS])
+    _check(lib().orc_gat_bwd(C.byref(gs), C.byref(cfg), _p(W), _p(a_src), _p(a_dst), C.byref(fwd["_struct"]),
+                             _p(H), _p(dHout), C.byref(st)))
+    return o
+
+
+def gcn_fwd(g, X, W, bits=8, seed=0x7A4E60, step=0, layer_id=0, chunk=256):
+    n, F = X.shape
+    O = W.shape[1]
+    gs = graph_struct(g, chunk)
+    cfg = _cfg(F, 1, O, 0.0, bits, seed, step, layer_id)
+    X, W = _c(X, np.float32), _c(W, np.float32)
+    o = dict(qX=np.zeros((n, F), np.int8), sX=np.zeros(1, np.float32), qW=np.zeros((F, O), np.int8),
+             sW=np.zeros(1, np.float32), Ys=np.zeros((n, O), np.float32), qYs=np.zeros((n, O), np.int8),
+             sYs=np.zeros(1, np.float32), ia=np.zeros((n, O), np.int32), out=np.zeros((n, O), np.float32))
+    st = GcnFwdOut(*[_p(o[f]) for f in _GCN_FWD_FIELDS])
+    _check(lib().orc_gcn_fwd(C.byref(gs), C.byref(cfg), _p(X), _p(W), C.byref(st)))
+    o["_struct"] = st
+    o["_cfg"] = dict(F=F, O=O, bits=bits, seed=seed, step=step, layer_id=layer_id, chunk=chunk)
+    return o
+
+
+def gcn_bwd(g, fwd, X, W, dout):
+    c = fwd["_cfg"]
+    n, F = X.shape
+    O = c["O"]
+    gs = graph_struct(g, c["chunk"])
+    cfg = _cfg(F, 1, O, 0.0, c["bits"], c["seed"], c["step"], c["layer_id"])
+    X, W, dout = _c(X, np.float32), _c(W, np.float32), _c(dout, np.float32)
+    o = dict(Gs=np.zeros((n, O), np.float32), qGs=np.zeros((n, O), np.int8), sGs=np.zeros(1, np.float32),
+             ib=np.zeros((n, O), np.int32), dY=np.zeros((n, O), np.float32), qdY=np.zeros((n, O), np.int8),
+             sdY=np.zeros(1, np.float32), dX=np.zeros((n, F), np.float32), dW=np.zeros((F, O), np.float32))
+    st = GcnBwdOut(*[_p(o[f]) for f in _GCN_BWD_FIELDS])
+    _check(lib().orc_gcn_bwd(C.byref(gs), C.byref(cfg), _p(X), _p(W), C.byref(fwd["_struct"]), _p(dout),
+                             C.byref(st)))
+    return o
