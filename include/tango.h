@@ -1,0 +1,277 @@
+/*
+ * tango.h — C ABI of libtango.so: the quantized GAT / GCN layer of Tango
+ * (arXiv 2308.00890, SC'23) as hand-written CUDA for sm_100a (B200).
+ *
+ * Paper citations: P:n = PAPER.md line n (section / equation given beside it).
+ * Readings of the paper (R#) are listed in DESIGN.md §2.
+ *
+ * CONVENTIONS (apply to every entry point)
+ *  - Every tensor pointer is a DEVICE pointer, allocated and owned by the caller
+ *    (e.g. by PyTorch).  The library never frees or retains a caller pointer
+ *    beyond the call, except `ctx`, which holds the forward -> backward cache.
+ *  - Every call is asynchronous on the given cudaStream_t (0 = legacy default
+ *    stream).  Scales and maxima stay in device memory: no call synchronizes
+ *    the host, except tango_status_poll and the optional launch-error check.
+ *  - A call returns a tango_status after validating its arguments on the host
+ *    (before any launch).  Errors that depend on tensor VALUES (a non-finite
+ *    input) are written asynchronously into the caller-provided device word
+ *    `dev_status` (int32, may be NULL); read it with tango_status_poll after
+ *    the stream has run.  Output tensors of a call that saw a non-finite input
+ *    are unspecified.
+ *  - Layouts are row-major.  Node rows are head-major concatenations
+ *    [h][d] (reading R15).  int8 matrices carry an explicit leading
+ *    dimension `ld` (elements) which must be a multiple of 16 (TMA) and,
+ *    for outputs written by the GEMM epilogue, of 32; bytes between the
+ *    logical width and ld are zero padding.
+ *  - Edge arrays are indexed by in-CSR position (destination-major, sources
+ *    ascending: reading R14).
+ *  - No C++ exception crosses this ABI.  All functions are reentrant; a
+ *    tango_comm may be used by one stream at a time.
+ */
+#ifndef TANGO_H_
+#define TANGO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TANGO_ABI_VERSION 1
+
+typedef enum {
+  TANGO_OK = 0,
+  TANGO_ERR_INVALID_ARG = 1,   /* NULL required pointer, bad enum, bad ctx size */
+  TANGO_ERR_SHAPE = 2,         /* inconsistent sizes / heads / leading dimensions */
+  TANGO_ERR_BITS = 3,          /* bit-width outside [2, 8] (reading R25) */
+  TANGO_ERR_NONFINITE = 4,     /* (device status) NaN / Inf in a tensor being quantized */
+  TANGO_ERR_OVERFLOW = 5,      /* a contraction length that could overflow int32 (reading R27) */
+  TANGO_ERR_UNSUPPORTED = 6,   /* a shape this build does not implement (e.g. HD not in {32..512}) */
+  TANGO_ERR_CUDA = 7,          /* a CUDA launch / runtime error */
+  TANGO_ERR_NCCL = 8           /* a NCCL error (multi-GPU) */
+} tango_status;
+
+const char* tango_status_string(tango_status s);
+int tango_abi_version(void);
+
+/* Reads a device status word written by earlier asynchronous work on `stream`.
+ * SYNCHRONIZES the stream.  *out receives TANGO_OK or the first error seen. */
+tango_status tango_status_poll(const int32_t* dev_status, cudaStream_t stream, tango_status* out);
+
+/* ------------------------------------------------------------------------- */
+/* Graph G ("sparse adjacency matrix G"; incidence rows P:831-832)  */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t n_global;        /* N: number of nodes in the whole graph */
+  int64_t row_begin;       /* owned node block [row_begin, row_end); one GPU: 0, N */
+  int64_t row_end;
+  /* in-CSR of the owned destination rows: in_ptr[n_local+1] (offsets from 0),
+   * in_src[e_in] = GLOBAL source ids, ascending within a row. */
+  const int64_t* in_ptr;
+  const int32_t* in_src;
+  int64_t e_in;
+  /* out-CSR of the owned source rows: out_ptr[n_local+1], out_dst[e_out] =
+   * GLOBAL destination ids ascending within a row; out_eid[e_out] = position
+   * of that edge in the in-CSR (needed only by the standalone OUT-direction
+   * primitives with explicit edge weights; may be NULL otherwise). */
+  const int64_t* out_ptr;
+  const int32_t* out_dst;
+  const int32_t* out_eid;
+  int64_t e_out;
+  int32_t chunk_edges;     /* C_E of the canonical chunked sums (reading R14); 0 => 256 */
+} tango_graph;
+
+/* Quantized tensor (DS6): int8 codes [rows][ld] + DEVICE fp32 scale s,
+ * dequantized value = code * s (Eq.2 with Z = 0, reading R1). */
+typedef struct {
+  int8_t* q;
+  float* scale;            /* device scalar */
+  int64_t rows, cols, ld;
+  int32_t bits;            /* 2..8 */
+} tango_qtensor;
+
+/* Philox4x32-10 stream for stochastic rounding (Eq.3; reading R4/R5):
+ * element g of a tensor draws half-word (g & 7) of
+ * Philox(ctr = {lo32(g>>3), hi32(g>>3), tag, step}, key = seed). */
+typedef struct {
+  uint64_t seed;
+  uint32_t step;           /* training iteration */
+  uint32_t tag;            /* (layer_id << 8) | role, roles: H=1 W=2 H'=3 S=4 D=5 dHout=6 dH'=7 Ys=8 Gs=9 dY=10 */
+} tango_rng;
+
+/* ------------------------------------------------------------------------- */
+/* Primitive 1 — quantize (§2.3 Eq.1; §3.2 Eq.3).         */
+/* x: fp32 [rows][cols] (row stride cols).  amax = max|x| over the tensor      */
+/* (or *amax_hint if non-NULL; a device scalar, e.g. produced by the previous  */
+/* kernel), s = amax/qmax, r = qmax/amax (s = r = 1 if amax = 0),              */
+/* q = clamp(floor(x*r) + (u < frac), ±qmax).  Element (i, j) uses the global  */
+/* index g = (global_row0 + i) * cols + j.  out->q: [rows][out->ld], padding   */
+/* columns are written as 0.  out->scale receives s.  amax_out (nullable):     */
+/* device scalar receiving amax.  Non-finite x => *dev_status = NONFINITE.    */
+/* ------------------------------------------------------------------------- */
+tango_status tango_quantize(const float* x, int64_t rows, int64_t cols, int64_t global_row0,
+                            const float* amax_hint, tango_rng rng, tango_qtensor* out, float* amax_out,
+                            int32_t* dev_status, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* Primitive 2 — quantization-aware GEMM (§3.2 Fig.4; P:736-739     */
+/* §3.3): acc = A·B in exact integer arithmetic on the int8 tensor cores      */
+/* (tcgen05.mma kind::i8), dequantized in the epilogue: C = (float)acc *      */
+/* (s_A*s_B).  Logical A is M×K, logical B is K×N.                             */
+/*   a_layout TANGO_K_MAJOR : A->q is [M][A->ld]  (row m holds K codes)        */
+/*   a_layout TANGO_MN_MAJOR: A->q is [K][A->ld]  (row k holds M codes)        */
+/*   b_layout TANGO_K_MAJOR : B->q is [N][B->ld]  (i.e. Bᵀ, row n holds K)     */
+/*   b_layout TANGO_MN_MAJOR: B->q is [K][B->ld]  (row k holds N codes)        */
+/* Outputs (each nullable, at least one non-NULL): C fp32 [M][N];             */
+/* C_i32 int32 [M][N] raw accumulator (requires K <= 133,144, reading R27);    */
+/* C_i64 int64 [M][N] raw accumulator for any K (split-K, int64 reduction;    */
+/* C_i64 is OVERWRITTEN).  C requires K <= 133,144 or uses split-K as well.   */
+/* ------------------------------------------------------------------------- */
+enum { TANGO_K_MAJOR = 0, TANGO_MN_MAJOR = 1 };
+tango_status tango_gemm_q(const tango_qtensor* A, int32_t a_layout, const tango_qtensor* B, int32_t b_layout,
+                          int64_t M, int64_t N, int64_t K, float* C, int32_t* C_i32, int64_t* C_i64,
+                          cudaStream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* Primitive 3 — SDDMM on quantized node features.                            */
+/*  TANGO_SDDMM_ADD (③, §2.1; on-the-fly dequantization P:864-873): */
+/*    e_pre[e,h] = q_S[u,h]*s_S + q_D[v,h]*s_D ; el = e_pre>0 ? e_pre : e_pre*slope */
+/*    Xsrc = S [N][heads], Xdst = D [n_local][heads]; out0 = e_pre, out1 = el  */
+/*  TANGO_SDDMM_DOT (⑤″; directly on codes P:875-876):             */
+/*    out0[e,h] = (float)(Σ_d q_A[v,h,d] q_B[u,h,d]) * (s_A*s_B)               */
+/*    Xdst = A (destination rows, e.g. ∂H_out), Xsrc = B (source rows, H′);    */
+/*    acc_i32 (nullable): raw int32 dots [e][heads].  out1 unused.             */
+/* Edge outputs are [e_in][heads] fp32 in in-CSR order.                       */
+/* ------------------------------------------------------------------------- */
+enum { TANGO_SDDMM_ADD = 0, TANGO_SDDMM_DOT = 1 };
+tango_status tango_sddmm_q(const tango_graph* G, int32_t op, const tango_qtensor* Xsrc, const tango_qtensor* Xdst,
+                           int32_t heads, float slope, float* out0, float* out1, int32_t* acc_i32,
+                           cudaStream_t stream);
+
+/* Edge softmax ④ in FP32 (full precision P:604-615, R9, R12, R13, */
+/* R14): m = max el over in-edges, den = Σᶜ exp_p(el-m), α = exp_p(el-m)/den. */
+/* el, alpha: [e_in][heads]; m, den: [n_local][heads] (m = den = 0 if empty). */
+tango_status tango_edge_softmax(const tango_graph* G, int32_t heads, const float* el, float* m, float* den,
+                                float* alpha, cudaStream_t stream);
+
+/* Softmax backward ④′ + LeakyReLU backward (R11):               */
+/* P[v,h] = Σᶜ fmaf(∂α, α); ∂E = α(∂α − P[v]); ∂E_pre = e_pre>0 ? ∂E : ∂E·slope */
+tango_status tango_softmax_bwd(const tango_graph* G, int32_t heads, const float* alpha, const float* dalpha,
+                               const float* e_pre, float slope, float* P, float* dE_pre, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* Primitive 4 — SPMM on quantized node features (⑤ P:224-227; ⑤′ P:248-251; */
+/* incidence SPMM ③′/③″ P:276; GCN P:347-348).                    */
+/*  edge_w != NULL: out[v,j] = (Σᶜ fmaf(w[e,h(j)], q_X[w_e,j])) * s_X, fp32   */
+/*     accumulation, dir TANGO_IN sums in-edges (w_e = source),               */
+/*     dir TANGO_OUT sums out-edges (w_e = destination, weight w[out_eid[e]]).*/
+/*  edge_w == NULL: out_i32[v,j] = Σ q_X[w_e,j] (exact int32, order-free);     */
+/*     out (nullable) = (float)out_i32 * s_X.                                  */
+/* X: [n_global][X->ld] codes with X->cols = heads*D.  out [n_local][cols].    */
+/* ------------------------------------------------------------------------- */
+enum { TANGO_IN = 0, TANGO_OUT = 1 };
+tango_status tango_spmm_q(const tango_graph* G, int32_t dir, const float* edge_w, const tango_qtensor* X,
+                          int32_t heads, float* out, int32_t* out_i32, cudaStream_t stream);
+
+/* Incidence-matrix SPMM for edge features (③″/③′):        */
+/* out[v,h] = Σᶜ x[e,h] over the in-edges (dir IN) or out-edges (dir OUT).    */
+tango_status tango_edge_sum(const tango_graph* G, int32_t dir, int32_t heads, const float* x, float* out,
+                            cudaStream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* Fused GAT layer (§2.1 Fig.1 with §3.2-3.3 quantization rules).  */
+/* Forward: F1 Q(H), F2 Q(W), F3 ①② tcgen05 GEMM + head dots, F4 Q(H′),Q(S),Q(D),
+ * F5/F6 ③④⑤ one destination-row kernel.  Backward: B1 Q(∂H_out), B2-B4 one  */
+/* destination-row kernel, B5-B7 one source-row kernel, B8 Q(∂H′), B9 ①′ GEMMs.*/
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  const float* W;          /* device [in_feats][heads*head_dim] fp32 master weights */
+  const float* a_src;      /* device [heads*head_dim] */
+  const float* a_dst;      /* device [heads*head_dim] */
+  int32_t in_feats, heads, head_dim;
+  float neg_slope;         /* LeakyReLU slope (R11) */
+  int32_t bits;            /* quantization bits B (8 on the hot path, R25) */
+} tango_gat_params;
+
+/* Size of the caller-allocated ctx (device memory, 256-B aligned) holding the
+ * forward->backward cache (q_H, q_W, q_H′, q_S, q_D, m, den, scales)
+ * and all scratch of both passes.  0 on invalid arguments. */
+size_t tango_gat_ctx_bytes(const tango_graph* G, const tango_gat_params* p);
+
+/* H: [n_local][in_feats] fp32 (this rank's rows).  amax_H_hint (nullable): device
+ * scalar max|H| over ALL ranks (e.g. the previous layer's amax_out) — skips the
+ * amax pass.  H_out: [n_local][heads*head_dim] fp32.  amax_out (nullable): device
+ * scalar receiving max|H_out| (hint for the next layer).  comm: NULL on one GPU. */
+struct tango_comm;
+tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p, const float* H,
+                                 const float* amax_H_hint, tango_rng rng, uint32_t layer_id, void* ctx,
+                                 size_t ctx_bytes, float* H_out, float* amax_out, struct tango_comm* comm,
+                                 int32_t* dev_status, cudaStream_t stream);
+
+/* dH_out: [n_local][heads*head_dim].  dH (nullable): [n_local][in_feats];
+ * dW: [in_feats][heads*head_dim]; da_src, da_dst: [heads*head_dim]; all fp32,
+ * all overwritten.  amax_dH (nullable): device scalar receiving max|dH|. */
+tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p, void* ctx, size_t ctx_bytes,
+                                 const float* dH_out, const float* amax_dH_hint, tango_rng rng, uint32_t layer_id,
+                                 float* dH, float* dW, float* da_src, float* da_dst, float* amax_dH,
+                                 struct tango_comm* comm, int32_t* dev_status, cudaStream_t stream);
+
+/* Debug views into a GAT ctx (device pointers inside ctx; for parity tests).  */
+typedef struct {
+  int8_t *qH, *qW, *qWt, *qHp, *qS, *qD, *qG, *qdHp;
+  int64_t ldF, ldHD, ldFt;
+  float *S, *D, *m, *den, *P, *dD, *dHp, *dalpha;
+  float *scalars;          /* see DESIGN.md §4 "ctx scalars" for the slot map */
+} tango_gat_ctx_view;
+tango_status tango_gat_ctx_get_view(const tango_graph* G, const tango_gat_params* p, void* ctx,
+                                    tango_gat_ctx_view* view);
+
+/* ------------------------------------------------------------------------- */
+/* GCN layer: GEMM + SPMM (§2.2), DGL norm='both' folded into rows  */
+/* (reading R26): out = diag(nd) · A · diag(ns) · (X·W), int32 aggregation.   */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  const float* W;          /* device [in_feats][out_feats] */
+  int32_t in_feats, out_feats;
+  int32_t bits;
+} tango_gcn_params;
+
+size_t tango_gcn_ctx_bytes(const tango_graph* G, const tango_gcn_params* p);
+tango_status tango_gcn_layer_fwd(const tango_graph* G, const tango_gcn_params* p, const float* X,
+                                 const float* amax_X_hint, tango_rng rng, uint32_t layer_id, void* ctx,
+                                 size_t ctx_bytes, float* out, float* amax_out, struct tango_comm* comm,
+                                 int32_t* dev_status, cudaStream_t stream);
+tango_status tango_gcn_layer_bwd(const tango_graph* G, const tango_gcn_params* p, void* ctx, size_t ctx_bytes,
+                                 const float* dout, tango_rng rng, uint32_t layer_id, float* dX, float* dW,
+                                 struct tango_comm* comm, int32_t* dev_status, cudaStream_t stream);
+
+typedef struct {
+  int8_t *qX, *qW, *qWt, *qYs, *qGs, *qdY;
+  int64_t ldF, ldO, ldFt;
+  int32_t *ia, *ib;
+  float *scalars;
+} tango_gcn_ctx_view;
+tango_status tango_gcn_ctx_get_view(const tango_graph* G, const tango_gcn_params* p, void* ctx,
+                                    tango_gcn_ctx_view* view);
+
+/* ------------------------------------------------------------------------- */
+/* Multi-GPU (destination-row partitioning): an NCCL          */
+/* communicator built from a 128-byte ncclUniqueId that the caller broadcasts  */
+/* (e.g. with torch.distributed).  Collectives are enqueued on the caller's    */
+/* stream: AllReduce-MAX of amax scalars (R28), AllGather of int8 node rows,   */
+/* AllReduce-SUM of int64 ∂W partials and fp32 ∂a.                            */
+/* ------------------------------------------------------------------------- */
+int32_t tango_comm_unique_id_bytes(void);
+tango_status tango_comm_get_unique_id(void* id_out /* tango_comm_unique_id_bytes() bytes */);
+tango_status tango_comm_init(struct tango_comm** out, const void* unique_id, int32_t nranks, int32_t rank);
+tango_status tango_comm_destroy(struct tango_comm* comm);
+/* Row partition of the node set: rank r owns [row_starts[r], row_starts[r+1]).
+ * Must be called (identically on every rank) before a layer call with this comm. */
+tango_status tango_comm_set_partition(struct tango_comm* comm, const int64_t* row_starts /* nranks+1, host */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TANGO_H_ */

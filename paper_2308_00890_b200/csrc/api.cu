@@ -1,0 +1,821 @@
+// api.cu — the C ABI of libtango.so (include/tango.h): argument validation, the ctx layout,
+// orchestration of the fused kernels for one GAT / GCN layer (forward, backward) and the NCCL
+// communicator for destination-row partitioning over several GPUs.
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/tango.h"
+#include "kernels.h"
+
+namespace tango {
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Philox tag = (layer_id << 8) | role (tango.h)
+enum Role : uint32_t { R_H = 1, R_W = 2, R_HP = 3, R_S = 4, R_D = 5, R_G = 6, R_DHP = 7, R_YS = 8, R_GS = 9, R_DY = 10 };
+static inline uint32_t tag_of(uint32_t layer, uint32_t role) { return (layer << 8) | role; }
+
+// ctx scalar slots: amax bit patterns and scales, 64 x 4 B at the start of ctx.
+enum Slot : int {
+  SL_AMAX_H = 0, SL_AMAX_W = 1, SL_AMAX_HP = 2, SL_AMAX_S = 3, SL_AMAX_D = 4, SL_AMAX_G = 6, SL_AMAX_DHP = 7,
+  SL_S_H = 8, SL_S_W = 9, SL_S_HP = 10, SL_S_S = 11, SL_S_D = 12, SL_S_G = 13, SL_S_DHP = 14,
+  SL_NSLOTS = 64
+};
+
+}  // namespace tango
+
+using namespace tango;
+
+struct tango_comm {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1, rank = 0;
+  std::vector<int64_t> starts;  // nranks + 1
+};
+
+#define TRY_CUDA(x)                                  \
+  do {                                               \
+    cudaError_t e_ = (x);                            \
+    if (e_ != cudaSuccess) {                         \
+      fprintf(stderr, "[tango] CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return TANGO_ERR_CUDA;                         \
+    }                                                \
+  } while (0)
+#define TRY_NCCL(x)                                  \
+  do {                                               \
+    ncclResult_t r_ = (x);                           \
+    if (r_ != ncclSuccess) {                         \
+      fprintf(stderr, "[tango] NCCL error %s at %s:%d\n", ncclGetErrorString(r_), __FILE__, __LINE__); \
+      return TANGO_ERR_NCCL;                         \
+    }                                                \
+  } while (0)
+#define TRY(x)                                       \
+  do {                                               \
+    tango_status s_ = (x);                           \
+    if (s_ != TANGO_OK) return s_;                   \
+  } while (0)
+
+extern "C" {
+
+const char* tango_status_string(tango_status s) {
+  switch (s) {
+    case TANGO_OK: return "ok";
+    case TANGO_ERR_INVALID_ARG: return "invalid argument";
+    case TANGO_ERR_SHAPE: return "shape mismatch";
+    case TANGO_ERR_BITS: return "bit-width outside [2,8]";
+    case TANGO_ERR_NONFINITE: return "non-finite value in a quantized tensor";
+    case TANGO_ERR_OVERFLOW: return "contraction length may overflow int32";
+    case TANGO_ERR_UNSUPPORTED: return "unsupported shape";
+    case TANGO_ERR_CUDA: return "CUDA error";
+    case TANGO_ERR_NCCL: return "NCCL error";
+  }
+  return "unknown";
+}
+
+int tango_abi_version(void) { return TANGO_ABI_VERSION; }
+
+tango_status tango_status_poll(const int32_t* dev_status, cudaStream_t stream, tango_status* out) {
+  if (!dev_status || !out) return TANGO_ERR_INVALID_ARG;
+  int32_t v = 0;
+  TRY_CUDA(cudaMemcpyAsync(&v, dev_status, sizeof(v), cudaMemcpyDeviceToHost, stream));
+  TRY_CUDA(cudaStreamSynchronize(stream));
+  *out = (tango_status)v;
+  return TANGO_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ validation helpers
+static tango_status check_graph(const tango_graph* G, bool need_out) {
+  if (!G || !G->in_ptr) return TANGO_ERR_INVALID_ARG;
+  if (G->n_global < 0 || G->row_begin < 0 || G->row_end < G->row_begin || G->row_end > G->n_global)
+    return TANGO_ERR_SHAPE;
+  if (G->e_in > 0 && !G->in_src) return TANGO_ERR_INVALID_ARG;
+  if (G->e_in >= (int64_t(1) << 31) || G->e_out >= (int64_t(1) << 31) || G->n_global >= (int64_t(1) << 31))
+    return TANGO_ERR_UNSUPPORTED;
+  if (need_out && (!G->out_ptr || (G->e_out > 0 && !G->out_dst))) return TANGO_ERR_INVALID_ARG;
+  if (G->chunk_edges < 0) return TANGO_ERR_INVALID_ARG;
+  return TANGO_OK;
+}
+static GraphDev dev_graph(const tango_graph* G) {
+  GraphDev g;
+  g.n_local = G->row_end - G->row_begin;
+  g.row_begin = G->row_begin;
+  g.in_ptr = G->in_ptr; g.in_src = G->in_src;
+  g.out_ptr = G->out_ptr; g.out_dst = G->out_dst; g.out_eid = G->out_eid;
+  g.chunk = G->chunk_edges > 0 ? G->chunk_edges : 256;
+  return g;
+}
+static tango_status check_q(const tango_qtensor* t) {
+  if (!t || !t->q || !t->scale) return TANGO_ERR_INVALID_ARG;
+  if (t->bits < 2 || t->bits > 8) return TANGO_ERR_BITS;
+  if (t->rows < 0 || t->cols < 0 || t->ld < t->cols) return TANGO_ERR_SHAPE;
+  return TANGO_OK;
+}
+static tango_status launch_status(cudaError_t e) {
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[tango] launch failed: %s\n", cudaGetErrorString(e));
+    return TANGO_ERR_CUDA;
+  }
+  return TANGO_OK;
+}
+
+// ------------------------------------------------------------------ collectives (caller stream)
+static tango_status comm_max(tango_comm* c, void* buf, size_t count, cudaStream_t st) {
+  if (!c || c->nranks == 1) return TANGO_OK;
+  TRY_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclMax, c->nccl, st));
+  return TANGO_OK;
+}
+static tango_status comm_sum_f32(tango_comm* c, float* buf, size_t count, cudaStream_t st) {
+  if (!c || c->nranks == 1) return TANGO_OK;
+  TRY_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, c->nccl, st));
+  return TANGO_OK;
+}
+static tango_status comm_sum_i64(tango_comm* c, int64_t* buf, size_t count, cudaStream_t st) {
+  if (!c || c->nranks == 1) return TANGO_OK;
+  TRY_NCCL(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, c->nccl, st));
+  return TANGO_OK;
+}
+// All-gather of node-row blocks of `row_bytes` bytes: rank r's block [starts[r], starts[r+1]) is
+// broadcast in place to every rank (grouped broadcasts: partitions have different sizes).
+static tango_status comm_gather_rows(tango_comm* c, void* base, size_t row_bytes, cudaStream_t st) {
+  if (!c || c->nranks == 1) return TANGO_OK;
+  TRY_NCCL(ncclGroupStart());
+  for (int r = 0; r < c->nranks; ++r) {
+    const size_t off = (size_t)c->starts[r] * row_bytes;
+    const size_t cnt = (size_t)(c->starts[r + 1] - c->starts[r]) * row_bytes;
+    if (cnt == 0) continue;
+    char* p = static_cast<char*>(base) + off;
+    TRY_NCCL(ncclBroadcast(p, p, cnt, ncclInt8, r, c->nccl, st));
+  }
+  TRY_NCCL(ncclGroupEnd());
+  return TANGO_OK;
+}
+static tango_status check_comm(const tango_graph* G, tango_comm* c) {
+  if (!c) return (G->row_begin == 0 && G->row_end == G->n_global) ? TANGO_OK : TANGO_ERR_SHAPE;
+  if ((int)c->starts.size() != c->nranks + 1) return TANGO_ERR_INVALID_ARG;
+  if (c->starts[c->rank] != G->row_begin || c->starts[c->rank + 1] != G->row_end ||
+      c->starts[c->nranks] != G->n_global)
+    return TANGO_ERR_SHAPE;
+  return TANGO_OK;
+}
+
+extern "C" {
+
+// ================================================================== primitives
+tango_status tango_quantize(const float* x, int64_t rows, int64_t cols, int64_t global_row0, const float* amax_hint,
+                            tango_rng rng, tango_qtensor* out, float* amax_out, int32_t* dev_status,
+                            cudaStream_t stream) {
+  TRY(check_q(out));
+  if (!x && rows * cols > 0) return TANGO_ERR_INVALID_ARG;
+  if (out->rows != rows || out->cols != cols || global_row0 < 0) return TANGO_ERR_SHAPE;
+  // the amax lives in amax_out if given, otherwise in a small stream-ordered scratch
+  float* slot = amax_out;
+  float* scratch = nullptr;
+  if (!slot) {
+    TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(float), stream));
+    slot = scratch;
+  }
+  if (amax_hint) {
+    TRY_CUDA(cudaMemcpyAsync(slot, amax_hint, sizeof(float), cudaMemcpyDeviceToDevice, stream));
+  } else {
+    TRY_CUDA(cudaMemsetAsync(slot, 0, sizeof(float), stream));
+    TRY(launch_status(launch_absmax(x, rows, cols, nullptr, reinterpret_cast<unsigned*>(slot), stream)));
+  }
+  TRY(launch_status(launch_quantize(x, rows, cols, nullptr, global_row0 * cols, reinterpret_cast<unsigned*>(slot),
+                                    out->bits, rng.seed, rng.step, rng.tag, out->q, out->ld, nullptr, 0, out->scale,
+                                    dev_status, stream)));
+  if (scratch) TRY_CUDA(cudaFreeAsync(scratch, stream));
+  return TANGO_OK;
+}
+
+tango_status tango_gemm_q(const tango_qtensor* A, int32_t a_layout, const tango_qtensor* B, int32_t b_layout,
+                          int64_t M, int64_t N, int64_t K, float* C, int32_t* C_i32, int64_t* C_i64,
+                          cudaStream_t stream) {
+  TRY(check_q(A));
+  TRY(check_q(B));
+  if ((a_layout != TANGO_K_MAJOR && a_layout != TANGO_MN_MAJOR) ||
+      (b_layout != TANGO_K_MAJOR && b_layout != TANGO_MN_MAJOR))
+    return TANGO_ERR_INVALID_ARG;
+  if (!C && !C_i32 && !C_i64) return TANGO_ERR_INVALID_ARG;
+  if (M < 0 || N < 0 || K < 0) return TANGO_ERR_SHAPE;
+  const bool amn = a_layout == TANGO_MN_MAJOR, bmn = b_layout == TANGO_MN_MAJOR;
+  // logical extents vs stored tensors
+  if (amn ? (A->rows != K || A->cols != M) : (A->rows != M || A->cols != K)) return TANGO_ERR_SHAPE;
+  if (bmn ? (B->rows != K || B->cols != N) : (B->rows != N || B->cols != K)) return TANGO_ERR_SHAPE;
+  if ((A->ld % 16) || (B->ld % 16)) return TANGO_ERR_SHAPE;
+  const bool small_k = K <= 133144;
+  if (C_i32 && !small_k) return TANGO_ERR_OVERFLOW;
+  if (C && !small_k && !C_i64) return TANGO_ERR_OVERFLOW;
+  if (M == 0 || N == 0) return TANGO_OK;
+  GemmArgs g{};
+  g.A = A->q; g.lda = A->ld; g.a_mn = amn;
+  g.B = B->q; g.ldb = B->ld; g.b_mn = bmn;
+  g.M = M; g.N = N; g.K = K; g.splits = 1;
+  g.sA = A->scale; g.sB = B->scale;
+  if (C_i32) {
+    g.mode = EPI_I32; g.C = C_i32; g.ldc = N;
+    TRY(launch_status(launch_gemm(g, stream)));
+  }
+  if (C_i64) {
+    TRY_CUDA(cudaMemsetAsync(C_i64, 0, sizeof(int64_t) * M * N, stream));
+    g.mode = EPI_ATOMIC64; g.C = C_i64; g.ldc = N;
+    const int64_t tiles = ((M + 127) / 128) * ((N + 255) / 256);
+    const int64_t kb = (K + 127) / 128;
+    int64_t splits = (2 * num_sms() + tiles - 1) / tiles;
+    const int64_t min_splits = (K + 131071) / 131072;   // int32-safe chunks (reading R27)
+    if (splits < min_splits) splits = min_splits;
+    if (splits > kb) splits = kb > 0 ? kb : 1;
+    g.splits = (int)splits;
+    TRY(launch_status(launch_gemm(g, stream)));
+    g.splits = 1;
+  }
+  if (C) {
+    if (small_k) {
+      g.mode = EPI_STORE; g.C = C; g.ldc = N;
+      TRY(launch_status(launch_gemm(g, stream)));
+    } else {
+      TRY(launch_status(launch_finalize_dw(C_i64, M * N, A->scale, B->scale, C, stream)));
+    }
+  }
+  return TANGO_OK;
+}
+
+tango_status tango_sddmm_q(const tango_graph* G, int32_t op, const tango_qtensor* Xsrc, const tango_qtensor* Xdst,
+                           int32_t heads, float slope, float* out0, float* out1, int32_t* acc_i32,
+                           cudaStream_t stream) {
+  TRY(check_graph(G, false));
+  TRY(check_q(Xsrc));
+  TRY(check_q(Xdst));
+  if (heads <= 0) return TANGO_ERR_SHAPE;
+  const GraphDev g = dev_graph(G);
+  if (Xsrc->rows != G->n_global || Xdst->rows < G->row_end) return TANGO_ERR_SHAPE;
+  if (op == TANGO_SDDMM_ADD) {
+    if (Xsrc->cols != heads || Xdst->cols != heads || Xsrc->ld != heads || Xdst->ld != heads) return TANGO_ERR_SHAPE;
+    if (!out0 && !out1) return TANGO_ERR_INVALID_ARG;
+    return launch_status(launch_sddmm_add(g, heads, Xsrc->q, Xsrc->scale, Xdst->q, Xdst->scale, slope, out0, out1,
+                                          stream));
+  }
+  if (op == TANGO_SDDMM_DOT) {
+    if (Xsrc->cols != Xdst->cols || Xsrc->cols % heads) return TANGO_ERR_SHAPE;
+    if (!out0 && !acc_i32) return TANGO_ERR_INVALID_ARG;
+    return launch_status(launch_sddmm_dot(g, heads, (int)Xsrc->cols, Xdst->q, Xdst->ld, Xdst->scale, Xsrc->q,
+                                          Xsrc->ld, Xsrc->scale, out0, acc_i32, stream));
+  }
+  return TANGO_ERR_INVALID_ARG;
+}
+
+tango_status tango_edge_softmax(const tango_graph* G, int32_t heads, const float* el, float* m, float* den,
+                                float* alpha, cudaStream_t stream) {
+  TRY(check_graph(G, false));
+  if (heads <= 0) return TANGO_ERR_SHAPE;
+  if (!alpha || (!el && G->e_in > 0)) return TANGO_ERR_INVALID_ARG;
+  return launch_status(launch_edge_softmax(dev_graph(G), heads, el, m, den, alpha, stream));
+}
+
+tango_status tango_softmax_bwd(const tango_graph* G, int32_t heads, const float* alpha, const float* dalpha,
+                               const float* e_pre, float slope, float* P, float* dE_pre, cudaStream_t stream) {
+  TRY(check_graph(G, false));
+  if (heads <= 0) return TANGO_ERR_SHAPE;
+  if (G->e_in > 0 && (!alpha || !dalpha || !e_pre || !dE_pre)) return TANGO_ERR_INVALID_ARG;
+  return launch_status(launch_softmax_bwd(dev_graph(G), heads, alpha, dalpha, e_pre, slope, P, dE_pre, stream));
+}
+
+tango_status tango_spmm_q(const tango_graph* G, int32_t dir, const float* edge_w, const tango_qtensor* X,
+                          int32_t heads, float* out, int32_t* out_i32, cudaStream_t stream) {
+  TRY(check_graph(G, dir == TANGO_OUT));
+  TRY(check_q(X));
+  if (dir != TANGO_IN && dir != TANGO_OUT) return TANGO_ERR_INVALID_ARG;
+  if (heads <= 0 || X->cols % heads || X->rows != G->n_global) return TANGO_ERR_SHAPE;
+  const GraphDev g = dev_graph(G);
+  if (edge_w) {
+    if (!out) return TANGO_ERR_INVALID_ARG;
+    if (dir == TANGO_OUT && G->e_out > 0 && !G->out_eid) return TANGO_ERR_INVALID_ARG;
+    return launch_status(launch_spmm_w(g, dir, heads, (int)X->cols, edge_w, X->q, X->ld, X->scale, out, stream));
+  }
+  if (!out && !out_i32) return TANGO_ERR_INVALID_ARG;
+  return launch_status(
+      launch_spmm_sum(g, dir, (int)X->cols, X->q, X->ld, X->scale, nullptr, out, out_i32, nullptr, stream));
+}
+
+tango_status tango_edge_sum(const tango_graph* G, int32_t dir, int32_t heads, const float* x, float* out,
+                            cudaStream_t stream) {
+  TRY(check_graph(G, dir == TANGO_OUT));
+  if (dir != TANGO_IN && dir != TANGO_OUT) return TANGO_ERR_INVALID_ARG;
+  if (dir == TANGO_OUT && G->e_out > 0 && !G->out_eid) return TANGO_ERR_INVALID_ARG;
+  if (heads <= 0) return TANGO_ERR_SHAPE;
+  if (!out) return TANGO_ERR_INVALID_ARG;
+  return launch_status(launch_edge_sum(dev_graph(G), dir, heads, x, out, stream));
+}
+
+}  // extern "C"
+
+// ================================================================== GAT ctx layout
+namespace {
+struct GatLayout {
+  int64_t n, N, E, F, H, Dh, HD, ldF, ldHD, ldFt;
+  size_t off_scal, off_qH, off_qW, off_qWt, off_qHp, off_S, off_D, off_qS, off_qD, off_m, off_den, off_P, off_dD,
+      off_qG, off_dal, off_dHp, off_qdHp, off_dW64, total;
+};
+GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
+  GatLayout L{};
+  L.n = G->row_end - G->row_begin;
+  L.N = G->n_global;
+  L.E = G->e_in;
+  L.F = p->in_feats; L.H = p->heads; L.Dh = p->head_dim; L.HD = L.H * L.Dh;
+  L.ldF = round_up(L.F, 32);
+  L.ldHD = round_up(L.HD, 32);
+  L.ldFt = L.ldF;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t at = o; o = align256(o + bytes); return at; };
+  L.off_scal = take(SL_NSLOTS * 4);
+  L.off_qH = take((size_t)L.n * L.ldF);
+  L.off_qW = take((size_t)L.F * L.ldHD);
+  L.off_qWt = take((size_t)L.HD * L.ldFt);
+  L.off_qHp = take((size_t)L.N * L.ldHD);
+  L.off_S = take((size_t)L.n * L.H * 4);
+  L.off_D = take((size_t)L.n * L.H * 4);
+  L.off_qS = take((size_t)L.N * L.H);
+  L.off_qD = take((size_t)L.N * L.H);
+  L.off_m = take((size_t)L.N * L.H * 4);
+  L.off_den = take((size_t)L.N * L.H * 4);
+  L.off_P = take((size_t)L.N * L.H * 4);
+  L.off_dD = take((size_t)L.N * L.H * 4);
+  L.off_qG = take((size_t)L.N * L.ldHD);
+  L.off_dal = take((size_t)L.E * L.H * 4);
+  L.off_dHp = take((size_t)L.n * L.HD * 4);
+  L.off_qdHp = take((size_t)L.n * L.ldHD);
+  L.off_dW64 = take((size_t)L.F * L.HD * 8);
+  L.total = o;
+  return L;
+}
+tango_status check_gat(const tango_graph* G, const tango_gat_params* p) {
+  TRY(check_graph(G, true));
+  if (!p || !p->W || !p->a_src || !p->a_dst) return TANGO_ERR_INVALID_ARG;
+  if (p->bits < 2 || p->bits > 8) return TANGO_ERR_BITS;
+  if (p->in_feats <= 0 || p->heads <= 0 || p->head_dim <= 0) return TANGO_ERR_SHAPE;
+  const int HD = p->heads * p->head_dim;
+  if (HD % 32 || HD < 64 || HD > 512) return TANGO_ERR_UNSUPPORTED;
+  const int vpl = HD / 32;
+  if (!(vpl == 2 || vpl == 4 || vpl == 8 || vpl == 16)) return TANGO_ERR_UNSUPPORTED;
+  if (!(p->heads == 1 || p->heads == 2 || p->heads == 4 || p->heads == 8)) return TANGO_ERR_UNSUPPORTED;
+  if (p->in_feats > 133144) return TANGO_ERR_OVERFLOW;
+  if (256 % p->head_dim && HD > 256) return TANGO_ERR_UNSUPPORTED;
+  return TANGO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+size_t tango_gat_ctx_bytes(const tango_graph* G, const tango_gat_params* p) {
+  if (check_gat(G, p) != TANGO_OK) return 0;
+  return gat_layout(G, p).total;
+}
+
+tango_status tango_gat_ctx_get_view(const tango_graph* G, const tango_gat_params* p, void* ctx,
+                                    tango_gat_ctx_view* v) {
+  TRY(check_gat(G, p));
+  if (!ctx || !v) return TANGO_ERR_INVALID_ARG;
+  const GatLayout L = gat_layout(G, p);
+  char* c = static_cast<char*>(ctx);
+  v->qH = (int8_t*)(c + L.off_qH); v->qW = (int8_t*)(c + L.off_qW); v->qWt = (int8_t*)(c + L.off_qWt);
+  v->qHp = (int8_t*)(c + L.off_qHp); v->qS = (int8_t*)(c + L.off_qS); v->qD = (int8_t*)(c + L.off_qD);
+  v->qG = (int8_t*)(c + L.off_qG); v->qdHp = (int8_t*)(c + L.off_qdHp);
+  v->ldF = L.ldF; v->ldHD = L.ldHD; v->ldFt = L.ldFt;
+  v->S = (float*)(c + L.off_S); v->D = (float*)(c + L.off_D); v->m = (float*)(c + L.off_m);
+  v->den = (float*)(c + L.off_den); v->P = (float*)(c + L.off_P); v->dD = (float*)(c + L.off_dD);
+  v->dHp = (float*)(c + L.off_dHp); v->dalpha = (float*)(c + L.off_dal);
+  v->scalars = (float*)(c + L.off_scal);
+  return TANGO_OK;
+}
+
+tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p, const float* H,
+                                 const float* amax_H_hint, tango_rng rng, uint32_t layer_id, void* ctx,
+                                 size_t ctx_bytes, float* H_out, float* amax_out, tango_comm* comm,
+                                 int32_t* dev_status, cudaStream_t st) {
+  TRY(check_gat(G, p));
+  TRY(check_comm(G, comm));
+  const GatLayout L = gat_layout(G, p);
+  if (!ctx || ctx_bytes < L.total) return TANGO_ERR_INVALID_ARG;
+  if ((L.n > 0 && (!H || !H_out))) return TANGO_ERR_INVALID_ARG;
+  char* c = static_cast<char*>(ctx);
+  unsigned* sc = reinterpret_cast<unsigned*>(c + L.off_scal);
+  float* scf = reinterpret_cast<float*>(sc);
+  int8_t* qH = (int8_t*)(c + L.off_qH);
+  int8_t* qW = (int8_t*)(c + L.off_qW);
+  int8_t* qWt = (int8_t*)(c + L.off_qWt);
+  int8_t* qHp = (int8_t*)(c + L.off_qHp);
+  float* S = (float*)(c + L.off_S);
+  float* D = (float*)(c + L.off_D);
+  int8_t* qS = (int8_t*)(c + L.off_qS);
+  int8_t* qD = (int8_t*)(c + L.off_qD);
+  float* m = (float*)(c + L.off_m);
+  float* den = (float*)(c + L.off_den);
+  const int64_t r0 = G->row_begin;
+  const GraphDev g = dev_graph(G);
+
+  TRY_CUDA(cudaMemsetAsync(sc, 0, SL_NSLOTS * 4, st));
+  // F1: amax(H) over all ranks (R28), Q(H)
+  if (amax_H_hint) {
+    TRY_CUDA(cudaMemcpyAsync(sc + SL_AMAX_H, amax_H_hint, 4, cudaMemcpyDeviceToDevice, st));
+  } else {
+    TRY(launch_status(launch_absmax(H, L.n, L.F, nullptr, sc + SL_AMAX_H, st)));
+    TRY(comm_max(comm, sc + SL_AMAX_H, 1, st));
+  }
+  TRY(launch_status(launch_quantize(H, L.n, L.F, nullptr, r0 * L.F, sc + SL_AMAX_H, p->bits, rng.seed, rng.step,
+                                    tag_of(layer_id, R_H), qH, L.ldF, nullptr, 0, scf + SL_S_H, dev_status, st)));
+  // F2: Q(W) (replicated; identical on every rank), row-major and transposed copies
+  TRY(launch_status(launch_absmax(p->W, L.F, L.HD, nullptr, sc + SL_AMAX_W, st)));
+  TRY(launch_status(launch_quantize(p->W, L.F, L.HD, nullptr, 0, sc + SL_AMAX_W, p->bits, rng.seed, rng.step,
+                                    tag_of(layer_id, R_W), qW, L.ldHD, qWt, L.ldFt, scf + SL_S_W, dev_status, st)));
+  // F3 phase A: acc = q_H·q_W on tcgen05; H′ = i2f(acc)·s_H s_W; S, D head dots; amax(H′), amax(S), amax(D)
+  GemmArgs ga{};
+  ga.A = qH; ga.lda = L.ldF; ga.a_mn = false;
+  ga.B = qWt; ga.ldb = L.ldFt; ga.b_mn = false;
+  ga.M = L.n; ga.N = L.HD; ga.K = L.F; ga.splits = 1;
+  ga.sA = scf + SL_S_H; ga.sB = scf + SL_S_W;
+  ga.mode = EPI_AMAX;
+  ga.amax_slot = sc + SL_AMAX_HP;
+  ga.a_src = p->a_src; ga.a_dst = p->a_dst; ga.head_dim = p->head_dim; ga.heads = p->heads;
+  ga.S = S; ga.Dd = D; ga.amax_S = sc + SL_AMAX_S; ga.amax_D = sc + SL_AMAX_D;
+  TRY(launch_status(launch_gemm(ga, st)));
+  TRY(comm_max(comm, sc + SL_AMAX_HP, 3, st));
+  // F4: phase B recomputes the MMA and emits q_H′ with Philox SR in the epilogue; then Q(S), Q(D)
+  GemmArgs gb = ga;
+  gb.mode = EPI_QUANT;
+  gb.a_src = nullptr; gb.a_dst = nullptr;
+  gb.amax_in = sc + SL_AMAX_HP; gb.bits = p->bits; gb.seed = rng.seed; gb.step = rng.step;
+  gb.tag = tag_of(layer_id, R_HP); gb.g_row0 = r0;
+  gb.q_out = qHp + r0 * L.ldHD; gb.ldq = L.ldHD; gb.scale_out = scf + SL_S_HP; gb.status = dev_status;
+  TRY(launch_status(launch_gemm(gb, st)));
+  TRY(launch_status(launch_quantize(S, L.n, L.H, nullptr, r0 * L.H, sc + SL_AMAX_S, p->bits, rng.seed, rng.step,
+                                    tag_of(layer_id, R_S), qS + r0 * L.H, L.H, nullptr, 0, scf + SL_S_S, dev_status,
+                                    st)));
+  TRY(launch_status(launch_quantize(D, L.n, L.H, nullptr, r0 * L.H, sc + SL_AMAX_D, p->bits, rng.seed, rng.step,
+                                    tag_of(layer_id, R_D), qD + r0 * L.H, L.H, nullptr, 0, scf + SL_S_D, dev_status,
+                                    st)));
+  TRY(comm_gather_rows(comm, qHp, (size_t)L.ldHD, st));
+  TRY(comm_gather_rows(comm, qS, (size_t)L.H, st));
+  TRY(comm_gather_rows(comm, qD, (size_t)L.H, st));
+  // F5 + F6: one destination-row kernel (③ SDDMM-add + LeakyReLU, ④ softmax, ⑤ SPMM)
+  if (amax_out) TRY_CUDA(cudaMemsetAsync(amax_out, 0, 4, st));
+  GatFwdDstArgs fa{};
+  fa.g = g; fa.d = {p->heads, p->head_dim, (int)L.HD}; fa.slope = p->neg_slope;
+  fa.qS = qS; fa.amax_S = sc + SL_AMAX_S; fa.qD = qD; fa.amax_D = sc + SL_AMAX_D;
+  fa.qHp = qHp; fa.ldHp = L.ldHD; fa.amax_Hp = sc + SL_AMAX_HP; fa.bits = p->bits;
+  fa.Hout = H_out; fa.m = m; fa.den = den; fa.amax_out = reinterpret_cast<unsigned*>(amax_out);
+  TRY(launch_status(launch_gat_fwd_dst(fa, st)));
+  TRY(comm_max(comm, amax_out, amax_out ? 1 : 0, st));
+  TRY(comm_gather_rows(comm, m, (size_t)L.H * 4, st));
+  TRY(comm_gather_rows(comm, den, (size_t)L.H * 4, st));
+  return TANGO_OK;
+}
+
+tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p, void* ctx, size_t ctx_bytes,
+                                 const float* dH_out, const float* amax_dH_hint, tango_rng rng, uint32_t layer_id,
+                                 float* dH, float* dW, float* da_src, float* da_dst, float* amax_dH, tango_comm* comm,
+                                 int32_t* dev_status, cudaStream_t st) {
+  TRY(check_gat(G, p));
+  TRY(check_comm(G, comm));
+  const GatLayout L = gat_layout(G, p);
+  if (!ctx || ctx_bytes < L.total) return TANGO_ERR_INVALID_ARG;
+  if (!dW || !da_src || !da_dst || (L.n > 0 && !dH_out)) return TANGO_ERR_INVALID_ARG;
+  char* c = static_cast<char*>(ctx);
+  unsigned* sc = reinterpret_cast<unsigned*>(c + L.off_scal);
+  float* scf = reinterpret_cast<float*>(sc);
+  int8_t* qH = (int8_t*)(c + L.off_qH);
+  int8_t* qW = (int8_t*)(c + L.off_qW);
+  int8_t* qHp = (int8_t*)(c + L.off_qHp);
+  int8_t* qS = (int8_t*)(c + L.off_qS);
+  int8_t* qD = (int8_t*)(c + L.off_qD);
+  float* m = (float*)(c + L.off_m);
+  float* den = (float*)(c + L.off_den);
+  float* P = (float*)(c + L.off_P);
+  float* dD = (float*)(c + L.off_dD);
+  int8_t* qG = (int8_t*)(c + L.off_qG);
+  float* dal = (float*)(c + L.off_dal);
+  float* dHp = (float*)(c + L.off_dHp);
+  int8_t* qdHp = (int8_t*)(c + L.off_qdHp);
+  int64_t* dW64 = (int64_t*)(c + L.off_dW64);
+  const int64_t r0 = G->row_begin;
+  const GraphDev g = dev_graph(G);
+
+  TRY_CUDA(cudaMemsetAsync(sc + SL_AMAX_G, 0, 8, st));   // amax_G, amax_dH′
+  TRY_CUDA(cudaMemsetAsync(da_src, 0, L.HD * 4, st));
+  TRY_CUDA(cudaMemsetAsync(da_dst, 0, L.HD * 4, st));
+  TRY_CUDA(cudaMemsetAsync(dW64, 0, L.F * L.HD * 8, st));
+  // B1: Q(∂H_out), shared by ⑤′ and ⑤″
+  if (amax_dH_hint) {
+    TRY_CUDA(cudaMemcpyAsync(sc + SL_AMAX_G, amax_dH_hint, 4, cudaMemcpyDeviceToDevice, st));
+  } else {
+    TRY(launch_status(launch_absmax(dH_out, L.n, L.HD, nullptr, sc + SL_AMAX_G, st)));
+    TRY(comm_max(comm, sc + SL_AMAX_G, 1, st));
+  }
+  TRY(launch_status(launch_quantize(dH_out, L.n, L.HD, nullptr, r0 * L.HD, sc + SL_AMAX_G, p->bits, rng.seed,
+                                    rng.step, tag_of(layer_id, R_G), qG + r0 * L.ldHD, L.ldHD, nullptr, 0,
+                                    scf + SL_S_G, dev_status, st)));
+  TRY(comm_gather_rows(comm, qG, (size_t)L.ldHD, st));
+  // B2-B4: destination rows
+  GatBwdDstArgs da{};
+  da.g = g; da.d = {p->heads, p->head_dim, (int)L.HD}; da.slope = p->neg_slope; da.bits = p->bits;
+  da.qS = qS; da.amax_S = sc + SL_AMAX_S; da.qD = qD; da.amax_D = sc + SL_AMAX_D;
+  da.qHp = qHp; da.ldHp = L.ldHD; da.amax_Hp = sc + SL_AMAX_HP;
+  da.qG = qG; da.ldG = L.ldHD; da.amax_G = sc + SL_AMAX_G;
+  da.m = m; da.den = den; da.dalpha = dal; da.P = P; da.dD = dD;
+  TRY(launch_status(launch_gat_bwd_dst(da, st)));
+  TRY(comm_gather_rows(comm, P, (size_t)L.H * 4, st));
+  // B5-B7: source rows
+  GatBwdSrcArgs sa{};
+  sa.g = g; sa.d = da.d; sa.slope = p->neg_slope; sa.bits = p->bits;
+  sa.qS = qS; sa.amax_S = da.amax_S; sa.qD = qD; sa.amax_D = da.amax_D;
+  sa.qHp = qHp; sa.ldHp = L.ldHD; sa.amax_Hp = da.amax_Hp;
+  sa.qG = qG; sa.ldG = L.ldHD; sa.amax_G = da.amax_G;
+  sa.m = m; sa.den = den; sa.P = P; sa.dD = dD; sa.a_src = p->a_src; sa.a_dst = p->a_dst;
+  sa.dHp = dHp; sa.amax_dHp = sc + SL_AMAX_DHP; sa.da_src = da_src; sa.da_dst = da_dst;
+  TRY(launch_status(launch_gat_bwd_src(sa, st)));
+  TRY(comm_max(comm, sc + SL_AMAX_DHP, 1, st));
+  TRY(comm_sum_f32(comm, da_src, (size_t)L.HD, st));
+  TRY(comm_sum_f32(comm, da_dst, (size_t)L.HD, st));
+  // B8: Q(∂H′)
+  TRY(launch_status(launch_quantize(dHp, L.n, L.HD, nullptr, r0 * L.HD, sc + SL_AMAX_DHP, p->bits, rng.seed,
+                                    rng.step, tag_of(layer_id, R_DHP), qdHp, L.ldHD, nullptr, 0, scf + SL_S_DHP,
+                                    dev_status, st)));
+  // B9 ①′: ∂H = q_dH′·q_Wᵀ (K = HD) and ∂W = q_Hᵀ·q_dH′ (K = n, split-K int64)
+  if (dH) {
+    GemmArgs gh{};
+    gh.A = qdHp; gh.lda = L.ldHD; gh.a_mn = false;
+    gh.B = qW; gh.ldb = L.ldHD; gh.b_mn = false;
+    gh.M = L.n; gh.N = L.F; gh.K = L.HD; gh.splits = 1;
+    gh.sA = scf + SL_S_DHP; gh.sB = scf + SL_S_W;
+    gh.mode = EPI_STORE; gh.C = dH; gh.ldc = L.F;
+    TRY(launch_status(launch_gemm(gh, st)));
+    if (amax_dH) {
+      TRY_CUDA(cudaMemsetAsync(amax_dH, 0, 4, st));
+      TRY(launch_status(launch_absmax(dH, L.n, L.F, nullptr, reinterpret_cast<unsigned*>(amax_dH), st)));
+      TRY(comm_max(comm, amax_dH, 1, st));
+    }
+  }
+  GemmArgs gw{};
+  gw.A = qH; gw.lda = L.ldF; gw.a_mn = true;
+  gw.B = qdHp; gw.ldb = L.ldHD; gw.b_mn = true;
+  gw.M = L.F; gw.N = L.HD; gw.K = L.n;
+  {
+    const int64_t tiles = ((L.F + 127) / 128) * ((L.HD + 255) / 256);
+    const int64_t kb = (L.n + 127) / 128;
+    int64_t splits = (num_sms() + tiles - 1) / tiles;
+    const int64_t min_splits = (L.n + 131071) / 131072;
+    if (splits < min_splits) splits = min_splits;
+    if (splits > kb) splits = kb > 0 ? kb : 1;
+    gw.splits = (int)splits;
+  }
+  gw.mode = EPI_ATOMIC64; gw.C = dW64; gw.ldc = L.HD;
+  TRY(launch_status(launch_gemm(gw, st)));
+  TRY(comm_sum_i64(comm, dW64, (size_t)(L.F * L.HD), st));
+  TRY(launch_status(launch_finalize_dw(dW64, L.F * L.HD, scf + SL_S_H, scf + SL_S_DHP, dW, st)));
+  return TANGO_OK;
+}
+
+}  // extern "C"
+
+// ================================================================== GCN
+namespace {
+struct GcnLayout {
+  int64_t n, N, F, O, ldF, ldO;
+  size_t off_scal, off_ns, off_nd, off_qX, off_qW, off_qWt, off_qYs, off_ia, off_qGs, off_ib, off_dY, off_qdY,
+      off_dW64, total;
+};
+GcnLayout gcn_layout(const tango_graph* G, const tango_gcn_params* p) {
+  GcnLayout L{};
+  L.n = G->row_end - G->row_begin; L.N = G->n_global; L.F = p->in_feats; L.O = p->out_feats;
+  L.ldF = round_up(L.F, 32); L.ldO = round_up(L.O, 32);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t at = o; o = align256(o + bytes); return at; };
+  L.off_scal = take(SL_NSLOTS * 4);
+  L.off_ns = take((size_t)L.n * 4);
+  L.off_nd = take((size_t)L.n * 4);
+  L.off_qX = take((size_t)L.n * L.ldF);
+  L.off_qW = take((size_t)L.F * L.ldO);
+  L.off_qWt = take((size_t)L.O * L.ldF);
+  L.off_qYs = take((size_t)L.N * L.ldO);
+  L.off_ia = take((size_t)L.n * L.O * 4);
+  L.off_qGs = take((size_t)L.N * L.ldO);
+  L.off_ib = take((size_t)L.n * L.O * 4);
+  L.off_dY = take((size_t)L.n * L.O * 4);
+  L.off_qdY = take((size_t)L.n * L.ldO);
+  L.off_dW64 = take((size_t)L.F * L.O * 8);
+  L.total = o;
+  return L;
+}
+tango_status check_gcn(const tango_graph* G, const tango_gcn_params* p) {
+  TRY(check_graph(G, true));
+  if (!p || !p->W) return TANGO_ERR_INVALID_ARG;
+  if (p->bits < 2 || p->bits > 8) return TANGO_ERR_BITS;
+  if (p->in_feats <= 0 || p->out_feats <= 0) return TANGO_ERR_SHAPE;
+  if (p->in_feats > 133144 || p->out_feats > 133144) return TANGO_ERR_OVERFLOW;
+  if (p->out_feats % 8) return TANGO_ERR_UNSUPPORTED;
+  return TANGO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+size_t tango_gcn_ctx_bytes(const tango_graph* G, const tango_gcn_params* p) {
+  if (check_gcn(G, p) != TANGO_OK) return 0;
+  return gcn_layout(G, p).total;
+}
+
+tango_status tango_gcn_ctx_get_view(const tango_graph* G, const tango_gcn_params* p, void* ctx,
+                                    tango_gcn_ctx_view* v) {
+  TRY(check_gcn(G, p));
+  if (!ctx || !v) return TANGO_ERR_INVALID_ARG;
+  const GcnLayout L = gcn_layout(G, p);
+  char* c = static_cast<char*>(ctx);
+  v->qX = (int8_t*)(c + L.off_qX); v->qW = (int8_t*)(c + L.off_qW); v->qWt = (int8_t*)(c + L.off_qWt);
+  v->qYs = (int8_t*)(c + L.off_qYs); v->qGs = (int8_t*)(c + L.off_qGs); v->qdY = (int8_t*)(c + L.off_qdY);
+  v->ldF = L.ldF; v->ldO = L.ldO; v->ldFt = L.ldF;
+  v->ia = (int32_t*)(c + L.off_ia); v->ib = (int32_t*)(c + L.off_ib);
+  v->scalars = (float*)(c + L.off_scal);
+  return TANGO_OK;
+}
+
+tango_status tango_gcn_layer_fwd(const tango_graph* G, const tango_gcn_params* p, const float* X,
+                                 const float* amax_X_hint, tango_rng rng, uint32_t layer_id, void* ctx,
+                                 size_t ctx_bytes, float* out, float* amax_out, tango_comm* comm, int32_t* dev_status,
+                                 cudaStream_t st) {
+  TRY(check_gcn(G, p));
+  TRY(check_comm(G, comm));
+  const GcnLayout L = gcn_layout(G, p);
+  if (!ctx || ctx_bytes < L.total) return TANGO_ERR_INVALID_ARG;
+  if (L.n > 0 && (!X || !out)) return TANGO_ERR_INVALID_ARG;
+  char* c = static_cast<char*>(ctx);
+  unsigned* sc = reinterpret_cast<unsigned*>(c + L.off_scal);
+  float* scf = reinterpret_cast<float*>(sc);
+  float* ns = (float*)(c + L.off_ns);
+  float* nd = (float*)(c + L.off_nd);
+  int8_t* qX = (int8_t*)(c + L.off_qX);
+  int8_t* qW = (int8_t*)(c + L.off_qW);
+  int8_t* qWt = (int8_t*)(c + L.off_qWt);
+  int8_t* qYs = (int8_t*)(c + L.off_qYs);
+  int32_t* ia = (int32_t*)(c + L.off_ia);
+  const int64_t r0 = G->row_begin;
+  const GraphDev g = dev_graph(G);
+  TRY_CUDA(cudaMemsetAsync(sc, 0, SL_NSLOTS * 4, st));
+  TRY(launch_status(launch_gcn_norms(g, ns, nd, st)));
+  if (amax_X_hint) {
+    TRY_CUDA(cudaMemcpyAsync(sc + SL_AMAX_H, amax_X_hint, 4, cudaMemcpyDeviceToDevice, st));
+  } else {
+    TRY(launch_status(launch_absmax(X, L.n, L.F, nullptr, sc + SL_AMAX_H, st)));
+    TRY(comm_max(comm, sc + SL_AMAX_H, 1, st));
+  }
+  TRY(launch_status(launch_quantize(X, L.n, L.F, nullptr, r0 * L.F, sc + SL_AMAX_H, p->bits, rng.seed, rng.step,
+                                    tag_of(layer_id, R_H), qX, L.ldF, nullptr, 0, scf + SL_S_H, dev_status, st)));
+  TRY(launch_status(launch_absmax(p->W, L.F, L.O, nullptr, sc + SL_AMAX_W, st)));
+  TRY(launch_status(launch_quantize(p->W, L.F, L.O, nullptr, 0, sc + SL_AMAX_W, p->bits, rng.seed, rng.step,
+                                    tag_of(layer_id, R_W), qW, L.ldO, qWt, L.ldF, scf + SL_S_W, dev_status, st)));
+  // G2 phase A: Ys = (i2f(acc)·s_X s_W)·ns[u], amax(Ys); phase B: q_Ys
+  GemmArgs ga{};
+  ga.A = qX; ga.lda = L.ldF; ga.B = qWt; ga.ldb = L.ldF;
+  ga.M = L.n; ga.N = L.O; ga.K = L.F; ga.splits = 1;
+  ga.sA = scf + SL_S_H; ga.sB = scf + SL_S_W; ga.rowscale = ns;
+  ga.mode = EPI_AMAX; ga.amax_slot = sc + SL_AMAX_HP;
+  TRY(launch_status(launch_gemm(ga, st)));
+  TRY(comm_max(comm, sc + SL_AMAX_HP, 1, st));
+  GemmArgs gb = ga;
+  gb.mode = EPI_QUANT; gb.amax_in = sc + SL_AMAX_HP; gb.bits = p->bits; gb.seed = rng.seed; gb.step = rng.step;
+  gb.tag = tag_of(layer_id, R_YS); gb.g_row0 = r0; gb.q_out = qYs + r0 * L.ldO; gb.ldq = L.ldO;
+  gb.scale_out = scf + SL_S_HP; gb.status = dev_status;
+  TRY(launch_status(launch_gemm(gb, st)));
+  TRY(comm_gather_rows(comm, qYs, (size_t)L.ldO, st));
+  // G3: int32 SPMM; out = ((float)ia · s_Ys)·nd[v]
+  if (amax_out) TRY_CUDA(cudaMemsetAsync(amax_out, 0, 4, st));
+  TRY(launch_status(launch_spmm_sum(g, TANGO_IN, (int)L.O, qYs, L.ldO, scf + SL_S_HP, nd, out, ia,
+                                    reinterpret_cast<unsigned*>(amax_out), st)));
+  TRY(comm_max(comm, amax_out, amax_out ? 1 : 0, st));
+  return TANGO_OK;
+}
+
+tango_status tango_gcn_layer_bwd(const tango_graph* G, const tango_gcn_params* p, void* ctx, size_t ctx_bytes,
+                                 const float* dout, tango_rng rng, uint32_t layer_id, float* dX, float* dW,
+                                 tango_comm* comm, int32_t* dev_status, cudaStream_t st) {
+  TRY(check_gcn(G, p));
+  TRY(check_comm(G, comm));
+  const GcnLayout L = gcn_layout(G, p);
+  if (!ctx || ctx_bytes < L.total) return TANGO_ERR_INVALID_ARG;
+  if (!dW || (L.n > 0 && !dout)) return TANGO_ERR_INVALID_ARG;
+  char* c = static_cast<char*>(ctx);
+  unsigned* sc = reinterpret_cast<unsigned*>(c + L.off_scal);
+  float* scf = reinterpret_cast<float*>(sc);
+  float* ns = (float*)(c + L.off_ns);
+  float* nd = (float*)(c + L.off_nd);
+  int8_t* qX = (int8_t*)(c + L.off_qX);
+  int8_t* qW = (int8_t*)(c + L.off_qW);
+  int8_t* qGs = (int8_t*)(c + L.off_qGs);
+  int32_t* ib = (int32_t*)(c + L.off_ib);
+  float* dY = (float*)(c + L.off_dY);
+  int8_t* qdY = (int8_t*)(c + L.off_qdY);
+  int64_t* dW64 = (int64_t*)(c + L.off_dW64);
+  const int64_t r0 = G->row_begin;
+  const GraphDev g = dev_graph(G);
+  TRY_CUDA(cudaMemsetAsync(sc + SL_AMAX_G, 0, 8, st));
+  TRY_CUDA(cudaMemsetAsync(dW64, 0, L.F * L.O * 8, st));
+  // Gs = ∂out·nd[v] -> q_Gs
+  TRY(launch_status(launch_absmax(dout, L.n, L.O, nd, sc + SL_AMAX_G, st)));
+  TRY(comm_max(comm, sc + SL_AMAX_G, 1, st));
+  TRY(launch_status(launch_quantize(dout, L.n, L.O, nd, r0 * L.O, sc + SL_AMAX_G, p->bits, rng.seed, rng.step,
+                                    tag_of(layer_id, R_GS), qGs + r0 * L.ldO, L.ldO, nullptr, 0, scf + SL_S_G,
+                                    dev_status, st)));
+  TRY(comm_gather_rows(comm, qGs, (size_t)L.ldO, st));
+  // reverse int32 SPMM: ib[u] = Σ_{u→v} q_Gs[v]; ∂Y = ((float)ib·s_Gs)·ns[u]
+  TRY(launch_status(launch_spmm_sum(g, TANGO_OUT, (int)L.O, qGs, L.ldO, scf + SL_S_G, ns, dY, ib,
+                                    sc + SL_AMAX_DHP, st)));
+  TRY(comm_max(comm, sc + SL_AMAX_DHP, 1, st));
+  TRY(launch_status(launch_quantize(dY, L.n, L.O, nullptr, r0 * L.O, sc + SL_AMAX_DHP, p->bits, rng.seed, rng.step,
+                                    tag_of(layer_id, R_DY), qdY, L.ldO, nullptr, 0, scf + SL_S_DHP, dev_status,
+                                    st)));
+  if (dX) {
+    GemmArgs gh{};
+    gh.A = qdY; gh.lda = L.ldO; gh.B = qW; gh.ldb = L.ldO;
+    gh.M = L.n; gh.N = L.F; gh.K = L.O; gh.splits = 1;
+    gh.sA = scf + SL_S_DHP; gh.sB = scf + SL_S_W;
+    gh.mode = EPI_STORE; gh.C = dX; gh.ldc = L.F;
+    TRY(launch_status(launch_gemm(gh, st)));
+  }
+  GemmArgs gw{};
+  gw.A = qX; gw.lda = L.ldF; gw.a_mn = true;
+  gw.B = qdY; gw.ldb = L.ldO; gw.b_mn = true;
+  gw.M = L.F; gw.N = L.O; gw.K = L.n;
+  {
+    const int64_t tiles = ((L.F + 127) / 128) * ((L.O + 255) / 256);
+    const int64_t kb = (L.n + 127) / 128;
+    int64_t splits = (num_sms() + tiles - 1) / tiles;
+    const int64_t min_splits = (L.n + 131071) / 131072;
+    if (splits < min_splits) splits = min_splits;
+    if (splits > kb) splits = kb > 0 ? kb : 1;
+    gw.splits = (int)splits;
+  }
+  gw.mode = EPI_ATOMIC64; gw.C = dW64; gw.ldc = L.O;
+  TRY(launch_status(launch_gemm(gw, st)));
+  TRY(comm_sum_i64(comm, dW64, (size_t)(L.F * L.O), st));
+  TRY(launch_status(launch_finalize_dw(dW64, L.F * L.O, scf + SL_S_H, scf + SL_S_DHP, dW, st)));
+  return TANGO_OK;
+}
+
+// ================================================================== communicator
+int32_t tango_comm_unique_id_bytes(void) { return (int32_t)sizeof(ncclUniqueId); }
+
+tango_status tango_comm_get_unique_id(void* id_out) {
+  if (!id_out) return TANGO_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  TRY_NCCL(ncclGetUniqueId(&id));
+  memcpy(id_out, &id, sizeof(id));
+  return TANGO_OK;
+}
+
+tango_status tango_comm_init(tango_comm** out, const void* unique_id, int32_t nranks, int32_t rank) {
+  if (!out || !unique_id || nranks <= 0 || rank < 0 || rank >= nranks) return TANGO_ERR_INVALID_ARG;
+  tango_comm* c = new (std::nothrow) tango_comm();
+  if (!c) return TANGO_ERR_INVALID_ARG;
+  c->nranks = nranks;
+  c->rank = rank;
+  ncclUniqueId id;
+  memcpy(&id, unique_id, sizeof(id));
+  ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
+  if (r != ncclSuccess) {
+    fprintf(stderr, "[tango] ncclCommInitRank: %s\n", ncclGetErrorString(r));
+    delete c;
+    return TANGO_ERR_NCCL;
+  }
+  *out = c;
+  return TANGO_OK;
+}
+
+tango_status tango_comm_set_partition(tango_comm* c, const int64_t* row_starts) {
+  if (!c || !row_starts) return TANGO_ERR_INVALID_ARG;
+  c->starts.assign(row_starts, row_starts + c->nranks + 1);
+  for (int r = 0; r < c->nranks; ++r)
+    if (c->starts[r] > c->starts[r + 1]) return TANGO_ERR_SHAPE;
+  return TANGO_OK;
+}
+
+tango_status tango_comm_destroy(tango_comm* c) {
+  if (!c) return TANGO_ERR_INVALID_ARG;
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+  return TANGO_OK;
+}
+
+}  // extern "C"

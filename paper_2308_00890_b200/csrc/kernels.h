@@ -1,0 +1,119 @@
+// kernels.h — internal launcher declarations of libtango (not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace tango {
+
+int num_sms();
+
+// ---- quant.cu
+cudaError_t launch_absmax(const float* x, int64_t rows, int64_t cols, const float* rowscale, unsigned* slot,
+                          cudaStream_t st);
+cudaError_t launch_quantize(const float* x, int64_t rows, int64_t cols, const float* rowscale, int64_t g0,
+                            const unsigned* amax_slot, int bits, uint64_t seed, uint32_t step, uint32_t tag,
+                            int8_t* q, int64_t ld, int8_t* qt, int64_t ldt, float* scale_out, int32_t* status,
+                            cudaStream_t st);
+
+// ---- gemm_tc.cu : tcgen05 int8 GEMM with fused epilogues
+enum EpiMode : int {
+  EPI_AMAX = 0,     // v = i2f(acc)*sAB[*rowscale]; amax(|v|); optional per-head dots S = v·a_src, D = v·a_dst
+  EPI_QUANT = 1,    // v as above -> SR quantize with the amax of a previous EPI_AMAX pass -> int8 out
+  EPI_STORE = 2,    // v -> fp32 out [M][ldc]
+  EPI_I32 = 3,      // raw int32 accumulator -> out [M][ldc]
+  EPI_ATOMIC64 = 4  // raw accumulator atomically added into int64 out [M][ldc] (split-K)
+};
+
+struct GemmArgs {
+  // operands
+  const int8_t* A; int64_t lda; bool a_mn;  // K-major: A[M][lda]; MN-major: A[K][lda]
+  const int8_t* B; int64_t ldb; bool b_mn;  // K-major: B[N][ldb]; MN-major: B[K][ldb]
+  int64_t M, N, K;
+  int splits;                               // split-K count (EPI_ATOMIC64 only)
+  // scales: sAB = sA * sB (device scalars, may be null for raw modes)
+  const float* sA; const float* sB;
+  const float* rowscale;                    // optional per-row multiplier (GCN ns)
+  int mode;
+  // EPI_AMAX
+  unsigned* amax_slot;                      // |v| max
+  const float* a_src; const float* a_dst;   // optional head dots
+  int head_dim;                             // D (columns per head)
+  float* S; float* Dd; int heads;           // [M][heads] outputs of the head dots
+  unsigned* amax_S; unsigned* amax_D;
+  // EPI_QUANT
+  const unsigned* amax_in; int bits; uint64_t seed; uint32_t step; uint32_t tag; int64_t g_row0;
+  int8_t* q_out; int64_t ldq; float* scale_out; int32_t* status;
+  // EPI_STORE / EPI_I32 / EPI_ATOMIC64
+  void* C; int64_t ldc;
+};
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st);
+
+// ---- gat.cu : fused GAT destination / source row kernels and standalone sparse primitives
+struct GatDims { int heads, head_dim, hd; };
+struct GraphDev {
+  int64_t n_local, row_begin;
+  const int64_t* in_ptr; const int32_t* in_src;
+  const int64_t* out_ptr; const int32_t* out_dst; const int32_t* out_eid;
+  int chunk;
+};
+
+struct GatFwdDstArgs {
+  GraphDev g; GatDims d; float slope;
+  const int8_t* qS; const unsigned* amax_S;   // [N][H]
+  const int8_t* qD; const unsigned* amax_D;   // [N][H] (rows row_begin.. used)
+  const int8_t* qHp; int64_t ldHp; const unsigned* amax_Hp; int bits;   // [N][ldHp]
+  float* Hout; float* m; float* den;          // Hout [n_local][HD]; m, den [N][H] (own rows written)
+  unsigned* amax_out;
+};
+cudaError_t launch_gat_fwd_dst(const GatFwdDstArgs& a, cudaStream_t st);
+
+struct GatBwdDstArgs {
+  GraphDev g; GatDims d; float slope; int bits;
+  const int8_t* qS; const unsigned* amax_S;
+  const int8_t* qD; const unsigned* amax_D;
+  const int8_t* qHp; int64_t ldHp; const unsigned* amax_Hp;
+  const int8_t* qG; int64_t ldG; const unsigned* amax_G;   // [N][ldG]
+  const float* m; const float* den;          // [N][H]
+  float* dalpha;                             // scratch [e_in][H]
+  float* P; float* dD;                       // [N][H] own rows written
+};
+cudaError_t launch_gat_bwd_dst(const GatBwdDstArgs& a, cudaStream_t st);
+
+struct GatBwdSrcArgs {
+  GraphDev g; GatDims d; float slope; int bits;
+  const int8_t* qS; const unsigned* amax_S;
+  const int8_t* qD; const unsigned* amax_D;
+  const int8_t* qHp; int64_t ldHp; const unsigned* amax_Hp;
+  const int8_t* qG; int64_t ldG; const unsigned* amax_G;
+  const float* m; const float* den; const float* P;   // [N][H]
+  const float* dD;                                    // [N][H] (own rows)
+  const float* a_src; const float* a_dst;
+  float* dHp; unsigned* amax_dHp;                     // [n_local][HD]
+  float* da_src; float* da_dst;                       // [HD], accumulated with atomics (pre-zeroed)
+};
+cudaError_t launch_gat_bwd_src(const GatBwdSrcArgs& a, cudaStream_t st);
+
+// standalone primitives (unfused; used by the primitive C-ABI entry points)
+cudaError_t launch_sddmm_add(const GraphDev& g, int heads, const int8_t* qS, const float* sS, const int8_t* qD,
+                             const float* sD, float slope, float* e_pre, float* el, cudaStream_t st);
+cudaError_t launch_sddmm_dot(const GraphDev& g, int heads, int hd_total, const int8_t* qA, int64_t lda,
+                             const float* sA, const int8_t* qB, int64_t ldb, const float* sB, float* out,
+                             int32_t* acc, cudaStream_t st);
+cudaError_t launch_edge_softmax(const GraphDev& g, int heads, const float* el, float* m, float* den, float* alpha,
+                                cudaStream_t st);
+cudaError_t launch_softmax_bwd(const GraphDev& g, int heads, const float* alpha, const float* dalpha,
+                               const float* e_pre, float slope, float* P, float* dEp, cudaStream_t st);
+cudaError_t launch_edge_sum(const GraphDev& g, int dir, int heads, const float* x, float* out, cudaStream_t st);
+cudaError_t launch_spmm_w(const GraphDev& g, int dir, int heads, int cols, const float* w, const int8_t* qX,
+                          int64_t ldx, const float* sX, float* out, cudaStream_t st);
+cudaError_t launch_spmm_sum(const GraphDev& g, int dir, int cols, const int8_t* qX, int64_t ldx, const float* sX,
+                            const float* rowscale, float* out, int32_t* out_i32, unsigned* amax_out,
+                            cudaStream_t st);
+
+// misc
+cudaError_t launch_finalize_dw(const int64_t* acc, int64_t count, const float* sA, const float* sB, float* out,
+                               cudaStream_t st);
+cudaError_t launch_gcn_norms(const GraphDev& g, float* ns, float* nd, cudaStream_t st);
+
+}  // namespace tango

@@ -1,0 +1,154 @@
+// quant.cu — dedicated quantization pass (§3.3: "a dedicated quantization kernel would
+// read 32-bit input floating-point matrices sequentially once and write the 8-bit quantized
+// matrices out, again, sequentially and once") with tensor-level dynamic symmetric scaling
+// and Philox stochastic rounding (Eq.3; readings R1-R7).
+//
+// Two kernels: k_absmax (HBM-bound read, warp/block max + one atomicMax per block) and
+// k_quantize (one Philox call per group of 8 consecutive elements, 16-B loads, 8-B stores).
+#include "kernels.h"
+
+namespace tango {
+
+// amax over |x * rowscale[row]| (rowscale optional, reading R26 for GCN's Gs = dout*nd)
+__global__ void __launch_bounds__(256) k_absmax(const float* __restrict__ x, int64_t rows, int64_t cols,
+                                                const float* __restrict__ rowscale, unsigned* __restrict__ slot) {
+  const int64_t count = rows * cols;
+  float m = 0.0f;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  if (rowscale == nullptr && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    const int64_t n4 = count >> 2;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int64_t i = tid; i < n4; i += nthr) {
+      float4 v = __ldg(x4 + i);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      // NaN must dominate: fmaxf drops NaN, so fold it explicitly
+      if (!(fabsf(v.x) <= 3.4e38f) || !(fabsf(v.y) <= 3.4e38f) || !(fabsf(v.z) <= 3.4e38f) ||
+          !(fabsf(v.w) <= 3.4e38f))
+        m = __uint_as_float(0x7FC00000u);
+    }
+    for (int64_t i = (n4 << 2) + tid; i < count; i += nthr) {
+      float a = fabsf(x[i]);
+      m = (a <= 3.4e38f) ? fmaxf(m, a) : __uint_as_float(0x7FC00000u);
+    }
+  } else {
+    for (int64_t i = tid; i < count; i += nthr) {
+      float v = x[i];
+      if (rowscale) v = __fmul_rn(v, rowscale[i / cols]);
+      float a = fabsf(v);
+      m = (a <= 3.4e38f) ? fmaxf(m, a) : __uint_as_float(0x7FC00000u);
+    }
+  }
+  // block reduce on bit patterns (non-negative floats and NaN order as unsigned)
+  unsigned b = __float_as_uint(m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+  __shared__ unsigned red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    b = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    if (threadIdx.x == 0) atomicMax(slot, b);
+  }
+}
+
+// q[i][j] = SR(x[i][j] * rowscale[i] * r) for the logical tensor rows x cols whose element (i, j)
+// has global index g = g0 + i*cols + j.  Out: q[i*ld + j] (and, if qt, the transpose qt[j*ldt + i]).
+__global__ void __launch_bounds__(256) k_quantize(const float* __restrict__ x, int64_t rows, int64_t cols,
+                                                  const float* __restrict__ rowscale, int64_t g0,
+                                                  const unsigned* __restrict__ amax_slot, int bits, uint64_t seed,
+                                                  uint32_t step, uint32_t tag, int8_t* __restrict__ q, int64_t ld,
+                                                  int8_t* __restrict__ qt, int64_t ldt, float* __restrict__ scale_out,
+                                                  int32_t* __restrict__ status) {
+  const Scale sc = scale_from_amax(amax_load(amax_slot), bits);
+  const int qmax = (1 << (bits - 1)) - 1;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid == 0) {
+    if (scale_out) *scale_out = sc.s;
+    if (sc.bad && status) atomicExch(status, ST_NONFINITE);
+  }
+  const int64_t count = rows * cols;
+  const int64_t blk0 = g0 >> 3, blk1 = (g0 + count + 7) >> 3;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const bool fast = (rowscale == nullptr) && (qt == nullptr) && ((g0 & 7) == 0) && ((cols & 7) == 0) &&
+                    ((ld & 7) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  for (int64_t blk = blk0 + tid; blk < blk1; blk += nthr) {
+    const SR8 rnd = sr_draw8((uint64_t)blk, tag, step, seed);
+    const int64_t gs = blk << 3;
+    if (fast) {
+      const int64_t e = gs - g0;  // first local element, multiple of 8, within one row
+      const int64_t i = e / cols, j = e - i * cols;
+      const float4* src = reinterpret_cast<const float4*>(x + e);
+      const float4 a = __ldg(src), b = __ldg(src + 1);
+      const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int qq = sr_quant(v[k], sc.r, sr_half(rnd, k), qmax);
+        const uint32_t byte = (uint32_t)(qq & 0xFF);
+        if (k < 4) lo |= byte << (8 * k);
+        else hi |= byte << (8 * (k - 4));
+      }
+      *reinterpret_cast<uint2*>(q + i * ld + j) = make_uint2(lo, hi);
+    } else {
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        const int64_t g = gs + k;
+        if (g < g0 || g >= g0 + count) continue;
+        const int64_t e = g - g0;
+        const int64_t i = e / cols, j = e - i * cols;
+        float v = x[e];
+        if (rowscale) v = __fmul_rn(v, rowscale[i]);
+        const int qq = sr_quant(v, sc.r, sr_half(rnd, k), qmax);
+        if (q) q[i * ld + j] = (int8_t)qq;
+        if (qt) qt[j * ldt + i] = (int8_t)qq;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static int grid_for(int64_t work, int threads, int per_sm = 8) {
+  int64_t g = (work + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * per_sm;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_absmax(const float* x, int64_t rows, int64_t cols, const float* rowscale, unsigned* slot,
+                          cudaStream_t st) {
+  if (rows * cols == 0) return cudaSuccess;
+  k_absmax<<<grid_for(rows * cols / 4 + 1, 256), 256, 0, st>>>(x, rows, cols, rowscale, slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize(const float* x, int64_t rows, int64_t cols, const float* rowscale, int64_t g0,
+                            const unsigned* amax_slot, int bits, uint64_t seed, uint32_t step, uint32_t tag,
+                            int8_t* q, int64_t ld, int8_t* qt, int64_t ldt, float* scale_out, int32_t* status,
+                            cudaStream_t st) {
+  const int64_t count = rows * cols;
+  if (count == 0) {
+    if (scale_out) {
+      // empty tensor: amax = 0 -> s = 1 (reading R7)
+      const float one = 1.0f;
+      return cudaMemcpyAsync(scale_out, &one, sizeof(float), cudaMemcpyHostToDevice, st);
+    }
+    return cudaSuccess;
+  }
+  if (q && ld > cols) {
+    cudaError_t e = cudaMemset2DAsync(q + cols, (size_t)ld, 0, (size_t)(ld - cols), (size_t)rows, st);
+    if (e != cudaSuccess) return e;
+  }
+  if (qt && ldt > rows) {
+    cudaError_t e = cudaMemset2DAsync(qt + rows, (size_t)ldt, 0, (size_t)(ldt - rows), (size_t)cols, st);
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t groups = (count + 15) / 8;
+  k_quantize<<<grid_for(groups, 256, 16), 256, 0, st>>>(x, rows, cols, rowscale, g0, amax_slot, bits, seed, step, tag,
+                                                       q, ld, qt, ldt, scale_out, status);
+  return cudaGetLastError();
+}
+
+}  // namespace tango

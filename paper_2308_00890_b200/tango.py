@@ -1,0 +1,435 @@
+"""Thin ctypes binding of libtango.so (include/tango.h).
+
+Argument marshalling only: every step of the path runs in the library's CUDA kernels.
+PyTorch provides device memory and the current CUDA stream.  There is no fallback:
+if libtango.so is missing or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtango.so")
+
+TANGO_K_MAJOR, TANGO_MN_MAJOR = 0, 1
+TANGO_SDDMM_ADD, TANGO_SDDMM_DOT = 0, 1
+TANGO_IN, TANGO_OUT = 0, 1
+ROLE = dict(H=1, W=2, Hp=3, S=4, D=5, G=6, dHp=7, Ys=8, Gs=9, dY=10)
+STATUS = {0: "ok", 1: "invalid argument", 2: "shape mismatch", 3: "bits", 4: "non-finite", 5: "overflow",
+          6: "unsupported", 7: "CUDA error", 8: "NCCL error"}
+
+
+class TangoError(RuntimeError):
+    def __init__(self, status, what=""):
+        super().__init__(f"{what}: tango status {status} ({STATUS.get(status, '?')})")
+        self.status = status
+
+
+_P = C.c_void_p
+
+
+class Graph(C.Structure):
+    _fields_ = [("n_global", C.c_int64), ("row_begin", C.c_int64), ("row_end", C.c_int64), ("in_ptr", _P),
+                ("in_src", _P), ("e_in", C.c_int64), ("out_ptr", _P), ("out_dst", _P), ("out_eid", _P),
+                ("e_out", C.c_int64), ("chunk_edges", C.c_int32)]
+
+
+class QTensor(C.Structure):
+    _fields_ = [("q", _P), ("scale", _P), ("rows", C.c_int64), ("cols", C.c_int64), ("ld", C.c_int64),
+                ("bits", C.c_int32)]
+
+
+class Rng(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("step", C.c_uint32), ("tag", C.c_uint32)]
+
+
+class GatParams(C.Structure):
+    _fields_ = [("W", _P), ("a_src", _P), ("a_dst", _P), ("in_feats", C.c_int32), ("heads", C.c_int32),
+                ("head_dim", C.c_int32), ("neg_slope", C.c_float), ("bits", C.c_int32)]
+
+
+class GatCtxView(C.Structure):
+    _fields_ = [(f, _P) for f in ("qH", "qW", "qWt", "qHp", "qS", "qD", "qG", "qdHp")] + \
+               [(f, C.c_int64) for f in ("ldF", "ldHD", "ldFt")] + \
+               [(f, _P) for f in ("S", "D", "m", "den", "P", "dD", "dHp", "dalpha", "scalars")]
+
+
+class GcnParams(C.Structure):
+    _fields_ = [("W", _P), ("in_feats", C.c_int32), ("out_feats", C.c_int32), ("bits", C.c_int32)]
+
+
+class GcnCtxView(C.Structure):
+    _fields_ = [(f, _P) for f in ("qX", "qW", "qWt", "qYs", "qGs", "qdY")] + \
+               [(f, C.c_int64) for f in ("ldF", "ldO", "ldFt")] + [(f, _P) for f in ("ia", "ib", "scalars")]
+
+
+_lib = None
+
+EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tango_quantize", "tango_gemm_q",
+           "tango_sddmm_q", "tango_edge_softmax", "tango_softmax_bwd", "tango_spmm_q", "tango_edge_sum",
+           "tango_gat_ctx_bytes", "tango_gat_layer_fwd", "tango_gat_layer_bwd", "tango_gat_ctx_get_view",
+           "tango_gcn_ctx_bytes", "tango_gcn_layer_fwd", "tango_gcn_layer_bwd", "tango_gcn_ctx_get_view",
+           "tango_comm_unique_id_bytes", "tango_comm_get_unique_id", "tango_comm_init", "tango_comm_destroy",
+           "tango_comm_set_partition"]
+
+
+def load(path: str = LIB_PATH):
+    """Load libtango.so (no compute call; works without a GPU)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -m paper_2308_00890_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = C.CDLL(path)
+    i32, i64, u32, f32, sz = C.c_int32, C.c_int64, C.c_uint32, C.c_float, C.c_size_t
+    PG, PQ = C.POINTER(Graph), C.POINTER(QTensor)
+    L.tango_status_string.restype = C.c_char_p
+    L.tango_status_string.argtypes = [C.c_int]
+    L.tango_status_poll.argtypes = [_P, _P, C.POINTER(C.c_int)]
+    L.tango_quantize.argtypes = [_P, i64, i64, i64, _P, Rng, PQ, _P, _P, _P]
+    L.tango_gemm_q.argtypes = [PQ, i32, PQ, i32, i64, i64, i64, _P, _P, _P, _P]
+    L.tango_sddmm_q.argtypes = [PG, i32, PQ, PQ, i32, f32, _P, _P, _P, _P]
+    L.tango_edge_softmax.argtypes = [PG, i32, _P, _P, _P, _P, _P]
+    L.tango_softmax_bwd.argtypes = [PG, i32, _P, _P, _P, f32, _P, _P, _P]
+    L.tango_spmm_q.argtypes = [PG, i32, _P, PQ, i32, _P, _P, _P]
+    L.tango_edge_sum.argtypes = [PG, i32, i32, _P, _P, _P]
+    L.tango_gat_ctx_bytes.restype = sz
+    L.tango_gat_ctx_bytes.argtypes = [PG, C.POINTER(GatParams)]
+    L.tango_gat_ctx_get_view.argtypes = [PG, C.POINTER(GatParams), _P, C.POINTER(GatCtxView)]
+    L.tango_gat_layer_fwd.argtypes = [PG, C.POINTER(GatParams), _P, _P, Rng, u32, _P, sz, _P, _P, _P, _P, _P]
+    L.tango_gat_layer_bwd.argtypes = [PG, C.POINTER(GatParams), _P, sz, _P, _P, Rng, u32, _P, _P, _P, _P, _P, _P,
+                                      _P, _P]
+    L.tango_gcn_ctx_bytes.restype = sz
+    L.tango_gcn_ctx_bytes.argtypes = [PG, C.POINTER(GcnParams)]
+    L.tango_gcn_ctx_get_view.argtypes = [PG, C.POINTER(GcnParams), _P, C.POINTER(GcnCtxView)]
+    L.tango_gcn_layer_fwd.argtypes = [PG, C.POINTER(GcnParams), _P, _P, Rng, u32, _P, sz, _P, _P, _P, _P, _P]
+    L.tango_gcn_layer_bwd.argtypes = [PG, C.POINTER(GcnParams), _P, sz, _P, Rng, u32, _P, _P, _P, _P, _P]
+    L.tango_comm_unique_id_bytes.restype = i32
+    L.tango_comm_get_unique_id.argtypes = [_P]
+    L.tango_comm_init.argtypes = [C.POINTER(_P), _P, i32, i32]
+    L.tango_comm_destroy.argtypes = [_P]
+    L.tango_comm_set_partition.argtypes = [_P, _P]
+    _lib = L
+    return L
+
+
+def _check(st, what):
+    if st != 0:
+        raise TangoError(st, what)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise TypeError("libtango takes CUDA tensors only")
+    return t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ld32(cols: int) -> int:
+    return (cols + 31) // 32 * 32
+
+
+# ---------------------------------------------------------------------------------------- graph
+class DeviceGraph:
+    """A graph (paper_2308_00890_b200.inputs.Graph) resident on the GPU, viewed as a tango_graph.
+
+    With row_begin/row_end the view covers this rank's node block (destination-row partitioning);
+    the in/out CSR arrays are then sliced to the owned rows.
+    """
+
+    def __init__(self, g, device="cuda", chunk=256, row_begin=0, row_end=None):
+        row_end = g.n if row_end is None else row_end
+        ib, ie = int(g.in_ptr[row_begin]), int(g.in_ptr[row_end])
+        ob, oe = int(g.out_ptr[row_begin]), int(g.out_ptr[row_end])
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
+        self.in_ptr = t(g.in_ptr[row_begin:row_end + 1] - ib, np.int64)
+        self.in_src = t(g.in_src[ib:ie], np.int32)
+        self.out_ptr = t(g.out_ptr[row_begin:row_end + 1] - ob, np.int64)
+        self.out_dst = t(g.out_dst[ob:oe], np.int32)
+        self.out_eid = t(g.out_eid[ob:oe], np.int32) if (row_begin == 0 and row_end == g.n) else None
+        self.n_global, self.row_begin, self.row_end = g.n, row_begin, row_end
+        self.n_local = row_end - row_begin
+        self.e_in, self.e_out = ie - ib, oe - ob
+        self.chunk = chunk
+        self.struct = Graph(g.n, row_begin, row_end, _ptr(self.in_ptr), _ptr(self.in_src) if self.e_in else None,
+                            self.e_in, _ptr(self.out_ptr), _ptr(self.out_dst) if self.e_out else None,
+                            _ptr(self.out_eid) if self.out_eid is not None and self.e_out else None, self.e_out,
+                            chunk)
+
+    def ref(self):
+        return C.byref(self.struct)
+
+
+def qtensor(q, scale, rows, cols, bits=8):
+    return QTensor(_ptr(q), _ptr(scale), rows, cols, q.shape[1] if q.dim() == 2 else cols, bits)
+
+
+# ---------------------------------------------------------------------------------------- primitives
+def quantize(x, bits=8, seed=0, step=0, tag=0, global_row0=0, amax_hint=None, ld=None, status=None):
+    """tango_quantize: returns (q int8 [rows, ld], scale f32 (1,), amax f32 (1,))."""
+    L = load()
+    x = x.contiguous()
+    rows, cols = x.shape
+    ld = ld if ld is not None else ld32(cols)
+    q = torch.empty((rows, ld), dtype=torch.int8, device=x.device)
+    s = torch.empty(1, dtype=torch.float32, device=x.device)
+    amax = torch.empty(1, dtype=torch.float32, device=x.device)
+    qt = QTensor(_ptr(q), _ptr(s), rows, cols, ld, bits)
+    _check(L.tango_quantize(_ptr(x), rows, cols, global_row0, _ptr(amax_hint), Rng(seed, step, tag), C.byref(qt),
+                            _ptr(amax), _ptr(status), _stream()), "tango_quantize")
+    return q, s, amax
+
+
+def gemm_q(A, sA, a_layout, B, sB, b_layout, M, N, K, want=("f32",), bits=8):
+    """tango_gemm_q. A/B: int8 2-D tensors (stored layouts per a_layout/b_layout)."""
+    L = load()
+    arows, acols = (K, M) if a_layout == TANGO_MN_MAJOR else (M, K)
+    brows, bcols = (K, N) if b_layout == TANGO_MN_MAJOR else (N, K)
+    qa = QTensor(_ptr(A), _ptr(sA), arows, acols, A.shape[1], bits)
+    qb = QTensor(_ptr(B), _ptr(sB), brows, bcols, B.shape[1], bits)
+    dev = A.device
+    out = {}
+    Cf = torch.empty((M, N), dtype=torch.float32, device=dev) if "f32" in want else None
+    Ci = torch.empty((M, N), dtype=torch.int32, device=dev) if "i32" in want else None
+    Cl = torch.empty((M, N), dtype=torch.int64, device=dev) if "i64" in want else None
+    _check(L.tango_gemm_q(C.byref(qa), a_layout, C.byref(qb), b_layout, M, N, K, _ptr(Cf), _ptr(Ci), _ptr(Cl),
+                          _stream()), "tango_gemm_q")
+    if Cf is not None:
+        out["f32"] = Cf
+    if Ci is not None:
+        out["i32"] = Ci
+    if Cl is not None:
+        out["i64"] = Cl
+    return out
+
+
+def sddmm_add(graph: DeviceGraph, qS, sS, qD, sD, heads, slope):
+    L = load()
+    e_pre = torch.empty((graph.e_in, heads), dtype=torch.float32, device="cuda")
+    el = torch.empty_like(e_pre)
+    xs = QTensor(_ptr(qS), _ptr(sS), qS.shape[0], heads, heads, 8)
+    xd = QTensor(_ptr(qD), _ptr(sD), qD.shape[0], heads, heads, 8)
+    _check(L.tango_sddmm_q(graph.ref(), TANGO_SDDMM_ADD, C.byref(xs), C.byref(xd), heads, slope, _ptr(e_pre),
+                           _ptr(el), None, _stream()), "tango_sddmm_q(add)")
+    return e_pre, el
+
+
+def sddmm_dot(graph: DeviceGraph, qA_dst, sA, qB_src, sB, heads, cols):
+    L = load()
+    out = torch.empty((graph.e_in, heads), dtype=torch.float32, device="cuda")
+    acc = torch.empty((graph.e_in, heads), dtype=torch.int32, device="cuda")
+    xs = QTensor(_ptr(qB_src), _ptr(sB), qB_src.shape[0], cols, qB_src.shape[1], 8)
+    xd = QTensor(_ptr(qA_dst), _ptr(sA), qA_dst.shape[0], cols, qA_dst.shape[1], 8)
+    _check(L.tango_sddmm_q(graph.ref(), TANGO_SDDMM_DOT, C.byref(xs), C.byref(xd), heads, 0.0, _ptr(out), None,
+                           _ptr(acc), _stream()), "tango_sddmm_q(dot)")
+    return out, acc
+
+
+def edge_softmax(graph: DeviceGraph, heads, el):
+    L = load()
+    m = torch.empty((graph.n_global, heads), dtype=torch.float32, device="cuda")
+    den = torch.empty_like(m)
+    alpha = torch.empty((graph.e_in, heads), dtype=torch.float32, device="cuda")
+    _check(L.tango_edge_softmax(graph.ref(), heads, _ptr(el.contiguous()), _ptr(m), _ptr(den), _ptr(alpha),
+                                _stream()), "tango_edge_softmax")
+    return m, den, alpha
+
+
+def softmax_bwd(graph: DeviceGraph, heads, alpha, dalpha, e_pre, slope):
+    L = load()
+    P = torch.empty((graph.n_global, heads), dtype=torch.float32, device="cuda")
+    dEp = torch.empty((graph.e_in, heads), dtype=torch.float32, device="cuda")
+    _check(L.tango_softmax_bwd(graph.ref(), heads, _ptr(alpha), _ptr(dalpha), _ptr(e_pre), slope, _ptr(P),
+                               _ptr(dEp), _stream()), "tango_softmax_bwd")
+    return P, dEp
+
+
+def spmm(graph: DeviceGraph, direction, qX, sX, cols, heads, edge_w=None):
+    L = load()
+    x = QTensor(_ptr(qX), _ptr(sX), qX.shape[0], cols, qX.shape[1], 8)
+    out = torch.empty((graph.n_local, cols), dtype=torch.float32, device="cuda")
+    oi = None if edge_w is not None else torch.empty((graph.n_local, cols), dtype=torch.int32, device="cuda")
+    _check(L.tango_spmm_q(graph.ref(), direction, _ptr(edge_w), C.byref(x), heads, _ptr(out), _ptr(oi), _stream()),
+           "tango_spmm_q")
+    return out, oi
+
+
+def edge_sum(graph: DeviceGraph, direction, heads, x):
+    L = load()
+    out = torch.empty((graph.n_local, heads), dtype=torch.float32, device="cuda")
+    _check(L.tango_edge_sum(graph.ref(), direction, heads, _ptr(x.contiguous()), _ptr(out), _stream()),
+           "tango_edge_sum")
+    return out
+
+
+# ---------------------------------------------------------------------------------------- layers
+class Comm:
+    """NCCL communicator (tango_comm) for destination-row partitioning; the unique id is
+    broadcast by the caller (torch.distributed)."""
+
+    def __init__(self, nranks, rank, unique_id: bytes, row_starts):
+        L = load()
+        self.handle = C.c_void_p()
+        buf = C.create_string_buffer(unique_id, len(unique_id))
+        _check(L.tango_comm_init(C.byref(self.handle), buf, nranks, rank), "tango_comm_init")
+        starts = np.ascontiguousarray(row_starts, dtype=np.int64)
+        _check(L.tango_comm_set_partition(self.handle, starts.ctypes.data), "tango_comm_set_partition")
+
+    @staticmethod
+    def unique_id() -> bytes:
+        L = load()
+        n = L.tango_comm_unique_id_bytes()
+        buf = C.create_string_buffer(n)
+        _check(L.tango_comm_get_unique_id(buf), "tango_comm_get_unique_id")
+        return buf.raw
+
+    def close(self):
+        if self.handle:
+            load().tango_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+
+class GATLayer:
+    """One quantized GAT layer (tango_gat_layer_fwd / _bwd) with its device ctx."""
+
+    def __init__(self, graph: DeviceGraph, W, a_src, a_dst, heads, head_dim, slope=0.2, bits=8, comm: Comm = None):
+        L = load()
+        self.graph, self.heads, self.head_dim, self.bits = graph, heads, head_dim, bits
+        self.W, self.a_src, self.a_dst = W.contiguous(), a_src.contiguous(), a_dst.contiguous()
+        self.F = W.shape[0]
+        self.HD = heads * head_dim
+        self.params = GatParams(_ptr(self.W), _ptr(self.a_src), _ptr(self.a_dst), self.F, heads, head_dim, slope, bits)
+        nbytes = L.tango_gat_ctx_bytes(graph.ref(), C.byref(self.params))
+        if nbytes == 0:
+            raise TangoError(2, "tango_gat_ctx_bytes")
+        self.ctx = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.comm = comm
+
+    def _comm(self):
+        return self.comm.handle if self.comm is not None else None
+
+    def forward(self, H, seed=0x7A4E60, step=0, layer_id=0, amax_hint=None, out=None, amax_out=None):
+        L = load()
+        n = self.graph.n_local
+        out = out if out is not None else torch.empty((n, self.HD), dtype=torch.float32, device="cuda")
+        amax_out = amax_out if amax_out is not None else torch.empty(1, dtype=torch.float32, device="cuda")
+        _check(L.tango_gat_layer_fwd(self.graph.ref(), C.byref(self.params), _ptr(H), _ptr(amax_hint),
+                                     Rng(seed, step, 0), layer_id, _ptr(self.ctx), self.ctx.numel(), _ptr(out),
+                                     _ptr(amax_out), self._comm(), _ptr(self.status), _stream()),
+               "tango_gat_layer_fwd")
+        return out, amax_out
+
+    def backward(self, dH_out, seed=0x7A4E60, step=0, layer_id=0, amax_hint=None, want_dH=True, outs=None):
+        L = load()
+        n = self.graph.n_local
+        if outs is None:
+            dH = torch.empty((n, self.F), dtype=torch.float32, device="cuda") if want_dH else None
+            dW = torch.empty((self.F, self.HD), dtype=torch.float32, device="cuda")
+            da_s = torch.empty(self.HD, dtype=torch.float32, device="cuda")
+            da_d = torch.empty(self.HD, dtype=torch.float32, device="cuda")
+        else:
+            dH, dW, da_s, da_d = outs
+        _check(L.tango_gat_layer_bwd(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), self.ctx.numel(),
+                                     _ptr(dH_out), _ptr(amax_hint), Rng(seed, step, 0), layer_id, _ptr(dH), _ptr(dW),
+                                     _ptr(da_s), _ptr(da_d), None, self._comm(), _ptr(self.status), _stream()),
+               "tango_gat_layer_bwd")
+        return dH, dW, da_s, da_d
+
+    def view(self):
+        """Device tensors inside ctx (copies), for parity tests."""
+        L = load()
+        v = GatCtxView()
+        _check(L.tango_gat_ctx_get_view(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), C.byref(v)),
+               "tango_gat_ctx_get_view")
+        base = self.ctx.data_ptr()
+        N, n, H, HD, F, E = self.graph.n_global, self.graph.n_local, self.heads, self.HD, self.F, self.graph.e_in
+
+        def sl(p, nbytes, dtype, shape):
+            off = p - base
+            return self.ctx[off:off + nbytes].view(dtype).reshape(shape).clone()
+
+        i8, f4 = torch.int8, torch.float32
+        out = dict(
+            qH=sl(v.qH, n * v.ldF, i8, (n, v.ldF))[:, :F], qW=sl(v.qW, F * v.ldHD, i8, (F, v.ldHD))[:, :HD],
+            qWt=sl(v.qWt, HD * v.ldFt, i8, (HD, v.ldFt))[:, :F],
+            qHp=sl(v.qHp, N * v.ldHD, i8, (N, v.ldHD))[:, :HD], qS=sl(v.qS, N * H, i8, (N, H)),
+            qD=sl(v.qD, N * H, i8, (N, H)), qG=sl(v.qG, N * v.ldHD, i8, (N, v.ldHD))[:, :HD],
+            qdHp=sl(v.qdHp, n * v.ldHD, i8, (n, v.ldHD))[:, :HD],
+            qH_full=sl(v.qH, n * v.ldF, i8, (n, v.ldF)), qHp_full=sl(v.qHp, N * v.ldHD, i8, (N, v.ldHD)),
+            S=sl(v.S, n * H * 4, f4, (n, H)), D=sl(v.D, n * H * 4, f4, (n, H)), m=sl(v.m, N * H * 4, f4, (N, H)),
+            den=sl(v.den, N * H * 4, f4, (N, H)), P=sl(v.P, N * H * 4, f4, (N, H)),
+            dD=sl(v.dD, N * H * 4, f4, (N, H)), dHp=sl(v.dHp, n * HD * 4, f4, (n, HD)),
+            dalpha=sl(v.dalpha, E * H * 4, f4, (E, H)), scalars=sl(v.scalars, 64 * 4, f4, (64,)))
+        return out
+
+    def check_status(self):
+        st = int(self.status.item())
+        if st != 0:
+            raise TangoError(st, "device status")
+
+
+class GCNLayer:
+    """One quantized GCN layer (tango_gcn_layer_fwd / _bwd)."""
+
+    def __init__(self, graph: DeviceGraph, W, bits=8, comm: Comm = None):
+        L = load()
+        self.graph, self.bits = graph, bits
+        self.W = W.contiguous()
+        self.F, self.O = W.shape
+        self.params = GcnParams(_ptr(self.W), self.F, self.O, bits)
+        nbytes = L.tango_gcn_ctx_bytes(graph.ref(), C.byref(self.params))
+        if nbytes == 0:
+            raise TangoError(2, "tango_gcn_ctx_bytes")
+        self.ctx = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.comm = comm
+
+    def forward(self, X, seed=0x7A4E60, step=0, layer_id=0, amax_hint=None):
+        L = load()
+        out = torch.empty((self.graph.n_local, self.O), dtype=torch.float32, device="cuda")
+        amax_out = torch.empty(1, dtype=torch.float32, device="cuda")
+        _check(L.tango_gcn_layer_fwd(self.graph.ref(), C.byref(self.params), _ptr(X), _ptr(amax_hint),
+                                     Rng(seed, step, 0), layer_id, _ptr(self.ctx), self.ctx.numel(), _ptr(out),
+                                     _ptr(amax_out), self.comm.handle if self.comm else None, _ptr(self.status),
+                                     _stream()), "tango_gcn_layer_fwd")
+        return out, amax_out
+
+    def backward(self, dout, seed=0x7A4E60, step=0, layer_id=0):
+        L = load()
+        dX = torch.empty((self.graph.n_local, self.F), dtype=torch.float32, device="cuda")
+        dW = torch.empty((self.F, self.O), dtype=torch.float32, device="cuda")
+        _check(L.tango_gcn_layer_bwd(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), self.ctx.numel(),
+                                     _ptr(dout), Rng(seed, step, 0), layer_id, _ptr(dX), _ptr(dW),
+                                     self.comm.handle if self.comm else None, _ptr(self.status), _stream()),
+               "tango_gcn_layer_bwd")
+        return dX, dW
+
+    def view(self):
+        L = load()
+        v = GcnCtxView()
+        _check(L.tango_gcn_ctx_get_view(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), C.byref(v)),
+               "tango_gcn_ctx_get_view")
+        base = self.ctx.data_ptr()
+        N, n, F, O = self.graph.n_global, self.graph.n_local, self.F, self.O
+
+        def sl(p, nbytes, dtype, shape):
+            off = p - base
+            return self.ctx[off:off + nbytes].view(dtype).reshape(shape).clone()
+
+        i8 = torch.int8
+        return dict(qX=sl(v.qX, n * v.ldF, i8, (n, v.ldF))[:, :F], qW=sl(v.qW, F * v.ldO, i8, (F, v.ldO))[:, :O],
+                    qYs=sl(v.qYs, N * v.ldO, i8, (N, v.ldO))[:, :O], qGs=sl(v.qGs, N * v.ldO, i8, (N, v.ldO))[:, :O],
+                    qdY=sl(v.qdY, n * v.ldO, i8, (n, v.ldO))[:, :O], ia=sl(v.ia, n * O * 4, torch.int32, (n, O)),
+                    ib=sl(v.ib, n * O * 4, torch.int32, (n, O)),
+                    scalars=sl(v.scalars, 64 * 4, torch.float32, (64,)))

@@ -1,0 +1,171 @@
+"""GPU parity of the libtango primitives against the CPU oracle (called through the C ABI).
+
+Bit-exact for int8 codes, integer accumulators and every fp32 value the oracle pins
+(DESIGN.md §2 readings R1-R14); ragged sizes span several tiles plus a tail.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2308_00890_b200 import inputs  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def T():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2308_00890_b200 import tango
+    tango.load()
+    return tango
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("rows,cols,row0", [(1, 1, 0), (7, 13, 0), (333, 100, 5), (1000, 512, 0), (4097, 602, 17),
+                                            (64, 1433, 0)])
+def test_quantize_parity(T, orc, rows, cols, row0):
+    rng = np.random.default_rng(rows + cols)
+    x = (rng.standard_normal((rows, cols)) * rng.uniform(0.01, 10)).astype(np.float32)
+    seed, step, tag = 0x7A4E60, 5, 0x103
+    q, s, amax = T.quantize(cu(x), bits=8, seed=seed, step=step, tag=tag, global_row0=row0)
+    torch.cuda.synchronize()
+    qo, so, ao = orc.quantize(x, 8, seed=seed, step=step, tag=tag, g0=row0 * cols)
+    qg = q.cpu().numpy()
+    assert np.array_equal(qg[:, :cols], qo)
+    assert np.all(qg[:, cols:] == 0)
+    assert s.item() == so and amax.item() == ao
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+def test_quantize_bits_and_hint(T, orc, bits):
+    x = np.random.default_rng(1).standard_normal((300, 64)).astype(np.float32)
+    hint = cu(np.array([7.5], np.float32))
+    q, s, amax = T.quantize(cu(x), bits=bits, seed=3, step=1, tag=9, amax_hint=hint)
+    qo, so, _ = orc.quantize(x, bits, seed=3, step=1, tag=9, amax=np.float32(7.5))
+    assert np.array_equal(q.cpu().numpy()[:, :64], qo) and s.item() == so
+
+
+def test_quantize_zero_and_nonfinite(T):
+    q, s, amax = T.quantize(torch.zeros((5, 32), device="cuda"))
+    assert s.item() == 1.0 and amax.item() == 0.0 and int(q.abs().max()) == 0
+    x = torch.ones((10, 32), device="cuda")
+    x[3, 4] = float("nan")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    T.quantize(x, status=st)
+    assert int(st.item()) == 4
+
+
+def test_quantize_bad_args(T):
+    with pytest.raises(T.TangoError):
+        T.quantize(torch.ones((4, 32), device="cuda"), bits=9)
+
+
+def _rand_i8(rng, shape):
+    return rng.integers(-127, 128, size=shape).astype(np.int8)
+
+
+def _pad(a, ld):
+    out = np.zeros((a.shape[0], ld), np.int8)
+    out[:, :a.shape[1]] = a
+    return out
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 32), (300, 512, 128), (1000, 96, 100), (257, 512, 602),
+                                   (129, 1440, 512), (5, 32, 1433)])
+def test_gemm_kmajor(T, M, N, K):
+    rng = np.random.default_rng(M * 7 + N + K)
+    A = _rand_i8(rng, (M, K))
+    Bt = _rand_i8(rng, (N, K))
+    ld = (K + 31) // 32 * 32
+    sA, sB = cu(np.array([0.0123], np.float32)), cu(np.array([1.7], np.float32))
+    out = T.gemm_q(cu(_pad(A, ld)), sA, T.TANGO_K_MAJOR, cu(_pad(Bt, ld)), sB, T.TANGO_K_MAJOR, M, N, K,
+                   want=("f32", "i32"))
+    ref = A.astype(np.int64) @ Bt.astype(np.int64).T
+    assert np.array_equal(out["i32"].cpu().numpy(), ref)
+    s = np.float32(np.float32(0.0123) * np.float32(1.7))
+    assert np.array_equal(out["f32"].cpu().numpy(), ref.astype(np.float32) * s)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 512, 1000), (100, 512, 4097), (602, 256, 300), (16, 64, 130000),
+                                   (128, 128, 300_000)])
+def test_gemm_mnmajor_splitk(T, M, N, K):
+    # ∂W = Hᵀ·∂H′: both operands stored [K][ld] (MN-major), int64 split-K reduction (reading R27)
+    rng = np.random.default_rng(M + N + K)
+    A = _rand_i8(rng, (K, M))
+    B = _rand_i8(rng, (K, N))
+    lda, ldb = (M + 31) // 32 * 32, (N + 31) // 32 * 32
+    sA, sB = cu(np.array([0.5], np.float32)), cu(np.array([0.25], np.float32))
+    out = T.gemm_q(cu(_pad(A, lda)), sA, T.TANGO_MN_MAJOR, cu(_pad(B, ldb)), sB, T.TANGO_MN_MAJOR, M, N, K,
+                   want=("i64", "f32"))
+    ref = A.astype(np.int64).T @ B.astype(np.int64)
+    assert np.array_equal(out["i64"].cpu().numpy(), ref)
+    assert np.array_equal(out["f32"].cpu().numpy(), ref.astype(np.float32) * np.float32(0.125))
+
+
+def test_gemm_mixed_layouts(T):
+    rng = np.random.default_rng(5)
+    M, N, K = 200, 160, 256
+    A = _rand_i8(rng, (M, K))
+    B = _rand_i8(rng, (K, N))
+    one = cu(np.array([1.0], np.float32))
+    ref = A.astype(np.int64) @ B.astype(np.int64)
+    o1 = T.gemm_q(cu(A), one, T.TANGO_K_MAJOR, cu(B), one, T.TANGO_MN_MAJOR, M, N, K, want=("i32",))
+    o2 = T.gemm_q(cu(np.ascontiguousarray(A.T)), one, T.TANGO_MN_MAJOR, cu(np.ascontiguousarray(B.T)), one,
+                  T.TANGO_K_MAJOR, M, N, K, want=("i32",))
+    assert np.array_equal(o1["i32"].cpu().numpy(), ref)
+    assert np.array_equal(o2["i32"].cpu().numpy(), ref)
+
+
+GRAPHS = [("toy", None), ("c0b", (64, 256, 0)), ("noself", (200, 500, 3)), ("mid", (3000, 30000, 4))]
+
+
+def make_graph(spec):
+    name, args = spec
+    if name == "toy":
+        return inputs.toy_graph()
+    n, d, s = args
+    return inputs.random_graph(n, d, seed=s, self_loops=(name != "noself"))
+
+
+@pytest.mark.parametrize("spec", GRAPHS, ids=[g[0] for g in GRAPHS])
+@pytest.mark.parametrize("chunk", [3, 256])
+def test_sparse_primitives_parity(T, orc, spec, chunk):
+    gr = make_graph(spec)
+    dg = T.DeviceGraph(gr, chunk=chunk)
+    rng = np.random.default_rng(gr.n)
+    H = 2
+    qS = _rand_i8(rng, (gr.n, H)); qD = _rand_i8(rng, (gr.n, H))
+    sS, sD = np.float32(0.031), np.float32(0.017)
+    e_pre, el = T.sddmm_add(dg, cu(qS), cu(np.array([sS])), cu(qD), cu(np.array([sD])), H, 0.2)
+    oe, oel = orc.sddmm_add(gr, H, orc.qref(q=qS, s=sS), orc.qref(q=qD, s=sD), 0.2, chunk=chunk)
+    assert np.array_equal(e_pre.cpu().numpy(), oe) and np.array_equal(el.cpu().numpy(), oel)
+    m, den, alpha = T.edge_softmax(dg, H, el)
+    om, oden, oa = orc.edge_softmax(gr, H, oel, chunk=chunk)
+    assert np.array_equal(alpha.cpu().numpy(), oa)
+    assert np.array_equal(m.cpu().numpy(), om) and np.array_equal(den.cpu().numpy(), oden)
+    cols = 64
+    qX = _rand_i8(rng, (gr.n, cols))
+    sX = np.float32(0.02)
+    for direction in (0, 1):
+        out, _ = T.spmm(dg, direction, cu(qX), cu(np.array([sX])), cols, H, edge_w=alpha)
+        ref = orc.spmm_alpha(gr, direction, H, cols, oa, orc.qref(q=qX, s=sX), chunk=chunk)
+        assert np.array_equal(out.cpu().numpy(), ref)
+        out, oi = T.spmm(dg, direction, cu(qX), cu(np.array([sX])), cols, H)
+        ri, rf = orc.spmm_sum(gr, direction, cols, orc.qref(q=qX, s=sX))
+        assert np.array_equal(oi.cpu().numpy(), ri)
+    qA = _rand_i8(rng, (gr.n, cols)); qB = _rand_i8(rng, (gr.n, cols))
+    dal, acc = T.sddmm_dot(dg, cu(qA), cu(np.array([np.float32(0.5)])), cu(qB), cu(np.array([np.float32(0.01)])),
+                           H, cols)
+    ref = orc.sddmm_dot(gr, H, cols, orc.qref(q=qA, s=np.float32(0.5)), orc.qref(q=qB, s=np.float32(0.01)))
+    assert np.array_equal(dal.cpu().numpy(), ref)
+    dalpha = rng.standard_normal((gr.e, H)).astype(np.float32)
+    P, dEp = T.softmax_bwd(dg, H, alpha, cu(dalpha), e_pre, 0.2)
+    oP, _, odEp = orc.softmax_bwd(gr, H, oa, dalpha, oe, 0.2, chunk=chunk)
+    assert np.array_equal(P.cpu().numpy(), oP) and np.array_equal(dEp.cpu().numpy(), odEp)
+    for direction in (0, 1):
+        s = T.edge_sum(dg, direction, H, dEp)
+        assert np.array_equal(s.cpu().numpy(), orc.edge_sum(gr, direction, H, odEp, chunk=chunk))
