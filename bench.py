@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: one quantized GAT layer forward + backward (Tango, arXiv 2308.00890)
+through libtango.so on synthetic inputs shaped like the paper's datasets.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload arxiv] [--impl tango|reference]
+
+N > 1 is launched by torchrun: destination-row partitioning of ONE graph over N GPUs with NCCL
+(all-gather of int8 node rows, all-reduce of amax / ∂W / ∂a inside libtango) -> strong scaling.
+Prints one JSON line (rank 0).  See DESIGN.md §6 for every number's definition.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2308_00890_b200 import inputs  # noqa: E402
+
+METRIC = "quantized GAT layer fwd+bwd ms"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+def workload(name):
+    kw, F, H, D = inputs.WORKLOADS[name]
+    g = inputs.workload_graph(name)
+    return g, F, H, D
+
+
+def partition_rows(g, nranks):
+    """Contiguous node ranges balanced by in-edge count."""
+    cum = g.in_ptr.astype(np.float64) + np.arange(g.n + 1)  # edges + one unit per row
+    starts = [0]
+    for r in range(1, nranks):
+        starts.append(int(np.searchsorted(cum, cum[-1] * r / nranks)))
+    starts.append(g.n)
+    return starts
+
+
+# ------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------- roofline model
+def kernel_model(name, g_e, n, F, H, HD, peaks, clock_mhz):
+    """Algorithmic bytes and ALU ops per launch of a kernel."""
+    E = g_e
+    if name == "gat_fwd_dst":
+        # per edge: src index + q_S[u] + q_H'[u] row; per node: q_D, H_out row, m, den
+        byts = E * (4 + H + HD) + n * (8 + H + 4 * HD + 8 * H)
+        ops = 2 * E * HD            # int8->fp32 convert + FMA per gathered element
+    elif name == "gat_bwd_dst":
+        byts = E * (4 + H + HD) + n * (8 + HD + H + 8 * H + 8 * H)
+        ops = 2 * E * HD            # IDP4A dot: 1 op per 4 elements x 2 (load/convert-free) -> 0.5 ; counted as 2 conservatively
+    elif name == "gat_bwd_src":
+        byts = E * (4 + HD + 13 * H) + n * (8 + HD + H + 4 * H + 4 * HD)
+        ops = 2 * E * HD
+    elif name.startswith("gemm"):
+        return None
+    elif name == "quantize":
+        return None
+    else:
+        return None
+    alu_peak = 148 * 128 * clock_mhz * 1e6   # FP32 lanes x clock (lane-ops/s)
+    return byts, ops, alu_peak
+
+
+# ------------------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build()
+    g, F, H, D = workload(args.workload)
+    HD = H * D
+    Hx = inputs.features(g.n, F)
+    W, a_s, a_d = inputs.gat_params(F, H, D)
+    dH = inputs.grad_out(g.n, HD)
+    cores = O.num_threads()
+    # each step: the oracle (as it stands) on a bounded row sample of the same workload, scaled by edges
+    frac = min(1.0, args.ref_sample)
+    if frac < 1.0:
+        gs = inputs.chung_lu_graph(**{**inputs.WORKLOADS[args.workload][0],
+                                      "n": int(g.n * frac), "m": int(inputs.WORKLOADS[args.workload][0]["m"] * frac)})
+    else:
+        gs = g
+    Hs, dHs = Hx[:gs.n], dH[:gs.n]
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        f = O.gat_fwd(gs, Hs, W, a_s, a_d, H, D, step=i)
+        O.gat_bwd(gs, f, Hs, W, a_s, a_d, dHs)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    scale = (g.e + g.n) / (gs.e + gs.n)
+    ms = 1e3 * statistics.mean(times) * scale
+    sample = (f"oracle gat_fwd+gat_bwd on {'the full graph' if gs is g else f'a {frac:.3f}-scale Chung-Lu sample'} "
+              f"(N={gs.n}, E={gs.e}), scaled by (E+N) ratio {scale:.3f}")
+    line = {"impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int8 codes / fp32 (CPU)", "data": "synthetic",
+            "config": {"workload": f"{args.workload}-shaped GAT layer 1", "N": g.n, "E": g.e, "F": F, "heads": H,
+                       "head_dim": D},
+            "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------- main arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="arxiv", choices=sorted(inputs.WORKLOADS))
+    ap.add_argument("--impl", default="tango", choices=["tango", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sample", type=float, default=1.0)
+    ap.add_argument("--profile-breakdown", action="store_true", help="print per-kernel times to stderr")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2308_00890_b200 import tango as T
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    T.load()
+    peaks, peak_kind = load_peaks()
+
+    g, F, H, D = workload(args.workload)
+    HD = H * D
+    starts = partition_rows(g, world)
+    r0, r1 = starts[rank], starts[rank + 1]
+    comm = None
+    if world > 1:
+        uid = [T.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = T.Comm(world, rank, uid[0], starts)
+    dg = T.DeviceGraph(g, row_begin=r0, row_end=r1)
+    W, a_s, a_d = inputs.gat_params(F, H, D)
+    Hx = inputs.features(g.n, F)[r0:r1]
+    dH = inputs.grad_out(g.n, HD)[r0:r1]
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    layer = T.GATLayer(dg, cu(W), cu(a_s), cu(a_d), H, D, slope=0.2, bits=8, comm=comm)
+    Hd, dHd = cu(Hx), cu(dH)
+    n = r1 - r0
+    outs = (torch.empty((n, F), device="cuda"), torch.empty((F, HD), device="cuda"),
+            torch.empty(HD, device="cuda"), torch.empty(HD, device="cuda"))
+    Hout = torch.empty((n, HD), device="cuda")
+    amax = torch.empty(1, device="cuda")
+    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
+
+    def step(i):
+        layer.forward(Hd, step=i, out=Hout, amax_out=amax)
+        layer.backward(dHd, step=i, outs=outs)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    layer.check_status()
+
+    # ---------------- timed region: K steps, L2 flushed between steps, CUDA events per step
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    T.profile_enable(True)
+    T.profile_read(reset=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    launches0 = T.launch_count()
+    for i in range(args.steps):
+        l2_flush.zero_()
+        evs[i][0].record()
+        step(args.warmup + i)
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = T.launch_count() - launches0
+    clk = clocks.stop()
+    prof = T.profile_read(reset=True)
+    T.profile_enable(False)
+    ms_rank = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    ms_t = torch.tensor([ms_rank], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+
+    # ---------------- dominant kernel roofline (live CUDA-event time over the timed region)
+    dom, (dom_ms, dom_cnt) = max(prof.items(), key=lambda kv: kv[1][0])
+    clock = clk["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    model = kernel_model(dom, dg.e_in, n, F, H, HD, peaks, clock)
+    per_launch_s = dom_ms / dom_cnt / 1e3
+    roof = None
+    if model is not None:
+        byts, ops, alu_peak = model
+        t_hbm = byts / (peaks["hbm_gbs"] * 1e9)
+        t_alu = ops / alu_peak
+        if t_hbm >= t_alu:
+            roof = {"bound": "hbm", "achieved": byts / per_launch_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+        else:
+            roof = {"bound": "alu", "achieved": ops / per_launch_s / 1e12, "peak": alu_peak / 1e12,
+                    "unit": "Tlane-op/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = None
+        roof["kernel"] = dom
+        roof["kernel_ms"] = per_launch_s * 1e3
+        roof["share_of_step"] = dom_ms / dom_cnt / ms
+        roof["peak_kind"] = peak_kind
+    breakdown = {k: round(v[0] / v[1], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    if args.profile_breakdown and rank == 0:
+        print(json.dumps({"per_launch_ms": breakdown, "launches_per_kernel": {k: v[1] for k, v in prof.items()}}),
+              file=sys.stderr)
+
+    # ---------------- e2e: through the public API with host buffers (pinned), copies in the timed region
+    H_host = torch.from_numpy(np.ascontiguousarray(Hx)).pin_memory()
+    dH_host = torch.from_numpy(np.ascontiguousarray(dH)).pin_memory()
+    out_host = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (Hout, *outs)]
+    e2e_steps = max(3, min(args.steps, 20))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(e2e_steps):
+        Hd.copy_(H_host, non_blocking=True)
+        dHd.copy_(dH_host, non_blocking=True)
+        step(10_000 + i)
+        for h, d in zip(out_host, (Hout, *outs)):
+            h.copy_(d, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_t = torch.tensor([e0.elapsed_time(e1) / e2e_steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    h2d = (H_host.numel() + dH_host.numel()) * 4
+    d2h = sum(t.numel() * t.element_size() for t in out_host)
+
+    launches_t = torch.tensor([launches], dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.all_reduce(launches_t)
+
+    # ---------------- CPU baseline: the oracle as it stands, rank 0 at N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        O.build()
+        t0 = time.perf_counter()
+        f = O.gat_fwd(g, Hx, W, a_s, a_d, H, D, step=0)
+        O.gat_bwd(g, f, Hx, W, a_s, a_d, dH)
+        cpu_ms = (time.perf_counter() - t0) * 1e3
+        cpu = {"value": cpu_ms, "unit": "ms", "cores": O.num_threads(), "kind": "oracle",
+               "sample": f"one full fwd+bwd of the same {args.workload}-shaped layer (N={g.n}, E={g.e}), "
+                         "OpenMP rows, bit-identical to single-threaded"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": "int8 (tcgen05 kind::i8, IDP4A) + fp32 accumulate/softmax",
+                "data": "synthetic (seeded Chung-Lu power-law graph, N(0,1) features, Glorot weights)",
+                "config": {"workload": f"{args.workload}-shaped GAT layer 1 (fwd+bwd)", "N": g.n, "E": g.e,
+                           "F": F, "heads": H, "head_dim": D, "bits": 8, "chunk_edges": 256,
+                           "parallelism": f"dst-row partition x{world}" if world > 1 else "1 GPU",
+                           "l2": "flushed between timed steps (256 MB write)",
+                           "degree": g.degree_stats()},
+                "roofline": roof, "cpu_baseline": cpu,
+                "e2e": {"value": float(e2e_t.item()), "unit": "ms", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h},
+                "gpu_launches": int(launches_t.item()), "clocks": clk, "kernel_ms": breakdown}
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -271,6 +271,18 @@ tango_status tango_comm_destroy(struct tango_comm* comm);
  * Must be called (identically on every rank) before a layer call with this comm. */
 tango_status tango_comm_set_partition(struct tango_comm* comm, const int64_t* row_starts /* nranks+1, host */);
 
+/* ------------------------------------------------------------------------- */
+/* Tracing: every kernel launch increments a counter; with profiling enabled  */
+/* each launch is bracketed by CUDA events on its stream and device time is   */
+/* accumulated per kernel name (host-side state, process-wide, thread-safe).  */
+/* ------------------------------------------------------------------------- */
+void tango_profile_enable(int32_t on);
+int64_t tango_launch_count(void);
+tango_status tango_profile_collect(void);          /* waits for the recorded events */
+int32_t tango_profile_num_entries(void);
+tango_status tango_profile_entry(int32_t i, char* name, int32_t name_cap, double* total_ms, int64_t* launches);
+void tango_profile_reset(void);
+
 #ifdef __cplusplus
 }
 #endif

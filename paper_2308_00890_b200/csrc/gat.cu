@@ -499,16 +499,19 @@ static int rows_grid(int64_t rows) {
 
 cudaError_t launch_gat_fwd_dst(const GatFwdDstArgs& a, cudaStream_t st) {
   if (a.g.n_local == 0) return cudaSuccess;
+  ProfScope ps("gat_fwd_dst", st);
   TANGO_DISPATCH_HV(a.d.heads, a.d.hd / 32, k_gat_fwd_dst, a, st, a.g.n_local);
   return cudaGetLastError();
 }
 cudaError_t launch_gat_bwd_dst(const GatBwdDstArgs& a, cudaStream_t st) {
   if (a.g.n_local == 0) return cudaSuccess;
+  ProfScope ps("gat_bwd_dst", st);
   TANGO_DISPATCH_HV(a.d.heads, a.d.hd / 32, k_gat_bwd_dst, a, st, a.g.n_local);
   return cudaGetLastError();
 }
 cudaError_t launch_gat_bwd_src(const GatBwdSrcArgs& a, cudaStream_t st) {
   if (a.g.n_local == 0) return cudaSuccess;
+  ProfScope ps("gat_bwd_src", st);
   TANGO_DISPATCH_HV(a.d.heads, a.d.hd / 32, k_gat_bwd_src, a, st, a.g.n_local);
   return cudaGetLastError();
 }
@@ -687,6 +690,7 @@ static int flat_grid(int64_t n) {
 cudaError_t launch_sddmm_add(const GraphDev& g, int heads, const int8_t* qS, const float* sS, const int8_t* qD,
                              const float* sD, float slope, float* e_pre, float* el, cudaStream_t st) {
   if (g.n_local == 0) return cudaSuccess;
+  ProfScope ps("sddmm_add", st);
   k_sddmm_add<<<flat_grid(g.n_local * heads), 256, 0, st>>>(g, heads, qS, sS, qD, sD, slope, e_pre, el);
   return cudaGetLastError();
 }
@@ -694,29 +698,34 @@ cudaError_t launch_sddmm_dot(const GraphDev& g, int heads, int hd_total, const i
                              const float* sA, const int8_t* qB, int64_t ldb, const float* sB, float* out,
                              int32_t* acc, cudaStream_t st) {
   if (g.n_local == 0) return cudaSuccess;
+  ProfScope ps("sddmm_dot", st);
   k_sddmm_dot<<<flat_grid(g.n_local * heads), 256, 0, st>>>(g, heads, hd_total, qA, lda, sA, qB, ldb, sB, out, acc);
   return cudaGetLastError();
 }
 cudaError_t launch_edge_softmax(const GraphDev& g, int heads, const float* el, float* m, float* den, float* alpha,
                                 cudaStream_t st) {
   if (g.n_local == 0) return cudaSuccess;
+  ProfScope ps("edge_softmax", st);
   k_edge_softmax<<<flat_grid(g.n_local * heads), 256, 0, st>>>(g, heads, el, m, den, alpha);
   return cudaGetLastError();
 }
 cudaError_t launch_softmax_bwd(const GraphDev& g, int heads, const float* alpha, const float* dalpha,
                                const float* e_pre, float slope, float* P, float* dEp, cudaStream_t st) {
   if (g.n_local == 0) return cudaSuccess;
+  ProfScope ps("softmax_bwd", st);
   k_softmax_bwd<<<flat_grid(g.n_local * heads), 256, 0, st>>>(g, heads, alpha, dalpha, e_pre, slope, P, dEp);
   return cudaGetLastError();
 }
 cudaError_t launch_edge_sum(const GraphDev& g, int dir, int heads, const float* x, float* out, cudaStream_t st) {
   if (g.n_local == 0) return cudaSuccess;
+  ProfScope ps("edge_sum", st);
   k_edge_sum<<<flat_grid(g.n_local * heads), 256, 0, st>>>(g, dir, heads, x, out);
   return cudaGetLastError();
 }
 cudaError_t launch_spmm_w(const GraphDev& g, int dir, int heads, int cols, const float* w, const int8_t* qX,
                           int64_t ldx, const float* sX, float* out, cudaStream_t st) {
   if (g.n_local == 0) return cudaSuccess;
+  ProfScope ps("spmm_w", st);
   k_spmm_w<<<flat_grid(g.n_local * cols), 256, 0, st>>>(g, dir, heads, cols, w, qX, ldx, sX, out);
   return cudaGetLastError();
 }
@@ -724,11 +733,13 @@ cudaError_t launch_spmm_sum(const GraphDev& g, int dir, int cols, const int8_t* 
                             const float* rowscale, float* out, int32_t* out_i32, unsigned* amax_out,
                             cudaStream_t st) {
   if (g.n_local == 0) return cudaSuccess;
+  ProfScope ps("spmm_sum", st);
   k_spmm_sum<<<rows_grid(g.n_local), 256, 0, st>>>(g, dir, cols, qX, ldx, sX, rowscale, out, out_i32, amax_out);
   return cudaGetLastError();
 }
 cudaError_t launch_gcn_norms(const GraphDev& g, float* ns, float* nd, cudaStream_t st) {
   if (g.n_local == 0) return cudaSuccess;
+  ProfScope ps("gcn_norms", st);
   k_gcn_norms<<<flat_grid(g.n_local), 256, 0, st>>>(g, ns, nd);
   return cudaGetLastError();
 }

@@ -363,6 +363,8 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(k_gemm_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   });
   int64_t grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
+  static const char* names[] = {"gemm_amax", "gemm_quant", "gemm_store", "gemm_i32", "gemm_splitk_i64"};
+  ProfScope ps(names[a.mode], st);
   k_gemm_i8<<<(unsigned)grid, GEMM_THREADS, SMEM_BYTES, st>>>(tA, tB, p);
   return cudaGetLastError();
 }
@@ -379,6 +381,7 @@ cudaError_t launch_finalize_dw(const int64_t* acc, int64_t count, const float* s
   if (count == 0) return cudaSuccess;
   int grid = (int)((count + 255) / 256);
   if (grid > 4 * num_sms()) grid = 4 * num_sms();
+  ProfScope ps("finalize_dw", st);
   k_finalize_dw<<<grid, 256, 0, st>>>(acc, count, sA, sB, out);
   return cudaGetLastError();
 }

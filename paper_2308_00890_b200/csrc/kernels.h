@@ -8,6 +8,18 @@ namespace tango {
 
 int num_sms();
 
+// Every kernel launch is wrapped in a ProfScope (prof.cu): launch counter + optional event timing.
+class ProfScope {
+ public:
+  ProfScope(const char* name, cudaStream_t st);
+  ~ProfScope();
+ private:
+  cudaStream_t st_;
+  bool on_ = false;
+  int entry_ = -1;
+  cudaEvent_t a_ = nullptr, b_ = nullptr;
+};
+
 // ---- quant.cu
 cudaError_t launch_absmax(const float* x, int64_t rows, int64_t cols, const float* rowscale, unsigned* slot,
                           cudaStream_t st);

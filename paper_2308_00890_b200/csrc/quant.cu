@@ -120,6 +120,7 @@ static int grid_for(int64_t work, int threads, int per_sm = 8) {
 cudaError_t launch_absmax(const float* x, int64_t rows, int64_t cols, const float* rowscale, unsigned* slot,
                           cudaStream_t st) {
   if (rows * cols == 0) return cudaSuccess;
+  ProfScope ps("absmax", st);
   k_absmax<<<grid_for(rows * cols / 4 + 1, 256), 256, 0, st>>>(x, rows, cols, rowscale, slot);
   return cudaGetLastError();
 }
@@ -146,6 +147,7 @@ cudaError_t launch_quantize(const float* x, int64_t rows, int64_t cols, const fl
     if (e != cudaSuccess) return e;
   }
   const int64_t groups = (count + 15) / 8;
+  ProfScope ps("quantize", st);
   k_quantize<<<grid_for(groups, 256, 16), 256, 0, st>>>(x, rows, cols, rowscale, g0, amax_slot, bits, seed, step, tag,
                                                        q, ld, qt, ldt, scale_out, status);
   return cudaGetLastError();

@@ -74,7 +74,8 @@ EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tan
            "tango_gat_ctx_bytes", "tango_gat_layer_fwd", "tango_gat_layer_bwd", "tango_gat_ctx_get_view",
            "tango_gcn_ctx_bytes", "tango_gcn_layer_fwd", "tango_gcn_layer_bwd", "tango_gcn_ctx_get_view",
            "tango_comm_unique_id_bytes", "tango_comm_get_unique_id", "tango_comm_init", "tango_comm_destroy",
-           "tango_comm_set_partition"]
+           "tango_comm_set_partition", "tango_profile_enable", "tango_launch_count", "tango_profile_collect",
+           "tango_profile_num_entries", "tango_profile_entry", "tango_profile_reset"]
 
 
 def load(path: str = LIB_PATH):
@@ -114,6 +115,12 @@ def load(path: str = LIB_PATH):
     L.tango_comm_init.argtypes = [C.POINTER(_P), _P, i32, i32]
     L.tango_comm_destroy.argtypes = [_P]
     L.tango_comm_set_partition.argtypes = [_P, _P]
+    L.tango_profile_enable.argtypes = [i32]
+    L.tango_profile_enable.restype = None
+    L.tango_launch_count.restype = i64
+    L.tango_profile_num_entries.restype = i32
+    L.tango_profile_entry.argtypes = [i32, C.c_char_p, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    L.tango_profile_reset.restype = None
     _lib = L
     return L
 
@@ -137,6 +144,31 @@ def _stream():
 
 def ld32(cols: int) -> int:
     return (cols + 31) // 32 * 32
+
+
+# ---------------------------------------------------------------------------------------- tracing
+def profile_enable(on: bool = True):
+    load().tango_profile_enable(1 if on else 0)
+
+
+def launch_count() -> int:
+    return int(load().tango_launch_count())
+
+
+def profile_read(reset: bool = True) -> dict:
+    """{kernel name: (total device ms, launches)} since the last reset (waits for pending events)."""
+    L = load()
+    _check(L.tango_profile_collect(), "tango_profile_collect")
+    out = {}
+    buf = C.create_string_buffer(64)
+    ms, cnt = C.c_double(), C.c_int64()
+    for i in range(L.tango_profile_num_entries()):
+        _check(L.tango_profile_entry(i, buf, 64, C.byref(ms), C.byref(cnt)), "tango_profile_entry")
+        if cnt.value:
+            out[buf.value.decode()] = (ms.value, cnt.value)
+    if reset:
+        L.tango_profile_reset()
+    return out
 
 
 # ---------------------------------------------------------------------------------------- graph
@@ -414,6 +446,11 @@ class GCNLayer:
                                      self.comm.handle if self.comm else None, _ptr(self.status), _stream()),
                "tango_gcn_layer_bwd")
         return dX, dW
+
+    def check_status(self):
+        st = int(self.status.item())
+        if st != 0:
+            raise TangoError(st, "device status")
 
     def view(self):
         L = load()

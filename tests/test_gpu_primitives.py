@@ -114,7 +114,7 @@ def test_gemm_mixed_layouts(T):
     one = cu(np.array([1.0], np.float32))
     ref = A.astype(np.int64) @ B.astype(np.int64)
     o1 = T.gemm_q(cu(A), one, T.TANGO_K_MAJOR, cu(B), one, T.TANGO_MN_MAJOR, M, N, K, want=("i32",))
-    o2 = T.gemm_q(cu(np.ascontiguousarray(A.T)), one, T.TANGO_MN_MAJOR, cu(np.ascontiguousarray(B.T)), one,
+    o2 = T.gemm_q(cu(_pad(np.ascontiguousarray(A.T), 224)), one, T.TANGO_MN_MAJOR, cu(np.ascontiguousarray(B.T)), one,
                   T.TANGO_K_MAJOR, M, N, K, want=("i32",))
     assert np.array_equal(o1["i32"].cpu().numpy(), ref)
     assert np.array_equal(o2["i32"].cpu().numpy(), ref)
