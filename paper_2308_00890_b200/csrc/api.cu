@@ -327,9 +327,12 @@ tango_status tango_edge_sum(const tango_graph* G, int32_t dir, int32_t heads, co
 // ================================================================== GAT ctx layout
 namespace {
 struct GatLayout {
-  int64_t n, N, E, F, H, Dh, HD, ldF, ldHD, ldFt;
+  int64_t n, N, E, Eo, F, H, Dh, HD, ldF, ldHD, ldFt, cap_in, cap_out;
   size_t off_scal, off_qH, off_qW, off_qWt, off_qHp, off_S, off_D, off_qS, off_qD, off_m, off_den, off_P, off_dD,
       off_qG, off_dal, off_dHp, off_qdHp, off_dW64, total;
+  // segment plans (gat.cu) and heavy-segment scratch
+  size_t off_pin_hbase, off_pin_hseg, off_pin_hrow, off_pin_cnt, off_pout_hbase, off_pout_hseg, off_pout_hrow,
+      off_pout_cnt, off_h1, off_h2, off_hdS, off_hagg;
 };
 GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   GatLayout L{};
@@ -360,8 +363,30 @@ GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   L.off_dHp = take((size_t)L.n * L.HD * 4);
   L.off_qdHp = take((size_t)L.n * L.ldHD);
   L.off_dW64 = take((size_t)L.F * L.HD * 8);
+  const int64_t C = G->chunk_edges > 0 ? G->chunk_edges : 256;
+  L.Eo = G->e_out;
+  L.cap_in = 2 * L.E / C + 1;
+  L.cap_out = 2 * L.Eo / C + 1;
+  L.off_pin_hbase = take((size_t)L.n * 4);
+  L.off_pin_hseg = take((size_t)L.cap_in * 4);
+  L.off_pin_hrow = take((size_t)L.n * 4);
+  L.off_pin_cnt = take(16);
+  L.off_pout_hbase = take((size_t)L.n * 4);
+  L.off_pout_hseg = take((size_t)L.cap_out * 4);
+  L.off_pout_hrow = take((size_t)L.n * 4);
+  L.off_pout_cnt = take(16);
+  L.off_h1 = take((size_t)L.cap_in * L.H * 4);     // fwd: hmax   bwd: hP
+  L.off_h2 = take((size_t)L.cap_in * L.H * 4);     // fwd: hden   bwd: hdD
+  L.off_hdS = take((size_t)L.cap_out * L.H * 4);
+  L.off_hagg = take((size_t)(L.cap_in > L.cap_out ? L.cap_in : L.cap_out) * L.HD * 4);
   L.total = o;
   return L;
+}
+PlanDev plan_of(char* c, size_t hb, size_t hs, size_t hr, size_t cn, int64_t cap) {
+  PlanDev p;
+  p.hbase = (int32_t*)(c + hb); p.hseg_row = (int32_t*)(c + hs); p.hrow = (int32_t*)(c + hr);
+  p.counts = (int32_t*)(c + cn); p.cap = cap;
+  return p;
 }
 tango_status check_gat(const tango_graph* G, const tango_gat_params* p) {
   TRY(check_graph(G, true));
@@ -471,14 +496,18 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   TRY(comm_gather_rows(comm, qHp, (size_t)L.ldHD, st));
   TRY(comm_gather_rows(comm, qS, (size_t)L.H, st));
   TRY(comm_gather_rows(comm, qD, (size_t)L.H, st));
-  // F5 + F6: one destination-row kernel (③ SDDMM-add + LeakyReLU, ④ softmax, ⑤ SPMM)
+  // F5 + F6: segment plan of the in-CSR, then softmax statistics, aggregation and heavy-row combine
   if (amax_out) TRY_CUDA(cudaMemsetAsync(amax_out, 0, 4, st));
-  GatFwdDstArgs fa{};
-  fa.g = g; fa.d = {p->heads, p->head_dim, (int)L.HD}; fa.slope = p->neg_slope;
+  const PlanDev pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in);
+  TRY_CUDA(cudaMemsetAsync(pin.counts, 0, 16, st));
+  TRY(launch_status(launch_plan(G->in_ptr, L.n, g.chunk, pin, st)));
+  GatFwdArgs fa{};
+  fa.g = g; fa.d = {p->heads, p->head_dim, (int)L.HD}; fa.slope = p->neg_slope; fa.bits = p->bits;
   fa.qS = qS; fa.amax_S = sc + SL_AMAX_S; fa.qD = qD; fa.amax_D = sc + SL_AMAX_D;
-  fa.qHp = qHp; fa.ldHp = L.ldHD; fa.amax_Hp = sc + SL_AMAX_HP; fa.bits = p->bits;
+  fa.qHp = qHp; fa.ldHp = L.ldHD; fa.amax_Hp = sc + SL_AMAX_HP;
   fa.Hout = H_out; fa.m = m; fa.den = den; fa.amax_out = reinterpret_cast<unsigned*>(amax_out);
-  TRY(launch_status(launch_gat_fwd_dst(fa, st)));
+  fa.plan = pin; fa.hmax = (float*)(c + L.off_h1); fa.hden = (float*)(c + L.off_h2); fa.hagg = (float*)(c + L.off_hagg);
+  TRY(launch_status(launch_gat_fwd(fa, st)));
   TRY(comm_max(comm, amax_out, amax_out ? 1 : 0, st));
   TRY(comm_gather_rows(comm, m, (size_t)L.H * 4, st));
   TRY(comm_gather_rows(comm, den, (size_t)L.H * 4, st));
@@ -529,24 +558,27 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
                                     rng.step, tag_of(layer_id, R_G), qG + r0 * L.ldHD, L.ldHD, nullptr, 0,
                                     scf + SL_S_G, dev_status, st)));
   TRY(comm_gather_rows(comm, qG, (size_t)L.ldHD, st));
-  // B2-B4: destination rows
-  GatBwdDstArgs da{};
-  da.g = g; da.d = {p->heads, p->head_dim, (int)L.HD}; da.slope = p->neg_slope; da.bits = p->bits;
-  da.qS = qS; da.amax_S = sc + SL_AMAX_S; da.qD = qD; da.amax_D = sc + SL_AMAX_D;
-  da.qHp = qHp; da.ldHp = L.ldHD; da.amax_Hp = sc + SL_AMAX_HP;
-  da.qG = qG; da.ldG = L.ldHD; da.amax_G = sc + SL_AMAX_G;
-  da.m = m; da.den = den; da.dalpha = dal; da.P = P; da.dD = dD;
-  TRY(launch_status(launch_gat_bwd_dst(da, st)));
+  // B2-B4: destination rows (in-CSR plan from the forward call), B5-B7: source rows (out-CSR plan)
+  const PlanDev pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in);
+  const PlanDev pout = plan_of(c, L.off_pout_hbase, L.off_pout_hseg, L.off_pout_hrow, L.off_pout_cnt, L.cap_out);
+  TRY_CUDA(cudaMemsetAsync(pin.counts, 0, 16, st));
+  TRY(launch_status(launch_plan(G->in_ptr, L.n, g.chunk, pin, st)));
+  TRY_CUDA(cudaMemsetAsync(pout.counts, 0, 16, st));
+  TRY(launch_status(launch_plan(G->out_ptr, L.n, g.chunk, pout, st)));
+  GatBwdArgs ba{};
+  ba.g = g; ba.d = {p->heads, p->head_dim, (int)L.HD}; ba.slope = p->neg_slope; ba.bits = p->bits;
+  ba.qS = qS; ba.amax_S = sc + SL_AMAX_S; ba.qD = qD; ba.amax_D = sc + SL_AMAX_D;
+  ba.qHp = qHp; ba.ldHp = L.ldHD; ba.amax_Hp = sc + SL_AMAX_HP;
+  ba.qG = qG; ba.ldG = L.ldHD; ba.amax_G = sc + SL_AMAX_G;
+  ba.m = m; ba.den = den; ba.dalpha = dal; ba.P = P; ba.dD = dD;
+  ba.a_src = p->a_src; ba.a_dst = p->a_dst;
+  ba.dHp = dHp; ba.amax_dHp = sc + SL_AMAX_DHP; ba.da_src = da_src; ba.da_dst = da_dst;
+  ba.pin = pin; ba.pout = pout;
+  ba.hP = (float*)(c + L.off_h1); ba.hdD = (float*)(c + L.off_h2); ba.hdS = (float*)(c + L.off_hdS);
+  ba.hagg = (float*)(c + L.off_hagg);
+  TRY(launch_status(launch_gat_bwd_dst(ba, st)));
   TRY(comm_gather_rows(comm, P, (size_t)L.H * 4, st));
-  // B5-B7: source rows
-  GatBwdSrcArgs sa{};
-  sa.g = g; sa.d = da.d; sa.slope = p->neg_slope; sa.bits = p->bits;
-  sa.qS = qS; sa.amax_S = da.amax_S; sa.qD = qD; sa.amax_D = da.amax_D;
-  sa.qHp = qHp; sa.ldHp = L.ldHD; sa.amax_Hp = da.amax_Hp;
-  sa.qG = qG; sa.ldG = L.ldHD; sa.amax_G = da.amax_G;
-  sa.m = m; sa.den = den; sa.P = P; sa.dD = dD; sa.a_src = p->a_src; sa.a_dst = p->a_dst;
-  sa.dHp = dHp; sa.amax_dHp = sc + SL_AMAX_DHP; sa.da_src = da_src; sa.da_dst = da_dst;
-  TRY(launch_status(launch_gat_bwd_src(sa, st)));
+  TRY(launch_status(launch_gat_bwd_src(ba, st)));
   TRY(comm_max(comm, sc + SL_AMAX_DHP, 1, st));
   TRY(comm_sum_f32(comm, da_src, (size_t)L.HD, st));
   TRY(comm_sum_f32(comm, da_dst, (size_t)L.HD, st));

@@ -70,17 +70,31 @@ struct GraphDev {
   int chunk;
 };
 
-struct GatFwdDstArgs {
-  GraphDev g; GatDims d; float slope;
+// Segment plan of one CSR (gat.cu k_plan): rows with deg > C_E are "heavy" and split into
+// ceil(deg/C_E) canonical chunks ("segments") with scratch slots [hbase[v], hbase[v] + nseg).
+struct PlanDev {
+  int32_t* hbase;      // [n_local] first slot of a heavy row, -1 for light rows
+  int32_t* hseg_row;   // [cap] local row of each heavy segment slot
+  int32_t* hrow;       // [n_local] heavy rows (first counts[1] entries)
+  int32_t* counts;     // [0] = #heavy segments, [1] = #heavy rows (zeroed before k_plan)
+  int64_t cap;         // slot capacity: 2 * e / C_E + 1
+};
+cudaError_t launch_plan(const int64_t* ptr, int64_t n, int chunk, const PlanDev& p, cudaStream_t st);
+
+struct GatFwdArgs {
+  GraphDev g; GatDims d; float slope; int bits;
   const int8_t* qS; const unsigned* amax_S;   // [N][H]
-  const int8_t* qD; const unsigned* amax_D;   // [N][H] (rows row_begin.. used)
-  const int8_t* qHp; int64_t ldHp; const unsigned* amax_Hp; int bits;   // [N][ldHp]
+  const int8_t* qD; const unsigned* amax_D;   // [N][H]
+  const int8_t* qHp; int64_t ldHp; const unsigned* amax_Hp;   // [N][ldHp]
   float* Hout; float* m; float* den;          // Hout [n_local][HD]; m, den [N][H] (own rows written)
   unsigned* amax_out;
+  PlanDev plan;                               // in-CSR plan
+  float* hmax; float* hden;                   // [cap][H] heavy-segment softmax partials
+  float* hagg;                                // [cap][HD] heavy-segment aggregation partials
 };
-cudaError_t launch_gat_fwd_dst(const GatFwdDstArgs& a, cudaStream_t st);
+cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st);
 
-struct GatBwdDstArgs {
+struct GatBwdArgs {
   GraphDev g; GatDims d; float slope; int bits;
   const int8_t* qS; const unsigned* amax_S;
   const int8_t* qD; const unsigned* amax_D;
@@ -89,22 +103,16 @@ struct GatBwdDstArgs {
   const float* m; const float* den;          // [N][H]
   float* dalpha;                             // scratch [e_in][H]
   float* P; float* dD;                       // [N][H] own rows written
-};
-cudaError_t launch_gat_bwd_dst(const GatBwdDstArgs& a, cudaStream_t st);
-
-struct GatBwdSrcArgs {
-  GraphDev g; GatDims d; float slope; int bits;
-  const int8_t* qS; const unsigned* amax_S;
-  const int8_t* qD; const unsigned* amax_D;
-  const int8_t* qHp; int64_t ldHp; const unsigned* amax_Hp;
-  const int8_t* qG; int64_t ldG; const unsigned* amax_G;
-  const float* m; const float* den; const float* P;   // [N][H]
-  const float* dD;                                    // [N][H] (own rows)
   const float* a_src; const float* a_dst;
-  float* dHp; unsigned* amax_dHp;                     // [n_local][HD]
-  float* da_src; float* da_dst;                       // [HD], accumulated with atomics (pre-zeroed)
+  float* dHp; unsigned* amax_dHp;            // [n_local][HD]
+  float* da_src; float* da_dst;              // [HD], accumulated with atomics (pre-zeroed)
+  PlanDev pin, pout;                         // in-CSR and out-CSR plans
+  float* hP; float* hdD;                     // [pin.cap][H]
+  float* hdS;                                // [pout.cap][H]
+  float* hagg;                               // [pout.cap][HD]
 };
-cudaError_t launch_gat_bwd_src(const GatBwdSrcArgs& a, cudaStream_t st);
+cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st);
+cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st);
 
 // standalone primitives (unfused; used by the primitive C-ABI entry points)
 cudaError_t launch_sddmm_add(const GraphDev& g, int heads, const int8_t* qS, const float* sS, const int8_t* qD,
