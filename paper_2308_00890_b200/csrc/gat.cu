@@ -585,17 +585,18 @@ __device__ __forceinline__ float bwd_src_seg(const GatBwdArgs& a, const Seg& s, 
 template <int VPL>
 __device__ __forceinline__ void bwd_src_finalize(const GatBwdArgs& a, int64_t ul, int64_t ug, int myh, float dS,
                                                  const float (&sum)[VPL], const Row<VPL>& hw, float sG, float sHp,
-                                                 const float (&asrc)[VPL], const float (&adst)[VPL],
                                                  float (&das)[VPL], float (&dad)[VPL], float& amax_loc, int H) {
   constexpr int HD = 32 * VPL;
   const int lane = threadIdx.x & 31;
   const float dD = a.dD[ug * H + myh];
   float* dst = a.dHp + ul * HD + lane * VPL;
+  const float* asrc = a.a_src + lane * VPL;
+  const float* adst = a.a_dst + lane * VPL;
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     const float agg = __fmul_rn(sum[k], sG);
-    const float t2 = __fadd_rn(agg, __fmul_rn(dS, asrc[k]));
-    const float o = __fadd_rn(t2, __fmul_rn(dD, adst[k]));
+    const float t2 = __fadd_rn(agg, __fmul_rn(dS, __ldg(asrc + k)));
+    const float o = __fadd_rn(t2, __fmul_rn(dD, __ldg(adst + k)));
     amax_loc = fmaxf(amax_loc, fabsf(o));
     dst[k] = o;
     const float hp = __fmul_rn(row_f<VPL>(hw, k), sHp);
@@ -644,11 +645,9 @@ __global__ void __launch_bounds__(256) k_bwd_src(const GatBwdArgs a) {
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
   const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
   const float sGH = __fmul_rn(scG.s, scH.s);
-  float asrc[VPL], adst[VPL], das[VPL], dad[VPL];
+  float das[VPL], dad[VPL];
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    asrc[k] = a.a_src[lane * VPL + k]; adst[k] = a.a_dst[lane * VPL + k]; das[k] = 0.0f; dad[k] = 0.0f;
-  }
+  for (int k = 0; k < VPL; ++k) { das[k] = 0.0f; dad[k] = 0.0f; }
   float amax_loc = 0.0f;
   const int64_t n = a.g.n_local, nitems = n + load_count(a.pout.counts);
   for (int64_t item = (int64_t)blockIdx.x * WPB + w; item < nitems; item += (int64_t)gridDim.x * WPB) {
@@ -671,7 +670,7 @@ __global__ void __launch_bounds__(256) k_bwd_src(const GatBwdArgs a) {
       continue;
     }
     const float dS = __shfl_sync(0xffffffffu, dSl, myh * LPH);
-    bwd_src_finalize<VPL>(a, s.vl, ug, myh, dS, part, hw, scG.s, scH.s, asrc, adst, das, dad, amax_loc, H);
+    bwd_src_finalize<VPL>(a, s.vl, ug, myh, dS, part, hw, scG.s, scH.s, das, dad, amax_loc, H);
   }
   bwd_src_flush<VPL>(a, sh_da, &sh_amax, das, dad, amax_loc);
 }
@@ -690,11 +689,9 @@ __global__ void __launch_bounds__(256) k_bwd_src_combine(const GatBwdArgs a) {
   __syncthreads();
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
   const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
-  float asrc[VPL], adst[VPL], das[VPL], dad[VPL];
+  float das[VPL], dad[VPL];
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    asrc[k] = a.a_src[lane * VPL + k]; adst[k] = a.a_dst[lane * VPL + k]; das[k] = 0.0f; dad[k] = 0.0f;
-  }
+  for (int k = 0; k < VPL; ++k) { das[k] = 0.0f; dad[k] = 0.0f; }
   float amax_loc = 0.0f;
   const int64_t hrows = load_count(a.pout.counts + 1);
   for (int64_t r = (int64_t)blockIdx.x * WPB + w; r < hrows; r += (int64_t)gridDim.x * WPB) {
@@ -715,7 +712,7 @@ __global__ void __launch_bounds__(256) k_bwd_src_combine(const GatBwdArgs a) {
       for (int k = 0; k < VPL; ++k) tot[k] = __fadd_rn(tot[k], p[k]);
     }
     const Row<VPL> hw = load_row<VPL>(a.qHp + ug * a.ldHp + lane * VPL);
-    bwd_src_finalize<VPL>(a, ul, ug, myh, dS, tot, hw, scG.s, scH.s, asrc, adst, das, dad, amax_loc, H);
+    bwd_src_finalize<VPL>(a, ul, ug, myh, dS, tot, hw, scG.s, scH.s, das, dad, amax_loc, H);
   }
   bwd_src_flush<VPL>(a, sh_da, &sh_amax, das, dad, amax_loc);
 }

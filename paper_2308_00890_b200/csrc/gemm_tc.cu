@@ -26,13 +26,14 @@ constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BKB;  // 16 KB
 constexpr int B_BYTES_MAX = 256 * BKB;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES_MAX;
-constexpr int GEMM_THREADS = 192;
+constexpr int EPI_WARPS = 8;       // two per TMEM sub-partition, each owning half of the N tile
+constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4096 + 1024;
 
 struct KParams {
   int64_t M, N, K;
   int BN, n_tiles_m, n_tiles_n, splits, kb_per_split, total_kb, nblk_b;
-  int a_mn, b_mn, mode;
+  int a_mn, b_mn, split_halves;
   int64_t total_tiles;
   uint32_t idesc, stage_tx, tmem_cols;
   const float* sA; const float* sB; const float* rowscale;
@@ -44,6 +45,13 @@ struct KParams {
   void* C; int64_t ldc;
 };
 
+// dequantized epilogue value: v = i2f(acc) * (s_A s_B) [* rowscale]  (two roundings)
+__device__ __forceinline__ float deq(uint32_t acc, float sAB, bool has_rs, float rs) {
+  float v = __fmul_rn(__int2float_rn((int)acc), sAB);
+  return has_rs ? __fmul_rn(v, rs) : v;
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ KParams p) {
@@ -62,7 +70,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 128); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 32 * EPI_WARPS); }
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
@@ -133,12 +141,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else {
-    // ------------------------------------------------------------- epilogue (warps 2..5)
+    // ------------------------------------------------------------- epilogue (warps 2..9)
+    const int ew = warp - 2;                  // 0..7
     const int sub = warp & 3;                 // TMEM sub-partition this warp may access
+    const int half = ew >> 2;                 // which half of the N tile
     const int rin = sub * 32 + lane;          // row within the tile
+    const int nch = p.BN / 32;
+    const int c_lo = p.split_halves ? half * (nch / 2) : 0;
+    const int c_hi = p.split_halves ? (half + 1) * (nch / 2) : (half == 0 ? nch : 0);
     const float sAB = (p.sA && p.sB) ? __fmul_rn(*p.sA, *p.sB) : 1.0f;
+    const bool has_rs = p.rowscale != nullptr;
     Scale qs = {1.0f, 1.0f, false};
-    if (p.mode == EPI_QUANT) {
+    if (MODE == EPI_QUANT) {
       qs = scale_from_amax(amax_load(p.amax_in), p.bits);
       if (blockIdx.x == 0 && threadIdx.x == 64) {
         if (p.scale_out) *p.scale_out = qs.s;
@@ -147,7 +161,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     const int qmax = (1 << (p.bits - 1)) - 1;
     float amax_v = 0.0f, amax_s = 0.0f, amax_d = 0.0f;
-    const bool dots = (p.mode == EPI_AMAX) && (p.a_src != nullptr);
+    const bool dots = (MODE == EPI_AMAX) && (p.a_src != nullptr);
+    const bool fast_heads = dots && (p.head_dim % 32 == 0);
     uint32_t lt = 0;
     int loaded_nt = -1;
     for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++lt) {
@@ -157,35 +172,60 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t buf = lt & 1, tph = (lt >> 1) & 1;
       if (dots && nt != loaded_nt) {
         // stage this N-tile's attention vectors in smem (epilogue warps only: named barrier 1)
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        for (int j = threadIdx.x - 64; j < p.BN; j += 128) {
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+        for (int j = threadIdx.x - 64; j < p.BN; j += 32 * EPI_WARPS) {
           const int64_t col = (int64_t)nt * p.BN + j;
           sm_asrc[j] = col < p.N ? p.a_src[col] : 0.0f;
           sm_adst[j] = col < p.N ? p.a_dst[col] : 0.0f;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
         loaded_nt = nt;
       }
       mbar_wait(&tfull[buf], tph);
       tc_fence_after();
       const int64_t row = (int64_t)mt * BM + rin;
       const bool row_ok = row < p.M;
-      const float rs = (p.rowscale && row_ok) ? p.rowscale[row] : 1.0f;
+      const float rs = (has_rs && row_ok) ? p.rowscale[row] : 1.0f;
       const uint32_t tbase = tmem_base + ((uint32_t)(sub * 32) << 16) + buf * (uint32_t)p.BN;
       float s_acc = 0.0f, d_acc = 0.0f;
       int dcount = 0;
-      for (int c = 0; c < p.BN / 32; ++c) {
+      for (int c = c_lo; c < c_hi; ++c) {
         uint32_t r[32];
         tmem_ld32(tbase + c * 32, r);
         tmem_ld_wait();
         const int64_t col0 = (int64_t)nt * p.BN + c * 32;
-        if (p.mode == EPI_AMAX) {
+        const bool full_chunk = col0 + 32 <= p.N;
+        if constexpr (MODE == EPI_AMAX) {
+          if (full_chunk && (fast_heads || !dots)) {
+            float v[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int64_t col = col0 + i;
-            if (col < p.N) {
-              float v = __fmul_rn(__int2float_rn((int)r[i]), sAB);
-              if (p.rowscale) v = __fmul_rn(v, rs);
+            for (int i = 0; i < 32; ++i) v[i] = deq(r[i], sAB, has_rs, rs);
+            if (row_ok) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) amax_v = fmaxf(amax_v, fabsf(v[i]));
+            }
+            if (dots) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                s_acc = __fmaf_rn(v[i], sm_asrc[c * 32 + i], s_acc);
+                d_acc = __fmaf_rn(v[i], sm_adst[c * 32 + i], d_acc);
+              }
+              if (((col0 + 32) % p.head_dim) == 0) {
+                if (row_ok) {
+                  const int h = (int)(col0 / p.head_dim);
+                  p.S[row * p.heads + h] = s_acc;
+                  p.Dd[row * p.heads + h] = d_acc;
+                  amax_s = fmaxf(amax_s, fabsf(s_acc));
+                  amax_d = fmaxf(amax_d, fabsf(d_acc));
+                }
+                s_acc = 0.0f; d_acc = 0.0f;
+              }
+            }
+          } else {
+            for (int i = 0; i < 32; ++i) {
+              const int64_t col = col0 + i;
+              if (col >= p.N) break;
+              const float v = deq(r[i], sAB, has_rs, rs);
               if (row_ok) amax_v = fmaxf(amax_v, fabsf(v));
               if (dots) {
                 s_acc = __fmaf_rn(v, sm_asrc[c * 32 + i], s_acc);
@@ -203,7 +243,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               }
             }
           }
-        } else if (p.mode == EPI_QUANT) {
+        } else if constexpr (MODE == EPI_QUANT) {
           uint32_t packed[8];
 #pragma unroll
           for (int g8 = 0; g8 < 4; ++g8) {
@@ -213,8 +253,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int i = g8 * 8 + k;
-              float v = __fmul_rn(__int2float_rn((int)r[i]), sAB);
-              if (p.rowscale) v = __fmul_rn(v, rs);
+              const float v = deq(r[i], sAB, has_rs, rs);
               const int qq = (col0 + i < p.N) ? sr_quant(v, qs.r, sr_half(rnd, k), qmax) : 0;
               const uint32_t byte = (uint32_t)(qq & 0xFF);
               if (k < 4) lo |= byte << (8 * k); else hi |= byte << (8 * (k - 4));
@@ -226,47 +265,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
             dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
           }
-        } else if (p.mode == EPI_STORE) {
+        } else if constexpr (MODE == EPI_STORE) {
           float* Cf = reinterpret_cast<float*>(p.C);
           if (row_ok) {
-            if (col0 + 32 <= p.N && ((p.ldc & 3) == 0)) {
+            if (full_chunk && ((p.ldc & 3) == 0)) {
               float4* dst = reinterpret_cast<float4*>(Cf + row * p.ldc + col0);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                float4 o;
-                o.x = __fmul_rn(__int2float_rn((int)r[4 * i + 0]), sAB);
-                o.y = __fmul_rn(__int2float_rn((int)r[4 * i + 1]), sAB);
-                o.z = __fmul_rn(__int2float_rn((int)r[4 * i + 2]), sAB);
-                o.w = __fmul_rn(__int2float_rn((int)r[4 * i + 3]), sAB);
-                if (p.rowscale) { o.x = __fmul_rn(o.x, rs); o.y = __fmul_rn(o.y, rs); o.z = __fmul_rn(o.z, rs); o.w = __fmul_rn(o.w, rs); }
-                dst[i] = o;
-              }
+              for (int i = 0; i < 8; ++i)
+                dst[i] = make_float4(deq(r[4 * i], sAB, has_rs, rs), deq(r[4 * i + 1], sAB, has_rs, rs),
+                                     deq(r[4 * i + 2], sAB, has_rs, rs), deq(r[4 * i + 3], sAB, has_rs, rs));
             } else {
-              for (int i = 0; i < 32; ++i)
-                if (col0 + i < p.N) {
-                  float v = __fmul_rn(__int2float_rn((int)r[i]), sAB);
-                  if (p.rowscale) v = __fmul_rn(v, rs);
-                  Cf[row * p.ldc + col0 + i] = v;
-                }
+              for (int i = 0; i < 32 && col0 + i < p.N; ++i) Cf[row * p.ldc + col0 + i] = deq(r[i], sAB, has_rs, rs);
             }
           }
-        } else if (p.mode == EPI_I32) {
+        } else if constexpr (MODE == EPI_I32) {
           int32_t* Ci = reinterpret_cast<int32_t*>(p.C);
           if (row_ok)
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i < p.N) Ci[row * p.ldc + col0 + i] = (int32_t)r[i];
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i) Ci[row * p.ldc + col0 + i] = (int32_t)r[i];
         } else {  // EPI_ATOMIC64
           unsigned long long* C64 = reinterpret_cast<unsigned long long*>(p.C);
           if (row_ok)
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i < p.N && r[i] != 0u)
-                atomicAdd(C64 + row * p.ldc + col0 + i, (unsigned long long)(long long)(int32_t)r[i]);
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i)
+              if (r[i] != 0u) atomicAdd(C64 + row * p.ldc + col0 + i, (unsigned long long)(long long)(int32_t)r[i]);
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[buf]);
     }
-    if (p.mode == EPI_AMAX) {
+    if (MODE == EPI_AMAX) {
       amax_v = warp_max(amax_v);
       if (lane == 0 && p.amax_slot) atomic_max_abs(p.amax_slot, amax_v);
       if (dots) {
@@ -335,7 +361,13 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
   p.kb_per_split = (p.total_kb + p.splits - 1) / p.splits;
   p.splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
   p.nblk_b = (BN + 127) / 128;
-  p.a_mn = a.a_mn; p.b_mn = a.b_mn; p.mode = a.mode;
+  p.a_mn = a.a_mn; p.b_mn = a.b_mn;
+  {
+    const int nch = BN / 32;
+    bool halves = (nch % 2) == 0;
+    if (halves && a.mode == EPI_AMAX && a.a_src && ((BN / 2) % a.head_dim) != 0) halves = false;
+    p.split_halves = halves ? 1 : 0;
+  }
   p.total_tiles = (int64_t)p.n_tiles_m * p.n_tiles_n * p.splits;
   p.idesc = make_idesc_i8(BM, BN, a.a_mn, a.b_mn);
   p.stage_tx = A_BYTES + (a.b_mn ? p.nblk_b * BKB * 128 : BN * BKB);
@@ -358,14 +390,23 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
   else ok = make_map(&tB, a.B, (uint64_t)a.ldb, (uint64_t)a.K, (uint64_t)a.ldb, 128, BKB);
   if (!ok) return cudaErrorInvalidValue;
 
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
-    cudaFuncSetAttribute(k_gemm_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  });
   int64_t grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
   static const char* names[] = {"gemm_amax", "gemm_quant", "gemm_store", "gemm_i32", "gemm_splitk_i64"};
   ProfScope ps(names[a.mode], st);
-  k_gemm_i8<<<(unsigned)grid, GEMM_THREADS, SMEM_BYTES, st>>>(tA, tB, p);
+  switch (a.mode) {
+#define LAUNCH(M_)                                                                                   \
+  case M_: {                                                                                         \
+    static std::once_flag once_##M_;                                                                 \
+    std::call_once(once_##M_, [] {                                                                   \
+      cudaFuncSetAttribute(k_gemm_i8<M_>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);  \
+    });                                                                                              \
+    k_gemm_i8<M_><<<(unsigned)grid, GEMM_THREADS, SMEM_BYTES, st>>>(tA, tB, p);                     \
+    break;                                                                                           \
+  }
+    LAUNCH(EPI_AMAX) LAUNCH(EPI_QUANT) LAUNCH(EPI_STORE) LAUNCH(EPI_I32) LAUNCH(EPI_ATOMIC64)
+#undef LAUNCH
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
