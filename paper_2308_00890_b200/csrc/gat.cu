@@ -55,17 +55,19 @@ struct Seg {
   int c, base, nseg;    // chunk index, first slot and segment count of a heavy row
 };
 
-// Decode work item `item` of the space [0, n) rows  U  [n, n + hcount) heavy segments.
-// Returns false for a light-row item that belongs to a heavy row (skipped).
-__device__ __forceinline__ bool decode_item(int64_t item, int64_t n, const int64_t* ptr, const PlanDev& p, int chunk,
-                                            Seg& s) {
-  if (item < n) {
-    s.vl = item;
-    if (p.hbase[item] >= 0) return false;
-    s.eb = ptr[item]; s.ee = ptr[item + 1]; s.slot = -1; s.c = 0; s.base = -1; s.nseg = 1;
+// Decode work item `item` of the space [0, hcount) heavy segments  U  [hcount, hcount + n) rows
+// (the long heavy segments are handed out first).  Returns false for a row item that belongs to a
+// heavy row (skipped).
+__device__ __forceinline__ bool decode_item(int64_t item, int64_t hcount, const int64_t* ptr, const PlanDev& p,
+                                            int chunk, Seg& s) {
+  if (item >= hcount) {
+    const int64_t r = item - hcount;
+    s.vl = r;
+    if (p.hbase[r] >= 0) return false;
+    s.eb = ptr[r]; s.ee = ptr[r + 1]; s.slot = -1; s.c = 0; s.base = -1; s.nseg = 1;
     return true;
   }
-  s.slot = (int)(item - n);
+  s.slot = (int)item;
   s.vl = p.hseg_row[s.slot];
   s.base = p.hbase[s.vl];
   s.c = s.slot - s.base;
@@ -76,6 +78,14 @@ __device__ __forceinline__ bool decode_item(int64_t item, int64_t n, const int64
   return true;
 }
 __device__ __forceinline__ int64_t load_count(const int32_t* c) { return (int64_t)*(volatile const int32_t*)c; }
+
+// Dynamic work queue: lane 0 claims the next item index, broadcast to the warp.
+__device__ __forceinline__ int64_t claim(int32_t* counter) {
+  int it = 0;
+  if ((threadIdx.x & 31) == 0) it = atomicAdd(counter, 1);
+  return (int64_t)__shfl_sync(0xffffffffu, it, 0);
+}
+#define FOR_ITEMS(item, counter, nitems) for (int64_t item = claim(counter); item < (nitems); item = claim(counter))
 
 template <int H>
 __device__ __forceinline__ float head_pick(const float (&x)[H], int h) {
@@ -190,10 +200,10 @@ __global__ void __launch_bounds__(256) k_fwd_stats(const GatFwdArgs a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
-  const int64_t n = a.g.n_local, nitems = n + load_count(a.plan.counts);
-  for (int64_t item = (int64_t)blockIdx.x * WPB + w; item < nitems; item += (int64_t)gridDim.x * WPB) {
+  const int64_t hc = load_count(a.plan.counts), nitems = a.g.n_local + hc;
+  FOR_ITEMS(item, a.work + 0, nitems) {
     Seg s;
-    if (!decode_item(item, n, a.g.in_ptr, a.plan, a.g.chunk, s)) continue;
+    if (!decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s)) continue;
     const int64_t vg = a.g.row_begin + s.vl;
     int8_t qd[H];
 #pragma unroll
@@ -222,10 +232,10 @@ __global__ void __launch_bounds__(256) k_fwd_stats2(const GatFwdArgs a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
-  const int64_t n = a.g.n_local, hcnt = load_count(a.plan.counts);
-  for (int64_t si = (int64_t)blockIdx.x * WPB + w; si < hcnt; si += (int64_t)gridDim.x * WPB) {
+  const int64_t hcnt = load_count(a.plan.counts);
+  FOR_ITEMS(si, a.work + 1, hcnt) {
     Seg s;
-    decode_item(n + si, n, a.g.in_ptr, a.plan, a.g.chunk, s);
+    decode_item(si, hcnt, a.g.in_ptr, a.plan, a.g.chunk, s);
     const int64_t vg = a.g.row_begin + s.vl;
     int8_t qd[H];
 #pragma unroll
@@ -253,12 +263,12 @@ __global__ void __launch_bounds__(256) k_fwd_agg(const GatFwdArgs a) {
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
-  const int64_t n = a.g.n_local, nitems = n + load_count(a.plan.counts);
+  const int64_t hc = load_count(a.plan.counts), nitems = a.g.n_local + hc;
   const int8_t* xbase = a.qHp + lane * VPL;
   float amax_loc = 0.0f;
-  for (int64_t item = (int64_t)blockIdx.x * WPB + w; item < nitems; item += (int64_t)gridDim.x * WPB) {
+  FOR_ITEMS(item, a.work + 2, nitems) {
     Seg s;
-    if (!decode_item(item, n, a.g.in_ptr, a.plan, a.g.chunk, s)) continue;
+    if (!decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s)) continue;
     const int64_t vg = a.g.row_begin + s.vl;
     int8_t qd[H];
     float mx[H], den[H];
@@ -320,7 +330,7 @@ __global__ void __launch_bounds__(256) k_fwd_combine(const GatFwdArgs a) {
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
   const int64_t hrows = load_count(a.plan.counts + 1);
   float amax_loc = 0.0f;
-  for (int64_t r = (int64_t)blockIdx.x * WPB + w; r < hrows; r += (int64_t)gridDim.x * WPB) {
+  FOR_ITEMS(r, a.work + 3, hrows) {
     const int64_t vl = a.plan.hrow[r];
     const int64_t vg = a.g.row_begin + vl;
     const int base = a.plan.hbase[vl];
@@ -449,10 +459,10 @@ __global__ void __launch_bounds__(256) k_bwd_dst1(const GatBwdArgs a) {
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
   const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
   const float sGH = __fmul_rn(scG.s, scH.s);
-  const int64_t n = a.g.n_local, nitems = n + load_count(a.pin.counts);
-  for (int64_t item = (int64_t)blockIdx.x * WPB + w; item < nitems; item += (int64_t)gridDim.x * WPB) {
+  const int64_t hc = load_count(a.pin.counts), nitems = a.g.n_local + hc;
+  FOR_ITEMS(item, a.work + 0, nitems) {
     Seg s;
-    if (!decode_item(item, n, a.g.in_ptr, a.pin, a.g.chunk, s)) continue;
+    if (!decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s)) continue;
     const int64_t vg = a.g.row_begin + s.vl;
     int8_t qd[H];
     float mh[H], dh[H];
@@ -482,10 +492,10 @@ __global__ void __launch_bounds__(256) k_bwd_dst2(const GatBwdArgs a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
-  const int64_t n = a.g.n_local, hcnt = load_count(a.pin.counts);
-  for (int64_t si = (int64_t)blockIdx.x * WPB + w; si < hcnt; si += (int64_t)gridDim.x * WPB) {
+  const int64_t hcnt = load_count(a.pin.counts);
+  FOR_ITEMS(si, a.work + 1, hcnt) {
     Seg s;
-    decode_item(n + si, n, a.g.in_ptr, a.pin, a.g.chunk, s);
+    decode_item(si, hcnt, a.g.in_ptr, a.pin, a.g.chunk, s);
     const int64_t vg = a.g.row_begin + s.vl;
     int8_t qd[H];
     float mh[H], dh[H], P[H];
@@ -649,10 +659,10 @@ __global__ void __launch_bounds__(256) k_bwd_src(const GatBwdArgs a) {
 #pragma unroll
   for (int k = 0; k < VPL; ++k) { das[k] = 0.0f; dad[k] = 0.0f; }
   float amax_loc = 0.0f;
-  const int64_t n = a.g.n_local, nitems = n + load_count(a.pout.counts);
-  for (int64_t item = (int64_t)blockIdx.x * WPB + w; item < nitems; item += (int64_t)gridDim.x * WPB) {
+  const int64_t hc = load_count(a.pout.counts), nitems = a.g.n_local + hc;
+  FOR_ITEMS(item, a.work + 2, nitems) {
     Seg s;
-    if (!decode_item(item, n, a.g.out_ptr, a.pout, a.g.chunk, s)) continue;
+    if (!decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s)) continue;
     const int64_t ug = a.g.row_begin + s.vl;
     int8_t qs[H];
 #pragma unroll
@@ -694,7 +704,7 @@ __global__ void __launch_bounds__(256) k_bwd_src_combine(const GatBwdArgs a) {
   for (int k = 0; k < VPL; ++k) { das[k] = 0.0f; dad[k] = 0.0f; }
   float amax_loc = 0.0f;
   const int64_t hrows = load_count(a.pout.counts + 1);
-  for (int64_t r = (int64_t)blockIdx.x * WPB + w; r < hrows; r += (int64_t)gridDim.x * WPB) {
+  FOR_ITEMS(r, a.work + 3, hrows) {
     const int64_t ul = a.pout.hrow[r];
     const int64_t ug = a.g.row_begin + ul;
     const int base = a.pout.hbase[ul];
@@ -720,7 +730,7 @@ __global__ void __launch_bounds__(256) k_bwd_src_combine(const GatBwdArgs a) {
 // ------------------------------------------------------------------ dispatch
 static int item_grid(int64_t items) {
   int64_t g = (items + WPB - 1) / WPB;
-  const int64_t cap = (int64_t)num_sms() * 24;
+  const int64_t cap = (int64_t)num_sms() * 4;     // >= resident blocks; the work queue balances
   if (g > cap) g = cap;
   return (int)(g < 1 ? 1 : g);
 }
