@@ -332,7 +332,7 @@ struct GatLayout {
       off_qG, off_dal, off_dHp, off_qdHp, off_dW64, total;
   // segment plans (gat.cu) and heavy-segment scratch
   size_t off_pin_hbase, off_pin_hseg, off_pin_hrow, off_pin_cnt, off_pout_hbase, off_pout_hseg, off_pout_hrow,
-      off_pout_cnt, off_h1, off_h2, off_hdS, off_hagg, off_work;
+      off_pout_cnt, off_h1, off_h2, off_hdS, off_hagg, off_work, off_dS;
 };
 GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   GatLayout L{};
@@ -380,6 +380,7 @@ GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   L.off_hdS = take((size_t)L.cap_out * L.H * 4);
   L.off_hagg = take((size_t)(L.cap_in > L.cap_out ? L.cap_in : L.cap_out) * L.HD * 4);
   L.off_work = take(64);
+  L.off_dS = take((size_t)L.N * L.H * 4);
   L.total = o;
   return L;
 }
@@ -580,6 +581,7 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   ba.hP = (float*)(c + L.off_h1); ba.hdD = (float*)(c + L.off_h2); ba.hdS = (float*)(c + L.off_hdS);
   ba.hagg = (float*)(c + L.off_hagg);
   ba.work = (int32_t*)(c + L.off_work);
+  ba.dS = (float*)(c + L.off_dS);
   TRY_CUDA(cudaMemsetAsync(ba.work, 0, 64, st));
   TRY(launch_status(launch_gat_bwd_dst(ba, st)));
   TRY(comm_gather_rows(comm, P, (size_t)L.H * 4, st));

@@ -192,6 +192,58 @@ __device__ __forceinline__ void gather_fma_batch(const int8_t* __restrict__ xbas
   }
 }
 
+
+// ------------------------------------------------------------------ light-row tiles
+// A tile = 32 consecutive local rows, lane j owning row r0 + j.  Heavy rows inside the tile are
+// skipped (their segments are separate work items).  The tile's light rows form ONE edge stream
+// t = 0..T-1 (row after row, canonical order inside each row), so the per-row latency chain
+// (row pointers -> indices -> attention inputs) is paid once per tile instead of once per row and
+// the 8-deep gather pipeline runs across row boundaries; accumulators flush when the row changes.
+constexpr int TILE = 32;
+
+struct TileLane {
+  int64_t r, eb;        // this lane's local row and its first edge
+  int deg, off, end;    // degree (0 for heavy / absent rows), exclusive and inclusive scan
+  bool light;           // row exists and is light
+};
+
+__device__ __forceinline__ TileLane tile_setup(const int64_t* __restrict__ ptr, const int32_t* __restrict__ hbase,
+                                               int64_t r0, int64_t n, int& T) {
+  const int lane = threadIdx.x & 31;
+  TileLane L;
+  L.r = r0 + lane;
+  const bool has = L.r < n;
+  L.light = has && hbase[L.r] < 0;
+  L.eb = has ? ptr[L.r] : 0;
+  const int64_t ee = has ? ptr[L.r + 1] : 0;
+  L.deg = L.light ? (int)(ee - L.eb) : 0;
+  int x = L.deg;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  L.end = x;
+  L.off = x - L.deg;
+  T = __shfl_sync(0xffffffffu, x, 31);
+  return L;
+}
+// lane (row) of stream position t: the smallest j with end_j > t (rows of degree 0 are skipped)
+__device__ __forceinline__ int tile_row(int t, int end) {
+  int pos = 0;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const int ev = __shfl_sync(0xffffffffu, end, pos + s - 1);
+    if (ev <= t) pos += s;
+  }
+  return pos & 31;
+}
+// next row (lane) after `cur` with edges, -1 if none
+__device__ __forceinline__ int tile_next(unsigned act, int cur) {
+  const unsigned rest = cur >= 31 ? 0u : (act & ~((2u << cur) - 1u));
+  return rest ? __ffs(rest) - 1 : -1;
+}
+
 // ================================================================== forward
 // FS: light rows -> m, den (final);  heavy segments -> segment max (hmax)
 template <int H>
@@ -247,10 +299,107 @@ __global__ void __launch_bounds__(256) k_fwd_stats2(const GatFwdArgs a) {
   }
 }
 
+
+// FA on a tile of light rows: α per edge (lane-parallel), aggregation streamed across rows.
+template <int H, int VPL>
+__device__ __forceinline__ void fwd_agg_tile(const GatFwdArgs& a, int64_t r0, float (*buf)[H], int* rb,
+                                             float sS, float sD, float sH, float& amax_loc) {
+  constexpr int LPH = 32 / H;
+  constexpr int HD = 32 * VPL;
+  const int lane = threadIdx.x & 31, myh = lane / LPH;
+  int T;
+  const TileLane L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, a.g.n_local, T);
+  const int64_t vg = a.g.row_begin + L.r;
+  float mj[H], dj[H];
+  int qdj[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    mj[h] = L.deg > 0 ? a.m[vg * H + h] : 0.0f;
+    dj[h] = L.deg > 0 ? a.den[vg * H + h] : 0.0f;
+    qdj[h] = L.deg > 0 ? (int)a.qD[vg * H + h] : 0;
+  }
+  unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
+  while (zm) {   // light rows without in-edges: H_out = 0
+    const int j = __ffs(zm) - 1;
+    zm &= zm - 1;
+    float* dst = a.Hout + (r0 + j) * HD + lane * VPL;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) dst[k] = 0.0f;
+  }
+  const int8_t* xbase = a.qHp + lane * VPL;
+  float part[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) part[k] = 0.0f;
+  int cur = -1;
+  auto flush = [&](int j) {
+    float* dst = a.Hout + (r0 + j) * HD + lane * VPL;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const float o = __fmul_rn(part[k], sH);
+      amax_loc = fmaxf(amax_loc, fabsf(o));
+      dst[k] = o;
+      part[k] = 0.0f;
+    }
+  };
+  for (int base = 0; base < T; base += 32) {
+    const int cnt = T - base < 32 ? T - base : 32;
+    const int t = base + lane;
+    const int row = tile_row(t, L.end);
+    const int64_t ebr = __shfl_sync(0xffffffffu, L.eb, row);
+    const int offr = __shfl_sync(0xffffffffu, L.off, row);
+    float mr[H], dr[H];
+    int qdr[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      mr[h] = __shfl_sync(0xffffffffu, mj[h], row);
+      dr[h] = __shfl_sync(0xffffffffu, dj[h], row);
+      qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row);
+    }
+    int u = 0;
+    if (lane < cnt) {
+      u = a.g.in_src[ebr + (t - offr)];
+#pragma unroll
+      for (int h = 0; h < H; ++h)
+        buf[lane][h] = __fdiv_rn(
+            exp_p(__fsub_rn(lrelu(sddmm_add1(a.qS[(int64_t)u * H + h], sS, (int8_t)qdr[h], sD), a.slope), mr[h])),
+            dr[h]);
+      rb[lane] = row;
+    }
+    __syncwarp();
+    for (int i0 = 0; i0 < cnt; i0 += UNR) {
+      Row<VPL> rr[UNR];
+#pragma unroll
+      for (int j = 0; j < UNR; ++j) {
+        const int w = __shfl_sync(0xffffffffu, u, (i0 + j) & 31);
+        if (i0 + j < cnt) rr[j] = load_row<VPL>(xbase + (int64_t)w * a.ldHp);
+      }
+#pragma unroll
+      for (int j = 0; j < UNR; ++j) {
+        if (i0 + j < cnt) {
+          const int ri = rb[i0 + j];
+          if (ri != cur) {
+            if (cur >= 0) flush(cur);
+            cur = ri;
+          }
+          const float al = buf[i0 + j][myh];
+#pragma unroll
+          for (int q = 0; q < (VPL + 3) / 4; ++q) {
+            const uint32_t wx = rr[j].w[q] ^ 0x80808080u;
+#pragma unroll
+            for (int k = 0; k < 4 && q * 4 + k < VPL; ++k) part[q * 4 + k] = __fmaf_rn(al, bx2f(wx, k), part[q * 4 + k]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (cur >= 0) flush(cur);
+}
+
 // FA: α = exp_p(el - m)/den and the aggregation Σ fmaf(α, q_H′[u]) per segment;
 // light rows finish H_out, heavy segments leave a partial in hagg.
 template <int H, int VPL>
-__global__ void __launch_bounds__(256) k_fwd_agg(const GatFwdArgs a) {
+__global__ void __launch_bounds__(256, 2) k_fwd_agg(const GatFwdArgs a) {
   constexpr int LPH = 32 / H;
   constexpr int HD = 32 * VPL;
   __shared__ float sh[WPB][32][H];
@@ -263,10 +412,15 @@ __global__ void __launch_bounds__(256) k_fwd_agg(const GatFwdArgs a) {
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
-  const int64_t hc = load_count(a.plan.counts), nitems = a.g.n_local + hc;
+  const int64_t hc = load_count(a.plan.counts), nitems = hc + (a.g.n_local + TILE - 1) / TILE;
   const int8_t* xbase = a.qHp + lane * VPL;
   float amax_loc = 0.0f;
+  __shared__ int sh_rb[WPB][32];
   FOR_ITEMS(item, a.work + 2, nitems) {
+    if (item >= hc) {
+      fwd_agg_tile<H, VPL>(a, (item - hc) * TILE, buf, sh_rb[w], scS.s, scD.s, scH.s, amax_loc);
+      continue;
+    }
     Seg s;
     if (!decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s)) continue;
     const int64_t vg = a.g.row_begin + s.vl;
@@ -447,9 +601,152 @@ __device__ __forceinline__ float bwd_dst_pass2(const GatBwdArgs& a, const Seg& s
   return part;
 }
 
+
+// BD1 on a tile of light destination rows: pass 1 streams ∂α (IDP4A dot with the row's q_G slice,
+// prefetched one row ahead) and P; pass 2 re-streams the tile for ∂E_pre and ∂D (lane j = row j).
+template <int H, int VPL>
+__device__ __forceinline__ void bwd_dst1_tile(const GatBwdArgs& a, int64_t r0, float (*ba)[H], float (*bd)[H],
+                                              int* rb, float (*pt)[H], float sS, float sD, float sGH) {
+  constexpr int LPH = 32 / H;
+  const int lane = threadIdx.x & 31, myh = lane / LPH;
+  const bool leader = (lane % LPH) == 0;
+  int T;
+  const TileLane L = tile_setup(a.g.in_ptr, a.pin.hbase, r0, a.g.n_local, T);
+  const int64_t vg = a.g.row_begin + L.r;
+  float mj[H], dj[H];
+  int qdj[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    mj[h] = L.deg > 0 ? a.m[vg * H + h] : 0.0f;
+    dj[h] = L.deg > 0 ? a.den[vg * H + h] : 0.0f;
+    qdj[h] = L.deg > 0 ? (int)a.qD[vg * H + h] : 0;
+  }
+  if (L.light && L.deg == 0) {
+#pragma unroll
+    for (int h = 0; h < H; ++h) { a.P[vg * H + h] = 0.0f; a.dD[vg * H + h] = 0.0f; }
+  }
+  const unsigned act = __ballot_sync(0xffffffffu, L.deg > 0);
+  const int8_t* gbase = a.qG + lane * VPL;
+  const int8_t* hbase = a.qHp + lane * VPL;
+  const int64_t vg0 = a.g.row_begin + r0;
+  int nxt = act ? __ffs(act) - 1 : -1;
+  Row<VPL> gw_nxt{}, gw{};
+  if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
+  float P = 0.0f;
+  int cur = -1;
+  // ---- pass 1
+  for (int base = 0; base < T; base += 32) {
+    const int cnt = T - base < 32 ? T - base : 32;
+    const int t = base + lane;
+    const int row = tile_row(t, L.end);
+    const int64_t ebr = __shfl_sync(0xffffffffu, L.eb, row);
+    const int offr = __shfl_sync(0xffffffffu, L.off, row);
+    float mr[H], dr[H];
+    int qdr[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      mr[h] = __shfl_sync(0xffffffffu, mj[h], row);
+      dr[h] = __shfl_sync(0xffffffffu, dj[h], row);
+      qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row);
+    }
+    int u = 0;
+    const int64_t e = ebr + (t - offr);
+    if (lane < cnt) {
+      u = a.g.in_src[e];
+#pragma unroll
+      for (int h = 0; h < H; ++h)
+        ba[lane][h] = __fdiv_rn(
+            exp_p(__fsub_rn(lrelu(sddmm_add1(a.qS[(int64_t)u * H + h], sS, (int8_t)qdr[h], sD), a.slope), mr[h])),
+            dr[h]);
+      rb[lane] = row;
+    }
+    __syncwarp();
+    for (int i0 = 0; i0 < cnt; i0 += UNR) {
+      Row<VPL> rr[UNR];
+#pragma unroll
+      for (int j = 0; j < UNR; ++j) {
+        const int w = __shfl_sync(0xffffffffu, u, (i0 + j) & 31);
+        if (i0 + j < cnt) rr[j] = load_row<VPL>(hbase + (int64_t)w * a.ldHp);
+      }
+#pragma unroll
+      for (int j = 0; j < UNR; ++j) {
+        if (i0 + j < cnt) {
+          const int ri = rb[i0 + j];
+          if (ri != cur) {
+            if (cur >= 0 && leader) pt[cur][myh] = P;
+            P = 0.0f;
+            cur = ri;
+            gw = gw_nxt;
+            nxt = tile_next(act, cur);
+            if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
+          }
+          int dot = row_dot<VPL>(gw, rr[j]);
+#pragma unroll
+          for (int o = 1; o < LPH; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+          if (leader) {
+            const float dal = __fmul_rn(__int2float_rn(dot), sGH);
+            P = __fmaf_rn(dal, ba[i0 + j][myh], P);
+            bd[i0 + j][myh] = dal;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane < cnt) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) a.dalpha[e * H + h] = bd[lane][h];
+    }
+    __syncwarp();
+  }
+  if (cur >= 0 && leader) pt[cur][myh] = P;
+  __syncwarp();
+  // ---- pass 2
+  float dDp[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) dDp[h] = 0.0f;
+  for (int base = 0; base < T; base += 32) {
+    const int cnt = T - base < 32 ? T - base : 32;
+    const int t = base + lane;
+    const int row = tile_row(t, L.end);
+    const int64_t ebr = __shfl_sync(0xffffffffu, L.eb, row);
+    const int offr = __shfl_sync(0xffffffffu, L.off, row);
+    float mr[H], dr[H];
+    int qdr[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      mr[h] = __shfl_sync(0xffffffffu, mj[h], row);
+      dr[h] = __shfl_sync(0xffffffffu, dj[h], row);
+      qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row);
+    }
+    if (lane < cnt) {
+      const int64_t e = ebr + (t - offr);
+      const int64_t u = a.g.in_src[e];
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const float ep = sddmm_add1(a.qS[u * H + h], sS, (int8_t)qdr[h], sD);
+        const float al = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), mr[h])), dr[h]);
+        const float dE = __fmul_rn(al, __fsub_rn(a.dalpha[e * H + h], pt[row][h]));
+        ba[lane][h] = ep > 0.0f ? dE : __fmul_rn(dE, a.slope);
+      }
+    }
+    __syncwarp();
+    const int lo = (L.off > base ? L.off : base) - base;
+    const int hi = (L.end < base + cnt ? L.end : base + cnt) - base;
+    for (int i = lo; i < hi; ++i)
+#pragma unroll
+      for (int h = 0; h < H; ++h) dDp[h] = __fadd_rn(dDp[h], ba[i][h]);
+    __syncwarp();
+  }
+  if (L.deg > 0) {
+#pragma unroll
+    for (int h = 0; h < H; ++h) { a.P[vg * H + h] = pt[lane][h]; a.dD[vg * H + h] = dDp[h]; }
+  }
+  __syncwarp();
+}
+
 // BD1: light rows -> ∂α, P, ∂D final; heavy segments -> ∂α, P partial (hP)
 template <int H, int VPL>
-__global__ void __launch_bounds__(256) k_bwd_dst1(const GatBwdArgs a) {
+__global__ void __launch_bounds__(256, 2) k_bwd_dst1(const GatBwdArgs a) {
   constexpr int LPH = 32 / H;
   __shared__ float sh_a[WPB][32][H];
   __shared__ float sh_d[WPB][32][H];
@@ -459,8 +756,14 @@ __global__ void __launch_bounds__(256) k_bwd_dst1(const GatBwdArgs a) {
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
   const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
   const float sGH = __fmul_rn(scG.s, scH.s);
-  const int64_t hc = load_count(a.pin.counts), nitems = a.g.n_local + hc;
+  const int64_t hc = load_count(a.pin.counts), nitems = hc + (a.g.n_local + TILE - 1) / TILE;
+  __shared__ int sh_rb[WPB][32];
+  __shared__ float sh_pt[WPB][32][H];
   FOR_ITEMS(item, a.work + 0, nitems) {
+    if (item >= hc) {
+      bwd_dst1_tile<H, VPL>(a, (item - hc) * TILE, sh_a[w], sh_d[w], sh_rb[w], sh_pt[w], scS.s, scD.s, sGH);
+      continue;
+    }
     Seg s;
     if (!decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s)) continue;
     const int64_t vg = a.g.row_begin + s.vl;
@@ -591,11 +894,10 @@ __device__ __forceinline__ float bwd_src_seg(const GatBwdArgs& a, const Seg& s, 
   return dS;
 }
 
-// ②′ finalize of source row u: ∂H′ = (agg·s_G + ∂S·a_src) + ∂D·a_dst ; ∂a partials
+// ②′ finalize of source row u: ∂H′ = (agg·s_G + ∂S·a_src) + ∂D·a_dst ; ∂S stored for the ∂a pass
 template <int VPL>
 __device__ __forceinline__ void bwd_src_finalize(const GatBwdArgs& a, int64_t ul, int64_t ug, int myh, float dS,
-                                                 const float (&sum)[VPL], const Row<VPL>& hw, float sG, float sHp,
-                                                 float (&das)[VPL], float (&dad)[VPL], float& amax_loc, int H) {
+                                                 const float (&sum)[VPL], float sG, float& amax_loc, int H) {
   constexpr int HD = 32 * VPL;
   const int lane = threadIdx.x & 31;
   const float dD = a.dD[ug * H + myh];
@@ -609,60 +911,146 @@ __device__ __forceinline__ void bwd_src_finalize(const GatBwdArgs& a, int64_t ul
     const float o = __fadd_rn(t2, __fmul_rn(dD, __ldg(adst + k)));
     amax_loc = fmaxf(amax_loc, fabsf(o));
     dst[k] = o;
-    const float hp = __fmul_rn(row_f<VPL>(hw, k), sHp);
-    das[k] = __fmaf_rn(dS, hp, das[k]);
-    dad[k] = __fmaf_rn(dD, hp, dad[k]);
   }
+  if ((lane % (32 / H)) == 0) a.dS[ug * H + myh] = dS;
 }
 
-template <int VPL>
-__device__ __forceinline__ void bwd_src_flush(const GatBwdArgs& a, float (*sh_da)[32 * VPL], unsigned* sh_amax,
-                                              const float (&das)[VPL], const float (&dad)[VPL], float amax_loc) {
-  constexpr int HD = 32 * VPL;
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    atomicAdd(&sh_da[0][lane * VPL + k], das[k]);
-    atomicAdd(&sh_da[1][lane * VPL + k], dad[k]);
-  }
+__device__ __forceinline__ void amax_flush(unsigned* slot, float amax_loc) {
   amax_loc = warp_max(amax_loc);
-  if (lane == 0) atomicMax(sh_amax, __float_as_uint(amax_loc));
-  __syncthreads();
-  for (int j = threadIdx.x; j < HD; j += blockDim.x) {
-    atomicAdd(a.da_src + j, sh_da[0][j]);
-    atomicAdd(a.da_dst + j, sh_da[1][j]);
-  }
-  if (threadIdx.x == 0 && a.amax_dHp) atomicMax(a.amax_dHp, *sh_amax);
+  if ((threadIdx.x & 31) == 0 && slot) atomicMax(slot, __float_as_uint(amax_loc));
 }
 
-// BS: light out-rows -> ∂H′ final; heavy out-segments -> ∂S, aggregation partials
+// BS on a tile of light source rows: per out-edge (u→v) recompute α, e_pre, ∂α, ∂E_pre; stream
+// the q_G[v] gathers across rows (own q_H′[u] slice prefetched one row ahead); finalize at row change.
 template <int H, int VPL>
-__global__ void __launch_bounds__(256) k_bwd_src(const GatBwdArgs a) {
+__device__ __forceinline__ void bwd_src_tile(const GatBwdArgs& a, int64_t r0, float (*ba)[H], float (*be)[H],
+                                             float (*bp)[H], int* rb, float sS, float sD, float sGH, float sG,
+                                             float& amax_loc) {
+  constexpr int LPH = 32 / H;
+  const int lane = threadIdx.x & 31, myh = lane / LPH;
+  const bool leader = (lane % LPH) == 0;
+  int T;
+  const TileLane L = tile_setup(a.g.out_ptr, a.pout.hbase, r0, a.g.n_local, T);
+  const int64_t ug0 = a.g.row_begin + r0;
+  int qsj[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) qsj[h] = L.deg > 0 ? (int)a.qS[(ug0 + lane) * H + h] : 0;
+  const int8_t* gbase = a.qG + lane * VPL;
+  const int8_t* hbase = a.qHp + lane * VPL;
+  float zero[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) zero[k] = 0.0f;
+  unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
+  while (zm) {   // light rows without out-edges: ∂H′ = (0 + 0·a_src) + ∂D·a_dst
+    const int j = __ffs(zm) - 1;
+    zm &= zm - 1;
+    bwd_src_finalize<VPL>(a, r0 + j, ug0 + j, myh, 0.0f, zero, sG, amax_loc, H);
+  }
+  const unsigned act = __ballot_sync(0xffffffffu, L.deg > 0);
+  int nxt = act ? __ffs(act) - 1 : -1;
+  Row<VPL> hw_nxt{}, hw{};
+  if (nxt >= 0) hw_nxt = load_row<VPL>(hbase + (ug0 + nxt) * a.ldHp);
+  float part[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) part[k] = 0.0f;
+  float dS = 0.0f;
+  int cur = -1;
+  auto flush = [&](int j) {
+    const float dSb = __shfl_sync(0xffffffffu, dS, myh * LPH);
+    bwd_src_finalize<VPL>(a, r0 + j, ug0 + j, myh, dSb, part, sG, amax_loc, H);
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) part[k] = 0.0f;
+    dS = 0.0f;
+  };
+  for (int base = 0; base < T; base += 32) {
+    const int cnt = T - base < 32 ? T - base : 32;
+    const int t = base + lane;
+    const int row = tile_row(t, L.end);
+    const int64_t ebr = __shfl_sync(0xffffffffu, L.eb, row);
+    const int offr = __shfl_sync(0xffffffffu, L.off, row);
+    int qsr[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) qsr[h] = __shfl_sync(0xffffffffu, qsj[h], row);
+    int v = 0;
+    if (lane < cnt) {
+      v = a.g.out_dst[ebr + (t - offr)];
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const int64_t k = (int64_t)v * H + h;
+        const float ep = sddmm_add1((int8_t)qsr[h], sS, a.qD[k], sD);
+        ba[lane][h] = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), a.m[k])), a.den[k]);
+        be[lane][h] = ep;
+        bp[lane][h] = a.P[k];
+      }
+      rb[lane] = row;
+    }
+    __syncwarp();
+    for (int i0 = 0; i0 < cnt; i0 += UNR) {
+      Row<VPL> rr[UNR];
+#pragma unroll
+      for (int j = 0; j < UNR; ++j) {
+        const int vv = __shfl_sync(0xffffffffu, v, (i0 + j) & 31);
+        if (i0 + j < cnt) rr[j] = load_row<VPL>(gbase + (int64_t)vv * a.ldG);
+      }
+#pragma unroll
+      for (int j = 0; j < UNR; ++j) {
+        if (i0 + j < cnt) {
+          const int ri = rb[i0 + j];
+          if (ri != cur) {
+            if (cur >= 0) flush(cur);
+            cur = ri;
+            hw = hw_nxt;
+            nxt = tile_next(act, cur);
+            if (nxt >= 0) hw_nxt = load_row<VPL>(hbase + (ug0 + nxt) * a.ldHp);
+          }
+          int dot = row_dot<VPL>(rr[j], hw);
+#pragma unroll
+          for (int o = 1; o < LPH; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+          const float al = ba[i0 + j][myh];
+          if (leader) {
+            const float dal = __fmul_rn(__int2float_rn(dot), sGH);
+            const float dE = __fmul_rn(al, __fsub_rn(dal, bp[i0 + j][myh]));
+            dS = __fadd_rn(dS, be[i0 + j][myh] > 0.0f ? dE : __fmul_rn(dE, a.slope));
+          }
+#pragma unroll
+          for (int q = 0; q < (VPL + 3) / 4; ++q) {
+            const uint32_t wx = rr[j].w[q] ^ 0x80808080u;
+#pragma unroll
+            for (int k = 0; k < 4 && q * 4 + k < VPL; ++k) part[q * 4 + k] = __fmaf_rn(al, bx2f(wx, k), part[q * 4 + k]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (cur >= 0) flush(cur);
+}
+
+// BS: light out-rows (tiles) -> ∂H′ final; heavy out-segments -> ∂S, aggregation partials
+template <int H, int VPL>
+__global__ void __launch_bounds__(256, 2) k_bwd_src(const GatBwdArgs a) {
   constexpr int LPH = 32 / H;
   constexpr int HD = 32 * VPL;
   __shared__ float sh_a[WPB][32][H];
   __shared__ float sh_e[WPB][32][H];
   __shared__ float sh_p[WPB][32][H];
-  __shared__ float sh_da[2][HD];
-  __shared__ unsigned sh_amax;
+  __shared__ int sh_rb[WPB][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int myh = lane / LPH;
-  for (int j = threadIdx.x; j < 2 * HD; j += blockDim.x) (&sh_da[0][0])[j] = 0.0f;
-  if (threadIdx.x == 0) sh_amax = 0u;
-  __syncthreads();
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
   const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
   const float sGH = __fmul_rn(scG.s, scH.s);
-  float das[VPL], dad[VPL];
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) { das[k] = 0.0f; dad[k] = 0.0f; }
   float amax_loc = 0.0f;
-  const int64_t hc = load_count(a.pout.counts), nitems = a.g.n_local + hc;
+  const int64_t hc = load_count(a.pout.counts), nitems = hc + (a.g.n_local + TILE - 1) / TILE;
   FOR_ITEMS(item, a.work + 2, nitems) {
+    if (item >= hc) {
+      bwd_src_tile<H, VPL>(a, (item - hc) * TILE, sh_a[w], sh_e[w], sh_p[w], sh_rb[w], scS.s, scD.s, sGH, scG.s,
+                           amax_loc);
+      continue;
+    }
     Seg s;
-    if (!decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s)) continue;
+    decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
     const int64_t ug = a.g.row_begin + s.vl;
     int8_t qs[H];
 #pragma unroll
@@ -672,17 +1060,12 @@ __global__ void __launch_bounds__(256) k_bwd_src(const GatBwdArgs a) {
 #pragma unroll
     for (int k = 0; k < VPL; ++k) part[k] = 0.0f;
     const float dSl = bwd_src_seg<H, VPL>(a, s, qs, hw, scS.s, scD.s, sGH, sh_a[w], sh_e[w], sh_p[w], part);
-    if (s.slot >= 0) {
-      if ((lane % LPH) == 0) a.hdS[(int64_t)s.slot * H + lane / LPH] = dSl;
-      float* dst = a.hagg + (int64_t)s.slot * HD + lane * VPL;
+    if ((lane % LPH) == 0) a.hdS[(int64_t)s.slot * H + lane / LPH] = dSl;
+    float* dst = a.hagg + (int64_t)s.slot * HD + lane * VPL;
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) dst[k] = part[k];
-      continue;
-    }
-    const float dS = __shfl_sync(0xffffffffu, dSl, myh * LPH);
-    bwd_src_finalize<VPL>(a, s.vl, ug, myh, dS, part, hw, scG.s, scH.s, das, dad, amax_loc, H);
+    for (int k = 0; k < VPL; ++k) dst[k] = part[k];
   }
-  bwd_src_flush<VPL>(a, sh_da, &sh_amax, das, dad, amax_loc);
+  amax_flush(a.amax_dHp, amax_loc);
 }
 
 // BC: heavy out-rows -> fold ∂S and aggregation partials in chunk order, finalize ∂H′
@@ -690,18 +1073,9 @@ template <int H, int VPL>
 __global__ void __launch_bounds__(256) k_bwd_src_combine(const GatBwdArgs a) {
   constexpr int LPH = 32 / H;
   constexpr int HD = 32 * VPL;
-  __shared__ float sh_da[2][HD];
-  __shared__ unsigned sh_amax;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const int myh = lane / LPH;
-  for (int j = threadIdx.x; j < 2 * HD; j += blockDim.x) (&sh_da[0][0])[j] = 0.0f;
-  if (threadIdx.x == 0) sh_amax = 0u;
-  __syncthreads();
-  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
   const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
-  float das[VPL], dad[VPL];
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) { das[k] = 0.0f; dad[k] = 0.0f; }
   float amax_loc = 0.0f;
   const int64_t hrows = load_count(a.pout.counts + 1);
   FOR_ITEMS(r, a.work + 3, hrows) {
@@ -721,10 +1095,49 @@ __global__ void __launch_bounds__(256) k_bwd_src_combine(const GatBwdArgs a) {
 #pragma unroll
       for (int k = 0; k < VPL; ++k) tot[k] = __fadd_rn(tot[k], p[k]);
     }
-    const Row<VPL> hw = load_row<VPL>(a.qHp + ug * a.ldHp + lane * VPL);
-    bwd_src_finalize<VPL>(a, ul, ug, myh, dS, tot, hw, scG.s, scH.s, das, dad, amax_loc, H);
+    bwd_src_finalize<VPL>(a, ul, ug, myh, dS, tot, scG.s, amax_loc, H);
   }
-  bwd_src_flush<VPL>(a, sh_da, &sh_amax, das, dad, amax_loc);
+  amax_flush(a.amax_dHp, amax_loc);
+}
+
+// ②′ for the attention vectors (reading R23): ∂a_src[j] = Σ_u ∂S[u,h(j)]·deq(q_H′)[u,j],
+// ∂a_dst likewise with ∂D.  A streaming reduction over the owned rows (q_H′ read once, coalesced);
+// summation order is free (fp32 atomics), checked against the oracle within the derived bound.
+template <int H, int VPL>
+__global__ void __launch_bounds__(256) k_bwd_attn_grad(const GatBwdArgs a) {
+  constexpr int LPH = 32 / H;
+  constexpr int HD = 32 * VPL;
+  __shared__ float sh_da[2][HD];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int myh = lane / LPH;
+  for (int j = threadIdx.x; j < 2 * HD; j += blockDim.x) (&sh_da[0][0])[j] = 0.0f;
+  __syncthreads();
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  float das[VPL], dad[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) { das[k] = 0.0f; dad[k] = 0.0f; }
+  for (int64_t ul = (int64_t)blockIdx.x * WPB + w; ul < a.g.n_local; ul += (int64_t)gridDim.x * WPB) {
+    const int64_t ug = a.g.row_begin + ul;
+    const float dS = a.dS[ug * H + myh];
+    const float dD = a.dD[ug * H + myh];
+    const Row<VPL> hw = load_row<VPL>(a.qHp + ug * a.ldHp + lane * VPL);
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const float hp = __fmul_rn(row_f<VPL>(hw, k), scH.s);
+      das[k] = __fmaf_rn(dS, hp, das[k]);
+      dad[k] = __fmaf_rn(dD, hp, dad[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    atomicAdd(&sh_da[0][lane * VPL + k], das[k]);
+    atomicAdd(&sh_da[1][lane * VPL + k], dad[k]);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < HD; j += blockDim.x) {
+    atomicAdd(a.da_src + j, sh_da[0][j]);
+    atomicAdd(a.da_dst + j, sh_da[1][j]);
+  }
 }
 
 // ------------------------------------------------------------------ dispatch
@@ -787,6 +1200,8 @@ cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st) {
     { ProfScope p("gat_bwd_src", st); k_bwd_src<H_, V_><<<item_grid(items), 256, 0, st>>>(a); }    \
     { ProfScope p("gat_bwd_src_combine", st);                                                      \
       k_bwd_src_combine<H_, V_><<<item_grid(a.g.n_local), 256, 0, st>>>(a); }                     \
+    { ProfScope p("gat_bwd_attn_grad", st);                                                        \
+      k_bwd_attn_grad<H_, V_><<<num_sms() * 2, 256, 0, st>>>(a); }                                 \
   }
   TANGO_HV_CASES(X)
 #undef X

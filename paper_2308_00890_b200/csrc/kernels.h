@@ -107,6 +107,7 @@ struct GatBwdArgs {
   const float* a_src; const float* a_dst;
   float* dHp; unsigned* amax_dHp;            // [n_local][HD]
   float* da_src; float* da_dst;              // [HD], accumulated with atomics (pre-zeroed)
+  float* dS;                                 // [N][H] ∂S of the owned rows (for the ∂a pass)
   PlanDev pin, pout;                         // in-CSR and out-CSR plans
   float* hP; float* hdD;                     // [pin.cap][H]
   float* hdS;                                // [pout.cap][H]
