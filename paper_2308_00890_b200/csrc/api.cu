@@ -332,7 +332,7 @@ struct GatLayout {
       off_qG, off_dal, off_dHp, off_qdHp, off_dW64, total;
   // segment plans (gat.cu) and heavy-segment scratch
   size_t off_pin_hbase, off_pin_hseg, off_pin_hrow, off_pin_cnt, off_pout_hbase, off_pout_hseg, off_pout_hrow,
-      off_pout_cnt, off_h1, off_h2, off_hdS, off_hagg, off_work, off_dS;
+      off_pout_cnt, off_h1, off_h2, off_hdS, off_hagg, off_work, off_dS, off_alpha;
 };
 GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   GatLayout L{};
@@ -381,6 +381,7 @@ GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   L.off_hagg = take((size_t)(L.cap_in > L.cap_out ? L.cap_in : L.cap_out) * L.HD * 4);
   L.off_work = take(64);
   L.off_dS = take((size_t)L.N * L.H * 4);
+  L.off_alpha = take((size_t)L.E * L.H * 4);
   L.total = o;
   return L;
 }
@@ -400,6 +401,7 @@ tango_status check_gat(const tango_graph* G, const tango_gat_params* p) {
   const int vpl = HD / 32;
   if (!(vpl == 2 || vpl == 4 || vpl == 8 || vpl == 16)) return TANGO_ERR_UNSUPPORTED;
   if (!(p->heads == 1 || p->heads == 2 || p->heads == 4 || p->heads == 8)) return TANGO_ERR_UNSUPPORTED;
+  if (!(p->head_dim == 8 || p->head_dim == 16 || p->head_dim % 32 == 0)) return TANGO_ERR_UNSUPPORTED;
   if (p->in_feats > 133144) return TANGO_ERR_OVERFLOW;
   if (256 % p->head_dim && HD > 256) return TANGO_ERR_UNSUPPORTED;
   return TANGO_OK;
@@ -510,6 +512,7 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   fa.Hout = H_out; fa.m = m; fa.den = den; fa.amax_out = reinterpret_cast<unsigned*>(amax_out);
   fa.plan = pin; fa.hmax = (float*)(c + L.off_h1); fa.hden = (float*)(c + L.off_h2); fa.hagg = (float*)(c + L.off_hagg);
   fa.work = (int32_t*)(c + L.off_work);
+  fa.alpha = (float*)(c + L.off_alpha);
   TRY_CUDA(cudaMemsetAsync(fa.work, 0, 64, st));
   TRY(launch_status(launch_gat_fwd(fa, st)));
   TRY(comm_max(comm, amax_out, amax_out ? 1 : 0, st));
@@ -582,6 +585,7 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   ba.hagg = (float*)(c + L.off_hagg);
   ba.work = (int32_t*)(c + L.off_work);
   ba.dS = (float*)(c + L.off_dS);
+  ba.alpha = (const float*)(c + L.off_alpha);
   TRY_CUDA(cudaMemsetAsync(ba.work, 0, 64, st));
   TRY(launch_status(launch_gat_bwd_dst(ba, st)));
   TRY(comm_gather_rows(comm, P, (size_t)L.H * 4, st));

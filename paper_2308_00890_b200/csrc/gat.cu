@@ -16,7 +16,9 @@
 //  * Per-edge scalars (α, ∂α, e_pre) are computed lane-parallel over 32-edge batches and staged
 //    in shared memory; α, ∂α and ∂E are recomputed from per-node data (reading R30), so the only
 //    edge-sized arrays are the CSR indices and one fp32 ∂α scratch (backward destination pass).
-//  * Row gathers are software-pipelined 8 edges deep (8 x 16-B loads in flight per lane).
+//  * Light rows are processed in tiles of 32 consecutive rows streamed as one edge sequence, and
+//    the three gather passes are split into head groups (one warp per group of WC = 32*VPL columns)
+//    so a warp gathers one 128-B line per edge with a 16-deep pipeline at low register cost.
 #include "rowops.cuh"
 
 namespace tango {
@@ -114,10 +116,12 @@ __device__ __forceinline__ void seg_max(const int32_t* __restrict__ src, int64_t
 
 // Σ over the segment of exp_p(el - m), sequential in edge order (one chunk: no folding).
 // Returns the sum for head `lane` in lanes < H.
+// Also stores ex with the sign of e_pre (the LeakyReLU branch) into sx[e][h] when sx != nullptr.
 template <int H>
 __device__ __forceinline__ float seg_sum_exp(const int32_t* __restrict__ src, int64_t eb, int64_t ee,
                                              const int8_t* __restrict__ qS, float sS, const int8_t (&qd)[H],
-                                             float sD, float slope, const float (&mx)[H], float (*buf)[H]) {
+                                             float sD, float slope, const float (&mx)[H], float (*buf)[H],
+                                             float* __restrict__ sx) {
   const int lane = threadIdx.x & 31;
   float part = 0.0f;
   for (int64_t base = eb; base < ee; base += 32) {
@@ -125,8 +129,12 @@ __device__ __forceinline__ float seg_sum_exp(const int32_t* __restrict__ src, in
     if (lane < cnt) {
       const int64_t u = src[base + lane];
 #pragma unroll
-      for (int h = 0; h < H; ++h)
-        buf[lane][h] = exp_p(__fsub_rn(lrelu(sddmm_add1(qS[u * H + h], sS, qd[h], sD), slope), mx[h]));
+      for (int h = 0; h < H; ++h) {
+        const float ep = sddmm_add1(qS[u * H + h], sS, qd[h], sD);
+        const float ex = exp_p(__fsub_rn(lrelu(ep, slope), mx[h]));
+        buf[lane][h] = ex;
+        if (sx) sx[(base + lane) * H + h] = ep > 0.0f ? ex : -ex;
+      }
     }
     __syncwarp();
     if (lane < H)
@@ -269,11 +277,23 @@ __global__ void __launch_bounds__(256) k_fwd_stats(const GatFwdArgs a) {
     if (s.ee == s.eb)
 #pragma unroll
       for (int h = 0; h < H; ++h) mx[h] = 0.0f;
-    const float den = seg_sum_exp<H>(a.g.in_src, s.eb, s.ee, a.qS, scS.s, qd, scD.s, a.slope, mx, sh[w]);
+    const float den = seg_sum_exp<H>(a.g.in_src, s.eb, s.ee, a.qS, scS.s, qd, scD.s, a.slope, mx, sh[w], a.alpha);
     if (lane < H) {
       a.m[vg * H + lane] = head_pick<H>(mx, lane);
       a.den[vg * H + lane] = den;
     }
+    // α = ex / den (IEEE division of |ex|; the sign bit keeps the LeakyReLU branch of e_pre)
+    float dh[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) dh[h] = __shfl_sync(0xffffffffu, den, h);
+    __syncwarp();
+    for (int64_t e = s.eb + lane; e < s.ee; e += 32)
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const float x = a.alpha[e * H + h];
+        const float al = __fdiv_rn(fabsf(x), dh[h]);
+        a.alpha[e * H + h] = x < 0.0f || (x == 0.0f && signbit(x)) ? -al : al;
+      }
   }
 }
 
@@ -294,183 +314,778 @@ __global__ void __launch_bounds__(256) k_fwd_stats2(const GatFwdArgs a) {
     for (int h = 0; h < H; ++h) qd[h] = a.qD[vg * H + h];
     float mx[H], dummy[H];
     heavy_row_stats<H>(a.hmax, nullptr, s.base, s.nseg, mx, dummy);
-    const float part = seg_sum_exp<H>(a.g.in_src, s.eb, s.ee, a.qS, scS.s, qd, scD.s, a.slope, mx, sh[w]);
+    const float part = seg_sum_exp<H>(a.g.in_src, s.eb, s.ee, a.qS, scS.s, qd, scD.s, a.slope, mx, sh[w], a.alpha);
     if (lane < H) a.hden[si * H + lane] = part;
   }
 }
 
-
-// FA on a tile of light rows: α per edge (lane-parallel), aggregation streamed across rows.
-template <int H, int VPL>
-__device__ __forceinline__ void fwd_agg_tile(const GatFwdArgs& a, int64_t r0, float (*buf)[H], int* rb,
-                                             float sS, float sD, float sH, float& amax_loc) {
-  constexpr int LPH = 32 / H;
-  constexpr int HD = 32 * VPL;
-  const int lane = threadIdx.x & 31, myh = lane / LPH;
-  int T;
-  const TileLane L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, a.g.n_local, T);
-  const int64_t vg = a.g.row_begin + L.r;
-  float mj[H], dj[H];
-  int qdj[H];
+// FS3: heavy segments -> α = ex / den with den the chunk-ordered fold of the row's segment sums
+template <int H>
+__global__ void __launch_bounds__(256) k_fwd_alpha3(const GatFwdArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t hcnt = load_count(a.plan.counts);
+  FOR_ITEMS(si, a.work + 4, hcnt) {
+    Seg s;
+    decode_item(si, hcnt, a.g.in_ptr, a.plan, a.g.chunk, s);
+    float mx[H], den[H];
+    heavy_row_stats<H>(a.hmax, a.hden, s.base, s.nseg, mx, den);
+    for (int64_t e = s.eb + lane; e < s.ee; e += 32)
 #pragma unroll
-  for (int h = 0; h < H; ++h) {
-    mj[h] = L.deg > 0 ? a.m[vg * H + h] : 0.0f;
-    dj[h] = L.deg > 0 ? a.den[vg * H + h] : 0.0f;
-    qdj[h] = L.deg > 0 ? (int)a.qD[vg * H + h] : 0;
-  }
-  unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
-  while (zm) {   // light rows without in-edges: H_out = 0
-    const int j = __ffs(zm) - 1;
-    zm &= zm - 1;
-    float* dst = a.Hout + (r0 + j) * HD + lane * VPL;
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) dst[k] = 0.0f;
-  }
-  const int8_t* xbase = a.qHp + lane * VPL;
-  float part[VPL];
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) part[k] = 0.0f;
-  int cur = -1;
-  auto flush = [&](int j) {
-    float* dst = a.Hout + (r0 + j) * HD + lane * VPL;
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) {
-      const float o = __fmul_rn(part[k], sH);
-      amax_loc = fmaxf(amax_loc, fabsf(o));
-      dst[k] = o;
-      part[k] = 0.0f;
-    }
-  };
-  for (int base = 0; base < T; base += 32) {
-    const int cnt = T - base < 32 ? T - base : 32;
-    const int t = base + lane;
-    const int row = tile_row(t, L.end);
-    const int64_t ebr = __shfl_sync(0xffffffffu, L.eb, row);
-    const int offr = __shfl_sync(0xffffffffu, L.off, row);
-    float mr[H], dr[H];
-    int qdr[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      mr[h] = __shfl_sync(0xffffffffu, mj[h], row);
-      dr[h] = __shfl_sync(0xffffffffu, dj[h], row);
-      qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row);
-    }
-    int u = 0;
-    if (lane < cnt) {
-      u = a.g.in_src[ebr + (t - offr)];
-#pragma unroll
-      for (int h = 0; h < H; ++h)
-        buf[lane][h] = __fdiv_rn(
-            exp_p(__fsub_rn(lrelu(sddmm_add1(a.qS[(int64_t)u * H + h], sS, (int8_t)qdr[h], sD), a.slope), mr[h])),
-            dr[h]);
-      rb[lane] = row;
-    }
-    __syncwarp();
-    for (int i0 = 0; i0 < cnt; i0 += UNR) {
-      Row<VPL> rr[UNR];
-#pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        const int w = __shfl_sync(0xffffffffu, u, (i0 + j) & 31);
-        if (i0 + j < cnt) rr[j] = load_row<VPL>(xbase + (int64_t)w * a.ldHp);
+      for (int h = 0; h < H; ++h) {
+        const float x = a.alpha[e * H + h];
+        const float al = __fdiv_rn(fabsf(x), den[h]);
+        a.alpha[e * H + h] = x < 0.0f || (x == 0.0f && signbit(x)) ? -al : al;
       }
+  }
+}
+
+
+// ②′ finalize of source row u: ∂H′ = (agg·s_G + ∂S·a_src) + ∂D·a_dst ; ∂S stored for the ∂a pass
+template <int VPL>
+__device__ __forceinline__ void bwd_src_finalize(const GatBwdArgs& a, int64_t ul, int64_t ug, int myh, float dS,
+                                                 const float (&sum)[VPL], float sG, float& amax_loc, int H) {
+  constexpr int HD = 32 * VPL;
+  const int lane = threadIdx.x & 31;
+  const float dD = a.dD[ug * H + myh];
+  float* dst = a.dHp + ul * HD + lane * VPL;
+  const float* asrc = a.a_src + lane * VPL;
+  const float* adst = a.a_dst + lane * VPL;
 #pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        if (i0 + j < cnt) {
+  for (int k = 0; k < VPL; ++k) {
+    const float agg = __fmul_rn(sum[k], sG);
+    const float t2 = __fadd_rn(agg, __fmul_rn(dS, __ldg(asrc + k)));
+    const float o = __fadd_rn(t2, __fmul_rn(dD, __ldg(adst + k)));
+    amax_loc = fmaxf(amax_loc, fabsf(o));
+    dst[k] = o;
+  }
+  if ((lane % (32 / H)) == 0) a.dS[ug * H + myh] = dS;
+}
+
+__device__ __forceinline__ void amax_flush(unsigned* slot, float amax_loc) {
+  amax_loc = warp_max(amax_loc);
+  if ((threadIdx.x & 31) == 0 && slot) atomicMax(slot, __float_as_uint(amax_loc));
+}
+
+// ================================================================== column-group gather kernels
+// A warp owns one head group: WC = 32*VPL consecutive columns holding HPW whole heads (D = WC/HPW),
+// for a tile of light rows or for one heavy segment.  Work item = (tile or segment) x (group), so a
+// warp gathers WC bytes (one 128-B line at D = 128) per edge with VPL accumulators per lane: few
+// registers, many resident warps and a 16-deep gather pipeline.  Heads are independent in every
+// gather pass (α, ∂α, P, ∂E, ∂S, ∂D are per head), so the canonical per-row order is unchanged.
+template <int VPL>
+struct CGCfg {
+  static constexpr int WORDS = (VPL + 3) / 4;
+  static constexpr int UNRC = WORDS == 1 ? 16 : (WORDS == 2 ? 8 : 4);
+};
+
+// fwd: α for the group's heads of one edge batch; lane l holds the edge's source u
+template <int HPW>
+__device__ __forceinline__ void cg_alpha_fwd(const GatFwdArgs& a, int H, int h0, int u, const int (&qdr)[HPW],
+                                             const float (&mr)[HPW], const float (&dr)[HPW], float sS, float sD,
+                                             float (*buf)[HPW]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < HPW; ++k)
+    buf[lane][k] = __fdiv_rn(
+        exp_p(__fsub_rn(lrelu(sddmm_add1(a.qS[(int64_t)u * H + h0 + k], sS, (int8_t)qdr[k], sD), a.slope), mr[k])),
+        dr[k]);
+}
+
+// part += α(edge i) * q_X[w_i][cols of this lane] over a staged batch, 16-deep gather pipeline.
+// If rb != nullptr, rows change inside the batch: `on_row(ri)` is called before the first edge of a row.
+template <int VPL, int HPW, typename F>
+__device__ __forceinline__ void cg_gather_fma(const int8_t* __restrict__ xbase, int64_t ldx, int idx, int cnt,
+                                              float (*buf)[HPW], const int* rb, int& cur, float (&part)[VPL],
+                                              F&& on_row) {
+  constexpr int UNRC = CGCfg<VPL>::UNRC;
+  const int lh = (threadIdx.x & 31) / (32 / HPW);
+  for (int i0 = 0; i0 < cnt; i0 += UNRC) {
+    Row<VPL> rr[UNRC];
+#pragma unroll
+    for (int j = 0; j < UNRC; ++j) {
+      const int wv = __shfl_sync(0xffffffffu, idx, (i0 + j) & 31);
+      if (i0 + j < cnt) rr[j] = load_row<VPL>(xbase + (int64_t)wv * ldx);
+    }
+#pragma unroll
+    for (int j = 0; j < UNRC; ++j) {
+      if (i0 + j < cnt) {
+        if (rb) {
           const int ri = rb[i0 + j];
-          if (ri != cur) {
-            if (cur >= 0) flush(cur);
-            cur = ri;
-          }
-          const float al = buf[i0 + j][myh];
+          if (ri != cur) { on_row(ri); cur = ri; }
+        }
+        const float al = buf[i0 + j][lh];
 #pragma unroll
-          for (int q = 0; q < (VPL + 3) / 4; ++q) {
-            const uint32_t wx = rr[j].w[q] ^ 0x80808080u;
+        for (int q = 0; q < CGCfg<VPL>::WORDS; ++q) {
+          const uint32_t wx = rr[j].w[q] ^ 0x80808080u;
 #pragma unroll
-            for (int k = 0; k < 4 && q * 4 + k < VPL; ++k) part[q * 4 + k] = __fmaf_rn(al, bx2f(wx, k), part[q * 4 + k]);
-          }
+          for (int k = 0; k < 4 && q * 4 + k < VPL; ++k) part[q * 4 + k] = __fmaf_rn(al, bx2f(wx, k), part[q * 4 + k]);
         }
       }
     }
-    __syncwarp();
   }
-  if (cur >= 0) flush(cur);
 }
 
-// FA: α = exp_p(el - m)/den and the aggregation Σ fmaf(α, q_H′[u]) per segment;
-// light rows finish H_out, heavy segments leave a partial in hagg.
-template <int H, int VPL>
-__global__ void __launch_bounds__(256, 2) k_fwd_agg(const GatFwdArgs a) {
-  constexpr int LPH = 32 / H;
-  constexpr int HD = 32 * VPL;
-  __shared__ float sh[WPB][32][H];
-  __shared__ unsigned sh_amax;
+// ---- FA: aggregation ⑤ per (tile | heavy segment, head group)
+template <int VPL, int HPW>
+__global__ void __launch_bounds__(256) k_fwd_agg_cg(const GatFwdArgs a) {
+  constexpr int WC = 32 * VPL;
+  __shared__ float sh_a[WPB][32][HPW];
+  __shared__ int sh_rb[WPB][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int myh = lane / LPH;
-  float (*buf)[H] = sh[w];
-  if (threadIdx.x == 0) sh_amax = 0u;
-  __syncthreads();
+  const int H = a.d.heads, HD = a.d.hd, NG = HD / WC;
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
-  const int64_t hc = load_count(a.plan.counts), nitems = hc + (a.g.n_local + TILE - 1) / TILE;
-  const int8_t* xbase = a.qHp + lane * VPL;
+  const int64_t n = a.g.n_local, hc = load_count(a.plan.counts);
+  const int64_t nitems = (hc + (n + TILE - 1) / TILE) * NG;
   float amax_loc = 0.0f;
-  __shared__ int sh_rb[WPB][32];
   FOR_ITEMS(item, a.work + 2, nitems) {
-    if (item >= hc) {
-      fwd_agg_tile<H, VPL>(a, (item - hc) * TILE, buf, sh_rb[w], scS.s, scD.s, scH.s, amax_loc);
-      continue;
-    }
-    Seg s;
-    if (!decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s)) continue;
-    const int64_t vg = a.g.row_begin + s.vl;
-    int8_t qd[H];
-    float mx[H], den[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) qd[h] = a.qD[vg * H + h];
-    if (s.slot < 0) {
-#pragma unroll
-      for (int h = 0; h < H; ++h) { mx[h] = a.m[vg * H + h]; den[h] = a.den[vg * H + h]; }
-    } else {
-      heavy_row_stats<H>(a.hmax, a.hden, s.base, s.nseg, mx, den);
-    }
+    const int64_t wi = item / NG;
+    const int g = (int)(item - wi * NG), h0 = g * HPW;
+    const int8_t* xbase = a.qHp + g * WC + lane * VPL;
     float part[VPL];
 #pragma unroll
     for (int k = 0; k < VPL; ++k) part[k] = 0.0f;
-    for (int64_t base = s.eb; base < s.ee; base += 32) {
-      const int cnt = (int)(s.ee - base < 32 ? s.ee - base : 32);
-      int u = 0;
-      if (lane < cnt) {
-        u = a.g.in_src[base + lane];
+    if (wi < hc) {   // ----------------------------------------------- heavy segment
+      Seg s;
+      decode_item(wi, hc, a.g.in_ptr, a.plan, a.g.chunk, s);
+      const int64_t vg = a.g.row_begin + s.vl;
+      float mr[HPW], dr[HPW];
+      int qdr[HPW];
 #pragma unroll
-        for (int h = 0; h < H; ++h)
-          buf[lane][h] = __fdiv_rn(
-              exp_p(__fsub_rn(lrelu(sddmm_add1(a.qS[(int64_t)u * H + h], scS.s, qd[h], scD.s), a.slope), mx[h])),
-              den[h]);
+      for (int k = 0; k < HPW; ++k) {
+        float mx = -INFINITY;
+        for (int j = lane; j < s.nseg; j += 32) mx = fmaxf(mx, a.hmax[(int64_t)(s.base + j) * H + h0 + k]);
+        mr[k] = warp_max(mx);
+        float tot = 0.0f;
+        if (lane == 0) {
+          tot = a.hden[(int64_t)s.base * H + h0 + k];
+          for (int j = 1; j < s.nseg; ++j) tot = __fadd_rn(tot, a.hden[(int64_t)(s.base + j) * H + h0 + k]);
+        }
+        dr[k] = __shfl_sync(0xffffffffu, tot, 0);
+        qdr[k] = (int)a.qD[vg * H + h0 + k];
       }
-      __syncwarp();
-      gather_fma_batch<VPL>(xbase, a.ldHp, u, cnt, &buf[0][myh], H, part);
-      __syncwarp();
-    }
-    if (s.slot < 0) {
-      float out[VPL];
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) { out[k] = __fmul_rn(part[k], scH.s); amax_loc = fmaxf(amax_loc, fabsf(out[k])); }
-      float* dst = a.Hout + s.vl * HD + lane * VPL;
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) dst[k] = out[k];
-    } else {
-      float* dst = a.hagg + (int64_t)s.slot * HD + lane * VPL;
+      int cur = 0;
+      for (int64_t base = s.eb; base < s.ee; base += 32) {
+        const int cnt = (int)(s.ee - base < 32 ? s.ee - base : 32);
+        int u = 0;
+        if (lane < cnt) {
+          u = a.g.in_src[base + lane];
+          cg_alpha_fwd<HPW>(a, H, h0, u, qdr, mr, dr, scS.s, scD.s, sh_a[w]);
+        }
+        __syncwarp();
+        cg_gather_fma<VPL, HPW>(xbase, a.ldHp, u, cnt, sh_a[w], nullptr, cur, part, [](int) {});
+        __syncwarp();
+      }
+      float* dst = a.hagg + (int64_t)s.slot * HD + g * WC + lane * VPL;
 #pragma unroll
       for (int k = 0; k < VPL; ++k) dst[k] = part[k];
+      continue;
+    }
+    // ------------------------------------------------------------- tile of light rows
+    const int64_t r0 = (wi - hc) * TILE;
+    int T;
+    const TileLane L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, n, T);
+    const int64_t vg = a.g.row_begin + L.r;
+    float mj[HPW], dj[HPW];
+    int qdj[HPW];
+#pragma unroll
+    for (int k = 0; k < HPW; ++k) {
+      mj[k] = L.deg > 0 ? a.m[vg * H + h0 + k] : 0.0f;
+      dj[k] = L.deg > 0 ? a.den[vg * H + h0 + k] : 0.0f;
+      qdj[k] = L.deg > 0 ? (int)a.qD[vg * H + h0 + k] : 0;
+    }
+    unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
+    while (zm) {   // light rows without in-edges: H_out = 0
+      const int j = __ffs(zm) - 1;
+      zm &= zm - 1;
+      float* dst = a.Hout + (r0 + j) * HD + g * WC + lane * VPL;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) dst[k] = 0.0f;
+    }
+    int cur = -1;
+    auto flush = [&](int j) {
+      float* dst = a.Hout + (r0 + j) * HD + g * WC + lane * VPL;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const float o = __fmul_rn(part[k], scH.s);
+        amax_loc = fmaxf(amax_loc, fabsf(o));
+        dst[k] = o;
+        part[k] = 0.0f;
+      }
+    };
+    for (int base = 0; base < T; base += 32) {
+      const int cnt = T - base < 32 ? T - base : 32;
+      const int t = base + lane;
+      const int row = tile_row(t, L.end);
+      const int64_t ebr = __shfl_sync(0xffffffffu, L.eb, row);
+      const int offr = __shfl_sync(0xffffffffu, L.off, row);
+      float mr[HPW], dr[HPW];
+      int qdr[HPW];
+#pragma unroll
+      for (int k = 0; k < HPW; ++k) {
+        mr[k] = __shfl_sync(0xffffffffu, mj[k], row);
+        dr[k] = __shfl_sync(0xffffffffu, dj[k], row);
+        qdr[k] = __shfl_sync(0xffffffffu, qdj[k], row);
+      }
+      int u = 0;
+      if (lane < cnt) {
+        u = a.g.in_src[ebr + (t - offr)];
+        cg_alpha_fwd<HPW>(a, H, h0, u, qdr, mr, dr, scS.s, scD.s, sh_a[w]);
+        sh_rb[w][lane] = row;
+      }
+      __syncwarp();
+      cg_gather_fma<VPL, HPW>(xbase, a.ldHp, u, cnt, sh_a[w], sh_rb[w], cur, part, [&](int ri) {
+        if (cur >= 0) flush(cur);
+      });
+      __syncwarp();
+    }
+    if (cur >= 0) flush(cur);
+  }
+  amax_flush(a.amax_out, amax_loc);
+}
+
+
+// ---- packed fp32x2 helpers (sm_100a FADD2 / FFMA2: IEEE rn per half, bit-identical to scalar ops)
+__device__ __forceinline__ uint64_t pk2(uint32_t lo, uint32_t hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t pkf(float x) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void unpk(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+// acc2 = fma(al, (float)q[k], acc2) for the 4 codes of one word: PRMT builds 2^23+128+q, FADD2 removes
+// the bias exactly, FFMA2 accumulates (2 instructions per element instead of 3)
+__device__ __forceinline__ void fma4_codes(uint32_t word, uint64_t al2, uint64_t& a01, uint64_t& a23) {
+  const uint32_t wx = word ^ 0x80808080u;
+  const uint64_t bias = 0xCB000080CB000080ull;   // {-8388736.0f, -8388736.0f}
+  uint64_t f01 = pk2(__byte_perm(wx, 0x4B000000u, 0x7440u), __byte_perm(wx, 0x4B000000u, 0x7441u));
+  uint64_t f23 = pk2(__byte_perm(wx, 0x4B000000u, 0x7442u), __byte_perm(wx, 0x4B000000u, 0x7443u));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(f01) : "l"(bias));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(f23) : "l"(bias));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a01) : "l"(al2), "l"(f01));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a23) : "l"(al2), "l"(f23));
+}
+
+// Streamed aggregation of one 32-edge chunk: rows q_X[w_i] gathered through a rolling ring of RING
+// loads in flight; edge i of the chunk uses weight sa[i][myh] and (if rb) belongs to row rb[i].
+template <int H, int VPL, int RING, typename F>
+__device__ __forceinline__ void agg_chunk(const int8_t* __restrict__ xbase, int64_t ldx, int w_l, int cnt,
+                                          const float (*sa)[H], const int* rb, int& cur, uint64_t (&acc)[VPL / 2],
+                                          F&& on_row) {
+  constexpr int WORDS = VPL / 4 > 0 ? VPL / 4 : 1;
+  const int myh = (threadIdx.x & 31) / (32 / H);
+  Row<VPL> ring[RING];
+#pragma unroll
+  for (int j = 0; j < RING; ++j) {
+    const int w = __shfl_sync(0xffffffffu, w_l, j);
+    if (j < cnt) ring[j] = load_row<VPL>(xbase + (int64_t)w * ldx);
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (i < cnt) {
+      const Row<VPL> r = ring[i % RING];
+      if (i + RING < 32) {
+        const int w = __shfl_sync(0xffffffffu, w_l, i + RING);
+        if (i + RING < cnt) ring[i % RING] = load_row<VPL>(xbase + (int64_t)w * ldx);
+      }
+      if (rb) {
+        const int ri = rb[i];
+        if (ri != cur) { on_row(ri); cur = ri; }
+      }
+      const uint64_t al2 = pkf(sa[i][myh]);
+      if constexpr (VPL >= 4) {
+#pragma unroll
+        for (int q = 0; q < WORDS; ++q) fma4_codes(r.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+      } else {   // VPL == 2: two codes in the low half-word
+        const uint32_t wx = r.w[0] ^ 0x80808080u;
+        uint64_t f01 = pk2(__byte_perm(wx, 0x4B000000u, 0x7440u), __byte_perm(wx, 0x4B000000u, 0x7441u));
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(f01) : "l"(0xCB000080CB000080ull));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[0]) : "l"(al2), "l"(f01));
+      }
     }
   }
-  if (a.amax_out) {
-    amax_loc = warp_max(amax_loc);
-    if (lane == 0) atomicMax(&sh_amax, __float_as_uint(amax_loc));
-    __syncthreads();
-    if (threadIdx.x == 0) atomicMax(a.amax_out, sh_amax);
+}
+
+// FA: ⑤ H_out = (Σ fmaf(α, q_H′[u])) * s_H′ over (heavy segment | tile of light rows); α is read from
+// the stored (signed) α of the stats passes, so the chunk attributes are two coalesced loads.
+template <int H, int VPL>
+__global__ void __launch_bounds__(256, 2) k_fwd_agg2(const GatFwdArgs a) {
+  constexpr int HD = 32 * VPL;
+  constexpr int RING = VPL >= 16 ? 4 : 8;
+  __shared__ float sh_a[WPB][32][H];
+  __shared__ int sh_rb[WPB][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const int64_t n = a.g.n_local, hc = load_count(a.plan.counts);
+  const int64_t nitems = hc + (n + TILE - 1) / TILE;
+  const int8_t* xbase = a.qHp + lane * VPL;
+  float amax_loc = 0.0f;
+  uint64_t acc[VPL / 2];
+  auto zero_acc = [&]() {
+#pragma unroll
+    for (int k = 0; k < VPL / 2; ++k) acc[k] = 0ull;
+  };
+  FOR_ITEMS(item, a.work + 2, nitems) {
+    zero_acc();
+    if (item < hc) {   // ------------------------------------------------ heavy segment -> hagg
+      Seg s;
+      decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s);
+      int cur = 0;
+      for (int64_t base = s.eb; base < s.ee; base += 32) {
+        const int cnt = (int)(s.ee - base < 32 ? s.ee - base : 32);
+        int u = 0;
+        if (lane < cnt) {
+          u = a.g.in_src[base + lane];
+#pragma unroll
+          for (int h = 0; h < H; ++h) sh_a[w][lane][h] = fabsf(a.alpha[(base + lane) * H + h]);
+        }
+        __syncwarp();
+        agg_chunk<H, VPL, RING>(xbase, a.ldHp, u, cnt, sh_a[w], nullptr, cur, acc, [](int) {});
+        __syncwarp();
+      }
+      float* dst = a.hagg + (int64_t)s.slot * HD + lane * VPL;
+#pragma unroll
+      for (int k = 0; k < VPL / 2; ++k) unpk(acc[k], dst[2 * k], dst[2 * k + 1]);
+      continue;
+    }
+    // --------------------------------------------------------------- tile of light rows
+    const int64_t r0 = (item - hc) * TILE;
+    int T;
+    const TileLane L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, n, T);
+    unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
+    while (zm) {   // light rows without in-edges: H_out = 0
+      const int j = __ffs(zm) - 1;
+      zm &= zm - 1;
+      float* dst = a.Hout + (r0 + j) * HD + lane * VPL;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) dst[k] = 0.0f;
+    }
+    int cur = -1;
+    auto flush = [&](int j) {
+      float* dst = a.Hout + (r0 + j) * HD + lane * VPL;
+#pragma unroll
+      for (int k = 0; k < VPL / 2; ++k) {
+        float x, y;
+        unpk(acc[k], x, y);
+        x = __fmul_rn(x, scH.s);
+        y = __fmul_rn(y, scH.s);
+        amax_loc = fmaxf(amax_loc, fmaxf(fabsf(x), fabsf(y)));
+        dst[2 * k] = x;
+        dst[2 * k + 1] = y;
+        acc[k] = 0ull;
+      }
+    };
+    for (int base = 0; base < T; base += 32) {
+      const int cnt = T - base < 32 ? T - base : 32;
+      const int t = base + lane;
+      const int row = tile_row(t, L.end);
+      const int64_t e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+      int u = 0;
+      if (lane < cnt) {
+        u = a.g.in_src[e];
+#pragma unroll
+        for (int h = 0; h < H; ++h) sh_a[w][lane][h] = fabsf(a.alpha[e * H + h]);
+        sh_rb[w][lane] = row;
+      }
+      __syncwarp();
+      agg_chunk<H, VPL, RING>(xbase, a.ldHp, u, cnt, sh_a[w], sh_rb[w], cur, acc, [&](int) {
+        if (cur >= 0) flush(cur);
+      });
+      __syncwarp();
+    }
+    if (cur >= 0) flush(cur);
   }
+  amax_flush(a.amax_out, amax_loc);
+}
+
+// ---- BD1: ⑤″ ∂α (IDP4A on codes) + ④′ P (+ ∂E_pre, ∂D for light rows) per (tile | segment, group)
+template <int VPL, int HPW>
+__device__ __forceinline__ int cg_dot(const Row<VPL>& x, const Row<VPL>& y) {
+  int dot = row_dot<VPL>(x, y);
+#pragma unroll
+  for (int o = 1; o < 32 / HPW; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  return dot;
+}
+
+template <int VPL, int HPW>
+__global__ void __launch_bounds__(256) k_bwd_dst1_cg(const GatBwdArgs a) {
+  constexpr int WC = 32 * VPL, LPH = 32 / HPW, UNRC = CGCfg<VPL>::UNRC;
+  __shared__ float sh_a[WPB][32][HPW];
+  __shared__ float sh_d[WPB][32][HPW];
+  __shared__ float sh_pt[WPB][32][HPW];
+  __shared__ int sh_rb[WPB][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lh = lane / LPH;
+  const bool leader = (lane % LPH) == 0;
+  const int H = a.d.heads, HD = a.d.hd, NG = HD / WC;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
+  const float sGH = __fmul_rn(scG.s, scH.s);
+  const int64_t n = a.g.n_local, hc = load_count(a.pin.counts);
+  const int64_t nitems = (hc + (n + TILE - 1) / TILE) * NG;
+  float (*ba)[HPW] = sh_a[w];
+  float (*bd)[HPW] = sh_d[w];
+  FOR_ITEMS(item, a.work + 0, nitems) {
+    const int64_t wi = item / NG;
+    const int g = (int)(item - wi * NG), h0 = g * HPW;
+    const int8_t* hbase = a.qHp + g * WC + lane * VPL;
+    const int8_t* gbase = a.qG + g * WC + lane * VPL;
+    if (wi < hc) {   // ----------------------------------------------- heavy segment: ∂α, P partial
+      Seg s;
+      decode_item(wi, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
+      const int64_t vg = a.g.row_begin + s.vl;
+      float mr[HPW], dr[HPW];
+      int qdr[HPW];
+#pragma unroll
+      for (int k = 0; k < HPW; ++k) {
+        mr[k] = a.m[vg * H + h0 + k]; dr[k] = a.den[vg * H + h0 + k]; qdr[k] = (int)a.qD[vg * H + h0 + k];
+      }
+      const Row<VPL> gw = load_row<VPL>(gbase + vg * a.ldG);
+      float P = 0.0f;
+      for (int64_t base = s.eb; base < s.ee; base += 32) {
+        const int cnt = (int)(s.ee - base < 32 ? s.ee - base : 32);
+        int u = 0;
+        if (lane < cnt) {
+          u = a.g.in_src[base + lane];
+#pragma unroll
+          for (int k = 0; k < HPW; ++k)
+            ba[lane][k] = __fdiv_rn(exp_p(__fsub_rn(lrelu(sddmm_add1(a.qS[(int64_t)u * H + h0 + k], scS.s,
+                                                                     (int8_t)qdr[k], scD.s), a.slope), mr[k])), dr[k]);
+        }
+        __syncwarp();
+        for (int i0 = 0; i0 < cnt; i0 += UNRC) {
+          Row<VPL> rr[UNRC];
+#pragma unroll
+          for (int j = 0; j < UNRC; ++j) {
+            const int wv = __shfl_sync(0xffffffffu, u, (i0 + j) & 31);
+            if (i0 + j < cnt) rr[j] = load_row<VPL>(hbase + (int64_t)wv * a.ldHp);
+          }
+#pragma unroll
+          for (int j = 0; j < UNRC; ++j) {
+            if (i0 + j < cnt) {
+              const int dot = cg_dot<VPL, HPW>(gw, rr[j]);
+              if (leader) {
+                const float dal = __fmul_rn(__int2float_rn(dot), sGH);
+                P = __fmaf_rn(dal, ba[i0 + j][lh], P);
+                bd[i0 + j][lh] = dal;
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane < cnt) {
+#pragma unroll
+          for (int k = 0; k < HPW; ++k) a.dalpha[(base + lane) * H + h0 + k] = bd[lane][k];
+        }
+        __syncwarp();
+      }
+      if (leader) a.hP[(int64_t)s.slot * H + h0 + lh] = P;
+      continue;
+    }
+    // ------------------------------------------------------------- tile of light rows
+    const int64_t r0 = (wi - hc) * TILE;
+    int T;
+    const TileLane L = tile_setup(a.g.in_ptr, a.pin.hbase, r0, n, T);
+    const int64_t vg = a.g.row_begin + L.r;
+    float mj[HPW], dj[HPW];
+    int qdj[HPW];
+#pragma unroll
+    for (int k = 0; k < HPW; ++k) {
+      mj[k] = L.deg > 0 ? a.m[vg * H + h0 + k] : 0.0f;
+      dj[k] = L.deg > 0 ? a.den[vg * H + h0 + k] : 0.0f;
+      qdj[k] = L.deg > 0 ? (int)a.qD[vg * H + h0 + k] : 0;
+    }
+    if (L.light && L.deg == 0) {
+#pragma unroll
+      for (int k = 0; k < HPW; ++k) { a.P[vg * H + h0 + k] = 0.0f; a.dD[vg * H + h0 + k] = 0.0f; }
+    }
+    const unsigned act = __ballot_sync(0xffffffffu, L.deg > 0);
+    const int64_t vg0 = a.g.row_begin + r0;
+    int nxt = act ? __ffs(act) - 1 : -1;
+    Row<VPL> gw_nxt{}, gw{};
+    if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
+    float P = 0.0f;
+    int cur = -1;
+    for (int base = 0; base < T; base += 32) {     // pass 1
+      const int cnt = T - base < 32 ? T - base : 32;
+      const int t = base + lane;
+      const int row = tile_row(t, L.end);
+      const int64_t e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+      float mr[HPW], dr[HPW];
+      int qdr[HPW];
+#pragma unroll
+      for (int k = 0; k < HPW; ++k) {
+        mr[k] = __shfl_sync(0xffffffffu, mj[k], row);
+        dr[k] = __shfl_sync(0xffffffffu, dj[k], row);
+        qdr[k] = __shfl_sync(0xffffffffu, qdj[k], row);
+      }
+      int u = 0;
+      if (lane < cnt) {
+        u = a.g.in_src[e];
+#pragma unroll
+        for (int k = 0; k < HPW; ++k)
+          ba[lane][k] = __fdiv_rn(exp_p(__fsub_rn(lrelu(sddmm_add1(a.qS[(int64_t)u * H + h0 + k], scS.s,
+                                                                   (int8_t)qdr[k], scD.s), a.slope), mr[k])), dr[k]);
+        sh_rb[w][lane] = row;
+      }
+      __syncwarp();
+      for (int i0 = 0; i0 < cnt; i0 += UNRC) {
+        Row<VPL> rr[UNRC];
+#pragma unroll
+        for (int j = 0; j < UNRC; ++j) {
+          const int wv = __shfl_sync(0xffffffffu, u, (i0 + j) & 31);
+          if (i0 + j < cnt) rr[j] = load_row<VPL>(hbase + (int64_t)wv * a.ldHp);
+        }
+#pragma unroll
+        for (int j = 0; j < UNRC; ++j) {
+          if (i0 + j < cnt) {
+            const int ri = sh_rb[w][i0 + j];
+            if (ri != cur) {
+              if (cur >= 0 && leader) sh_pt[w][cur][lh] = P;
+              P = 0.0f;
+              cur = ri;
+              gw = gw_nxt;
+              nxt = tile_next(act, cur);
+              if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
+            }
+            const int dot = cg_dot<VPL, HPW>(gw, rr[j]);
+            if (leader) {
+              const float dal = __fmul_rn(__int2float_rn(dot), sGH);
+              P = __fmaf_rn(dal, ba[i0 + j][lh], P);
+              bd[i0 + j][lh] = dal;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < cnt) {
+#pragma unroll
+        for (int k = 0; k < HPW; ++k) a.dalpha[e * H + h0 + k] = bd[lane][k];
+      }
+      __syncwarp();
+    }
+    if (cur >= 0 && leader) sh_pt[w][cur][lh] = P;
+    __syncwarp();
+    float dDp[HPW];
+#pragma unroll
+    for (int k = 0; k < HPW; ++k) dDp[k] = 0.0f;
+    for (int base = 0; base < T; base += 32) {     // pass 2: ∂E_pre, ∂D
+      const int cnt = T - base < 32 ? T - base : 32;
+      const int t = base + lane;
+      const int row = tile_row(t, L.end);
+      const int64_t e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+      float mr[HPW], dr[HPW];
+      int qdr[HPW];
+#pragma unroll
+      for (int k = 0; k < HPW; ++k) {
+        mr[k] = __shfl_sync(0xffffffffu, mj[k], row);
+        dr[k] = __shfl_sync(0xffffffffu, dj[k], row);
+        qdr[k] = __shfl_sync(0xffffffffu, qdj[k], row);
+      }
+      if (lane < cnt) {
+        const int64_t u = a.g.in_src[e];
+#pragma unroll
+        for (int k = 0; k < HPW; ++k) {
+          const float ep = sddmm_add1(a.qS[u * H + h0 + k], scS.s, (int8_t)qdr[k], scD.s);
+          const float al = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), mr[k])), dr[k]);
+          const float dE = __fmul_rn(al, __fsub_rn(a.dalpha[e * H + h0 + k], sh_pt[w][row][k]));
+          ba[lane][k] = ep > 0.0f ? dE : __fmul_rn(dE, a.slope);
+        }
+      }
+      __syncwarp();
+      const int lo = (L.off > base ? L.off : base) - base;
+      const int hi = (L.end < base + cnt ? L.end : base + cnt) - base;
+      for (int i = lo; i < hi; ++i)
+#pragma unroll
+        for (int k = 0; k < HPW; ++k) dDp[k] = __fadd_rn(dDp[k], ba[i][k]);
+      __syncwarp();
+    }
+    if (L.deg > 0) {
+#pragma unroll
+      for (int k = 0; k < HPW; ++k) { a.P[vg * H + h0 + k] = sh_pt[w][lane][k]; a.dD[vg * H + h0 + k] = dDp[k]; }
+    }
+    __syncwarp();
+  }
+}
+
+// ---- BS: ⑤′ + ③′ + ②′ per (tile | heavy segment, group) over out-edges (u→v)
+// finalize of row u for the group's columns: ∂H′ = (agg·s_G + ∂S·a_src) + ∂D·a_dst ; ∂S stored
+template <int VPL, int HPW>
+__device__ __forceinline__ void cg_src_finalize(const GatBwdArgs& a, int64_t ul, int64_t ug, int g, float dS,
+                                                float (&part)[VPL], float sG, float& amax_loc) {
+  constexpr int WC = 32 * VPL, LPH = 32 / HPW;
+  const int lane = threadIdx.x & 31, lh = lane / LPH;
+  const int H = a.d.heads, HD = a.d.hd, h = g * HPW + lh;
+  const float dD = a.dD[ug * H + h];
+  const int c0 = g * WC + lane * VPL;
+  float* dst = a.dHp + ul * HD + c0;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const float agg = __fmul_rn(part[k], sG);
+    const float t2 = __fadd_rn(agg, __fmul_rn(dS, __ldg(a.a_src + c0 + k)));
+    const float o = __fadd_rn(t2, __fmul_rn(dD, __ldg(a.a_dst + c0 + k)));
+    amax_loc = fmaxf(amax_loc, fabsf(o));
+    dst[k] = o;
+    part[k] = 0.0f;
+  }
+  if ((lane % LPH) == 0) a.dS[ug * H + h] = dS;
+}
+
+template <int VPL, int HPW>
+__global__ void __launch_bounds__(256) k_bwd_src_cg(const GatBwdArgs a) {
+  constexpr int WC = 32 * VPL, LPH = 32 / HPW, UNRC = CGCfg<VPL>::UNRC;
+  __shared__ float sh_a[WPB][32][HPW];
+  __shared__ float sh_e[WPB][32][HPW];
+  __shared__ float sh_p[WPB][32][HPW];
+  __shared__ int sh_rb[WPB][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lh = lane / LPH;
+  const bool leader = (lane % LPH) == 0;
+  const int H = a.d.heads, HD = a.d.hd, NG = HD / WC;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
+  const float sGH = __fmul_rn(scG.s, scH.s);
+  const int64_t n = a.g.n_local, hc = load_count(a.pout.counts);
+  const int64_t nitems = (hc + (n + TILE - 1) / TILE) * NG;
+  float (*ba)[HPW] = sh_a[w];
+  float (*be)[HPW] = sh_e[w];
+  float (*bp)[HPW] = sh_p[w];
+  float amax_loc = 0.0f;
+  FOR_ITEMS(item, a.work + 2, nitems) {
+    const int64_t wi = item / NG;
+    const int g = (int)(item - wi * NG), h0 = g * HPW;
+    const int8_t* hbase = a.qHp + g * WC + lane * VPL;
+    const int8_t* gbase = a.qG + g * WC + lane * VPL;
+    float part[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) part[k] = 0.0f;
+    float dS = 0.0f;
+    // one 32-edge batch of out-edges: per-edge α, e_pre, P[v] (lane-parallel), then the q_G gathers
+    auto batch = [&](int cnt, int v, const int (&qsr)[HPW], const int* rb, int& cur, Row<VPL>& hw, auto&& on_row) {
+      if ((threadIdx.x & 31) < cnt) {
+#pragma unroll
+        for (int k = 0; k < HPW; ++k) {
+          const int64_t kk = (int64_t)v * H + h0 + k;
+          const float ep = sddmm_add1((int8_t)qsr[k], scS.s, a.qD[kk], scD.s);
+          ba[lane][k] = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), a.m[kk])), a.den[kk]);
+          be[lane][k] = ep;
+          bp[lane][k] = a.P[kk];
+        }
+      }
+      __syncwarp();
+      for (int i0 = 0; i0 < cnt; i0 += UNRC) {
+        Row<VPL> rr[UNRC];
+#pragma unroll
+        for (int j = 0; j < UNRC; ++j) {
+          const int vv = __shfl_sync(0xffffffffu, v, (i0 + j) & 31);
+          if (i0 + j < cnt) rr[j] = load_row<VPL>(gbase + (int64_t)vv * a.ldG);
+        }
+#pragma unroll
+        for (int j = 0; j < UNRC; ++j) {
+          if (i0 + j < cnt) {
+            if (rb) {
+              const int ri = rb[i0 + j];
+              if (ri != cur) { on_row(ri); cur = ri; }
+            }
+            const int dot = cg_dot<VPL, HPW>(rr[j], hw);
+            const float al = ba[i0 + j][lh];
+            if (leader) {
+              const float dal = __fmul_rn(__int2float_rn(dot), sGH);
+              const float dE = __fmul_rn(al, __fsub_rn(dal, bp[i0 + j][lh]));
+              dS = __fadd_rn(dS, be[i0 + j][lh] > 0.0f ? dE : __fmul_rn(dE, a.slope));
+            }
+#pragma unroll
+            for (int q = 0; q < CGCfg<VPL>::WORDS; ++q) {
+              const uint32_t wx = rr[j].w[q] ^ 0x80808080u;
+#pragma unroll
+              for (int k = 0; k < 4 && q * 4 + k < VPL; ++k) part[q * 4 + k] = __fmaf_rn(al, bx2f(wx, k), part[q * 4 + k]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+    };
+    if (wi < hc) {   // ----------------------------------------------- heavy segment: partials
+      Seg s;
+      decode_item(wi, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
+      const int64_t ug = a.g.row_begin + s.vl;
+      int qs[HPW];
+#pragma unroll
+      for (int k = 0; k < HPW; ++k) qs[k] = (int)a.qS[ug * H + h0 + k];
+      Row<VPL> hw = load_row<VPL>(hbase + ug * a.ldHp);
+      int cur = 0;
+      for (int64_t base = s.eb; base < s.ee; base += 32) {
+        const int cnt = (int)(s.ee - base < 32 ? s.ee - base : 32);
+        const int v = lane < cnt ? a.g.out_dst[base + lane] : 0;
+        batch(cnt, v, qs, nullptr, cur, hw, [](int) {});
+      }
+      if (leader) a.hdS[(int64_t)s.slot * H + h0 + lh] = dS;
+      float* dst = a.hagg + (int64_t)s.slot * HD + g * WC + lane * VPL;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) dst[k] = part[k];
+      continue;
+    }
+    // ------------------------------------------------------------- tile of light source rows
+    const int64_t r0 = (wi - hc) * TILE;
+    int T;
+    const TileLane L = tile_setup(a.g.out_ptr, a.pout.hbase, r0, n, T);
+    const int64_t ug0 = a.g.row_begin + r0;
+    int qsj[HPW];
+#pragma unroll
+    for (int k = 0; k < HPW; ++k) qsj[k] = L.deg > 0 ? (int)a.qS[(ug0 + lane) * H + h0 + k] : 0;
+    unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
+    while (zm) {   // light rows without out-edges: ∂H′ = (0 + 0·a_src) + ∂D·a_dst
+      const int j = __ffs(zm) - 1;
+      zm &= zm - 1;
+      cg_src_finalize<VPL, HPW>(a, r0 + j, ug0 + j, g, 0.0f, part, scG.s, amax_loc);
+    }
+    const unsigned act = __ballot_sync(0xffffffffu, L.deg > 0);
+    int nxt = act ? __ffs(act) - 1 : -1;
+    Row<VPL> hw_nxt{}, hw{};
+    if (nxt >= 0) hw_nxt = load_row<VPL>(hbase + (ug0 + nxt) * a.ldHp);
+    int cur = -1;
+    auto on_row = [&](int ri) {
+      if (cur >= 0) {
+        const float dSb = __shfl_sync(0xffffffffu, dS, lh * LPH);
+        cg_src_finalize<VPL, HPW>(a, r0 + cur, ug0 + cur, g, dSb, part, scG.s, amax_loc);
+        dS = 0.0f;
+      }
+      hw = hw_nxt;
+      nxt = tile_next(act, ri);
+      if (nxt >= 0) hw_nxt = load_row<VPL>(hbase + (ug0 + nxt) * a.ldHp);
+    };
+    for (int base = 0; base < T; base += 32) {
+      const int cnt = T - base < 32 ? T - base : 32;
+      const int t = base + lane;
+      const int row = tile_row(t, L.end);
+      const int64_t e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+      int qsr[HPW];
+#pragma unroll
+      for (int k = 0; k < HPW; ++k) qsr[k] = __shfl_sync(0xffffffffu, qsj[k], row);
+      int v = 0;
+      if (lane < cnt) {
+        v = a.g.out_dst[e];
+        sh_rb[w][lane] = row;
+      }
+      batch(cnt, v, qsr, sh_rb[w], cur, hw, on_row);
+    }
+    if (cur >= 0) {
+      const float dSb = __shfl_sync(0xffffffffu, dS, lh * LPH);
+      cg_src_finalize<VPL, HPW>(a, r0 + cur, ug0 + cur, g, dSb, part, scG.s, amax_loc);
+    }
+  }
+  amax_flush(a.amax_dHp, amax_loc);
 }
 
 // FC: heavy rows — fold segment partials in chunk order, write m, den, H_out
@@ -521,58 +1136,6 @@ __global__ void __launch_bounds__(256) k_fwd_combine(const GatFwdArgs a) {
   }
 }
 
-// ================================================================== backward, destination side
-// Pass 1 over a segment of v's in-edges: ∂α = i2f(q_G[v]·q_H′[u]) (s_G s_H′) -> dalpha scratch,
-// P partial = Σ fmaf(∂α, α) (sequential, leader lane of each head).  Returns P partial in leaders.
-template <int H, int VPL>
-__device__ __forceinline__ float bwd_dst_pass1(const GatBwdArgs& a, const Seg& s, const int8_t (&qd)[H],
-                                               const float (&mh)[H], const float (&dh)[H], const Row<VPL>& gw,
-                                               float sS, float sD, float sGH, float (*ba)[H], float (*bd)[H]) {
-  constexpr int LPH = 32 / H;
-  const int lane = threadIdx.x & 31;
-  const int myh = lane / LPH;
-  const bool leader = (lane % LPH) == 0;
-  float P = 0.0f;
-  const int8_t* hbase = a.qHp + lane * VPL;
-  for (int64_t base = s.eb; base < s.ee; base += 32) {
-    const int cnt = (int)(s.ee - base < 32 ? s.ee - base : 32);
-    int u = 0;
-    if (lane < cnt) {
-      u = a.g.in_src[base + lane];
-#pragma unroll
-      for (int h = 0; h < H; ++h)
-        ba[lane][h] = __fdiv_rn(
-            exp_p(__fsub_rn(lrelu(sddmm_add1(a.qS[(int64_t)u * H + h], sS, qd[h], sD), a.slope), mh[h])), dh[h]);
-    }
-    __syncwarp();
-    for (int i0 = 0; i0 < cnt; i0 += UNR) {
-      Row<VPL> r[UNR];
-#pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        const int w = __shfl_sync(0xffffffffu, u, (i0 + j) & 31);
-        if (i0 + j < cnt) r[j] = load_row<VPL>(hbase + (int64_t)w * a.ldHp);
-      }
-#pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        if (i0 + j < cnt) {
-          int dot = row_dot<VPL>(gw, r[j]);
-#pragma unroll
-          for (int o = 1; o < LPH; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-          if (leader) {
-            const float dal = __fmul_rn(__int2float_rn(dot), sGH);
-            P = __fmaf_rn(dal, ba[i0 + j][myh], P);
-            bd[i0 + j][myh] = dal;
-          }
-        }
-      }
-    }
-    __syncwarp();
-    for (int idx = lane; idx < cnt * H; idx += 32) a.dalpha[base * H + idx] = bd[idx / H][idx % H];
-    __syncwarp();
-  }
-  return P;
-}
-
 // Pass 2 over a segment: ∂E = α(∂α − P[v]), ∂E_pre (LeakyReLU backward), Σ ∂E_pre (lane h).
 template <int H>
 __device__ __forceinline__ float bwd_dst_pass2(const GatBwdArgs& a, const Seg& s, const int8_t (&qd)[H],
@@ -601,192 +1164,6 @@ __device__ __forceinline__ float bwd_dst_pass2(const GatBwdArgs& a, const Seg& s
   return part;
 }
 
-
-// BD1 on a tile of light destination rows: pass 1 streams ∂α (IDP4A dot with the row's q_G slice,
-// prefetched one row ahead) and P; pass 2 re-streams the tile for ∂E_pre and ∂D (lane j = row j).
-template <int H, int VPL>
-__device__ __forceinline__ void bwd_dst1_tile(const GatBwdArgs& a, int64_t r0, float (*ba)[H], float (*bd)[H],
-                                              int* rb, float (*pt)[H], float sS, float sD, float sGH) {
-  constexpr int LPH = 32 / H;
-  const int lane = threadIdx.x & 31, myh = lane / LPH;
-  const bool leader = (lane % LPH) == 0;
-  int T;
-  const TileLane L = tile_setup(a.g.in_ptr, a.pin.hbase, r0, a.g.n_local, T);
-  const int64_t vg = a.g.row_begin + L.r;
-  float mj[H], dj[H];
-  int qdj[H];
-#pragma unroll
-  for (int h = 0; h < H; ++h) {
-    mj[h] = L.deg > 0 ? a.m[vg * H + h] : 0.0f;
-    dj[h] = L.deg > 0 ? a.den[vg * H + h] : 0.0f;
-    qdj[h] = L.deg > 0 ? (int)a.qD[vg * H + h] : 0;
-  }
-  if (L.light && L.deg == 0) {
-#pragma unroll
-    for (int h = 0; h < H; ++h) { a.P[vg * H + h] = 0.0f; a.dD[vg * H + h] = 0.0f; }
-  }
-  const unsigned act = __ballot_sync(0xffffffffu, L.deg > 0);
-  const int8_t* gbase = a.qG + lane * VPL;
-  const int8_t* hbase = a.qHp + lane * VPL;
-  const int64_t vg0 = a.g.row_begin + r0;
-  int nxt = act ? __ffs(act) - 1 : -1;
-  Row<VPL> gw_nxt{}, gw{};
-  if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
-  float P = 0.0f;
-  int cur = -1;
-  // ---- pass 1
-  for (int base = 0; base < T; base += 32) {
-    const int cnt = T - base < 32 ? T - base : 32;
-    const int t = base + lane;
-    const int row = tile_row(t, L.end);
-    const int64_t ebr = __shfl_sync(0xffffffffu, L.eb, row);
-    const int offr = __shfl_sync(0xffffffffu, L.off, row);
-    float mr[H], dr[H];
-    int qdr[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      mr[h] = __shfl_sync(0xffffffffu, mj[h], row);
-      dr[h] = __shfl_sync(0xffffffffu, dj[h], row);
-      qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row);
-    }
-    int u = 0;
-    const int64_t e = ebr + (t - offr);
-    if (lane < cnt) {
-      u = a.g.in_src[e];
-#pragma unroll
-      for (int h = 0; h < H; ++h)
-        ba[lane][h] = __fdiv_rn(
-            exp_p(__fsub_rn(lrelu(sddmm_add1(a.qS[(int64_t)u * H + h], sS, (int8_t)qdr[h], sD), a.slope), mr[h])),
-            dr[h]);
-      rb[lane] = row;
-    }
-    __syncwarp();
-    for (int i0 = 0; i0 < cnt; i0 += UNR) {
-      Row<VPL> rr[UNR];
-#pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        const int w = __shfl_sync(0xffffffffu, u, (i0 + j) & 31);
-        if (i0 + j < cnt) rr[j] = load_row<VPL>(hbase + (int64_t)w * a.ldHp);
-      }
-#pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        if (i0 + j < cnt) {
-          const int ri = rb[i0 + j];
-          if (ri != cur) {
-            if (cur >= 0 && leader) pt[cur][myh] = P;
-            P = 0.0f;
-            cur = ri;
-            gw = gw_nxt;
-            nxt = tile_next(act, cur);
-            if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
-          }
-          int dot = row_dot<VPL>(gw, rr[j]);
-#pragma unroll
-          for (int o = 1; o < LPH; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-          if (leader) {
-            const float dal = __fmul_rn(__int2float_rn(dot), sGH);
-            P = __fmaf_rn(dal, ba[i0 + j][myh], P);
-            bd[i0 + j][myh] = dal;
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if (lane < cnt) {
-#pragma unroll
-      for (int h = 0; h < H; ++h) a.dalpha[e * H + h] = bd[lane][h];
-    }
-    __syncwarp();
-  }
-  if (cur >= 0 && leader) pt[cur][myh] = P;
-  __syncwarp();
-  // ---- pass 2
-  float dDp[H];
-#pragma unroll
-  for (int h = 0; h < H; ++h) dDp[h] = 0.0f;
-  for (int base = 0; base < T; base += 32) {
-    const int cnt = T - base < 32 ? T - base : 32;
-    const int t = base + lane;
-    const int row = tile_row(t, L.end);
-    const int64_t ebr = __shfl_sync(0xffffffffu, L.eb, row);
-    const int offr = __shfl_sync(0xffffffffu, L.off, row);
-    float mr[H], dr[H];
-    int qdr[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      mr[h] = __shfl_sync(0xffffffffu, mj[h], row);
-      dr[h] = __shfl_sync(0xffffffffu, dj[h], row);
-      qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row);
-    }
-    if (lane < cnt) {
-      const int64_t e = ebr + (t - offr);
-      const int64_t u = a.g.in_src[e];
-#pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const float ep = sddmm_add1(a.qS[u * H + h], sS, (int8_t)qdr[h], sD);
-        const float al = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), mr[h])), dr[h]);
-        const float dE = __fmul_rn(al, __fsub_rn(a.dalpha[e * H + h], pt[row][h]));
-        ba[lane][h] = ep > 0.0f ? dE : __fmul_rn(dE, a.slope);
-      }
-    }
-    __syncwarp();
-    const int lo = (L.off > base ? L.off : base) - base;
-    const int hi = (L.end < base + cnt ? L.end : base + cnt) - base;
-    for (int i = lo; i < hi; ++i)
-#pragma unroll
-      for (int h = 0; h < H; ++h) dDp[h] = __fadd_rn(dDp[h], ba[i][h]);
-    __syncwarp();
-  }
-  if (L.deg > 0) {
-#pragma unroll
-    for (int h = 0; h < H; ++h) { a.P[vg * H + h] = pt[lane][h]; a.dD[vg * H + h] = dDp[h]; }
-  }
-  __syncwarp();
-}
-
-// BD1: light rows -> ∂α, P, ∂D final; heavy segments -> ∂α, P partial (hP)
-template <int H, int VPL>
-__global__ void __launch_bounds__(256, 2) k_bwd_dst1(const GatBwdArgs a) {
-  constexpr int LPH = 32 / H;
-  __shared__ float sh_a[WPB][32][H];
-  __shared__ float sh_d[WPB][32][H];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
-  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
-  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
-  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
-  const float sGH = __fmul_rn(scG.s, scH.s);
-  const int64_t hc = load_count(a.pin.counts), nitems = hc + (a.g.n_local + TILE - 1) / TILE;
-  __shared__ int sh_rb[WPB][32];
-  __shared__ float sh_pt[WPB][32][H];
-  FOR_ITEMS(item, a.work + 0, nitems) {
-    if (item >= hc) {
-      bwd_dst1_tile<H, VPL>(a, (item - hc) * TILE, sh_a[w], sh_d[w], sh_rb[w], sh_pt[w], scS.s, scD.s, sGH);
-      continue;
-    }
-    Seg s;
-    if (!decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s)) continue;
-    const int64_t vg = a.g.row_begin + s.vl;
-    int8_t qd[H];
-    float mh[H], dh[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) { qd[h] = a.qD[vg * H + h]; mh[h] = a.m[vg * H + h]; dh[h] = a.den[vg * H + h]; }
-    const Row<VPL> gw = load_row<VPL>(a.qG + vg * a.ldG + lane * VPL);
-    const float Pl = bwd_dst_pass1<H, VPL>(a, s, qd, mh, dh, gw, scS.s, scD.s, sGH, sh_a[w], sh_d[w]);
-    if (s.slot >= 0) {
-      if ((lane % LPH) == 0) a.hP[(int64_t)s.slot * H + lane / LPH] = Pl;
-      continue;
-    }
-    float P[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) P[h] = __shfl_sync(0xffffffffu, Pl, h * LPH);
-    const float dD = bwd_dst_pass2<H>(a, s, qd, mh, dh, P, scS.s, scD.s, sh_a[w]);
-    if (lane < H) {
-      a.P[vg * H + lane] = head_pick<H>(P, lane);
-      a.dD[vg * H + lane] = dD;
-    }
-  }
-}
 
 // BD2: heavy segments -> P (fold of hP; segment 0 writes it), ∂D partial (hdD)
 template <int H>
@@ -831,241 +1208,6 @@ __global__ void __launch_bounds__(256) k_bwd_dst3(const GatBwdArgs a) {
   float tot = a.hdD[(int64_t)base * H + h];
   for (int j = 1; j < nseg; ++j) tot = __fadd_rn(tot, a.hdD[(int64_t)(base + j) * H + h]);
   a.dD[(a.g.row_begin + vl) * H + h] = tot;
-}
-
-// ================================================================== backward, source side
-// One segment of u's out-edges: recompute α, e_pre, ∂α, ∂E_pre per out-edge (u→v) from per-node
-// data; ∂S partial (leaders) and the ⑤′ aggregation partial Σ fmaf(α, q_G[v]).
-template <int H, int VPL>
-__device__ __forceinline__ float bwd_src_seg(const GatBwdArgs& a, const Seg& s, const int8_t (&qs)[H],
-                                             const Row<VPL>& hw, float sS, float sD, float sGH, float (*ba)[H],
-                                             float (*be)[H], float (*bp)[H], float (&part)[VPL]) {
-  constexpr int LPH = 32 / H;
-  const int lane = threadIdx.x & 31;
-  const int myh = lane / LPH;
-  const bool leader = (lane % LPH) == 0;
-  float dS = 0.0f;
-  const int8_t* gbase = a.qG + lane * VPL;
-  for (int64_t base = s.eb; base < s.ee; base += 32) {
-    const int cnt = (int)(s.ee - base < 32 ? s.ee - base : 32);
-    int v = 0;
-    if (lane < cnt) {
-      v = a.g.out_dst[base + lane];
-#pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const int64_t k = (int64_t)v * H + h;
-        const float ep = sddmm_add1(qs[h], sS, a.qD[k], sD);
-        ba[lane][h] = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), a.m[k])), a.den[k]);
-        be[lane][h] = ep;
-        bp[lane][h] = a.P[k];
-      }
-    }
-    __syncwarp();
-    for (int i0 = 0; i0 < cnt; i0 += UNR) {
-      Row<VPL> r[UNR];
-#pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        const int vv = __shfl_sync(0xffffffffu, v, (i0 + j) & 31);
-        if (i0 + j < cnt) r[j] = load_row<VPL>(gbase + (int64_t)vv * a.ldG);
-      }
-#pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        if (i0 + j < cnt) {
-          int dot = row_dot<VPL>(r[j], hw);
-#pragma unroll
-          for (int o = 1; o < LPH; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-          const float al = ba[i0 + j][myh];
-          if (leader) {
-            const float dal = __fmul_rn(__int2float_rn(dot), sGH);
-            const float dE = __fmul_rn(al, __fsub_rn(dal, bp[i0 + j][myh]));
-            dS = __fadd_rn(dS, be[i0 + j][myh] > 0.0f ? dE : __fmul_rn(dE, a.slope));
-          }
-#pragma unroll
-          for (int q = 0; q < (VPL + 3) / 4; ++q) {
-            const uint32_t wx = r[j].w[q] ^ 0x80808080u;
-#pragma unroll
-            for (int k = 0; k < 4 && q * 4 + k < VPL; ++k) part[q * 4 + k] = __fmaf_rn(al, bx2f(wx, k), part[q * 4 + k]);
-          }
-        }
-      }
-    }
-    __syncwarp();
-  }
-  return dS;
-}
-
-// ②′ finalize of source row u: ∂H′ = (agg·s_G + ∂S·a_src) + ∂D·a_dst ; ∂S stored for the ∂a pass
-template <int VPL>
-__device__ __forceinline__ void bwd_src_finalize(const GatBwdArgs& a, int64_t ul, int64_t ug, int myh, float dS,
-                                                 const float (&sum)[VPL], float sG, float& amax_loc, int H) {
-  constexpr int HD = 32 * VPL;
-  const int lane = threadIdx.x & 31;
-  const float dD = a.dD[ug * H + myh];
-  float* dst = a.dHp + ul * HD + lane * VPL;
-  const float* asrc = a.a_src + lane * VPL;
-  const float* adst = a.a_dst + lane * VPL;
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    const float agg = __fmul_rn(sum[k], sG);
-    const float t2 = __fadd_rn(agg, __fmul_rn(dS, __ldg(asrc + k)));
-    const float o = __fadd_rn(t2, __fmul_rn(dD, __ldg(adst + k)));
-    amax_loc = fmaxf(amax_loc, fabsf(o));
-    dst[k] = o;
-  }
-  if ((lane % (32 / H)) == 0) a.dS[ug * H + myh] = dS;
-}
-
-__device__ __forceinline__ void amax_flush(unsigned* slot, float amax_loc) {
-  amax_loc = warp_max(amax_loc);
-  if ((threadIdx.x & 31) == 0 && slot) atomicMax(slot, __float_as_uint(amax_loc));
-}
-
-// BS on a tile of light source rows: per out-edge (u→v) recompute α, e_pre, ∂α, ∂E_pre; stream
-// the q_G[v] gathers across rows (own q_H′[u] slice prefetched one row ahead); finalize at row change.
-template <int H, int VPL>
-__device__ __forceinline__ void bwd_src_tile(const GatBwdArgs& a, int64_t r0, float (*ba)[H], float (*be)[H],
-                                             float (*bp)[H], int* rb, float sS, float sD, float sGH, float sG,
-                                             float& amax_loc) {
-  constexpr int LPH = 32 / H;
-  const int lane = threadIdx.x & 31, myh = lane / LPH;
-  const bool leader = (lane % LPH) == 0;
-  int T;
-  const TileLane L = tile_setup(a.g.out_ptr, a.pout.hbase, r0, a.g.n_local, T);
-  const int64_t ug0 = a.g.row_begin + r0;
-  int qsj[H];
-#pragma unroll
-  for (int h = 0; h < H; ++h) qsj[h] = L.deg > 0 ? (int)a.qS[(ug0 + lane) * H + h] : 0;
-  const int8_t* gbase = a.qG + lane * VPL;
-  const int8_t* hbase = a.qHp + lane * VPL;
-  float zero[VPL];
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) zero[k] = 0.0f;
-  unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
-  while (zm) {   // light rows without out-edges: ∂H′ = (0 + 0·a_src) + ∂D·a_dst
-    const int j = __ffs(zm) - 1;
-    zm &= zm - 1;
-    bwd_src_finalize<VPL>(a, r0 + j, ug0 + j, myh, 0.0f, zero, sG, amax_loc, H);
-  }
-  const unsigned act = __ballot_sync(0xffffffffu, L.deg > 0);
-  int nxt = act ? __ffs(act) - 1 : -1;
-  Row<VPL> hw_nxt{}, hw{};
-  if (nxt >= 0) hw_nxt = load_row<VPL>(hbase + (ug0 + nxt) * a.ldHp);
-  float part[VPL];
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) part[k] = 0.0f;
-  float dS = 0.0f;
-  int cur = -1;
-  auto flush = [&](int j) {
-    const float dSb = __shfl_sync(0xffffffffu, dS, myh * LPH);
-    bwd_src_finalize<VPL>(a, r0 + j, ug0 + j, myh, dSb, part, sG, amax_loc, H);
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) part[k] = 0.0f;
-    dS = 0.0f;
-  };
-  for (int base = 0; base < T; base += 32) {
-    const int cnt = T - base < 32 ? T - base : 32;
-    const int t = base + lane;
-    const int row = tile_row(t, L.end);
-    const int64_t ebr = __shfl_sync(0xffffffffu, L.eb, row);
-    const int offr = __shfl_sync(0xffffffffu, L.off, row);
-    int qsr[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) qsr[h] = __shfl_sync(0xffffffffu, qsj[h], row);
-    int v = 0;
-    if (lane < cnt) {
-      v = a.g.out_dst[ebr + (t - offr)];
-#pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const int64_t k = (int64_t)v * H + h;
-        const float ep = sddmm_add1((int8_t)qsr[h], sS, a.qD[k], sD);
-        ba[lane][h] = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), a.m[k])), a.den[k]);
-        be[lane][h] = ep;
-        bp[lane][h] = a.P[k];
-      }
-      rb[lane] = row;
-    }
-    __syncwarp();
-    for (int i0 = 0; i0 < cnt; i0 += UNR) {
-      Row<VPL> rr[UNR];
-#pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        const int vv = __shfl_sync(0xffffffffu, v, (i0 + j) & 31);
-        if (i0 + j < cnt) rr[j] = load_row<VPL>(gbase + (int64_t)vv * a.ldG);
-      }
-#pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        if (i0 + j < cnt) {
-          const int ri = rb[i0 + j];
-          if (ri != cur) {
-            if (cur >= 0) flush(cur);
-            cur = ri;
-            hw = hw_nxt;
-            nxt = tile_next(act, cur);
-            if (nxt >= 0) hw_nxt = load_row<VPL>(hbase + (ug0 + nxt) * a.ldHp);
-          }
-          int dot = row_dot<VPL>(rr[j], hw);
-#pragma unroll
-          for (int o = 1; o < LPH; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-          const float al = ba[i0 + j][myh];
-          if (leader) {
-            const float dal = __fmul_rn(__int2float_rn(dot), sGH);
-            const float dE = __fmul_rn(al, __fsub_rn(dal, bp[i0 + j][myh]));
-            dS = __fadd_rn(dS, be[i0 + j][myh] > 0.0f ? dE : __fmul_rn(dE, a.slope));
-          }
-#pragma unroll
-          for (int q = 0; q < (VPL + 3) / 4; ++q) {
-            const uint32_t wx = rr[j].w[q] ^ 0x80808080u;
-#pragma unroll
-            for (int k = 0; k < 4 && q * 4 + k < VPL; ++k) part[q * 4 + k] = __fmaf_rn(al, bx2f(wx, k), part[q * 4 + k]);
-          }
-        }
-      }
-    }
-    __syncwarp();
-  }
-  if (cur >= 0) flush(cur);
-}
-
-// BS: light out-rows (tiles) -> ∂H′ final; heavy out-segments -> ∂S, aggregation partials
-template <int H, int VPL>
-__global__ void __launch_bounds__(256, 2) k_bwd_src(const GatBwdArgs a) {
-  constexpr int LPH = 32 / H;
-  constexpr int HD = 32 * VPL;
-  __shared__ float sh_a[WPB][32][H];
-  __shared__ float sh_e[WPB][32][H];
-  __shared__ float sh_p[WPB][32][H];
-  __shared__ int sh_rb[WPB][32];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
-  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
-  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
-  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
-  const float sGH = __fmul_rn(scG.s, scH.s);
-  float amax_loc = 0.0f;
-  const int64_t hc = load_count(a.pout.counts), nitems = hc + (a.g.n_local + TILE - 1) / TILE;
-  FOR_ITEMS(item, a.work + 2, nitems) {
-    if (item >= hc) {
-      bwd_src_tile<H, VPL>(a, (item - hc) * TILE, sh_a[w], sh_e[w], sh_p[w], sh_rb[w], scS.s, scD.s, sGH, scG.s,
-                           amax_loc);
-      continue;
-    }
-    Seg s;
-    decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
-    const int64_t ug = a.g.row_begin + s.vl;
-    int8_t qs[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) qs[h] = a.qS[ug * H + h];
-    const Row<VPL> hw = load_row<VPL>(a.qHp + ug * a.ldHp + lane * VPL);
-    float part[VPL];
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) part[k] = 0.0f;
-    const float dSl = bwd_src_seg<H, VPL>(a, s, qs, hw, scS.s, scD.s, sGH, sh_a[w], sh_e[w], sh_p[w], part);
-    if ((lane % LPH) == 0) a.hdS[(int64_t)s.slot * H + lane / LPH] = dSl;
-    float* dst = a.hagg + (int64_t)s.slot * HD + lane * VPL;
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) dst[k] = part[k];
-  }
-  amax_flush(a.amax_dHp, amax_loc);
 }
 
 // BC: heavy out-rows -> fold ∂S and aggregation partials in chunk order, finalize ∂H′
@@ -1143,42 +1285,83 @@ __global__ void __launch_bounds__(256) k_bwd_attn_grad(const GatBwdArgs a) {
 // ------------------------------------------------------------------ dispatch
 static int item_grid(int64_t items) {
   int64_t g = (items + WPB - 1) / WPB;
-  const int64_t cap = (int64_t)num_sms() * 4;     // >= resident blocks; the work queue balances
+  const int64_t cap = (int64_t)num_sms() * 8;     // >= resident blocks; the work queue balances
   if (g > cap) g = cap;
   return (int)(g < 1 ? 1 : g);
 }
 
+// (H, HD/32) for the row-wide kernels, (VPL, HPW) head-group shape for the gather kernels
 #define TANGO_HV_CASES(X) X(1, 2) X(1, 4) X(1, 8) X(1, 16) X(2, 2) X(2, 4) X(2, 8) X(2, 16) \
                           X(4, 2) X(4, 4) X(4, 8) X(4, 16) X(8, 2) X(8, 4) X(8, 8) X(8, 16)
+#define TANGO_CG_CASES(X) X(1, 4) X(1, 2) X(1, 1) X(2, 1) X(4, 1) X(8, 1) X(16, 1)
+
+static bool cg_shape(int D, int& vpl, int& hpw) {
+  if (D >= 32 && D % 32 == 0) {
+    vpl = D / 32; hpw = 1;
+    return vpl == 1 || vpl == 2 || vpl == 4 || vpl == 8 || vpl == 16;
+  }
+  if (D == 16) { vpl = 1; hpw = 2; return true; }
+  if (D == 8) { vpl = 1; hpw = 4; return true; }
+  return false;
+}
+bool gat_shape_supported(int heads, int head_dim) {
+  int v, p;
+  return cg_shape(head_dim, v, p);
+}
 
 cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
   if (a.g.n_local == 0) return cudaSuccess;
   const int hv = a.d.heads * 100 + a.d.hd / 32;
   const int64_t items = a.g.n_local + a.plan.cap;
+  int vpl, hpw;
+  if (!cg_shape(a.d.head_dim, vpl, hpw)) return cudaErrorInvalidValue;
+  const int64_t cg_items = (a.plan.cap + (a.g.n_local + TILE - 1) / TILE) * (a.d.hd / (32 * vpl));
   bool ok = false;
 #define X(H_, V_)                                                                                  \
   if (hv == H_ * 100 + V_) {                                                                       \
     ok = true;                                                                                     \
     { ProfScope p("gat_fwd_stats", st);  k_fwd_stats<H_><<<item_grid(items), 256, 0, st>>>(a); }   \
     { ProfScope p("gat_fwd_stats2", st); k_fwd_stats2<H_><<<item_grid(a.plan.cap), 256, 0, st>>>(a); } \
-    { ProfScope p("gat_fwd_agg", st);    k_fwd_agg<H_, V_><<<item_grid(items), 256, 0, st>>>(a); }  \
-    { ProfScope p("gat_fwd_combine", st); k_fwd_combine<H_, V_><<<item_grid(a.g.n_local), 256, 0, st>>>(a); } \
   }
   TANGO_HV_CASES(X)
 #undef X
   if (!ok) return cudaErrorInvalidValue;
+  (void)cg_items;
+  ok = false;
+#define X(H_, V_)                                                                                  \
+  if (hv == H_ * 100 + V_) {                                                                       \
+    ok = true;                                                                                     \
+    { ProfScope p("gat_fwd_alpha3", st); k_fwd_alpha3<H_><<<item_grid(a.plan.cap), 256, 0, st>>>(a); } \
+    { ProfScope p("gat_fwd_agg", st);                                                              \
+      k_fwd_agg2<H_, V_><<<item_grid(a.plan.cap + (a.g.n_local + TILE - 1) / TILE), 256, 0, st>>>(a); } \
+    { ProfScope p("gat_fwd_combine", st);                                                          \
+      k_fwd_combine<H_, V_><<<item_grid(a.g.n_local), 256, 0, st>>>(a); }                           \
+  }
+  TANGO_HV_CASES(X)
+#undef X
   return cudaGetLastError();
 }
 
 cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st) {
   if (a.g.n_local == 0) return cudaSuccess;
-  const int hv = a.d.heads * 100 + a.d.hd / 32;
-  const int64_t items = a.g.n_local + a.pin.cap;
+  int vpl, hpw;
+  if (!cg_shape(a.d.head_dim, vpl, hpw)) return cudaErrorInvalidValue;
+  const int64_t cg_items = (a.pin.cap + (a.g.n_local + TILE - 1) / TILE) * (a.d.hd / (32 * vpl));
   bool ok = false;
+#define X(V_, P_)                                                                                  \
+  if (vpl == V_ && hpw == P_) {                                                                    \
+    ok = true;                                                                                     \
+    ProfScope p("gat_bwd_dst1", st);                                                               \
+    k_bwd_dst1_cg<V_, P_><<<item_grid(cg_items), 256, 0, st>>>(a);                                  \
+  }
+  TANGO_CG_CASES(X)
+#undef X
+  if (!ok) return cudaErrorInvalidValue;
+  ok = false;
+  const int hv = a.d.heads * 100 + a.d.hd / 32;
 #define X(H_, V_)                                                                                  \
   if (hv == H_ * 100 + V_) {                                                                       \
     ok = true;                                                                                     \
-    { ProfScope p("gat_bwd_dst1", st); k_bwd_dst1<H_, V_><<<item_grid(items), 256, 0, st>>>(a); }  \
     { ProfScope p("gat_bwd_dst2", st); k_bwd_dst2<H_><<<item_grid(a.pin.cap), 256, 0, st>>>(a); }  \
     { ProfScope p("gat_bwd_dst3", st);                                                             \
       k_bwd_dst3<H_><<<(unsigned)((a.g.n_local * H_ + 255) / 256), 256, 0, st>>>(a); }            \
@@ -1191,13 +1374,24 @@ cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st) {
 
 cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st) {
   if (a.g.n_local == 0) return cudaSuccess;
-  const int hv = a.d.heads * 100 + a.d.hd / 32;
-  const int64_t items = a.g.n_local + a.pout.cap;
+  int vpl, hpw;
+  if (!cg_shape(a.d.head_dim, vpl, hpw)) return cudaErrorInvalidValue;
+  const int64_t cg_items = (a.pout.cap + (a.g.n_local + TILE - 1) / TILE) * (a.d.hd / (32 * vpl));
   bool ok = false;
+#define X(V_, P_)                                                                                  \
+  if (vpl == V_ && hpw == P_) {                                                                    \
+    ok = true;                                                                                     \
+    ProfScope p("gat_bwd_src", st);                                                                \
+    k_bwd_src_cg<V_, P_><<<item_grid(cg_items), 256, 0, st>>>(a);                                   \
+  }
+  TANGO_CG_CASES(X)
+#undef X
+  if (!ok) return cudaErrorInvalidValue;
+  ok = false;
+  const int hv = a.d.heads * 100 + a.d.hd / 32;
 #define X(H_, V_)                                                                                  \
   if (hv == H_ * 100 + V_) {                                                                       \
     ok = true;                                                                                     \
-    { ProfScope p("gat_bwd_src", st); k_bwd_src<H_, V_><<<item_grid(items), 256, 0, st>>>(a); }    \
     { ProfScope p("gat_bwd_src_combine", st);                                                      \
       k_bwd_src_combine<H_, V_><<<item_grid(a.g.n_local), 256, 0, st>>>(a); }                     \
     { ProfScope p("gat_bwd_attn_grad", st);                                                        \

@@ -91,7 +91,8 @@ struct GatFwdArgs {
   PlanDev plan;                               // in-CSR plan
   float* hmax; float* hden;                   // [cap][H] heavy-segment softmax partials
   float* hagg;                                // [cap][HD] heavy-segment aggregation partials
-  int32_t* work;                              // [4] work-queue counters (zeroed before the launch)
+  int32_t* work;                              // [8] work-queue counters (zeroed before the launch)
+  float* alpha;                               // [e_in][H] α with the sign of e_pre (LeakyReLU branch)
 };
 cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st);
 
@@ -112,7 +113,8 @@ struct GatBwdArgs {
   float* hP; float* hdD;                     // [pin.cap][H]
   float* hdS;                                // [pout.cap][H]
   float* hagg;                               // [pout.cap][HD]
-  int32_t* work;                             // [4] work-queue counters (zeroed before the launch)
+  int32_t* work;                             // [8] work-queue counters (zeroed before the launch)
+  const float* alpha;                        // [e_in][H] signed α from the forward
 };
 cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st);
 cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st);
