@@ -332,7 +332,8 @@ struct GatLayout {
       off_qG, off_dal, off_dHp, off_qdHp, off_dW64, total;
   // segment plans (gat.cu) and heavy-segment scratch
   size_t off_pin_hbase, off_pin_hseg, off_pin_hrow, off_pin_cnt, off_pout_hbase, off_pout_hseg, off_pout_hrow,
-      off_pout_cnt, off_h1, off_h2, off_hdS, off_hagg, off_work, off_dS, off_alpha;
+      off_pout_cnt, off_h1, off_h2, off_hdS, off_hagg, off_work, off_dS, off_alpha, off_pin_tiles, off_pout_tiles;
+  int64_t tcap;
 };
 GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   GatLayout L{};
@@ -382,13 +383,17 @@ GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   L.off_work = take(64);
   L.off_dS = take((size_t)L.N * L.H * 4);
   L.off_alpha = take((size_t)L.E * L.H * 4);
+  L.tcap = L.n + L.n / 32 + 1;
+  L.off_pin_tiles = take((size_t)L.tcap * 4);
+  L.off_pout_tiles = take((size_t)L.tcap * 4);
   L.total = o;
   return L;
 }
-PlanDev plan_of(char* c, size_t hb, size_t hs, size_t hr, size_t cn, int64_t cap) {
+PlanDev plan_of(char* c, size_t hb, size_t hs, size_t hr, size_t cn, int64_t cap, size_t tl, int64_t tcap) {
   PlanDev p;
   p.hbase = (int32_t*)(c + hb); p.hseg_row = (int32_t*)(c + hs); p.hrow = (int32_t*)(c + hr);
   p.counts = (int32_t*)(c + cn); p.cap = cap;
+  p.tiles = (int32_t*)(c + tl); p.tcap = tcap;
   return p;
 }
 tango_status check_gat(const tango_graph* G, const tango_gat_params* p) {
@@ -502,9 +507,10 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   TRY(comm_gather_rows(comm, qD, (size_t)L.H, st));
   // F5 + F6: segment plan of the in-CSR, then softmax statistics, aggregation and heavy-row combine
   if (amax_out) TRY_CUDA(cudaMemsetAsync(amax_out, 0, 4, st));
-  const PlanDev pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in);
+  const PlanDev pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in, L.off_pin_tiles, L.tcap);
   TRY_CUDA(cudaMemsetAsync(pin.counts, 0, 16, st));
   TRY(launch_status(launch_plan(G->in_ptr, L.n, g.chunk, pin, st)));
+  TRY(launch_status(launch_plan_tiles(G->in_ptr, L.n, pin, st)));
   GatFwdArgs fa{};
   fa.g = g; fa.d = {p->heads, p->head_dim, (int)L.HD}; fa.slope = p->neg_slope; fa.bits = p->bits;
   fa.qS = qS; fa.amax_S = sc + SL_AMAX_S; fa.qD = qD; fa.amax_D = sc + SL_AMAX_D;
@@ -566,12 +572,14 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
                                     scf + SL_S_G, dev_status, st)));
   TRY(comm_gather_rows(comm, qG, (size_t)L.ldHD, st));
   // B2-B4: destination rows (in-CSR plan from the forward call), B5-B7: source rows (out-CSR plan)
-  const PlanDev pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in);
-  const PlanDev pout = plan_of(c, L.off_pout_hbase, L.off_pout_hseg, L.off_pout_hrow, L.off_pout_cnt, L.cap_out);
+  const PlanDev pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in, L.off_pin_tiles, L.tcap);
+  const PlanDev pout = plan_of(c, L.off_pout_hbase, L.off_pout_hseg, L.off_pout_hrow, L.off_pout_cnt, L.cap_out, L.off_pout_tiles, L.tcap);
   TRY_CUDA(cudaMemsetAsync(pin.counts, 0, 16, st));
   TRY(launch_status(launch_plan(G->in_ptr, L.n, g.chunk, pin, st)));
+  TRY(launch_status(launch_plan_tiles(G->in_ptr, L.n, pin, st)));
   TRY_CUDA(cudaMemsetAsync(pout.counts, 0, 16, st));
   TRY(launch_status(launch_plan(G->out_ptr, L.n, g.chunk, pout, st)));
+  TRY(launch_status(launch_plan_tiles(G->out_ptr, L.n, pout, st)));
   GatBwdArgs ba{};
   ba.g = g; ba.d = {p->heads, p->head_dim, (int)L.HD}; ba.slope = p->neg_slope; ba.bits = p->bits;
   ba.qS = qS; ba.amax_S = sc + SL_AMAX_S; ba.qD = qD; ba.amax_D = sc + SL_AMAX_D;

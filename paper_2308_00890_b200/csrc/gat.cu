@@ -50,6 +50,47 @@ cudaError_t launch_plan(const int64_t* ptr, int64_t n, int chunk, const PlanDev&
   return cudaGetLastError();
 }
 
+// Edge-balanced sub-tiles of light rows: each 32-row block is cut into runs of rows whose first
+// edge falls in the same BIN-edge window, so a work item holds at most BIN + C_E edges.  Items are
+// encoded (block << 10) | (lo << 5) | (hi - 1) for rows [32*block + lo, 32*block + hi).
+constexpr int TILE_BIN = 128;
+__global__ void k_plan_tiles(const int64_t* __restrict__ ptr, int64_t n, PlanDev p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (b * 32 >= n) return;
+  const int64_t r = b * 32 + lane;
+  const bool has = r < n;
+  const bool light = has && p.hbase[r] < 0;
+  const int deg = light ? (int)(ptr[r + 1] - ptr[r]) : 0;
+  int cum = deg;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, cum, o);
+    if (lane >= o) cum += y;
+  }
+  const int key = (cum - deg) / TILE_BIN;
+  const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const unsigned starts = __ballot_sync(0xffffffffu, has && (lane == 0 || key != prev));
+  const unsigned valid = __ballot_sync(0xffffffffu, has);
+  const int nrun = __popc(starts);
+  int slot = 0;
+  if (lane == 0) slot = atomicAdd(&p.counts[2], nrun);
+  slot = __shfl_sync(0xffffffffu, slot, 0);
+  if (starts & (1u << lane)) {
+    const unsigned later = lane >= 31 ? 0u : (starts & ~((2u << lane) - 1u));
+    const int hi = later ? __ffs(later) - 1 : 32 - __clz(valid);
+    const int idx = __popc(starts & ((1u << lane) - 1u));
+    p.tiles[slot + idx] = (int32_t)((b << 10) | (lane << 5) | (hi - 1));
+  }
+}
+cudaError_t launch_plan_tiles(const int64_t* ptr, int64_t n, const PlanDev& p, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  ProfScope ps("plan_tiles", st);
+  const int64_t blocks = (n + 31) / 32;
+  k_plan_tiles<<<(unsigned)((blocks * 32 + 255) / 256), 256, 0, st>>>(ptr, n, p);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ shared device pieces
 struct Seg {
   int64_t vl, eb, ee;   // local row, edge range
@@ -216,11 +257,11 @@ struct TileLane {
 };
 
 __device__ __forceinline__ TileLane tile_setup(const int64_t* __restrict__ ptr, const int32_t* __restrict__ hbase,
-                                               int64_t r0, int64_t n, int& T) {
+                                               int64_t r0, int64_t n, int& T, int lo = 0, int hi = 32) {
   const int lane = threadIdx.x & 31;
   TileLane L;
   L.r = r0 + lane;
-  const bool has = L.r < n;
+  const bool has = L.r < n && lane >= lo && lane < hi;
   L.light = has && hbase[L.r] < 0;
   L.eb = has ? ptr[L.r] : 0;
   const int64_t ee = has ? ptr[L.r + 1] : 0;
@@ -587,36 +628,44 @@ __device__ __forceinline__ void agg_chunk(const int8_t* __restrict__ xbase, int6
     const int w = __shfl_sync(0xffffffffu, w_l, j);
     if (j < cnt) ring[j] = load_row<VPL>(xbase + (int64_t)w * ldx);
   }
+  // rolling ring: a RING-wide unrolled body inside a runtime loop keeps RING rows in flight with
+  // small code (the fully unrolled 32-edge body overflowed the instruction cache)
+  for (int i0 = 0; i0 < cnt; i0 += RING) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    if (i < cnt) {
-      const Row<VPL> r = ring[i % RING];
-      if (i + RING < 32) {
-        const int w = __shfl_sync(0xffffffffu, w_l, i + RING);
-        if (i + RING < cnt) ring[i % RING] = load_row<VPL>(xbase + (int64_t)w * ldx);
-      }
-      if (rb) {
-        const int ri = rb[i];
-        if (ri != cur) { on_row(ri); cur = ri; }
-      }
-      const uint64_t al2 = pkf(sa[i][myh]);
-      if constexpr (VPL >= 4) {
+    for (int j = 0; j < RING; ++j) {
+      const int i = i0 + j;
+      if (i < cnt) {
+        const Row<VPL> r = ring[j];
+        const int nx = i + RING;
+        const int w = __shfl_sync(0xffffffffu, w_l, nx & 31);
+        if (nx < cnt) ring[j] = load_row<VPL>(xbase + (int64_t)w * ldx);
+        if (rb) {
+          const int ri = rb[i];
+          if (ri != cur) { on_row(ri); cur = ri; }
+        }
+        const uint64_t al2 = pkf(sa[i][myh]);
+        if constexpr (VPL >= 4) {
 #pragma unroll
-        for (int q = 0; q < WORDS; ++q) fma4_codes(r.w[q], al2, acc[2 * q], acc[2 * q + 1]);
-      } else {   // VPL == 2: two codes in the low half-word
-        const uint32_t wx = r.w[0] ^ 0x80808080u;
-        uint64_t f01 = pk2(__byte_perm(wx, 0x4B000000u, 0x7440u), __byte_perm(wx, 0x4B000000u, 0x7441u));
-        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(f01) : "l"(0xCB000080CB000080ull));
-        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[0]) : "l"(al2), "l"(f01));
+          for (int q = 0; q < WORDS; ++q) fma4_codes(r.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+        } else {   // VPL == 2: two codes in the low half-word
+          const uint32_t wx = r.w[0] ^ 0x80808080u;
+          uint64_t f01 = pk2(__byte_perm(wx, 0x4B000000u, 0x7440u), __byte_perm(wx, 0x4B000000u, 0x7441u));
+          asm("add.rn.f32x2 %0, %0, %1;" : "+l"(f01) : "l"(0xCB000080CB000080ull));
+          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[0]) : "l"(al2), "l"(f01));
+        }
       }
     }
   }
 }
 
+// evict-first (streaming) stores for outputs that are not re-read by this pass: keep L2 for the
+// gathered int8 table
+__device__ __forceinline__ void st_cs(float* p, float v) { __stcs(p, v); }
+
 // FA: ⑤ H_out = (Σ fmaf(α, q_H′[u])) * s_H′ over (heavy segment | tile of light rows); α is read from
 // the stored (signed) α of the stats passes, so the chunk attributes are two coalesced loads.
 template <int H, int VPL>
-__global__ void __launch_bounds__(256, 2) k_fwd_agg2(const GatFwdArgs a) {
+__global__ void __launch_bounds__(256, 3) k_fwd_agg2(const GatFwdArgs a) {
   constexpr int HD = 32 * VPL;
   constexpr int RING = VPL >= 16 ? 4 : 8;
   __shared__ float sh_a[WPB][32][H];
@@ -624,7 +673,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd_agg2(const GatFwdArgs a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
   const int64_t n = a.g.n_local, hc = load_count(a.plan.counts);
-  const int64_t nitems = hc + (n + TILE - 1) / TILE;
+  const int64_t nitems = hc + load_count(a.plan.counts + 2);
   const int8_t* xbase = a.qHp + lane * VPL;
   float amax_loc = 0.0f;
   uint64_t acc[VPL / 2];
@@ -655,10 +704,11 @@ __global__ void __launch_bounds__(256, 2) k_fwd_agg2(const GatFwdArgs a) {
       for (int k = 0; k < VPL / 2; ++k) unpk(acc[k], dst[2 * k], dst[2 * k + 1]);
       continue;
     }
-    // --------------------------------------------------------------- tile of light rows
-    const int64_t r0 = (item - hc) * TILE;
+    // --------------------------------------------------------------- sub-tile of light rows
+    const int32_t code = a.plan.tiles[item - hc];
+    const int64_t r0 = (int64_t)(code >> 10) * TILE;
     int T;
-    const TileLane L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, n, T);
+    const TileLane L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
     unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
     while (zm) {   // light rows without in-edges: H_out = 0
       const int j = __ffs(zm) - 1;
@@ -677,8 +727,8 @@ __global__ void __launch_bounds__(256, 2) k_fwd_agg2(const GatFwdArgs a) {
         x = __fmul_rn(x, scH.s);
         y = __fmul_rn(y, scH.s);
         amax_loc = fmaxf(amax_loc, fmaxf(fabsf(x), fabsf(y)));
-        dst[2 * k] = x;
-        dst[2 * k + 1] = y;
+        st_cs(dst + 2 * k, x);
+        st_cs(dst + 2 * k + 1, y);
         acc[k] = 0ull;
       }
     };
@@ -1333,7 +1383,7 @@ cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
     ok = true;                                                                                     \
     { ProfScope p("gat_fwd_alpha3", st); k_fwd_alpha3<H_><<<item_grid(a.plan.cap), 256, 0, st>>>(a); } \
     { ProfScope p("gat_fwd_agg", st);                                                              \
-      k_fwd_agg2<H_, V_><<<item_grid(a.plan.cap + (a.g.n_local + TILE - 1) / TILE), 256, 0, st>>>(a); } \
+      k_fwd_agg2<H_, V_><<<item_grid(a.plan.cap + a.plan.tcap), 256, 0, st>>>(a); } \
     { ProfScope p("gat_fwd_combine", st);                                                          \
       k_fwd_combine<H_, V_><<<item_grid(a.g.n_local), 256, 0, st>>>(a); }                           \
   }

@@ -76,10 +76,13 @@ struct PlanDev {
   int32_t* hbase;      // [n_local] first slot of a heavy row, -1 for light rows
   int32_t* hseg_row;   // [cap] local row of each heavy segment slot
   int32_t* hrow;       // [n_local] heavy rows (first counts[1] entries)
-  int32_t* counts;     // [0] = #heavy segments, [1] = #heavy rows (zeroed before k_plan)
+  int32_t* counts;     // [0] = #heavy segments, [1] = #heavy rows, [2] = #light sub-tiles (zeroed first)
   int64_t cap;         // slot capacity: 2 * e / C_E + 1
+  int32_t* tiles;      // [tcap] light-row sub-tiles (block, lo, hi) of k_plan_tiles
+  int64_t tcap;        // n_local + n_local / 32 + 1
 };
 cudaError_t launch_plan(const int64_t* ptr, int64_t n, int chunk, const PlanDev& p, cudaStream_t st);
+cudaError_t launch_plan_tiles(const int64_t* ptr, int64_t n, const PlanDev& p, cudaStream_t st);
 
 struct GatFwdArgs {
   GraphDev g; GatDims d; float slope; int bits;
