@@ -601,24 +601,24 @@ __device__ __forceinline__ uint64_t pkf(float x) {
 __device__ __forceinline__ void unpk(uint64_t v, float& lo, float& hi) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
-// acc2 = fma(al, (float)q[k], acc2) for the 4 codes of one word: PRMT builds 2^23+128+q, FADD2 removes
-// the bias exactly, FFMA2 accumulates (2 instructions per element instead of 3)
-__device__ __forceinline__ void fma4_codes(uint32_t word, uint64_t al2, uint64_t& a01, uint64_t& a23) {
+// acc = fma(al, (float)q[k], acc) for the 4 codes of one word: PRMT builds 2^23+128+q, FADD2 removes
+// the bias exactly, FFMA2 accumulates (sm_100a packed fp32: IEEE rn per half, bit-identical to fmaf)
+__device__ __forceinline__ float2 codes2(uint32_t wx, uint32_t s0, uint32_t s1) {
+  return __fadd2_rn(make_float2(__uint_as_float(__byte_perm(wx, 0x4B000000u, s0)),
+                                __uint_as_float(__byte_perm(wx, 0x4B000000u, s1))),
+                    make_float2(-8388736.0f, -8388736.0f));
+}
+__device__ __forceinline__ void fma4_codes(uint32_t word, float2 al2, float2& a01, float2& a23) {
   const uint32_t wx = word ^ 0x80808080u;
-  const uint64_t bias = 0xCB000080CB000080ull;   // {-8388736.0f, -8388736.0f}
-  uint64_t f01 = pk2(__byte_perm(wx, 0x4B000000u, 0x7440u), __byte_perm(wx, 0x4B000000u, 0x7441u));
-  uint64_t f23 = pk2(__byte_perm(wx, 0x4B000000u, 0x7442u), __byte_perm(wx, 0x4B000000u, 0x7443u));
-  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(f01) : "l"(bias));
-  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(f23) : "l"(bias));
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a01) : "l"(al2), "l"(f01));
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a23) : "l"(al2), "l"(f23));
+  a01 = __ffma2_rn(al2, codes2(wx, 0x7440u, 0x7441u), a01);
+  a23 = __ffma2_rn(al2, codes2(wx, 0x7442u, 0x7443u), a23);
 }
 
 // Streamed aggregation of one 32-edge chunk: rows q_X[w_i] gathered through a rolling ring of RING
 // loads in flight; edge i of the chunk uses weight sa[i][myh] and (if rb) belongs to row rb[i].
 template <int H, int VPL, int RING, typename F>
 __device__ __forceinline__ void agg_chunk(const int8_t* __restrict__ xbase, int64_t ldx, int w_l, int cnt,
-                                          const float (*sa)[H], const int* rb, int& cur, uint64_t (&acc)[VPL / 2],
+                                          const float (*sa)[H], const int* rb, int& cur, float2 (&acc)[VPL / 2],
                                           F&& on_row) {
   constexpr int WORDS = VPL / 4 > 0 ? VPL / 4 : 1;
   const int myh = (threadIdx.x & 31) / (32 / H);
@@ -635,24 +635,22 @@ __device__ __forceinline__ void agg_chunk(const int8_t* __restrict__ xbase, int6
     for (int j = 0; j < RING; ++j) {
       const int i = i0 + j;
       if (i < cnt) {
-        const Row<VPL> r = ring[j];
-        const int nx = i + RING;
-        const int w = __shfl_sync(0xffffffffu, w_l, nx & 31);
-        if (nx < cnt) ring[j] = load_row<VPL>(xbase + (int64_t)w * ldx);
         if (rb) {
           const int ri = rb[i];
           if (ri != cur) { on_row(ri); cur = ri; }
         }
-        const uint64_t al2 = pkf(sa[i][myh]);
+        const float al = sa[i][myh];
+        const float2 al2 = make_float2(al, al);
         if constexpr (VPL >= 4) {
 #pragma unroll
-          for (int q = 0; q < WORDS; ++q) fma4_codes(r.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+          for (int q = 0; q < WORDS; ++q) fma4_codes(ring[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
         } else {   // VPL == 2: two codes in the low half-word
-          const uint32_t wx = r.w[0] ^ 0x80808080u;
-          uint64_t f01 = pk2(__byte_perm(wx, 0x4B000000u, 0x7440u), __byte_perm(wx, 0x4B000000u, 0x7441u));
-          asm("add.rn.f32x2 %0, %0, %1;" : "+l"(f01) : "l"(0xCB000080CB000080ull));
-          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[0]) : "l"(al2), "l"(f01));
+          acc[0] = __ffma2_rn(al2, codes2(ring[j].w[0] ^ 0x80808080u, 0x7440u, 0x7441u), acc[0]);
         }
+        // refill the consumed slot (no register copy of the in-flight row)
+        const int nx = i + RING;
+        const int w = __shfl_sync(0xffffffffu, w_l, nx & 31);
+        if (nx < cnt) ring[j] = load_row<VPL>(xbase + (int64_t)w * ldx);
       }
     }
   }
@@ -676,10 +674,10 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg2(const GatFwdArgs a) {
   const int64_t nitems = hc + load_count(a.plan.counts + 2);
   const int8_t* xbase = a.qHp + lane * VPL;
   float amax_loc = 0.0f;
-  uint64_t acc[VPL / 2];
+  float2 acc[VPL / 2];
   auto zero_acc = [&]() {
 #pragma unroll
-    for (int k = 0; k < VPL / 2; ++k) acc[k] = 0ull;
+    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
   };
   FOR_ITEMS(item, a.work + 2, nitems) {
     zero_acc();
@@ -701,7 +699,7 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg2(const GatFwdArgs a) {
       }
       float* dst = a.hagg + (int64_t)s.slot * HD + lane * VPL;
 #pragma unroll
-      for (int k = 0; k < VPL / 2; ++k) unpk(acc[k], dst[2 * k], dst[2 * k + 1]);
+      for (int k = 0; k < VPL / 2; ++k) { dst[2 * k] = acc[k].x; dst[2 * k + 1] = acc[k].y; }
       continue;
     }
     // --------------------------------------------------------------- sub-tile of light rows
@@ -722,14 +720,11 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg2(const GatFwdArgs a) {
       float* dst = a.Hout + (r0 + j) * HD + lane * VPL;
 #pragma unroll
       for (int k = 0; k < VPL / 2; ++k) {
-        float x, y;
-        unpk(acc[k], x, y);
-        x = __fmul_rn(x, scH.s);
-        y = __fmul_rn(y, scH.s);
+        const float x = __fmul_rn(acc[k].x, scH.s), y = __fmul_rn(acc[k].y, scH.s);
         amax_loc = fmaxf(amax_loc, fmaxf(fabsf(x), fabsf(y)));
         st_cs(dst + 2 * k, x);
         st_cs(dst + 2 * k + 1, y);
-        acc[k] = 0ull;
+        acc[k] = make_float2(0.0f, 0.0f);
       }
     };
     for (int base = 0; base < T; base += 32) {
@@ -751,6 +746,200 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg2(const GatFwdArgs a) {
       __syncwarp();
     }
     if (cur >= 0) flush(cur);
+  }
+  amax_flush(a.amax_out, amax_loc);
+}
+
+
+// ================================================================== cp.async gather engine
+// Each lane copies its own VPL-byte slice of a gathered row into a per-warp shared-memory ring of R
+// rows (cp.async.cg: L2 only, no register held while in flight), waits with cp.async.wait_group and
+// reads back only the bytes it copied itself (no cross-lane synchronisation).  The next 32-edge
+// chunk's indices and α are loaded one chunk ahead so the ring streams across chunk boundaries.
+__device__ __forceinline__ void cp_async_bytes16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_bytes8(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_bytes4(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int VPL>
+__device__ __forceinline__ void cp_row_slice(uint32_t saddr, const int8_t* g) {
+  if constexpr (VPL == 16) cp_async_bytes16(saddr, g);
+  else if constexpr (VPL == 8) cp_async_bytes8(saddr, g);
+  else cp_async_bytes4(saddr, g);
+}
+template <int VPL>
+__device__ __forceinline__ Row<VPL> lds_row_slice(uint32_t saddr) {
+  Row<VPL> r;
+  if constexpr (VPL == 16) {
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]) : "r"(saddr));
+  } else if constexpr (VPL == 8) {
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(r.w[0]), "=r"(r.w[1]) : "r"(saddr));
+  } else {
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r.w[0]) : "r"(saddr));
+  }
+  return r;
+}
+
+constexpr int AGG_RING = 16;
+template <int H, int VPL>
+__host__ __device__ constexpr int agg3_warp_smem() { return AGG_RING * 32 * VPL + 2 * 32 * H * 4 + 2 * 32 * 4; }
+
+// FA (VPL >= 4): ⑤ H_out = (Σ fmaf(α, q_H′[u])) * s_H′ over (heavy segment | light sub-tile)
+template <int H, int VPL>
+__global__ void __launch_bounds__(256, 3) k_fwd_agg3(const GatFwdArgs a) {
+  constexpr int HD = 32 * VPL, R = AGG_RING, RB = 32 * VPL;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int myh = lane / (32 / H);
+  uint8_t* wsm = dsm + w * agg3_warp_smem<H, VPL>();
+  float (*sa)[32][H] = reinterpret_cast<float (*)[32][H]>(wsm + R * RB);
+  int (*srb)[32] = reinterpret_cast<int (*)[32]>(wsm + R * RB + 2 * 32 * H * 4);
+  const uint32_t ring_s = smem_u32(wsm) + lane * VPL;
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const int64_t n = a.g.n_local, hc = load_count(a.plan.counts);
+  const int64_t nitems = hc + load_count(a.plan.counts + 2);
+  const int8_t* xbase = a.qHp + lane * VPL;
+  const uint32_t ld32 = (uint32_t)a.ldHp;
+  float amax_loc = 0.0f;
+  FOR_ITEMS(item, a.work + 2, nitems) {
+    // ---- stream set-up: a heavy segment (one row) or a light sub-tile (rows change)
+    const bool tile = item >= hc;
+    Seg s;
+    TileLane L;
+    int64_t r0 = 0;
+    int T;
+    if (!tile) {
+      decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s);
+      T = (int)(s.ee - s.eb);
+      L.eb = 0; L.off = 0; L.end = 0;
+    } else {
+      const int32_t code = a.plan.tiles[item - hc];
+      r0 = (int64_t)(code >> 10) * TILE;
+      L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
+      unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
+      while (zm) {   // light rows without in-edges: H_out = 0
+        const int j = __ffs(zm) - 1;
+        zm &= zm - 1;
+        float* dst = a.Hout + (r0 + j) * HD + lane * VPL;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) __stcs(dst + k, 0.0f);
+      }
+    }
+    auto attrs = [&](int c, int& u, float (&al)[H], int& row) {
+      const int t = c * 32 + lane;
+      int64_t e;
+      if (tile) {
+        row = tile_row(t, L.end);
+        e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+      } else {
+        row = 0;
+        e = s.eb + t;
+      }
+      u = 0;
+#pragma unroll
+      for (int h = 0; h < H; ++h) al[h] = 0.0f;
+      if (t < T) {
+        u = a.g.in_src[e];
+        if constexpr (H == 4) {
+          const float4 v = *reinterpret_cast<const float4*>(a.alpha + e * 4);
+          al[0] = fabsf(v.x); al[1] = fabsf(v.y); al[2] = fabsf(v.z); al[3] = fabsf(v.w);
+        } else {
+#pragma unroll
+          for (int h = 0; h < H; ++h) al[h] = fabsf(a.alpha[e * H + h]);
+        }
+      }
+    };
+    int uA, rowA;
+    float alA[H];
+    attrs(0, uA, alA, rowA);
+#pragma unroll
+    for (int h = 0; h < H; ++h) sa[0][lane][h] = alA[h];
+    srb[0][lane] = rowA;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {   // ring prologue: edges 0 .. R-1, one commit group per 4 edges
+      const int uu = __shfl_sync(0xffffffffu, uA, j);
+      if (j < T) cp_row_slice<VPL>(ring_s + j * RB, xbase + (uint32_t)uu * ld32);
+      if ((j & 3) == 3) cp_commit();
+    }
+    float2 acc[VPL / 2];
+#pragma unroll
+    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
+    int cur = -1;
+    auto flush = [&](int j) {
+      float* dst = a.Hout + (r0 + j) * HD + lane * VPL;
+#pragma unroll
+      for (int k = 0; k < VPL / 2; ++k) {
+        const float x = __fmul_rn(acc[k].x, scH.s), y = __fmul_rn(acc[k].y, scH.s);
+        amax_loc = fmaxf(amax_loc, fmaxf(fabsf(x), fabsf(y)));
+        __stcs(dst + 2 * k, x);
+        __stcs(dst + 2 * k + 1, y);
+        acc[k] = make_float2(0.0f, 0.0f);
+      }
+    };
+    const int nch = (T + 31) >> 5;
+    for (int c = 0; c < nch; ++c) {
+      int uB, rowB;
+      float alB[H];
+      attrs(c + 1, uB, alB, rowB);   // next chunk, in flight while this chunk streams
+      __syncwarp();
+      const int cb = c & 1;
+      for (int i0 = 0; i0 < 32; i0 += 4) {
+        const int t0 = c * 32 + i0;
+        if (t0 >= T) break;
+        cp_wait<R / 4 - 1>();        // the 4 rows of this group have landed
+        const uint32_t slot0 = ring_s + (uint32_t)(t0 & (R - 1)) * RB;
+        Row<VPL> r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = lds_row_slice<VPL>(slot0 + j * RB);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (t0 + j < T) {
+            if (tile) {
+              const int ri = srb[cb][i0 + j];
+              if (ri != cur) {
+                if (cur >= 0) flush(cur);
+                cur = ri;
+              }
+            }
+            const float al = sa[cb][i0 + j][myh];
+            const float2 al2 = make_float2(al, al);
+#pragma unroll
+            for (int q = 0; q < VPL / 4; ++q) fma4_codes(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {   // refill the 4 consumed slots with edges t0+R .. t0+R+3
+          const int tn = t0 + R + j;
+          const int ua = __shfl_sync(0xffffffffu, uA, tn & 31);
+          const int ub = __shfl_sync(0xffffffffu, uB, tn & 31);
+          const uint32_t un = (uint32_t)(tn < (c + 1) * 32 ? ua : ub);
+          if (tn < T) cp_row_slice<VPL>(slot0 + j * RB, xbase + un * ld32);   // 32-bit offset (N*ld < 2^32)
+        }
+        cp_commit();
+      }
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < H; ++h) sa[cb ^ 1][lane][h] = alB[h];
+      srb[cb ^ 1][lane] = rowB;
+      uA = uB;
+    }
+    cp_wait<0>();
+    __syncwarp();
+    if (tile) {
+      if (cur >= 0) flush(cur);
+    } else {
+      float* dst = a.hagg + (int64_t)s.slot * HD + lane * VPL;
+#pragma unroll
+      for (int k = 0; k < VPL / 2; ++k) { dst[2 * k] = acc[k].x; dst[2 * k + 1] = acc[k].y; }
+    }
   }
   amax_flush(a.amax_out, amax_loc);
 }
@@ -1383,7 +1572,18 @@ cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
     ok = true;                                                                                     \
     { ProfScope p("gat_fwd_alpha3", st); k_fwd_alpha3<H_><<<item_grid(a.plan.cap), 256, 0, st>>>(a); } \
     { ProfScope p("gat_fwd_agg", st);                                                              \
-      k_fwd_agg2<H_, V_><<<item_grid(a.plan.cap + a.plan.tcap), 256, 0, st>>>(a); } \
+      if (V_ >= 4) {                                                                               \
+        constexpr int smem = 8 * agg3_warp_smem<H_, (V_ >= 4 ? V_ : 4)>();                         \
+        static bool attr_set = false;                                                              \
+        if (!attr_set) {                                                                           \
+          cudaFuncSetAttribute(k_fwd_agg3<H_, (V_ >= 4 ? V_ : 4)>,                                 \
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                 \
+          attr_set = true;                                                                         \
+        }                                                                                          \
+        k_fwd_agg3<H_, (V_ >= 4 ? V_ : 4)><<<item_grid(a.plan.cap + a.plan.tcap), 256, smem, st>>>(a); \
+      } else {                                                                                     \
+        k_fwd_agg2<H_, V_><<<item_grid(a.plan.cap + a.plan.tcap), 256, 0, st>>>(a);               \
+      } }                                                                                          \
     { ProfScope p("gat_fwd_combine", st);                                                          \
       k_fwd_combine<H_, V_><<<item_grid(a.g.n_local), 256, 0, st>>>(a); }                           \
   }
