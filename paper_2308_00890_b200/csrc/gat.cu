@@ -944,6 +944,421 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg3(const GatFwdArgs a) {
   amax_flush(a.amax_out, amax_loc);
 }
 
+
+// ================================================================== backward gather kernels (cp.async engine)
+template <int H, int VPL>
+__host__ __device__ constexpr int bwd3_warp_smem() {
+  // ring + α[2][32][H] + (∂α | P[v])[2][32][H] + row[2][32] + edge[2][32] + P-tile[32][H]
+  return AGG_RING * 32 * VPL + 2 * 32 * H * 4 * 2 + 2 * 32 * 4 * 2 + 32 * H * 4;
+}
+
+// exact i8·i8 dot of this lane's slice, reduced over the LPH lanes of its head
+template <int VPL, int LPH>
+__device__ __forceinline__ int head_dot(const Row<VPL>& x, const Row<VPL>& y) {
+  int dot = row_dot<VPL>(x, y);
+#pragma unroll
+  for (int o = 1; o < LPH; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  return dot;
+}
+
+// BD1: ⑤″ ∂α = i2f(q_G[v]·q_H′[u]) (s_G s_H′) (IDP4A on codes), ④′ P = Σ fmaf(∂α, α) per
+// destination row (heavy segments: P partials), then for light rows ∂E_pre and ∂D.
+template <int H, int VPL>
+__global__ void __launch_bounds__(256, 2) k_bwd_dst1_v3(const GatBwdArgs a) {
+  constexpr int HD = 32 * VPL, R = AGG_RING, RB = 32 * VPL, LPH = 32 / H;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int myh = lane / LPH;
+  const bool leader = (lane % LPH) == 0;
+  uint8_t* wsm = dsm + w * bwd3_warp_smem<H, VPL>();
+  float (*sa)[32][H] = reinterpret_cast<float (*)[32][H]>(wsm + R * RB);
+  float (*sd)[32][H] = reinterpret_cast<float (*)[32][H]>(wsm + R * RB + 2 * 32 * H * 4);
+  int (*srb)[32] = reinterpret_cast<int (*)[32]>(wsm + R * RB + 4 * 32 * H * 4);
+  int (*sed)[32] = reinterpret_cast<int (*)[32]>(wsm + R * RB + 4 * 32 * H * 4 + 2 * 32 * 4);
+  float (*pt)[H] = reinterpret_cast<float (*)[H]>(wsm + R * RB + 4 * 32 * H * 4 + 4 * 32 * 4);
+  const uint32_t ring_s = smem_u32(wsm) + lane * VPL;
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
+  const float sGH = __fmul_rn(scG.s, scH.s);
+  const int64_t n = a.g.n_local, hc = load_count(a.pin.counts);
+  const int64_t nitems = hc + load_count(a.pin.counts + 2);
+  const int8_t* xbase = a.qHp + lane * VPL;
+  const int8_t* gbase = a.qG + lane * VPL;
+  const uint32_t ld32 = (uint32_t)a.ldHp;
+  FOR_ITEMS(item, a.work + 0, nitems) {
+    const bool tile = item >= hc;
+    Seg s;
+    TileLane L;
+    int64_t r0 = 0;
+    int T;
+    if (!tile) {
+      decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
+      T = (int)(s.ee - s.eb);
+      L.eb = 0; L.off = 0; L.end = 0; L.deg = 0; L.light = false;
+    } else {
+      const int32_t code = a.pin.tiles[item - hc];
+      r0 = (int64_t)(code >> 10) * TILE;
+      L = tile_setup(a.g.in_ptr, a.pin.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
+      if (L.light && L.deg == 0) {
+        const int64_t vg = a.g.row_begin + L.r;
+#pragma unroll
+        for (int h = 0; h < H; ++h) { a.P[vg * H + h] = 0.0f; a.dD[vg * H + h] = 0.0f; }
+      }
+    }
+    auto attrs = [&](int c, int& u, float (&al)[H], int& row, int& e32) {
+      const int t = c * 32 + lane;
+      int64_t e;
+      if (tile) {
+        row = tile_row(t, L.end);
+        e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+      } else {
+        row = 0;
+        e = s.eb + t;
+      }
+      u = 0;
+      e32 = (int)e;
+#pragma unroll
+      for (int h = 0; h < H; ++h) al[h] = 0.0f;
+      if (t < T) {
+        u = a.g.in_src[e];
+#pragma unroll
+        for (int h = 0; h < H; ++h) al[h] = fabsf(a.alpha[e * H + h]);
+      }
+    };
+    // own q_G[v] slice per row (prefetched one row ahead)
+    const unsigned act = tile ? __ballot_sync(0xffffffffu, L.deg > 0) : 1u;
+    const int64_t vg0 = tile ? a.g.row_begin + r0 : a.g.row_begin + s.vl;
+    int nxt = act ? __ffs(act) - 1 : -1;
+    Row<VPL> gw{}, gw_nxt{};
+    if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
+    int uA, rowA, eA;
+    float alA[H];
+    attrs(0, uA, alA, rowA, eA);
+#pragma unroll
+    for (int h = 0; h < H; ++h) sa[0][lane][h] = alA[h];
+    srb[0][lane] = rowA;
+    sed[0][lane] = eA;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int uu = __shfl_sync(0xffffffffu, uA, j);
+      if (j < T) cp_row_slice<VPL>(ring_s + j * RB, xbase + (uint32_t)uu * ld32);
+      if ((j & 3) == 3) cp_commit();
+    }
+    float P = 0.0f;
+    int cur = -1;
+    const int nch = (T + 31) >> 5;
+    for (int c = 0; c < nch; ++c) {
+      int uB, rowB, eB;
+      float alB[H];
+      attrs(c + 1, uB, alB, rowB, eB);
+      __syncwarp();
+      const int cb = c & 1;
+      for (int i0 = 0; i0 < 32; i0 += 4) {
+        const int t0 = c * 32 + i0;
+        if (t0 >= T) break;
+        cp_wait<R / 4 - 1>();
+        const uint32_t slot0 = ring_s + (uint32_t)(t0 & (R - 1)) * RB;
+        Row<VPL> r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = lds_row_slice<VPL>(slot0 + j * RB);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (t0 + j < T) {
+            const int ri = tile ? srb[cb][i0 + j] : 0;
+            if (ri != cur) {
+              if (cur >= 0 && leader) pt[cur][myh] = P;
+              P = 0.0f;
+              cur = ri;
+              gw = gw_nxt;
+              nxt = tile ? tile_next(act, cur) : -1;
+              if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
+            }
+            const int dot = head_dot<VPL, LPH>(gw, r[j]);
+            if (leader) {
+              const float dal = __fmul_rn(__int2float_rn(dot), sGH);
+              P = __fmaf_rn(dal, sa[cb][i0 + j][myh], P);
+              sd[cb][i0 + j][myh] = dal;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int tn = t0 + R + j;
+          const int ua = __shfl_sync(0xffffffffu, uA, tn & 31);
+          const int ub = __shfl_sync(0xffffffffu, uB, tn & 31);
+          const uint32_t un = (uint32_t)(tn < (c + 1) * 32 ? ua : ub);
+          if (tn < T) cp_row_slice<VPL>(slot0 + j * RB, xbase + un * ld32);
+        }
+        cp_commit();
+      }
+      __syncwarp();
+      if (c * 32 + lane < T) {   // ∂α of this chunk -> scratch (edge-major, coalesced per edge)
+#pragma unroll
+        for (int h = 0; h < H; ++h) a.dalpha[(int64_t)sed[cb][lane] * H + h] = sd[cb][lane][h];
+      }
+#pragma unroll
+      for (int h = 0; h < H; ++h) sa[cb ^ 1][lane][h] = alB[h];
+      srb[cb ^ 1][lane] = rowB;
+      sed[cb ^ 1][lane] = eB;
+      uA = uB;
+      __syncwarp();
+    }
+    cp_wait<0>();
+    __syncwarp();
+    if (!tile) {
+      if (leader) a.hP[(int64_t)s.slot * H + myh] = P;
+      continue;
+    }
+    if (cur >= 0 && leader) pt[cur][myh] = P;
+    __syncwarp();
+    // ---- pass 2 (light rows): ∂E = α(∂α − P[v]), ∂E_pre, ∂D = Σ ∂E_pre (lane j sums row j)
+    float dDp[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) dDp[h] = 0.0f;
+    for (int base = 0; base < T; base += 32) {
+      const int cnt = T - base < 32 ? T - base : 32;
+      const int t = base + lane;
+      const int row = tile_row(t, L.end);
+      const int64_t e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+      if (lane < cnt) {
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const float x = a.alpha[e * H + h];
+          const float dE = __fmul_rn(fabsf(x), __fsub_rn(a.dalpha[e * H + h], pt[row][h]));
+          sd[0][lane][h] = signbit(x) ? __fmul_rn(dE, a.slope) : dE;
+        }
+      }
+      __syncwarp();
+      const int lo = (L.off > base ? L.off : base) - base;
+      const int hi = (L.end < base + cnt ? L.end : base + cnt) - base;
+      for (int i = lo; i < hi; ++i)
+#pragma unroll
+        for (int h = 0; h < H; ++h) dDp[h] = __fadd_rn(dDp[h], sd[0][i][h]);
+      __syncwarp();
+    }
+    if (L.deg > 0) {
+      const int64_t vg = a.g.row_begin + L.r;
+#pragma unroll
+      for (int h = 0; h < H; ++h) { a.P[vg * H + h] = pt[lane][h]; a.dD[vg * H + h] = dDp[h]; }
+    }
+    __syncwarp();
+  }
+}
+
+// ②′ finalize of source row u (full row): ∂H′ = (agg·s_G + ∂S·a_src) + ∂D·a_dst ; ∂S stored
+template <int VPL>
+__device__ __forceinline__ void src_finalize_full(const GatBwdArgs& a, int64_t ul, int64_t ug, int myh, int H,
+                                                  float dS, float2 (&acc)[VPL / 2], float sG, float& amax_loc) {
+  constexpr int HD = 32 * VPL;
+  const int lane = threadIdx.x & 31;
+  const float dD = a.dD[ug * H + myh];
+  const int c0 = lane * VPL;
+  float* dst = a.dHp + ul * HD + c0;
+#pragma unroll
+  for (int k = 0; k < VPL / 2; ++k) {
+    float v2[2] = {acc[k].x, acc[k].y};
+#pragma unroll
+    for (int z = 0; z < 2; ++z) {
+      const int col = c0 + 2 * k + z;
+      const float agg = __fmul_rn(v2[z], sG);
+      const float t2 = __fadd_rn(agg, __fmul_rn(dS, __ldg(a.a_src + col)));
+      const float o = __fadd_rn(t2, __fmul_rn(dD, __ldg(a.a_dst + col)));
+      amax_loc = fmaxf(amax_loc, fabsf(o));
+      dst[2 * k + z] = o;
+    }
+    acc[k] = make_float2(0.0f, 0.0f);
+  }
+  if ((lane % (32 / H)) == 0) a.dS[ug * H + myh] = dS;
+}
+
+// BS: ⑤′ ∂H′_agg = Σ fmaf(α, q_G[v]) over out-edges, ③′ ∂S = Σ ∂E_pre, ②′ finalize (light rows);
+// heavy out-segments leave ∂S / aggregation partials.  α comes from the stored signed α via out_eid
+// when available (one GPU), otherwise it is recomputed from per-node data.
+template <int H, int VPL>
+__global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
+  constexpr int HD = 32 * VPL, R = AGG_RING, RB = 32 * VPL, LPH = 32 / H;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int myh = lane / LPH;
+  const bool leader = (lane % LPH) == 0;
+  uint8_t* wsm = dsm + w * bwd3_warp_smem<H, VPL>();
+  float (*sa)[32][H] = reinterpret_cast<float (*)[32][H]>(wsm + R * RB);                 // signed α
+  float (*sp)[32][H] = reinterpret_cast<float (*)[32][H]>(wsm + R * RB + 2 * 32 * H * 4);  // P[v]
+  int (*srb)[32] = reinterpret_cast<int (*)[32]>(wsm + R * RB + 4 * 32 * H * 4);
+  const uint32_t ring_s = smem_u32(wsm) + lane * VPL;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
+  const float sGH = __fmul_rn(scG.s, scH.s);
+  const int64_t n = a.g.n_local, hc = load_count(a.pout.counts);
+  const int64_t nitems = hc + load_count(a.pout.counts + 2);
+  const int8_t* gbase = a.qG + lane * VPL;
+  const int8_t* hbase = a.qHp + lane * VPL;
+  const uint32_t ld32 = (uint32_t)a.ldG;
+  const bool use_eid = a.g.out_eid != nullptr;
+  float amax_loc = 0.0f;
+  FOR_ITEMS(item, a.work + 2, nitems) {
+    const bool tile = item >= hc;
+    Seg s;
+    TileLane L;
+    int64_t r0 = 0;
+    int T;
+    if (!tile) {
+      decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
+      T = (int)(s.ee - s.eb);
+      L.eb = 0; L.off = 0; L.end = 0; L.deg = 0; L.light = false;
+      r0 = s.vl;
+    } else {
+      const int32_t code = a.pout.tiles[item - hc];
+      r0 = (int64_t)(code >> 10) * TILE;
+      L = tile_setup(a.g.out_ptr, a.pout.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
+    }
+    const int64_t ug0 = a.g.row_begin + r0;
+    int qsj[H];   // own q_S of lane j's row (recompute path)
+#pragma unroll
+    for (int h = 0; h < H; ++h) qsj[h] = (!use_eid && (tile ? L.deg > 0 : lane == 0)) ? (int)a.qS[(ug0 + lane) * H + h] : 0;
+    float2 acc[VPL / 2];
+#pragma unroll
+    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
+    if (tile) {
+      unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
+      while (zm) {   // light rows without out-edges: ∂H′ = (0 + 0·a_src) + ∂D·a_dst
+        const int j = __ffs(zm) - 1;
+        zm &= zm - 1;
+        src_finalize_full<VPL>(a, r0 + j, ug0 + j, myh, H, 0.0f, acc, scG.s, amax_loc);
+      }
+    }
+    auto attrs = [&](int c, int& v, float (&al)[H], float (&pv)[H], int& row) {
+      const int t = c * 32 + lane;
+      int64_t e;
+      if (tile) {
+        row = tile_row(t, L.end);
+        e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+      } else {
+        row = 0;
+        e = s.eb + t;
+      }
+      int qsr[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) qsr[h] = __shfl_sync(0xffffffffu, qsj[h], row);
+      v = 0;
+#pragma unroll
+      for (int h = 0; h < H; ++h) { al[h] = 0.0f; pv[h] = 0.0f; }
+      if (t < T) {
+        v = a.g.out_dst[e];
+        if (use_eid) {
+          const int64_t eid = a.g.out_eid[e];
+#pragma unroll
+          for (int h = 0; h < H; ++h) al[h] = a.alpha[eid * H + h];
+        } else {
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            const int64_t k = (int64_t)v * H + h;
+            const float ep = sddmm_add1((int8_t)qsr[h], scS.s, a.qD[k], scD.s);
+            const float al_ = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), a.m[k])), a.den[k]);
+            al[h] = ep > 0.0f ? al_ : -al_;
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < H; ++h) pv[h] = a.P[(int64_t)v * H + h];
+      }
+    };
+    const unsigned act = tile ? __ballot_sync(0xffffffffu, L.deg > 0) : 1u;
+    int nxt = act ? __ffs(act) - 1 : -1;
+    Row<VPL> hw{}, hw_nxt{};
+    if (nxt >= 0) hw_nxt = load_row<VPL>(hbase + (ug0 + nxt) * a.ldHp);
+    int vA, rowA;
+    float alA[H], pA[H];
+    attrs(0, vA, alA, pA, rowA);
+#pragma unroll
+    for (int h = 0; h < H; ++h) { sa[0][lane][h] = alA[h]; sp[0][lane][h] = pA[h]; }
+    srb[0][lane] = rowA;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int vv = __shfl_sync(0xffffffffu, vA, j);
+      if (j < T) cp_row_slice<VPL>(ring_s + j * RB, gbase + (uint32_t)vv * ld32);
+      if ((j & 3) == 3) cp_commit();
+    }
+    float dS = 0.0f;
+    int cur = -1;
+    const int nch = (T + 31) >> 5;
+    for (int c = 0; c < nch; ++c) {
+      int vB, rowB;
+      float alB[H], pB[H];
+      attrs(c + 1, vB, alB, pB, rowB);
+      __syncwarp();
+      const int cb = c & 1;
+      for (int i0 = 0; i0 < 32; i0 += 4) {
+        const int t0 = c * 32 + i0;
+        if (t0 >= T) break;
+        cp_wait<R / 4 - 1>();
+        const uint32_t slot0 = ring_s + (uint32_t)(t0 & (R - 1)) * RB;
+        Row<VPL> r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = lds_row_slice<VPL>(slot0 + j * RB);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (t0 + j < T) {
+            const int ri = tile ? srb[cb][i0 + j] : 0;
+            if (ri != cur) {
+              if (cur >= 0) {
+                const float dSb = __shfl_sync(0xffffffffu, dS, myh * LPH);
+                src_finalize_full<VPL>(a, r0 + cur, ug0 + cur, myh, H, dSb, acc, scG.s, amax_loc);
+                dS = 0.0f;
+              }
+              cur = ri;
+              hw = hw_nxt;
+              nxt = tile ? tile_next(act, cur) : -1;
+              if (nxt >= 0) hw_nxt = load_row<VPL>(hbase + (ug0 + nxt) * a.ldHp);
+            }
+            const int dot = head_dot<VPL, LPH>(r[j], hw);
+            const float x = sa[cb][i0 + j][myh];
+            const float al = fabsf(x);
+            if (leader) {
+              const float dal = __fmul_rn(__int2float_rn(dot), sGH);
+              const float dE = __fmul_rn(al, __fsub_rn(dal, sp[cb][i0 + j][myh]));
+              dS = __fadd_rn(dS, signbit(x) ? __fmul_rn(dE, a.slope) : dE);
+            }
+            const float2 al2 = make_float2(al, al);
+#pragma unroll
+            for (int q = 0; q < VPL / 4; ++q) fma4_codes(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int tn = t0 + R + j;
+          const int va = __shfl_sync(0xffffffffu, vA, tn & 31);
+          const int vb = __shfl_sync(0xffffffffu, vB, tn & 31);
+          const uint32_t vn = (uint32_t)(tn < (c + 1) * 32 ? va : vb);
+          if (tn < T) cp_row_slice<VPL>(slot0 + j * RB, gbase + vn * ld32);
+        }
+        cp_commit();
+      }
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < H; ++h) { sa[cb ^ 1][lane][h] = alB[h]; sp[cb ^ 1][lane][h] = pB[h]; }
+      srb[cb ^ 1][lane] = rowB;
+      vA = vB;
+      __syncwarp();
+    }
+    cp_wait<0>();
+    __syncwarp();
+    if (!tile) {
+      if (leader) a.hdS[(int64_t)s.slot * H + myh] = dS;
+      float* dst = a.hagg + (int64_t)s.slot * HD + lane * VPL;
+#pragma unroll
+      for (int k = 0; k < VPL / 2; ++k) { dst[2 * k] = acc[k].x; dst[2 * k + 1] = acc[k].y; }
+      continue;
+    }
+    if (cur >= 0) {
+      const float dSb = __shfl_sync(0xffffffffu, dS, myh * LPH);
+      src_finalize_full<VPL>(a, r0 + cur, ug0 + cur, myh, H, dSb, acc, scG.s, amax_loc);
+    }
+  }
+  amax_flush(a.amax_dHp, amax_loc);
+}
+
 // ---- BD1: ⑤″ ∂α (IDP4A on codes) + ④′ P (+ ∂E_pre, ∂D for light rows) per (tile | segment, group)
 template <int VPL, int HPW>
 __device__ __forceinline__ int cg_dot(const Row<VPL>& x, const Row<VPL>& y) {
@@ -1598,17 +2013,35 @@ cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st) {
   if (!cg_shape(a.d.head_dim, vpl, hpw)) return cudaErrorInvalidValue;
   const int64_t cg_items = (a.pin.cap + (a.g.n_local + TILE - 1) / TILE) * (a.d.hd / (32 * vpl));
   bool ok = false;
-#define X(V_, P_)                                                                                  \
-  if (vpl == V_ && hpw == P_) {                                                                    \
-    ok = true;                                                                                     \
-    ProfScope p("gat_bwd_dst1", st);                                                               \
-    k_bwd_dst1_cg<V_, P_><<<item_grid(cg_items), 256, 0, st>>>(a);                                  \
-  }
-  TANGO_CG_CASES(X)
+  const int hv = a.d.heads * 100 + a.d.hd / 32;
+  if (a.d.hd / 32 >= 4) {
+#define X(H_, V_)                                                                                  \
+    if (hv == H_ * 100 + V_ && V_ >= 4) {                                                          \
+      ok = true;                                                                                   \
+      constexpr int VV = V_ >= 4 ? V_ : 4;                                                          \
+      constexpr int smem = 8 * bwd3_warp_smem<H_, VV>();                                           \
+      static bool attr_set = false;                                                                \
+      if (!attr_set) {                                                                             \
+        cudaFuncSetAttribute(k_bwd_dst1_v3<H_, VV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        attr_set = true;                                                                           \
+      }                                                                                            \
+      ProfScope p("gat_bwd_dst1", st);                                                             \
+      k_bwd_dst1_v3<H_, VV><<<item_grid(a.pin.cap + a.pin.tcap), 256, smem, st>>>(a);              \
+    }
+    TANGO_HV_CASES(X)
 #undef X
+  } else {
+#define X(V_, P_)                                                                                  \
+    if (vpl == V_ && hpw == P_) {                                                                  \
+      ok = true;                                                                                   \
+      ProfScope p("gat_bwd_dst1", st);                                                             \
+      k_bwd_dst1_cg<V_, P_><<<item_grid(cg_items), 256, 0, st>>>(a);                                \
+    }
+    TANGO_CG_CASES(X)
+#undef X
+  }
   if (!ok) return cudaErrorInvalidValue;
   ok = false;
-  const int hv = a.d.heads * 100 + a.d.hd / 32;
 #define X(H_, V_)                                                                                  \
   if (hv == H_ * 100 + V_) {                                                                       \
     ok = true;                                                                                     \
@@ -1628,17 +2061,35 @@ cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st) {
   if (!cg_shape(a.d.head_dim, vpl, hpw)) return cudaErrorInvalidValue;
   const int64_t cg_items = (a.pout.cap + (a.g.n_local + TILE - 1) / TILE) * (a.d.hd / (32 * vpl));
   bool ok = false;
-#define X(V_, P_)                                                                                  \
-  if (vpl == V_ && hpw == P_) {                                                                    \
-    ok = true;                                                                                     \
-    ProfScope p("gat_bwd_src", st);                                                                \
-    k_bwd_src_cg<V_, P_><<<item_grid(cg_items), 256, 0, st>>>(a);                                   \
-  }
-  TANGO_CG_CASES(X)
+  const int hv = a.d.heads * 100 + a.d.hd / 32;
+  if (a.d.hd / 32 >= 4) {
+#define X(H_, V_)                                                                                  \
+    if (hv == H_ * 100 + V_ && V_ >= 4) {                                                          \
+      ok = true;                                                                                   \
+      constexpr int VV = V_ >= 4 ? V_ : 4;                                                          \
+      constexpr int smem = 8 * bwd3_warp_smem<H_, VV>();                                           \
+      static bool attr_set = false;                                                                \
+      if (!attr_set) {                                                                             \
+        cudaFuncSetAttribute(k_bwd_src_v3<H_, VV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        attr_set = true;                                                                           \
+      }                                                                                            \
+      ProfScope p("gat_bwd_src", st);                                                              \
+      k_bwd_src_v3<H_, VV><<<item_grid(a.pout.cap + a.pout.tcap), 256, smem, st>>>(a);             \
+    }
+    TANGO_HV_CASES(X)
 #undef X
+  } else {
+#define X(V_, P_)                                                                                  \
+    if (vpl == V_ && hpw == P_) {                                                                  \
+      ok = true;                                                                                   \
+      ProfScope p("gat_bwd_src", st);                                                              \
+      k_bwd_src_cg<V_, P_><<<item_grid(cg_items), 256, 0, st>>>(a);                                 \
+    }
+    TANGO_CG_CASES(X)
+#undef X
+  }
   if (!ok) return cudaErrorInvalidValue;
   ok = false;
-  const int hv = a.d.heads * 100 + a.d.hd / 32;
 #define X(H_, V_)                                                                                  \
   if (hv == H_ * 100 + V_) {                                                                       \
     ok = true;                                                                                     \
