@@ -1125,7 +1125,9 @@ __global__ void __launch_bounds__(256, 2) k_bwd_dst1_v3(const GatBwdArgs a) {
         for (int h = 0; h < H; ++h) {
           const float x = a.alpha[e * H + h];
           const float dE = __fmul_rn(fabsf(x), __fsub_rn(a.dalpha[e * H + h], pt[row][h]));
-          sd[0][lane][h] = signbit(x) ? __fmul_rn(dE, a.slope) : dE;
+          const float dEp = signbit(x) ? __fmul_rn(dE, a.slope) : dE;
+          sd[0][lane][h] = dEp;
+          a.dalpha[e * H + h] = dEp;   // the scratch now holds ∂E_pre (read by the source pass)
         }
       }
       __syncwarp();
@@ -1247,10 +1249,10 @@ __global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
       for (int h = 0; h < H; ++h) { al[h] = 0.0f; pv[h] = 0.0f; }
       if (t < T) {
         v = a.g.out_dst[e];
-        if (use_eid) {
+        if (use_eid) {   // one GPU: α and ∂E_pre of the destination-side passes, by in-CSR edge id
           const int64_t eid = a.g.out_eid[e];
 #pragma unroll
-          for (int h = 0; h < H; ++h) al[h] = a.alpha[eid * H + h];
+          for (int h = 0; h < H; ++h) { al[h] = a.alpha[eid * H + h]; pv[h] = a.dalpha[eid * H + h]; }
         } else {
 #pragma unroll
           for (int h = 0; h < H; ++h) {
@@ -1260,8 +1262,10 @@ __global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
             al[h] = ep > 0.0f ? al_ : -al_;
           }
         }
+        if (!use_eid) {
 #pragma unroll
-        for (int h = 0; h < H; ++h) pv[h] = a.P[(int64_t)v * H + h];
+          for (int h = 0; h < H; ++h) pv[h] = a.P[(int64_t)v * H + h];
+        }
       }
     };
     const unsigned act = tile ? __ballot_sync(0xffffffffu, L.deg > 0) : 1u;
@@ -1312,13 +1316,17 @@ __global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
               nxt = tile ? tile_next(act, cur) : -1;
               if (nxt >= 0) hw_nxt = load_row<VPL>(hbase + (ug0 + nxt) * a.ldHp);
             }
-            const int dot = head_dot<VPL, LPH>(r[j], hw);
             const float x = sa[cb][i0 + j][myh];
             const float al = fabsf(x);
-            if (leader) {
-              const float dal = __fmul_rn(__int2float_rn(dot), sGH);
-              const float dE = __fmul_rn(al, __fsub_rn(dal, sp[cb][i0 + j][myh]));
-              dS = __fadd_rn(dS, signbit(x) ? __fmul_rn(dE, a.slope) : dE);
+            if (use_eid) {   // ∂E_pre read from the destination pass
+              if (leader) dS = __fadd_rn(dS, sp[cb][i0 + j][myh]);
+            } else {         // recompute ∂α = q_G[v]·q_H′[u] and ∂E_pre (partitioned graphs)
+              const int dot = head_dot<VPL, LPH>(r[j], hw);
+              if (leader) {
+                const float dal = __fmul_rn(__int2float_rn(dot), sGH);
+                const float dE = __fmul_rn(al, __fsub_rn(dal, sp[cb][i0 + j][myh]));
+                dS = __fadd_rn(dS, signbit(x) ? __fmul_rn(dE, a.slope) : dE);
+              }
             }
             const float2 al2 = make_float2(al, al);
 #pragma unroll
@@ -1553,6 +1561,7 @@ __global__ void __launch_bounds__(256) k_bwd_dst1_cg(const GatBwdArgs a) {
           const float al = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), mr[k])), dr[k]);
           const float dE = __fmul_rn(al, __fsub_rn(a.dalpha[e * H + h0 + k], sh_pt[w][row][k]));
           ba[lane][k] = ep > 0.0f ? dE : __fmul_rn(dE, a.slope);
+          a.dalpha[e * H + h0 + k] = ba[lane][k];   // scratch now holds ∂E_pre
         }
       }
       __syncwarp();
@@ -1808,6 +1817,7 @@ __device__ __forceinline__ float bwd_dst_pass2(const GatBwdArgs& a, const Seg& s
         const float al = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), mh[h])), dh[h]);
         const float dE = __fmul_rn(al, __fsub_rn(a.dalpha[e * H + h], P[h]));
         ba[lane][h] = ep > 0.0f ? dE : __fmul_rn(dE, a.slope);
+        a.dalpha[e * H + h] = ba[lane][h];   // scratch now holds ∂E_pre
       }
     }
     __syncwarp();

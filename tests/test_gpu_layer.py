@@ -99,7 +99,8 @@ def test_gat_layer_parity(T, orc, case):
     eq("amax_out", amax_out, f["amax_out"])
     # backward: B1-B9
     eq("qG", bv["qG"], b["qG"])
-    eq("dalpha", bv["dalpha"], b["dalpha"])
+    # the edge scratch holds ∂α after the dst pass-1 and ∂E_pre (B3) at the end of the backward
+    eq("dE_pre", bv["dalpha"], b["dE_pre"])
     eq("P", bv["P"], b["P"])
     eq("dD", bv["dD"], b["dD"])
     eq("dHp", bv["dHp"], b["dHp"])
