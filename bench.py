@@ -93,22 +93,22 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------------- roofline model
 def kernel_model(name, g_e, n, F, H, HD, peaks, clock_mhz):
-    """Algorithmic bytes and ALU ops per launch of a kernel."""
+    """Algorithmic bytes and ALU lane-ops per launch of a kernel.
+
+    Bytes count each gathered int8 row once per edge (no cache reuse assumed), every per-edge
+    attribute and every per-row output once.  ALU ops count 2 lane-ops per gathered element for the
+    exact int8->fp32 convert + FMA (aggregations) and 1/4 per element for the IDP4A dots.
+    """
     E = g_e
-    if name == "gat_fwd_dst":
-        # per edge: src index + q_S[u] + q_H'[u] row; per node: q_D, H_out row, m, den
-        byts = E * (4 + H + HD) + n * (8 + H + 4 * HD + 8 * H)
-        ops = 2 * E * HD            # int8->fp32 convert + FMA per gathered element
-    elif name == "gat_bwd_dst":
-        byts = E * (4 + H + HD) + n * (8 + HD + H + 8 * H + 8 * H)
-        ops = 2 * E * HD            # IDP4A dot: 1 op per 4 elements x 2 (load/convert-free) -> 0.5 ; counted as 2 conservatively
-    elif name == "gat_bwd_src":
-        byts = E * (4 + HD + 13 * H) + n * (8 + HD + H + 4 * H + 4 * HD)
+    if name == "gat_fwd_agg":        # ⑤: index + stored α + q_H′[u] row per edge; H_out row per node
+        byts = E * (4 + 4 * H + HD) + n * (8 + 4 * HD)
         ops = 2 * E * HD
-    elif name.startswith("gemm"):
-        return None
-    elif name == "quantize":
-        return None
+    elif name == "gat_bwd_dst1":     # ⑤″+④′: index + α + q_H′[u] row + ∂α/∂E_pre scratch; q_G[v] row, P, ∂D
+        byts = E * (4 + 4 * H + HD + 12 * H) + n * (8 + HD + 8 * H)
+        ops = E * HD // 4
+    elif name == "gat_bwd_src":      # ⑤′+③′+②′: dst index + eid + α + ∂E_pre + q_G[v] row; ∂H′ row per node
+        byts = E * (8 + 8 * H + HD) + n * (8 + 4 * HD + 8 * H)
+        ops = 2 * E * HD
     else:
         return None
     alu_peak = 148 * 128 * clock_mhz * 1e6   # FP32 lanes x clock (lane-ops/s)

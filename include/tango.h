@@ -222,7 +222,8 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
 typedef struct {
   int8_t *qH, *qW, *qWt, *qHp, *qS, *qD, *qG, *qdHp;
   int64_t ldF, ldHD, ldFt;
-  float *S, *D, *m, *den, *P, *dD, *dHp, *dalpha;   /* dalpha: [e_in][H] scratch, holds ∂E_pre after bwd */
+  float *S, *D, *m, *den, *P, *dD, *dHp, *dalpha;   /* dalpha: [e_in][H] ∂α */
+  float *alpha_pack;       /* [e_in][2H]: α (sign bit = LeakyReLU branch of e_pre) | ∂E_pre */
   float *scalars;          /* see DESIGN.md §4 "ctx scalars" for the slot map */
 } tango_gat_ctx_view;
 tango_status tango_gat_ctx_get_view(const tango_graph* G, const tango_gat_params* p, void* ctx,

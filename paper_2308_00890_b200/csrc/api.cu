@@ -382,7 +382,7 @@ GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   L.off_hagg = take((size_t)(L.cap_in > L.cap_out ? L.cap_in : L.cap_out) * L.HD * 4);
   L.off_work = take(64);
   L.off_dS = take((size_t)L.N * L.H * 4);
-  L.off_alpha = take((size_t)L.E * L.H * 4);
+  L.off_alpha = take((size_t)L.E * L.H * 8);     // [E][2H]: α | ∂E_pre
   L.tcap = L.n + L.n / 32 + 1;
   L.off_pin_tiles = take((size_t)L.tcap * 4);
   L.off_pout_tiles = take((size_t)L.tcap * 4);
@@ -433,6 +433,7 @@ tango_status tango_gat_ctx_get_view(const tango_graph* G, const tango_gat_params
   v->S = (float*)(c + L.off_S); v->D = (float*)(c + L.off_D); v->m = (float*)(c + L.off_m);
   v->den = (float*)(c + L.off_den); v->P = (float*)(c + L.off_P); v->dD = (float*)(c + L.off_dD);
   v->dHp = (float*)(c + L.off_dHp); v->dalpha = (float*)(c + L.off_dal);
+  v->alpha_pack = (float*)(c + L.off_alpha);
   v->scalars = (float*)(c + L.off_scal);
   return TANGO_OK;
 }
@@ -594,6 +595,7 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   ba.work = (int32_t*)(c + L.off_work);
   ba.dS = (float*)(c + L.off_dS);
   ba.alpha = (const float*)(c + L.off_alpha);
+  ba.alpha_dE = (float*)(c + L.off_alpha);
   TRY_CUDA(cudaMemsetAsync(ba.work, 0, 64, st));
   TRY(launch_status(launch_gat_bwd_dst(ba, st)));
   TRY(comm_gather_rows(comm, P, (size_t)L.H * 4, st));

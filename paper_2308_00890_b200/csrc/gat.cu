@@ -174,7 +174,7 @@ __device__ __forceinline__ float seg_sum_exp(const int32_t* __restrict__ src, in
         const float ep = sddmm_add1(qS[u * H + h], sS, qd[h], sD);
         const float ex = exp_p(__fsub_rn(lrelu(ep, slope), mx[h]));
         buf[lane][h] = ex;
-        if (sx) sx[(base + lane) * H + h] = ep > 0.0f ? ex : -ex;
+        if (sx) sx[(base + lane) * 2 * H + h] = ep > 0.0f ? ex : -ex;
       }
     }
     __syncwarp();
@@ -331,9 +331,9 @@ __global__ void __launch_bounds__(256) k_fwd_stats(const GatFwdArgs a) {
     for (int64_t e = s.eb + lane; e < s.ee; e += 32)
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        const float x = a.alpha[e * H + h];
+        const float x = a.alpha[e * 2 * H + h];
         const float al = __fdiv_rn(fabsf(x), dh[h]);
-        a.alpha[e * H + h] = x < 0.0f || (x == 0.0f && signbit(x)) ? -al : al;
+        a.alpha[e * 2 * H + h] = signbit(x) ? -al : al;
       }
   }
 }
@@ -373,9 +373,9 @@ __global__ void __launch_bounds__(256) k_fwd_alpha3(const GatFwdArgs a) {
     for (int64_t e = s.eb + lane; e < s.ee; e += 32)
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        const float x = a.alpha[e * H + h];
+        const float x = a.alpha[e * 2 * H + h];
         const float al = __fdiv_rn(fabsf(x), den[h]);
-        a.alpha[e * H + h] = x < 0.0f || (x == 0.0f && signbit(x)) ? -al : al;
+        a.alpha[e * 2 * H + h] = signbit(x) ? -al : al;
       }
   }
 }
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg2(const GatFwdArgs a) {
         if (lane < cnt) {
           u = a.g.in_src[base + lane];
 #pragma unroll
-          for (int h = 0; h < H; ++h) sh_a[w][lane][h] = fabsf(a.alpha[(base + lane) * H + h]);
+          for (int h = 0; h < H; ++h) sh_a[w][lane][h] = fabsf(a.alpha[(base + lane) * 2 * H + h]);
         }
         __syncwarp();
         agg_chunk<H, VPL, RING>(xbase, a.ldHp, u, cnt, sh_a[w], nullptr, cur, acc, [](int) {});
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg2(const GatFwdArgs a) {
       if (lane < cnt) {
         u = a.g.in_src[e];
 #pragma unroll
-        for (int h = 0; h < H; ++h) sh_a[w][lane][h] = fabsf(a.alpha[e * H + h]);
+        for (int h = 0; h < H; ++h) sh_a[w][lane][h] = fabsf(a.alpha[e * 2 * H + h]);
         sh_rb[w][lane] = row;
       }
       __syncwarp();
@@ -849,11 +849,11 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg3(const GatFwdArgs a) {
       if (t < T) {
         u = a.g.in_src[e];
         if constexpr (H == 4) {
-          const float4 v = *reinterpret_cast<const float4*>(a.alpha + e * 4);
+          const float4 v = *reinterpret_cast<const float4*>(a.alpha + e * 8);
           al[0] = fabsf(v.x); al[1] = fabsf(v.y); al[2] = fabsf(v.z); al[3] = fabsf(v.w);
         } else {
 #pragma unroll
-          for (int h = 0; h < H; ++h) al[h] = fabsf(a.alpha[e * H + h]);
+          for (int h = 0; h < H; ++h) al[h] = fabsf(a.alpha[e * 2 * H + h]);
         }
       }
     };
@@ -1022,7 +1022,7 @@ __global__ void __launch_bounds__(256, 2) k_bwd_dst1_v3(const GatBwdArgs a) {
       if (t < T) {
         u = a.g.in_src[e];
 #pragma unroll
-        for (int h = 0; h < H; ++h) al[h] = fabsf(a.alpha[e * H + h]);
+        for (int h = 0; h < H; ++h) al[h] = fabsf(a.alpha[e * 2 * H + h]);
       }
     };
     // own q_G[v] slice per row (prefetched one row ahead)
@@ -1123,11 +1123,11 @@ __global__ void __launch_bounds__(256, 2) k_bwd_dst1_v3(const GatBwdArgs a) {
       if (lane < cnt) {
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-          const float x = a.alpha[e * H + h];
+          const float x = a.alpha[e * 2 * H + h];
           const float dE = __fmul_rn(fabsf(x), __fsub_rn(a.dalpha[e * H + h], pt[row][h]));
           const float dEp = signbit(x) ? __fmul_rn(dE, a.slope) : dE;
           sd[0][lane][h] = dEp;
-          a.dalpha[e * H + h] = dEp;   // the scratch now holds ∂E_pre (read by the source pass)
+          a.alpha_dE[e * 2 * H + H + h] = dEp;   // ∂E_pre beside α (one sector per edge for the source pass)
         }
       }
       __syncwarp();
@@ -1252,7 +1252,7 @@ __global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
         if (use_eid) {   // one GPU: α and ∂E_pre of the destination-side passes, by in-CSR edge id
           const int64_t eid = a.g.out_eid[e];
 #pragma unroll
-          for (int h = 0; h < H; ++h) { al[h] = a.alpha[eid * H + h]; pv[h] = a.dalpha[eid * H + h]; }
+          for (int h = 0; h < H; ++h) { al[h] = a.alpha[eid * 2 * H + h]; pv[h] = a.alpha[eid * 2 * H + H + h]; }
         } else {
 #pragma unroll
           for (int h = 0; h < H; ++h) {
@@ -1561,7 +1561,7 @@ __global__ void __launch_bounds__(256) k_bwd_dst1_cg(const GatBwdArgs a) {
           const float al = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), mr[k])), dr[k]);
           const float dE = __fmul_rn(al, __fsub_rn(a.dalpha[e * H + h0 + k], sh_pt[w][row][k]));
           ba[lane][k] = ep > 0.0f ? dE : __fmul_rn(dE, a.slope);
-          a.dalpha[e * H + h0 + k] = ba[lane][k];   // scratch now holds ∂E_pre
+          a.alpha_dE[e * 2 * H + H + h0 + k] = ba[lane][k];   // ∂E_pre beside α
         }
       }
       __syncwarp();
@@ -1817,7 +1817,7 @@ __device__ __forceinline__ float bwd_dst_pass2(const GatBwdArgs& a, const Seg& s
         const float al = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), mh[h])), dh[h]);
         const float dE = __fmul_rn(al, __fsub_rn(a.dalpha[e * H + h], P[h]));
         ba[lane][h] = ep > 0.0f ? dE : __fmul_rn(dE, a.slope);
-        a.dalpha[e * H + h] = ba[lane][h];   // scratch now holds ∂E_pre
+        a.alpha_dE[e * 2 * H + H + h] = ba[lane][h];   // ∂E_pre beside α
       }
     }
     __syncwarp();

@@ -95,7 +95,7 @@ struct GatFwdArgs {
   float* hmax; float* hden;                   // [cap][H] heavy-segment softmax partials
   float* hagg;                                // [cap][HD] heavy-segment aggregation partials
   int32_t* work;                              // [8] work-queue counters (zeroed before the launch)
-  float* alpha;                               // [e_in][H] α with the sign of e_pre (LeakyReLU branch)
+  float* alpha;                               // [e_in][2H]: α with the sign of e_pre (LeakyReLU branch) | ∂E_pre
 };
 cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st);
 
@@ -117,7 +117,8 @@ struct GatBwdArgs {
   float* hdS;                                // [pout.cap][H]
   float* hagg;                               // [pout.cap][HD]
   int32_t* work;                             // [8] work-queue counters (zeroed before the launch)
-  const float* alpha;                        // [e_in][H] signed α from the forward
+  const float* alpha;                        // [e_in][2H]: signed α from the forward | ∂E_pre (written here)
+  float* alpha_dE;                           // same buffer, written by the destination passes
 };
 cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st);
 cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st);

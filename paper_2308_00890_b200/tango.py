@@ -55,7 +55,7 @@ class GatParams(C.Structure):
 class GatCtxView(C.Structure):
     _fields_ = [(f, _P) for f in ("qH", "qW", "qWt", "qHp", "qS", "qD", "qG", "qdHp")] + \
                [(f, C.c_int64) for f in ("ldF", "ldHD", "ldFt")] + \
-               [(f, _P) for f in ("S", "D", "m", "den", "P", "dD", "dHp", "dalpha", "scalars")]
+               [(f, _P) for f in ("S", "D", "m", "den", "P", "dD", "dHp", "dalpha", "alpha_pack", "scalars")]
 
 
 class GcnParams(C.Structure):
@@ -403,6 +403,10 @@ class GATLayer:
             den=sl(v.den, N * H * 4, f4, (N, H)), P=sl(v.P, N * H * 4, f4, (N, H)),
             dD=sl(v.dD, N * H * 4, f4, (N, H)), dHp=sl(v.dHp, n * HD * 4, f4, (n, HD)),
             dalpha=sl(v.dalpha, E * H * 4, f4, (E, H)), scalars=sl(v.scalars, 64 * 4, f4, (64,)))
+        pack = sl(v.alpha_pack, E * 2 * H * 4, f4, (E, 2 * H))
+        out["alpha"] = pack[:, :H].abs()
+        out["e_pre_pos"] = ~torch.signbit(pack[:, :H])
+        out["dE_pre"] = pack[:, H:]
         return out
 
     def check_status(self):

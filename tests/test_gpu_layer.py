@@ -95,12 +95,14 @@ def test_gat_layer_parity(T, orc, case):
     eq("qD", fv["qD"], f["qD"])
     eq("m", fv["m"], f["m"])
     eq("den", fv["den"], f["den"])
+    eq("alpha", fv["alpha"], f["alpha"])
+    assert np.array_equal(fv["e_pre_pos"].cpu().numpy(), f["e_pre"] > 0)
     eq("H_out", Hout, f["Hout"])
     eq("amax_out", amax_out, f["amax_out"])
     # backward: B1-B9
     eq("qG", bv["qG"], b["qG"])
-    # the edge scratch holds ∂α after the dst pass-1 and ∂E_pre (B3) at the end of the backward
-    eq("dE_pre", bv["dalpha"], b["dE_pre"])
+    eq("dalpha", bv["dalpha"], b["dalpha"])
+    eq("dE_pre", bv["dE_pre"], b["dE_pre"])
     eq("P", bv["P"], b["P"])
     eq("dD", bv["dD"], b["dD"])
     eq("dHp", bv["dHp"], b["dHp"])
