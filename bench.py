@@ -24,6 +24,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_2308_00890_b200 import inputs  # noqa: E402
+from paper_2308_00890_b200.partition import partition_rows  # noqa: E402
 
 METRIC = "quantized GAT layer fwd+bwd ms"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}
@@ -42,16 +43,6 @@ def workload(name):
     kw, F, H, D = inputs.WORKLOADS[name]
     g = inputs.workload_graph(name)
     return g, F, H, D
-
-
-def partition_rows(g, nranks):
-    """Contiguous node ranges balanced by in-edge count."""
-    cum = g.in_ptr.astype(np.float64) + np.arange(g.n + 1)  # edges + one unit per row
-    starts = [0]
-    for r in range(1, nranks):
-        starts.append(int(np.searchsorted(cum, cum[-1] * r / nranks)))
-    starts.append(g.n)
-    return starts
 
 
 # ------------------------------------------------------------------------------------- clocks

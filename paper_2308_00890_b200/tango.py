@@ -12,6 +12,8 @@ import os
 import numpy as np
 import torch
 
+from .partition import local_graph
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtango.so")
 
@@ -180,18 +182,14 @@ class DeviceGraph:
     """
 
     def __init__(self, g, device="cuda", chunk=256, row_begin=0, row_end=None):
-        row_end = g.n if row_end is None else row_end
-        ib, ie = int(g.in_ptr[row_begin]), int(g.in_ptr[row_end])
-        ob, oe = int(g.out_ptr[row_begin]), int(g.out_ptr[row_end])
-        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
-        self.in_ptr = t(g.in_ptr[row_begin:row_end + 1] - ib, np.int64)
-        self.in_src = t(g.in_src[ib:ie], np.int32)
-        self.out_ptr = t(g.out_ptr[row_begin:row_end + 1] - ob, np.int64)
-        self.out_dst = t(g.out_dst[ob:oe], np.int32)
-        self.out_eid = t(g.out_eid[ob:oe], np.int32) if (row_begin == 0 and row_end == g.n) else None
-        self.n_global, self.row_begin, self.row_end = g.n, row_begin, row_end
-        self.n_local = row_end - row_begin
-        self.e_in, self.e_out = ie - ib, oe - ob
+        lg = local_graph(g, row_begin, row_end)
+        t = lambda a: torch.from_numpy(a).to(device)
+        self.in_ptr, self.in_src = t(lg.in_ptr), t(lg.in_src)
+        self.out_ptr, self.out_dst = t(lg.out_ptr), t(lg.out_dst)
+        self.out_eid = t(lg.out_eid) if lg.out_eid is not None else None
+        self.n_global, self.row_begin, self.row_end = g.n, lg.row_begin, lg.row_end
+        self.n_local = lg.n
+        self.e_in, self.e_out = lg.e, lg.e_out
         self.chunk = chunk
         self.struct = Graph(g.n, row_begin, row_end, _ptr(self.in_ptr), _ptr(self.in_src) if self.e_in else None,
                             self.e_in, _ptr(self.out_ptr), _ptr(self.out_dst) if self.e_out else None,
