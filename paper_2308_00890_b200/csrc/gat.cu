@@ -945,6 +945,218 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg3(const GatFwdArgs a) {
 }
 
 
+// ================================================================== gather engine v4
+// One warp streams a heavy segment or a light sub-tile: the 32-edge chunk attributes (gather index,
+// tile row, |α| per head, optional per-edge addend x per head) are loaded one chunk ahead into
+// registers and stashed in per-warp shared memory as [head][edge] so a group of 4 edges reads them
+// with one LDS.128 each; rows are gathered by cp.async into a ring of AGG_RING slots whose refill
+// indices also come from shared memory (one LDS.128 per 4 edges, no shuffles).  The tail group is
+// padded with α = +0, x = +0 and the last row: fmaf(+0, q, acc) == acc and acc + (+0) == acc for
+// every acc these sums can hold (never -0), so padding is exact and the group loop is branch-free.
+template <int H, int VPL, bool HAS_X>
+__host__ __device__ constexpr int g4_warp_smem() {
+  return AGG_RING * 32 * VPL + 2 * H * 32 * 4 * (HAS_X ? 2 : 1) + 2 * 32 * 4 + 2 * 32;
+}
+
+template <int H, int VPL, bool HAS_X, typename AttrF, typename RowF>
+__device__ __forceinline__ int g4_stream(uint8_t* wsm, const int8_t* __restrict__ xbase, uint32_t ld32, bool tile,
+                                         int64_t seg_eb, const TileLane& L, int T, AttrF&& attr, RowF&& on_row,
+                                         float2 (&acc)[VPL / 2], float& xs) {
+  constexpr int R = AGG_RING, RB = 32 * VPL;
+  const int lane = threadIdx.x & 31, myh = lane / (32 / H);
+  float* sa = reinterpret_cast<float*>(wsm + R * RB);                       // [2][H][32] |α|
+  float* sx = sa + 2 * H * 32;                                              // [2][H][32] x (HAS_X)
+  int* sidx = reinterpret_cast<int*>(wsm + R * RB + 2 * H * 32 * 4 * (HAS_X ? 2 : 1));   // [2][32]
+  uint8_t* srow = reinterpret_cast<uint8_t*>(sidx + 64);                   // [2][32]
+  const uint32_t ring_s = smem_u32(wsm) + lane * VPL;
+  const int tlast = T - 1;
+  auto load = [&](int c, int& idx, int& row, float (&al)[H], float (&x)[H]) {
+    const int t = c * 32 + lane;
+    int64_t e;
+    if (tile) {
+      row = tile_row(t < T ? t : tlast, L.end);
+      e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+    } else {
+      row = 0;
+      e = seg_eb + t;
+    }
+    idx = 0;
+#pragma unroll
+    for (int h = 0; h < H; ++h) { al[h] = 0.0f; x[h] = 0.0f; }
+    if (t < T) attr(e, idx, al, x);
+  };
+  auto stash = [&](int b, int row, const float (&al)[H], const float (&x)[H]) {
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      sa[(b * H + h) * 32 + lane] = al[h];
+      if constexpr (HAS_X) sx[(b * H + h) * 32 + lane] = x[h];
+    }
+    srow[b * 32 + lane] = (uint8_t)row;
+  };
+  auto group = [&](const Row<VPL> (&r)[4], float4 a4, float4 x4, uint32_t rw, int& cur) {
+    const float al[4] = {a4.x, a4.y, a4.z, a4.w};
+    const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
+    if ((int)(rw >> 24) == cur) {   // rows are non-decreasing: the whole group continues the row
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 al2 = make_float2(al[j], al[j]);
+#pragma unroll
+        for (int q = 0; q < VPL / 4; ++q) fma4_codes(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
+        if constexpr (HAS_X) xs = __fadd_rn(xs, xv[j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int rj = (int)((rw >> (8 * j)) & 0xffu);
+        if (rj != cur) {
+          if (cur >= 0) on_row(cur);
+          cur = rj;
+        }
+        const float2 al2 = make_float2(al[j], al[j]);
+#pragma unroll
+        for (int q = 0; q < VPL / 4; ++q) fma4_codes(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
+        if constexpr (HAS_X) xs = __fadd_rn(xs, xv[j]);
+      }
+    }
+  };
+  {
+    int idxA, rowA;
+    float alA[H], xA[H];
+    load(0, idxA, rowA, alA, xA);
+    stash(0, rowA, alA, xA);
+    sidx[lane] = idxA;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int g = 0; g < R / 4; ++g) {   // ring prologue: edges 0 .. R-1, one commit group per 4 edges
+    const int4 nx = *reinterpret_cast<const int4*>(sidx + 4 * g);
+    const int nv[4] = {nx.x, nx.y, nx.z, nx.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (4 * g + j < T) cp_row_slice<VPL>(ring_s + (4 * g + j) * RB, xbase + (uint32_t)nv[j] * ld32);
+    cp_commit();
+  }
+  int cur = tile ? -1 : 0;
+  const int nch = (T + 31) >> 5;
+  for (int c = 0; c < nch; ++c) {
+    int idxB, rowB;
+    float alB[H], xB[H];
+    load(c + 1, idxB, rowB, alB, xB);   // next chunk, in flight while this chunk streams
+    const int cb = c & 1;
+    const float* sac = sa + (cb * H + myh) * 32;
+    const float* sxc = sx + (cb * H + myh) * 32;
+    const uint8_t* src_ = srow + cb * 32;
+    for (int i0 = 0; i0 < 32; i0 += 4) {
+      const int t0 = c * 32 + i0;
+      if (t0 >= T) break;
+      if (i0 == 12) {   // refills from group 16 on read the next chunk's indices
+        sidx[(cb ^ 1) * 32 + lane] = idxB;
+        __syncwarp();
+      }
+      cp_wait<R / 4 - 1>();   // the 4 rows of this group have landed
+      const uint32_t slot0 = ring_s + (uint32_t)(t0 & (R - 1)) * RB;
+      Row<VPL> r[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r[j] = lds_row_slice<VPL>(slot0 + j * RB);
+      const float4 a4 = *reinterpret_cast<const float4*>(sac + i0);
+      float4 x4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      if constexpr (HAS_X) x4 = *reinterpret_cast<const float4*>(sxc + i0);
+      const uint32_t rw = *reinterpret_cast<const uint32_t*>(src_ + i0);
+      group(r, a4, x4, rw, cur);
+      const int tn0 = t0 + R;   // refill the 4 consumed slots with edges t0+R .. t0+R+3
+      const int4 nx = *reinterpret_cast<const int4*>(sidx + ((tn0 >> 5) & 1) * 32 + (tn0 & 31));
+      const int nv[4] = {nx.x, nx.y, nx.z, nx.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (tn0 + j < T) cp_row_slice<VPL>(slot0 + j * RB, xbase + (uint32_t)nv[j] * ld32);   // N*ld < 2^32
+      cp_commit();
+    }
+    __syncwarp();
+    stash(cb ^ 1, rowB, alB, xB);
+    __syncwarp();
+  }
+  cp_wait<0>();
+  __syncwarp();
+  return cur;
+}
+
+// FA (VPL >= 4): ⑤ H_out = (Σ fmaf(α, q_H′[u])) * s_H′ over (heavy segment | light sub-tile)
+template <int H, int VPL>
+__global__ void __launch_bounds__(256, 3) k_fwd_agg4(const GatFwdArgs a) {
+  constexpr int HD = 32 * VPL;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wsm = dsm + w * g4_warp_smem<H, VPL, false>();
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const int64_t n = a.g.n_local, hc = load_count(a.plan.counts);
+  const int64_t nitems = hc + load_count(a.plan.counts + 2);
+  const int8_t* xbase = a.qHp + lane * VPL;
+  const uint32_t ld32 = (uint32_t)a.ldHp;
+  float amax_loc = 0.0f;
+  FOR_ITEMS(item, a.work + 2, nitems) {
+    const bool tile = item >= hc;
+    Seg s;
+    s.eb = 0;
+    TileLane L;
+    int64_t r0 = 0;
+    int T;
+    if (!tile) {
+      decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s);
+      T = (int)(s.ee - s.eb);
+      L.eb = 0; L.off = 0; L.end = 0;
+    } else {
+      const int32_t code = a.plan.tiles[item - hc];
+      r0 = (int64_t)(code >> 10) * TILE;
+      L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
+      unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
+      while (zm) {   // light rows without in-edges: H_out = 0
+        const int j = __ffs(zm) - 1;
+        zm &= zm - 1;
+        float4* dst = reinterpret_cast<float4*>(a.Hout + (r0 + j) * HD + lane * VPL);
+#pragma unroll
+        for (int k = 0; k < VPL / 4; ++k) __stcs(dst + k, make_float4(0.0f, 0.0f, 0.0f, 0.0f));
+      }
+    }
+    float2 acc[VPL / 2];
+#pragma unroll
+    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
+    float xs = 0.0f;
+    auto flush = [&](int j) {
+      float4* dst = reinterpret_cast<float4*>(a.Hout + (r0 + j) * HD + lane * VPL);
+#pragma unroll
+      for (int k = 0; k < VPL / 4; ++k) {
+        const float4 o = make_float4(__fmul_rn(acc[2 * k].x, scH.s), __fmul_rn(acc[2 * k].y, scH.s),
+                                     __fmul_rn(acc[2 * k + 1].x, scH.s), __fmul_rn(acc[2 * k + 1].y, scH.s));
+        amax_loc = fmaxf(amax_loc, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
+        __stcs(dst + k, o);
+        acc[2 * k] = make_float2(0.0f, 0.0f);
+        acc[2 * k + 1] = make_float2(0.0f, 0.0f);
+      }
+    };
+    auto attr = [&](int64_t e, int& u, float (&al)[H], float (&)[H]) {
+      u = a.g.in_src[e];
+      if constexpr (H == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(a.alpha + e * 8);
+        al[0] = fabsf(v.x); al[1] = fabsf(v.y); al[2] = fabsf(v.z); al[3] = fabsf(v.w);
+      } else {
+#pragma unroll
+        for (int h = 0; h < H; ++h) al[h] = fabsf(a.alpha[e * 2 * H + h]);
+      }
+    };
+    const int cur = g4_stream<H, VPL, false>(wsm, xbase, ld32, tile, s.eb, L, T, attr, flush, acc, xs);
+    if (tile) {
+      if (cur >= 0) flush(cur);
+    } else {
+      float4* dst = reinterpret_cast<float4*>(a.hagg + (int64_t)s.slot * HD + lane * VPL);
+#pragma unroll
+      for (int k = 0; k < VPL / 4; ++k)
+        dst[k] = make_float4(acc[2 * k].x, acc[2 * k].y, acc[2 * k + 1].x, acc[2 * k + 1].y);
+    }
+  }
+  amax_flush(a.amax_out, amax_loc);
+}
+
+
 // ================================================================== backward gather kernels (cp.async engine)
 template <int H, int VPL>
 __host__ __device__ constexpr int bwd3_warp_smem() {
@@ -1362,6 +1574,111 @@ __global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
     if (cur >= 0) {
       const float dSb = __shfl_sync(0xffffffffu, dS, myh * LPH);
       src_finalize_full<VPL>(a, r0 + cur, ug0 + cur, myh, H, dSb, acc, scG.s, amax_loc);
+    }
+  }
+  amax_flush(a.amax_dHp, amax_loc);
+}
+
+// ②′ finalize of one source row (vectorized): ∂H′ = (agg·s_G + ∂S·a_src) + ∂D·a_dst
+template <int H, int VPL>
+__device__ __forceinline__ void src_finalize4(const GatBwdArgs& a, int64_t ul, int64_t ug, int myh, bool leader,
+                                              float dS, float2 (&acc)[VPL / 2], float sG, float& amax_loc) {
+  constexpr int HD = 32 * VPL;
+  const int lane = threadIdx.x & 31;
+  const float dD = a.dD[ug * H + myh];
+  const int c0 = lane * VPL;
+  float4* dst = reinterpret_cast<float4*>(a.dHp + ul * HD + c0);
+  const float4* as = reinterpret_cast<const float4*>(a.a_src + c0);
+  const float4* ad = reinterpret_cast<const float4*>(a.a_dst + c0);
+#pragma unroll
+  for (int k = 0; k < VPL / 4; ++k) {
+    const float4 s4 = __ldg(as + k), d4 = __ldg(ad + k);
+    const float v[4] = {acc[2 * k].x, acc[2 * k].y, acc[2 * k + 1].x, acc[2 * k + 1].y};
+    const float sv[4] = {s4.x, s4.y, s4.z, s4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+    float o[4];
+#pragma unroll
+    for (int z = 0; z < 4; ++z) {
+      const float t2 = __fadd_rn(__fmul_rn(v[z], sG), __fmul_rn(dS, sv[z]));
+      o[z] = __fadd_rn(t2, __fmul_rn(dD, dv[z]));
+      amax_loc = fmaxf(amax_loc, fabsf(o[z]));
+    }
+    dst[k] = make_float4(o[0], o[1], o[2], o[3]);
+    acc[2 * k] = make_float2(0.0f, 0.0f);
+    acc[2 * k + 1] = make_float2(0.0f, 0.0f);
+  }
+  if (leader) a.dS[ug * H + myh] = dS;
+}
+
+// BS (one GPU, out_eid present): ⑤′ ∂H′_agg = Σ fmaf(|α|, q_G[v]) and ③′ ∂S = Σ ∂E_pre over out-edges,
+// with |α| and ∂E_pre read through the edge-id map from the packed [E][2H] array; ②′ finalize.
+template <int H, int VPL, int NW>
+__global__ void __maxnreg__(96) k_bwd_src4(const GatBwdArgs a) {
+  constexpr int HD = 32 * VPL;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int myh = lane / (32 / H);
+  const bool leader = (lane % (32 / H)) == 0;
+  uint8_t* wsm = dsm + w * g4_warp_smem<H, VPL, true>();
+  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
+  const int64_t n = a.g.n_local, hc = load_count(a.pout.counts);
+  const int64_t nitems = hc + load_count(a.pout.counts + 2);
+  const int8_t* gbase = a.qG + lane * VPL;
+  const uint32_t ld32 = (uint32_t)a.ldG;
+  float amax_loc = 0.0f;
+  FOR_ITEMS(item, a.work + 2, nitems) {
+    const bool tile = item >= hc;
+    Seg s;
+    s.eb = 0;
+    TileLane L;
+    int64_t r0 = 0;
+    int T;
+    float2 acc[VPL / 2];
+#pragma unroll
+    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
+    if (!tile) {
+      decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
+      T = (int)(s.ee - s.eb);
+      L.eb = 0; L.off = 0; L.end = 0;
+      r0 = s.vl;
+    } else {
+      const int32_t code = a.pout.tiles[item - hc];
+      r0 = (int64_t)(code >> 10) * TILE;
+      L = tile_setup(a.g.out_ptr, a.pout.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
+      unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
+      while (zm) {   // light rows without out-edges: ∂H′ = (0 + 0·a_src) + ∂D·a_dst
+        const int j = __ffs(zm) - 1;
+        zm &= zm - 1;
+        src_finalize4<H, VPL>(a, r0 + j, a.g.row_begin + r0 + j, myh, leader, 0.0f, acc, scG.s, amax_loc);
+      }
+    }
+    const int64_t ug0 = a.g.row_begin + r0;
+    float dS = 0.0f;
+    auto flush = [&](int j) {
+      src_finalize4<H, VPL>(a, r0 + j, ug0 + j, myh, leader, dS, acc, scG.s, amax_loc);
+      dS = 0.0f;
+    };
+    auto attr = [&](int64_t e, int& v, float (&al)[H], float (&x)[H]) {
+      v = a.g.out_dst[e];
+      const int64_t eid = a.g.out_eid[e];
+      if constexpr (H == 4) {
+        const float4 p = *reinterpret_cast<const float4*>(a.alpha + eid * 8);
+        const float4 q = *reinterpret_cast<const float4*>(a.alpha + eid * 8 + 4);
+        al[0] = fabsf(p.x); al[1] = fabsf(p.y); al[2] = fabsf(p.z); al[3] = fabsf(p.w);
+        x[0] = q.x; x[1] = q.y; x[2] = q.z; x[3] = q.w;
+      } else {
+#pragma unroll
+        for (int h = 0; h < H; ++h) { al[h] = fabsf(a.alpha[eid * 2 * H + h]); x[h] = a.alpha[eid * 2 * H + H + h]; }
+      }
+    };
+    const int cur = g4_stream<H, VPL, true>(wsm, gbase, ld32, tile, s.eb, L, T, attr, flush, acc, dS);
+    if (tile) {
+      if (cur >= 0) flush(cur);
+    } else {
+      if (leader) a.hdS[(int64_t)s.slot * H + myh] = dS;
+      float4* dst = reinterpret_cast<float4*>(a.hagg + (int64_t)s.slot * HD + lane * VPL);
+#pragma unroll
+      for (int k = 0; k < VPL / 4; ++k)
+        dst[k] = make_float4(acc[2 * k].x, acc[2 * k].y, acc[2 * k + 1].x, acc[2 * k + 1].y);
     }
   }
   amax_flush(a.amax_dHp, amax_loc);
@@ -1998,14 +2315,14 @@ cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
     { ProfScope p("gat_fwd_alpha3", st); k_fwd_alpha3<H_><<<item_grid(a.plan.cap), 256, 0, st>>>(a); } \
     { ProfScope p("gat_fwd_agg", st);                                                              \
       if (V_ >= 4) {                                                                               \
-        constexpr int smem = 8 * agg3_warp_smem<H_, (V_ >= 4 ? V_ : 4)>();                         \
+        constexpr int smem = 8 * g4_warp_smem<H_, (V_ >= 4 ? V_ : 4), false>();                     \
         static bool attr_set = false;                                                              \
         if (!attr_set) {                                                                           \
-          cudaFuncSetAttribute(k_fwd_agg3<H_, (V_ >= 4 ? V_ : 4)>,                                 \
+          cudaFuncSetAttribute(k_fwd_agg4<H_, (V_ >= 4 ? V_ : 4)>,                                 \
                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                 \
           attr_set = true;                                                                         \
         }                                                                                          \
-        k_fwd_agg3<H_, (V_ >= 4 ? V_ : 4)><<<item_grid(a.plan.cap + a.plan.tcap), 256, smem, st>>>(a); \
+        k_fwd_agg4<H_, (V_ >= 4 ? V_ : 4)><<<item_grid(a.plan.cap + a.plan.tcap), 256, smem, st>>>(a); \
       } else {                                                                                     \
         k_fwd_agg2<H_, V_><<<item_grid(a.plan.cap + a.plan.tcap), 256, 0, st>>>(a);               \
       } }                                                                                          \
@@ -2084,7 +2401,17 @@ cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st) {
         attr_set = true;                                                                           \
       }                                                                                            \
       ProfScope p("gat_bwd_src", st);                                                              \
-      k_bwd_src_v3<H_, VV><<<item_grid(a.pout.cap + a.pout.tcap), 256, smem, st>>>(a);             \
+      if (a.g.out_eid) {                                                                           \
+        constexpr int NW = 7, smem4 = NW * g4_warp_smem<H_, VV, true>();                           \
+        static bool attr4_set = false;                                                             \
+        if (!attr4_set) {                                                                          \
+          cudaFuncSetAttribute(k_bwd_src4<H_, VV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); \
+          attr4_set = true;                                                                        \
+        }                                                                                          \
+        k_bwd_src4<H_, VV, NW><<<item_grid(a.pout.cap + a.pout.tcap), NW * 32, smem4, st>>>(a);    \
+      } else {                                                                                     \
+        k_bwd_src_v3<H_, VV><<<item_grid(a.pout.cap + a.pout.tcap), 256, smem, st>>>(a);           \
+      }                                                                                            \
     }
     TANGO_HV_CASES(X)
 #undef X

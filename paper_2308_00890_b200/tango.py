@@ -181,8 +181,8 @@ class DeviceGraph:
     the in/out CSR arrays are then sliced to the owned rows.
     """
 
-    def __init__(self, g, device="cuda", chunk=256, row_begin=0, row_end=None):
-        lg = local_graph(g, row_begin, row_end)
+    def __init__(self, g, device="cuda", chunk=256, row_begin=0, row_end=None, keep_eid=None):
+        lg = local_graph(g, row_begin, row_end, keep_eid)
         t = lambda a: torch.from_numpy(a).to(device)
         self.in_ptr, self.in_src = t(lg.in_ptr), t(lg.in_src)
         self.out_ptr, self.out_dst = t(lg.out_ptr), t(lg.out_dst)
@@ -191,7 +191,7 @@ class DeviceGraph:
         self.n_local = lg.n
         self.e_in, self.e_out = lg.e, lg.e_out
         self.chunk = chunk
-        self.struct = Graph(g.n, row_begin, row_end, _ptr(self.in_ptr), _ptr(self.in_src) if self.e_in else None,
+        self.struct = Graph(g.n, lg.row_begin, lg.row_end, _ptr(self.in_ptr), _ptr(self.in_src) if self.e_in else None,
                             self.e_in, _ptr(self.out_ptr), _ptr(self.out_dst) if self.e_out else None,
                             _ptr(self.out_eid) if self.out_eid is not None and self.e_out else None, self.e_out,
                             chunk)

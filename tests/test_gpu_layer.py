@@ -62,6 +62,17 @@ def build_graph(spec):
 
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
 def test_gat_layer_parity(T, orc, case):
+    _gat_parity(T, orc, case, keep_eid=None)
+
+
+# Without out_eid the source pass recomputes α / ∂α / ∂E_pre from per-node data (the path a
+# partitioned graph takes); run it on one GPU by dropping the edge-id map.
+@pytest.mark.parametrize("case", [CASES[1], CASES[2], CASES[3], CASES[5]], ids=lambda c: c[0])
+def test_gat_layer_parity_recompute_src(T, orc, case):
+    _gat_parity(T, orc, case, keep_eid=False)
+
+
+def _gat_parity(T, orc, case, keep_eid):
     name, spec, F, heads, hd, chunk = case
     gr = build_graph(spec)
     HD = heads * hd
@@ -69,7 +80,7 @@ def test_gat_layer_parity(T, orc, case):
     W, a_src, a_dst = inputs.gat_params(F, heads, hd, seed=12)
     dH = inputs.grad_out(gr.n, HD, seed=13)
     step, layer_id, slope = 2, 1, 0.2
-    dg = T.DeviceGraph(gr, chunk=chunk)
+    dg = T.DeviceGraph(gr, chunk=chunk, keep_eid=keep_eid)
     layer = T.GATLayer(dg, cu(W), cu(a_src), cu(a_dst), heads, hd, slope=slope, bits=8)
     Hout, amax_out = layer.forward(cu(H), step=step, layer_id=layer_id)
     fv = layer.view()
