@@ -1579,6 +1579,275 @@ __global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
   amax_flush(a.amax_dHp, amax_loc);
 }
 
+// 4-edge transposed reduction of per-lane partial dots over the LPH lanes of a head: afterwards the
+// lane holds the full (exact, integer) dot of edge k = (lane & LPH/2 ? 2 : 0) + (lane & LPH/4 ? 1 : 0)
+// of the group; 4 shuffles instead of 4 * log2(LPH).
+template <int LPH>
+__device__ __forceinline__ int group_dot_reduce(const int (&d)[4], int& k) {
+  const int lane = threadIdx.x & 31;
+  const bool hi = lane & (LPH / 2), mid = lane & (LPH / 4);
+  const int x0 = (hi ? d[2] : d[0]) + __shfl_xor_sync(0xffffffffu, hi ? d[0] : d[2], LPH / 2);
+  const int x1 = (hi ? d[3] : d[1]) + __shfl_xor_sync(0xffffffffu, hi ? d[1] : d[3], LPH / 2);
+  int y = (mid ? x1 : x0) + __shfl_xor_sync(0xffffffffu, mid ? x0 : x1, LPH / 4);
+#pragma unroll
+  for (int o = LPH / 8; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+  k = (hi ? 2 : 0) + (mid ? 1 : 0);
+  return y;
+}
+
+template <int H, int VPL>
+__host__ __device__ constexpr int dst4_warp_smem() {
+  // ring | |α| [2][H][32] | gather idx [2][32] | row [2][32] u8 | ∂α [H][32] (pass 2: [32][H]) | P [32][H]
+  return AGG_RING * 32 * VPL + 2 * H * 32 * 4 + 2 * 32 * 4 + 2 * 32 + H * 32 * 4 + 32 * H * 4;
+}
+
+// BD1 (v4 engine): ⑤″ ∂α = i2f(q_G[v]·q_H′[u]) (s_G s_H′), ④′ P = Σ fmaf(∂α, α) in edge order per
+// destination row (heavy segments: P partials), then for light rows ∂E_pre and ∂D (pass 2).
+template <int H, int VPL, int NW>
+__global__ void __maxnreg__(96) k_bwd_dst1_v4(const GatBwdArgs a) {
+  constexpr int R = AGG_RING, RB = 32 * VPL, LPH = 32 / H;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int myh = lane / LPH;
+  const bool leader = (lane % LPH) == 0;
+  uint8_t* wsm = dsm + w * dst4_warp_smem<H, VPL>();
+  float* sa = reinterpret_cast<float*>(wsm + R * RB);                 // [2][H][32]
+  int* sidx = reinterpret_cast<int*>(sa + 2 * H * 32);                // [2][32]
+  uint8_t* srow = reinterpret_cast<uint8_t*>(sidx + 64);             // [2][32]
+  float* sd = reinterpret_cast<float*>(srow + 64);                    // [H][32]
+  float (*pt)[H] = reinterpret_cast<float (*)[H]>(sd + H * 32);       // [32][H]
+  const uint32_t ring_s = smem_u32(wsm) + lane * VPL;
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
+  const float sGH = __fmul_rn(scG.s, scH.s);
+  const int64_t n = a.g.n_local, hc = load_count(a.pin.counts);
+  const int64_t nitems = hc + load_count(a.pin.counts + 2);
+  const int8_t* xbase = a.qHp + lane * VPL;
+  const int8_t* gbase = a.qG + lane * VPL;
+  const uint32_t ld32 = (uint32_t)a.ldHp;
+  FOR_ITEMS(item, a.work + 0, nitems) {
+    const bool tile = item >= hc;
+    Seg s;
+    s.eb = 0;
+    TileLane L;
+    int64_t r0 = 0;
+    int T;
+    if (!tile) {
+      decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
+      T = (int)(s.ee - s.eb);
+      L.eb = 0; L.off = 0; L.end = 0; L.deg = 0; L.light = false;
+    } else {
+      const int32_t code = a.pin.tiles[item - hc];
+      r0 = (int64_t)(code >> 10) * TILE;
+      L = tile_setup(a.g.in_ptr, a.pin.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
+      if (L.light && L.deg == 0) {
+        const int64_t vg = a.g.row_begin + L.r;
+#pragma unroll
+        for (int h = 0; h < H; ++h) { a.P[vg * H + h] = 0.0f; a.dD[vg * H + h] = 0.0f; }
+      }
+    }
+    const int tlast = T - 1;
+    auto load = [&](int c, int& u, int& row, int64_t& e, float (&al)[H]) {
+      const int t = c * 32 + lane;
+      if (tile) {
+        row = tile_row(t < T ? t : tlast, L.end);
+        e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+      } else {
+        row = 0;
+        e = s.eb + t;
+      }
+      u = 0;
+#pragma unroll
+      for (int h = 0; h < H; ++h) al[h] = 0.0f;
+      if (t < T) {
+        u = a.g.in_src[e];
+        if constexpr (H == 4) {
+          const float4 v = *reinterpret_cast<const float4*>(a.alpha + e * 8);
+          al[0] = fabsf(v.x); al[1] = fabsf(v.y); al[2] = fabsf(v.z); al[3] = fabsf(v.w);
+        } else {
+#pragma unroll
+          for (int h = 0; h < H; ++h) al[h] = fabsf(a.alpha[e * 2 * H + h]);
+        }
+      }
+    };
+    auto stash = [&](int b, int row, const float (&al)[H]) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) sa[(b * H + h) * 32 + lane] = al[h];
+      srow[b * 32 + lane] = (uint8_t)row;
+    };
+    // own q_G[v] slice per row, prefetched one row ahead
+    const unsigned act = tile ? __ballot_sync(0xffffffffu, L.deg > 0) : 1u;
+    const int64_t vg0 = a.g.row_begin + (tile ? r0 : s.vl);
+    int nxt = act ? __ffs(act) - 1 : -1;
+    Row<VPL> gw{}, gw_nxt{};
+    if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
+    int64_t eA;
+    {
+      int uA, rowA;
+      float alA[H];
+      load(0, uA, rowA, eA, alA);
+      stash(0, rowA, alA);
+      sidx[lane] = uA;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int g = 0; g < R / 4; ++g) {
+      const int4 nx = *reinterpret_cast<const int4*>(sidx + 4 * g);
+      const int nv[4] = {nx.x, nx.y, nx.z, nx.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (4 * g + j < T) cp_row_slice<VPL>(ring_s + (4 * g + j) * RB, xbase + (uint32_t)nv[j] * ld32);
+      cp_commit();
+    }
+    float P = 0.0f;
+    int cur = -1, pcur = -1;
+    if (!tile) {   // a heavy segment is one row
+      cur = 0; pcur = 0;
+      gw = gw_nxt;
+    }
+    const int nch = (T + 31) >> 5;
+    for (int c = 0; c < nch; ++c) {
+      int uB, rowB;
+      int64_t eB;
+      float alB[H];
+      load(c + 1, uB, rowB, eB, alB);
+      const int cb = c & 1;
+      const float* sac = sa + (cb * H + myh) * 32;
+      const uint8_t* src_ = srow + cb * 32;
+      for (int i0 = 0; i0 < 32; i0 += 4) {
+        const int t0 = c * 32 + i0;
+        if (t0 >= T) break;
+        if (i0 == 12) {
+          sidx[(cb ^ 1) * 32 + lane] = uB;
+          __syncwarp();
+        }
+        cp_wait<R / 4 - 1>();
+        const uint32_t slot0 = ring_s + (uint32_t)(t0 & (R - 1)) * RB;
+        Row<VPL> r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = lds_row_slice<VPL>(slot0 + j * RB);
+        const float4 a4 = *reinterpret_cast<const float4*>(sac + i0);
+        const uint32_t rw = *reinterpret_cast<const uint32_t*>(src_ + i0);
+        int d[4];
+        const bool same = (int)(rw >> 24) == cur;
+        if (same) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) d[j] = row_dot<VPL>(gw, r[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int rj = (int)((rw >> (8 * j)) & 0xffu);
+            if (rj != cur) {
+              cur = rj;
+              gw = gw_nxt;
+              nxt = tile_next(act, cur);
+              if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
+            }
+            d[j] = row_dot<VPL>(gw, r[j]);
+          }
+        }
+        int k;
+        const int dot = group_dot_reduce<LPH>(d, k);
+        sd[myh * 32 + i0 + k] = __fmul_rn(__int2float_rn(dot), sGH);
+        __syncwarp();
+        const float4 d4 = *reinterpret_cast<const float4*>(sd + myh * 32 + i0);
+        const float dal[4] = {d4.x, d4.y, d4.z, d4.w}, al[4] = {a4.x, a4.y, a4.z, a4.w};
+        if (same) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) P = __fmaf_rn(dal[j], al[j], P);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int rj = (int)((rw >> (8 * j)) & 0xffu);
+            if (rj != pcur) {
+              if (pcur >= 0 && leader) pt[pcur][myh] = P;
+              P = 0.0f;
+              pcur = rj;
+            }
+            P = __fmaf_rn(dal[j], al[j], P);
+          }
+        }
+        const int tn0 = t0 + R;
+        const int4 nx = *reinterpret_cast<const int4*>(sidx + ((tn0 >> 5) & 1) * 32 + (tn0 & 31));
+        const int nv[4] = {nx.x, nx.y, nx.z, nx.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (tn0 + j < T) cp_row_slice<VPL>(slot0 + j * RB, xbase + (uint32_t)nv[j] * ld32);
+        cp_commit();
+      }
+      __syncwarp();
+      if (c * 32 + lane < T) {   // ∂α of this chunk -> scratch (edge-major)
+        if constexpr (H == 4) {
+          *reinterpret_cast<float4*>(a.dalpha + eA * 4) = make_float4(sd[lane], sd[32 + lane], sd[64 + lane], sd[96 + lane]);
+        } else {
+#pragma unroll
+          for (int h = 0; h < H; ++h) a.dalpha[eA * H + h] = sd[h * 32 + lane];
+        }
+      }
+      __syncwarp();
+      stash(cb ^ 1, rowB, alB);
+      eA = eB;
+      __syncwarp();
+    }
+    cp_wait<0>();
+    __syncwarp();
+    if (!tile) {
+      if (leader) a.hP[(int64_t)s.slot * H + myh] = P;
+      continue;
+    }
+    if (pcur >= 0 && leader) pt[pcur][myh] = P;
+    __syncwarp();
+    // ---- pass 2 (light rows): ∂E = α(∂α − P[v]), ∂E_pre, ∂D = Σ ∂E_pre (lane j folds row j)
+    float (*sdx)[H] = reinterpret_cast<float (*)[H]>(sd);   // [32][H]
+    float dDp[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) dDp[h] = 0.0f;
+    for (int base = 0; base < T; base += 32) {
+      const int cnt = T - base < 32 ? T - base : 32;
+      const int t = base + lane;
+      const int row = tile_row(t < T ? t : tlast, L.end);
+      const int64_t e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+      if (lane < cnt) {
+        float x[H], dl[H], o[H];
+        if constexpr (H == 4) {
+          const float4 xv = *reinterpret_cast<const float4*>(a.alpha + e * 8);
+          const float4 dv = *reinterpret_cast<const float4*>(a.dalpha + e * 4);
+          x[0] = xv.x; x[1] = xv.y; x[2] = xv.z; x[3] = xv.w;
+          dl[0] = dv.x; dl[1] = dv.y; dl[2] = dv.z; dl[3] = dv.w;
+        } else {
+#pragma unroll
+          for (int h = 0; h < H; ++h) { x[h] = a.alpha[e * 2 * H + h]; dl[h] = a.dalpha[e * H + h]; }
+        }
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const float dE = __fmul_rn(fabsf(x[h]), __fsub_rn(dl[h], pt[row][h]));
+          o[h] = signbit(x[h]) ? __fmul_rn(dE, a.slope) : dE;
+          sdx[lane][h] = o[h];
+        }
+        if constexpr (H == 4) {
+          *reinterpret_cast<float4*>(a.alpha_dE + e * 8 + 4) = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+          for (int h = 0; h < H; ++h) a.alpha_dE[e * 2 * H + H + h] = o[h];
+        }
+      }
+      __syncwarp();
+      const int lo = (L.off > base ? L.off : base) - base;
+      const int hi = (L.end < base + cnt ? L.end : base + cnt) - base;
+      for (int i = lo; i < hi; ++i)
+#pragma unroll
+        for (int h = 0; h < H; ++h) dDp[h] = __fadd_rn(dDp[h], sdx[i][h]);
+      __syncwarp();
+    }
+    if (L.deg > 0) {
+      const int64_t vg = a.g.row_begin + L.r;
+#pragma unroll
+      for (int h = 0; h < H; ++h) { a.P[vg * H + h] = pt[lane][h]; a.dD[vg * H + h] = dDp[h]; }
+    }
+    __syncwarp();
+  }
+}
+
 // ②′ finalize of one source row (vectorized): ∂H′ = (agg·s_G + ∂S·a_src) + ∂D·a_dst
 template <int H, int VPL>
 __device__ __forceinline__ void src_finalize4(const GatBwdArgs& a, int64_t ul, int64_t ug, int myh, bool leader,
@@ -2353,7 +2622,17 @@ cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st) {
         attr_set = true;                                                                           \
       }                                                                                            \
       ProfScope p("gat_bwd_dst1", st);                                                             \
-      k_bwd_dst1_v3<H_, VV><<<item_grid(a.pin.cap + a.pin.tcap), 256, smem, st>>>(a);              \
+      if (H_ <= 8) {                                                                               \
+        constexpr int NW = 7, smem4 = NW * dst4_warp_smem<H_, VV>();                               \
+        static bool attr4_set = false;                                                             \
+        if (!attr4_set) {                                                                          \
+          cudaFuncSetAttribute(k_bwd_dst1_v4<H_, VV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); \
+          attr4_set = true;                                                                        \
+        }                                                                                          \
+        k_bwd_dst1_v4<H_, VV, NW><<<item_grid(a.pin.cap + a.pin.tcap), NW * 32, smem4, st>>>(a);   \
+      } else {                                                                                     \
+        k_bwd_dst1_v3<H_, VV><<<item_grid(a.pin.cap + a.pin.tcap), 256, smem, st>>>(a);            \
+      }                                                                                            \
     }
     TANGO_HV_CASES(X)
 #undef X
