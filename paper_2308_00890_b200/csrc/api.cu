@@ -114,6 +114,7 @@ static tango_status check_graph(const tango_graph* G, bool need_out) {
 static GraphDev dev_graph(const tango_graph* G) {
   GraphDev g;
   g.n_local = G->row_end - G->row_begin;
+  g.n_global = G->n_global;
   g.row_begin = G->row_begin;
   g.in_ptr = G->in_ptr; g.in_src = G->in_src;
   g.out_ptr = G->out_ptr; g.out_dst = G->out_dst; g.out_eid = G->out_eid;

@@ -341,6 +341,22 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
   return r == CUDA_SUCCESS;
 }
 
+// Row-gather map for TMA tile::gather4 (gat.cu): the int8 table [rows][ld] viewed as uint32
+// [rows][ld/4] with a {row_bytes/4, 1} box, no swizzle — one gather4 lands 4 rows of row_bytes
+// contiguously in shared memory.
+bool make_row_gather_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t row_bytes, uint64_t ld_bytes) {
+  auto fn = encode_fn();
+  if (!fn || row_bytes % 16 || ld_bytes % 16 || row_bytes / 4 > 256 || rows == 0) return false;
+  cuuint64_t dims[2] = {ld_bytes / 4, rows};
+  cuuint64_t strides[1] = {ld_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)(row_bytes / 4), 1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0) return cudaSuccess;
   KParams p{};

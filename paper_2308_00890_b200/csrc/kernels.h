@@ -60,11 +60,12 @@ struct GemmArgs {
   void* C; int64_t ldc;
 };
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st);
+bool make_row_gather_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t row_bytes, uint64_t ld_bytes);
 
 // ---- gat.cu : fused GAT destination / source row kernels and standalone sparse primitives
 struct GatDims { int heads, head_dim, hd; };
 struct GraphDev {
-  int64_t n_local, row_begin;
+  int64_t n_local, row_begin, n_global;
   const int64_t* in_ptr; const int32_t* in_src;
   const int64_t* out_ptr; const int32_t* out_dst; const int32_t* out_eid;
   int chunk;
