@@ -340,6 +340,156 @@ __global__ void __launch_bounds__(256) k_fwd_stats(const GatFwdArgs a) {
   }
 }
 
+// FS (tiles): heavy segments -> segment max (hmax); light sub-tiles -> m, den and α for every edge.
+// Lane = edge of the tile's stream: the per-row max is a segmented lane scan (order-free), the per-row
+// Σ exp_p(el − m) is folded sequentially in edge order by the row's owner lane (canonical order; a
+// light row is one chunk), then α = |ex| / den keeps the sign of e_pre.
+template <int H>
+__global__ void __launch_bounds__(256) k_fwd_stats_t(const GatFwdArgs a) {
+  __shared__ float smx[WPB][32][H];
+  __shared__ float sbuf[WPB][32][H];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t n = a.g.n_local, hc = load_count(a.plan.counts);
+  const int64_t nitems = hc + load_count(a.plan.counts + 2);
+  FOR_ITEMS(item, a.work + 0, nitems) {
+    if (item < hc) {
+      Seg s;
+      decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s);
+      const int64_t vg = a.g.row_begin + s.vl;
+      int8_t qd[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) qd[h] = a.qD[vg * H + h];
+      float mx[H];
+      seg_max<H>(a.g.in_src, s.eb, s.ee, a.qS, scS.s, qd, scD.s, a.slope, mx);
+      if (lane < H) a.hmax[(int64_t)s.slot * H + lane] = head_pick<H>(mx, lane);
+      continue;
+    }
+    const int32_t code = a.plan.tiles[item - hc];
+    const int64_t r0 = (int64_t)(code >> 10) * TILE;
+    int T;
+    const TileLane L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
+    const int64_t vg = a.g.row_begin + L.r;
+    int qdj[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      qdj[h] = L.light ? (int)a.qD[vg * H + h] : 0;
+      smx[w][lane][h] = -INFINITY;
+    }
+    __syncwarp();
+    const int tlast = T - 1, nch = (T + 31) >> 5;
+    auto edge_of = [&](int t, int& row) -> int64_t {
+      row = tile_row(t < T ? t : tlast, L.end);
+      return __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
+    };
+    // pass A: per-row max of el = lrelu(e_pre)
+    for (int c = 0; c < nch; ++c) {
+      const int t = c * 32 + lane;
+      int row;
+      const int64_t e = edge_of(t, row);
+      float el[H];
+      int qdr[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) { qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row); el[h] = -INFINITY; }
+      if (t < T) {
+        const int64_t u = a.g.in_src[e];
+#pragma unroll
+        for (int h = 0; h < H; ++h) el[h] = lrelu(sddmm_add1(a.qS[u * H + h], scS.s, (int8_t)qdr[h], scD.s), a.slope);
+      }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ro = __shfl_up_sync(0xffffffffu, row, o);
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const float v = __shfl_up_sync(0xffffffffu, el[h], o);
+          if (lane >= o && ro == row) el[h] = fmaxf(el[h], v);
+        }
+      }
+      const int rn = __shfl_down_sync(0xffffffffu, row, 1);
+      if (lane == 31 || rn != row)
+#pragma unroll
+        for (int h = 0; h < H; ++h) smx[w][row][h] = fmaxf(smx[w][row][h], el[h]);
+      __syncwarp();
+    }
+    float mown[H], den[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) { mown[h] = (L.light && L.deg > 0) ? smx[w][lane][h] : 0.0f; den[h] = 0.0f; }
+    // pass B: ex = exp_p(el − m) (signed copy to alpha), den = sequential sum by the row owner
+    for (int c = 0; c < nch; ++c) {
+      const int base = c * 32, t = base + lane;
+      const int cnt = T - base < 32 ? T - base : 32;
+      int row;
+      const int64_t e = edge_of(t, row);
+      int qdr[H];
+      float mr[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row);
+        mr[h] = __shfl_sync(0xffffffffu, mown[h], row);
+      }
+      if (t < T) {
+        const int64_t u = a.g.in_src[e];
+        float sx[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const float ep = sddmm_add1(a.qS[u * H + h], scS.s, (int8_t)qdr[h], scD.s);
+          const float ex = exp_p(__fsub_rn(lrelu(ep, a.slope), mr[h]));
+          sbuf[w][lane][h] = ex;
+          sx[h] = ep > 0.0f ? ex : -ex;
+        }
+        if constexpr (H == 4) {
+          *reinterpret_cast<float4*>(a.alpha + e * 8) = make_float4(sx[0], sx[1], sx[2], sx[3]);
+        } else {
+#pragma unroll
+          for (int h = 0; h < H; ++h) a.alpha[e * 2 * H + h] = sx[h];
+        }
+      }
+      __syncwarp();
+      const int lo = (L.off > base ? L.off : base) - base;
+      const int hi = (L.end < base + cnt ? L.end : base + cnt) - base;
+      for (int i = lo; i < hi; ++i)
+#pragma unroll
+        for (int h = 0; h < H; ++h) den[h] = __fadd_rn(den[h], sbuf[w][i][h]);
+      __syncwarp();
+    }
+    if (L.light) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) { a.m[vg * H + h] = mown[h]; a.den[vg * H + h] = den[h]; }
+    }
+    // pass C: α = |ex| / den with the sign of e_pre
+    for (int c = 0; c < nch; ++c) {
+      const int t = c * 32 + lane;
+      int row;
+      const int64_t e = edge_of(t, row);
+      float dr[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) dr[h] = __shfl_sync(0xffffffffu, den[h], row);
+      if (t < T) {
+        if constexpr (H == 4) {
+          float4* p = reinterpret_cast<float4*>(a.alpha + e * 8);
+          const float4 x = *p;
+          const float xs[4] = {x.x, x.y, x.z, x.w};
+          float o[4];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const float al = __fdiv_rn(fabsf(xs[h]), dr[h]);
+            o[h] = signbit(xs[h]) ? -al : al;
+          }
+          *p = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            const float x = a.alpha[e * 2 * H + h];
+            const float al = __fdiv_rn(fabsf(x), dr[h]);
+            a.alpha[e * 2 * H + h] = signbit(x) ? -al : al;
+          }
+        }
+      }
+    }
+  }
+}
+
 // FS2: heavy segments -> segment Σ exp_p(el - m) (hden), m from all segment maxima of the row
 template <int H>
 __global__ void __launch_bounds__(256) k_fwd_stats2(const GatFwdArgs a) {
@@ -1339,7 +1489,7 @@ template <int H, int VPL>
 __global__ void __launch_bounds__(256, 3) k_fwd_agg5(const __grid_constant__ GatFwdArgs a,
                                                     const __grid_constant__ CUtensorMap tmap) {
   constexpr int HD = 32 * VPL;
-  extern __shared__ __align__(128) uint8_t dsm[];
+  extern __shared__ __align__(16) uint8_t dsm[];
   const int lane = threadIdx.x & 31;
   G5Warp W = g5_setup<H, VPL, false, 0>(dsm, 8);
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
@@ -2210,7 +2360,7 @@ template <int H, int VPL, int NW>
 __global__ void __launch_bounds__(NW * 32, 3) k_bwd_src5(const __grid_constant__ GatBwdArgs a,
                                                         const __grid_constant__ CUtensorMap tmap) {
   constexpr int HD = 32 * VPL;
-  extern __shared__ __align__(128) uint8_t dsm[];
+  extern __shared__ __align__(16) uint8_t dsm[];
   const int lane = threadIdx.x & 31;
   const int myh = lane / (32 / H);
   const bool leader = (lane % (32 / H)) == 0;
@@ -2833,17 +2983,27 @@ __global__ void __launch_bounds__(256) k_bwd_attn_grad(const GatBwdArgs a) {
   float das[VPL], dad[VPL];
 #pragma unroll
   for (int k = 0; k < VPL; ++k) { das[k] = 0.0f; dad[k] = 0.0f; }
-  for (int64_t ul = (int64_t)blockIdx.x * WPB + w; ul < a.g.n_local; ul += (int64_t)gridDim.x * WPB) {
-    const int64_t ug = a.g.row_begin + ul;
-    const float dS = a.dS[ug * H + myh];
-    const float dD = a.dD[ug * H + myh];
-    const Row<VPL> hw = load_row<VPL>(a.qHp + ug * a.ldHp + lane * VPL);
+  constexpr int RU = 4;   // rows in flight per warp
+  const int64_t nw = (int64_t)gridDim.x * WPB;
+  for (int64_t ul0 = (int64_t)blockIdx.x * WPB + w; ul0 < a.g.n_local; ul0 += nw * RU) {
+    Row<VPL> hw[RU];
+    float dS[RU], dD[RU];
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) {
-      const float hp = __fmul_rn(row_f<VPL>(hw, k), scH.s);
-      das[k] = __fmaf_rn(dS, hp, das[k]);
-      dad[k] = __fmaf_rn(dD, hp, dad[k]);
+    for (int i = 0; i < RU; ++i) {
+      const int64_t ul = ul0 + i * nw;
+      const int64_t ug = a.g.row_begin + (ul < a.g.n_local ? ul : 0);
+      dS[i] = ul < a.g.n_local ? a.dS[ug * H + myh] : 0.0f;
+      dD[i] = ul < a.g.n_local ? a.dD[ug * H + myh] : 0.0f;
+      hw[i] = load_row<VPL>(a.qHp + ug * a.ldHp + lane * VPL);
     }
+#pragma unroll
+    for (int i = 0; i < RU; ++i)
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const float hp = __fmul_rn(row_f<VPL>(hw[i], k), scH.s);
+        das[k] = __fmaf_rn(dS[i], hp, das[k]);
+        dad[k] = __fmaf_rn(dD[i], hp, dad[k]);
+      }
   }
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
@@ -2897,7 +3057,6 @@ bool gat_shape_supported(int heads, int head_dim) {
 cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
   if (a.g.n_local == 0) return cudaSuccess;
   const int hv = a.d.heads * 100 + a.d.hd / 32;
-  const int64_t items = a.g.n_local + a.plan.cap;
   int vpl, hpw;
   if (!cg_shape(a.d.head_dim, vpl, hpw)) return cudaErrorInvalidValue;
   const int64_t cg_items = (a.plan.cap + (a.g.n_local + TILE - 1) / TILE) * (a.d.hd / (32 * vpl));
@@ -2905,7 +3064,8 @@ cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
 #define X(H_, V_)                                                                                  \
   if (hv == H_ * 100 + V_) {                                                                       \
     ok = true;                                                                                     \
-    { ProfScope p("gat_fwd_stats", st);  k_fwd_stats<H_><<<item_grid(items), 256, 0, st>>>(a); }   \
+    { ProfScope p("gat_fwd_stats", st);                                                            \
+      k_fwd_stats_t<H_><<<item_grid(a.plan.cap + a.plan.tcap), 256, 0, st>>>(a); }                 \
     { ProfScope p("gat_fwd_stats2", st); k_fwd_stats2<H_><<<item_grid(a.plan.cap), 256, 0, st>>>(a); } \
   }
   TANGO_HV_CASES(X)
@@ -3074,7 +3234,7 @@ cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st) {
     { ProfScope p("gat_bwd_src_combine", st);                                                      \
       k_bwd_src_combine<H_, V_><<<item_grid(a.g.n_local), 256, 0, st>>>(a); }                     \
     { ProfScope p("gat_bwd_attn_grad", st);                                                        \
-      k_bwd_attn_grad<H_, V_><<<num_sms() * 2, 256, 0, st>>>(a); }                                 \
+      k_bwd_attn_grad<H_, V_><<<num_sms() * 4, 256, 0, st>>>(a); }                                 \
   }
   TANGO_HV_CASES(X)
 #undef X
