@@ -52,16 +52,41 @@ __device__ __forceinline__ uint32_t sr_half(const SR8& s, int j) {
   return (j & 1) ? (word >> 16) : (word & 0xFFFFu);
 }
 
-// Stochastic rounding of x*r (reading R4/R6): q = floor(xs) + (u < xs - floor(xs)), clamped.
-__device__ __forceinline__ int sr_quant(float x, float r, uint32_t hw16, int qmax) {
+// Stochastic rounding of x*r (reading R4/R6): q = floor(xs) + (u < xs - floor(xs)), clamped, with
+// u = hw16 * 2^-16.  Evaluated on the FMA/ALU pipes only (no XU conversions), bit-identical to the
+// plain definition: n = rint(xs) via the 1.5*2^23 magic (|xs| < 2^22), d = xs - n (exact), so
+// floor(xs) = n - [d < 0] and xs - floor(xs) = fl(d + 1) if d < 0 else d; u = (1 + hw16*2^-16) - 1
+// exactly.  Returns q as an integral float.
+__device__ __forceinline__ float sr_quant_f(float x, float r, uint32_t ubits /* hw16 << 7 */, float qmaxf) {
   const float xs = __fmul_rn(x, r);
-  const float f = floorf(xs);
-  const float fr = __fsub_rn(xs, f);
-  const float u = __fmul_rn(__uint2float_rn(hw16), 0x1p-16f);
-  int q = __float2int_rz(f) + (u < fr ? 1 : 0);
-  q = q > qmax ? qmax : q;
-  q = q < -qmax ? -qmax : q;
-  return q;
+  const float n = __fsub_rn(__fadd_rn(xs, 12582912.0f), 12582912.0f);
+  const float d = __fsub_rn(xs, n);
+  const bool neg = d < 0.0f;
+  const float fr = neg ? __fadd_rn(d, 1.0f) : d;
+  const float u = __fsub_rn(__uint_as_float(ubits | 0x3F800000u), 1.0f);
+  float q = neg ? __fsub_rn(n, 1.0f) : n;
+  q = (u < fr) ? __fadd_rn(q, 1.0f) : q;
+  return fminf(fmaxf(q, -qmaxf), qmaxf);
+}
+// bits (hw16 << 7) of half-word j of the group's Philox output
+__device__ __forceinline__ uint32_t sr_ubits(const SR8& s, int j) {
+  const uint32_t w = s.w[j >> 1];
+  return (j & 1) ? ((w >> 9) & 0x7FFF80u) : ((w << 7) & 0x7FFF80u);
+}
+// int8 code of an integral float q (|q| <= 127): low byte of the bits of q + 1.5*2^23
+__device__ __forceinline__ uint32_t q_byte_word(float q) { return __float_as_uint(__fadd_rn(q, 12582912.0f)); }
+__device__ __forceinline__ uint32_t pack4_low_bytes(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+  return __byte_perm(__byte_perm(b0, b1, 0x0040u), __byte_perm(b2, b3, 0x0040u), 0x5410u);
+}
+// SR of 8 consecutive elements sharing one Philox draw -> 8 codes packed little-endian
+__device__ __forceinline__ uint2 sr_quant8(const float (&v)[8], float r, const SR8& rnd, float qmaxf) {
+  uint32_t b[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) b[k] = q_byte_word(sr_quant_f(v[k], r, sr_ubits(rnd, k), qmaxf));
+  return make_uint2(pack4_low_bytes(b[0], b[1], b[2], b[3]), pack4_low_bytes(b[4], b[5], b[6], b[7]));
+}
+__device__ __forceinline__ int sr_quant(float x, float r, uint32_t hw16, int qmax) {
+  return (int)sr_quant_f(x, r, hw16 << 7, (float)qmax);
 }
 
 // Scale pair from amax (reading R1/R3/R7): s = amax/qmax, r = qmax/amax; amax = 0 -> s = r = 1.

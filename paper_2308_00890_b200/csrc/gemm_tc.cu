@@ -249,16 +249,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int g8 = 0; g8 < 4; ++g8) {
             const int64_t g = (p.g_row0 + row) * p.N + col0 + g8 * 8;   // N % 8 == 0
             const SR8 rnd = sr_draw8((uint64_t)(g >> 3), p.tag, p.step, p.seed);
-            uint32_t lo = 0, hi = 0;
+            float v[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const int i = g8 * 8 + k;
-              const float v = deq(r[i], sAB, has_rs, rs);
-              const int qq = (col0 + i < p.N) ? sr_quant(v, qs.r, sr_half(rnd, k), qmax) : 0;
-              const uint32_t byte = (uint32_t)(qq & 0xFF);
-              if (k < 4) lo |= byte << (8 * k); else hi |= byte << (8 * (k - 4));
-            }
-            packed[g8 * 2] = lo; packed[g8 * 2 + 1] = hi;
+            for (int k = 0; k < 8; ++k) v[k] = deq(r[g8 * 8 + k], sAB, has_rs, rs);
+            const uint2 pk = sr_quant8(v, qs.r, rnd, (float)qmax);
+            const bool in = col0 + g8 * 8 < p.N;   // N % 8 == 0: whole groups are in or out
+            packed[g8 * 2] = in ? pk.x : 0u; packed[g8 * 2 + 1] = in ? pk.y : 0u;
           }
           if (row_ok && col0 < p.ldq) {
             uint4* dst = reinterpret_cast<uint4*>(p.q_out + row * p.ldq + col0);

@@ -83,15 +83,7 @@ __global__ void __launch_bounds__(256) k_quantize(const float* __restrict__ x, i
       const float4* src = reinterpret_cast<const float4*>(x + e);
       const float4 a = __ldg(src), b = __ldg(src + 1);
       const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      uint32_t lo = 0, hi = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int qq = sr_quant(v[k], sc.r, sr_half(rnd, k), qmax);
-        const uint32_t byte = (uint32_t)(qq & 0xFF);
-        if (k < 4) lo |= byte << (8 * k);
-        else hi |= byte << (8 * (k - 4));
-      }
-      *reinterpret_cast<uint2*>(q + i * ld + j) = make_uint2(lo, hi);
+      *reinterpret_cast<uint2*>(q + i * ld + j) = sr_quant8(v, sc.r, rnd, (float)qmax);
     } else {
 #pragma unroll 1
       for (int k = 0; k < 8; ++k) {
