@@ -25,15 +25,25 @@ enum : int32_t { ST_OK = 0, ST_NONFINITE = 4 };
 // ------------------------------------------------------------------ Philox4x32-10 (reading R5)
 struct u32x4 { uint32_t x, y, z, w; };
 
-__device__ __forceinline__ u32x4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                           uint32_t k0, uint32_t k1) {
+// Round keys of Philox4x32-10 for a 64-bit seed (k0 = lo32, k1 = hi32, bumped by the Weyl constants
+// after each round), precomputed on the host so kernels read them as constant-bank operands.
+struct PhiloxKey { uint32_t k0[10], k1[10]; };
+__host__ __device__ inline PhiloxKey philox_key(uint64_t seed) {
+  PhiloxKey K;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    K.k0[r] = k0; K.k1[r] = k1;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  return K;
+}
+__device__ __forceinline__ u32x4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const PhiloxKey& K) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
     const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
     const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    const uint32_t n0 = hi1 ^ c1 ^ K.k0[r], n2 = hi0 ^ c3 ^ K.k1[r];
     c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;   // bump after each round (the last bump is unused)
   }
   return {c0, c1, c2, c3};
 }
@@ -41,8 +51,8 @@ __device__ __forceinline__ u32x4 philox10(uint32_t c0, uint32_t c1, uint32_t c2,
 // The 8 16-bit uniforms of the group of 8 consecutive elements starting at global index g8 = 8*blk
 // (reading R4): element j of the group takes half-word j: word j>>1, low half for even j.
 struct SR8 { uint32_t w[4]; };
-__device__ __forceinline__ SR8 sr_draw8(uint64_t blk, uint32_t tag, uint32_t step, uint64_t seed) {
-  u32x4 r = philox10((uint32_t)blk, (uint32_t)(blk >> 32), tag, step, (uint32_t)seed, (uint32_t)(seed >> 32));
+__device__ __forceinline__ SR8 sr_draw8(uint64_t blk, uint32_t tag, uint32_t step, const PhiloxKey& K) {
+  u32x4 r = philox10((uint32_t)blk, (uint32_t)(blk >> 32), tag, step, K);
   SR8 s;
   s.w[0] = r.x; s.w[1] = r.y; s.w[2] = r.z; s.w[3] = r.w;
   return s;
@@ -52,41 +62,40 @@ __device__ __forceinline__ uint32_t sr_half(const SR8& s, int j) {
   return (j & 1) ? (word >> 16) : (word & 0xFFFFu);
 }
 
-// Stochastic rounding of x*r (reading R4/R6): q = floor(xs) + (u < xs - floor(xs)), clamped, with
+// Stochastic rounding of x*r (reading R4/R6): q = floor(xs) + (u < xs - floor(xs)), clamped to ±qmax,
 // u = hw16 * 2^-16.  Evaluated on the FMA/ALU pipes only (no XU conversions), bit-identical to the
-// plain definition: n = rint(xs) via the 1.5*2^23 magic (|xs| < 2^22), d = xs - n (exact), so
-// floor(xs) = n - [d < 0] and xs - floor(xs) = fl(d + 1) if d < 0 else d; u = (1 + hw16*2^-16) - 1
-// exactly.  Returns q as an integral float.
-__device__ __forceinline__ float sr_quant_f(float x, float r, uint32_t ubits /* hw16 << 7 */, float qmaxf) {
+// plain definition: t = xs + 1.5*2^23 holds n = rint(xs) as bits 0x4B400000 + n (|xs| < 2^22),
+// d = xs - n is exact, floor(xs) = n - [d < 0] and xs - floor(xs) = fl(d + 1) if d < 0 else d;
+// u = (1 + hw16*2^-16) - 1 exactly.  Returns the bits 0x4B400000 + q (low byte = the int8 code).
+__device__ __forceinline__ uint32_t sr_qbits(float x, float r, uint32_t ubits /* hw16 << 7 */, int qmax) {
   const float xs = __fmul_rn(x, r);
-  const float n = __fsub_rn(__fadd_rn(xs, 12582912.0f), 12582912.0f);
+  const float t = __fadd_rn(xs, 12582912.0f);
+  const float n = __fsub_rn(t, 12582912.0f);
   const float d = __fsub_rn(xs, n);
   const bool neg = d < 0.0f;
   const float fr = neg ? __fadd_rn(d, 1.0f) : d;
   const float u = __fsub_rn(__uint_as_float(ubits | 0x3F800000u), 1.0f);
-  float q = neg ? __fsub_rn(n, 1.0f) : n;
-  q = (u < fr) ? __fadd_rn(q, 1.0f) : q;
-  return fminf(fmaxf(q, -qmaxf), qmaxf);
+  int qb = (int)__float_as_uint(t) - (neg ? 1 : 0) + (u < fr ? 1 : 0);
+  qb = min(max(qb, 0x4B400000 - qmax), 0x4B400000 + qmax);
+  return (uint32_t)qb;
 }
 // bits (hw16 << 7) of half-word j of the group's Philox output
 __device__ __forceinline__ uint32_t sr_ubits(const SR8& s, int j) {
   const uint32_t w = s.w[j >> 1];
   return (j & 1) ? ((w >> 9) & 0x7FFF80u) : ((w << 7) & 0x7FFF80u);
 }
-// int8 code of an integral float q (|q| <= 127): low byte of the bits of q + 1.5*2^23
-__device__ __forceinline__ uint32_t q_byte_word(float q) { return __float_as_uint(__fadd_rn(q, 12582912.0f)); }
 __device__ __forceinline__ uint32_t pack4_low_bytes(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
   return __byte_perm(__byte_perm(b0, b1, 0x0040u), __byte_perm(b2, b3, 0x0040u), 0x5410u);
 }
 // SR of 8 consecutive elements sharing one Philox draw -> 8 codes packed little-endian
-__device__ __forceinline__ uint2 sr_quant8(const float (&v)[8], float r, const SR8& rnd, float qmaxf) {
+__device__ __forceinline__ uint2 sr_quant8(const float (&v)[8], float r, const SR8& rnd, int qmax) {
   uint32_t b[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) b[k] = q_byte_word(sr_quant_f(v[k], r, sr_ubits(rnd, k), qmaxf));
+  for (int k = 0; k < 8; ++k) b[k] = sr_qbits(v[k], r, sr_ubits(rnd, k), qmax);
   return make_uint2(pack4_low_bytes(b[0], b[1], b[2], b[3]), pack4_low_bytes(b[4], b[5], b[6], b[7]));
 }
 __device__ __forceinline__ int sr_quant(float x, float r, uint32_t hw16, int qmax) {
-  return (int)sr_quant_f(x, r, hw16 << 7, (float)qmax);
+  return (int)sr_qbits(x, r, hw16 << 7, qmax) - 0x4B400000;
 }
 
 // Scale pair from amax (reading R1/R3/R7): s = amax/qmax, r = qmax/amax; amax = 0 -> s = r = 1.

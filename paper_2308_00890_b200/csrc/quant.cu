@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(256) k_absmax(const float* __restrict__ x, int
 // has global index g = g0 + i*cols + j.  Out: q[i*ld + j] (and, if qt, the transpose qt[j*ldt + i]).
 __global__ void __launch_bounds__(256) k_quantize(const float* __restrict__ x, int64_t rows, int64_t cols,
                                                   const float* __restrict__ rowscale, int64_t g0,
-                                                  const unsigned* __restrict__ amax_slot, int bits, uint64_t seed,
+                                                  const unsigned* __restrict__ amax_slot, int bits, const PhiloxKey key,
                                                   uint32_t step, uint32_t tag, int8_t* __restrict__ q, int64_t ld,
                                                   int8_t* __restrict__ qt, int64_t ldt, float* __restrict__ scale_out,
                                                   int32_t* __restrict__ status) {
@@ -74,16 +74,21 @@ __global__ void __launch_bounds__(256) k_quantize(const float* __restrict__ x, i
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const bool fast = (rowscale == nullptr) && (qt == nullptr) && ((g0 & 7) == 0) && ((cols & 7) == 0) &&
                     ((ld & 7) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  const bool dense = ld == cols;   // q[i*ld + j] = q[e]: no division in the fast loop
   for (int64_t blk = blk0 + tid; blk < blk1; blk += nthr) {
-    const SR8 rnd = sr_draw8((uint64_t)blk, tag, step, seed);
+    const SR8 rnd = sr_draw8((uint64_t)blk, tag, step, key);
     const int64_t gs = blk << 3;
     if (fast) {
       const int64_t e = gs - g0;  // first local element, multiple of 8, within one row
-      const int64_t i = e / cols, j = e - i * cols;
+      int64_t i = 0, j = e;
+      if (!dense) {
+        i = e / cols;
+        j = e - i * cols;
+      }
       const float4* src = reinterpret_cast<const float4*>(x + e);
       const float4 a = __ldg(src), b = __ldg(src + 1);
       const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      *reinterpret_cast<uint2*>(q + i * ld + j) = sr_quant8(v, sc.r, rnd, (float)qmax);
+      *reinterpret_cast<uint2*>(q + i * ld + j) = sr_quant8(v, sc.r, rnd, qmax);
     } else {
 #pragma unroll 1
       for (int k = 0; k < 8; ++k) {
@@ -140,7 +145,7 @@ cudaError_t launch_quantize(const float* x, int64_t rows, int64_t cols, const fl
   }
   const int64_t groups = (count + 15) / 8;
   ProfScope ps("quantize", st);
-  k_quantize<<<grid_for(groups, 256, 16), 256, 0, st>>>(x, rows, cols, rowscale, g0, amax_slot, bits, seed, step, tag,
+  k_quantize<<<grid_for(groups, 256, 16), 256, 0, st>>>(x, rows, cols, rowscale, g0, amax_slot, bits, philox_key(seed), step, tag,
                                                        q, ld, qt, ldt, scale_out, status);
   return cudaGetLastError();
 }
