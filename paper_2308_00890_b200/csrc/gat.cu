@@ -140,6 +140,26 @@ __device__ __forceinline__ float head_pick(const float (&x)[H], int h) {
   return r;
 }
 
+// ---- heavy-row helpers: every load of a batch is issued before the dependent arithmetic (hub rows
+// span up to ~32 segments; the folds stay in canonical order, only the loads are hoisted).
+template <int H>
+__device__ __forceinline__ void load_qh(const int8_t* __restrict__ p, int8_t (&o)[H]) {
+  if constexpr (H == 4) {
+    const uint32_t w = __ldg(reinterpret_cast<const unsigned*>(p));
+#pragma unroll
+    for (int h = 0; h < 4; ++h) o[h] = (int8_t)(w >> (8 * h));
+  } else if constexpr (H == 2) {
+    const uint32_t w = __ldg(reinterpret_cast<const unsigned short*>(p));
+    o[0] = (int8_t)w; o[1] = (int8_t)(w >> 8);
+  } else {
+#pragma unroll
+    for (int h = 0; h < H; ++h) o[h] = p[h];
+  }
+}
+constexpr int SEGB = 8;   // 32-edge chunks loaded per batch (256 edges)
+template <int H>
+__host__ __device__ constexpr int segb() { return H >= 8 ? 4 : SEGB; }   // staging fits 48 KB static smem
+
 // max over the segment of el = lrelu(e_pre) (lane-parallel; order-free), all lanes get the result
 template <int H>
 __device__ __forceinline__ void seg_max(const int32_t* __restrict__ src, int64_t eb, int64_t ee,
@@ -148,18 +168,30 @@ __device__ __forceinline__ void seg_max(const int32_t* __restrict__ src, int64_t
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int h = 0; h < H; ++h) mx[h] = -INFINITY;
-  for (int64_t e = eb + lane; e < ee; e += 32) {
-    const int64_t u = src[e];
+  for (int64_t base = eb; base < ee; base += 32 * SEGB) {
+    int u[SEGB];
 #pragma unroll
-    for (int h = 0; h < H; ++h) mx[h] = fmaxf(mx[h], lrelu(sddmm_add1(qS[u * H + h], sS, qd[h], sD), slope));
+    for (int i = 0; i < SEGB; ++i) {
+      const int64_t e = base + i * 32 + lane;
+      u[i] = e < ee ? src[e] : -1;
+    }
+    int8_t qs[SEGB][H];
+#pragma unroll
+    for (int i = 0; i < SEGB; ++i)
+      if (u[i] >= 0) load_qh<H>(qS + (int64_t)u[i] * H, qs[i]);
+#pragma unroll
+    for (int i = 0; i < SEGB; ++i)
+      if (u[i] >= 0)
+#pragma unroll
+        for (int h = 0; h < H; ++h) mx[h] = fmaxf(mx[h], lrelu(sddmm_add1(qs[i][h], sS, qd[h], sD), slope));
   }
 #pragma unroll
   for (int h = 0; h < H; ++h) mx[h] = warp_max(mx[h]);
 }
 
 // Σ over the segment of exp_p(el - m), sequential in edge order (one chunk: no folding).
-// Returns the sum for head `lane` in lanes < H.
-// Also stores ex with the sign of e_pre (the LeakyReLU branch) into sx[e][h] when sx != nullptr.
+// Returns the sum for head `lane` in lanes < H.  Stores ex with the sign of e_pre (the LeakyReLU
+// branch) into sx[e][h] (stride 2H).  buf: per-warp [32*SEGB][H] staging.
 template <int H>
 __device__ __forceinline__ float seg_sum_exp(const int32_t* __restrict__ src, int64_t eb, int64_t ee,
                                              const int8_t* __restrict__ qS, float sS, const int8_t (&qd)[H],
@@ -167,19 +199,38 @@ __device__ __forceinline__ float seg_sum_exp(const int32_t* __restrict__ src, in
                                              float* __restrict__ sx) {
   const int lane = threadIdx.x & 31;
   float part = 0.0f;
-  for (int64_t base = eb; base < ee; base += 32) {
-    const int cnt = (int)(ee - base < 32 ? ee - base : 32);
-    if (lane < cnt) {
-      const int64_t u = src[base + lane];
+  for (int64_t base = eb; base < ee; base += 32 * segb<H>()) {
+    int u[segb<H>()];
+#pragma unroll
+    for (int i = 0; i < segb<H>(); ++i) {
+      const int64_t e = base + i * 32 + lane;
+      u[i] = e < ee ? src[e] : -1;
+    }
+    int8_t qs[segb<H>()][H];
+#pragma unroll
+    for (int i = 0; i < segb<H>(); ++i)
+      if (u[i] >= 0) load_qh<H>(qS + (int64_t)u[i] * H, qs[i]);
+#pragma unroll
+    for (int i = 0; i < segb<H>(); ++i) {
+      if (u[i] < 0) continue;
+      const int64_t e = base + i * 32 + lane;
+      float o[H];
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        const float ep = sddmm_add1(qS[u * H + h], sS, qd[h], sD);
+        const float ep = sddmm_add1(qs[i][h], sS, qd[h], sD);
         const float ex = exp_p(__fsub_rn(lrelu(ep, slope), mx[h]));
-        buf[lane][h] = ex;
-        if (sx) sx[(base + lane) * 2 * H + h] = ep > 0.0f ? ex : -ex;
+        buf[i * 32 + lane][h] = ex;
+        o[h] = ep > 0.0f ? ex : -ex;
+      }
+      if constexpr (H == 4) {
+        *reinterpret_cast<float4*>(sx + e * 8) = make_float4(o[0], o[1], o[2], o[3]);
+      } else {
+#pragma unroll
+        for (int h = 0; h < H; ++h) sx[e * 2 * H + h] = o[h];
       }
     }
     __syncwarp();
+    const int cnt = (int)(ee - base < 32 * segb<H>() ? ee - base : 32 * segb<H>());
     if (lane < H)
       for (int i = 0; i < cnt; ++i) part = __fadd_rn(part, buf[i][lane]);
     __syncwarp();
@@ -187,7 +238,60 @@ __device__ __forceinline__ float seg_sum_exp(const int32_t* __restrict__ src, in
   return part;
 }
 
-// m = max over a heavy row's segment maxima, den = left fold of its segment sums (lane h), broadcast
+// Left fold x[base + 0] + x[base + 1] + ... (segment order) of per-segment scalars [slot][H], all
+// heads, all lanes get the result.  Lanes load one segment each; the fold runs over shuffles.
+template <int H>
+__device__ __forceinline__ void fold_segments(const float* __restrict__ x, int base, int nseg, float (&tot)[H]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int h = 0; h < H; ++h) tot[h] = 0.0f;
+  for (int j0 = 0; j0 < nseg; j0 += 32) {
+    const int j = j0 + lane;
+    float v[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) v[h] = j < nseg ? x[(int64_t)(base + j) * H + h] : 0.0f;
+    const int cnt = nseg - j0 < 32 ? nseg - j0 : 32;
+    for (int i = 0; i < cnt; ++i)
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const float y = __shfl_sync(0xffffffffu, v[h], i);
+        tot[h] = (j0 + i == 0) ? y : __fadd_rn(tot[h], y);
+      }
+  }
+}
+
+// Left fold of nseg per-segment row slices (this lane's VPL floats at src + j*stride), 4 in flight
+template <int VPL>
+__device__ __forceinline__ void fold_rows(const float* __restrict__ src, int64_t stride, int nseg,
+                                          float (&tot)[VPL]) {
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) tot[k] = src[k];
+  for (int j = 1; j < nseg; j += 4) {
+    float b[4][VPL];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (j + q < nseg) {
+        const float* p = src + (j + q) * stride;
+        if constexpr (VPL % 4 == 0) {
+#pragma unroll
+          for (int k = 0; k < VPL / 4; ++k) {
+            const float4 v = *reinterpret_cast<const float4*>(p + 4 * k);
+            b[q][4 * k] = v.x; b[q][4 * k + 1] = v.y; b[q][4 * k + 2] = v.z; b[q][4 * k + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) b[q][k] = p[k];
+        }
+      }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (j + q < nseg)
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) tot[k] = __fadd_rn(tot[k], b[q][k]);
+  }
+}
+
+// m = max over a heavy row's segment maxima, den = left fold of its segment sums, all lanes
 template <int H>
 __device__ __forceinline__ void heavy_row_stats(const float* __restrict__ hmax, const float* __restrict__ hden,
                                                 int base, int nseg, float (&mx)[H], float (&den)[H]) {
@@ -199,15 +303,7 @@ __device__ __forceinline__ void heavy_row_stats(const float* __restrict__ hmax, 
     for (int h = 0; h < H; ++h) mx[h] = fmaxf(mx[h], hmax[(int64_t)(base + j) * H + h]);
 #pragma unroll
   for (int h = 0; h < H; ++h) mx[h] = warp_max(mx[h]);
-  if (hden) {
-    float tot = 0.0f;
-    if (lane < H) {
-      tot = hden[(int64_t)base * H + lane];
-      for (int j = 1; j < nseg; ++j) tot = __fadd_rn(tot, hden[(int64_t)(base + j) * H + lane]);
-    }
-#pragma unroll
-    for (int h = 0; h < H; ++h) den[h] = __shfl_sync(0xffffffffu, tot, h);
-  }
+  if (hden) fold_segments<H>(hden, base, nseg, den);
 }
 
 // exact int8 -> fp32 of byte k of a word pre-XORed with 0x80808080: 2^23 + 128 + q - (2^23 + 128)
@@ -296,49 +392,6 @@ __device__ __forceinline__ int tile_next(unsigned act, int cur) {
 }
 
 // ================================================================== forward
-// FS: light rows -> m, den (final);  heavy segments -> segment max (hmax)
-template <int H>
-__global__ void __launch_bounds__(256) k_fwd_stats(const GatFwdArgs a) {
-  __shared__ float sh[WPB][32][H];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
-  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
-  const int64_t hc = load_count(a.plan.counts), nitems = a.g.n_local + hc;
-  FOR_ITEMS(item, a.work + 0, nitems) {
-    Seg s;
-    if (!decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s)) continue;
-    const int64_t vg = a.g.row_begin + s.vl;
-    int8_t qd[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) qd[h] = a.qD[vg * H + h];
-    float mx[H];
-    seg_max<H>(a.g.in_src, s.eb, s.ee, a.qS, scS.s, qd, scD.s, a.slope, mx);
-    if (s.slot >= 0) {
-      if (lane < H) a.hmax[(int64_t)s.slot * H + lane] = head_pick<H>(mx, lane);
-      continue;
-    }
-    if (s.ee == s.eb)
-#pragma unroll
-      for (int h = 0; h < H; ++h) mx[h] = 0.0f;
-    const float den = seg_sum_exp<H>(a.g.in_src, s.eb, s.ee, a.qS, scS.s, qd, scD.s, a.slope, mx, sh[w], a.alpha);
-    if (lane < H) {
-      a.m[vg * H + lane] = head_pick<H>(mx, lane);
-      a.den[vg * H + lane] = den;
-    }
-    // α = ex / den (IEEE division of |ex|; the sign bit keeps the LeakyReLU branch of e_pre)
-    float dh[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) dh[h] = __shfl_sync(0xffffffffu, den, h);
-    __syncwarp();
-    for (int64_t e = s.eb + lane; e < s.ee; e += 32)
-#pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const float x = a.alpha[e * 2 * H + h];
-        const float al = __fdiv_rn(fabsf(x), dh[h]);
-        a.alpha[e * 2 * H + h] = signbit(x) ? -al : al;
-      }
-  }
-}
 
 // FS (tiles): heavy segments -> segment max (hmax); light sub-tiles -> m, den and α for every edge.
 // Lane = edge of the tile's stream: the per-row max is a segmented lane scan (order-free), the per-row
@@ -493,7 +546,7 @@ __global__ void __launch_bounds__(256) k_fwd_stats_t(const GatFwdArgs a) {
 // FS2: heavy segments -> segment Σ exp_p(el - m) (hden), m from all segment maxima of the row
 template <int H>
 __global__ void __launch_bounds__(256) k_fwd_stats2(const GatFwdArgs a) {
-  __shared__ float sh[WPB][32][H];
+  __shared__ float sh[WPB][32 * segb<H>()][H];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
@@ -522,13 +575,26 @@ __global__ void __launch_bounds__(256) k_fwd_alpha3(const GatFwdArgs a) {
     decode_item(si, hcnt, a.g.in_ptr, a.plan, a.g.chunk, s);
     float mx[H], den[H];
     heavy_row_stats<H>(a.hmax, a.hden, s.base, s.nseg, mx, den);
-    for (int64_t e = s.eb + lane; e < s.ee; e += 32)
+    for (int64_t base = s.eb; base < s.ee; base += 32 * SEGB) {
+      float x[SEGB][H];
 #pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const float x = a.alpha[e * 2 * H + h];
-        const float al = __fdiv_rn(fabsf(x), den[h]);
-        a.alpha[e * 2 * H + h] = signbit(x) ? -al : al;
+      for (int i = 0; i < SEGB; ++i) {
+        const int64_t e = base + i * 32 + lane;
+        if (e < s.ee)
+#pragma unroll
+          for (int h = 0; h < H; ++h) x[i][h] = a.alpha[e * 2 * H + h];
       }
+#pragma unroll
+      for (int i = 0; i < SEGB; ++i) {
+        const int64_t e = base + i * 32 + lane;
+        if (e < s.ee)
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            const float al = __fdiv_rn(fabsf(x[i][h]), den[h]);
+            a.alpha[e * 2 * H + h] = signbit(x[i][h]) ? -al : al;
+          }
+      }
+    }
   }
 }
 
@@ -2836,14 +2902,7 @@ __global__ void __launch_bounds__(256) k_fwd_combine(const GatFwdArgs a) {
       a.den[vg * H + lane] = head_pick<H>(den, lane);
     }
     float tot[VPL];
-    const float* src = a.hagg + (int64_t)base * HD + lane * VPL;
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) tot[k] = src[k];
-    for (int j = 1; j < nseg; ++j) {
-      const float* p = src + (int64_t)j * HD;
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) tot[k] = __fadd_rn(tot[k], p[k]);
-    }
+    fold_rows<VPL>(a.hagg + (int64_t)base * HD + lane * VPL, HD, nseg, tot);
     float* dst = a.Hout + vl * HD + lane * VPL;
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
@@ -2860,79 +2919,75 @@ __global__ void __launch_bounds__(256) k_fwd_combine(const GatFwdArgs a) {
   }
 }
 
-// Pass 2 over a segment: ∂E = α(∂α − P[v]), ∂E_pre (LeakyReLU backward), Σ ∂E_pre (lane h).
+// ∂E = |α|(∂α − P[v]), ∂E_pre (stored beside α) and the segment's sequential Σ ∂E_pre (returned in
+// lanes < H), from the stored signed α (its sign bit is the LeakyReLU branch of e_pre).
 template <int H>
-__device__ __forceinline__ float bwd_dst_pass2(const GatBwdArgs& a, const Seg& s, const int8_t (&qd)[H],
-                                               const float (&mh)[H], const float (&dh)[H], const float (&P)[H],
-                                               float sS, float sD, float (*ba)[H]) {
+__device__ __forceinline__ float bwd_dst_pass2(const GatBwdArgs& a, const Seg& s, const float (&P)[H],
+                                               float (*buf)[H]) {
   const int lane = threadIdx.x & 31;
   float part = 0.0f;
-  for (int64_t base = s.eb; base < s.ee; base += 32) {
-    const int cnt = (int)(s.ee - base < 32 ? s.ee - base : 32);
-    if (lane < cnt) {
-      const int64_t e = base + lane;
-      const int64_t u = a.g.in_src[e];
+  for (int64_t base = s.eb; base < s.ee; base += 32 * segb<H>()) {
+    float x[segb<H>()][H], dl[segb<H>()][H];
 #pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const float ep = sddmm_add1(a.qS[u * H + h], sS, qd[h], sD);
-        const float al = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, a.slope), mh[h])), dh[h]);
-        const float dE = __fmul_rn(al, __fsub_rn(a.dalpha[e * H + h], P[h]));
-        ba[lane][h] = ep > 0.0f ? dE : __fmul_rn(dE, a.slope);
-        a.alpha_dE[e * 2 * H + H + h] = ba[lane][h];   // ∂E_pre beside α
-      }
+    for (int i = 0; i < segb<H>(); ++i) {
+      const int64_t e = base + i * 32 + lane;
+      if (e < s.ee)
+#pragma unroll
+        for (int h = 0; h < H; ++h) { x[i][h] = a.alpha[e * 2 * H + h]; dl[i][h] = a.dalpha[e * H + h]; }
+    }
+#pragma unroll
+    for (int i = 0; i < segb<H>(); ++i) {
+      const int64_t e = base + i * 32 + lane;
+      if (e < s.ee)
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const float dE = __fmul_rn(fabsf(x[i][h]), __fsub_rn(dl[i][h], P[h]));
+          const float o = signbit(x[i][h]) ? __fmul_rn(dE, a.slope) : dE;
+          buf[i * 32 + lane][h] = o;
+          a.alpha_dE[e * 2 * H + H + h] = o;
+        }
     }
     __syncwarp();
+    const int cnt = (int)(s.ee - base < 32 * segb<H>() ? s.ee - base : 32 * segb<H>());
     if (lane < H)
-      for (int i = 0; i < cnt; ++i) part = __fadd_rn(part, ba[i][lane]);
+      for (int i = 0; i < cnt; ++i) part = __fadd_rn(part, buf[i][lane]);
     __syncwarp();
   }
   return part;
 }
 
-
 // BD2: heavy segments -> P (fold of hP; segment 0 writes it), ∂D partial (hdD)
 template <int H>
 __global__ void __launch_bounds__(256) k_bwd_dst2(const GatBwdArgs a) {
-  __shared__ float sh_a[WPB][32][H];
+  __shared__ float sh_a[WPB][32 * segb<H>()][H];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
-  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t hcnt = load_count(a.pin.counts);
   FOR_ITEMS(si, a.work + 1, hcnt) {
     Seg s;
     decode_item(si, hcnt, a.g.in_ptr, a.pin, a.g.chunk, s);
     const int64_t vg = a.g.row_begin + s.vl;
-    int8_t qd[H];
-    float mh[H], dh[H], P[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) { qd[h] = a.qD[vg * H + h]; mh[h] = a.m[vg * H + h]; dh[h] = a.den[vg * H + h]; }
-    float tot = 0.0f;
-    if (lane < H) {
-      tot = a.hP[(int64_t)s.base * H + lane];
-      for (int j = 1; j < s.nseg; ++j) tot = __fadd_rn(tot, a.hP[(int64_t)(s.base + j) * H + lane]);
-      if (s.c == 0) a.P[vg * H + lane] = tot;
-    }
-#pragma unroll
-    for (int h = 0; h < H; ++h) P[h] = __shfl_sync(0xffffffffu, tot, h);
-    const float dDp = bwd_dst_pass2<H>(a, s, qd, mh, dh, P, scS.s, scD.s, sh_a[w]);
+    float P[H];
+    fold_segments<H>(a.hP, s.base, s.nseg, P);
+    if (s.c == 0 && lane < H) a.P[vg * H + lane] = head_pick<H>(P, lane);
+    const float dDp = bwd_dst_pass2<H>(a, s, P, sh_a[w]);
     if (lane < H) a.hdD[si * H + lane] = dDp;
   }
 }
 
-// BD3: heavy rows -> ∂D = fold of hdD
+// BD3: heavy rows -> ∂D = fold of hdD (one warp per heavy row)
 template <int H>
 __global__ void __launch_bounds__(256) k_bwd_dst3(const GatBwdArgs a) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
   const int64_t hrows = load_count(a.pin.counts + 1);
-  if (t >= hrows * H) return;
-  const int64_t vl = a.pin.hrow[t / H];
-  const int h = (int)(t % H);
-  const int base = a.pin.hbase[vl];
-  const int64_t deg = a.g.in_ptr[vl + 1] - a.g.in_ptr[vl];
-  const int nseg = (int)((deg + a.g.chunk - 1) / a.g.chunk);
-  float tot = a.hdD[(int64_t)base * H + h];
-  for (int j = 1; j < nseg; ++j) tot = __fadd_rn(tot, a.hdD[(int64_t)(base + j) * H + h]);
-  a.dD[(a.g.row_begin + vl) * H + h] = tot;
+  FOR_ITEMS(r, a.work + 5, hrows) {
+    const int64_t vl = a.pin.hrow[r];
+    const int base = a.pin.hbase[vl];
+    const int64_t deg = a.g.in_ptr[vl + 1] - a.g.in_ptr[vl];
+    const int nseg = (int)((deg + a.g.chunk - 1) / a.g.chunk);
+    float tot[H];
+    fold_segments<H>(a.hdD, base, nseg, tot);
+    if (lane < H) a.dD[(a.g.row_begin + vl) * H + lane] = head_pick<H>(tot, lane);
+  }
 }
 
 // BC: heavy out-rows -> fold ∂S and aggregation partials in chunk order, finalize ∂H′
@@ -2951,17 +3006,11 @@ __global__ void __launch_bounds__(256) k_bwd_src_combine(const GatBwdArgs a) {
     const int base = a.pout.hbase[ul];
     const int64_t deg = a.g.out_ptr[ul + 1] - a.g.out_ptr[ul];
     const int nseg = (int)((deg + a.g.chunk - 1) / a.g.chunk);
-    float dS = a.hdS[(int64_t)base * H + myh];
-    for (int j = 1; j < nseg; ++j) dS = __fadd_rn(dS, a.hdS[(int64_t)(base + j) * H + myh]);
+    float dSh[H];
+    fold_segments<H>(a.hdS, base, nseg, dSh);
+    const float dS = head_pick<H>(dSh, myh);
     float tot[VPL];
-    const float* src = a.hagg + (int64_t)base * HD + lane * VPL;
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) tot[k] = src[k];
-    for (int j = 1; j < nseg; ++j) {
-      const float* p = src + (int64_t)j * HD;
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) tot[k] = __fadd_rn(tot[k], p[k]);
-    }
+    fold_rows<VPL>(a.hagg + (int64_t)base * HD + lane * VPL, HD, nseg, tot);
     bwd_src_finalize<VPL>(a, ul, ug, myh, dS, tot, scG.s, amax_loc, H);
   }
   amax_flush(a.amax_dHp, amax_loc);
@@ -3162,7 +3211,7 @@ cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st) {
     ok = true;                                                                                     \
     { ProfScope p("gat_bwd_dst2", st); k_bwd_dst2<H_><<<item_grid(a.pin.cap), 256, 0, st>>>(a); }  \
     { ProfScope p("gat_bwd_dst3", st);                                                             \
-      k_bwd_dst3<H_><<<(unsigned)((a.g.n_local * H_ + 255) / 256), 256, 0, st>>>(a); }            \
+      k_bwd_dst3<H_><<<num_sms() * 2, 256, 0, st>>>(a); }                                         \
   }
   TANGO_HV_CASES(X)
 #undef X
