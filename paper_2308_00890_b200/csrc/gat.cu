@@ -3084,6 +3084,14 @@ static int item_grid(int64_t items) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// Heavy-row kernels: the number of heavy segments / rows is a device count (plan), usually small;
+// a grid of 2 blocks per SM keeps the work-queue claims (one atomic per warp) cheap.
+static int heavy_grid(int64_t cap) {
+  const int g = item_grid(cap);
+  const int c = num_sms() * 2;
+  return g < c ? g : c;
+}
+
 // (H, HD/32) for the row-wide kernels, (VPL, HPW) head-group shape for the gather kernels
 #define TANGO_HV_CASES(X) X(1, 2) X(1, 4) X(1, 8) X(1, 16) X(2, 2) X(2, 4) X(2, 8) X(2, 16) \
                           X(4, 2) X(4, 4) X(4, 8) X(4, 16) X(8, 2) X(8, 4) X(8, 8) X(8, 16)
@@ -3115,7 +3123,7 @@ cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
     ok = true;                                                                                     \
     { ProfScope p("gat_fwd_stats", st);                                                            \
       k_fwd_stats_t<H_><<<item_grid(a.plan.cap + a.plan.tcap), 256, 0, st>>>(a); }                 \
-    { ProfScope p("gat_fwd_stats2", st); k_fwd_stats2<H_><<<item_grid(a.plan.cap), 256, 0, st>>>(a); } \
+    { ProfScope p("gat_fwd_stats2", st); k_fwd_stats2<H_><<<heavy_grid(a.plan.cap), 256, 0, st>>>(a); } \
   }
   TANGO_HV_CASES(X)
 #undef X
@@ -3125,7 +3133,7 @@ cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
 #define X(H_, V_)                                                                                  \
   if (hv == H_ * 100 + V_) {                                                                       \
     ok = true;                                                                                     \
-    { ProfScope p("gat_fwd_alpha3", st); k_fwd_alpha3<H_><<<item_grid(a.plan.cap), 256, 0, st>>>(a); } \
+    { ProfScope p("gat_fwd_alpha3", st); k_fwd_alpha3<H_><<<heavy_grid(a.plan.cap), 256, 0, st>>>(a); } \
     { ProfScope p("gat_fwd_agg", st);                                                              \
       if (V_ >= 4) {                                                                               \
         constexpr int smem = 8 * g4_warp_smem<H_, (V_ >= 4 ? V_ : 4), false>();                     \
@@ -3154,7 +3162,7 @@ cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
         k_fwd_agg2<H_, V_><<<item_grid(a.plan.cap + a.plan.tcap), 256, 0, st>>>(a);               \
       } }                                                                                          \
     { ProfScope p("gat_fwd_combine", st);                                                          \
-      k_fwd_combine<H_, V_><<<item_grid(a.g.n_local), 256, 0, st>>>(a); }                           \
+      k_fwd_combine<H_, V_><<<heavy_grid(a.plan.cap), 256, 0, st>>>(a); }                           \
   }
   TANGO_HV_CASES(X)
 #undef X
@@ -3209,9 +3217,9 @@ cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st) {
 #define X(H_, V_)                                                                                  \
   if (hv == H_ * 100 + V_) {                                                                       \
     ok = true;                                                                                     \
-    { ProfScope p("gat_bwd_dst2", st); k_bwd_dst2<H_><<<item_grid(a.pin.cap), 256, 0, st>>>(a); }  \
+    { ProfScope p("gat_bwd_dst2", st); k_bwd_dst2<H_><<<heavy_grid(a.pin.cap), 256, 0, st>>>(a); }  \
     { ProfScope p("gat_bwd_dst3", st);                                                             \
-      k_bwd_dst3<H_><<<num_sms() * 2, 256, 0, st>>>(a); }                                         \
+      k_bwd_dst3<H_><<<heavy_grid(a.pin.cap), 256, 0, st>>>(a); }                                         \
   }
   TANGO_HV_CASES(X)
 #undef X
@@ -3281,7 +3289,7 @@ cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st) {
   if (hv == H_ * 100 + V_) {                                                                       \
     ok = true;                                                                                     \
     { ProfScope p("gat_bwd_src_combine", st);                                                      \
-      k_bwd_src_combine<H_, V_><<<item_grid(a.g.n_local), 256, 0, st>>>(a); }                     \
+      k_bwd_src_combine<H_, V_><<<heavy_grid(a.pout.cap), 256, 0, st>>>(a); }                     \
     { ProfScope p("gat_bwd_attn_grad", st);                                                        \
       k_bwd_attn_grad<H_, V_><<<num_sms() * 4, 256, 0, st>>>(a); }                                 \
   }
