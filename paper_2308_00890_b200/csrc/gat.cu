@@ -396,12 +396,23 @@ __device__ __forceinline__ int tile_next(unsigned act, int cur) {
 // FS (tiles): heavy segments -> segment max (hmax); light sub-tiles -> m, den and α for every edge.
 // Lane = edge of the tile's stream: the per-row max is a segmented lane scan (order-free), the per-row
 // Σ exp_p(el − m) is folded sequentially in edge order by the row's owner lane (canonical order; a
-// light row is one chunk), then α = |ex| / den keeps the sign of e_pre.
+// light row is one chunk), then α = |ex| / den keeps the sign of e_pre.  Tiles of up to FS_TC edges
+// keep el / ex, the row and the edge id of every stream position in shared memory (one global pass);
+// longer tiles recompute them per pass.
+constexpr int FS_TC = 384;
+template <int H>
+__host__ __device__ constexpr int fs_warp_smem() { return FS_TC * H * 4 + FS_TC * 4 + FS_TC + 2 * 32 * H * 4; }
+
 template <int H>
 __global__ void __launch_bounds__(256) k_fwd_stats_t(const GatFwdArgs a) {
-  __shared__ float smx[WPB][32][H];
-  __shared__ float sbuf[WPB][32][H];
+  extern __shared__ __align__(16) uint8_t fsm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wsm = fsm + w * fs_warp_smem<H>();
+  float (*cx)[H] = reinterpret_cast<float (*)[H]>(wsm);                          // [FS_TC][H] el -> ex
+  int* ce = reinterpret_cast<int*>(wsm + FS_TC * H * 4);                          // [FS_TC] edge id
+  float (*smx)[H] = reinterpret_cast<float (*)[H]>(wsm + FS_TC * H * 4 + FS_TC * 4);        // [32][H]
+  float (*sbuf)[H] = smx + 32;                                                    // [32][H]
+  uint8_t* crow = wsm + FS_TC * H * 4 + FS_TC * 4 + 2 * 32 * H * 4;               // [FS_TC]
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t n = a.g.n_local, hc = load_count(a.plan.counts);
@@ -424,11 +435,12 @@ __global__ void __launch_bounds__(256) k_fwd_stats_t(const GatFwdArgs a) {
     int T;
     const TileLane L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
     const int64_t vg = a.g.row_begin + L.r;
+    const bool cached = T <= FS_TC;
     int qdj[H];
 #pragma unroll
     for (int h = 0; h < H; ++h) {
       qdj[h] = L.light ? (int)a.qD[vg * H + h] : 0;
-      smx[w][lane][h] = -INFINITY;
+      smx[lane][h] = -INFINITY;
     }
     __syncwarp();
     const int tlast = T - 1, nch = (T + 31) >> 5;
@@ -436,19 +448,32 @@ __global__ void __launch_bounds__(256) k_fwd_stats_t(const GatFwdArgs a) {
       row = tile_row(t < T ? t : tlast, L.end);
       return __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
     };
-    // pass A: per-row max of el = lrelu(e_pre)
+    // el of stream position t (lane), computed from the graph (pass A, or any pass when not cached)
+    auto el_of = [&](int t, int row, int64_t e, float (&ep)[H]) {
+      int qdr[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row);
+      if (t < T) {
+        int8_t qs[H];
+        load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, qs);
+#pragma unroll
+        for (int h = 0; h < H; ++h) ep[h] = sddmm_add1(qs[h], scS.s, (int8_t)qdr[h], scD.s);
+      }
+    };
+    // pass A: e_pre, per-row max of el = lrelu(e_pre)
     for (int c = 0; c < nch; ++c) {
       const int t = c * 32 + lane;
       int row;
       const int64_t e = edge_of(t, row);
-      float el[H];
-      int qdr[H];
+      float ep[H], el[H];
+      el_of(t, row, e, ep);
 #pragma unroll
-      for (int h = 0; h < H; ++h) { qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row); el[h] = -INFINITY; }
-      if (t < T) {
-        const int64_t u = a.g.in_src[e];
+      for (int h = 0; h < H; ++h) el[h] = t < T ? lrelu(ep[h], a.slope) : -INFINITY;
+      if (cached && t < T) {
 #pragma unroll
-        for (int h = 0; h < H; ++h) el[h] = lrelu(sddmm_add1(a.qS[u * H + h], scS.s, (int8_t)qdr[h], scD.s), a.slope);
+        for (int h = 0; h < H; ++h) cx[t][h] = ep[h];
+        ce[t] = (int)e;
+        crow[t] = (uint8_t)row;
       }
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -462,36 +487,43 @@ __global__ void __launch_bounds__(256) k_fwd_stats_t(const GatFwdArgs a) {
       const int rn = __shfl_down_sync(0xffffffffu, row, 1);
       if (lane == 31 || rn != row)
 #pragma unroll
-        for (int h = 0; h < H; ++h) smx[w][row][h] = fmaxf(smx[w][row][h], el[h]);
+        for (int h = 0; h < H; ++h) smx[row][h] = fmaxf(smx[row][h], el[h]);
       __syncwarp();
     }
     float mown[H], den[H];
 #pragma unroll
-    for (int h = 0; h < H; ++h) { mown[h] = (L.light && L.deg > 0) ? smx[w][lane][h] : 0.0f; den[h] = 0.0f; }
-    // pass B: ex = exp_p(el − m) (signed copy to alpha), den = sequential sum by the row owner
+    for (int h = 0; h < H; ++h) { mown[h] = (L.light && L.deg > 0) ? smx[lane][h] : 0.0f; den[h] = 0.0f; }
+    // pass B: ex = exp_p(el − m) with the sign of e_pre, den = sequential sum by the row owner
     for (int c = 0; c < nch; ++c) {
       const int base = c * 32, t = base + lane;
       const int cnt = T - base < 32 ? T - base : 32;
       int row;
-      const int64_t e = edge_of(t, row);
-      int qdr[H];
+      int64_t e = 0;
+      float ep[H];
+      if (cached) {
+        row = crow[t < T ? t : tlast];
+        if (t < T)
+#pragma unroll
+          for (int h = 0; h < H; ++h) ep[h] = cx[t][h];
+      } else {
+        e = edge_of(t, row);
+        el_of(t, row, e, ep);
+      }
       float mr[H];
 #pragma unroll
-      for (int h = 0; h < H; ++h) {
-        qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row);
-        mr[h] = __shfl_sync(0xffffffffu, mown[h], row);
-      }
+      for (int h = 0; h < H; ++h) mr[h] = __shfl_sync(0xffffffffu, mown[h], row);
       if (t < T) {
-        const int64_t u = a.g.in_src[e];
         float sx[H];
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-          const float ep = sddmm_add1(a.qS[u * H + h], scS.s, (int8_t)qdr[h], scD.s);
-          const float ex = exp_p(__fsub_rn(lrelu(ep, a.slope), mr[h]));
-          sbuf[w][lane][h] = ex;
-          sx[h] = ep > 0.0f ? ex : -ex;
+          const float ex = exp_p(__fsub_rn(lrelu(ep[h], a.slope), mr[h]));
+          sbuf[lane][h] = ex;
+          sx[h] = ep[h] > 0.0f ? ex : -ex;
         }
-        if constexpr (H == 4) {
+        if (cached) {
+#pragma unroll
+          for (int h = 0; h < H; ++h) cx[t][h] = sx[h];
+        } else if constexpr (H == 4) {
           *reinterpret_cast<float4*>(a.alpha + e * 8) = make_float4(sx[0], sx[1], sx[2], sx[3]);
         } else {
 #pragma unroll
@@ -503,7 +535,7 @@ __global__ void __launch_bounds__(256) k_fwd_stats_t(const GatFwdArgs a) {
       const int hi = (L.end < base + cnt ? L.end : base + cnt) - base;
       for (int i = lo; i < hi; ++i)
 #pragma unroll
-        for (int h = 0; h < H; ++h) den[h] = __fadd_rn(den[h], sbuf[w][i][h]);
+        for (int h = 0; h < H; ++h) den[h] = __fadd_rn(den[h], sbuf[i][h]);
       __syncwarp();
     }
     if (L.light) {
@@ -514,32 +546,39 @@ __global__ void __launch_bounds__(256) k_fwd_stats_t(const GatFwdArgs a) {
     for (int c = 0; c < nch; ++c) {
       const int t = c * 32 + lane;
       int row;
-      const int64_t e = edge_of(t, row);
+      int64_t e;
+      if (cached) {
+        row = crow[t < T ? t : tlast];
+        e = t < T ? ce[t] : 0;
+      } else {
+        e = edge_of(t, row);
+      }
       float dr[H];
 #pragma unroll
       for (int h = 0; h < H; ++h) dr[h] = __shfl_sync(0xffffffffu, den[h], row);
       if (t < T) {
-        if constexpr (H == 4) {
-          float4* p = reinterpret_cast<float4*>(a.alpha + e * 8);
-          const float4 x = *p;
-          const float xs[4] = {x.x, x.y, x.z, x.w};
-          float o[4];
+        float xs[H], o[H];
+        if (cached) {
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const float al = __fdiv_rn(fabsf(xs[h]), dr[h]);
-            o[h] = signbit(xs[h]) ? -al : al;
-          }
-          *p = make_float4(o[0], o[1], o[2], o[3]);
+          for (int h = 0; h < H; ++h) xs[h] = cx[t][h];
         } else {
 #pragma unroll
-          for (int h = 0; h < H; ++h) {
-            const float x = a.alpha[e * 2 * H + h];
-            const float al = __fdiv_rn(fabsf(x), dr[h]);
-            a.alpha[e * 2 * H + h] = signbit(x) ? -al : al;
-          }
+          for (int h = 0; h < H; ++h) xs[h] = a.alpha[e * 2 * H + h];
+        }
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const float al = __fdiv_rn(fabsf(xs[h]), dr[h]);
+          o[h] = signbit(xs[h]) ? -al : al;
+        }
+        if constexpr (H == 4) {
+          *reinterpret_cast<float4*>(a.alpha + e * 8) = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+          for (int h = 0; h < H; ++h) a.alpha[e * 2 * H + h] = o[h];
         }
       }
     }
+    __syncwarp();
   }
 }
 
@@ -3023,46 +3062,64 @@ template <int H, int VPL>
 __global__ void __launch_bounds__(256) k_bwd_attn_grad(const GatBwdArgs a) {
   constexpr int LPH = 32 / H;
   constexpr int HD = 32 * VPL;
-  __shared__ float sh_da[2][HD];
+  constexpr int RU = 8;   // rows in flight per warp
+  __shared__ float sh_da[WPB][2][HD];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int myh = lane / LPH;
-  for (int j = threadIdx.x; j < 2 * HD; j += blockDim.x) (&sh_da[0][0])[j] = 0.0f;
-  __syncthreads();
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
   float das[VPL], dad[VPL];
 #pragma unroll
   for (int k = 0; k < VPL; ++k) { das[k] = 0.0f; dad[k] = 0.0f; }
-  constexpr int RU = 4;   // rows in flight per warp
-  const int64_t nw = (int64_t)gridDim.x * WPB;
-  for (int64_t ul0 = (int64_t)blockIdx.x * WPB + w; ul0 < a.g.n_local; ul0 += nw * RU) {
+  // each warp streams a contiguous range of rows, RU rows per step
+  const int64_t nw = (int64_t)gridDim.x * WPB, wid = (int64_t)blockIdx.x * WPB + w;
+  const int64_t per = (a.g.n_local + nw - 1) / nw;
+  const int64_t rb = wid * per, re = rb + per < a.g.n_local ? rb + per : a.g.n_local;
+  for (int64_t ul0 = rb; ul0 < re; ul0 += RU) {
     Row<VPL> hw[RU];
     float dS[RU], dD[RU];
 #pragma unroll
     for (int i = 0; i < RU; ++i) {
-      const int64_t ul = ul0 + i * nw;
-      const int64_t ug = a.g.row_begin + (ul < a.g.n_local ? ul : 0);
-      dS[i] = ul < a.g.n_local ? a.dS[ug * H + myh] : 0.0f;
-      dD[i] = ul < a.g.n_local ? a.dD[ug * H + myh] : 0.0f;
+      const int64_t ul = ul0 + i < re ? ul0 + i : rb;
+      const int64_t ug = a.g.row_begin + ul;
+      dS[i] = ul0 + i < re ? a.dS[ug * H + myh] : 0.0f;
+      dD[i] = ul0 + i < re ? a.dD[ug * H + myh] : 0.0f;
       hw[i] = load_row<VPL>(a.qHp + ug * a.ldHp + lane * VPL);
     }
 #pragma unroll
-    for (int i = 0; i < RU; ++i)
+    for (int i = 0; i < RU; ++i) {
+      if constexpr (VPL < 4) {
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) {
-        const float hp = __fmul_rn(row_f<VPL>(hw[i], k), scH.s);
-        das[k] = __fmaf_rn(dS[i], hp, das[k]);
-        dad[k] = __fmaf_rn(dD[i], hp, dad[k]);
+        for (int k = 0; k < VPL; ++k) {
+          const float hp = __fmul_rn(row_f<VPL>(hw[i], k), scH.s);
+          das[k] = __fmaf_rn(dS[i], hp, das[k]);
+          dad[k] = __fmaf_rn(dD[i], hp, dad[k]);
+        }
+        continue;
       }
+      const float2 s2 = make_float2(dS[i], dS[i]), d2 = make_float2(dD[i], dD[i]);
+#pragma unroll
+      for (int q = 0; q < VPL / 4; ++q) {
+        const uint32_t wx = hw[i].w[q] ^ 0x80808080u;
+#pragma unroll
+        for (int z = 0; z < 2; ++z) {
+          const float2 c = codes2(wx, z ? 0x7442u : 0x7440u, z ? 0x7443u : 0x7441u);
+          const float2 hp = make_float2(__fmul_rn(c.x, scH.s), __fmul_rn(c.y, scH.s));
+          const float2 sa = __ffma2_rn(s2, hp, make_float2(das[4 * q + 2 * z], das[4 * q + 2 * z + 1]));
+          const float2 da = __ffma2_rn(d2, hp, make_float2(dad[4 * q + 2 * z], dad[4 * q + 2 * z + 1]));
+          das[4 * q + 2 * z] = sa.x; das[4 * q + 2 * z + 1] = sa.y;
+          dad[4 * q + 2 * z] = da.x; dad[4 * q + 2 * z + 1] = da.y;
+        }
+      }
+    }
   }
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    atomicAdd(&sh_da[0][lane * VPL + k], das[k]);
-    atomicAdd(&sh_da[1][lane * VPL + k], dad[k]);
-  }
+  for (int k = 0; k < VPL; ++k) { sh_da[w][0][lane * VPL + k] = das[k]; sh_da[w][1][lane * VPL + k] = dad[k]; }
   __syncthreads();
-  for (int j = threadIdx.x; j < HD; j += blockDim.x) {
-    atomicAdd(a.da_src + j, sh_da[0][j]);
-    atomicAdd(a.da_dst + j, sh_da[1][j]);
+  for (int j = threadIdx.x; j < 2 * HD; j += blockDim.x) {
+    float t = 0.0f;
+#pragma unroll
+    for (int v = 0; v < WPB; ++v) t = __fadd_rn(t, (&sh_da[v][0][0])[j]);
+    atomicAdd((j < HD ? a.da_src : a.da_dst) + (j % HD), t);
   }
 }
 
@@ -3122,7 +3179,13 @@ cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
   if (hv == H_ * 100 + V_) {                                                                       \
     ok = true;                                                                                     \
     { ProfScope p("gat_fwd_stats", st);                                                            \
-      k_fwd_stats_t<H_><<<item_grid(a.plan.cap + a.plan.tcap), 256, 0, st>>>(a); }                 \
+      constexpr int fsm = 8 * fs_warp_smem<H_>();                                                  \
+      static bool fs_attr = false;                                                                 \
+      if (!fs_attr) {                                                                              \
+        cudaFuncSetAttribute(k_fwd_stats_t<H_>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm); \
+        fs_attr = true;                                                                            \
+      }                                                                                            \
+      k_fwd_stats_t<H_><<<item_grid(a.plan.cap + a.plan.tcap), 256, fsm, st>>>(a); }               \
     { ProfScope p("gat_fwd_stats2", st); k_fwd_stats2<H_><<<heavy_grid(a.plan.cap), 256, 0, st>>>(a); } \
   }
   TANGO_HV_CASES(X)

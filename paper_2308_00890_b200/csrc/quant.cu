@@ -75,6 +75,27 @@ __global__ void __launch_bounds__(256) k_quantize(const float* __restrict__ x, i
   const bool fast = (rowscale == nullptr) && (qt == nullptr) && ((g0 & 7) == 0) && ((cols & 7) == 0) &&
                     ((ld & 7) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   const bool dense = ld == cols;   // q[i*ld + j] = q[e]: no division in the fast loop
+  if (fast && dense) {   // streaming path: the next group's 32 bytes are loaded before this one is rounded
+    int64_t blk = blk0 + tid;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (blk < blk1) {
+      const float4* src = reinterpret_cast<const float4*>(x + ((blk << 3) - g0));
+      a = __ldcs(src); b = __ldcs(src + 1);
+    }
+    for (; blk < blk1; blk += nthr) {
+      const int64_t nb = blk + nthr;
+      float4 na = a, nbv = b;
+      if (nb < blk1) {
+        const float4* src = reinterpret_cast<const float4*>(x + ((nb << 3) - g0));
+        na = __ldcs(src); nbv = __ldcs(src + 1);
+      }
+      const SR8 rnd = sr_draw8((uint64_t)blk, tag, step, key);
+      const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      *reinterpret_cast<uint2*>(q + ((blk << 3) - g0)) = sr_quant8(v, sc.r, rnd, qmax);
+      a = na; b = nbv;
+    }
+    return;
+  }
   for (int64_t blk = blk0 + tid; blk < blk1; blk += nthr) {
     const SR8 rnd = sr_draw8((uint64_t)blk, tag, step, key);
     const int64_t gs = blk << 3;
