@@ -2111,7 +2111,7 @@ __host__ __device__ constexpr int dst4_warp_smem() {
 // BD1 (v4 engine): ⑤″ ∂α = i2f(q_G[v]·q_H′[u]) (s_G s_H′), ④′ P = Σ fmaf(∂α, α) in edge order per
 // destination row (heavy segments: P partials), then for light rows ∂E_pre and ∂D (pass 2).
 template <int H, int VPL, int NW>
-__global__ void __maxnreg__(96) k_bwd_dst1_v4(const GatBwdArgs a) {
+__global__ void __maxnreg__(80) k_bwd_dst1_v4(const GatBwdArgs a) {
   constexpr int R = AGG_RING, RB = 32 * VPL, LPH = 32 / H;
   extern __shared__ __align__(16) uint8_t dsm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
