@@ -3310,7 +3310,7 @@ cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st) {
       }                                                                                            \
       ProfScope p("gat_bwd_src", st);                                                              \
       if (a.g.out_eid) {                                                                           \
-        constexpr int NW = 7, smem4 = NW * g4_warp_smem<H_, VV, true>();                           \
+        constexpr int NW = 4, smem4 = NW * g4_warp_smem<H_, VV, true>();                           \
         static bool attr4_set = false;                                                             \
         if (!attr4_set) {                                                                          \
           cudaFuncSetAttribute(k_bwd_src4<H_, VV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); \
