@@ -210,7 +210,9 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
                                  size_t ctx_bytes, float* H_out, float* amax_out, struct tango_comm* comm,
                                  int32_t* dev_status, cudaStream_t stream);
 
-/* dH_out: [n_local][heads*head_dim].  dH (nullable): [n_local][in_feats];
+/* Must follow tango_gat_layer_fwd on the same graph, params and ctx (it reuses the
+ * forward's cache, including the in-CSR segment plan).
+ * dH_out: [n_local][heads*head_dim].  dH (nullable): [n_local][in_feats];
  * dW: [in_feats][heads*head_dim]; da_src, da_dst: [heads*head_dim]; all fp32,
  * all overwritten.  amax_dH (nullable): device scalar receiving max|dH|. */
 tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p, void* ctx, size_t ctx_bytes,

@@ -576,9 +576,7 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   // B2-B4: destination rows (in-CSR plan from the forward call), B5-B7: source rows (out-CSR plan)
   const PlanDev pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in, L.off_pin_tiles, L.tcap);
   const PlanDev pout = plan_of(c, L.off_pout_hbase, L.off_pout_hseg, L.off_pout_hrow, L.off_pout_cnt, L.cap_out, L.off_pout_tiles, L.tcap);
-  TRY_CUDA(cudaMemsetAsync(pin.counts, 0, 16, st));
-  TRY(launch_status(launch_plan(G->in_ptr, L.n, g.chunk, pin, st)));
-  TRY(launch_status(launch_plan_tiles(G->in_ptr, L.n, pin, st)));
+  // the in-CSR plan (a function of the graph only) is the one the forward call left in ctx
   TRY_CUDA(cudaMemsetAsync(pout.counts, 0, 16, st));
   TRY(launch_status(launch_plan(G->out_ptr, L.n, g.chunk, pout, st)));
   TRY(launch_status(launch_plan_tiles(G->out_ptr, L.n, pout, st)));

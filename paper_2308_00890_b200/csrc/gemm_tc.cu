@@ -51,12 +51,13 @@ __device__ __forceinline__ float deq(uint32_t acc, float sAB, bool has_rs, float
   return has_rs ? __fmul_rn(v, rs) : v;
 }
 
-template <int MODE>
+template <int MODE, bool RS>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ KParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned by pointer arithmetic on the shared array (keeps the shared address space visible)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int c_lo = p.split_halves ? half * (nch / 2) : 0;
     const int c_hi = p.split_halves ? (half + 1) * (nch / 2) : (half == 0 ? nch : 0);
     const float sAB = (p.sA && p.sB) ? __fmul_rn(*p.sA, *p.sB) : 1.0f;
-    const bool has_rs = p.rowscale != nullptr;
+    constexpr bool has_rs = RS;   // per-row multiplier (GCN), a template parameter: no select per element
     Scale qs = {1.0f, 1.0f, false};
     if (MODE == EPI_QUANT) {
       qs = scale_from_amax(amax_load(p.amax_in), p.bits);
@@ -189,6 +190,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t tbase = tmem_base + ((uint32_t)(sub * 32) << 16) + buf * (uint32_t)p.BN;
       float s_acc = 0.0f, d_acc = 0.0f;
       int dcount = 0;
+      const int cph = fast_heads ? p.head_dim / 32 : 1;   // 32-column chunks per head
+      int hcnt = fast_heads ? (c_lo % cph) : 0;
+      int h_next = fast_heads ? (int)(((int64_t)nt * p.BN + c_lo * 32) / p.head_dim) : 0;
       for (int c = c_lo; c < c_hi; ++c) {
         uint32_t r[32];
         tmem_ld32(tbase + c * 32, r);
@@ -210,9 +214,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 s_acc = __fmaf_rn(v[i], sm_asrc[c * 32 + i], s_acc);
                 d_acc = __fmaf_rn(v[i], sm_adst[c * 32 + i], d_acc);
               }
-              if (((col0 + 32) % p.head_dim) == 0) {
+              if (++hcnt == cph) {   // the chunk closes a head (head_dim % 32 == 0 here)
+                hcnt = 0;
+                const int h = h_next++;
                 if (row_ok) {
-                  const int h = (int)(col0 / p.head_dim);
                   p.S[row * p.heads + h] = s_acc;
                   p.Dd[row * p.heads + h] = d_acc;
                   amax_s = fmaxf(amax_s, fabsf(s_acc));
@@ -410,9 +415,11 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
   case M_: {                                                                                         \
     static std::once_flag once_##M_;                                                                 \
     std::call_once(once_##M_, [] {                                                                   \
-      cudaFuncSetAttribute(k_gemm_i8<M_>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);  \
+      cudaFuncSetAttribute(k_gemm_i8<M_, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES); \
+      cudaFuncSetAttribute(k_gemm_i8<M_, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);  \
     });                                                                                              \
-    k_gemm_i8<M_><<<(unsigned)grid, GEMM_THREADS, SMEM_BYTES, st>>>(tA, tB, p);                     \
+    if (p.rowscale) k_gemm_i8<M_, true><<<(unsigned)grid, GEMM_THREADS, SMEM_BYTES, st>>>(tA, tB, p);  \
+    else k_gemm_i8<M_, false><<<(unsigned)grid, GEMM_THREADS, SMEM_BYTES, st>>>(tA, tB, p);           \
     break;                                                                                           \
   }
     LAUNCH(EPI_AMAX) LAUNCH(EPI_QUANT) LAUNCH(EPI_STORE) LAUNCH(EPI_I32) LAUNCH(EPI_ATOMIC64)
