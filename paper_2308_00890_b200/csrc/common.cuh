@@ -64,25 +64,26 @@ __device__ __forceinline__ uint32_t sr_half(const SR8& s, int j) {
 
 // Stochastic rounding of x*r (reading R4/R6): q = floor(xs) + (u < xs - floor(xs)), clamped to ±qmax,
 // u = hw16 * 2^-16.  Evaluated on the FMA/ALU pipes only (no XU conversions), bit-identical to the
-// plain definition: t = xs + 1.5*2^23 holds n = rint(xs) as bits 0x4B400000 + n (|xs| < 2^22),
-// d = xs - n is exact, floor(xs) = n - [d < 0] and xs - floor(xs) = fl(d + 1) if d < 0 else d;
-// u = (1 + hw16*2^-16) - 1 exactly.  Returns the bits 0x4B400000 + q (low byte = the int8 code).
-__device__ __forceinline__ uint32_t sr_qbits(float x, float r, uint32_t ubits /* hw16 << 7 */, int qmax) {
+// plain definition (all steps exact, |xs| < 2^22):
+//   t  = fl_rd(xs + 1.5*2^23)  -> bits 0x4B400000 + floor(xs)
+//   f  = t - 1.5*2^23, fr = fl(xs - f)                  (fr exactly as in the definition)
+//   u < fr  <=>  hw16 < fr*2^16  <=>  2^23 + hw16 < fl_ru(fr*2^16 + 2^23)  (= 2^23 + ceil(fr*2^16))
+// with kf = 2^23 + hw16 built by one PRMT; the sign bit of kf - rhs (exact) is the carry into q.
+// Returns the bits 0x4B400000 + q (low byte = the int8 code).
+__device__ __forceinline__ uint32_t sr_qbits(float x, float r, float kf /* 2^23 + hw16 */, int qmax) {
   const float xs = __fmul_rn(x, r);
-  const float t = __fadd_rn(xs, 12582912.0f);
-  const float n = __fsub_rn(t, 12582912.0f);
-  const float d = __fsub_rn(xs, n);
-  const bool neg = d < 0.0f;
-  const float fr = neg ? __fadd_rn(d, 1.0f) : d;
-  const float u = __fsub_rn(__uint_as_float(ubits | 0x3F800000u), 1.0f);
-  int qb = (int)__float_as_uint(t) - (neg ? 1 : 0) + (u < fr ? 1 : 0);
+  const float t = __fadd_rd(xs, 12582912.0f);
+  const float f = __fsub_rn(t, 12582912.0f);
+  const float fr = __fsub_rn(xs, f);
+  const float rhs = __fmaf_ru(fr, 65536.0f, 8388608.0f);
+  const uint32_t up = __float_as_uint(__fsub_rn(kf, rhs)) >> 31;
+  int qb = (int)(__float_as_uint(t) + up);
   qb = min(max(qb, 0x4B400000 - qmax), 0x4B400000 + qmax);
   return (uint32_t)qb;
 }
-// bits (hw16 << 7) of half-word j of the group's Philox output
-__device__ __forceinline__ uint32_t sr_ubits(const SR8& s, int j) {
-  const uint32_t w = s.w[j >> 1];
-  return (j & 1) ? ((w >> 9) & 0x7FFF80u) : ((w << 7) & 0x7FFF80u);
+// 2^23 + (half-word j of the group's Philox output), as a float (one PRMT)
+__device__ __forceinline__ float sr_kf(const SR8& s, int j) {
+  return __uint_as_float(__byte_perm(s.w[j >> 1], 0x4B000000u, (j & 1) ? 0x7632u : 0x7610u));
 }
 __device__ __forceinline__ uint32_t pack4_low_bytes(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
   return __byte_perm(__byte_perm(b0, b1, 0x0040u), __byte_perm(b2, b3, 0x0040u), 0x5410u);
@@ -91,11 +92,11 @@ __device__ __forceinline__ uint32_t pack4_low_bytes(uint32_t b0, uint32_t b1, ui
 __device__ __forceinline__ uint2 sr_quant8(const float (&v)[8], float r, const SR8& rnd, int qmax) {
   uint32_t b[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) b[k] = sr_qbits(v[k], r, sr_ubits(rnd, k), qmax);
+  for (int k = 0; k < 8; ++k) b[k] = sr_qbits(v[k], r, sr_kf(rnd, k), qmax);
   return make_uint2(pack4_low_bytes(b[0], b[1], b[2], b[3]), pack4_low_bytes(b[4], b[5], b[6], b[7]));
 }
 __device__ __forceinline__ int sr_quant(float x, float r, uint32_t hw16, int qmax) {
-  return (int)sr_qbits(x, r, hw16 << 7, qmax) - 0x4B400000;
+  return (int)sr_qbits(x, r, __uint_as_float(0x4B000000u | hw16), qmax) - 0x4B400000;
 }
 
 // Scale pair from amax (reading R1/R3/R7): s = amax/qmax, r = qmax/amax; amax = 0 -> s = r = 1.
