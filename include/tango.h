@@ -48,7 +48,7 @@ typedef enum {
   TANGO_ERR_BITS = 3,          /* bit-width outside [2, 8] (reading R25) */
   TANGO_ERR_NONFINITE = 4,     /* (device status) NaN / Inf in a tensor being quantized */
   TANGO_ERR_OVERFLOW = 5,      /* a contraction length that could overflow int32 (reading R27) */
-  TANGO_ERR_UNSUPPORTED = 6,   /* a shape this build does not implement (e.g. HD not in {32..512}) */
+  TANGO_ERR_UNSUPPORTED = 6,   /* a shape this build does not implement (HD not in {64..512}, n_global*HD >= 2^32) */
   TANGO_ERR_CUDA = 7,          /* a CUDA launch / runtime error */
   TANGO_ERR_NCCL = 8           /* a NCCL error (multi-GPU) */
 } tango_status;

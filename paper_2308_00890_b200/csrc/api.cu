@@ -410,6 +410,8 @@ tango_status check_gat(const tango_graph* G, const tango_gat_params* p) {
   if (!(p->head_dim == 8 || p->head_dim == 16 || p->head_dim % 32 == 0)) return TANGO_ERR_UNSUPPORTED;
   if (p->in_feats > 133144) return TANGO_ERR_OVERFLOW;
   if (256 % p->head_dim && HD > 256) return TANGO_ERR_UNSUPPORTED;
+  // gathered rows are addressed by 32-bit byte offsets (row * ld) inside the gather kernels
+  if ((uint64_t)G->n_global * (uint64_t)HD >= (1ull << 32)) return TANGO_ERR_UNSUPPORTED;
   return TANGO_OK;
 }
 }  // namespace

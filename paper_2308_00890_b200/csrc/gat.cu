@@ -1281,7 +1281,7 @@ __device__ __forceinline__ int g4_stream(uint8_t* wsm, const int8_t* __restrict_
     float alA[H], xA[H];
     load(0, idxA, rowA, alA, xA);
     stash(0, rowA, alA, xA);
-    sidx[lane] = idxA;
+    sidx[lane] = (int)((uint32_t)idxA * ld32);   // byte offset of the gathered row
   }
   __syncwarp();
 #pragma unroll
@@ -1290,7 +1290,7 @@ __device__ __forceinline__ int g4_stream(uint8_t* wsm, const int8_t* __restrict_
     const int nv[4] = {nx.x, nx.y, nx.z, nx.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      if (4 * g + j < T) cp_row_slice<VPL>(ring_s + (4 * g + j) * RB, xbase + (uint32_t)nv[j] * ld32);
+      if (4 * g + j < T) cp_row_slice<VPL>(ring_s + (4 * g + j) * RB, xbase + (uint32_t)nv[j]);
     cp_commit();
   }
   int cur = tile ? -1 : 0;
@@ -1307,7 +1307,7 @@ __device__ __forceinline__ int g4_stream(uint8_t* wsm, const int8_t* __restrict_
       const int t0 = c * 32 + i0;
       if (t0 >= T) break;
       if (i0 == 12) {   // refills from group 16 on read the next chunk's indices
-        sidx[(cb ^ 1) * 32 + lane] = idxB;
+        sidx[(cb ^ 1) * 32 + lane] = (int)((uint32_t)idxB * ld32);
         __syncwarp();
       }
       cp_wait<R / 4 - 1>();   // the 4 rows of this group have landed
@@ -1325,7 +1325,7 @@ __device__ __forceinline__ int g4_stream(uint8_t* wsm, const int8_t* __restrict_
       const int nv[4] = {nx.x, nx.y, nx.z, nx.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (tn0 + j < T) cp_row_slice<VPL>(slot0 + j * RB, xbase + (uint32_t)nv[j] * ld32);   // N*ld < 2^32
+        if (tn0 + j < T) cp_row_slice<VPL>(slot0 + j * RB, xbase + (uint32_t)nv[j]);   // N*ld < 2^32
       cp_commit();
     }
     __syncwarp();
@@ -2194,7 +2194,7 @@ __global__ void __maxnreg__(80) k_bwd_dst1_v4(const GatBwdArgs a) {
       float alA[H];
       load(0, uA, rowA, eA, alA);
       stash(0, rowA, alA);
-      sidx[lane] = uA;
+      sidx[lane] = (int)((uint32_t)uA * ld32);   // byte offset of the gathered row
     }
     __syncwarp();
 #pragma unroll
@@ -2203,7 +2203,7 @@ __global__ void __maxnreg__(80) k_bwd_dst1_v4(const GatBwdArgs a) {
       const int nv[4] = {nx.x, nx.y, nx.z, nx.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (4 * g + j < T) cp_row_slice<VPL>(ring_s + (4 * g + j) * RB, xbase + (uint32_t)nv[j] * ld32);
+        if (4 * g + j < T) cp_row_slice<VPL>(ring_s + (4 * g + j) * RB, xbase + (uint32_t)nv[j]);
       cp_commit();
     }
     float P = 0.0f;
@@ -2225,7 +2225,7 @@ __global__ void __maxnreg__(80) k_bwd_dst1_v4(const GatBwdArgs a) {
         const int t0 = c * 32 + i0;
         if (t0 >= T) break;
         if (i0 == 12) {
-          sidx[(cb ^ 1) * 32 + lane] = uB;
+          sidx[(cb ^ 1) * 32 + lane] = (int)((uint32_t)uB * ld32);
           __syncwarp();
         }
         cp_wait<R / 4 - 1>();
@@ -2279,7 +2279,7 @@ __global__ void __maxnreg__(80) k_bwd_dst1_v4(const GatBwdArgs a) {
         const int nv[4] = {nx.x, nx.y, nx.z, nx.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (tn0 + j < T) cp_row_slice<VPL>(slot0 + j * RB, xbase + (uint32_t)nv[j] * ld32);
+          if (tn0 + j < T) cp_row_slice<VPL>(slot0 + j * RB, xbase + (uint32_t)nv[j]);
         cp_commit();
       }
       __syncwarp();
