@@ -106,6 +106,29 @@ def kernel_model(name, g_e, n, F, H, HD, peaks, clock_mhz):
     return byts, ops, alu_peak
 
 
+def gemm_microbench(T, torch, int8_peak, size=8192, reps=10):
+    """tango_gemm_q (tcgen05 kind::i8, int32 out) on a ridge-crossing size^3 problem: achieved int8
+    TOPS vs the int8 tensor peak (SURVEY.md §8(d) metric 3)."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randint(-127, 128, (size, size), dtype=torch.int8, device="cuda", generator=g)
+    B = torch.randint(-127, 128, (size, size), dtype=torch.int8, device="cuda", generator=g)
+    s = torch.ones(1, device="cuda")
+    for _ in range(2):
+        T.gemm_q(A, s, T.TANGO_K_MAJOR, B, s, T.TANGO_K_MAJOR, size, size, size, want=("i32",))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        T.gemm_q(A, s, T.TANGO_K_MAJOR, B, s, T.TANGO_K_MAJOR, size, size, size, want=("i32",))
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps / 1e3
+    tops = 2.0 * size ** 3 / t / 1e12
+    return {"gemm": f"{size}^3 int8 x int8 -> int32, K-major, tcgen05 kind::i8 (tango_gemm_q)",
+            "ms": round(t * 1e3, 3), "tops": round(tops, 1), "peak_tops": round(int8_peak, 1),
+            "frac": round(tops / int8_peak, 3), "peak_source": "MEASURED_PEAKS bf16 x 2 (nominal int8:bf16)"}
+
+
 # ------------------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     if rank != 0:
@@ -297,6 +320,26 @@ def main():
         roof["share_of_step"] = dom_ms / dom_cnt / ms
         roof["peak_kind"] = peak_kind
     breakdown = {k: round(v[0] / v[1], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    # per-kernel rooflines of SURVEY.md §8(d): sparse kernels vs HBM (algorithmic bytes) and the
+    # ALU, GEMMs as int8 TOPS vs the int8 tensor peak (measured bf16 x the nominal int8:bf16 ratio 2)
+    int8_peak = 2.0 * peaks["bf16_tflops"]
+    kroof = {}
+    for kname in ("gat_fwd_agg", "gat_bwd_dst1", "gat_bwd_src"):
+        if kname not in prof:
+            continue
+        km = kernel_model(kname, dg.e_in, n, F, H, HD, peaks, clock)
+        t_s = prof[kname][0] / prof[kname][1] / 1e3
+        kroof[kname] = {"ms": round(t_s * 1e3, 4), "hbm_gbs": round(km[0] / t_s / 1e9, 1),
+                        "hbm_frac": round(km[0] / t_s / 1e9 / peaks["hbm_gbs"], 3),
+                        "alu_frac": round(km[1] / t_s / km[2], 3)}
+    gemm_ops = {"gemm_amax": 2 * n * F * HD, "gemm_quant": 2 * n * F * HD, "gemm_store": 2 * n * HD * F,
+                "gemm_splitk_i64": 2 * n * F * HD}
+    for kname, ops in gemm_ops.items():
+        if kname in prof:
+            t_s = prof[kname][0] / prof[kname][1] / 1e3
+            kroof[kname] = {"ms": round(t_s * 1e3, 4), "tops": round(ops / t_s / 1e12, 1),
+                            "tensor_frac": round(ops / t_s / 1e12 / int8_peak, 3)}
+    tensor = gemm_microbench(T, torch, int8_peak) if (rank == 0 and world == 1) else None
     if args.profile_breakdown and rank == 0:
         print(json.dumps({"per_launch_ms": breakdown, "launches_per_kernel": {k: v[1] for k, v in prof.items()}}),
               file=sys.stderr)
@@ -352,7 +395,7 @@ def main():
                            "parallelism": f"dst-row partition x{world}" if world > 1 else "1 GPU",
                            "l2": "flushed between timed steps (256 MB write)",
                            "degree": g.degree_stats()},
-                "roofline": roof, "cpu_baseline": cpu,
+                "roofline": roof, "kernel_roofline": kroof, "tensor": tensor, "cpu_baseline": cpu,
                 "e2e": {"value": float(e2e_t.item()), "unit": "ms", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},
                 "gpu_launches": int(launches_t.item()), "clocks": clk, "kernel_ms": breakdown,
