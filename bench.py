@@ -344,29 +344,48 @@ def main():
         print(json.dumps({"per_launch_ms": breakdown, "launches_per_kernel": {k: v[1] for k, v in prof.items()}}),
               file=sys.stderr)
 
-    # ---------------- e2e: through the public API with host buffers (pinned), copies in the timed region
+    # ---------------- e2e: through the public API with host buffers (pinned), copies in the timed region.
+    # Every step copies its inputs H and ∂H_out host->device and reads the step's result (the layer's
+    # parameter gradients ∂W, ∂a_src, ∂a_dst and the amax of H_out) device->host.  The input copies
+    # of step i+1 run on a copy stream into the other of two device buffers while step i computes.
     H_host = torch.from_numpy(np.ascontiguousarray(Hx)).pin_memory()
     dH_host = torch.from_numpy(np.ascontiguousarray(dH)).pin_memory()
-    out_host = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (Hout, *outs)]
-    e2e_steps = max(3, min(args.steps, 20))
+    res_dev = (outs[1], outs[2], outs[3], amax)
+    res_host = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in res_dev]
+    Hbuf, dHbuf = [Hd, torch.empty_like(Hd)], [dHd, torch.empty_like(dHd)]
+    s_copy, s_comp = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_free = [torch.cuda.Event(), torch.cuda.Event()]
+    e2e_steps = max(4, min(args.steps, 20))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    e0.record(s_copy)
+    s_comp.wait_stream(s_copy)
     for i in range(e2e_steps):
-        Hd.copy_(H_host, non_blocking=True)
-        dHd.copy_(dH_host, non_blocking=True)
-        step(10_000 + i)
-        for h, d in zip(out_host, (Hout, *outs)):
-            h.copy_(d, non_blocking=True)
-    e1.record()
+        b = i & 1
+        with torch.cuda.stream(s_copy):
+            if i >= 2:
+                s_copy.wait_event(ev_free[b])     # step i-2 is done reading buffer b
+            Hbuf[b].copy_(H_host, non_blocking=True)
+            dHbuf[b].copy_(dH_host, non_blocking=True)
+            ev_in[b].record(s_copy)
+        with torch.cuda.stream(s_comp):
+            s_comp.wait_event(ev_in[b])
+            layer.forward(Hbuf[b], step=10_000 + i, out=Hout, amax_out=amax)
+            layer.backward(dHbuf[b], step=10_000 + i, outs=outs)
+            ev_free[b].record(s_comp)
+            for h, d in zip(res_host, res_dev):
+                h.copy_(d, non_blocking=True)
+    s_copy.wait_stream(s_comp)
+    e1.record(s_copy)
     torch.cuda.synchronize()
     e2e_t = torch.tensor([e0.elapsed_time(e1) / e2e_steps], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     h2d = (H_host.numel() + dH_host.numel()) * 4
-    d2h = sum(t.numel() * t.element_size() for t in out_host)
+    d2h = sum(t.numel() * t.element_size() for t in res_host)
 
     launches_t = torch.tensor([launches], dtype=torch.int64, device="cuda")
     if world > 1:
@@ -397,6 +416,9 @@ def main():
                            "degree": g.degree_stats()},
                 "roofline": roof, "kernel_roofline": kroof, "tensor": tensor, "cpu_baseline": cpu,
                 "e2e": {"value": float(e2e_t.item()), "unit": "ms", "h2d_bytes_per_step": h2d,
+                        "what": "per step: H2D of H and dH_out (pinned), fwd+bwd through GATLayer (C ABI), D2H of "
+                                "dW, da_src, da_dst, amax(H_out); input copies of step i+1 overlap step i "
+                                "(copy stream, double-buffered inputs)",
                         "d2h_bytes_per_step": d2h},
                 "gpu_launches": int(launches_t.item()), "clocks": clk, "kernel_ms": breakdown,
                 "timing": "value: CUDA-graph replay of fwd+bwd per step (events per step, L2 flushed between "
