@@ -121,6 +121,31 @@ static GraphDev dev_graph(const tango_graph* G) {
   g.chunk = G->chunk_edges > 0 ? G->chunk_edges : 256;
   return g;
 }
+// Auxiliary stream (per thread and device) for work that does not depend on the main chain (graph
+// plans, Q(W), the ∂a reduction): forked from and joined back into the caller's stream with events,
+// so the API stays asynchronous on `st` and CUDA-graph capture of `st` records the fork/join.
+struct AuxStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[6] = {};
+};
+static AuxStream* aux_stream() {
+  thread_local AuxStream per_dev[16];
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 16) return nullptr;
+  AuxStream& a = per_dev[d];
+  if (!a.s) {
+    if (cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess) { a.s = nullptr; return nullptr; }
+    for (auto& e : a.ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  }
+  return &a;
+}
+// `to` waits for the work enqueued so far on `from` (event slot k)
+static cudaError_t stream_after(cudaStream_t to, cudaStream_t from, cudaEvent_t ev) {
+  cudaError_t e = cudaEventRecord(ev, from);
+  return e == cudaSuccess ? cudaStreamWaitEvent(to, ev, 0) : e;
+}
+
 static tango_status check_q(const tango_qtensor* t) {
   if (!t || !t->q || !t->scale) return TANGO_ERR_INVALID_ARG;
   if (t->bits < 2 || t->bits > 8) return TANGO_ERR_BITS;
@@ -467,6 +492,20 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   const GraphDev g = dev_graph(G);
 
   TRY_CUDA(cudaMemsetAsync(sc, 0, SL_NSLOTS * 4, st));
+  // side stream: F2 Q(W) and the in-CSR segment plan (graph only) run beside F1
+  AuxStream* aux = aux_stream();
+  if (!aux) return TANGO_ERR_CUDA;
+  const PlanDev pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in, L.off_pin_tiles, L.tcap);
+  TRY_CUDA(stream_after(aux->s, st, aux->ev[0]));
+  // F2: Q(W) (replicated; identical on every rank), row-major and transposed copies
+  TRY(launch_status(launch_absmax(p->W, L.F, L.HD, nullptr, sc + SL_AMAX_W, aux->s)));
+  TRY(launch_status(launch_quantize(p->W, L.F, L.HD, nullptr, 0, sc + SL_AMAX_W, p->bits, rng.seed, rng.step,
+                                    tag_of(layer_id, R_W), qW, L.ldHD, qWt, L.ldFt, scf + SL_S_W, dev_status, aux->s)));
+  TRY_CUDA(cudaEventRecord(aux->ev[1], aux->s));
+  TRY_CUDA(cudaMemsetAsync(pin.counts, 0, 16, aux->s));
+  TRY(launch_status(launch_plan(G->in_ptr, L.n, g.chunk, pin, aux->s)));
+  TRY(launch_status(launch_plan_tiles(G->in_ptr, L.n, pin, aux->s)));
+  TRY_CUDA(cudaEventRecord(aux->ev[2], aux->s));
   // F1: amax(H) over all ranks (R28), Q(H)
   if (amax_H_hint) {
     TRY_CUDA(cudaMemcpyAsync(sc + SL_AMAX_H, amax_H_hint, 4, cudaMemcpyDeviceToDevice, st));
@@ -476,10 +515,7 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   }
   TRY(launch_status(launch_quantize(H, L.n, L.F, nullptr, r0 * L.F, sc + SL_AMAX_H, p->bits, rng.seed, rng.step,
                                     tag_of(layer_id, R_H), qH, L.ldF, nullptr, 0, scf + SL_S_H, dev_status, st)));
-  // F2: Q(W) (replicated; identical on every rank), row-major and transposed copies
-  TRY(launch_status(launch_absmax(p->W, L.F, L.HD, nullptr, sc + SL_AMAX_W, st)));
-  TRY(launch_status(launch_quantize(p->W, L.F, L.HD, nullptr, 0, sc + SL_AMAX_W, p->bits, rng.seed, rng.step,
-                                    tag_of(layer_id, R_W), qW, L.ldHD, qWt, L.ldFt, scf + SL_S_W, dev_status, st)));
+  TRY_CUDA(cudaStreamWaitEvent(st, aux->ev[1], 0));   // Q(W) done
   // F3 phase A: acc = q_H·q_W on tcgen05; H′ = i2f(acc)·s_H s_W; S, D head dots; amax(H′), amax(S), amax(D)
   GemmArgs ga{};
   ga.A = qH; ga.lda = L.ldF; ga.a_mn = false;
@@ -511,10 +547,7 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   TRY(comm_gather_rows(comm, qD, (size_t)L.H, st));
   // F5 + F6: segment plan of the in-CSR, then softmax statistics, aggregation and heavy-row combine
   if (amax_out) TRY_CUDA(cudaMemsetAsync(amax_out, 0, 4, st));
-  const PlanDev pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in, L.off_pin_tiles, L.tcap);
-  TRY_CUDA(cudaMemsetAsync(pin.counts, 0, 16, st));
-  TRY(launch_status(launch_plan(G->in_ptr, L.n, g.chunk, pin, st)));
-  TRY(launch_status(launch_plan_tiles(G->in_ptr, L.n, pin, st)));
+  TRY_CUDA(cudaStreamWaitEvent(st, aux->ev[2], 0));   // in-CSR plan done
   GatFwdArgs fa{};
   fa.g = g; fa.d = {p->heads, p->head_dim, (int)L.HD}; fa.slope = p->neg_slope; fa.bits = p->bits;
   fa.qS = qS; fa.amax_S = sc + SL_AMAX_S; fa.qD = qD; fa.amax_D = sc + SL_AMAX_D;
@@ -564,6 +597,17 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   TRY_CUDA(cudaMemsetAsync(da_src, 0, L.HD * 4, st));
   TRY_CUDA(cudaMemsetAsync(da_dst, 0, L.HD * 4, st));
   TRY_CUDA(cudaMemsetAsync(dW64, 0, L.F * L.HD * 8, st));
+  AuxStream* aux = aux_stream();
+  if (!aux) return TANGO_ERR_CUDA;
+  {
+    const PlanDev pout = plan_of(c, L.off_pout_hbase, L.off_pout_hseg, L.off_pout_hrow, L.off_pout_cnt, L.cap_out,
+                                 L.off_pout_tiles, L.tcap);
+    TRY_CUDA(stream_after(aux->s, st, aux->ev[0]));
+    TRY_CUDA(cudaMemsetAsync(pout.counts, 0, 16, aux->s));
+    TRY(launch_status(launch_plan(G->out_ptr, L.n, g.chunk, pout, aux->s)));
+    TRY(launch_status(launch_plan_tiles(G->out_ptr, L.n, pout, aux->s)));
+    TRY_CUDA(cudaEventRecord(aux->ev[1], aux->s));
+  }
   // B1: Q(∂H_out), shared by ⑤′ and ⑤″
   if (amax_dH_hint) {
     TRY_CUDA(cudaMemcpyAsync(sc + SL_AMAX_G, amax_dH_hint, 4, cudaMemcpyDeviceToDevice, st));
@@ -575,13 +619,10 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
                                     rng.step, tag_of(layer_id, R_G), qG + r0 * L.ldHD, L.ldHD, nullptr, 0,
                                     scf + SL_S_G, dev_status, st)));
   TRY(comm_gather_rows(comm, qG, (size_t)L.ldHD, st));
-  // B2-B4: destination rows (in-CSR plan from the forward call), B5-B7: source rows (out-CSR plan)
+  // B2-B4: destination rows (in-CSR plan from the forward call), B5-B7: source rows (out-CSR plan,
+  // built on the side stream since the start of the call)
   const PlanDev pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in, L.off_pin_tiles, L.tcap);
   const PlanDev pout = plan_of(c, L.off_pout_hbase, L.off_pout_hseg, L.off_pout_hrow, L.off_pout_cnt, L.cap_out, L.off_pout_tiles, L.tcap);
-  // the in-CSR plan (a function of the graph only) is the one the forward call left in ctx
-  TRY_CUDA(cudaMemsetAsync(pout.counts, 0, 16, st));
-  TRY(launch_status(launch_plan(G->out_ptr, L.n, g.chunk, pout, st)));
-  TRY(launch_status(launch_plan_tiles(G->out_ptr, L.n, pout, st)));
   GatBwdArgs ba{};
   ba.g = g; ba.d = {p->heads, p->head_dim, (int)L.HD}; ba.slope = p->neg_slope; ba.bits = p->bits;
   ba.qS = qS; ba.amax_S = sc + SL_AMAX_S; ba.qD = qD; ba.amax_D = sc + SL_AMAX_D;
@@ -600,10 +641,13 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   TRY_CUDA(cudaMemsetAsync(ba.work, 0, 64, st));
   TRY(launch_status(launch_gat_bwd_dst(ba, st)));
   TRY(comm_gather_rows(comm, P, (size_t)L.H * 4, st));
+  TRY_CUDA(cudaStreamWaitEvent(st, aux->ev[1], 0));   // out-CSR plan done
   TRY(launch_status(launch_gat_bwd_src(ba, st)));
+  // ∂a (needs ∂S, ∂D) on the side stream, beside B8/B9
+  TRY_CUDA(stream_after(aux->s, st, aux->ev[2]));
+  TRY(launch_status(launch_gat_attn_grad(ba, aux->s)));
+  TRY_CUDA(cudaEventRecord(aux->ev[3], aux->s));
   TRY(comm_max(comm, sc + SL_AMAX_DHP, 1, st));
-  TRY(comm_sum_f32(comm, da_src, (size_t)L.HD, st));
-  TRY(comm_sum_f32(comm, da_dst, (size_t)L.HD, st));
   // B8: Q(∂H′)
   TRY(launch_status(launch_quantize(dHp, L.n, L.HD, nullptr, r0 * L.HD, sc + SL_AMAX_DHP, p->bits, rng.seed,
                                     rng.step, tag_of(layer_id, R_DHP), qdHp, L.ldHD, nullptr, 0, scf + SL_S_DHP,
@@ -640,6 +684,9 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   TRY(launch_status(launch_gemm(gw, st)));
   TRY(comm_sum_i64(comm, dW64, (size_t)(L.F * L.HD), st));
   TRY(launch_status(launch_finalize_dw(dW64, L.F * L.HD, scf + SL_S_H, scf + SL_S_DHP, dW, st)));
+  TRY_CUDA(cudaStreamWaitEvent(st, aux->ev[3], 0));   // ∂a done (join)
+  TRY(comm_sum_f32(comm, da_src, (size_t)L.HD, st));
+  TRY(comm_sum_f32(comm, da_dst, (size_t)L.HD, st));
   return TANGO_OK;
 }
 

@@ -3353,8 +3353,23 @@ cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st) {
     ok = true;                                                                                     \
     { ProfScope p("gat_bwd_src_combine", st);                                                      \
       k_bwd_src_combine<H_, V_><<<heavy_grid(a.pout.cap), 256, 0, st>>>(a); }                     \
-    { ProfScope p("gat_bwd_attn_grad", st);                                                        \
-      k_bwd_attn_grad<H_, V_><<<num_sms() * 4, 256, 0, st>>>(a); }                                 \
+  }
+  TANGO_HV_CASES(X)
+#undef X
+  if (!ok) return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+// ②′ for the attention vectors (∂a_src, ∂a_dst); needs ∂S, ∂D of the owned rows (after the source pass)
+cudaError_t launch_gat_attn_grad(const GatBwdArgs& a, cudaStream_t st) {
+  if (a.g.n_local == 0) return cudaSuccess;
+  const int hv = a.d.heads * 100 + a.d.hd / 32;
+  bool ok = false;
+#define X(H_, V_)                                                                                  \
+  if (hv == H_ * 100 + V_) {                                                                       \
+    ok = true;                                                                                     \
+    ProfScope p("gat_bwd_attn_grad", st);                                                          \
+    k_bwd_attn_grad<H_, V_><<<num_sms() * 4, 256, 0, st>>>(a);                                     \
   }
   TANGO_HV_CASES(X)
 #undef X

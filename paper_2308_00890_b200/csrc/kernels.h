@@ -123,6 +123,7 @@ struct GatBwdArgs {
 };
 cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st);
 cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st);
+cudaError_t launch_gat_attn_grad(const GatBwdArgs& a, cudaStream_t st);
 
 // standalone primitives (unfused; used by the primitive C-ABI entry points)
 cudaError_t launch_sddmm_add(const GraphDev& g, int heads, const int8_t* qS, const float* sS, const int8_t* qD,
