@@ -270,6 +270,15 @@ int32_t tango_comm_unique_id_bytes(void);
 tango_status tango_comm_get_unique_id(void* id_out /* tango_comm_unique_id_bytes() bytes */);
 tango_status tango_comm_init(struct tango_comm** out, const void* unique_id, int32_t nranks, int32_t rank);
 tango_status tango_comm_destroy(struct tango_comm* comm);
+/* In-process loopback group (validation of the partitioned path on ONE GPU): nranks
+ * host threads, one tango_comm each (tango_comm_init_local), exchange through device
+ * memory with host barriers; the collectives have the NCCL semantics above (fp32 sums
+ * in rank order).  Every rank must enter every collective (blocking rendezvous).  Not
+ * CUDA-graph capturable.  nranks <= 16. */
+struct tango_local_group;
+tango_status tango_local_group_create(struct tango_local_group** out, int32_t nranks);
+tango_status tango_local_group_destroy(struct tango_local_group* group);
+tango_status tango_comm_init_local(struct tango_comm** out, struct tango_local_group* group, int32_t rank);
 /* Row partition of the node set: rank r owns [row_starts[r], row_starts[r+1]).
  * Must be called (identically on every rank) before a layer call with this comm. */
 tango_status tango_comm_set_partition(struct tango_comm* comm, const int64_t* row_starts /* nranks+1, host */);

@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cstring>
 #include <vector>
+#include <mutex>
+#include <condition_variable>
 
 #include "../../include/tango.h"
 #include "kernels.h"
@@ -41,8 +43,34 @@ enum Slot : int {
 
 using namespace tango;
 
+// In-process loopback group: nranks host threads on one device exchange through device memory
+// (tests and one-GPU validation of the partitioned path; the NCCL communicator is the product path).
+struct tango_local_group {
+  int nranks = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<void*> ptr;             // per rank: buffer of the current collective
+  std::vector<cudaEvent_t> ev_a, ev_b;
+  std::vector<void*> tmp;             // per rank: reduction scratch (device)
+  std::vector<size_t> tmp_bytes;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t my = gen;
+    if (++arrived == nranks) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != my; });
+    }
+  }
+};
+
 struct tango_comm {
   ncclComm_t nccl = nullptr;
+  tango_local_group* local = nullptr;
   int nranks = 1, rank = 0;
   std::vector<int64_t> starts;  // nranks + 1
 };
@@ -160,19 +188,89 @@ static tango_status launch_status(cudaError_t e) {
   return TANGO_OK;
 }
 
+// ------------------------------------------------------------------ loopback group (in-process)
+namespace {
+struct LocalPtrs { const void* p[16]; };
+template <int OP>   // 0: max, 1: sum (rank order)
+__global__ void k_local_reduce_f32(float* out, LocalPtrs in, int n, size_t count) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    float v = static_cast<const float*>(in.p[0])[i];
+    for (int k = 1; k < n; ++k) {
+      const float x = static_cast<const float*>(in.p[k])[i];
+      v = OP == 0 ? fmaxf(v, x) : __fadd_rn(v, x);
+    }
+    out[i] = v;
+  }
+}
+__global__ void k_local_reduce_i64(int64_t* out, LocalPtrs in, int n, size_t count) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    int64_t v = 0;
+    for (int k = 0; k < n; ++k) v += static_cast<const int64_t*>(in.p[k])[i];
+    out[i] = v;
+  }
+}
+}  // namespace
+
+// Every rank registers its buffer and the event of its producer, then waits for all peers'.
+static tango_status local_begin(tango_comm* c, void* buf, cudaStream_t st) {
+  tango_local_group* g = c->local;
+  const int r = c->rank;
+  g->ptr[r] = buf;
+  TRY_CUDA(cudaEventRecord(g->ev_a[r], st));
+  g->barrier();
+  for (int k = 0; k < g->nranks; ++k)
+    if (k != r) TRY_CUDA(cudaStreamWaitEvent(st, g->ev_a[k], 0));
+  g->barrier();
+  return TANGO_OK;
+}
+// No rank reuses its buffer before every peer has finished reading it.
+static tango_status local_end(tango_comm* c, cudaStream_t st) {
+  tango_local_group* g = c->local;
+  const int r = c->rank;
+  TRY_CUDA(cudaEventRecord(g->ev_b[r], st));
+  g->barrier();
+  for (int k = 0; k < g->nranks; ++k)
+    if (k != r) TRY_CUDA(cudaStreamWaitEvent(st, g->ev_b[k], 0));
+  g->barrier();
+  return TANGO_OK;
+}
+static tango_status local_reduce(tango_comm* c, void* buf, size_t count, size_t esize, int op, cudaStream_t st) {
+  tango_local_group* g = c->local;
+  const int r = c->rank;
+  if (g->tmp_bytes[r] < count * esize) {
+    if (g->tmp[r]) cudaFree(g->tmp[r]);
+    TRY_CUDA(cudaMalloc(&g->tmp[r], count * esize));
+    g->tmp_bytes[r] = count * esize;
+  }
+  TRY(local_begin(c, buf, st));
+  LocalPtrs lp{};
+  for (int k = 0; k < g->nranks; ++k) lp.p[k] = g->ptr[k];
+  const int grid = (int)((count + 255) / 256 < 1024 ? (count + 255) / 256 : 1024);
+  if (esize == 8) k_local_reduce_i64<<<grid, 256, 0, st>>>(static_cast<int64_t*>(g->tmp[r]), lp, g->nranks, count);
+  else if (op == 0) k_local_reduce_f32<0><<<grid, 256, 0, st>>>(static_cast<float*>(g->tmp[r]), lp, g->nranks, count);
+  else k_local_reduce_f32<1><<<grid, 256, 0, st>>>(static_cast<float*>(g->tmp[r]), lp, g->nranks, count);
+  TRY_CUDA(cudaGetLastError());
+  TRY(local_end(c, st));
+  TRY_CUDA(cudaMemcpyAsync(buf, g->tmp[r], count * esize, cudaMemcpyDeviceToDevice, st));
+  return TANGO_OK;
+}
+
 // ------------------------------------------------------------------ collectives (caller stream)
 static tango_status comm_max(tango_comm* c, void* buf, size_t count, cudaStream_t st) {
-  if (!c || c->nranks == 1) return TANGO_OK;
+  if (!c || c->nranks == 1 || count == 0) return TANGO_OK;
+  if (c->local) return local_reduce(c, buf, count, 4, 0, st);
   TRY_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclMax, c->nccl, st));
   return TANGO_OK;
 }
 static tango_status comm_sum_f32(tango_comm* c, float* buf, size_t count, cudaStream_t st) {
-  if (!c || c->nranks == 1) return TANGO_OK;
+  if (!c || c->nranks == 1 || count == 0) return TANGO_OK;
+  if (c->local) return local_reduce(c, buf, count, 4, 1, st);
   TRY_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, c->nccl, st));
   return TANGO_OK;
 }
 static tango_status comm_sum_i64(tango_comm* c, int64_t* buf, size_t count, cudaStream_t st) {
-  if (!c || c->nranks == 1) return TANGO_OK;
+  if (!c || c->nranks == 1 || count == 0) return TANGO_OK;
+  if (c->local) return local_reduce(c, buf, count, 8, 1, st);
   TRY_NCCL(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, c->nccl, st));
   return TANGO_OK;
 }
@@ -180,6 +278,17 @@ static tango_status comm_sum_i64(tango_comm* c, int64_t* buf, size_t count, cuda
 // broadcast in place to every rank (grouped broadcasts: partitions have different sizes).
 static tango_status comm_gather_rows(tango_comm* c, void* base, size_t row_bytes, cudaStream_t st) {
   if (!c || c->nranks == 1) return TANGO_OK;
+  if (c->local) {
+    TRY(local_begin(c, base, st));
+    for (int k = 0; k < c->nranks; ++k) {
+      const size_t off = (size_t)c->starts[k] * row_bytes;
+      const size_t cnt = (size_t)(c->starts[k + 1] - c->starts[k]) * row_bytes;
+      if (k == c->rank || cnt == 0) continue;
+      TRY_CUDA(cudaMemcpyAsync(static_cast<char*>(base) + off, static_cast<const char*>(c->local->ptr[k]) + off, cnt,
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    return local_end(c, st);
+  }
   TRY_NCCL(ncclGroupStart());
   for (int r = 0; r < c->nranks; ++r) {
     const size_t off = (size_t)c->starts[r] * row_bytes;
@@ -916,6 +1025,49 @@ tango_status tango_comm_destroy(tango_comm* c) {
   if (!c) return TANGO_ERR_INVALID_ARG;
   if (c->nccl) ncclCommDestroy(c->nccl);
   delete c;
+  return TANGO_OK;
+}
+
+tango_status tango_local_group_create(tango_local_group** out, int32_t nranks) {
+  if (!out || nranks < 1 || nranks > 16) return TANGO_ERR_INVALID_ARG;
+  tango_local_group* g = new (std::nothrow) tango_local_group();
+  if (!g) return TANGO_ERR_INVALID_ARG;
+  g->nranks = nranks;
+  g->ptr.assign(nranks, nullptr);
+  g->ev_a.assign(nranks, nullptr);
+  g->ev_b.assign(nranks, nullptr);
+  g->tmp.assign(nranks, nullptr);
+  g->tmp_bytes.assign(nranks, 0);
+  for (int r = 0; r < nranks; ++r) {
+    if (cudaEventCreateWithFlags(&g->ev_a[r], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_b[r], cudaEventDisableTiming) != cudaSuccess) {
+      delete g;
+      return TANGO_ERR_CUDA;
+    }
+  }
+  *out = g;
+  return TANGO_OK;
+}
+
+tango_status tango_local_group_destroy(tango_local_group* g) {
+  if (!g) return TANGO_ERR_INVALID_ARG;
+  for (int r = 0; r < g->nranks; ++r) {
+    if (g->ev_a[r]) cudaEventDestroy(g->ev_a[r]);
+    if (g->ev_b[r]) cudaEventDestroy(g->ev_b[r]);
+    if (g->tmp[r]) cudaFree(g->tmp[r]);
+  }
+  delete g;
+  return TANGO_OK;
+}
+
+tango_status tango_comm_init_local(tango_comm** out, tango_local_group* g, int32_t rank) {
+  if (!out || !g || rank < 0 || rank >= g->nranks) return TANGO_ERR_INVALID_ARG;
+  tango_comm* c = new (std::nothrow) tango_comm();
+  if (!c) return TANGO_ERR_INVALID_ARG;
+  c->local = g;
+  c->nranks = g->nranks;
+  c->rank = rank;
+  *out = c;
   return TANGO_OK;
 }
 

@@ -76,7 +76,8 @@ EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tan
            "tango_gat_ctx_bytes", "tango_gat_layer_fwd", "tango_gat_layer_bwd", "tango_gat_ctx_get_view",
            "tango_gcn_ctx_bytes", "tango_gcn_layer_fwd", "tango_gcn_layer_bwd", "tango_gcn_ctx_get_view",
            "tango_comm_unique_id_bytes", "tango_comm_get_unique_id", "tango_comm_init", "tango_comm_destroy",
-           "tango_comm_set_partition", "tango_profile_enable", "tango_launch_count", "tango_profile_collect",
+           "tango_comm_set_partition", "tango_local_group_create", "tango_local_group_destroy",
+           "tango_comm_init_local", "tango_profile_enable", "tango_launch_count", "tango_profile_collect",
            "tango_profile_num_entries", "tango_profile_entry", "tango_profile_reset"]
 
 
@@ -117,6 +118,9 @@ def load(path: str = LIB_PATH):
     L.tango_comm_init.argtypes = [C.POINTER(_P), _P, i32, i32]
     L.tango_comm_destroy.argtypes = [_P]
     L.tango_comm_set_partition.argtypes = [_P, _P]
+    L.tango_local_group_create.argtypes = [C.POINTER(_P), i32]
+    L.tango_local_group_destroy.argtypes = [_P]
+    L.tango_comm_init_local.argtypes = [C.POINTER(_P), _P, i32]
     L.tango_profile_enable.argtypes = [i32]
     L.tango_profile_enable.restype = None
     L.tango_launch_count.restype = i64
@@ -315,6 +319,17 @@ class Comm:
         starts = np.ascontiguousarray(row_starts, dtype=np.int64)
         _check(L.tango_comm_set_partition(self.handle, starts.ctypes.data), "tango_comm_set_partition")
 
+    @classmethod
+    def local(cls, group: "LocalGroup", rank, row_starts):
+        """Loopback communicator of an in-process group (one host thread per rank, one GPU)."""
+        L = load()
+        self = cls.__new__(cls)
+        self.handle = C.c_void_p()
+        _check(L.tango_comm_init_local(C.byref(self.handle), group.handle, rank), "tango_comm_init_local")
+        starts = np.ascontiguousarray(row_starts, dtype=np.int64)
+        _check(L.tango_comm_set_partition(self.handle, starts.ctypes.data), "tango_comm_set_partition")
+        return self
+
     @staticmethod
     def unique_id() -> bytes:
         L = load()
@@ -326,6 +341,20 @@ class Comm:
     def close(self):
         if self.handle:
             load().tango_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+
+class LocalGroup:
+    """tango_local_group: nranks in-process ranks exchanging through device memory (tests)."""
+
+    def __init__(self, nranks):
+        L = load()
+        self.handle = C.c_void_p()
+        _check(L.tango_local_group_create(C.byref(self.handle), nranks), "tango_local_group_create")
+
+    def close(self):
+        if self.handle:
+            load().tango_local_group_destroy(self.handle)
             self.handle = C.c_void_p()
 
 
