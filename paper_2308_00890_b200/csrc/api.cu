@@ -154,7 +154,8 @@ static GraphDev dev_graph(const tango_graph* G) {
 // so the API stays asynchronous on `st` and CUDA-graph capture of `st` records the fork/join.
 struct AuxStream {
   cudaStream_t s = nullptr;
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[10] = {};
+  SideStream side(int k) const { return SideStream{s, ev[k], ev[k + 1]}; }
 };
 static AuxStream* aux_stream() {
   thread_local AuxStream per_dev[16];
@@ -162,7 +163,9 @@ static AuxStream* aux_stream() {
   if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 16) return nullptr;
   AuxStream& a = per_dev[d];
   if (!a.s) {
-    if (cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess) { a.s = nullptr; return nullptr; }
+    int lo = 0, hi = 0;   // highest priority: the latency-bound hub chain gets SM slots first
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&a.s, cudaStreamNonBlocking, hi) != cudaSuccess) { a.s = nullptr; return nullptr; }
     for (auto& e : a.ev)
       if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
   }
@@ -666,7 +669,10 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   fa.work = (int32_t*)(c + L.off_work);
   fa.alpha = (float*)(c + L.off_alpha);
   TRY_CUDA(cudaMemsetAsync(fa.work, 0, 64, st));
-  TRY(launch_status(launch_gat_fwd(fa, st)));
+  {
+    const SideStream side = aux->side(4);
+    TRY(launch_status(launch_gat_fwd(fa, st, &side)));
+  }
   TRY(comm_max(comm, amax_out, amax_out ? 1 : 0, st));
   TRY(comm_gather_rows(comm, m, (size_t)L.H * 4, st));
   TRY(comm_gather_rows(comm, den, (size_t)L.H * 4, st));
@@ -748,10 +754,11 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   ba.alpha = (const float*)(c + L.off_alpha);
   ba.alpha_dE = (float*)(c + L.off_alpha);
   TRY_CUDA(cudaMemsetAsync(ba.work, 0, 64, st));
-  TRY(launch_status(launch_gat_bwd_dst(ba, st)));
+  const SideStream side_d = aux->side(4), side_s = aux->side(6);
+  TRY(launch_status(launch_gat_bwd_dst(ba, st, &side_d)));
   TRY(comm_gather_rows(comm, P, (size_t)L.H * 4, st));
   TRY_CUDA(cudaStreamWaitEvent(st, aux->ev[1], 0));   // out-CSR plan done
-  TRY(launch_status(launch_gat_bwd_src(ba, st)));
+  TRY(launch_status(launch_gat_bwd_src(ba, st, &side_s)));
   // ∂a (needs ∂S, ∂D) on the side stream, beside B8/B9
   TRY_CUDA(stream_after(aux->s, st, aux->ev[2]));
   TRY(launch_status(launch_gat_attn_grad(ba, aux->s)));

@@ -417,7 +417,9 @@ __global__ void __launch_bounds__(256) k_fwd_stats_t(const GatFwdArgs a) {
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t n = a.g.n_local, hc = load_count(a.plan.counts);
   const int64_t nitems = hc + load_count(a.plan.counts + 2);
-  FOR_ITEMS(item, a.work + 0, nitems) {
+  const int64_t i_lo = a.part == 2 ? hc : 0, i_hi = a.part == 1 ? hc : nitems;   // hub / light split
+  FOR_ITEMS(it, a.work + 0 + (a.part == 1 ? 8 : 0), i_hi - i_lo) {
+    const int64_t item = i_lo + it;
     if (item < hc) {
       Seg s;
       decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s);
@@ -1350,7 +1352,9 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg4(const GatFwdArgs a) {
   const int8_t* xbase = a.qHp + lane * VPL;
   const uint32_t ld32 = (uint32_t)a.ldHp;
   float amax_loc = 0.0f;
-  FOR_ITEMS(item, a.work + 2, nitems) {
+  const int64_t i_lo = a.part == 2 ? hc : 0, i_hi = a.part == 1 ? hc : nitems;   // hub / light split
+  FOR_ITEMS(it, a.work + 2 + (a.part == 1 ? 8 : 0), i_hi - i_lo) {
+    const int64_t item = i_lo + it;
     const bool tile = item >= hc;
     Seg s;
     s.eb = 0;
@@ -2132,7 +2136,9 @@ __global__ void __maxnreg__(80) k_bwd_dst1_v4(const GatBwdArgs a) {
   const int8_t* xbase = a.qHp + lane * VPL;
   const int8_t* gbase = a.qG + lane * VPL;
   const uint32_t ld32 = (uint32_t)a.ldHp;
-  FOR_ITEMS(item, a.work + 0, nitems) {
+  const int64_t i_lo = a.part == 2 ? hc : 0, i_hi = a.part == 1 ? hc : nitems;   // hub / light split
+  FOR_ITEMS(it, a.work + 0 + (a.part == 1 ? 8 : 0), i_hi - i_lo) {
+    const int64_t item = i_lo + it;
     const bool tile = item >= hc;
     Seg s;
     s.eb = 0;
@@ -2401,7 +2407,9 @@ __global__ void __maxnreg__(96) k_bwd_src4(const GatBwdArgs a) {
   const int8_t* gbase = a.qG + lane * VPL;
   const uint32_t ld32 = (uint32_t)a.ldG;
   float amax_loc = 0.0f;
-  FOR_ITEMS(item, a.work + 2, nitems) {
+  const int64_t i_lo = a.part == 2 ? hc : 0, i_hi = a.part == 1 ? hc : nitems;   // hub / light split
+  FOR_ITEMS(it, a.work + 2 + (a.part == 1 ? 8 : 0), i_hi - i_lo) {
+    const int64_t item = i_lo + it;
     const bool tile = item >= hc;
     Seg s;
     s.eb = 0;
@@ -3168,8 +3176,119 @@ bool gat_shape_supported(int heads, int head_dim) {
   return cg_shape(head_dim, v, p);
 }
 
-cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
+// ---- hub / light split: the hub-row chain (segment statistics, folds) runs on a side stream beside
+// the light sub-tiles, which need none of it (v4 engine, VPL >= 4).
+static cudaError_t fork_to(cudaStream_t st, const SideStream& x) {
+  cudaError_t e = cudaEventRecord(x.fork, st);
+  return e == cudaSuccess ? cudaStreamWaitEvent(x.s, x.fork, 0) : e;
+}
+static cudaError_t join_from(cudaStream_t st, const SideStream& x) {
+  cudaError_t e = cudaEventRecord(x.join, x.s);
+  return e == cudaSuccess ? cudaStreamWaitEvent(st, x.join, 0) : e;
+}
+
+static cudaError_t launch_gat_fwd_split(const GatFwdArgs& a, cudaStream_t st, const SideStream& x) {
+  const int hv = a.d.heads * 100 + a.d.hd / 32;
+  GatFwdArgs ah = a, al = a;
+  ah.part = 1;
+  al.part = 2;
+  cudaError_t e = fork_to(st, x);
+  if (e != cudaSuccess) return e;
+  bool ok = false;
+#define X(H_, V_)                                                                                  \
+  if (hv == H_ * 100 + V_ && V_ >= 4) {                                                            \
+    ok = true;                                                                                     \
+    constexpr int VV = V_ >= 4 ? V_ : 4;                                                           \
+    constexpr int fsm = 8 * fs_warp_smem<H_>();                                                    \
+    constexpr int smem = 8 * g4_warp_smem<H_, VV, false>();                                        \
+    static bool attr_set = false;                                                                  \
+    if (!attr_set) {                                                                               \
+      cudaFuncSetAttribute(k_fwd_stats_t<H_>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);   \
+      cudaFuncSetAttribute(k_fwd_agg4<H_, VV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      attr_set = true;                                                                             \
+    }                                                                                              \
+    { ProfScope p("gat_fwd_stats_hub", x.s); k_fwd_stats_t<H_><<<heavy_grid(a.plan.cap), 256, fsm, x.s>>>(ah); } \
+    { ProfScope p("gat_fwd_stats2", x.s); k_fwd_stats2<H_><<<heavy_grid(a.plan.cap), 256, 0, x.s>>>(ah); } \
+    { ProfScope p("gat_fwd_alpha3", x.s); k_fwd_alpha3<H_><<<heavy_grid(a.plan.cap), 256, 0, x.s>>>(ah); } \
+    { ProfScope p("gat_fwd_agg_hub", x.s); k_fwd_agg4<H_, VV><<<heavy_grid(a.plan.cap), 256, smem, x.s>>>(ah); } \
+    { ProfScope p("gat_fwd_combine", x.s); k_fwd_combine<H_, V_><<<heavy_grid(a.plan.cap), 256, 0, x.s>>>(ah); } \
+    { ProfScope p("gat_fwd_stats", st); k_fwd_stats_t<H_><<<item_grid(a.plan.tcap), 256, fsm, st>>>(al); } \
+    { ProfScope p("gat_fwd_agg", st); k_fwd_agg4<H_, VV><<<item_grid(a.plan.tcap), 256, smem, st>>>(al); } \
+  }
+  TANGO_HV_CASES(X)
+#undef X
+  if (!ok) return cudaErrorInvalidValue;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return join_from(st, x);
+}
+
+static cudaError_t launch_gat_bwd_dst_split(const GatBwdArgs& a, cudaStream_t st, const SideStream& x) {
+  const int hv = a.d.heads * 100 + a.d.hd / 32;
+  GatBwdArgs ah = a, al = a;
+  ah.part = 1;
+  al.part = 2;
+  cudaError_t e = fork_to(st, x);
+  if (e != cudaSuccess) return e;
+  bool ok = false;
+#define X(H_, V_)                                                                                  \
+  if (hv == H_ * 100 + V_ && V_ >= 4 && H_ <= 8) {                                                 \
+    ok = true;                                                                                     \
+    constexpr int VV = V_ >= 4 ? V_ : 4;                                                           \
+    constexpr int NW = 7, smem4 = NW * dst4_warp_smem<H_, VV>();                                   \
+    static bool attr_set = false;                                                                  \
+    if (!attr_set) {                                                                               \
+      cudaFuncSetAttribute(k_bwd_dst1_v4<H_, VV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); \
+      attr_set = true;                                                                             \
+    }                                                                                              \
+    { ProfScope p("gat_bwd_dst1_hub", x.s);                                                        \
+      k_bwd_dst1_v4<H_, VV, NW><<<heavy_grid(a.pin.cap), NW * 32, smem4, x.s>>>(ah); }             \
+    { ProfScope p("gat_bwd_dst2", x.s); k_bwd_dst2<H_><<<heavy_grid(a.pin.cap), 256, 0, x.s>>>(ah); } \
+    { ProfScope p("gat_bwd_dst3", x.s); k_bwd_dst3<H_><<<heavy_grid(a.pin.cap), 256, 0, x.s>>>(ah); } \
+    { ProfScope p("gat_bwd_dst1", st);                                                             \
+      k_bwd_dst1_v4<H_, VV, NW><<<item_grid(a.pin.tcap), NW * 32, smem4, st>>>(al); }              \
+  }
+  TANGO_HV_CASES(X)
+#undef X
+  if (!ok) return cudaErrorInvalidValue;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return join_from(st, x);
+}
+
+static cudaError_t launch_gat_bwd_src_split(const GatBwdArgs& a, cudaStream_t st, const SideStream& x) {
+  const int hv = a.d.heads * 100 + a.d.hd / 32;
+  GatBwdArgs ah = a, al = a;
+  ah.part = 1;
+  al.part = 2;
+  cudaError_t e = fork_to(st, x);
+  if (e != cudaSuccess) return e;
+  bool ok = false;
+#define X(H_, V_)                                                                                  \
+  if (hv == H_ * 100 + V_ && V_ >= 4) {                                                            \
+    ok = true;                                                                                     \
+    constexpr int VV = V_ >= 4 ? V_ : 4;                                                           \
+    constexpr int NW = 4, smem4 = NW * g4_warp_smem<H_, VV, true>();                               \
+    static bool attr_set = false;                                                                  \
+    if (!attr_set) {                                                                               \
+      cudaFuncSetAttribute(k_bwd_src4<H_, VV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); \
+      attr_set = true;                                                                             \
+    }                                                                                              \
+    { ProfScope p("gat_bwd_src_hub", x.s);                                                         \
+      k_bwd_src4<H_, VV, NW><<<heavy_grid(a.pout.cap), NW * 32, smem4, x.s>>>(ah); }               \
+    { ProfScope p("gat_bwd_src_combine", x.s);                                                     \
+      k_bwd_src_combine<H_, V_><<<heavy_grid(a.pout.cap), 256, 0, x.s>>>(ah); }                    \
+    { ProfScope p("gat_bwd_src", st);                                                              \
+      k_bwd_src4<H_, VV, NW><<<item_grid(a.pout.tcap), NW * 32, smem4, st>>>(al); }                \
+  }
+  TANGO_HV_CASES(X)
+#undef X
+  if (!ok) return cudaErrorInvalidValue;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return join_from(st, x);
+}
+
+cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st, const SideStream* aux) {
   if (a.g.n_local == 0) return cudaSuccess;
+  if (aux && a.d.hd / 32 >= 4 && !gather_tma()) return launch_gat_fwd_split(a, st, *aux);
   const int hv = a.d.heads * 100 + a.d.hd / 32;
   int vpl, hpw;
   if (!cg_shape(a.d.head_dim, vpl, hpw)) return cudaErrorInvalidValue;
@@ -3232,8 +3351,9 @@ cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st) {
+cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st, const SideStream* aux) {
   if (a.g.n_local == 0) return cudaSuccess;
+  if (aux && a.d.hd / 32 >= 4 && a.d.heads <= 8) return launch_gat_bwd_dst_split(a, st, *aux);
   int vpl, hpw;
   if (!cg_shape(a.d.head_dim, vpl, hpw)) return cudaErrorInvalidValue;
   const int64_t cg_items = (a.pin.cap + (a.g.n_local + TILE - 1) / TILE) * (a.d.hd / (32 * vpl));
@@ -3290,8 +3410,9 @@ cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st) {
+cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st, const SideStream* aux) {
   if (a.g.n_local == 0) return cudaSuccess;
+  if (aux && a.d.hd / 32 >= 4 && a.g.out_eid && !gather_tma()) return launch_gat_bwd_src_split(a, st, *aux);
   int vpl, hpw;
   if (!cg_shape(a.d.head_dim, vpl, hpw)) return cudaErrorInvalidValue;
   const int64_t cg_items = (a.pout.cap + (a.g.n_local + TILE - 1) / TILE) * (a.d.hd / (32 * vpl));

@@ -97,8 +97,12 @@ struct GatFwdArgs {
   float* hagg;                                // [cap][HD] heavy-segment aggregation partials
   int32_t* work;                              // [8] work-queue counters (zeroed before the launch)
   float* alpha;                               // [e_in][2H]: α with the sign of e_pre (LeakyReLU branch) | ∂E_pre
+  int part;                                   // work items: 0 all, 1 hub segments only, 2 light sub-tiles only
 };
-cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st);
+// aux (nullable): a second stream that runs the hub-row chain beside the light sub-tiles
+// (fork/join with the two events); null -> everything in order on st.
+struct SideStream { cudaStream_t s; cudaEvent_t fork, join; };
+cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st, const SideStream* aux = nullptr);
 
 struct GatBwdArgs {
   GraphDev g; GatDims d; float slope; int bits;
@@ -120,9 +124,10 @@ struct GatBwdArgs {
   int32_t* work;                             // [8] work-queue counters (zeroed before the launch)
   const float* alpha;                        // [e_in][2H]: signed α from the forward | ∂E_pre (written here)
   float* alpha_dE;                           // same buffer, written by the destination passes
+  int part;                                  // as GatFwdArgs::part
 };
-cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st);
-cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st);
+cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st, const SideStream* aux = nullptr);
+cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st, const SideStream* aux = nullptr);
 cudaError_t launch_gat_attn_grad(const GatBwdArgs& a, cudaStream_t st);
 
 // standalone primitives (unfused; used by the primitive C-ABI entry points)
