@@ -227,6 +227,7 @@ typedef struct {
   float *S, *D, *m, *den, *P, *dD, *dHp, *dalpha;   /* dalpha: [e_in][H] ∂α */
   float *alpha_pack;       /* [e_in][2H]: α (sign bit = LeakyReLU branch of e_pre) | ∂E_pre */
   float *scalars;          /* see DESIGN.md §4 "ctx scalars" for the slot map */
+  int32_t codes_biased;    /* 1: qHp and qG hold excess-128 codes (bit pattern q ^ 0x80) */
 } tango_gat_ctx_view;
 tango_status tango_gat_ctx_get_view(const tango_graph* G, const tango_gat_params* p, void* ctx,
                                     tango_gat_ctx_view* view);

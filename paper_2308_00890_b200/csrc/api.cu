@@ -575,6 +575,7 @@ tango_status tango_gat_ctx_get_view(const tango_graph* G, const tango_gat_params
   v->dHp = (float*)(c + L.off_dHp); v->dalpha = (float*)(c + L.off_dal);
   v->alpha_pack = (float*)(c + L.off_alpha);
   v->scalars = (float*)(c + L.off_scal);
+  v->codes_biased = gat_codes_biased(p->heads, (int)L.HD) ? 1 : 0;
   return TANGO_OK;
 }
 
@@ -647,6 +648,8 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   gb.amax_in = sc + SL_AMAX_HP; gb.bits = p->bits; gb.seed = rng.seed; gb.step = rng.step;
   gb.tag = tag_of(layer_id, R_HP); gb.g_row0 = r0;
   gb.q_out = qHp + r0 * L.ldHD; gb.ldq = L.ldHD; gb.scale_out = scf + SL_S_HP; gb.status = dev_status;
+  const bool biased = gat_codes_biased(p->heads, (int)L.HD);   // q_H′ / q_G as excess-128 codes
+  gb.code_xor = biased ? 0x80808080u : 0u;
   TRY(launch_status(launch_gemm(gb, st)));
   TRY(launch_status(launch_quantize(S, L.n, L.H, nullptr, r0 * L.H, sc + SL_AMAX_S, p->bits, rng.seed, rng.step,
                                     tag_of(layer_id, R_S), qS + r0 * L.H, L.H, nullptr, 0, scf + SL_S_S, dev_status,
@@ -668,6 +671,7 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   fa.plan = pin; fa.hmax = (float*)(c + L.off_h1); fa.hden = (float*)(c + L.off_h2); fa.hagg = (float*)(c + L.off_hagg);
   fa.work = (int32_t*)(c + L.off_work);
   fa.alpha = (float*)(c + L.off_alpha);
+  fa.codes_biased = biased;
   TRY_CUDA(cudaMemsetAsync(fa.work, 0, 64, st));
   {
     const SideStream side = aux->side(4);
@@ -730,9 +734,10 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
     TRY(launch_status(launch_absmax(dH_out, L.n, L.HD, nullptr, sc + SL_AMAX_G, st)));
     TRY(comm_max(comm, sc + SL_AMAX_G, 1, st));
   }
+  const bool biased = gat_codes_biased(p->heads, (int)L.HD);   // q_H′ / q_G as excess-128 codes
   TRY(launch_status(launch_quantize(dH_out, L.n, L.HD, nullptr, r0 * L.HD, sc + SL_AMAX_G, p->bits, rng.seed,
                                     rng.step, tag_of(layer_id, R_G), qG + r0 * L.ldHD, L.ldHD, nullptr, 0,
-                                    scf + SL_S_G, dev_status, st)));
+                                    scf + SL_S_G, dev_status, st, biased ? 0x80808080u : 0u)));
   TRY(comm_gather_rows(comm, qG, (size_t)L.ldHD, st));
   // B2-B4: destination rows (in-CSR plan from the forward call), B5-B7: source rows (out-CSR plan,
   // built on the side stream since the start of the call)
@@ -753,6 +758,7 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   ba.dS = (float*)(c + L.off_dS);
   ba.alpha = (const float*)(c + L.off_alpha);
   ba.alpha_dE = (float*)(c + L.off_alpha);
+  ba.codes_biased = biased;
   TRY_CUDA(cudaMemsetAsync(ba.work, 0, 64, st));
   const SideStream side_d = aux->side(4), side_s = aux->side(6);
   TRY(launch_status(launch_gat_bwd_dst(ba, st, &side_d)));

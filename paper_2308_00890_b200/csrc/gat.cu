@@ -867,10 +867,47 @@ __device__ __forceinline__ float2 codes2(uint32_t wx, uint32_t s0, uint32_t s1) 
                                 __uint_as_float(__byte_perm(wx, 0x4B000000u, s1))),
                     make_float2(-8388736.0f, -8388736.0f));
 }
+// the same for 4 excess-128 codes (q + 128): the PRMT already yields 2^23 + 128 + q, no sign flip
+__device__ __forceinline__ void fma4_biased(uint32_t word, float2 al2, float2& a01, float2& a23) {
+  a01 = __ffma2_rn(al2, codes2(word, 0x7440u, 0x7441u), a01);
+  a23 = __ffma2_rn(al2, codes2(word, 0x7442u, 0x7443u), a23);
+}
+// Σ_k a_k·b_k over 4 byte lanes with a unsigned (excess-128 codes) and b signed
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
+  int d;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+// exact q_x·q_y of this lane's slice where x holds excess-128 codes and y plain codes:
+// Σ (q_x + 128)·q_y − 128·Σ q_y
+template <int VPL>
+__device__ __forceinline__ int row_dot_biased(const Row<VPL>& x, const Row<VPL>& y, int ysum) {
+  int acc = 0;
+#pragma unroll
+  for (int i = 0; i < VPL / 4; ++i) acc = dp4a_us(x.w[i], y.w[i], acc);
+  return acc - 128 * ysum;
+}
+// Σ of this lane's plain codes (for the correction above); flips excess-128 codes to plain first
+template <int VPL>
+__device__ __forceinline__ int row_sum_plain(Row<VPL>& y, bool flip) {
+  int s = 0;
+#pragma unroll
+  for (int i = 0; i < VPL / 4; ++i) {
+    if (flip) y.w[i] ^= 0x80808080u;
+    s = __dp4a((int)y.w[i], 0x01010101, s);
+  }
+  return s;
+}
+
 __device__ __forceinline__ void fma4_codes(uint32_t word, float2 al2, float2& a01, float2& a23) {
   const uint32_t wx = word ^ 0x80808080u;
   a01 = __ffma2_rn(al2, codes2(wx, 0x7440u, 0x7441u), a01);
   a23 = __ffma2_rn(al2, codes2(wx, 0x7442u, 0x7443u), a23);
+}
+template <bool BIASED>
+__device__ __forceinline__ void fma4_any(uint32_t word, float2 al2, float2& a01, float2& a23) {
+  if constexpr (BIASED) fma4_biased(word, al2, a01, a23);
+  else fma4_codes(word, al2, a01, a23);
 }
 
 // Streamed aggregation of one 32-edge chunk: rows q_X[w_i] gathered through a rolling ring of RING
@@ -1212,6 +1249,7 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg3(const GatFwdArgs a) {
 // indices also come from shared memory (one LDS.128 per 4 edges, no shuffles).  The tail group is
 // padded with α = +0, x = +0 and the last row: fmaf(+0, q, acc) == acc and acc + (+0) == acc for
 // every acc these sums can hold (never -0), so padding is exact and the group loop is branch-free.
+// The gathered tables hold excess-128 codes (gat_codes_biased), converted without a sign flip.
 template <int H, int VPL, bool HAS_X>
 __host__ __device__ constexpr int g4_warp_smem() {
   return AGG_RING * 32 * VPL + 2 * H * 32 * 4 * (HAS_X ? 2 : 1) + 2 * 32 * 4 + 2 * 32;
@@ -1260,7 +1298,7 @@ __device__ __forceinline__ int g4_stream(uint8_t* wsm, const int8_t* __restrict_
       for (int j = 0; j < 4; ++j) {
         const float2 al2 = make_float2(al[j], al[j]);
 #pragma unroll
-        for (int q = 0; q < VPL / 4; ++q) fma4_codes(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
+        for (int q = 0; q < VPL / 4; ++q) fma4_biased(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
         if constexpr (HAS_X) xs = __fadd_rn(xs, xv[j]);
       }
     } else {
@@ -1273,7 +1311,7 @@ __device__ __forceinline__ int g4_stream(uint8_t* wsm, const int8_t* __restrict_
         }
         const float2 al2 = make_float2(al[j], al[j]);
 #pragma unroll
-        for (int q = 0; q < VPL / 4; ++q) fma4_codes(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
+        for (int q = 0; q < VPL / 4; ++q) fma4_biased(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
         if constexpr (HAS_X) xs = __fadd_rn(xs, xv[j]);
       }
     }
@@ -1899,7 +1937,7 @@ __device__ __forceinline__ void src_finalize_full(const GatBwdArgs& a, int64_t u
 // BS: ⑤′ ∂H′_agg = Σ fmaf(α, q_G[v]) over out-edges, ③′ ∂S = Σ ∂E_pre, ②′ finalize (light rows);
 // heavy out-segments leave ∂S / aggregation partials.  α comes from the stored signed α via out_eid
 // when available (one GPU), otherwise it is recomputed from per-node data.
-template <int H, int VPL>
+template <int H, int VPL, bool B>
 __global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
   constexpr int HD = 32 * VPL, R = AGG_RING, RB = 32 * VPL, LPH = 32 / H;
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -1994,6 +2032,7 @@ __global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
     const unsigned act = tile ? __ballot_sync(0xffffffffu, L.deg > 0) : 1u;
     int nxt = act ? __ffs(act) - 1 : -1;
     Row<VPL> hw{}, hw_nxt{};
+    int hsum = 0;   // Σ of the own q_H′ slice in plain codes (excess-128 correction of the dots)
     if (nxt >= 0) hw_nxt = load_row<VPL>(hbase + (ug0 + nxt) * a.ldHp);
     int vA, rowA;
     float alA[H], pA[H];
@@ -2036,6 +2075,7 @@ __global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
               }
               cur = ri;
               hw = hw_nxt;
+              if constexpr (B) hsum = row_sum_plain<VPL>(hw, true);
               nxt = tile ? tile_next(act, cur) : -1;
               if (nxt >= 0) hw_nxt = load_row<VPL>(hbase + (ug0 + nxt) * a.ldHp);
             }
@@ -2044,7 +2084,14 @@ __global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
             if (use_eid) {   // ∂E_pre read from the destination pass
               if (leader) dS = __fadd_rn(dS, sp[cb][i0 + j][myh]);
             } else {         // recompute ∂α = q_G[v]·q_H′[u] and ∂E_pre (partitioned graphs)
-              const int dot = head_dot<VPL, LPH>(r[j], hw);
+              int dot;
+              if constexpr (B) {
+                dot = row_dot_biased<VPL>(r[j], hw, hsum);
+#pragma unroll
+                for (int o = 1; o < LPH; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+              } else {
+                dot = head_dot<VPL, LPH>(r[j], hw);
+              }
               if (leader) {
                 const float dal = __fmul_rn(__int2float_rn(dot), sGH);
                 const float dE = __fmul_rn(al, __fsub_rn(dal, sp[cb][i0 + j][myh]));
@@ -2053,7 +2100,7 @@ __global__ void __launch_bounds__(256, 2) k_bwd_src_v3(const GatBwdArgs a) {
             }
             const float2 al2 = make_float2(al, al);
 #pragma unroll
-            for (int q = 0; q < VPL / 4; ++q) fma4_codes(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
+            for (int q = 0; q < VPL / 4; ++q) fma4_any<B>(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
           }
         }
 #pragma unroll
@@ -2114,7 +2161,7 @@ __host__ __device__ constexpr int dst4_warp_smem() {
 
 // BD1 (v4 engine): ⑤″ ∂α = i2f(q_G[v]·q_H′[u]) (s_G s_H′), ④′ P = Σ fmaf(∂α, α) in edge order per
 // destination row (heavy segments: P partials), then for light rows ∂E_pre and ∂D (pass 2).
-template <int H, int VPL, int NW>
+template <int H, int VPL, int NW, bool B>
 __global__ void __maxnreg__(80) k_bwd_dst1_v4(const GatBwdArgs a) {
   constexpr int R = AGG_RING, RB = 32 * VPL, LPH = 32 / H;
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -2193,6 +2240,7 @@ __global__ void __maxnreg__(80) k_bwd_dst1_v4(const GatBwdArgs a) {
     const int64_t vg0 = a.g.row_begin + (tile ? r0 : s.vl);
     int nxt = act ? __ffs(act) - 1 : -1;
     Row<VPL> gw{}, gw_nxt{};
+    int gsum = 0;   // Σ of the own q_G slice in plain codes (excess-128 correction of the dots)
     if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
     int64_t eA;
     {
@@ -2217,6 +2265,7 @@ __global__ void __maxnreg__(80) k_bwd_dst1_v4(const GatBwdArgs a) {
     if (!tile) {   // a heavy segment is one row
       cur = 0; pcur = 0;
       gw = gw_nxt;
+      if constexpr (B) gsum = row_sum_plain<VPL>(gw, true);
     }
     const int nch = (T + 31) >> 5;
     for (int c = 0; c < nch; ++c) {
@@ -2245,7 +2294,7 @@ __global__ void __maxnreg__(80) k_bwd_dst1_v4(const GatBwdArgs a) {
         const bool same = (int)(rw >> 24) == cur;
         if (same) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) d[j] = row_dot<VPL>(gw, r[j]);
+          for (int j = 0; j < 4; ++j) d[j] = B ? row_dot_biased<VPL>(r[j], gw, gsum) : row_dot<VPL>(gw, r[j]);
         } else {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -2253,10 +2302,11 @@ __global__ void __maxnreg__(80) k_bwd_dst1_v4(const GatBwdArgs a) {
             if (rj != cur) {
               cur = rj;
               gw = gw_nxt;
+              if constexpr (B) gsum = row_sum_plain<VPL>(gw, true);
               nxt = tile_next(act, cur);
               if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
             }
-            d[j] = row_dot<VPL>(gw, r[j]);
+            d[j] = B ? row_dot_biased<VPL>(r[j], gw, gsum) : row_dot<VPL>(gw, r[j]);
           }
         }
         int k;
@@ -3075,6 +3125,7 @@ __global__ void __launch_bounds__(256) k_bwd_attn_grad(const GatBwdArgs a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int myh = lane / LPH;
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const uint32_t flip = a.codes_biased ? 0u : 0x80808080u;   // to excess-128 for the PRMT conversion
   float das[VPL], dad[VPL];
 #pragma unroll
   for (int k = 0; k < VPL; ++k) { das[k] = 0.0f; dad[k] = 0.0f; }
@@ -3107,7 +3158,7 @@ __global__ void __launch_bounds__(256) k_bwd_attn_grad(const GatBwdArgs a) {
       const float2 s2 = make_float2(dS[i], dS[i]), d2 = make_float2(dD[i], dD[i]);
 #pragma unroll
       for (int q = 0; q < VPL / 4; ++q) {
-        const uint32_t wx = hw[i].w[q] ^ 0x80808080u;
+        const uint32_t wx = hw[i].w[q] ^ flip;
 #pragma unroll
         for (int z = 0; z < 2; ++z) {
           const float2 c = codes2(wx, z ? 0x7442u : 0x7440u, z ? 0x7443u : 0x7441u);
@@ -3156,6 +3207,8 @@ static int heavy_grid(int64_t cap) {
   const int c = num_sms() * 2;
   return g < c ? g : c;
 }
+
+bool gat_codes_biased(int heads, int hd) { return hd / 32 >= 4 && heads <= 8 && !gather_tma(); }
 
 // (H, HD/32) for the row-wide kernels, (VPL, HPW) head-group shape for the gather kernels
 #define TANGO_HV_CASES(X) X(1, 2) X(1, 4) X(1, 8) X(1, 16) X(2, 2) X(2, 4) X(2, 8) X(2, 16) \
@@ -3237,15 +3290,15 @@ static cudaError_t launch_gat_bwd_dst_split(const GatBwdArgs& a, cudaStream_t st
     constexpr int NW = 7, smem4 = NW * dst4_warp_smem<H_, VV>();                                   \
     static bool attr_set = false;                                                                  \
     if (!attr_set) {                                                                               \
-      cudaFuncSetAttribute(k_bwd_dst1_v4<H_, VV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); \
+      cudaFuncSetAttribute(k_bwd_dst1_v4<H_, VV, NW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); cudaFuncSetAttribute(k_bwd_dst1_v4<H_, VV, NW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); \
       attr_set = true;                                                                             \
     }                                                                                              \
     { ProfScope p("gat_bwd_dst1_hub", x.s);                                                        \
-      k_bwd_dst1_v4<H_, VV, NW><<<heavy_grid(a.pin.cap), NW * 32, smem4, x.s>>>(ah); }             \
+      if (a.codes_biased) k_bwd_dst1_v4<H_, VV, NW, true><<<heavy_grid(a.pin.cap), NW * 32, smem4, x.s>>>(ah); else k_bwd_dst1_v4<H_, VV, NW, false><<<heavy_grid(a.pin.cap), NW * 32, smem4, x.s>>>(ah); }             \
     { ProfScope p("gat_bwd_dst2", x.s); k_bwd_dst2<H_><<<heavy_grid(a.pin.cap), 256, 0, x.s>>>(ah); } \
     { ProfScope p("gat_bwd_dst3", x.s); k_bwd_dst3<H_><<<heavy_grid(a.pin.cap), 256, 0, x.s>>>(ah); } \
     { ProfScope p("gat_bwd_dst1", st);                                                             \
-      k_bwd_dst1_v4<H_, VV, NW><<<item_grid(a.pin.tcap), NW * 32, smem4, st>>>(al); }              \
+      if (a.codes_biased) k_bwd_dst1_v4<H_, VV, NW, true><<<item_grid(a.pin.tcap), NW * 32, smem4, st>>>(al); else k_bwd_dst1_v4<H_, VV, NW, false><<<item_grid(a.pin.tcap), NW * 32, smem4, st>>>(al); }              \
   }
   TANGO_HV_CASES(X)
 #undef X
@@ -3375,10 +3428,10 @@ cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st, const SideS
         constexpr int NW = 7, smem4 = NW * dst4_warp_smem<H_, VV>();                               \
         static bool attr4_set = false;                                                             \
         if (!attr4_set) {                                                                          \
-          cudaFuncSetAttribute(k_bwd_dst1_v4<H_, VV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); \
+          cudaFuncSetAttribute(k_bwd_dst1_v4<H_, VV, NW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); cudaFuncSetAttribute(k_bwd_dst1_v4<H_, VV, NW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); \
           attr4_set = true;                                                                        \
         }                                                                                          \
-        k_bwd_dst1_v4<H_, VV, NW><<<item_grid(a.pin.cap + a.pin.tcap), NW * 32, smem4, st>>>(a);   \
+        if (a.codes_biased) k_bwd_dst1_v4<H_, VV, NW, true><<<item_grid(a.pin.cap + a.pin.tcap), NW * 32, smem4, st>>>(a); else k_bwd_dst1_v4<H_, VV, NW, false><<<item_grid(a.pin.cap + a.pin.tcap), NW * 32, smem4, st>>>(a);   \
       } else {                                                                                     \
         k_bwd_dst1_v3<H_, VV><<<item_grid(a.pin.cap + a.pin.tcap), 256, smem, st>>>(a);            \
       }                                                                                            \
@@ -3426,7 +3479,8 @@ cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st, const SideS
       constexpr int smem = 8 * bwd3_warp_smem<H_, VV>();                                           \
       static bool attr_set = false;                                                                \
       if (!attr_set) {                                                                             \
-        cudaFuncSetAttribute(k_bwd_src_v3<H_, VV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        cudaFuncSetAttribute(k_bwd_src_v3<H_, VV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        cudaFuncSetAttribute(k_bwd_src_v3<H_, VV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
         attr_set = true;                                                                           \
       }                                                                                            \
       ProfScope p("gat_bwd_src", st);                                                              \
@@ -3452,7 +3506,8 @@ cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st, const SideS
           k_bwd_src4<H_, VV, NW><<<item_grid(a.pout.cap + a.pout.tcap), NW * 32, smem4, st>>>(a);  \
         }                                                                                          \
       } else {                                                                                     \
-        k_bwd_src_v3<H_, VV><<<item_grid(a.pout.cap + a.pout.tcap), 256, smem, st>>>(a);           \
+        if (a.codes_biased) k_bwd_src_v3<H_, VV, true><<<item_grid(a.pout.cap + a.pout.tcap), 256, smem, st>>>(a); \
+        else k_bwd_src_v3<H_, VV, false><<<item_grid(a.pout.cap + a.pout.tcap), 256, smem, st>>>(a);  \
       }                                                                                            \
     }
     TANGO_HV_CASES(X)

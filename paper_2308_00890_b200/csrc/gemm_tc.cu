@@ -40,6 +40,7 @@ struct KParams {
   unsigned* amax_slot;
   const float* a_src; const float* a_dst; int head_dim; float* S; float* Dd; int heads;
   unsigned* amax_S; unsigned* amax_D;
+  uint32_t code_xor;   // EPI_QUANT: 0x80808080 stores excess-128 codes (q + 128) for the gather kernels
   const unsigned* amax_in; int bits; PhiloxKey key; uint32_t step; uint32_t tag; int64_t g_row0;
   int8_t* q_out; int64_t ldq; float* scale_out; int32_t* status;
   void* C; int64_t ldc;
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             for (int k = 0; k < 8; ++k) v[k] = deq(r[g8 * 8 + k], sAB, has_rs, rs);
             const uint2 pk = sr_quant8(v, qs.r, rnd, qmax);
             const bool in = col0 + g8 * 8 < p.N;   // N % 8 == 0: whole groups are in or out
-            packed[g8 * 2] = in ? pk.x : 0u; packed[g8 * 2 + 1] = in ? pk.y : 0u;
+            packed[g8 * 2] = in ? pk.x ^ p.code_xor : 0u; packed[g8 * 2 + 1] = in ? pk.y ^ p.code_xor : 0u;
           }
           if (row_ok && col0 < p.ldq) {
             uint4* dst = reinterpret_cast<uint4*>(p.q_out + row * p.ldq + col0);
@@ -394,7 +395,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
   p.sA = a.sA; p.sB = a.sB; p.rowscale = a.rowscale;
   p.amax_slot = a.amax_slot; p.a_src = a.a_src; p.a_dst = a.a_dst; p.head_dim = a.head_dim > 0 ? a.head_dim : 1;
   p.S = a.S; p.Dd = a.Dd; p.heads = a.heads; p.amax_S = a.amax_S; p.amax_D = a.amax_D;
-  p.amax_in = a.amax_in; p.bits = a.bits > 0 ? a.bits : 8; p.key = philox_key(a.seed); p.step = a.step; p.tag = a.tag;
+  p.amax_in = a.amax_in; p.bits = a.bits > 0 ? a.bits : 8; p.key = philox_key(a.seed); p.code_xor = a.code_xor; p.step = a.step; p.tag = a.tag;
   p.g_row0 = a.g_row0; p.q_out = a.q_out; p.ldq = a.ldq; p.scale_out = a.scale_out; p.status = a.status;
   p.C = a.C; p.ldc = a.ldc;
 

@@ -26,7 +26,7 @@ cudaError_t launch_absmax(const float* x, int64_t rows, int64_t cols, const floa
 cudaError_t launch_quantize(const float* x, int64_t rows, int64_t cols, const float* rowscale, int64_t g0,
                             const unsigned* amax_slot, int bits, uint64_t seed, uint32_t step, uint32_t tag,
                             int8_t* q, int64_t ld, int8_t* qt, int64_t ldt, float* scale_out, int32_t* status,
-                            cudaStream_t st);
+                            cudaStream_t st, uint32_t code_xor = 0u);
 
 // ---- gemm_tc.cu : tcgen05 int8 GEMM with fused epilogues
 enum EpiMode : int {
@@ -56,6 +56,7 @@ struct GemmArgs {
   // EPI_QUANT
   const unsigned* amax_in; int bits; uint64_t seed; uint32_t step; uint32_t tag; int64_t g_row0;
   int8_t* q_out; int64_t ldq; float* scale_out; int32_t* status;
+  uint32_t code_xor;                        // 0x80808080: store excess-128 codes (q + 128)
   // EPI_STORE / EPI_I32 / EPI_ATOMIC64
   void* C; int64_t ldc;
 };
@@ -98,11 +99,15 @@ struct GatFwdArgs {
   int32_t* work;                              // [8] work-queue counters (zeroed before the launch)
   float* alpha;                               // [e_in][2H]: α with the sign of e_pre (LeakyReLU branch) | ∂E_pre
   int part;                                   // work items: 0 all, 1 hub segments only, 2 light sub-tiles only
+  int codes_biased;                           // q_H′ holds excess-128 codes (gat_codes_biased)
 };
 // aux (nullable): a second stream that runs the hub-row chain beside the light sub-tiles
 // (fork/join with the two events); null -> everything in order on st.
 struct SideStream { cudaStream_t s; cudaEvent_t fork, join; };
 cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st, const SideStream* aux = nullptr);
+// true when the layer kernels for this shape take q_H′ and q_G as excess-128 codes (q + 128, stored
+// as int8 bit patterns q ^ 0x80): the v4 gather engine then converts without the sign flip
+bool gat_codes_biased(int heads, int hd);
 
 struct GatBwdArgs {
   GraphDev g; GatDims d; float slope; int bits;
@@ -125,6 +130,7 @@ struct GatBwdArgs {
   const float* alpha;                        // [e_in][2H]: signed α from the forward | ∂E_pre (written here)
   float* alpha_dE;                           // same buffer, written by the destination passes
   int part;                                  // as GatFwdArgs::part
+  int codes_biased;                          // q_H′ and q_G hold excess-128 codes (gat_codes_biased)
 };
 cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st, const SideStream* aux = nullptr);
 cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st, const SideStream* aux = nullptr);

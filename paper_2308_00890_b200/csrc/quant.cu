@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) k_quantize(const float* __restrict__ x, i
                                                   const unsigned* __restrict__ amax_slot, int bits, const PhiloxKey key,
                                                   uint32_t step, uint32_t tag, int8_t* __restrict__ q, int64_t ld,
                                                   int8_t* __restrict__ qt, int64_t ldt, float* __restrict__ scale_out,
-                                                  int32_t* __restrict__ status) {
+                                                  int32_t* __restrict__ status, uint32_t code_xor) {
   const Scale sc = scale_from_amax(amax_load(amax_slot), bits);
   const int qmax = (1 << (bits - 1)) - 1;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -91,7 +91,9 @@ __global__ void __launch_bounds__(256) k_quantize(const float* __restrict__ x, i
       }
       const SR8 rnd = sr_draw8((uint64_t)blk, tag, step, key);
       const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      *reinterpret_cast<uint2*>(q + ((blk << 3) - g0)) = sr_quant8(v, sc.r, rnd, qmax);
+      uint2 pk = sr_quant8(v, sc.r, rnd, qmax);
+      pk.x ^= code_xor; pk.y ^= code_xor;
+      *reinterpret_cast<uint2*>(q + ((blk << 3) - g0)) = pk;
       a = na; b = nbv;
     }
     return;
@@ -109,7 +111,9 @@ __global__ void __launch_bounds__(256) k_quantize(const float* __restrict__ x, i
       const float4* src = reinterpret_cast<const float4*>(x + e);
       const float4 a = __ldg(src), b = __ldg(src + 1);
       const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      *reinterpret_cast<uint2*>(q + i * ld + j) = sr_quant8(v, sc.r, rnd, qmax);
+      uint2 pk = sr_quant8(v, sc.r, rnd, qmax);
+      pk.x ^= code_xor; pk.y ^= code_xor;
+      *reinterpret_cast<uint2*>(q + i * ld + j) = pk;
     } else {
 #pragma unroll 1
       for (int k = 0; k < 8; ++k) {
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(256) k_quantize(const float* __restrict__ x, i
         float v = x[e];
         if (rowscale) v = __fmul_rn(v, rowscale[i]);
         const int qq = sr_quant(v, sc.r, sr_half(rnd, k), qmax);
-        if (q) q[i * ld + j] = (int8_t)qq;
+        if (q) q[i * ld + j] = (int8_t)(qq ^ (int)(code_xor & 0xFFu));
         if (qt) qt[j * ldt + i] = (int8_t)qq;
       }
     }
@@ -146,7 +150,7 @@ cudaError_t launch_absmax(const float* x, int64_t rows, int64_t cols, const floa
 cudaError_t launch_quantize(const float* x, int64_t rows, int64_t cols, const float* rowscale, int64_t g0,
                             const unsigned* amax_slot, int bits, uint64_t seed, uint32_t step, uint32_t tag,
                             int8_t* q, int64_t ld, int8_t* qt, int64_t ldt, float* scale_out, int32_t* status,
-                            cudaStream_t st) {
+                            cudaStream_t st, uint32_t code_xor) {
   const int64_t count = rows * cols;
   if (count == 0) {
     if (scale_out) {
@@ -167,7 +171,7 @@ cudaError_t launch_quantize(const float* x, int64_t rows, int64_t cols, const fl
   const int64_t groups = (count + 15) / 8;
   ProfScope ps("quantize", st);
   k_quantize<<<grid_for(groups, 256, 16), 256, 0, st>>>(x, rows, cols, rowscale, g0, amax_slot, bits, philox_key(seed), step, tag,
-                                                       q, ld, qt, ldt, scale_out, status);
+                                                       q, ld, qt, ldt, scale_out, status, code_xor);
   return cudaGetLastError();
 }
 

@@ -57,7 +57,8 @@ class GatParams(C.Structure):
 class GatCtxView(C.Structure):
     _fields_ = [(f, _P) for f in ("qH", "qW", "qWt", "qHp", "qS", "qD", "qG", "qdHp")] + \
                [(f, C.c_int64) for f in ("ldF", "ldHD", "ldFt")] + \
-               [(f, _P) for f in ("S", "D", "m", "den", "P", "dD", "dHp", "dalpha", "alpha_pack", "scalars")]
+               [(f, _P) for f in ("S", "D", "m", "den", "P", "dD", "dHp", "dalpha", "alpha_pack", "scalars")] + \
+               [("codes_biased", C.c_int32)]
 
 
 class GcnParams(C.Structure):
@@ -430,6 +431,11 @@ class GATLayer:
             den=sl(v.den, N * H * 4, f4, (N, H)), P=sl(v.P, N * H * 4, f4, (N, H)),
             dD=sl(v.dD, N * H * 4, f4, (N, H)), dHp=sl(v.dHp, n * HD * 4, f4, (n, HD)),
             dalpha=sl(v.dalpha, E * H * 4, f4, (E, H)), scalars=sl(v.scalars, 64 * 4, f4, (64,)))
+        if v.codes_biased:   # excess-128 storage of q_H′ / q_G -> plain codes
+            flip = torch.tensor(-128, dtype=i8, device=self.ctx.device)
+            out["qHp"] = torch.bitwise_xor(out["qHp"], flip)
+            out["qG"] = torch.bitwise_xor(out["qG"], flip)
+        out["codes_biased"] = bool(v.codes_biased)
         pack = sl(v.alpha_pack, E * 2 * H * 4, f4, (E, 2 * H))
         out["alpha"] = pack[:, :H].abs()
         out["e_pre_pos"] = ~torch.signbit(pack[:, :H])
