@@ -1422,12 +1422,12 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg4(const GatFwdArgs a) {
     float xs = 0.0f;
     auto flush = [&](int j) {
       float4* dst = reinterpret_cast<float4*>(a.Hout + (r0 + j) * HD + lane * VPL);
+      const float2 sH2 = make_float2(scH.s, scH.s);
 #pragma unroll
       for (int k = 0; k < VPL / 4; ++k) {
-        const float4 o = make_float4(__fmul_rn(acc[2 * k].x, scH.s), __fmul_rn(acc[2 * k].y, scH.s),
-                                     __fmul_rn(acc[2 * k + 1].x, scH.s), __fmul_rn(acc[2 * k + 1].y, scH.s));
-        amax_loc = fmaxf(amax_loc, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
-        __stcs(dst + k, o);
+        const float2 o01 = __fmul2_rn(acc[2 * k], sH2), o23 = __fmul2_rn(acc[2 * k + 1], sH2);
+        amax_loc = fmaxf(amax_loc, fmaxf(fmaxf(fabsf(o01.x), fabsf(o01.y)), fmaxf(fabsf(o23.x), fabsf(o23.y))));
+        __stcs(dst + k, make_float4(o01.x, o01.y, o23.x, o23.y));
         acc[2 * k] = make_float2(0.0f, 0.0f);
         acc[2 * k + 1] = make_float2(0.0f, 0.0f);
       }
@@ -2429,7 +2429,7 @@ __device__ __forceinline__ void src_finalize4(const GatBwdArgs& a, int64_t ul, i
     const float sv[4] = {s4.x, s4.y, s4.z, s4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
     float o[4];
 #pragma unroll
-    for (int z = 0; z < 4; ++z) {
+    for (int z = 0; z < 4; ++z) {   // scalar: ptxas contracts packed FMUL2 + FADD2 into FFMA2
       const float t2 = __fadd_rn(__fmul_rn(v[z], sG), __fmul_rn(dS, sv[z]));
       o[z] = __fadd_rn(t2, __fmul_rn(dD, dv[z]));
       amax_loc = fmaxf(amax_loc, fabsf(o[z]));
