@@ -650,14 +650,18 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   gb.q_out = qHp + r0 * L.ldHD; gb.ldq = L.ldHD; gb.scale_out = scf + SL_S_HP; gb.status = dev_status;
   const bool biased = gat_codes_biased(p->heads, (int)L.HD);   // q_H′ / q_G as excess-128 codes
   gb.code_xor = biased ? 0x80808080u : 0u;
-  TRY(launch_status(launch_gemm(gb, st)));
+  // Q(S), Q(D) (tiny, latency-bound) on the side stream beside phase B
+  TRY_CUDA(stream_after(aux->s, st, aux->ev[3]));
   TRY(launch_status(launch_quantize(S, L.n, L.H, nullptr, r0 * L.H, sc + SL_AMAX_S, p->bits, rng.seed, rng.step,
                                     tag_of(layer_id, R_S), qS + r0 * L.H, L.H, nullptr, 0, scf + SL_S_S, dev_status,
-                                    st)));
+                                    aux->s)));
   TRY(launch_status(launch_quantize(D, L.n, L.H, nullptr, r0 * L.H, sc + SL_AMAX_D, p->bits, rng.seed, rng.step,
                                     tag_of(layer_id, R_D), qD + r0 * L.H, L.H, nullptr, 0, scf + SL_S_D, dev_status,
-                                    st)));
+                                    aux->s)));
+  TRY_CUDA(cudaEventRecord(aux->ev[6], aux->s));
+  TRY(launch_status(launch_gemm(gb, st)));
   TRY(comm_gather_rows(comm, qHp, (size_t)L.ldHD, st));
+  TRY_CUDA(cudaStreamWaitEvent(st, aux->ev[6], 0));   // Q(S), Q(D) done
   TRY(comm_gather_rows(comm, qS, (size_t)L.H, st));
   TRY(comm_gather_rows(comm, qD, (size_t)L.H, st));
   // F5 + F6: segment plan of the in-CSR, then softmax statistics, aggregation and heavy-row combine
