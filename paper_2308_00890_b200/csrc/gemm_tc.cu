@@ -26,14 +26,14 @@ constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BKB;  // 16 KB
 constexpr int B_BYTES_MAX = 256 * BKB;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES_MAX;
-constexpr int EPI_WARPS = 8;       // two per TMEM sub-partition, each owning half of the N tile
+constexpr int EPI_WARPS = 8;       // two per TMEM sub-partition, each owning a column group of the N tile
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4096 + 1024;
 
 struct KParams {
   int64_t M, N, K;
   int BN, n_tiles_m, n_tiles_n, splits, kb_per_split, total_kb, nblk_b;
-  int a_mn, b_mn, split_halves;
+  int a_mn, b_mn, col_groups;   // epilogue column groups per sub-partition (1..3; whole heads with dots)
   int64_t total_tiles;
   uint32_t idesc, stage_tx, tmem_cols;
   const float* sA; const float* sB; const float* rowscale;
@@ -144,13 +144,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------- epilogue (warps 2..9)
-    const int ew = warp - 2;                  // 0..7
+    const int ew = warp - 2;                  // 0 .. EPI_WARPS-1
     const int sub = warp & 3;                 // TMEM sub-partition this warp may access
-    const int half = ew >> 2;                 // which half of the N tile
+    const int grp = ew >> 2;                  // column group of the N tile (idle if >= col_groups)
     const int rin = sub * 32 + lane;          // row within the tile
     const int nch = p.BN / 32;
-    const int c_lo = p.split_halves ? half * (nch / 2) : 0;
-    const int c_hi = p.split_halves ? (half + 1) * (nch / 2) : (half == 0 ? nch : 0);
+    const int c_lo = grp < p.col_groups ? (grp * nch) / p.col_groups : 0;
+    const int c_hi = grp < p.col_groups ? ((grp + 1) * nch) / p.col_groups : 0;
     const float sAB = (p.sA && p.sB) ? __fmul_rn(*p.sA, *p.sB) : 1.0f;
     constexpr bool has_rs = RS;   // per-row multiplier (GCN), a template parameter: no select per element
     Scale qs = {1.0f, 1.0f, false};
@@ -380,11 +380,16 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
   p.splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
   p.nblk_b = (BN + 127) / 128;
   p.a_mn = a.a_mn; p.b_mn = a.b_mn;
-  {
+  {   // as many column groups as the epilogue warps allow; with head dots every group holds whole heads
     const int nch = BN / 32;
-    bool halves = (nch % 2) == 0;
-    if (halves && a.mode == EPI_AMAX && a.a_src && ((BN / 2) % a.head_dim) != 0) halves = false;
-    p.split_halves = halves ? 1 : 0;
+    const bool dots = a.mode == EPI_AMAX && a.a_src;
+    int g = EPI_WARPS / 4;
+    for (; g > 1; --g) {
+      if (g > nch) continue;
+      if (dots && (nch % g || ((BN / g) % a.head_dim) != 0)) continue;
+      break;
+    }
+    p.col_groups = g;
   }
   p.total_tiles = (int64_t)p.n_tiles_m * p.n_tiles_n * p.splits;
   p.idesc = make_idesc_i8(BM, BN, a.a_mn, a.b_mn);
