@@ -181,6 +181,24 @@ tango_status tango_edge_sum(const tango_graph* G, int32_t dir, int32_t heads, co
                             cudaStream_t stream);
 
 /* ------------------------------------------------------------------------- */
+/* Bit-width derivation (§3.2 Eq.4, Fig.5).  */
+/* ------------------------------------------------------------------------- */
+/* Error_X of codes q (with their scale) against x: the mean over the rows x cols
+ * tensor of |X − X̂| / (|X| + |X̂| + ε), X̂ = i2f(q)·s, ε = 0.0005; the
+ * denominator takes absolute values (reading A24: the printed X + X̂ + ε can be
+ * <= 0 for small negative values, contradicting the stated [0, 1] range).  Terms
+ * in fp32 (rn), the sum in fp64 (order not fixed).  err_out: device double. */
+tango_status tango_quant_error(const float* x, int64_t rows, int64_t cols, const tango_qtensor* q, double* err_out,
+                               cudaStream_t stream);
+/* select_bits: for B in [bmin, bmax] (2 <= bmin <= bmax <= 8) the Error_X of x
+ * quantized to B bits with NEAREST rounding (reading R31) -> errs_out[B − bmin]
+ * (device doubles); bits_out (device int32) = the smallest B with Error_X <=
+ * threshold ("we let Error_X = 0.3"), or −bmax if no width qualifies.
+ * bits_out doubles as scratch for amax(x) during the call. */
+tango_status tango_select_bits(const float* x, int64_t count, float threshold, int32_t bmin, int32_t bmax,
+                               double* errs_out, int32_t* bits_out, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------- */
 /* Fused GAT layer (§2.1 Fig.1 with §3.2-3.3 quantization rules).  */
 /* Forward: F1 Q(H), F2 Q(W), F3 ①② tcgen05 GEMM + head dots, F4 Q(H′),Q(S),Q(D),
  * F5/F6 ③④⑤ one destination-row kernel.  Backward: B1 Q(∂H_out), B2-B4 one  */

@@ -83,6 +83,12 @@ def lib():
                                    _P, _P, _P]
         L.orc_exp_p.argtypes = [C.c_float]
         L.orc_exp_p.restype = C.c_float
+        L.orc_error_term.argtypes = [C.c_float, C.c_float]
+        L.orc_error_term.restype = C.c_float
+        L.orc_error_x.argtypes = [_P, _P, C.c_float, C.c_int64]
+        L.orc_error_x.restype = C.c_double
+        L.orc_select_bits.argtypes = [_P, C.c_int64, C.c_float, C.c_int, C.c_int, _P, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int)]
         L.orc_sddmm_add.argtypes = [C.POINTER(Graph), C.c_int, QRef, QRef, C.c_float, _P, _P]
         L.orc_edge_softmax.argtypes = [C.POINTER(Graph), C.c_int, _P, _P, _P, _P]
         L.orc_spmm_alpha.argtypes = [C.POINTER(Graph), C.c_int, C.c_int, C.c_int, _P, QRef, _P]
@@ -150,6 +156,28 @@ def quantize(x, bits=8, seed=0, step=0, tag=0, g0=0, amax=None):
     st = lib().orc_quantize(_p(x), x.size, bits, seed, step, tag, g0, _p(amin), _p(q), _p(s), _p(am))
     _check(st)
     return q, np.float32(s[0]), np.float32(am[0])
+
+
+def error_term(x, xh) -> np.float32:
+    return np.float32(lib().orc_error_term(float(np.float32(x)), float(np.float32(xh))))
+
+
+def error_x(x, q, s) -> float:
+    """Error_X (Eq.4, reading A24 denominator) of codes q with scale s against x."""
+    x = _c(x, np.float32)
+    q = _c(q, np.int8)
+    return float(lib().orc_error_x(_p(x), _p(q), float(s), x.size))
+
+
+def select_bits(x, threshold=0.3, bmin=2, bmax=8):
+    """(bits, errs[bmin..bmax], none) with nearest rounding (reading R31)."""
+    x = _c(x, np.float32)
+    errs = np.zeros(bmax - bmin + 1, np.float64)
+    bits = C.c_int(0)
+    none = C.c_int(0)
+    _check(lib().orc_select_bits(_p(x), x.size, float(threshold), bmin, bmax, _p(errs), C.byref(bits),
+                                 C.byref(none)))
+    return bits.value, errs, bool(none.value)
 
 
 def exp_p(x: float) -> np.float32:

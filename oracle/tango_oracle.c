@@ -127,6 +127,57 @@ int orc_quantize(const float* x, int64_t count, int bits, uint64_t seed, uint32_
 }
 
 /* ------------------------------------------------------------------------- */
+/* Error_X (§3.2 Eq.4) with the reading A24 denominator (SURVEY.md  */
+/* §8(c.7)): Error_X = (1/N) Σ |X_i − X̂_i| / (|X_i| + |X̂_i| + ε), ε = 0.0005  */
+/* ("Tango chooses ε = 0.0005"), X̂_i = i2f(q_i)·s.  Each term in fp32   */
+/* (rn), the mean in fp64.  N = 0 -> 0.                                      */
+/* ------------------------------------------------------------------------- */
+float orc_error_term(float x, float xh) {
+  float num = fabsf(x - xh);
+  float den = (fabsf(x) + fabsf(xh)) + 0.0005f;
+  return num / den;
+}
+double orc_error_x(const float* x, const int8_t* q, float s, int64_t count) {
+  if (count <= 0) return 0.0;
+  double acc = 0.0;
+  for (int64_t i = 0; i < count; ++i) acc += (double)orc_error_term(x[i], (float)q[i] * s);
+  return acc / (double)count;
+}
+
+/* select_bits (§3.2: "we compute Error_X of the output tensor of the first GNN layer",
+ * "when Error_X < 0.3, Tango can maintain the accuracy ... we let Error_X = 0.3"): for every B in
+ * [bmin, bmax] quantize X with NEAREST rounding (reading R31: the paper does not say which rounding
+ * feeds Eq.4; nearest keeps the one-shot decision free of rounding noise), q = clamp(rintf(X*r_B)),
+ * errs[B - bmin] = Error_X; returns the smallest B with Error_X <= threshold, or bmax if none
+ * (*none = 1), in *bits.  Scales as orc_scale (amax over the whole tensor).  Returns a status. */
+int orc_select_bits(const float* x, int64_t count, float threshold, int bmin, int bmax, double* errs, int* bits,
+                    int* none) {
+  int bad;
+  float amax = orc_absmax(x, count, &bad);
+  if (bad) return ORC_ERR_NONFINITE;
+  if (bmin < 2 || bmax > 8 || bmin > bmax) return ORC_ERR_BITS;
+  int chosen = -1;
+  for (int B = bmin; B <= bmax; ++B) {
+    float s, r;
+    orc_scale(amax, B, &s, &r);
+    const float qmax = (float)((1 << (B - 1)) - 1);
+    double acc = 0.0;
+    for (int64_t i = 0; i < count; ++i) {
+      float q = rintf(x[i] * r);
+      if (q > qmax) q = qmax;
+      if (q < -qmax) q = -qmax;
+      acc += (double)orc_error_term(x[i], q * s);
+    }
+    errs[B - bmin] = count > 0 ? acc / (double)count : 0.0;
+    if (chosen < 0 && errs[B - bmin] <= (double)threshold) chosen = B;
+  }
+  *none = chosen < 0;
+  *bits = chosen < 0 ? bmax : chosen;
+  return ORC_OK;
+}
+
+
+/* ------------------------------------------------------------------------- */
 /* Pinned exponential exp_p (reading R13): argument always <= 0.              */
 /* t = x*log2(e); t < -125 -> 0; n = rint(t); f = t-n;                       */
 /* p = Horner(c6..c0) with fmaf; result = ldexpf(p, n); c_k = (float)ln2^k/k! */

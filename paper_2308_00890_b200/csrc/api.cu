@@ -1001,6 +1001,26 @@ tango_status tango_gcn_layer_bwd(const tango_graph* G, const tango_gcn_params* p
   return TANGO_OK;
 }
 
+// ================================================================== bit-width derivation (NEXT-2)
+tango_status tango_quant_error(const float* x, int64_t rows, int64_t cols, const tango_qtensor* q, double* err_out,
+                               cudaStream_t st) {
+  if (!err_out || rows < 0 || cols < 0) return TANGO_ERR_INVALID_ARG;
+  if (rows * cols > 0) {
+    if (!x) return TANGO_ERR_INVALID_ARG;
+    TRY(check_q(q));
+    if (q->rows != rows || q->cols != cols) return TANGO_ERR_SHAPE;
+  }
+  return launch_status(launch_error_x(x, rows, cols, rows * cols > 0 ? q->q : nullptr, rows * cols > 0 ? q->ld : 0,
+                                      rows * cols > 0 ? q->scale : nullptr, err_out, st));
+}
+
+tango_status tango_select_bits(const float* x, int64_t count, float threshold, int32_t bmin, int32_t bmax,
+                               double* errs_out, int32_t* bits_out, cudaStream_t st) {
+  if (!errs_out || !bits_out || count < 0 || (count > 0 && !x)) return TANGO_ERR_INVALID_ARG;
+  if (bmin < 2 || bmax > 8 || bmin > bmax) return TANGO_ERR_BITS;
+  return launch_status(launch_select_bits(x, count, threshold, bmin, bmax, errs_out, bits_out, st));
+}
+
 // ================================================================== communicator
 int32_t tango_comm_unique_id_bytes(void) { return (int32_t)sizeof(ncclUniqueId); }
 

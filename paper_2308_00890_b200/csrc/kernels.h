@@ -28,6 +28,11 @@ cudaError_t launch_quantize(const float* x, int64_t rows, int64_t cols, const fl
                             int8_t* q, int64_t ld, int8_t* qt, int64_t ldt, float* scale_out, int32_t* status,
                             cudaStream_t st, uint32_t code_xor = 0u);
 
+cudaError_t launch_error_x(const float* x, int64_t rows, int64_t cols, const int8_t* q, int64_t ld, const float* s,
+                           double* err, cudaStream_t st);
+cudaError_t launch_select_bits(const float* x, int64_t count, float threshold, int bmin, int bmax, double* errs,
+                               int32_t* bits, cudaStream_t st);
+
 // ---- gemm_tc.cu : tcgen05 int8 GEMM with fused epilogues
 enum EpiMode : int {
   EPI_AMAX = 0,     // v = i2f(acc)*sAB[*rowscale]; amax(|v|); optional per-head dots S = v·a_src, D = v·a_dst

@@ -176,3 +176,112 @@ cudaError_t launch_quantize(const float* x, int64_t rows, int64_t cols, const fl
 }
 
 }  // namespace tango
+
+// ================================================================== Error_X and bit selection (NEXT-2)
+namespace tango {
+namespace {
+// Eq.4 term with the reading-A24 denominator: |x − x̂| / (|x| + |x̂| + ε), ε = 0.0005, fp32 rn ops
+__device__ __forceinline__ float error_term(float x, float xh) {
+  return __fdiv_rn(fabsf(__fsub_rn(x, xh)), __fadd_rn(__fadd_rn(fabsf(x), fabsf(xh)), 0.0005f));
+}
+__device__ __forceinline__ double block_sum_d(double v) {
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  return t;   // valid in thread 0
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_error_x(const float* __restrict__ x, int64_t rows, int64_t cols,
+                                                 const int8_t* __restrict__ q, int64_t ld, const float* __restrict__ s,
+                                                 double* __restrict__ sum) {
+  const float sc = *s;
+  const int64_t count = rows * cols;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    acc += (double)error_term(x[i], __fmul_rn((float)q[r * ld + c], sc));
+  }
+  acc = block_sum_d(acc);
+  if (threadIdx.x == 0) atomicAdd(sum, acc);
+}
+// nb bit widths at once (nearest rounding, reading R31): one pass over x
+template <int NB>
+__global__ void __launch_bounds__(256) k_select_bits_sweep(const float* __restrict__ x, int64_t count, int bmin,
+                                                           const int32_t* __restrict__ amax_bits,
+                                                           double* __restrict__ sums) {
+  const float amax = __int_as_float(*amax_bits);
+  float s[NB], r[NB], qm[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const Scale sc = scale_from_amax(amax, bmin + b);
+    s[b] = sc.s; r[b] = sc.r; qm[b] = (float)((1 << (bmin + b - 1)) - 1);
+  }
+  double acc[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) acc[b] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const float q = fminf(fmaxf(rintf(__fmul_rn(v, r[b])), -qm[b]), qm[b]);
+      acc[b] += (double)error_term(v, __fmul_rn(q, s[b]));
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const double t = block_sum_d(acc[b]);
+    if (threadIdx.x == 0) atomicAdd(sums + b, t);
+  }
+}
+__global__ void k_select_bits_final(double* errs, int nb, int bmin, int64_t count, float threshold, int32_t* bits) {
+  int chosen = -1;
+  for (int b = 0; b < nb; ++b) {
+    errs[b] = count > 0 ? errs[b] / (double)count : 0.0;
+    if (chosen < 0 && errs[b] <= (double)threshold) chosen = bmin + b;
+  }
+  *bits = chosen < 0 ? -(bmin + nb - 1) : chosen;   // negative: no width met the threshold (|value| = bmax)
+}
+__global__ void k_div_count(double* v, int64_t count) { *v = count > 0 ? *v / (double)count : 0.0; }
+
+cudaError_t launch_error_x(const float* x, int64_t rows, int64_t cols, const int8_t* q, int64_t ld, const float* s,
+                           double* err, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(err, 0, sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  if (rows * cols > 0) {
+    ProfScope ps("error_x", st);
+    k_error_x<<<grid_for(rows * cols, 256), 256, 0, st>>>(x, rows, cols, q, ld, s, err);
+  }
+  k_div_count<<<1, 1, 0, st>>>(err, rows * cols);
+  return cudaGetLastError();
+}
+cudaError_t launch_select_bits(const float* x, int64_t count, float threshold, int bmin, int bmax, double* errs,
+                               int32_t* bits, cudaStream_t st) {
+  const int nb = bmax - bmin + 1;
+  cudaError_t e = cudaMemsetAsync(errs, 0, sizeof(double) * nb, st);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(bits, 0, sizeof(int32_t), st)) != cudaSuccess) return e;
+  if (count > 0) {
+    // amax into *bits (float bit pattern, non-negative: unsigned max == float max), then the sweep
+    if ((e = launch_absmax(x, count, 1, nullptr, reinterpret_cast<unsigned*>(bits), st)) != cudaSuccess) return e;
+    ProfScope ps("select_bits", st);
+    switch (nb) {
+#define NB_CASE(K) case K: k_select_bits_sweep<K><<<grid_for(count, 256), 256, 0, st>>>(x, count, bmin, bits, errs); break;
+      NB_CASE(1) NB_CASE(2) NB_CASE(3) NB_CASE(4) NB_CASE(5) NB_CASE(6) NB_CASE(7)
+#undef NB_CASE
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  k_select_bits_final<<<1, 1, 0, st>>>(errs, nb, bmin, count, threshold, bits);
+  return cudaGetLastError();
+}
+}  // namespace tango

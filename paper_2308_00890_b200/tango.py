@@ -78,7 +78,7 @@ EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tan
            "tango_gcn_ctx_bytes", "tango_gcn_layer_fwd", "tango_gcn_layer_bwd", "tango_gcn_ctx_get_view",
            "tango_comm_unique_id_bytes", "tango_comm_get_unique_id", "tango_comm_init", "tango_comm_destroy",
            "tango_comm_set_partition", "tango_local_group_create", "tango_local_group_destroy",
-           "tango_comm_init_local", "tango_profile_enable", "tango_launch_count", "tango_profile_collect",
+           "tango_comm_init_local", "tango_quant_error", "tango_select_bits", "tango_profile_enable", "tango_launch_count", "tango_profile_collect",
            "tango_profile_num_entries", "tango_profile_entry", "tango_profile_reset"]
 
 
@@ -119,6 +119,8 @@ def load(path: str = LIB_PATH):
     L.tango_comm_init.argtypes = [C.POINTER(_P), _P, i32, i32]
     L.tango_comm_destroy.argtypes = [_P]
     L.tango_comm_set_partition.argtypes = [_P, _P]
+    L.tango_quant_error.argtypes = [_P, i64, i64, PQ, _P, _P]
+    L.tango_select_bits.argtypes = [_P, i64, f32, i32, i32, _P, _P, _P]
     L.tango_local_group_create.argtypes = [C.POINTER(_P), i32]
     L.tango_local_group_destroy.argtypes = [_P]
     L.tango_comm_init_local.argtypes = [C.POINTER(_P), _P, i32]
@@ -343,6 +345,28 @@ class Comm:
         if self.handle:
             load().tango_comm_destroy(self.handle)
             self.handle = C.c_void_p()
+
+
+def quant_error(x, q, s, bits=8):
+    """tango_quant_error: Error_X (Eq.4) of codes q [rows, ld] with scale s (1,) against x [rows, cols]."""
+    L = load()
+    x = x.contiguous()
+    rows, cols = x.shape
+    out = torch.empty(1, dtype=torch.float64, device=x.device)
+    qt = QTensor(_ptr(q), _ptr(s), rows, cols, q.shape[1], bits)
+    _check(L.tango_quant_error(_ptr(x), rows, cols, C.byref(qt), _ptr(out), _stream()), "tango_quant_error")
+    return out
+
+
+def select_bits(x, threshold=0.3, bmin=2, bmax=8):
+    """tango_select_bits: (bits int32 (1,), errs float64 (bmax-bmin+1,)); bits < 0: none qualified."""
+    L = load()
+    x = x.contiguous()
+    errs = torch.empty(bmax - bmin + 1, dtype=torch.float64, device=x.device)
+    bits = torch.empty(1, dtype=torch.int32, device=x.device)
+    _check(L.tango_select_bits(_ptr(x), x.numel(), threshold, bmin, bmax, _ptr(errs), _ptr(bits), _stream()),
+           "tango_select_bits")
+    return bits, errs
 
 
 class LocalGroup:
