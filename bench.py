@@ -100,6 +100,15 @@ def kernel_model(name, g_e, n, F, H, HD, peaks, clock_mhz):
     elif name == "gat_bwd_src":      # ⑤′+③′+②′: dst index + eid + α + ∂E_pre + q_G[v] row; ∂H′ row per node
         byts = E * (8 + 8 * H + HD) + n * (8 + 4 * HD + 8 * H)
         ops = 2 * E * HD
+    elif name == "quantize":         # SR quantize: 4 B read + 1 B code written per element.  Per step:
+        # Q(W) F*HD, Q(H) n*F, Q(S) and Q(D) n*H each, Q(dH_out) and Q(dH') n*HD each = 6 launches;
+        # returned per launch (average), like the per-launch time it is divided by.
+        elems = F * HD + n * F + 2 * n * H + 2 * n * HD
+        byts = 5 * elems / 6
+        ops = 20 * elems / 6          # ~20 lane-instructions per element (Philox share + SR)
+    elif name == "absmax":           # amax of an input tensor: 4 B read per element (H and dH_out per step)
+        byts = 4 * (n * F + n * HD) / 2
+        ops = 2 * (n * F + n * HD) / 2
     else:
         return None
     alu_peak = 148 * 128 * clock_mhz * 1e6   # FP32 lanes x clock (lane-ops/s)
@@ -290,7 +299,16 @@ def main():
     eager_ms = sum(v[0] for v in prof.values()) / args.steps
 
     # ---------------- dominant kernel roofline (live CUDA-event time over the timed region)
-    dom, (dom_ms, dom_cnt) = max(prof.items(), key=lambda kv: kv[1][0])
+    # dominant = largest device time per step; a kernel without a bytes/ops model falls through to
+    # the next one (and is named in "skipped")
+    ranked = sorted(prof.items(), key=lambda kv: -kv[1][0])
+    dom, (dom_ms, dom_cnt) = ranked[0]
+    skipped = []
+    for kname, kv in ranked:
+        if kernel_model(kname, dg.e_in, n, F, H, HD, peaks, 1965.0) is not None:
+            dom, (dom_ms, dom_cnt) = kname, kv
+            break
+        skipped.append(kname)
     clock = clk["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
     model = kernel_model(dom, dg.e_in, n, F, H, HD, peaks, clock)
     per_launch_s = dom_ms / dom_cnt / 1e3
@@ -317,9 +335,13 @@ def main():
         roof["algorithmic_bytes"] = byts
         roof["kernel"] = dom
         roof["kernel_ms"] = per_launch_s * 1e3
-        roof["share_of_step"] = dom_ms / dom_cnt / ms
+        roof["launches_per_step"] = dom_cnt / args.steps
+        roof["share_of_step"] = dom_ms / args.steps / ms
+        if skipped:
+            roof["unmodelled_larger_kernels"] = skipped
         roof["peak_kind"] = peak_kind
     breakdown = {k: round(v[0] / v[1], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    per_step = {k: round(v[0] / args.steps, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     # per-kernel rooflines of SURVEY.md §8(d): sparse kernels vs HBM (algorithmic bytes) and the
     # ALU, GEMMs as int8 TOPS vs the int8 tensor peak (measured bf16 x the nominal int8:bf16 ratio 2)
     int8_peak = 2.0 * peaks["bf16_tflops"]
@@ -420,7 +442,7 @@ def main():
                                 "dW, da_src, da_dst, amax(H_out); input copies of step i+1 overlap step i "
                                 "(copy stream, double-buffered inputs)",
                         "d2h_bytes_per_step": d2h},
-                "gpu_launches": int(launches_t.item()), "clocks": clk, "kernel_ms": breakdown,
+                "gpu_launches": int(launches_t.item()), "clocks": clk, "kernel_ms": breakdown, "kernel_ms_per_step": per_step,
                 "timing": "value: CUDA-graph replay of fwd+bwd per step (events per step, L2 flushed between "
                           "steps); kernel_ms/roofline: eager pass with events around every launch "
                           f"(sum of kernel times {eager_ms:.3f} ms/step)"}
