@@ -71,6 +71,23 @@ class GcnBwdOut(C.Structure):
     _fields_ = [(f, _P) for f in _GCN_BWD_FIELDS]
 
 
+class OutCfg(C.Structure):
+    _fields_ = [("F", C.c_int32), ("H", C.c_int32), ("C", C.c_int32), ("slope", C.c_float)]
+
+
+_OUT_FWD_FIELDS = ["Hp", "S", "Dd", "e_pre", "alpha", "m", "den", "agg", "logits"]
+_OUT_BWD_FIELDS = ["db", "G", "dalpha", "P", "dE", "dE_pre", "dD", "dS", "dHp_agg", "dHp", "da_src", "da_dst",
+                   "da_src_abs", "da_dst_abs", "dH", "dW"]
+
+
+class OutFwdOut(C.Structure):
+    _fields_ = [(f, _P) for f in _OUT_FWD_FIELDS]
+
+
+class OutBwdOut(C.Structure):
+    _fields_ = [(f, _P) for f in _OUT_BWD_FIELDS]
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -104,6 +121,16 @@ def lib():
         L.orc_gcn_fwd.argtypes = [C.POINTER(Graph), C.POINTER(Cfg), _P, _P, C.POINTER(GcnFwdOut)]
         L.orc_gcn_bwd.argtypes = [C.POINTER(Graph), C.POINTER(Cfg), _P, _P, C.POINTER(GcnFwdOut), _P,
                                   C.POINTER(GcnBwdOut)]
+        L.orc_sgemm.argtypes = [C.c_int64, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int, _P, C.c_int64, C.c_int, _P]
+        L.orc_colsum.argtypes = [_P, C.c_int64, C.c_int64, _P]
+        L.orc_bias_relu_fwd.argtypes = [_P, _P, C.c_int64, C.c_int64, _P, _P]
+        L.orc_bias_relu_bwd.argtypes = [_P, _P, C.c_int64, C.c_int64, _P, _P, _P]
+        L.orc_gat_out_fwd.argtypes = [C.POINTER(Graph), C.POINTER(OutCfg), _P, _P, _P, _P, _P,
+                                      C.POINTER(OutFwdOut)]
+        L.orc_gat_out_bwd.argtypes = [C.POINTER(Graph), C.POINTER(OutCfg), _P, _P, _P, _P, C.POINTER(OutFwdOut),
+                                      _P, C.POINTER(OutBwdOut)]
+        L.orc_cross_entropy.argtypes = [_P, _P, C.c_int64, C.c_int32, C.c_int64, _P, _P, _P]
+        L.orc_sgd.argtypes = [_P, _P, C.c_int64, C.c_float]
         L.orc_num_threads.restype = C.c_int
         L.orc_set_threads.argtypes = [C.c_int]
     return _lib
@@ -353,3 +380,149 @@ def gcn_bwd(g, fwd, X, W, dout):
     _check(lib().orc_gcn_bwd(C.byref(gs), C.byref(cfg), _p(X), _p(W), C.byref(fwd["_struct"]), _p(dout),
                              C.byref(st)))
     return o
+
+
+# ------------------------------------------------------------------ NEXT-1: the training step around the layer
+def sgemm(A, B, transA=False, transB=False):
+    """Full-precision GEMM with the pinned K-chunked FMA order (reading R33)."""
+    A, B = _c(A, np.float32), _c(B, np.float32)
+    M, K = (A.shape[1], A.shape[0]) if transA else A.shape
+    N = B.shape[0] if transB else B.shape[1]
+    out = np.zeros((M, N), np.float32)
+    lib().orc_sgemm(M, N, K, _p(A), A.shape[1], int(transA), _p(B), B.shape[1], int(transB), _p(out))
+    return out
+
+
+def colsum(x):
+    x = _c(x, np.float32)
+    out = np.zeros(x.shape[1], np.float32)
+    lib().orc_colsum(_p(x), x.shape[0], x.shape[1], _p(out))
+    return out
+
+
+def bias_relu_fwd(x, b):
+    x, b = _c(x, np.float32), _c(b, np.float32)
+    a = np.zeros_like(x)
+    am = np.zeros(1, np.float32)
+    lib().orc_bias_relu_fwd(_p(x), _p(b), x.shape[0], x.shape[1], _p(a), _p(am))
+    return a, np.float32(am[0])
+
+
+def bias_relu_bwd(a, da):
+    a, da = _c(a, np.float32), _c(da, np.float32)
+    dx = np.zeros_like(a)
+    db = np.zeros(a.shape[1], np.float32)
+    am = np.zeros(1, np.float32)
+    lib().orc_bias_relu_bwd(_p(a), _p(da), a.shape[0], a.shape[1], _p(dx), _p(db), _p(am))
+    return dx, db, np.float32(am[0])
+
+
+def gat_out_fwd(g, H, W, a_src, a_dst, bias, heads, classes, slope=0.2, chunk=256):
+    """Full-precision final GAT layer with head mean and bias (reading R35)."""
+    n, F = H.shape
+    HC = heads * classes
+    gs = graph_struct(g, chunk)
+    cfg = OutCfg(F, heads, classes, slope)
+    H, W, a_src, a_dst, bias = (_c(a, np.float32) for a in (H, W, a_src, a_dst, bias))
+    o = dict(Hp=np.zeros((n, HC), np.float32), S=np.zeros((n, heads), np.float32),
+             Dd=np.zeros((n, heads), np.float32), e_pre=np.zeros((g.e, heads), np.float32),
+             alpha=np.zeros((g.e, heads), np.float32), m=np.zeros((n, heads), np.float32),
+             den=np.zeros((n, heads), np.float32), agg=np.zeros((n, HC), np.float32),
+             logits=np.zeros((n, classes), np.float32))
+    st = OutFwdOut(*[_p(o[f]) for f in _OUT_FWD_FIELDS])
+    _check(lib().orc_gat_out_fwd(C.byref(gs), C.byref(cfg), _p(H), _p(W), _p(a_src), _p(a_dst), _p(bias),
+                                 C.byref(st)))
+    o["_struct"] = st
+    o["_cfg"] = dict(F=F, heads=heads, classes=classes, slope=slope, chunk=chunk)
+    return o
+
+
+def gat_out_bwd(g, fwd, H, W, a_src, a_dst, dlogits, want_dH=True):
+    c = fwd["_cfg"]
+    n, F = H.shape
+    heads, classes = c["heads"], c["classes"]
+    HC = heads * classes
+    E = g.e
+    gs = graph_struct(g, c["chunk"])
+    cfg = OutCfg(F, heads, classes, c["slope"])
+    H, W, a_src, a_dst, dlogits = (_c(a, np.float32) for a in (H, W, a_src, a_dst, dlogits))
+    o = dict(db=np.zeros(classes, np.float32), G=np.zeros((n, classes), np.float32),
+             dalpha=np.zeros((E, heads), np.float32), P=np.zeros((n, heads), np.float32),
+             dE=np.zeros((E, heads), np.float32), dE_pre=np.zeros((E, heads), np.float32),
+             dD=np.zeros((n, heads), np.float32), dS=np.zeros((n, heads), np.float32),
+             dHp_agg=np.zeros((n, HC), np.float32), dHp=np.zeros((n, HC), np.float32),
+             da_src=np.zeros(HC, np.float32), da_dst=np.zeros(HC, np.float32),
+             da_src_abs=np.zeros(HC, np.float32), da_dst_abs=np.zeros(HC, np.float32),
+             dH=np.zeros((n, F), np.float32) if want_dH else None, dW=np.zeros((F, HC), np.float32))
+    st = OutBwdOut(*[_p(o[f]) for f in _OUT_BWD_FIELDS])
+    _check(lib().orc_gat_out_bwd(C.byref(gs), C.byref(cfg), _p(H), _p(W), _p(a_src), _p(a_dst),
+                                 C.byref(fwd["_struct"]), _p(dlogits), C.byref(st)))
+    return o
+
+
+def cross_entropy(z, labels, n_lab=None):
+    """(loss, dz, row_loss) over rows with label >= 0 (reading R36)."""
+    z = _c(z, np.float32)
+    labels = _c(labels, np.int32)
+    n, Cc = z.shape
+    if n_lab is None:
+        n_lab = int((labels >= 0).sum())
+    dz = np.zeros_like(z)
+    rl = np.zeros(n, np.float32)
+    loss = C.c_double(0.0)
+    _check(lib().orc_cross_entropy(_p(z), _p(labels), n, Cc, n_lab, _p(rl), C.byref(loss), _p(dz)))
+    return loss.value, dz, rl
+
+
+def sgd(w, g, lr):
+    """Returns W − lr·∂W (Eq.6: the FP32 master takes the FP32 gradient)."""
+    w = _c(w, np.float32).copy()
+    g = _c(g, np.float32)
+    lib().orc_sgd(_p(w), _p(g), w.size, float(lr))
+    return w
+
+
+def gat_model_step(g, X, hidden, out, labels, lr, bits=8, seed=0x7A4E60, step=0, slope=0.2, chunk=256):
+    """One full-batch training step of the multi-layer GAT, composed from the
+    oracle's layer functions in the paper's order:
+
+      hidden layer l = 1..L-1 (quantized, heads concatenated, layer_id = l):
+          H_l = ReLU(gat_fwd(H_{l-1}) + b_l)                     (reading R34)
+      final layer (FP32; heads averaged, reading R35):
+          logits = gat_out_fwd(H_{L-1}) ; loss = CE(logits, labels) (R36)
+      backward in reverse (the first layer's ∂H is not needed), then
+      W ← W − lr·∂W for every FP32 master (Eq.6).
+
+    hidden: list of dicts {W, a_src, a_dst, b, heads, head_dim}; out: {W, a_src, a_dst, b, heads, classes}.
+    Returns dict(loss, logits, fwd/bwd records, grads, new params)."""
+    hs = [np.asarray(X, np.float32)]
+    fws, acts = [], []
+    for l, p in enumerate(hidden, start=1):
+        f = gat_fwd(g, hs[-1], p["W"], p["a_src"], p["a_dst"], p["heads"], p["head_dim"], slope=slope, bits=bits,
+                    seed=seed, step=step, layer_id=l, chunk=chunk)
+        a, am = bias_relu_fwd(f["Hout"], p["b"])
+        fws.append(f)
+        acts.append(am)
+        hs.append(a)
+    fo = gat_out_fwd(g, hs[-1], out["W"], out["a_src"], out["a_dst"], out["b"], out["heads"], out["classes"],
+                     slope=slope, chunk=chunk)
+    loss, dz, _ = cross_entropy(fo["logits"], labels)
+    bo = gat_out_bwd(g, fo, hs[-1], out["W"], out["a_src"], out["a_dst"], dz, want_dH=len(hidden) > 0)
+    grads = [None] * len(hidden)
+    dA = bo["dH"]
+    bws = [None] * len(hidden)
+    for i in range(len(hidden) - 1, -1, -1):
+        p = hidden[i]
+        dx, db, _ = bias_relu_bwd(hs[i + 1], dA)
+        b = gat_bwd(g, fws[i], hs[i], p["W"], p["a_src"], p["a_dst"], dx)
+        bws[i] = b
+        grads[i] = dict(W=b["dW"], a_src=b["da_src"], a_dst=b["da_dst"], b=db, da_src_abs=b["da_src_abs"],
+                        da_dst_abs=b["da_dst_abs"])
+        dA = b["dH"]
+    ogr = dict(W=bo["dW"], a_src=bo["da_src"], a_dst=bo["da_dst"], b=bo["db"], da_src_abs=bo["da_src_abs"],
+               da_dst_abs=bo["da_dst_abs"])
+    new_hidden = [{**p, **{k: sgd(p[k], gr[k], lr) for k in ("W", "a_src", "a_dst", "b")}}
+                  for p, gr in zip(hidden, grads)]
+    new_out = {**out, **{k: sgd(out[k], ogr[k], lr) for k in ("W", "a_src", "a_dst", "b")}}
+    return dict(loss=loss, logits=fo["logits"], hs=hs, fwd=fws, out_fwd=fo, out_bwd=bo, bwd=bws, grads=grads,
+                out_grads=ogr, hidden=new_hidden, out=new_out)

@@ -794,3 +794,233 @@ void orc_set_threads(int t) {
   (void)t;
 #endif
 }
+
+/* ========================================================================= */
+/* NEXT-1: the training step around the quantized layer.   */
+/* Full-precision final layer (§3.2 Eq.7-8), activation + bias,    */
+/* cross-entropy, FP32 master-weight update (§3.2 Eq.5-6).         */
+/* ========================================================================= */
+
+/* Full-precision contraction order (reading R33): the K-chunked canonical sum
+ * Σᶜ of R14 with chunk ORC_CK = 1024 and FMA terms:
+ *   C[m][n] = Σᶜ_k fmaf(A(m,k), B(k,n), ·)
+ * A(m,k) = transA ? A[k*lda + m] : A[m*lda + k];  B(k,n) = transB ? B[n*ldb + k] : B[k*ldb + n]. */
+#define ORC_CK 1024
+void orc_sgemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, int transA, const float* B,
+               int64_t ldb, int transB, float* C) {
+#pragma omp parallel for schedule(static)
+  for (int64_t m = 0; m < M; ++m)
+    for (int64_t n = 0; n < N; ++n) {
+      float total = 0.0f, part = 0.0f;
+      for (int64_t k = 0; k < K; ++k) {
+        csum_fold(&total, &part, k, ORC_CK);
+        float a = transA ? A[k * lda + m] : A[m * lda + k];
+        float b = transB ? B[n * ldb + k] : B[k * ldb + n];
+        part = fmaf(a, b, part);
+      }
+      C[m * N + n] = csum_finish(total, part, K, ORC_CK);
+    }
+}
+
+/* Column sum over rows with the same chunked order (reading R33): out[j] = Σᶜ_r x[r][j]. */
+void orc_colsum(const float* x, int64_t rows, int64_t cols, float* out) {
+  for (int64_t j = 0; j < cols; ++j) {
+    float total = 0.0f, part = 0.0f;
+    for (int64_t r = 0; r < rows; ++r) {
+      csum_fold(&total, &part, r, ORC_CK);
+      part = part + x[r * cols + j];
+    }
+    out[j] = csum_finish(total, part, rows, ORC_CK);
+  }
+}
+
+/* Hidden-layer bias + activation (reading R34: ReLU after the concatenated
+ * heads, bias per output column; the paper fixes neither):
+ *   y = x + b[j] ; a = y > 0 ? y : 0 ;  amax = max |a| (the next layer's Q hint) */
+void orc_bias_relu_fwd(const float* x, const float* b, int64_t rows, int64_t cols, float* a, float* amax) {
+  float m = 0.0f;
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t j = 0; j < cols; ++j) {
+      float y = x[r * cols + j] + b[j];
+      float v = (y > 0.0f) ? y : 0.0f;
+      a[r * cols + j] = v;
+      m = fmaxf(m, v);
+    }
+  if (amax) *amax = m;
+}
+
+/* Backward: dx = a > 0 ? da : 0 (a > 0 <=> y > 0), db = Σᶜ_r dx (R33),
+ * amax_dx = max |dx| (the quantized layer's ∂H_out hint). */
+void orc_bias_relu_bwd(const float* a, const float* da, int64_t rows, int64_t cols, float* dx, float* db,
+                       float* amax_dx) {
+  float m = 0.0f;
+  for (int64_t i = 0; i < rows * cols; ++i) {
+    float d = (a[i] > 0.0f) ? da[i] : 0.0f;
+    dx[i] = d;
+    m = fmaxf(m, fabsf(d));
+  }
+  orc_colsum(dx, rows, cols, db);
+  if (amax_dx) *amax_dx = m;
+}
+
+/* Full-precision final GAT layer ("use full precision to compute the
+ * layer before the Softmax"; reading R35: heads averaged), FP32
+ * end to end, the same steps ①-⑤ as orc_gat_fwd in bypass form:
+ *   H′ = sgemm(H, W) [n][H·C] ; S, D = sequential fmaf over c (R10) ;
+ *   ③ el (orc_sddmm_add, scale 1) ; ④ orc_edge_softmax ; ⑤ agg = orc_spmm_alpha ;
+ *   logits[v,c] = ((Σ_h agg[v,h,c], left to right) / heads) + bias[c]. */
+typedef struct { int32_t F, H, C; float slope; } orc_out_cfg;
+typedef struct {
+  float* Hp;                  /* [n][H*C] */
+  float* S; float* Dd;        /* [n][H] */
+  float* e_pre; float* alpha; /* [e][H] */
+  float* m; float* den;       /* [n][H] */
+  float* agg;                 /* [n][H*C] */
+  float* logits;              /* [n][C] */
+} orc_out_fwd_out;
+
+int orc_gat_out_fwd(const orc_graph* g, const orc_out_cfg* c, const float* H, const float* W,
+                    const float* a_src, const float* a_dst, const float* bias, orc_out_fwd_out* o) {
+  int64_t n = g->n, F = c->F, heads = c->H, C = c->C, HC = heads * C;
+  orc_sgemm(n, HC, F, H, F, 0, W, HC, 0, o->Hp);
+  for (int64_t v = 0; v < n; ++v)
+    for (int64_t h = 0; h < heads; ++h) {
+      float s = 0.0f, d = 0.0f;
+      for (int64_t k = 0; k < C; ++k) {
+        s = fmaf(o->Hp[v * HC + h * C + k], a_src[h * C + k], s);
+        d = fmaf(o->Hp[v * HC + h * C + k], a_dst[h * C + k], d);
+      }
+      o->S[v * heads + h] = s;
+      o->Dd[v * heads + h] = d;
+    }
+  float* el = (float*)malloc(sizeof(float) * (size_t)(g->e * heads > 0 ? g->e * heads : 1));
+  if (!el) return ORC_ERR_ALLOC;
+  orc_sddmm_add(g, (int)heads, (orc_qref){NULL, o->S, 1.0f}, (orc_qref){NULL, o->Dd, 1.0f}, c->slope, o->e_pre, el);
+  orc_edge_softmax(g, (int)heads, el, o->m, o->den, o->alpha);
+  free(el);
+  int st = orc_spmm_alpha(g, 0, (int)heads, (int)HC, o->alpha, (orc_qref){NULL, o->Hp, 1.0f}, o->agg);
+  if (st) return st;
+  for (int64_t v = 0; v < n; ++v)
+    for (int64_t k = 0; k < C; ++k) {
+      float t = o->agg[v * HC + k];
+      for (int64_t h = 1; h < heads; ++h) t = t + o->agg[v * HC + h * C + k];
+      t = t / (float)heads;
+      o->logits[v * C + k] = t + bias[k];
+    }
+  return ORC_OK;
+}
+
+typedef struct {
+  float* db;                  /* [C]  Σᶜ_v ∂logits */
+  float* G;                   /* [n][C] ∂logits / heads = ∂agg of every head */
+  float* dalpha;              /* [e][H] ⑤″ sequential fmaf over c */
+  float* P; float* dE; float* dE_pre;
+  float* dD; float* dS;
+  float* dHp_agg; float* dHp; /* [n][H*C] */
+  float* da_src; float* da_dst; float* da_src_abs; float* da_dst_abs;
+  float* dH;                  /* [n][F] = sgemm(∂H′, Wᵀ) */
+  float* dW;                  /* [F][H*C] = sgemm(Hᵀ, ∂H′) */
+} orc_out_bwd_out;
+
+int orc_gat_out_bwd(const orc_graph* g, const orc_out_cfg* c, const float* H, const float* W,
+                    const float* a_src, const float* a_dst, const orc_out_fwd_out* f, const float* dlogits,
+                    orc_out_bwd_out* o) {
+  int64_t n = g->n, F = c->F, heads = c->H, C = c->C, HC = heads * C;
+  int st;
+  orc_colsum(dlogits, n, C, o->db);
+  for (int64_t i = 0; i < n * C; ++i) o->G[i] = dlogits[i] / (float)heads;
+  /* ∂agg[v,h,c] = G[v,c] for every head (mean), materialised for ⑤′ */
+  float* dagg = (float*)malloc(sizeof(float) * (size_t)(n * HC > 0 ? n * HC : 1));
+  if (!dagg) return ORC_ERR_ALLOC;
+  for (int64_t v = 0; v < n; ++v)
+    for (int64_t h = 0; h < heads; ++h)
+      for (int64_t k = 0; k < C; ++k) dagg[v * HC + h * C + k] = o->G[v * C + k];
+  /* ⑤″ ∂α[e,h] = Σ_c fmaf(G[v,c], H′[u,h,c]) sequential */
+  for (int64_t v = 0; v < n; ++v)
+    for (int64_t p = g->in_ptr[v]; p < g->in_ptr[v + 1]; ++p) {
+      int64_t u = g->in_src[p];
+      for (int64_t h = 0; h < heads; ++h) {
+        float acc = 0.0f;
+        for (int64_t k = 0; k < C; ++k) acc = fmaf(o->G[v * C + k], f->Hp[u * HC + h * C + k], acc);
+        o->dalpha[p * heads + h] = acc;
+      }
+    }
+  /* ④′, ③″, ③′, ⑤′ as in orc_gat_bwd */
+  orc_softmax_bwd(g, (int)heads, f->alpha, o->dalpha, f->e_pre, c->slope, o->P, o->dE, o->dE_pre);
+  if ((st = orc_edge_sum(g, 0, (int)heads, o->dE_pre, o->dD))) return st;
+  if ((st = orc_edge_sum(g, 1, (int)heads, o->dE_pre, o->dS))) return st;
+  if ((st = orc_spmm_alpha(g, 1, (int)heads, (int)HC, f->alpha, (orc_qref){NULL, dagg, 1.0f}, o->dHp_agg))) return st;
+  free(dagg);
+  /* ②′ (reading R23) */
+  for (int64_t u = 0; u < n; ++u)
+    for (int64_t j = 0; j < HC; ++j) {
+      int64_t h = j / C;
+      float t1 = o->dS[u * heads + h] * a_src[j];
+      float t2 = o->dHp_agg[u * HC + j] + t1;
+      float t3 = o->dD[u * heads + h] * a_dst[j];
+      o->dHp[u * HC + j] = t2 + t3;
+    }
+  for (int64_t j = 0; j < HC; ++j) {
+    int64_t h = j / C;
+    double as = 0.0, ad = 0.0, as_abs = 0.0, ad_abs = 0.0;
+    for (int64_t u = 0; u < n; ++u) {
+      double ts = (double)o->dS[u * heads + h] * (double)f->Hp[u * HC + j];
+      double td = (double)o->dD[u * heads + h] * (double)f->Hp[u * HC + j];
+      as += ts; ad += td; as_abs += fabs(ts); ad_abs += fabs(td);
+    }
+    o->da_src[j] = (float)as;
+    o->da_dst[j] = (float)ad;
+    if (o->da_src_abs) o->da_src_abs[j] = (float)as_abs;
+    if (o->da_dst_abs) o->da_dst_abs[j] = (float)ad_abs;
+  }
+  /* ①′ */
+  if (o->dH) orc_sgemm(n, F, HC, o->dHp, HC, 0, W, HC, 1, o->dH);
+  orc_sgemm(F, HC, n, H, F, 1, o->dHp, HC, 0, o->dW);
+  return ORC_OK;
+}
+
+/* Cross-entropy over labelled rows ("mean negative log-softmax";
+ * reading R36): label < 0 = unlabelled (zero gradient).  Per labelled row v:
+ *   m = max_c z ; ssum = Σ_c exp_p(z_c − m) (sequential) ; loss_v = (m + logf(ssum)) − z_y
+ *   ∂z_c = (exp_p(z_c − m)/ssum − [c = y]) / n_lab
+ * loss = (Σ_v loss_v in double) / n_lab.  Returns ORC_ERR_BITS+100 (=103) on a
+ * label >= C (the caller's error).  logf is glibc's (not pinned: the loss is
+ * compared within a tolerance, the gradient uses only exp_p and IEEE ops). */
+int orc_cross_entropy(const float* z, const int32_t* labels, int64_t n, int32_t C, int64_t n_lab,
+                      float* row_loss, double* loss, float* dz) {
+  double acc = 0.0;
+  float nl = (float)n_lab;
+  for (int64_t v = 0; v < n; ++v) {
+    int32_t y = labels[v];
+    if (y >= C) return 103;
+    if (y < 0) {
+      for (int32_t k = 0; k < C; ++k) dz[v * C + k] = 0.0f;
+      if (row_loss) row_loss[v] = 0.0f;
+      continue;
+    }
+    float m = -INFINITY;
+    for (int32_t k = 0; k < C; ++k) m = fmaxf(m, z[v * C + k]);
+    float ssum = 0.0f;
+    for (int32_t k = 0; k < C; ++k) ssum = ssum + orc_exp_p(z[v * C + k] - m);
+    float lv = (m + logf(ssum)) - z[v * C + y];
+    if (row_loss) row_loss[v] = lv;
+    acc += (double)lv;
+    for (int32_t k = 0; k < C; ++k) {
+      float p = orc_exp_p(z[v * C + k] - m) / ssum;
+      float t = p - (k == y ? 1.0f : 0.0f);
+      dz[v * C + k] = t / nl;
+    }
+  }
+  *loss = n_lab > 0 ? acc / (double)n_lab : 0.0;
+  return ORC_OK;
+}
+
+/* FP32 master-weight update (§3.2 Eq.6, add-then-quantize): the
+ * dequantized FP32 gradient is applied to the FP32 master, W ← W − lr·∂W (two
+ * rn ops); the next iteration's Q(W) sees the updated master. */
+void orc_sgd(float* w, const float* g, int64_t count, float lr) {
+  for (int64_t i = 0; i < count; ++i) {
+    float t = lr * g[i];
+    w[i] = w[i] - t;
+  }
+}

@@ -181,3 +181,40 @@ def grad_out(n: int, cols: int, seed: int = SEED_GRAD) -> np.ndarray:
     """Upstream gradient dH_out ~ N(0,1), float32 [n][cols]."""
     rng = np.random.Generator(np.random.PCG64(seed))
     return rng.standard_normal((n, cols), dtype=np.float32)
+
+
+# ----------------------------------------------------------------------------------------------
+# NEXT-1 (training step) inputs: labels and the parameters of a multi-layer GAT
+# ----------------------------------------------------------------------------------------------
+SEED_LABEL = 5
+ARXIV_CLASSES, ARXIV_TRAIN_FRAC = 40, 90_941 / 169_343   # ogbn-arxiv: 40 classes, 53.7 % train split
+
+
+def labels(n: int, classes: int, train_frac: float = 1.0, seed: int = SEED_LABEL) -> np.ndarray:
+    """Class ids int32 [n] uniform in [0, classes); rows outside a seeded train subset get -1."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    y = rng.integers(0, classes, size=n).astype(np.int32)
+    if train_frac < 1.0:
+        y[rng.random(n) >= train_frac] = -1
+    return y
+
+
+def gat_model_params(f: int, heads: int, head_dim: int, layers: int, classes: int, out_heads: int | None = None,
+                     bias_scale: float = 0.0, seed: int = SEED_PARAM):
+    """(hidden, out) parameter dicts of an L-layer GAT: L-1 hidden layers f -> heads*head_dim
+    (concatenated) and a final layer -> out_heads x classes (averaged).  Glorot W / a; biases
+    N(0, bias_scale) (0 = zeros, DGL's default)."""
+    hidden = []
+    fin = f
+    for l in range(layers - 1):
+        W, a_s, a_d = gat_params(fin, heads, head_dim, seed=seed + 10 * l)
+        rng = np.random.Generator(np.random.PCG64(seed + 10 * l + 1))
+        b = (rng.standard_normal(heads * head_dim) * bias_scale).astype(np.float32)
+        hidden.append(dict(W=W, a_src=a_s, a_dst=a_d, b=b, heads=heads, head_dim=head_dim))
+        fin = heads * head_dim
+    oh = out_heads or heads
+    W, a_s, a_d = gat_params(fin, oh, classes, seed=seed + 10 * (layers - 1))
+    rng = np.random.Generator(np.random.PCG64(seed + 10 * (layers - 1) + 1))
+    b = (rng.standard_normal(classes) * bias_scale).astype(np.float32)
+    out = dict(W=W, a_src=a_s, a_dst=a_d, b=b, heads=oh, classes=classes)
+    return hidden, out
