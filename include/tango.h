@@ -279,6 +279,85 @@ tango_status tango_gcn_ctx_get_view(const tango_graph* G, const tango_gcn_params
                                     tango_gcn_ctx_view* view);
 
 /* ------------------------------------------------------------------------- */
+/* NEXT-1: the training step around the quantized layer.     */
+/* ------------------------------------------------------------------------- */
+/* Full-precision GEMM (the FP32 final layer, §3.2 Eq.7-8) with the  */
+/* pinned order of reading R33: C[m][n] = Σᶜ_k fmaf(A(m,k), B(k,n)), chunks of */
+/* 1024 k folded left to right (a K <= 1024 contraction is one fmaf chain).    */
+/* Layouts as tango_gemm_q: a_layout K_MAJOR: A is [M][lda]; MN_MAJOR: A is    */
+/* [K][lda].  b_layout K_MAJOR: B is [N][ldb] (Bᵀ); MN_MAJOR: B is [K][ldb].   */
+/* C: fp32 [M][N] (row stride N), overwritten.  workspace: device scratch of   */
+/* tango_sgemm_workspace_bytes(M,N,K) bytes (0 when K <= 1024; may be NULL).  */
+size_t tango_sgemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+tango_status tango_sgemm(const float* A, int64_t lda, int32_t a_layout, const float* B, int64_t ldb, int32_t b_layout,
+                         int64_t M, int64_t N, int64_t K, float* C, void* workspace, size_t ws_bytes,
+                         cudaStream_t stream);
+
+/* Column sums over rows with the same chunked order (R33): out[j] = Σᶜ_r x[r][j].
+ * x: [rows][cols] fp32; out: [cols]; workspace as tango_colsum_workspace_bytes. */
+size_t tango_colsum_workspace_bytes(int64_t rows, int64_t cols);
+tango_status tango_colsum(const float* x, int64_t rows, int64_t cols, float* out, void* workspace, size_t ws_bytes,
+                          cudaStream_t stream);
+
+/* Hidden-layer bias + ReLU (reading R34; P:998-1001 does not fix them):
+ * y = max(x + bias[j], 0) (one rn add), amax_out (nullable device scalar) = max y,
+ * the amax hint of the next layer's Q(H).  x, y: [rows][cols] (may alias). */
+tango_status tango_bias_act_fwd(const float* x, const float* bias, int64_t rows, int64_t cols, float* y,
+                                float* amax_out, cudaStream_t stream);
+/* Backward: dx = y > 0 ? dy : 0, dbias = Σᶜ_r dx (R33), amax_dx (nullable) = max|dx|,
+ * the ∂H_out amax hint of the quantized layer below.  workspace: tango_colsum_workspace_bytes. */
+tango_status tango_bias_act_bwd(const float* y, const float* dy, int64_t rows, int64_t cols, float* dx, float* dbias,
+                                float* amax_dx, void* workspace, size_t ws_bytes, cudaStream_t stream);
+
+/* Mean cross-entropy over labelled rows (reading R36; node classification P:987-990):
+ * labels[v] in [0, classes) or −1 (unlabelled: zero gradient).  Per labelled row:
+ * m = max z, Σ = Σ_c exp_p(z_c − m) in class order, loss_v = (m + logf Σ) − z_y,
+ * dlogits_c = (exp_p(z_c − m)/Σ − [c = y]) / n_labeled.  loss_out: device double =
+ * Σ_v loss_v / n_labeled (order-free double sum).  A label >= classes writes
+ * TANGO_ERR_INVALID_ARG to *dev_status.  classes <= 1024. */
+tango_status tango_cross_entropy(const float* logits, const int32_t* labels, int64_t rows, int32_t classes,
+                                 int64_t n_labeled, float* dlogits, double* loss_out, int32_t* dev_status,
+                                 cudaStream_t stream);
+
+/* FP32 master-weight update (§3.2 Eq.6, add-then-quantize; reading R37):
+ * w ← w − lr·g (two rn ops) for every listed tensor, in one launch (<= 32 tensors;
+ * the host array is read during the call only).  The next step's Q(W) quantizes the
+ * updated master. */
+typedef struct { float* w; const float* g; int64_t count; } tango_sgd_tensor;
+tango_status tango_sgd_update(const tango_sgd_tensor* tensors, int32_t count, float lr, cudaStream_t stream);
+
+/* Full-precision final GAT layer ("use full precision to compute the layer
+ * before the Softmax"; reading R35): FP32 ① H′ = H·W (tango_sgemm order), ② S, D
+ * (sequential fmaf per head), ③ e_pre = S[u] + D[v] + LeakyReLU, ④ edge softmax
+ * (exp_p, Σᶜ), ⑤ Σᶜ fmaf(α, H′[u]) per head, then logits = ((Σ_h, in head order)/heads)
+ * + bias.  One GPU only (row_begin = 0, row_end = n_global; out_eid required):
+ * TANGO_ERR_UNSUPPORTED otherwise.  heads*classes <= 1024. */
+typedef struct {
+  const float* W;          /* device [in_feats][heads*classes] */
+  const float* a_src;      /* device [heads*classes] */
+  const float* a_dst;
+  const float* bias;       /* device [classes] */
+  int32_t in_feats, heads, classes;
+  float neg_slope;
+} tango_gat_out_params;
+size_t tango_gat_out_ctx_bytes(const tango_graph* G, const tango_gat_out_params* p);
+/* H: [n][in_feats]; logits: [n][classes]. */
+tango_status tango_gat_out_fwd(const tango_graph* G, const tango_gat_out_params* p, const float* H, void* ctx,
+                               size_t ctx_bytes, float* logits, cudaStream_t stream);
+/* Must follow tango_gat_out_fwd on the same H and ctx.  dlogits: [n][classes].
+ * dH (nullable): [n][in_feats]; dW [in_feats][heads*classes]; da_src, da_dst
+ * [heads*classes] (order-free atomics); dbias [classes]; all overwritten. */
+tango_status tango_gat_out_bwd(const tango_graph* G, const tango_gat_out_params* p, void* ctx, size_t ctx_bytes,
+                               const float* H, const float* dlogits, float* dH, float* dW, float* da_src,
+                               float* da_dst, float* dbias, cudaStream_t stream);
+typedef struct {
+  float *Hp, *S, *D, *e_pre, *alpha, *m, *den;      /* forward: [n][HC], [n][H] x2, [e][H] x2, [n][H] x2 */
+  float *G, *dalpha, *dE_pre, *P, *dD, *dS, *dHp;  /* backward: [n][C], [e][H] x2, [n][H] x3, [n][HC] */
+} tango_gat_out_ctx_view;
+tango_status tango_gat_out_ctx_get_view(const tango_graph* G, const tango_gat_out_params* p, void* ctx,
+                                        tango_gat_out_ctx_view* view);
+
+/* ------------------------------------------------------------------------- */
 /* Multi-GPU (destination-row partitioning): an NCCL          */
 /* communicator built from a 128-byte ncclUniqueId that the caller broadcasts  */
 /* (e.g. with torch.distributed).  Collectives are enqueued on the caller's    */

@@ -70,6 +70,22 @@ class GcnCtxView(C.Structure):
                [(f, C.c_int64) for f in ("ldF", "ldO", "ldFt")] + [(f, _P) for f in ("ia", "ib", "scalars")]
 
 
+class GatOutParams(C.Structure):
+    _fields_ = [("W", _P), ("a_src", _P), ("a_dst", _P), ("bias", _P), ("in_feats", C.c_int32),
+                ("heads", C.c_int32), ("classes", C.c_int32), ("neg_slope", C.c_float)]
+
+
+_OUT_VIEW = ("Hp", "S", "D", "e_pre", "alpha", "m", "den", "G", "dalpha", "dE_pre", "P", "dD", "dS", "dHp")
+
+
+class GatOutCtxView(C.Structure):
+    _fields_ = [(f, _P) for f in _OUT_VIEW]
+
+
+class SgdTensor(C.Structure):
+    _fields_ = [("w", _P), ("g", _P), ("count", C.c_int64)]
+
+
 _lib = None
 
 EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tango_quantize", "tango_gemm_q",
@@ -79,7 +95,10 @@ EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tan
            "tango_comm_unique_id_bytes", "tango_comm_get_unique_id", "tango_comm_init", "tango_comm_destroy",
            "tango_comm_set_partition", "tango_local_group_create", "tango_local_group_destroy",
            "tango_comm_init_local", "tango_quant_error", "tango_select_bits", "tango_profile_enable", "tango_launch_count", "tango_profile_collect",
-           "tango_profile_num_entries", "tango_profile_entry", "tango_profile_reset"]
+           "tango_profile_num_entries", "tango_profile_entry", "tango_profile_reset",
+           "tango_sgemm_workspace_bytes", "tango_sgemm", "tango_colsum_workspace_bytes", "tango_colsum",
+           "tango_bias_act_fwd", "tango_bias_act_bwd", "tango_cross_entropy", "tango_sgd_update",
+           "tango_gat_out_ctx_bytes", "tango_gat_out_fwd", "tango_gat_out_bwd", "tango_gat_out_ctx_get_view"]
 
 
 def load(path: str = LIB_PATH):
@@ -130,6 +149,22 @@ def load(path: str = LIB_PATH):
     L.tango_profile_num_entries.restype = i32
     L.tango_profile_entry.argtypes = [i32, C.c_char_p, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     L.tango_profile_reset.restype = None
+    L.tango_sgemm_workspace_bytes.restype = sz
+    L.tango_sgemm_workspace_bytes.argtypes = [i64, i64, i64]
+    L.tango_sgemm.argtypes = [_P, i64, i32, _P, i64, i32, i64, i64, i64, _P, _P, sz, _P]
+    L.tango_colsum_workspace_bytes.restype = sz
+    L.tango_colsum_workspace_bytes.argtypes = [i64, i64]
+    L.tango_colsum.argtypes = [_P, i64, i64, _P, _P, sz, _P]
+    L.tango_bias_act_fwd.argtypes = [_P, _P, i64, i64, _P, _P, _P]
+    L.tango_bias_act_bwd.argtypes = [_P, _P, i64, i64, _P, _P, _P, _P, sz, _P]
+    L.tango_cross_entropy.argtypes = [_P, _P, i64, i32, i64, _P, _P, _P, _P]
+    L.tango_sgd_update.argtypes = [C.POINTER(SgdTensor), i32, f32, _P]
+    PO = C.POINTER(GatOutParams)
+    L.tango_gat_out_ctx_bytes.restype = sz
+    L.tango_gat_out_ctx_bytes.argtypes = [PG, PO]
+    L.tango_gat_out_fwd.argtypes = [PG, PO, _P, _P, sz, _P, _P]
+    L.tango_gat_out_bwd.argtypes = [PG, PO, _P, sz, _P, _P, _P, _P, _P, _P, _P, _P]
+    L.tango_gat_out_ctx_get_view.argtypes = [PG, PO, _P, C.POINTER(GatOutCtxView)]
     _lib = L
     return L
 
@@ -531,3 +566,133 @@ class GCNLayer:
                     qdY=sl(v.qdY, n * v.ldO, i8, (n, v.ldO))[:, :O], ia=sl(v.ia, n * O * 4, torch.int32, (n, O)),
                     ib=sl(v.ib, n * O * 4, torch.int32, (n, O)),
                     scalars=sl(v.scalars, 64 * 4, torch.float32, (64,)))
+
+
+# ---------------------------------------------------------------------------------------- NEXT-1
+def sgemm(A, B, a_layout=TANGO_K_MAJOR, b_layout=TANGO_MN_MAJOR, out=None, workspace=None):
+    """tango_sgemm (full-precision GEMM, reading R33).  Default layouts: A [M][K], B [K][N]."""
+    L = load()
+    M, K = (A.shape[1], A.shape[0]) if a_layout == TANGO_MN_MAJOR else A.shape
+    N = B.shape[0] if b_layout == TANGO_K_MAJOR else B.shape[1]
+    out = out if out is not None else torch.empty((M, N), dtype=torch.float32, device=A.device)
+    need = L.tango_sgemm_workspace_bytes(M, N, K)
+    if workspace is None and need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=A.device)
+    _check(L.tango_sgemm(_ptr(A), A.shape[1], a_layout, _ptr(B), B.shape[1], b_layout, M, N, K, _ptr(out),
+                         _ptr(workspace), workspace.numel() if workspace is not None else 0, _stream()),
+           "tango_sgemm")
+    return out
+
+
+def colsum(x, out=None, workspace=None):
+    L = load()
+    rows, cols = x.shape
+    out = out if out is not None else torch.empty(cols, dtype=torch.float32, device=x.device)
+    need = L.tango_colsum_workspace_bytes(rows, cols)
+    if workspace is None and need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    _check(L.tango_colsum(_ptr(x), rows, cols, _ptr(out), _ptr(workspace),
+                          workspace.numel() if workspace is not None else 0, _stream()), "tango_colsum")
+    return out
+
+
+def bias_act_fwd(x, bias, out=None, amax_out=None):
+    """tango_bias_act_fwd: (ReLU(x + b), max of it)."""
+    L = load()
+    rows, cols = x.shape
+    out = out if out is not None else torch.empty_like(x)
+    amax_out = amax_out if amax_out is not None else torch.empty(1, dtype=torch.float32, device=x.device)
+    _check(L.tango_bias_act_fwd(_ptr(x), _ptr(bias), rows, cols, _ptr(out), _ptr(amax_out), _stream()),
+           "tango_bias_act_fwd")
+    return out, amax_out
+
+
+def bias_act_bwd(y, dy, dx=None, dbias=None, amax_out=None, workspace=None):
+    """tango_bias_act_bwd: (dx, dbias, max|dx|)."""
+    L = load()
+    rows, cols = y.shape
+    dx = dx if dx is not None else torch.empty_like(y)
+    dbias = dbias if dbias is not None else torch.empty(cols, dtype=torch.float32, device=y.device)
+    amax_out = amax_out if amax_out is not None else torch.empty(1, dtype=torch.float32, device=y.device)
+    need = L.tango_colsum_workspace_bytes(rows, cols)
+    if workspace is None and need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=y.device)
+    _check(L.tango_bias_act_bwd(_ptr(y), _ptr(dy), rows, cols, _ptr(dx), _ptr(dbias), _ptr(amax_out),
+                                _ptr(workspace), workspace.numel() if workspace is not None else 0, _stream()),
+           "tango_bias_act_bwd")
+    return dx, dbias, amax_out
+
+
+def cross_entropy(logits, labels, n_labeled, dlogits=None, loss=None, status=None):
+    """tango_cross_entropy: (loss f64 (1,), dlogits)."""
+    L = load()
+    rows, classes = logits.shape
+    dlogits = dlogits if dlogits is not None else torch.empty_like(logits)
+    loss = loss if loss is not None else torch.empty(1, dtype=torch.float64, device=logits.device)
+    _check(L.tango_cross_entropy(_ptr(logits), _ptr(labels), rows, classes, int(n_labeled), _ptr(dlogits),
+                                 _ptr(loss), _ptr(status), _stream()), "tango_cross_entropy")
+    return loss, dlogits
+
+
+def sgd_update(pairs, lr):
+    """tango_sgd_update over [(w, g), ...] (in place on w)."""
+    L = load()
+    arr = (SgdTensor * len(pairs))(*[SgdTensor(_ptr(w), _ptr(g), w.numel()) for w, g in pairs])
+    _check(L.tango_sgd_update(arr, len(pairs), float(lr), _stream()), "tango_sgd_update")
+
+
+class GATOutLayer:
+    """The full-precision final GAT layer (tango_gat_out_fwd / _bwd) with its device ctx."""
+
+    def __init__(self, graph: DeviceGraph, W, a_src, a_dst, bias, heads, classes, slope=0.2):
+        L = load()
+        self.graph, self.heads, self.classes = graph, heads, classes
+        self.W, self.a_src, self.a_dst, self.bias = (t.contiguous() for t in (W, a_src, a_dst, bias))
+        self.F = W.shape[0]
+        self.HC = heads * classes
+        self.params = GatOutParams(_ptr(self.W), _ptr(self.a_src), _ptr(self.a_dst), _ptr(self.bias), self.F, heads,
+                                   classes, slope)
+        nbytes = L.tango_gat_out_ctx_bytes(graph.ref(), C.byref(self.params))
+        if nbytes == 0:
+            raise TangoError(2, "tango_gat_out_ctx_bytes")
+        self.ctx = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+
+    def forward(self, H, out=None):
+        L = load()
+        out = out if out is not None else torch.empty((self.graph.n_local, self.classes), dtype=torch.float32,
+                                                      device="cuda")
+        _check(L.tango_gat_out_fwd(self.graph.ref(), C.byref(self.params), _ptr(H), _ptr(self.ctx), self.ctx.numel(),
+                                   _ptr(out), _stream()), "tango_gat_out_fwd")
+        return out
+
+    def backward(self, H, dlogits, want_dH=True, outs=None):
+        L = load()
+        n = self.graph.n_local
+        if outs is None:
+            dH = torch.empty((n, self.F), dtype=torch.float32, device="cuda") if want_dH else None
+            dW = torch.empty((self.F, self.HC), dtype=torch.float32, device="cuda")
+            da_s = torch.empty(self.HC, dtype=torch.float32, device="cuda")
+            da_d = torch.empty(self.HC, dtype=torch.float32, device="cuda")
+            db = torch.empty(self.classes, dtype=torch.float32, device="cuda")
+        else:
+            dH, dW, da_s, da_d, db = outs
+        _check(L.tango_gat_out_bwd(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), self.ctx.numel(), _ptr(H),
+                                   _ptr(dlogits), _ptr(dH), _ptr(dW), _ptr(da_s), _ptr(da_d), _ptr(db), _stream()),
+               "tango_gat_out_bwd")
+        return dH, dW, da_s, da_d, db
+
+    def view(self):
+        L = load()
+        v = GatOutCtxView()
+        _check(L.tango_gat_out_ctx_get_view(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), C.byref(v)),
+               "tango_gat_out_ctx_get_view")
+        base = self.ctx.data_ptr()
+        n, H, E, HC, Cc = self.graph.n_local, self.heads, self.graph.e_in, self.HC, self.classes
+        shapes = dict(Hp=(n, HC), S=(n, H), D=(n, H), e_pre=(E, H), alpha=(E, H), m=(n, H), den=(n, H), G=(n, Cc),
+                      dalpha=(E, H), dE_pre=(E, H), P=(n, H), dD=(n, H), dS=(n, H), dHp=(n, HC))
+        out = {}
+        for f, shp in shapes.items():
+            off = getattr(v, f) - base
+            cnt = shp[0] * shp[1]
+            out[f] = self.ctx[off:off + 4 * cnt].view(torch.float32).reshape(shp).clone()
+        return out
