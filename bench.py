@@ -138,6 +138,69 @@ def gemm_microbench(T, torch, int8_peak, size=8192, reps=10):
             "frac": round(tops / int8_peak, 3), "peak_source": "MEASURED_PEAKS bf16 x 2 (nominal int8:bf16)"}
 
 
+# ------------------------------------------------------------------------------------- NEXT-1 train step
+def train_step_bench(T, torch, dg, g, F, H, D, args, l2_flush):
+    """One full-batch training step of the 3-layer GAT of BASELINE.json configs[2] (arxiv-shaped):
+    two quantized hidden layers F -> HxD -> HxD (bias + ReLU) and the FP32 final layer -> H x 40
+    (heads averaged), cross-entropy over the 53.7 % train split, SGD on the FP32 masters.  Timed as
+    CUDA-graph replays with the L2 flushed between steps; per-kernel times from an eager pass."""
+    from paper_2308_00890_b200.model import GATModel
+    C = inputs.ARXIV_CLASSES
+    hidden, out = inputs.gat_model_params(F, H, D, 3, C)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    hid_d = [{k: (cu(v) if isinstance(v, np.ndarray) else v) for k, v in p.items()} for p in hidden]
+    out_d = {k: (cu(v) if isinstance(v, np.ndarray) else v) for k, v in out.items()}
+    model = GATModel(dg, hid_d, out_d, slope=0.2, bits=8)
+    X = cu(inputs.features(g.n, F))
+    lab = inputs.labels(g.n, C, train_frac=inputs.ARXIV_TRAIN_FRAC)
+    n_lab = int((lab >= 0).sum())
+    labd = cu(lab)
+    lr = 0.01
+    for i in range(args.warmup):
+        model.step(X, labd, n_lab, lr, step=i)
+    torch.cuda.synchronize()
+    model.check_status()
+    T.profile_enable(True)
+    T.profile_read(reset=True)
+    for i in range(args.steps):
+        l2_flush.zero_()
+        model.step(X, labd, n_lab, lr, step=args.warmup + i)
+    torch.cuda.synchronize()
+    prof = T.profile_read(reset=True)
+    T.profile_enable(False)
+    graph = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cs):
+        model.step(X, labd, n_lab, lr, step=0)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=cs):
+            model.step(X, labd, n_lab, lr, step=1)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        l2_flush.zero_()
+        evs[i][0].record()
+        graph.replay()
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    model.check_status()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    per_step = {k: round(v[0] / args.steps, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    top = dict(list(per_step.items())[:12])
+    sg = prof.get("sgemm")
+    # final layer: H' = H·W, ∂H = ∂H'·Wᵀ, ∂W = Hᵀ·∂H' — three contractions of n x (H*D) x (H*C)
+    sg_flops = 3 * 2.0 * g.n * (H * D) * (H * C)
+    res = {"model": f"3-layer GAT {F}->{H}x{D}->{H}x{D}->{H}x{C} (mean), int8 hidden layers, FP32 final layer",
+           "ms_per_step": round(ms, 4), "unit": "ms (one full-batch step = one epoch)",
+           "loss": float(model.loss.item()), "n_labeled": n_lab,
+           "eager_kernel_ms_per_step": round(sum(v[0] for v in prof.values()) / args.steps, 4),
+           "top_kernels_ms_per_step": top, "timing": "CUDA-graph replay per step, L2 flushed between steps"}
+    if sg:
+        res["sgemm_fp32_tflops"] = round(sg_flops / (sg[0] / args.steps / 1e3) / 1e12, 1)
+    return res
+
+
 # ------------------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     if rank != 0:
@@ -189,6 +252,7 @@ def main():
     ap.add_argument("--workload", default="arxiv", choices=sorted(inputs.WORKLOADS))
     ap.add_argument("--impl", default="tango", choices=["tango", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train-step", action="store_true")
     ap.add_argument("--ref-sample", type=float, default=1.0)
     ap.add_argument("--profile-breakdown", action="store_true", help="print per-kernel times to stderr")
     args = ap.parse_args()
@@ -413,6 +477,11 @@ def main():
     if world > 1:
         dist.all_reduce(launches_t)
 
+    # ---------------- NEXT-1: the training step around the layer (one GPU, arxiv workload)
+    train = None
+    if world == 1 and args.workload == "arxiv" and not args.no_train_step:
+        train = train_step_bench(T, torch, dg, g, F, H, D, args, l2_flush)
+
     # ---------------- CPU baseline: the oracle as it stands, rank 0 at N = 1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -443,6 +512,7 @@ def main():
                                 "(copy stream, double-buffered inputs)",
                         "d2h_bytes_per_step": d2h},
                 "gpu_launches": int(launches_t.item()), "clocks": clk, "kernel_ms": breakdown, "kernel_ms_per_step": per_step,
+                "train_step": train,
                 "timing": "value: CUDA-graph replay of fwd+bwd per step (events per step, L2 flushed between "
                           "steps); kernel_ms/roofline: eager pass with events around every launch "
                           f"(sum of kernel times {eager_ms:.3f} ms/step)"}

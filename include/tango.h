@@ -353,6 +353,7 @@ tango_status tango_gat_out_bwd(const tango_graph* G, const tango_gat_out_params*
 typedef struct {
   float *Hp, *S, *D, *e_pre, *alpha, *m, *den;      /* forward: [n][HC], [n][H] x2, [e][H] x2, [n][H] x2 */
   float *G, *dalpha, *dE_pre, *P, *dD, *dS, *dHp;  /* backward: [n][C], [e][H] x2, [n][H] x3, [n][HC] */
+  float *agg;                                      /* forward ⑤ before the head mean: [n][HC] */
 } tango_gat_out_ctx_view;
 tango_status tango_gat_out_ctx_get_view(const tango_graph* G, const tango_gat_out_params* p, void* ctx,
                                         tango_gat_out_ctx_view* view);

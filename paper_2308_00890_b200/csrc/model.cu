@@ -339,53 +339,256 @@ __global__ void k_out_sd(const float* __restrict__ Hp, int64_t n, int heads, int
   D[tid] = d;
 }
 
-// ③ in FP32: e_pre = S[u] + D[v], el = LeakyReLU(e_pre) (thread per (row, head), in-CSR order)
-__global__ void k_out_el(GraphDev g, int heads, const float* __restrict__ S, const float* __restrict__ D, float slope,
-                         float* __restrict__ e_pre, float* __restrict__ el) {
+// The final layer's per-row chunked sums (R14) are split by row weight: a LIGHT row (degree
+// <= C_E) is one chunk and is summed by one thread / one warp sequentially; a HEAVY row (degree >
+// C_E) is handled by one block whose threads compute the chunk partials in parallel and fold them
+// left to right (the same value the sequential definition gives).  The heavy-row lists of the
+// in- and out-CSR and the in-CSR destination of every edge come from k_out_plan.
+constexpr int OUT_MAXHC = 1024;
+constexpr int OUT_PART = 4096;   // shared-memory partials per pass of a heavy-row block
+
+__global__ void __launch_bounds__(256) k_out_plan(GraphDev g, int32_t* __restrict__ in_dst, int32_t* __restrict__ hin,
+                                                  int32_t* __restrict__ hout, int32_t* counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t v = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); v < g.n_local; v += nw) {
+    const int64_t b = g.in_ptr[v], e1 = g.in_ptr[v + 1];
+    for (int64_t e = b + lane; e < e1; e += 32) in_dst[e] = (int32_t)v;
+    if (lane == 0) {
+      if (e1 - b > g.chunk) hin[atomicAdd(counts + 0, 1)] = (int32_t)v;
+      if (g.out_ptr[v + 1] - g.out_ptr[v] > g.chunk) hout[atomicAdd(counts + 1, 1)] = (int32_t)v;
+    }
+  }
+}
+
+// ③ in FP32: e_pre = S[u] + D[v], el = LeakyReLU(e_pre); thread per edge (all heads)
+__global__ void k_out_el(int64_t e_in, int heads, const int32_t* __restrict__ in_src,
+                         const int32_t* __restrict__ in_dst, const float* __restrict__ S, const float* __restrict__ D,
+                         float slope, float* __restrict__ e_pre, float* __restrict__ el) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e_in; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = in_src[e], v = in_dst[e];
+    for (int h = 0; h < heads; ++h) {
+      const float x = __fadd_rn(S[u * heads + h], D[v * heads + h]);
+      e_pre[e * heads + h] = x;
+      el[e * heads + h] = x > 0.0f ? x : __fmul_rn(x, slope);
+    }
+  }
+}
+
+// Chunked sums of one heavy row inside a block: for every head h, total_h = Σᶜ over the row's
+// list positions i in [0, len) of the accumulation acc = op(acc, i, h) (chunks of `chunk`
+// positions, partials folded left to right).  Results in out_h[h] (shared).  All threads call it.
+template <class Op>
+__device__ void heavy_row_sums(int64_t len, int chunk, int heads, Op op, float* part, float* out_h) {
+  const int64_t nch = (len + chunk - 1) / chunk;
+  const int grp = OUT_PART / heads;
+  float total = 0.0f;
+  for (int64_t c0 = 0; c0 < nch; c0 += grp) {
+    const int64_t nc = min((int64_t)grp, nch - c0);
+    for (int64_t it = threadIdx.x; it < nc * heads; it += blockDim.x) {
+      const int64_t c = c0 + it / heads;
+      const int h = (int)(it % heads);
+      const int64_t i0 = c * chunk, i1 = min(len, i0 + chunk);
+      float acc = 0.0f;
+      for (int64_t i = i0; i < i1; ++i) acc = op(acc, i, h);
+      part[it] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x < heads) {
+      for (int64_t c = 0; c < nc; ++c) {
+        const float p = part[c * heads + threadIdx.x];
+        total = (c0 + c == 0) ? p : __fadd_rn(total, p);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < heads) out_h[threadIdx.x] = total;
+  __syncthreads();
+}
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float r = -INFINITY;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmaxf(r, red[w]);
+  __syncthreads();
+  return r;
+}
+
+// ④ edge softmax, light rows: thread per (row, head), one sequential chunk
+__global__ void k_out_softmax_light(GraphDev g, int heads, const float* __restrict__ el, float* __restrict__ m,
+                                    float* __restrict__ den, float* __restrict__ alpha) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (tid >= g.n_local * heads) return;
   const int64_t v = tid / heads;
   const int h = (int)(tid % heads);
-  const float dv = D[v * heads + h];
-  for (int64_t e = g.in_ptr[v]; e < g.in_ptr[v + 1]; ++e) {
-    const float x = __fadd_rn(S[(int64_t)g.in_src[e] * heads + h], dv);
-    e_pre[e * heads + h] = x;
-    el[e * heads + h] = x > 0.0f ? x : __fmul_rn(x, slope);
+  const int64_t b = g.in_ptr[v], e1 = g.in_ptr[v + 1];
+  if (e1 - b > g.chunk) return;
+  float mx = -INFINITY;
+  for (int64_t e = b; e < e1; ++e) mx = fmaxf(mx, el[e * heads + h]);
+  if (e1 == b) mx = 0.0f;
+  float dn = 0.0f;
+  for (int64_t e = b; e < e1; ++e) dn = __fadd_rn(dn, exp_p(__fsub_rn(el[e * heads + h], mx)));
+  for (int64_t e = b; e < e1; ++e) alpha[e * heads + h] = __fdiv_rn(exp_p(__fsub_rn(el[e * heads + h], mx)), dn);
+  m[tid] = mx;
+  den[tid] = dn;
+}
+
+// ④ edge softmax, heavy rows: block per row
+__global__ void __launch_bounds__(256) k_out_softmax_heavy(GraphDev g, int heads, const int32_t* __restrict__ hin,
+                                                           const int32_t* counts, const float* __restrict__ el,
+                                                           float* __restrict__ m, float* __restrict__ den,
+                                                           float* __restrict__ alpha) {
+  __shared__ float part[OUT_PART];
+  __shared__ float red[32];
+  __shared__ float mh[32], dh[32];
+  for (int i = blockIdx.x; i < counts[0]; i += gridDim.x) {
+    const int64_t v = hin[i];
+    const int64_t b = g.in_ptr[v], len = g.in_ptr[v + 1] - b;
+    for (int h = 0; h < heads; ++h) {
+      float mx = -INFINITY;
+      for (int64_t k = threadIdx.x; k < len; k += blockDim.x) mx = fmaxf(mx, el[(b + k) * heads + h]);
+      mx = block_max(mx, red);
+      if (threadIdx.x == 0) mh[h] = mx;
+    }
+    __syncthreads();
+    heavy_row_sums(len, g.chunk, heads,
+                   [&](float acc, int64_t k, int h) {
+                     return __fadd_rn(acc, exp_p(__fsub_rn(el[(b + k) * heads + h], mh[h])));
+                   }, part, dh);
+    for (int64_t it = threadIdx.x; it < len * heads; it += blockDim.x) {
+      const int h = (int)(it % heads);
+      const int64_t e = b + it / heads;
+      alpha[e * heads + h] = __fdiv_rn(exp_p(__fsub_rn(el[e * heads + h], mh[h])), dh[h]);
+    }
+    if (threadIdx.x < heads) {
+      m[v * heads + threadIdx.x] = mh[threadIdx.x];
+      den[v * heads + threadIdx.x] = dh[threadIdx.x];
+    }
+    __syncthreads();
   }
 }
 
-// ⑤ + head mean + bias: warp per destination row; column j of head h = j / C sums
-// Σᶜ fmaf(α[e,h], H′[u,j]) over the in-edges (R14), then logits = ((Σ_h agg) / heads) + b.
-constexpr int OUT_MAXHC = 1024;
-__global__ void __launch_bounds__(256) k_out_agg(GraphDev g, int heads, int C, const float* __restrict__ alpha,
-                                                 const float* __restrict__ Hp, const float* __restrict__ bias,
-                                                 float* __restrict__ logits) {
-  extern __shared__ float sh[];
-  const int HC = heads * C;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* agg = sh + warp * HC;
+// Column sums of rows gathered along a CSR row: out[v, j] = Σᶜ over the row's list positions p of
+// fmaf(w(p, h(j)), X[r(p), c(j)]) with h = j / C, and c = j (IN: X = H′ rows of width HC, weights
+// α[e,h], r = in_src) or c = j % C (OUT: X = G rows of width C, weights α[out_eid,h], r = out_dst).
+template <bool OUT>
+struct GatherRow {
+  const int64_t* ptr; const int32_t* idx; const int32_t* eid;
+  const float* alpha; const float* X; int heads, C, HC, ldx;
+  __device__ __forceinline__ int64_t edge(int64_t p) const { return OUT ? (int64_t)eid[p] : p; }
+  __device__ __forceinline__ int col(int j) const { return OUT ? j % C : j; }
+};
+
+// light rows: warp per row, NC columns per lane (j = lane + 32 t)
+template <bool OUT, int NC>
+__global__ void __launch_bounds__(256) k_out_gather_light(GatherRow<OUT> R, int64_t n, int chunk,
+                                                          float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t v = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; v < g.n_local; v += nw) {
-    const int64_t b = g.in_ptr[v], e1 = g.in_ptr[v + 1];
-    for (int j = lane; j < HC; j += 32) {
-      const int h = j / C;
-      CSum cs; cs.init();
-      int left = g.chunk;
-      for (int64_t e = b; e < e1; ++e) {
-        if (left == 0) { cs.fold(); left = g.chunk; }
-        cs.part = __fmaf_rn(alpha[e * heads + h], Hp[(int64_t)g.in_src[e] * HC + j], cs.part);
-        --left;
+  int h[NC], c[NC];
+  bool ok[NC];
+#pragma unroll
+  for (int t = 0; t < NC; ++t) {
+    const int j = lane + 32 * t;
+    ok[t] = j < R.HC;
+    h[t] = ok[t] ? j / R.C : 0;
+    c[t] = ok[t] ? R.col(j) : 0;
+  }
+  for (int64_t v = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); v < n; v += nw) {
+    const int64_t b = R.ptr[v], e1 = R.ptr[v + 1];
+    if (e1 - b > chunk) continue;
+    float acc[NC];
+#pragma unroll
+    for (int t = 0; t < NC; ++t) acc[t] = 0.0f;
+#pragma unroll 4
+    for (int64_t p = b; p < e1; ++p) {
+      const int64_t e = R.edge(p);
+      const float* xr = R.X + (int64_t)R.idx[p] * R.ldx;
+#pragma unroll
+      for (int t = 0; t < NC; ++t)
+        if (ok[t]) acc[t] = __fmaf_rn(R.alpha[e * R.heads + h[t]], xr[c[t]], acc[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < NC; ++t)
+      if (ok[t]) out[v * R.HC + lane + 32 * t] = acc[t];
+  }
+}
+
+// heavy rows: block per (row, 32-column slab); warps compute chunk partials, lane = column
+template <bool OUT>
+__global__ void __launch_bounds__(256) k_out_gather_heavy(GatherRow<OUT> R, const int32_t* __restrict__ hrows,
+                                                          const int32_t* count, int chunk, float* __restrict__ out) {
+  constexpr int PASS = 64;
+  __shared__ float part[PASS][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int nslab = (R.HC + 31) / 32;
+  for (int64_t item = blockIdx.x; item < (int64_t)count[0] * nslab; item += gridDim.x) {
+    const int64_t v = hrows[item / nslab];
+    const int j = (int)(item % nslab) * 32 + lane;
+    const bool ok = j < R.HC;
+    const int h = ok ? j / R.C : 0, c = ok ? R.col(j) : 0;
+    const int64_t b = R.ptr[v], len = R.ptr[v + 1] - b;
+    const int64_t nch = (len + chunk - 1) / chunk;
+    float total = 0.0f;
+    for (int64_t c0 = 0; c0 < nch; c0 += PASS) {
+      const int64_t nc = min((int64_t)PASS, nch - c0);
+      for (int64_t k = warp; k < nc; k += nwarp) {
+        const int64_t p0 = b + (c0 + k) * chunk, p1 = min(b + len, p0 + chunk);
+        float acc = 0.0f;
+        if (ok) {
+#pragma unroll 4
+          for (int64_t p = p0; p < p1; ++p)
+            acc = __fmaf_rn(R.alpha[R.edge(p) * R.heads + h], R.X[(int64_t)R.idx[p] * R.ldx + c], acc);
+        }
+        part[k][lane] = acc;
       }
-      agg[j] = cs.finish(e1 - b);
+      __syncthreads();
+      if (warp == 0)
+        for (int64_t k = 0; k < nc; ++k) total = (c0 + k == 0) ? part[k][lane] : __fadd_rn(total, part[k][lane]);
+      __syncthreads();
     }
-    __syncwarp();
-    for (int c = lane; c < C; c += 32) {
-      float t = agg[c];
-      for (int h = 1; h < heads; ++h) t = __fadd_rn(t, agg[h * C + c]);
-      t = __fdiv_rn(t, (float)heads);
-      logits[v * C + c] = __fadd_rn(t, bias[c]);
+    if (warp == 0 && ok) out[v * R.HC + j] = total;
+  }
+}
+
+template <bool OUT>
+static cudaError_t launch_gather(const GatherRow<OUT>& R, int64_t n, int chunk, const int32_t* hrows,
+                                 const int32_t* count, float* out, cudaStream_t st) {
+  const int nc = (R.HC + 31) / 32;
+  const int grid = grid_1d(n, 8);
+  {
+    ProfScope ps(OUT ? "out_dhp_light" : "out_agg_light", st);
+    switch (nc) {
+      case 1: k_out_gather_light<OUT, 1><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
+      case 2: k_out_gather_light<OUT, 2><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
+      case 3: k_out_gather_light<OUT, 3><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
+      case 4: k_out_gather_light<OUT, 4><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
+      case 5: k_out_gather_light<OUT, 5><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
+      case 6: k_out_gather_light<OUT, 6><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
+      case 7: k_out_gather_light<OUT, 7><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
+      case 8: k_out_gather_light<OUT, 8><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
+      default: k_out_gather_light<OUT, 32><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
     }
-    __syncwarp();
+  }
+  {
+    ProfScope ps(OUT ? "out_dhp_heavy" : "out_agg_heavy", st);
+    k_out_gather_heavy<OUT><<<num_sms() * 4, 256, 0, st>>>(R, hrows, count, chunk, out);
+  }
+  return cudaGetLastError();
+}
+
+// logits[v,c] = ((Σ_h agg[v,h,c], head order) / heads) + bias[c]
+__global__ void k_out_logits(const float* __restrict__ agg, int64_t n, int heads, int C, const float* __restrict__ bias,
+                             float* __restrict__ logits) {
+  const int HC = heads * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * C; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / C;
+    const int c = (int)(i % C);
+    float t = agg[v * HC + c];
+    for (int h = 1; h < heads; ++h) t = __fadd_rn(t, agg[v * HC + h * C + c]);
+    logits[i] = __fadd_rn(__fdiv_rn(t, (float)heads), bias[c]);
   }
 }
 
@@ -395,50 +598,121 @@ __global__ void k_out_g(const float* __restrict__ dz, int64_t count, float heads
     G[i] = __fdiv_rn(dz[i], heads);
 }
 
-// ⑤″ in FP32: ∂α[e,h] = Σ_c fmaf(G[v,c], H′[u,h,c]) sequential in c
-__global__ void k_out_dalpha(GraphDev g, int heads, int C, const float* __restrict__ G, const float* __restrict__ Hp,
-                             float* __restrict__ dalpha) {
+// ⑤″ in FP32: ∂α[e,h] = Σ_c fmaf(G[v,c], H′[u,h,c]) sequential in c; thread per (edge, head)
+__global__ void k_out_dalpha(int64_t e_in, int heads, int C, const int32_t* __restrict__ in_src,
+                             const int32_t* __restrict__ in_dst, const float* __restrict__ G,
+                             const float* __restrict__ Hp, float* __restrict__ dalpha) {
+  const int HC = heads * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e_in * heads;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / heads;
+    const int h = (int)(i % heads);
+    const float* gv = G + (int64_t)in_dst[e] * C;
+    const float* hu = Hp + (int64_t)in_src[e] * HC + (int64_t)h * C;
+    float acc = 0.0f;
+#pragma unroll 8
+    for (int c = 0; c < C; ++c) acc = __fmaf_rn(gv[c], hu[c], acc);
+    dalpha[i] = acc;
+  }
+}
+
+// ④′ + LeakyReLU′ + ③″ (∂D over in-edges), light rows: thread per (row, head)
+__global__ void k_out_sbwd_light(GraphDev g, int heads, const float* __restrict__ alpha,
+                                 const float* __restrict__ dalpha, const float* __restrict__ e_pre, float slope,
+                                 float* __restrict__ P, float* __restrict__ dEp, float* __restrict__ dD) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (tid >= g.n_local * heads) return;
   const int64_t v = tid / heads;
   const int h = (int)(tid % heads);
-  const int HC = heads * C;
-  const float* gv = G + v * C;
-  for (int64_t e = g.in_ptr[v]; e < g.in_ptr[v + 1]; ++e) {
-    const float* hu = Hp + (int64_t)g.in_src[e] * HC + (int64_t)h * C;
-    float acc = 0.0f;
-    for (int c = 0; c < C; ++c) acc = __fmaf_rn(gv[c], hu[c], acc);
-    dalpha[e * heads + h] = acc;
+  const int64_t b = g.in_ptr[v], e1 = g.in_ptr[v + 1];
+  if (e1 - b > g.chunk) return;
+  float p = 0.0f;
+  for (int64_t e = b; e < e1; ++e) p = __fmaf_rn(dalpha[e * heads + h], alpha[e * heads + h], p);
+  float dd = 0.0f;
+  for (int64_t e = b; e < e1; ++e) {
+    const int64_t k = e * heads + h;
+    const float dE = __fmul_rn(alpha[k], __fsub_rn(dalpha[k], p));
+    const float x = e_pre[k] > 0.0f ? dE : __fmul_rn(dE, slope);
+    dEp[k] = x;
+    dd = __fadd_rn(dd, x);
+  }
+  P[tid] = p;
+  dD[tid] = dd;
+}
+
+__global__ void __launch_bounds__(256) k_out_sbwd_heavy(GraphDev g, int heads, const int32_t* __restrict__ hin,
+                                                        const int32_t* counts, const float* __restrict__ alpha,
+                                                        const float* __restrict__ dalpha,
+                                                        const float* __restrict__ e_pre, float slope,
+                                                        float* __restrict__ P, float* __restrict__ dEp,
+                                                        float* __restrict__ dD) {
+  __shared__ float part[OUT_PART];
+  __shared__ float ph[32], dh[32];
+  for (int i = blockIdx.x; i < counts[0]; i += gridDim.x) {
+    const int64_t v = hin[i];
+    const int64_t b = g.in_ptr[v], len = g.in_ptr[v + 1] - b;
+    heavy_row_sums(len, g.chunk, heads,
+                   [&](float acc, int64_t k, int h) {
+                     return __fmaf_rn(dalpha[(b + k) * heads + h], alpha[(b + k) * heads + h], acc);
+                   }, part, ph);
+    for (int64_t it = threadIdx.x; it < len * heads; it += blockDim.x) {
+      const int64_t k = b * heads + it;
+      const int h = (int)(it % heads);
+      const float dE = __fmul_rn(alpha[k], __fsub_rn(dalpha[k], ph[h]));
+      dEp[k] = e_pre[k] > 0.0f ? dE : __fmul_rn(dE, slope);
+    }
+    __syncthreads();
+    heavy_row_sums(len, g.chunk, heads,
+                   [&](float acc, int64_t k, int h) { return __fadd_rn(acc, dEp[(b + k) * heads + h]); }, part, dh);
+    if (threadIdx.x < heads) {
+      P[v * heads + threadIdx.x] = ph[threadIdx.x];
+      dD[v * heads + threadIdx.x] = dh[threadIdx.x];
+    }
+    __syncthreads();
   }
 }
 
-// ⑤′ + ②′ in FP32: warp per source row u; ∂H′_agg[u,j] = Σᶜ over out-edges fmaf(α[eid,h], G[v,c]),
-// ∂H′ = (∂H′_agg + ∂S·a_src) + ∂D·a_dst (R23)
-__global__ void __launch_bounds__(256) k_out_dhp(GraphDev g, int heads, int C, const float* __restrict__ alpha,
-                                                 const float* __restrict__ G, const float* __restrict__ dS,
-                                                 const float* __restrict__ dD, const float* __restrict__ a_src,
-                                                 const float* __restrict__ a_dst, float* __restrict__ dHp) {
+// ③′ ∂S over out-edges (out order, edge values by out_eid): light thread per (row, head), heavy block per row
+__global__ void k_out_dS_light(GraphDev g, int heads, const float* __restrict__ dEp, float* __restrict__ dS) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid >= g.n_local * heads) return;
+  const int64_t u = tid / heads;
+  const int h = (int)(tid % heads);
+  const int64_t b = g.out_ptr[u], e1 = g.out_ptr[u + 1];
+  if (e1 - b > g.chunk) return;
+  float s = 0.0f;
+  for (int64_t p = b; p < e1; ++p) s = __fadd_rn(s, dEp[(int64_t)g.out_eid[p] * heads + h]);
+  dS[tid] = s;
+}
+__global__ void __launch_bounds__(256) k_out_dS_heavy(GraphDev g, int heads, const int32_t* __restrict__ hout,
+                                                      const int32_t* counts, const float* __restrict__ dEp,
+                                                      float* __restrict__ dS) {
+  __shared__ float part[OUT_PART];
+  __shared__ float sh[32];
+  for (int i = blockIdx.x; i < counts[1]; i += gridDim.x) {
+    const int64_t u = hout[i];
+    const int64_t b = g.out_ptr[u], len = g.out_ptr[u + 1] - b;
+    heavy_row_sums(len, g.chunk, heads,
+                   [&](float acc, int64_t k, int h) {
+                     return __fadd_rn(acc, dEp[(int64_t)g.out_eid[b + k] * heads + h]);
+                   }, part, sh);
+    if (threadIdx.x < heads) dS[u * heads + threadIdx.x] = sh[threadIdx.x];
+    __syncthreads();
+  }
+}
+
+// ②′: ∂H′ = (∂H′_agg + ∂S·a_src) + ∂D·a_dst (R23), in place on the aggregated buffer
+__global__ void k_out_dhp_combine(float* __restrict__ dHp, int64_t n, int heads, int C, const float* __restrict__ dS,
+                                  const float* __restrict__ dD, const float* __restrict__ a_src,
+                                  const float* __restrict__ a_dst) {
   const int HC = heads * C;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; u < g.n_local; u += nw) {
-    const int64_t b = g.out_ptr[u], e1 = g.out_ptr[u + 1];
-    for (int j = lane; j < HC; j += 32) {
-      const int h = j / C, c = j - h * C;
-      CSum cs; cs.init();
-      int left = g.chunk;
-      for (int64_t p = b; p < e1; ++p) {
-        if (left == 0) { cs.fold(); left = g.chunk; }
-        const int64_t eid = g.out_eid[p];
-        cs.part = __fmaf_rn(alpha[eid * heads + h], G[(int64_t)g.out_dst[p] * C + c], cs.part);
-        --left;
-      }
-      const float agg = cs.finish(e1 - b);
-      const float t1 = __fmul_rn(dS[u * heads + h], a_src[j]);
-      const float t2 = __fadd_rn(agg, t1);
-      const float t3 = __fmul_rn(dD[u * heads + h], a_dst[j]);
-      dHp[u * HC + j] = __fadd_rn(t2, t3);
-    }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * HC; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = i / HC;
+    const int j = (int)(i % HC), h = j / C;
+    const float t1 = __fmul_rn(dS[u * heads + h], a_src[j]);
+    const float t2 = __fadd_rn(dHp[i], t1);
+    const float t3 = __fmul_rn(dD[u * heads + h], a_dst[j]);
+    dHp[i] = __fadd_rn(t2, t3);
   }
 }
 
@@ -480,7 +754,7 @@ namespace {
 struct OutLayout {
   int64_t n, e, F, H, C, HC;
   size_t off_Hp, off_S, off_D, off_epre, off_el, off_alpha, off_m, off_den, off_G, off_dalpha, off_dEp, off_P,
-      off_dD, off_dS, off_dHp, off_ws, total;
+      off_dD, off_dS, off_dHp, off_agg, off_indst, off_hin, off_hout, off_cnt, off_ws, total;
 };
 inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 bool out_layout(const tango_graph* G, const tango_gat_out_params* p, OutLayout* L) {
@@ -507,6 +781,11 @@ bool out_layout(const tango_graph* G, const tango_gat_out_params* p, OutLayout* 
   L->off_dD = take(4 * n * H);
   L->off_dS = take(4 * n * H);
   L->off_dHp = take(4 * n * HC);
+  L->off_agg = take(4 * n * HC);
+  L->off_indst = take(4 * e);
+  L->off_hin = take(4 * n);
+  L->off_hout = take(4 * n);
+  L->off_cnt = take(4 * 8);
   size_t ws = sgemm_ws_bytes(F, HC, n);
   ws = std::max(ws, sgemm_ws_bytes(n, F, HC));
   ws = std::max(ws, colsum_ws_bytes(n, L->C));
@@ -677,23 +956,42 @@ tango_status tango_gat_out_fwd(const tango_graph* G, const tango_gat_out_params*
   float* m = reinterpret_cast<float*>(c + L.off_m);
   float* den = reinterpret_cast<float*>(c + L.off_den);
   float* ws = reinterpret_cast<float*>(c + L.off_ws);
+  float* agg = reinterpret_cast<float*>(c + L.off_agg);
+  int32_t* in_dst = reinterpret_cast<int32_t*>(c + L.off_indst);
+  int32_t* hin = reinterpret_cast<int32_t*>(c + L.off_hin);
+  int32_t* hout = reinterpret_cast<int32_t*>(c + L.off_hout);
+  int32_t* cnt = reinterpret_cast<int32_t*>(c + L.off_cnt);
   const GraphDev g = dev_graph(G);
   const int H_ = (int)L.H, C_ = (int)L.C;
+  // plan: in-CSR destinations, heavy rows (degree > C_E) of both CSRs
+  M_TRY_CUDA(cudaMemsetAsync(cnt, 0, 8 * sizeof(int32_t), stream));
+  {
+    ProfScope ps("out_plan", stream);
+    k_out_plan<<<grid_1d(L.n, 8), 256, 0, stream>>>(g, in_dst, hin, hout, cnt);
+  }
   // ① H′ = H·W (R33)
   M_TRY_CUDA(launch_sgemm(H, L.F, false, p->W, L.HC, false, L.n, L.HC, L.F, Hp, ws, stream));
   {
     ProfScope ps("out_sd", stream);
     k_out_sd<<<(unsigned)((L.n * H_ + 255) / 256), 256, 0, stream>>>(Hp, L.n, H_, C_, p->a_src, p->a_dst, S, D);
   }
-  {
+  if (L.e > 0) {
     ProfScope ps("out_el", stream);
-    k_out_el<<<(unsigned)((L.n * H_ + 255) / 256), 256, 0, stream>>>(g, H_, S, D, p->neg_slope, epre, el);
+    k_out_el<<<grid_1d(L.e), 256, 0, stream>>>(L.e, H_, G->in_src, in_dst, S, D, p->neg_slope, epre, el);
   }
-  M_TRY_CUDA(launch_edge_softmax(g, H_, el, m, den, alpha, stream));
   {
-    ProfScope ps("out_agg", stream);
-    const size_t smem = 8 * sizeof(float) * (size_t)L.HC;
-    k_out_agg<<<grid_1d(L.n, 8), 256, smem, stream>>>(g, H_, C_, alpha, Hp, p->bias, logits);
+    ProfScope ps("out_softmax_light", stream);
+    k_out_softmax_light<<<(unsigned)((L.n * H_ + 255) / 256), 256, 0, stream>>>(g, H_, el, m, den, alpha);
+  }
+  {
+    ProfScope ps("out_softmax_heavy", stream);
+    k_out_softmax_heavy<<<num_sms() * 2, 256, 0, stream>>>(g, H_, hin, cnt, el, m, den, alpha);
+  }
+  GatherRow<false> R{G->in_ptr, G->in_src, nullptr, alpha, Hp, H_, C_, (int)L.HC, (int)L.HC};
+  M_TRY_CUDA(launch_gather<false>(R, L.n, g.chunk, hin, cnt, agg, stream));
+  {
+    ProfScope ps("out_logits", stream);
+    k_out_logits<<<grid_1d(L.n * L.C), 256, 0, stream>>>(agg, L.n, H_, C_, p->bias, logits);
   }
   M_TRY_CUDA(cudaGetLastError());
   return TANGO_OK;
@@ -735,16 +1033,37 @@ tango_status tango_gat_out_bwd(const tango_graph* G, const tango_gat_out_params*
     ProfScope ps("out_g", stream);
     k_out_g<<<grid_1d(L.n * L.C), 256, 0, stream>>>(dlogits, L.n * L.C, (float)H_, Gm);
   }
-  {
+  int32_t* in_dst = reinterpret_cast<int32_t*>(c + L.off_indst);
+  int32_t* hin = reinterpret_cast<int32_t*>(c + L.off_hin);
+  int32_t* hout = reinterpret_cast<int32_t*>(c + L.off_hout);
+  int32_t* cnt = reinterpret_cast<int32_t*>(c + L.off_cnt);
+  if (L.e > 0) {
     ProfScope ps("out_dalpha", stream);
-    k_out_dalpha<<<(unsigned)((L.n * H_ + 255) / 256), 256, 0, stream>>>(g, H_, C_, Gm, Hp, dalpha);
+    k_out_dalpha<<<grid_1d(L.e * H_), 256, 0, stream>>>(L.e, H_, C_, G->in_src, in_dst, Gm, Hp, dalpha);
   }
-  M_TRY_CUDA(launch_softmax_bwd(g, H_, alpha, dalpha, epre, p->neg_slope, P, dEp, stream));
-  M_TRY_CUDA(launch_edge_sum(g, 0, H_, dEp, dD, stream));
-  M_TRY_CUDA(launch_edge_sum(g, 1, H_, dEp, dS, stream));
   {
-    ProfScope ps("out_dhp", stream);
-    k_out_dhp<<<grid_1d(L.n, 8), 256, 0, stream>>>(g, H_, C_, alpha, Gm, dS, dD, p->a_src, p->a_dst, dHp);
+    ProfScope ps("out_sbwd_light", stream);
+    k_out_sbwd_light<<<(unsigned)((L.n * H_ + 255) / 256), 256, 0, stream>>>(g, H_, alpha, dalpha, epre,
+                                                                               p->neg_slope, P, dEp, dD);
+  }
+  {
+    ProfScope ps("out_sbwd_heavy", stream);
+    k_out_sbwd_heavy<<<num_sms() * 2, 256, 0, stream>>>(g, H_, hin, cnt, alpha, dalpha, epre, p->neg_slope, P, dEp,
+                                                        dD);
+  }
+  {
+    ProfScope ps("out_dS_light", stream);
+    k_out_dS_light<<<(unsigned)((L.n * H_ + 255) / 256), 256, 0, stream>>>(g, H_, dEp, dS);
+  }
+  {
+    ProfScope ps("out_dS_heavy", stream);
+    k_out_dS_heavy<<<num_sms() * 2, 256, 0, stream>>>(g, H_, hout, cnt, dEp, dS);
+  }
+  GatherRow<true> R{G->out_ptr, G->out_dst, G->out_eid, alpha, Gm, H_, C_, (int)L.HC, C_};
+  M_TRY_CUDA(launch_gather<true>(R, L.n, g.chunk, hout, cnt + 1, dHp, stream));
+  {
+    ProfScope ps("out_dhp_combine", stream);
+    k_out_dhp_combine<<<grid_1d(L.n * L.HC), 256, 0, stream>>>(dHp, L.n, H_, C_, dS, dD, p->a_src, p->a_dst);
   }
   {
     ProfScope ps("out_da", stream);
@@ -778,6 +1097,7 @@ tango_status tango_gat_out_ctx_get_view(const tango_graph* G, const tango_gat_ou
   view->dD = reinterpret_cast<float*>(c + L.off_dD);
   view->dS = reinterpret_cast<float*>(c + L.off_dS);
   view->dHp = reinterpret_cast<float*>(c + L.off_dHp);
+  view->agg = reinterpret_cast<float*>(c + L.off_agg);
   return TANGO_OK;
 }
 

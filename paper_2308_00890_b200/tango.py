@@ -75,7 +75,7 @@ class GatOutParams(C.Structure):
                 ("heads", C.c_int32), ("classes", C.c_int32), ("neg_slope", C.c_float)]
 
 
-_OUT_VIEW = ("Hp", "S", "D", "e_pre", "alpha", "m", "den", "G", "dalpha", "dE_pre", "P", "dD", "dS", "dHp")
+_OUT_VIEW = ("Hp", "S", "D", "e_pre", "alpha", "m", "den", "G", "dalpha", "dE_pre", "P", "dD", "dS", "dHp", "agg")
 
 
 class GatOutCtxView(C.Structure):
@@ -689,7 +689,7 @@ class GATOutLayer:
         base = self.ctx.data_ptr()
         n, H, E, HC, Cc = self.graph.n_local, self.heads, self.graph.e_in, self.HC, self.classes
         shapes = dict(Hp=(n, HC), S=(n, H), D=(n, H), e_pre=(E, H), alpha=(E, H), m=(n, H), den=(n, H), G=(n, Cc),
-                      dalpha=(E, H), dE_pre=(E, H), P=(n, H), dD=(n, H), dS=(n, H), dHp=(n, HC))
+                      dalpha=(E, H), dE_pre=(E, H), P=(n, H), dD=(n, H), dS=(n, H), dHp=(n, HC), agg=(n, HC))
         out = {}
         for f, shp in shapes.items():
             off = getattr(v, f) - base

@@ -96,6 +96,7 @@ OUT_CASES = [
     ((1000, 4000, 2, True), 100, 4, 40, 7),
     ((500, 900, 5, False), 48, 1, 7, 256),
     ((2000, 20000, 6, True), 512, 4, 40, 64),
+    ((3000, 30000, 9, True), 64, 8, 100, 5),   # HC = 800 (> 8 columns per lane), chunk 5: most rows heavy
 ]
 
 
@@ -123,6 +124,7 @@ def test_gat_out_layer_parity(T, orc, gspec, F, heads, C, chunk):
     eq("alpha", v["alpha"], f["alpha"])
     eq("m", v["m"], f["m"])
     eq("den", v["den"], f["den"])
+    eq("agg", v["agg"], f["agg"])
     eq("logits", logits, f["logits"])
     eq("G", v["G"], bo["G"])
     eq("dalpha", v["dalpha"], bo["dalpha"])
