@@ -161,6 +161,7 @@ def train_step_bench(T, torch, dg, g, F, H, D, args, l2_flush):
     torch.cuda.synchronize()
     model.check_status()
     T.profile_enable(True)
+    T.profile_serialize(True)
     T.profile_read(reset=True)
     for i in range(args.steps):
         l2_flush.zero_()
@@ -168,6 +169,7 @@ def train_step_bench(T, torch, dg, g, F, H, D, args, l2_flush):
     torch.cuda.synchronize()
     prof = T.profile_read(reset=True)
     T.profile_enable(False)
+    T.profile_serialize(False)
     graph = torch.cuda.CUDAGraph()
     cs = torch.cuda.Stream()
     cs.wait_stream(torch.cuda.current_stream())
@@ -310,6 +312,7 @@ def main():
     # (ProfScope, on the launching stream); gives the per-kernel times, the dominant kernel's
     # roofline and the launch count per step.  L2 flushed before every step.
     T.profile_enable(True)
+    T.profile_serialize(True)     # per-kernel pass: side-stream work in order, each launch timed alone
     T.profile_read(reset=True)
     torch.cuda.synchronize()
     launches0 = T.launch_count()
@@ -320,6 +323,7 @@ def main():
     launches_per_step = (T.launch_count() - launches0) / args.steps
     prof = T.profile_read(reset=True)
     T.profile_enable(False)
+    T.profile_serialize(False)
 
     # ---------------- timed region: K steps replayed from one CUDA graph (fwd + bwd of the layer,
     # captured once: no host launch gaps), L2 flushed between steps, CUDA events per step
@@ -514,7 +518,7 @@ def main():
                 "gpu_launches": int(launches_t.item()), "clocks": clk, "kernel_ms": breakdown, "kernel_ms_per_step": per_step,
                 "train_step": train,
                 "timing": "value: CUDA-graph replay of fwd+bwd per step (events per step, L2 flushed between "
-                          "steps); kernel_ms/roofline: eager pass with events around every launch "
+                          "steps); kernel_ms/roofline: eager pass, side-stream work serialised, events around every launch "
                           f"(sum of kernel times {eager_ms:.3f} ms/step)"}
         print(json.dumps(line), flush=True)
     if comm is not None:

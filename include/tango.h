@@ -393,6 +393,10 @@ tango_status tango_profile_collect(void);          /* waits for the recorded eve
 int32_t tango_profile_num_entries(void);
 tango_status tango_profile_entry(int32_t i, char* name, int32_t name_cap, double* total_ms, int64_t* launches);
 void tango_profile_reset(void);
+/* on != 0: layer calls run their side-stream work (Q(W), graph plans, hub-row chains, the ∂a
+ * reduction) in order on the caller's stream instead, so that per-launch event times measure each
+ * kernel alone (bench.py's per-kernel pass).  Results are identical either way.  Process-wide. */
+void tango_profile_serialize(int32_t on);
 
 #ifdef __cplusplus
 }

@@ -8,6 +8,7 @@
 #include <vector>
 #include <mutex>
 #include <condition_variable>
+#include <atomic>
 
 #include "../../include/tango.h"
 #include "kernels.h"
@@ -24,6 +25,9 @@ int num_sms() {
   }
   return n;
 }
+
+// tango_profile_serialize (see aux_stream)
+static std::atomic<int> g_serialize{0};
 
 static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -116,6 +120,8 @@ const char* tango_status_string(tango_status s) {
 
 int tango_abi_version(void) { return TANGO_ABI_VERSION; }
 
+void tango_profile_serialize(int32_t on) { g_serialize.store(on ? 1 : 0, std::memory_order_relaxed); }
+
 tango_status tango_status_poll(const int32_t* dev_status, cudaStream_t stream, tango_status* out) {
   if (!dev_status || !out) return TANGO_ERR_INVALID_ARG;
   int32_t v = 0;
@@ -157,10 +163,21 @@ struct AuxStream {
   cudaEvent_t ev[10] = {};
   SideStream side(int k) const { return SideStream{s, ev[k], ev[k + 1]}; }
 };
-static AuxStream* aux_stream() {
+// tango_profile_serialize(1): the side-stream work runs in order on the caller's stream, so that
+// per-launch event times (tango_profile_*) measure each kernel alone.
+static AuxStream* aux_stream(cudaStream_t st) {
   thread_local AuxStream per_dev[16];
+  thread_local AuxStream serial[16];
   int d = 0;
   if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 16) return nullptr;
+  if (g_serialize.load(std::memory_order_relaxed)) {
+    AuxStream& a = serial[d];
+    if (!a.ev[0])
+      for (auto& e : a.ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    a.s = st;
+    return &a;
+  }
   AuxStream& a = per_dev[d];
   if (!a.s) {
     int lo = 0, hi = 0;   // highest priority: the latency-bound hub chain gets SM slots first
@@ -606,7 +623,7 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
 
   TRY_CUDA(cudaMemsetAsync(sc, 0, SL_NSLOTS * 4, st));
   // side stream: F2 Q(W) and the in-CSR segment plan (graph only) run beside F1
-  AuxStream* aux = aux_stream();
+  AuxStream* aux = aux_stream(st);
   if (!aux) return TANGO_ERR_CUDA;
   const PlanDev pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in, L.off_pin_tiles, L.tcap);
   TRY_CUDA(stream_after(aux->s, st, aux->ev[0]));
@@ -720,7 +737,7 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   TRY_CUDA(cudaMemsetAsync(da_src, 0, L.HD * 4, st));
   TRY_CUDA(cudaMemsetAsync(da_dst, 0, L.HD * 4, st));
   TRY_CUDA(cudaMemsetAsync(dW64, 0, L.F * L.HD * 8, st));
-  AuxStream* aux = aux_stream();
+  AuxStream* aux = aux_stream(st);
   if (!aux) return TANGO_ERR_CUDA;
   {
     const PlanDev pout = plan_of(c, L.off_pout_hbase, L.off_pout_hseg, L.off_pout_hrow, L.off_pout_cnt, L.cap_out,

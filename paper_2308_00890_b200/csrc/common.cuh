@@ -88,11 +88,37 @@ __device__ __forceinline__ float sr_kf(const SR8& s, int j) {
 __device__ __forceinline__ uint32_t pack4_low_bytes(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
   return __byte_perm(__byte_perm(b0, b1, 0x0040u), __byte_perm(b2, b3, 0x0040u), 0x5410u);
 }
+// Packed-pair form of sr_qbits on the f32x2 pipes (FMUL2 / FADD2 / FFMA2 with the same rounding
+// modes, one instruction per two elements): identical results element by element.
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void sr_qbits2(float x0, float x1, float r, float kf0, float kf1, int qmax, uint32_t& q0,
+                                          uint32_t& q1) {
+  const uint64_t M = pk2(12582912.0f, 12582912.0f), R = pk2(r, r), K = pk2(kf0, kf1);
+  const uint64_t S = pk2(65536.0f, 65536.0f), T23 = pk2(8388608.0f, 8388608.0f);
+  uint64_t xs, t, f, fr, rhs, d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(xs) : "l"(pk2(x0, x1)), "l"(R));
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(t) : "l"(xs), "l"(M));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f) : "l"(t), "l"(M));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(fr) : "l"(xs), "l"(f));
+  asm("fma.rp.f32x2 %0, %1, %2, %3;" : "=l"(rhs) : "l"(fr), "l"(S), "l"(T23));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(K), "l"(rhs));
+  const uint32_t t0 = (uint32_t)t, t1 = (uint32_t)(t >> 32);
+  const uint32_t u0 = (uint32_t)d >> 31, u1 = (uint32_t)(d >> 63);
+  int a0 = (int)(t0 + u0), a1 = (int)(t1 + u1);
+  a0 = min(max(a0, 0x4B400000 - qmax), 0x4B400000 + qmax);
+  a1 = min(max(a1, 0x4B400000 - qmax), 0x4B400000 + qmax);
+  q0 = (uint32_t)a0;
+  q1 = (uint32_t)a1;
+}
 // SR of 8 consecutive elements sharing one Philox draw -> 8 codes packed little-endian
 __device__ __forceinline__ uint2 sr_quant8(const float (&v)[8], float r, const SR8& rnd, int qmax) {
   uint32_t b[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) b[k] = sr_qbits(v[k], r, sr_kf(rnd, k), qmax);
+  for (int k = 0; k < 8; k += 2) sr_qbits2(v[k], v[k + 1], r, sr_kf(rnd, k), sr_kf(rnd, k + 1), qmax, b[k], b[k + 1]);
   return make_uint2(pack4_low_bytes(b[0], b[1], b[2], b[3]), pack4_low_bytes(b[4], b[5], b[6], b[7]));
 }
 __device__ __forceinline__ int sr_quant(float x, float r, uint32_t hw16, int qmax) {

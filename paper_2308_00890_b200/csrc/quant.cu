@@ -72,10 +72,24 @@ __global__ void __launch_bounds__(256) k_quantize(const float* __restrict__ x, i
   const int64_t count = rows * cols;
   const int64_t blk0 = g0 >> 3, blk1 = (g0 + count + 7) >> 3;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-  const bool fast = (rowscale == nullptr) && (qt == nullptr) && ((g0 & 7) == 0) && ((cols & 7) == 0) &&
-                    ((ld & 7) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  const bool aligned = (rowscale == nullptr) && (qt == nullptr) && ((g0 & 7) == 0) && ((ld & 7) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && ((reinterpret_cast<uintptr_t>(q) & 7) == 0);
+  const bool fast = aligned && ((cols & 7) == 0);
   const bool dense = ld == cols;   // q[i*ld + j] = q[e]: no division in the fast loop
-  if (fast && dense) {   // streaming path: the next group's 32 bytes are loaded before this one is rounded
+  if (aligned && dense) {
+    // streaming path over the whole groups (any cols: the tensor is one flat run of codes); the
+    // next group's 32 bytes are loaded before this one is rounded.  A partial last group (count
+    // not a multiple of 8) is rounded element by element by one thread.
+    const int64_t full1 = blk0 + (count >> 3);
+    if ((count & 7) && tid == nthr - 1) {
+      const SR8 rnd = sr_draw8((uint64_t)full1, tag, step, key);
+      for (int k = 0; k < (int)(count & 7); ++k) {
+        const int64_t e = ((full1 << 3) - g0) + k;
+        const int qq = sr_quant(x[e], sc.r, sr_half(rnd, k), qmax);
+        q[e] = (int8_t)(qq ^ (int)(code_xor & 0xFFu));
+      }
+    }
+    const int64_t blk1 = full1;
     int64_t blk = blk0 + tid;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
     if (blk < blk1) {

@@ -95,7 +95,7 @@ EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tan
            "tango_comm_unique_id_bytes", "tango_comm_get_unique_id", "tango_comm_init", "tango_comm_destroy",
            "tango_comm_set_partition", "tango_local_group_create", "tango_local_group_destroy",
            "tango_comm_init_local", "tango_quant_error", "tango_select_bits", "tango_profile_enable", "tango_launch_count", "tango_profile_collect",
-           "tango_profile_num_entries", "tango_profile_entry", "tango_profile_reset",
+           "tango_profile_num_entries", "tango_profile_entry", "tango_profile_reset", "tango_profile_serialize",
            "tango_sgemm_workspace_bytes", "tango_sgemm", "tango_colsum_workspace_bytes", "tango_colsum",
            "tango_bias_act_fwd", "tango_bias_act_bwd", "tango_cross_entropy", "tango_sgd_update",
            "tango_gat_out_ctx_bytes", "tango_gat_out_fwd", "tango_gat_out_bwd", "tango_gat_out_ctx_get_view"]
@@ -149,6 +149,8 @@ def load(path: str = LIB_PATH):
     L.tango_profile_num_entries.restype = i32
     L.tango_profile_entry.argtypes = [i32, C.c_char_p, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     L.tango_profile_reset.restype = None
+    L.tango_profile_serialize.argtypes = [i32]
+    L.tango_profile_serialize.restype = None
     L.tango_sgemm_workspace_bytes.restype = sz
     L.tango_sgemm_workspace_bytes.argtypes = [i64, i64, i64]
     L.tango_sgemm.argtypes = [_P, i64, i32, _P, i64, i32, i64, i64, i64, _P, _P, sz, _P]
@@ -193,6 +195,11 @@ def ld32(cols: int) -> int:
 # ---------------------------------------------------------------------------------------- tracing
 def profile_enable(on: bool = True):
     load().tango_profile_enable(1 if on else 0)
+
+
+def profile_serialize(on: bool = True):
+    """Side-stream work in order on the caller's stream (per-kernel event times without overlap)."""
+    load().tango_profile_serialize(1 if on else 0)
 
 
 def launch_count() -> int:
