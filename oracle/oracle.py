@@ -80,6 +80,14 @@ _OUT_BWD_FIELDS = ["db", "G", "dalpha", "P", "dE", "dE_pre", "dD", "dS", "dHp_ag
                    "da_src_abs", "da_dst_abs", "dH", "dW"]
 
 
+class GcnOutFwdOut(C.Structure):
+    _fields_ = [(f, _P) for f in ("Y", "Ys", "agg", "logits")]
+
+
+class GcnOutBwdOut(C.Structure):
+    _fields_ = [(f, _P) for f in ("db", "Gs", "aggb", "dY", "dX", "dW")]
+
+
 class OutFwdOut(C.Structure):
     _fields_ = [(f, _P) for f in _OUT_FWD_FIELDS]
 
@@ -131,6 +139,9 @@ def lib():
                                       _P, C.POINTER(OutBwdOut)]
         L.orc_cross_entropy.argtypes = [_P, _P, C.c_int64, C.c_int32, C.c_int64, _P, _P, _P]
         L.orc_sgd.argtypes = [_P, _P, C.c_int64, C.c_float]
+        L.orc_spmm_alpha_unit.argtypes = [C.POINTER(Graph), C.c_int, C.c_int, _P, _P]
+        L.orc_gcn_out_fwd.argtypes = [C.POINTER(Graph), C.c_int, C.c_int, _P, _P, _P, C.POINTER(GcnOutFwdOut)]
+        L.orc_gcn_out_bwd.argtypes = [C.POINTER(Graph), C.c_int, C.c_int, _P, _P, _P, C.POINTER(GcnOutBwdOut)]
         L.orc_num_threads.restype = C.c_int
         L.orc_set_threads.argtypes = [C.c_int]
     return _lib
@@ -526,3 +537,68 @@ def gat_model_step(g, X, hidden, out, labels, lr, bits=8, seed=0x7A4E60, step=0,
     new_out = {**out, **{k: sgd(out[k], ogr[k], lr) for k in ("W", "a_src", "a_dst", "b")}}
     return dict(loss=loss, logits=fo["logits"], hs=hs, fwd=fws, out_fwd=fo, out_bwd=bo, bwd=bws, grads=grads,
                 out_grads=ogr, hidden=new_hidden, out=new_out)
+
+
+def gather_sum(g, direction, x, chunk=256):
+    """Unweighted fp32 chunked row gather (R14): in-edges (0) or out-edges (1)."""
+    gs = graph_struct(g, chunk)
+    x = _c(x, np.float32)
+    out = np.zeros((g.n, x.shape[1]), np.float32)
+    _check(lib().orc_spmm_alpha_unit(C.byref(gs), direction, x.shape[1], _p(x), _p(out)))
+    return out
+
+
+def gcn_out_fwd(g, X, W, bias, chunk=256):
+    """Full-precision final GCN layer (R26 norms, R35 bias)."""
+    n, F = X.shape
+    Cc = W.shape[1]
+    gs = graph_struct(g, chunk)
+    X, W, bias = (_c(a, np.float32) for a in (X, W, bias))
+    o = {k: np.zeros((n, Cc), np.float32) for k in ("Y", "Ys", "agg", "logits")}
+    st = GcnOutFwdOut(*[_p(o[k]) for k in ("Y", "Ys", "agg", "logits")])
+    _check(lib().orc_gcn_out_fwd(C.byref(gs), F, Cc, _p(X), _p(W), _p(bias), C.byref(st)))
+    o["_cfg"] = dict(F=F, C=Cc, chunk=chunk)
+    return o
+
+
+def gcn_out_bwd(g, fwd, X, W, dlogits, want_dX=True):
+    c = fwd["_cfg"]
+    n, F = X.shape
+    Cc = c["C"]
+    gs = graph_struct(g, c["chunk"])
+    X, W, dlogits = (_c(a, np.float32) for a in (X, W, dlogits))
+    o = dict(db=np.zeros(Cc, np.float32), Gs=np.zeros((n, Cc), np.float32), aggb=np.zeros((n, Cc), np.float32),
+             dY=np.zeros((n, Cc), np.float32), dX=np.zeros((n, F), np.float32) if want_dX else None,
+             dW=np.zeros((F, Cc), np.float32))
+    st = GcnOutBwdOut(*[_p(o[k]) for k in ("db", "Gs", "aggb", "dY", "dX", "dW")])
+    _check(lib().orc_gcn_out_bwd(C.byref(gs), F, Cc, _p(X), _p(W), _p(dlogits), C.byref(st)))
+    return o
+
+
+def gcn_model_step(g, X, hidden, out, labels, lr, bits=8, seed=0x7A4E60, step=0, chunk=256):
+    """One full-batch training step of a multi-layer GCN (NEXT-1): hidden layers l = 1..L-1 are the
+    quantized GCN layer (orc_gcn_fwd, layer_id = l) followed by bias + ReLU (R34); the final layer is
+    FP32 (gcn_out_fwd); cross-entropy (R36); backward in reverse; SGD on every FP32 master (R37).
+    hidden: [{W, b}], out: {W, b}."""
+    hs = [np.asarray(X, np.float32)]
+    fws = []
+    for l, p in enumerate(hidden, start=1):
+        f = gcn_fwd(g, hs[-1], p["W"], bits=bits, seed=seed, step=step, layer_id=l, chunk=chunk)
+        a, _ = bias_relu_fwd(f["out"], p["b"])
+        fws.append(f)
+        hs.append(a)
+    fo = gcn_out_fwd(g, hs[-1], out["W"], out["b"], chunk=chunk)
+    loss, dz, _ = cross_entropy(fo["logits"], labels)
+    bo = gcn_out_bwd(g, fo, hs[-1], out["W"], dz, want_dX=len(hidden) > 0)
+    grads = [None] * len(hidden)
+    dA = bo["dX"]
+    for i in range(len(hidden) - 1, -1, -1):
+        dx, db, _ = bias_relu_bwd(hs[i + 1], dA)
+        b = gcn_bwd(g, fws[i], hs[i], hidden[i]["W"], dx)
+        grads[i] = dict(W=b["dW"], b=db)
+        dA = b["dX"]
+    ogr = dict(W=bo["dW"], b=bo["db"])
+    new_hidden = [{**p, **{k: sgd(p[k], gr[k], lr) for k in ("W", "b")}} for p, gr in zip(hidden, grads)]
+    new_out = {**out, **{k: sgd(out[k], ogr[k], lr) for k in ("W", "b")}}
+    return dict(loss=loss, logits=fo["logits"], hs=hs, out_fwd=fo, out_bwd=bo, grads=grads, out_grads=ogr,
+                hidden=new_hidden, out=new_out)

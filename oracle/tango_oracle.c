@@ -346,6 +346,29 @@ int orc_spmm_alpha(const orc_graph* g, int dir, int heads, int cols, const float
   return st;
 }
 
+/* Unweighted fp32 row gather with the chunked order (R14), plain adds:
+ *   out[v,j] = Σᶜ_{e} x[w,j]  over in-edges (dir 0, w = source) or out-edges
+ *   (dir 1, w = destination) — the FP32 GCN aggregation (final layer, R35). */
+int orc_spmm_alpha_unit(const orc_graph* g, int dir, int cols, const float* x, float* out) {
+  orc_rev rv = {0};
+  if (dir == 1 && orc_build_rev(g, &rv)) return ORC_ERR_ALLOC;
+  for (int64_t v = 0; v < g->n; ++v) {
+    const int64_t* ptr = dir ? rv.ptr : g->in_ptr;
+    int64_t b = ptr[v], len = ptr[v + 1] - b;
+    for (int j = 0; j < cols; ++j) {
+      float total = 0.0f, part = 0.0f;
+      for (int64_t i = 0; i < len; ++i) {
+        int64_t w = dir ? rv.dst[b + i] : g->in_src[b + i];
+        csum_fold(&total, &part, i, g->chunk);
+        part = part + x[w * cols + j];
+      }
+      out[v * cols + j] = csum_finish(total, part, len, g->chunk);
+    }
+  }
+  if (dir == 1) orc_free_rev(&rv);
+  return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------- */
 /* ⑤″ SDDMM-dot directly on quantized values (§2.1):    */
 /*   ∂α[e,h] = (float)(Σ_d QV(A,v,h,d)·QV(B,u,h,d)) * (s_A*s_B)              */
@@ -1023,4 +1046,53 @@ void orc_sgd(float* w, const float* g, int64_t count, float lr) {
     float t = lr * g[i];
     w[i] = w[i] - t;
   }
+}
+
+/* Full-precision final GCN layer (P:604-615 FP32 rule; GCN P:347-348 with the
+ * DGL norm='both' of reading R26, folded into rows; reading R35 for the bias):
+ *   Y = sgemm(X, W) [n][C] (R33) ; Ys[u] = Y[u]·ns[u] ;
+ *   agg[v] = Σᶜ over in-edges (in-CSR order) Ys[u] (plain adds, R14) ;
+ *   logits[v] = agg[v]·nd[v] + b.                                             */
+typedef struct { float* Y; float* Ys; float* agg; float* logits; } orc_gcn_out_fwd_out;
+typedef struct { float* db; float* Gs; float* aggb; float* dY; float* dX; float* dW; } orc_gcn_out_bwd_out;
+
+static int gcn_gather_sum(const orc_graph* g, int dir, int cols, const float* x, float* out) {
+  return orc_spmm_alpha_unit(g, dir, cols, x, out);
+}
+
+int orc_gcn_out_fwd(const orc_graph* g, int F, int C, const float* X, const float* W, const float* bias,
+                    orc_gcn_out_fwd_out* o) {
+  int64_t n = g->n;
+  float* ns = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+  float* nd = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+  gcn_norms(g, ns, nd);
+  orc_sgemm(n, C, F, X, F, 0, W, C, 0, o->Y);
+  for (int64_t u = 0; u < n; ++u)
+    for (int j = 0; j < C; ++j) o->Ys[u * C + j] = o->Y[u * C + j] * ns[u];
+  int st = gcn_gather_sum(g, 0, C, o->Ys, o->agg);
+  for (int64_t v = 0; v < n; ++v)
+    for (int j = 0; j < C; ++j) o->logits[v * C + j] = (o->agg[v * C + j] * nd[v]) + bias[j];
+  free(ns); free(nd);
+  return st;
+}
+
+/* Backward: db = Σᶜ_v ∂logits (R33); Gs[v] = ∂logits[v]·nd[v];
+ * aggb[u] = Σᶜ over out-edges (out order) Gs[v]; dY[u] = aggb[u]·ns[u];
+ * dX = sgemm(dY, Wᵀ) (nullable), dW = sgemm(Xᵀ, dY). */
+int orc_gcn_out_bwd(const orc_graph* g, int F, int C, const float* X, const float* W, const float* dlogits,
+                    orc_gcn_out_bwd_out* o) {
+  int64_t n = g->n;
+  float* ns = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+  float* nd = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+  gcn_norms(g, ns, nd);
+  orc_colsum(dlogits, n, C, o->db);
+  for (int64_t v = 0; v < n; ++v)
+    for (int j = 0; j < C; ++j) o->Gs[v * C + j] = dlogits[v * C + j] * nd[v];
+  int st = gcn_gather_sum(g, 1, C, o->Gs, o->aggb);
+  for (int64_t u = 0; u < n; ++u)
+    for (int j = 0; j < C; ++j) o->dY[u * C + j] = o->aggb[u * C + j] * ns[u];
+  if (o->dX) orc_sgemm(n, F, C, o->dY, C, 0, W, C, 1, o->dX);
+  orc_sgemm(F, C, n, X, F, 1, o->dY, C, 0, o->dW);
+  free(ns); free(nd);
+  return st;
 }

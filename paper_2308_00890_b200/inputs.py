@@ -218,3 +218,21 @@ def gat_model_params(f: int, heads: int, head_dim: int, layers: int, classes: in
     b = (rng.standard_normal(classes) * bias_scale).astype(np.float32)
     out = dict(W=W, a_src=a_s, a_dst=a_d, b=b, heads=oh, classes=classes)
     return hidden, out
+
+
+CORA_CLASSES = 7
+
+
+def gcn_model_params(f: int, hidden_dim: int, layers: int, classes: int, bias_scale: float = 0.0,
+                     seed: int = SEED_PARAM):
+    """(hidden, out) of an L-layer GCN: L-1 hidden layers -> hidden_dim and the final layer -> classes.
+    Glorot W, biases N(0, bias_scale)."""
+    hidden, fin = [], f
+    for l in range(layers - 1):
+        W = gcn_params(fin, hidden_dim, seed=seed + 10 * l)
+        rng = np.random.Generator(np.random.PCG64(seed + 10 * l + 1))
+        hidden.append(dict(W=W, b=(rng.standard_normal(hidden_dim) * bias_scale).astype(np.float32)))
+        fin = hidden_dim
+    W = gcn_params(fin, classes, seed=seed + 10 * (layers - 1))
+    rng = np.random.Generator(np.random.PCG64(seed + 10 * (layers - 1) + 1))
+    return hidden, dict(W=W, b=(rng.standard_normal(classes) * bias_scale).astype(np.float32))

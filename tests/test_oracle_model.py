@@ -215,3 +215,47 @@ def test_model_step_quantized_trains(orc):
         assert losses[-1] < 0.9 * losses[0], losses
         final[bits] = losses[-1]
     assert abs(final[8] - final[0]) < 0.02 * final[0], final
+
+
+def torch_gcn_bias(gr, X, W, b):
+    from test_oracle_layer import torch_gcn
+    return torch_gcn(gr, X, W) + b
+
+
+def test_gather_sum_dense(orc):
+    # unweighted chunked gather = dense adjacency products (in: A·x, out: Aᵀ·x) within fp32 rounding
+    gr = inputs.random_graph(60, 300, seed=31)
+    x = inputs.features(gr.n, 5, seed=32)
+    A = np.zeros((gr.n, gr.n))
+    A[gr.in_dst(), gr.in_src] = 1.0
+    for d, M in ((0, A), (1, A.T)):
+        got = orc.gather_sum(gr, d, x, chunk=3)
+        ref = M @ x.astype(np.float64)
+        assert np.all(np.abs(got - ref) <= 64 * 2.0 ** -24 * (np.abs(M) @ np.abs(x.astype(np.float64))))
+
+
+@pytest.mark.parametrize("layers,seed", [(2, 41), (3, 42)])
+def test_gcn_model_step_bypass_vs_autograd(orc, layers, seed):
+    gr = inputs.random_graph(50, 160, seed=seed)
+    X = inputs.features(gr.n, 20, seed=seed + 1)
+    hidden, out = inputs.gcn_model_params(20, 16, layers, 4, bias_scale=0.3, seed=seed + 2)
+    lab = inputs.labels(gr.n, 4, train_frac=0.7, seed=seed + 3)
+    r = orc.gcn_model_step(gr, X, hidden, out, lab, lr=0.5, bits=0, chunk=4)
+    T = lambda a: torch.tensor(a, dtype=torch.float64, requires_grad=True)
+    h = torch.tensor(X, dtype=torch.float64)
+    leaves = []
+    for p in hidden:
+        ps = {k: T(p[k]) for k in ("W", "b")}
+        leaves.append(ps)
+        h = torch.relu(torch_gcn_bias(gr, h, ps["W"], ps["b"]))
+    ps = {k: T(out[k]) for k in ("W", "b")}
+    leaves.append(ps)
+    z = torch_gcn_bias(gr, h, ps["W"], ps["b"])
+    loss = torch.nn.functional.cross_entropy(z, torch.from_numpy(lab.astype(np.int64)), ignore_index=-1)
+    loss.backward()
+    assert abs(r["loss"] - loss.item()) < 1e-5 * abs(loss.item())
+    assert np.linalg.norm(r["logits"] - z.detach().numpy()) < 1e-5 * np.linalg.norm(z.detach().numpy())
+    for gr_o, lv in zip(r["grads"] + [r["out_grads"]], leaves):
+        for k in ("W", "b"):
+            ref = lv[k].grad.numpy()
+            assert np.linalg.norm(gr_o[k] - ref) <= 1e-5 * max(np.linalg.norm(ref), 1e-6), k
