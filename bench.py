@@ -203,6 +203,49 @@ def train_step_bench(T, torch, dg, g, F, H, D, args, l2_flush):
     return res
 
 
+def train_step_gcn_bench(T, torch, args, l2_flush):
+    """BASELINE.json configs[1]: the Cora-shaped 2-layer GCN (1433 -> 128 quantized hidden layer + bias +
+    ReLU, FP32 final layer -> 7 classes), one full-batch step per replay of a CUDA graph."""
+    from paper_2308_00890_b200.model import GCNModel
+    g = inputs.workload_graph("cora")
+    _, F, _, hid = inputs.WORKLOADS["cora"]
+    C = inputs.CORA_CLASSES
+    hidden, out = inputs.gcn_model_params(F, hid, 2, C)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    model = GCNModel(T.DeviceGraph(g), [{k: cu(v) for k, v in p.items()} for p in hidden],
+                     {k: cu(v) for k, v in out.items()}, bits=8)
+    X = cu(inputs.features(g.n, F))
+    lab = inputs.labels(g.n, C, train_frac=140 / 2708)     # Cora's public split: 140 labelled nodes
+    n_lab = int((lab >= 0).sum())
+    labd = cu(lab)
+    for i in range(args.warmup):
+        model.step(X, labd, n_lab, 0.01, step=i)
+    torch.cuda.synchronize()
+    model.check_status()
+    graph = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cs):
+        model.step(X, labd, n_lab, 0.01, step=0)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=cs):
+            model.step(X, labd, n_lab, 0.01, step=1)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        l2_flush.zero_()
+        evs[i][0].record()
+        graph.replay()
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    model.check_status()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    return {"model": f"2-layer GCN {F}->{hid}->{C} (Cora-shaped, N={g.n}, E={g.e}), int8 hidden layer, FP32 final layer",
+            "ms_per_step": round(ms, 4), "unit": "ms (one full-batch step = one epoch)",
+            "loss": float(model.loss.item()), "n_labeled": n_lab,
+            "timing": "CUDA-graph replay per step, L2 flushed between steps"}
+
+
 # ------------------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     if rank != 0:
@@ -485,6 +528,7 @@ def main():
     train = None
     if world == 1 and args.workload == "arxiv" and not args.no_train_step:
         train = train_step_bench(T, torch, dg, g, F, H, D, args, l2_flush)
+        train["gcn_cora"] = train_step_gcn_bench(T, torch, args, l2_flush)
 
     # ---------------- CPU baseline: the oracle as it stands, rank 0 at N = 1 only
     cpu = None

@@ -358,6 +358,26 @@ typedef struct {
 tango_status tango_gat_out_ctx_get_view(const tango_graph* G, const tango_gat_out_params* p, void* ctx,
                                         tango_gat_out_ctx_view* view);
 
+/* Full-precision final GCN layer (P:604-615 FP32 rule; GCN P:347-348 with the norm='both'
+ * rows of reading R26; bias R35): Y = X·W (tango_sgemm order), Ys = Y·ns[u],
+ * agg[v] = Σᶜ over in-edges Ys[u] (plain adds, R14), logits = agg·nd[v] + bias.
+ * Backward: dbias = Σᶜ_v dlogits, Gs = dlogits·nd[v], aggb[u] = Σᶜ over out-edges Gs[v],
+ * dY = aggb·ns[u], dX = dY·Wᵀ (nullable), dW = Xᵀ·dY.  One GPU only; classes <= 1024. */
+typedef struct {
+  const float* W;          /* device [in_feats][classes] */
+  const float* bias;       /* device [classes] */
+  int32_t in_feats, classes;
+} tango_gcn_out_params;
+size_t tango_gcn_out_ctx_bytes(const tango_graph* G, const tango_gcn_out_params* p);
+tango_status tango_gcn_out_fwd(const tango_graph* G, const tango_gcn_out_params* p, const float* X, void* ctx,
+                               size_t ctx_bytes, float* logits, cudaStream_t stream);
+tango_status tango_gcn_out_bwd(const tango_graph* G, const tango_gcn_out_params* p, void* ctx, size_t ctx_bytes,
+                               const float* X, const float* dlogits, float* dX, float* dW, float* dbias,
+                               cudaStream_t stream);
+typedef struct { float *Y, *Ys, *agg, *Gs, *aggb, *dY; } tango_gcn_out_ctx_view;   /* each [n][classes] */
+tango_status tango_gcn_out_ctx_get_view(const tango_graph* G, const tango_gcn_out_params* p, void* ctx,
+                                        tango_gcn_out_ctx_view* view);
+
 /* ------------------------------------------------------------------------- */
 /* Multi-GPU (destination-row partitioning): an NCCL          */
 /* communicator built from a 128-byte ncclUniqueId that the caller broadcasts  */

@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(256) k_out_softmax_heavy(GraphDev g, int heads
 // Column sums of rows gathered along a CSR row: out[v, j] = Σᶜ over the row's list positions p of
 // fmaf(w(p, h(j)), X[r(p), c(j)]) with h = j / C, and c = j (IN: X = H′ rows of width HC, weights
 // α[e,h], r = in_src) or c = j % C (OUT: X = G rows of width C, weights α[out_eid,h], r = out_dst).
+// alpha == nullptr: unweighted, acc + X (the FP32 GCN aggregation, heads = 1).
 template <bool OUT>
 struct GatherRow {
   const int64_t* ptr; const int32_t* idx; const int32_t* eid;
@@ -508,7 +509,8 @@ __global__ void __launch_bounds__(256) k_out_gather_light(GatherRow<OUT> R, int6
       const float* xr = R.X + (int64_t)R.idx[p] * R.ldx;
 #pragma unroll
       for (int t = 0; t < NC; ++t)
-        if (ok[t]) acc[t] = __fmaf_rn(R.alpha[e * R.heads + h[t]], xr[c[t]], acc[t]);
+        if (ok[t]) acc[t] = R.alpha ? __fmaf_rn(R.alpha[e * R.heads + h[t]], xr[c[t]], acc[t])
+                                    : __fadd_rn(acc[t], xr[c[t]]);
     }
 #pragma unroll
     for (int t = 0; t < NC; ++t)
@@ -539,8 +541,10 @@ __global__ void __launch_bounds__(256) k_out_gather_heavy(GatherRow<OUT> R, cons
         float acc = 0.0f;
         if (ok) {
 #pragma unroll 4
-          for (int64_t p = p0; p < p1; ++p)
-            acc = __fmaf_rn(R.alpha[R.edge(p) * R.heads + h], R.X[(int64_t)R.idx[p] * R.ldx + c], acc);
+          for (int64_t p = p0; p < p1; ++p) {
+            const float x = R.X[(int64_t)R.idx[p] * R.ldx + c];
+            acc = R.alpha ? __fmaf_rn(R.alpha[R.edge(p) * R.heads + h], x, acc) : __fadd_rn(acc, x);
+          }
         }
         part[k][lane] = acc;
       }
@@ -555,11 +559,12 @@ __global__ void __launch_bounds__(256) k_out_gather_heavy(GatherRow<OUT> R, cons
 
 template <bool OUT>
 static cudaError_t launch_gather(const GatherRow<OUT>& R, int64_t n, int chunk, const int32_t* hrows,
-                                 const int32_t* count, float* out, cudaStream_t st) {
+                                 const int32_t* count, float* out, cudaStream_t st, const char* light_name = nullptr,
+                                 const char* heavy_name = nullptr) {
   const int nc = (R.HC + 31) / 32;
   const int grid = grid_1d(n, 8);
   {
-    ProfScope ps(OUT ? "out_dhp_light" : "out_agg_light", st);
+    ProfScope ps(light_name ? light_name : (OUT ? "out_dhp_light" : "out_agg_light"), st);
     switch (nc) {
       case 1: k_out_gather_light<OUT, 1><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
       case 2: k_out_gather_light<OUT, 2><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
@@ -573,7 +578,7 @@ static cudaError_t launch_gather(const GatherRow<OUT>& R, int64_t n, int chunk, 
     }
   }
   {
-    ProfScope ps(OUT ? "out_dhp_heavy" : "out_agg_heavy", st);
+    ProfScope ps(heavy_name ? heavy_name : (OUT ? "out_dhp_heavy" : "out_agg_heavy"), st);
     k_out_gather_heavy<OUT><<<num_sms() * 4, 256, 0, st>>>(R, hrows, count, chunk, out);
   }
   return cudaGetLastError();
@@ -734,6 +739,17 @@ __global__ void __launch_bounds__(256) k_out_da(const float* __restrict__ Hp, in
     }
     atomicAdd(da_src + j, as);
     atomicAdd(da_dst + j, ad);
+  }
+}
+
+// FP32 GCN final layer row scalings (R26 norms folded into rows, R35 bias)
+// MODE 0: out = x·ns[u]   MODE 1: out = x·nd[v] + b   MODE 2: out = x·nd[v]
+template <int MODE>
+__global__ void k_gcn_rowscale(const float* __restrict__ x, int64_t n, int C, const float* __restrict__ sc,
+                               const float* __restrict__ bias, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * C; i += (int64_t)gridDim.x * blockDim.x) {
+    const float t = __fmul_rn(x[i], sc[i / C]);
+    out[i] = MODE == 1 ? __fadd_rn(t, bias[i % C]) : t;
   }
 }
 
@@ -1098,6 +1114,153 @@ tango_status tango_gat_out_ctx_get_view(const tango_graph* G, const tango_gat_ou
   view->dS = reinterpret_cast<float*>(c + L.off_dS);
   view->dHp = reinterpret_cast<float*>(c + L.off_dHp);
   view->agg = reinterpret_cast<float*>(c + L.off_agg);
+  return TANGO_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ FP32 final GCN layer (R26, R35)
+namespace {
+struct GcnOutLayout {
+  int64_t n, e, F, C;
+  size_t off_Y, off_Ys, off_agg, off_Gs, off_aggb, off_dY, off_ns, off_nd, off_indst, off_hin, off_hout, off_cnt,
+      off_ws, total;
+};
+bool gcn_out_layout(const tango_graph* G, const tango_gcn_out_params* p, GcnOutLayout* L) {
+  if (!G || !p || p->in_feats <= 0 || p->classes <= 0) return false;
+  L->n = G->row_end - G->row_begin;
+  L->e = G->e_in;
+  L->F = p->in_feats;
+  L->C = p->classes;
+  const int64_t n = L->n, C = L->C;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = al256(o + bytes); return r; };
+  L->off_Y = take(4 * n * C);
+  L->off_Ys = take(4 * n * C);
+  L->off_agg = take(4 * n * C);
+  L->off_Gs = take(4 * n * C);
+  L->off_aggb = take(4 * n * C);
+  L->off_dY = take(4 * n * C);
+  L->off_ns = take(4 * n);
+  L->off_nd = take(4 * n);
+  L->off_indst = take(4 * L->e);
+  L->off_hin = take(4 * n);
+  L->off_hout = take(4 * n);
+  L->off_cnt = take(4 * 8);
+  size_t ws = std::max(sgemm_ws_bytes(L->F, C, n), sgemm_ws_bytes(n, L->F, C));
+  ws = std::max(ws, colsum_ws_bytes(n, C));
+  L->off_ws = take(ws > 0 ? ws : 4);
+  L->total = o;
+  return true;
+}
+tango_status check_gcn_out(const tango_graph* G, const tango_gcn_out_params* p) {
+  if (!G || !p || !p->W || !p->bias) return TANGO_ERR_INVALID_ARG;
+  if (p->in_feats <= 0 || p->classes <= 0) return TANGO_ERR_SHAPE;
+  if (p->classes > OUT_MAXHC) return TANGO_ERR_UNSUPPORTED;
+  if (G->row_begin != 0 || G->row_end != G->n_global) return TANGO_ERR_UNSUPPORTED;
+  if (G->n_global > 0 && (!G->in_ptr || !G->out_ptr)) return TANGO_ERR_INVALID_ARG;
+  if (G->e_in > 0 && (!G->in_src || !G->out_dst || !G->out_eid)) return TANGO_ERR_INVALID_ARG;
+  if (G->e_in != G->e_out) return TANGO_ERR_SHAPE;
+  return TANGO_OK;
+}
+template <class T>
+T* at(void* ctx, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ctx) + off); }
+}  // namespace
+
+extern "C" {
+
+size_t tango_gcn_out_ctx_bytes(const tango_graph* G, const tango_gcn_out_params* p) {
+  GcnOutLayout L;
+  if (check_gcn_out(G, p) != TANGO_OK || !gcn_out_layout(G, p, &L)) return 0;
+  return L.total;
+}
+
+tango_status tango_gcn_out_fwd(const tango_graph* G, const tango_gcn_out_params* p, const float* X, void* ctx,
+                               size_t ctx_bytes, float* logits, cudaStream_t stream) {
+  tango_status s = check_gcn_out(G, p);
+  if (s != TANGO_OK) return s;
+  GcnOutLayout L;
+  gcn_out_layout(G, p, &L);
+  if (!ctx || ctx_bytes < L.total) return TANGO_ERR_INVALID_ARG;
+  if (L.n == 0) return TANGO_OK;
+  if (!X || !logits) return TANGO_ERR_INVALID_ARG;
+  const GraphDev g = dev_graph(G);
+  const int C = (int)L.C;
+  float *Y = at<float>(ctx, L.off_Y), *Ys = at<float>(ctx, L.off_Ys), *agg = at<float>(ctx, L.off_agg);
+  float *ns = at<float>(ctx, L.off_ns), *nd = at<float>(ctx, L.off_nd), *ws = at<float>(ctx, L.off_ws);
+  int32_t* cnt = at<int32_t>(ctx, L.off_cnt);
+  M_TRY_CUDA(cudaMemsetAsync(cnt, 0, 8 * sizeof(int32_t), stream));
+  {
+    ProfScope ps("out_plan", stream);
+    k_out_plan<<<grid_1d(L.n, 8), 256, 0, stream>>>(g, at<int32_t>(ctx, L.off_indst), at<int32_t>(ctx, L.off_hin),
+                                                    at<int32_t>(ctx, L.off_hout), cnt);
+  }
+  M_TRY_CUDA(launch_gcn_norms(g, ns, nd, stream));
+  M_TRY_CUDA(launch_sgemm(X, L.F, false, p->W, C, false, L.n, C, L.F, Y, ws, stream));
+  {
+    ProfScope ps("gcn_out_scale", stream);
+    k_gcn_rowscale<0><<<grid_1d(L.n * C), 256, 0, stream>>>(Y, L.n, C, ns, nullptr, Ys);
+  }
+  GatherRow<false> R{G->in_ptr, G->in_src, nullptr, nullptr, Ys, 1, C, C, C};
+  M_TRY_CUDA(launch_gather<false>(R, L.n, g.chunk, at<int32_t>(ctx, L.off_hin), cnt, agg, stream, "gcn_out_agg_light",
+                                  "gcn_out_agg_heavy"));
+  {
+    ProfScope ps("gcn_out_scale", stream);
+    k_gcn_rowscale<1><<<grid_1d(L.n * C), 256, 0, stream>>>(agg, L.n, C, nd, p->bias, logits);
+  }
+  M_TRY_CUDA(cudaGetLastError());
+  return TANGO_OK;
+}
+
+tango_status tango_gcn_out_bwd(const tango_graph* G, const tango_gcn_out_params* p, void* ctx, size_t ctx_bytes,
+                               const float* X, const float* dlogits, float* dX, float* dW, float* dbias,
+                               cudaStream_t stream) {
+  tango_status s = check_gcn_out(G, p);
+  if (s != TANGO_OK) return s;
+  GcnOutLayout L;
+  gcn_out_layout(G, p, &L);
+  if (!ctx || ctx_bytes < L.total) return TANGO_ERR_INVALID_ARG;
+  if (!dW || !dbias) return TANGO_ERR_INVALID_ARG;
+  if (L.n > 0 && (!X || !dlogits)) return TANGO_ERR_INVALID_ARG;
+  const GraphDev g = dev_graph(G);
+  const int C = (int)L.C;
+  float *Gs = at<float>(ctx, L.off_Gs), *aggb = at<float>(ctx, L.off_aggb), *dY = at<float>(ctx, L.off_dY);
+  float *ns = at<float>(ctx, L.off_ns), *nd = at<float>(ctx, L.off_nd), *ws = at<float>(ctx, L.off_ws);
+  int32_t* cnt = at<int32_t>(ctx, L.off_cnt);
+  M_TRY_CUDA(launch_colsum<0>(dlogits, nullptr, L.n, C, dbias, ws, nullptr, nullptr, stream));
+  if (L.n == 0) {
+    M_TRY_CUDA(cudaMemsetAsync(dW, 0, sizeof(float) * L.F * C, stream));
+    return TANGO_OK;
+  }
+  {
+    ProfScope ps("gcn_out_scale", stream);
+    k_gcn_rowscale<2><<<grid_1d(L.n * C), 256, 0, stream>>>(dlogits, L.n, C, nd, nullptr, Gs);
+  }
+  GatherRow<true> R{G->out_ptr, G->out_dst, G->out_eid, nullptr, Gs, 1, C, C, C};
+  M_TRY_CUDA(launch_gather<true>(R, L.n, g.chunk, at<int32_t>(ctx, L.off_hout), cnt + 1, aggb, stream,
+                                 "gcn_out_aggb_light", "gcn_out_aggb_heavy"));
+  {
+    ProfScope ps("gcn_out_scale", stream);
+    k_gcn_rowscale<0><<<grid_1d(L.n * C), 256, 0, stream>>>(aggb, L.n, C, ns, nullptr, dY);
+  }
+  if (dX) M_TRY_CUDA(launch_sgemm(dY, C, false, p->W, C, true, L.n, L.F, C, dX, ws, stream));
+  M_TRY_CUDA(launch_sgemm(X, L.F, true, dY, C, false, L.F, C, L.n, dW, ws, stream));
+  return TANGO_OK;
+}
+
+tango_status tango_gcn_out_ctx_get_view(const tango_graph* G, const tango_gcn_out_params* p, void* ctx,
+                                        tango_gcn_out_ctx_view* view) {
+  tango_status s = check_gcn_out(G, p);
+  if (s != TANGO_OK) return s;
+  if (!ctx || !view) return TANGO_ERR_INVALID_ARG;
+  GcnOutLayout L;
+  gcn_out_layout(G, p, &L);
+  view->Y = at<float>(ctx, L.off_Y);
+  view->Ys = at<float>(ctx, L.off_Ys);
+  view->agg = at<float>(ctx, L.off_agg);
+  view->Gs = at<float>(ctx, L.off_Gs);
+  view->aggb = at<float>(ctx, L.off_aggb);
+  view->dY = at<float>(ctx, L.off_dY);
   return TANGO_OK;
 }
 

@@ -82,6 +82,14 @@ class GatOutCtxView(C.Structure):
     _fields_ = [(f, _P) for f in _OUT_VIEW]
 
 
+class GcnOutParams(C.Structure):
+    _fields_ = [("W", _P), ("bias", _P), ("in_feats", C.c_int32), ("classes", C.c_int32)]
+
+
+class GcnOutCtxView(C.Structure):
+    _fields_ = [(f, _P) for f in ("Y", "Ys", "agg", "Gs", "aggb", "dY")]
+
+
 class SgdTensor(C.Structure):
     _fields_ = [("w", _P), ("g", _P), ("count", C.c_int64)]
 
@@ -98,7 +106,8 @@ EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tan
            "tango_profile_num_entries", "tango_profile_entry", "tango_profile_reset", "tango_profile_serialize",
            "tango_sgemm_workspace_bytes", "tango_sgemm", "tango_colsum_workspace_bytes", "tango_colsum",
            "tango_bias_act_fwd", "tango_bias_act_bwd", "tango_cross_entropy", "tango_sgd_update",
-           "tango_gat_out_ctx_bytes", "tango_gat_out_fwd", "tango_gat_out_bwd", "tango_gat_out_ctx_get_view"]
+           "tango_gat_out_ctx_bytes", "tango_gat_out_fwd", "tango_gat_out_bwd", "tango_gat_out_ctx_get_view",
+           "tango_gcn_out_ctx_bytes", "tango_gcn_out_fwd", "tango_gcn_out_bwd", "tango_gcn_out_ctx_get_view"]
 
 
 def load(path: str = LIB_PATH):
@@ -167,6 +176,12 @@ def load(path: str = LIB_PATH):
     L.tango_gat_out_fwd.argtypes = [PG, PO, _P, _P, sz, _P, _P]
     L.tango_gat_out_bwd.argtypes = [PG, PO, _P, sz, _P, _P, _P, _P, _P, _P, _P, _P]
     L.tango_gat_out_ctx_get_view.argtypes = [PG, PO, _P, C.POINTER(GatOutCtxView)]
+    PGO = C.POINTER(GcnOutParams)
+    L.tango_gcn_out_ctx_bytes.restype = sz
+    L.tango_gcn_out_ctx_bytes.argtypes = [PG, PGO]
+    L.tango_gcn_out_fwd.argtypes = [PG, PGO, _P, _P, sz, _P, _P]
+    L.tango_gcn_out_bwd.argtypes = [PG, PGO, _P, sz, _P, _P, _P, _P, _P, _P]
+    L.tango_gcn_out_ctx_get_view.argtypes = [PG, PGO, _P, C.POINTER(GcnOutCtxView)]
     _lib = L
     return L
 
@@ -530,20 +545,24 @@ class GCNLayer:
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.comm = comm
 
-    def forward(self, X, seed=0x7A4E60, step=0, layer_id=0, amax_hint=None):
+    def forward(self, X, seed=0x7A4E60, step=0, layer_id=0, amax_hint=None, out=None, amax_out=None):
         L = load()
-        out = torch.empty((self.graph.n_local, self.O), dtype=torch.float32, device="cuda")
-        amax_out = torch.empty(1, dtype=torch.float32, device="cuda")
+        out = out if out is not None else torch.empty((self.graph.n_local, self.O), dtype=torch.float32,
+                                                      device="cuda")
+        amax_out = amax_out if amax_out is not None else torch.empty(1, dtype=torch.float32, device="cuda")
         _check(L.tango_gcn_layer_fwd(self.graph.ref(), C.byref(self.params), _ptr(X), _ptr(amax_hint),
                                      Rng(seed, step, 0), layer_id, _ptr(self.ctx), self.ctx.numel(), _ptr(out),
                                      _ptr(amax_out), self.comm.handle if self.comm else None, _ptr(self.status),
                                      _stream()), "tango_gcn_layer_fwd")
         return out, amax_out
 
-    def backward(self, dout, seed=0x7A4E60, step=0, layer_id=0):
+    def backward(self, dout, seed=0x7A4E60, step=0, layer_id=0, want_dX=True, outs=None):
         L = load()
-        dX = torch.empty((self.graph.n_local, self.F), dtype=torch.float32, device="cuda")
-        dW = torch.empty((self.F, self.O), dtype=torch.float32, device="cuda")
+        if outs is None:
+            dX = torch.empty((self.graph.n_local, self.F), dtype=torch.float32, device="cuda") if want_dX else None
+            dW = torch.empty((self.F, self.O), dtype=torch.float32, device="cuda")
+        else:
+            dX, dW = outs
         _check(L.tango_gcn_layer_bwd(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), self.ctx.numel(),
                                      _ptr(dout), Rng(seed, step, 0), layer_id, _ptr(dX), _ptr(dW),
                                      self.comm.handle if self.comm else None, _ptr(self.status), _stream()),
@@ -702,4 +721,50 @@ class GATOutLayer:
             off = getattr(v, f) - base
             cnt = shp[0] * shp[1]
             out[f] = self.ctx[off:off + 4 * cnt].view(torch.float32).reshape(shp).clone()
+        return out
+
+
+class GCNOutLayer:
+    """The full-precision final GCN layer (tango_gcn_out_fwd / _bwd) with its device ctx."""
+
+    def __init__(self, graph: DeviceGraph, W, bias):
+        L = load()
+        self.graph = graph
+        self.W, self.bias = W.contiguous(), bias.contiguous()
+        self.F, self.classes = W.shape
+        self.params = GcnOutParams(_ptr(self.W), _ptr(self.bias), self.F, self.classes)
+        nbytes = L.tango_gcn_out_ctx_bytes(graph.ref(), C.byref(self.params))
+        if nbytes == 0:
+            raise TangoError(2, "tango_gcn_out_ctx_bytes")
+        self.ctx = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+
+    def forward(self, X, out=None):
+        out = out if out is not None else torch.empty((self.graph.n_local, self.classes), dtype=torch.float32,
+                                                      device="cuda")
+        _check(load().tango_gcn_out_fwd(self.graph.ref(), C.byref(self.params), _ptr(X), _ptr(self.ctx),
+                                        self.ctx.numel(), _ptr(out), _stream()), "tango_gcn_out_fwd")
+        return out
+
+    def backward(self, X, dlogits, want_dX=True, outs=None):
+        n = self.graph.n_local
+        if outs is None:
+            dX = torch.empty((n, self.F), dtype=torch.float32, device="cuda") if want_dX else None
+            dW = torch.empty((self.F, self.classes), dtype=torch.float32, device="cuda")
+            db = torch.empty(self.classes, dtype=torch.float32, device="cuda")
+        else:
+            dX, dW, db = outs
+        _check(load().tango_gcn_out_bwd(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), self.ctx.numel(),
+                                        _ptr(X), _ptr(dlogits), _ptr(dX), _ptr(dW), _ptr(db), _stream()),
+               "tango_gcn_out_bwd")
+        return dX, dW, db
+
+    def view(self):
+        v = GcnOutCtxView()
+        _check(load().tango_gcn_out_ctx_get_view(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), C.byref(v)),
+               "tango_gcn_out_ctx_get_view")
+        base, n, Cc = self.ctx.data_ptr(), self.graph.n_local, self.classes
+        out = {}
+        for f in ("Y", "Ys", "agg", "Gs", "aggb", "dY"):
+            off = getattr(v, f) - base
+            out[f] = self.ctx[off:off + 4 * n * Cc].view(torch.float32).reshape(n, Cc).clone()
         return out

@@ -181,3 +181,59 @@ def test_model_step_parity(T, orc, gspec, F, heads, hd, layers, C, chunk):
     da_ok(model.out_grads["a_src"], og["a_src"], og["da_src_abs"])
     eq("out W updated", out_d["W"], r["out"]["W"])
     eq("out b updated", out_d["b"], r["out"]["b"])
+
+
+@pytest.mark.parametrize("gspec,F,C,chunk", [((64, 256, 0, True), 16, 5, 256), ((1000, 4000, 2, True), 100, 7, 7),
+                                             ((2708, 5278, 3, True), 1433, 7, 256), ((500, 900, 5, False), 48, 40, 3)])
+def test_gcn_out_layer_parity(T, orc, gspec, F, C, chunk):
+    n, d, s, loops = gspec
+    gr = inputs.random_graph(n, d, seed=s, self_loops=loops)
+    X = _rand((gr.n, F), 41)
+    W = inputs.gcn_params(F, C, seed=42)
+    b = _rand(C, 43)
+    dz = _rand((gr.n, C), 44, 0.01)
+    f = orc.gcn_out_fwd(gr, X, W, b, chunk=chunk)
+    bo = orc.gcn_out_bwd(gr, f, X, W, dz)
+    layer = T.GCNOutLayer(T.DeviceGraph(gr, chunk=chunk), cu(W), cu(b))
+    Xd = cu(X)
+    logits = layer.forward(Xd)
+    dX, dW, db = layer.backward(Xd, cu(dz))
+    torch.cuda.synchronize()
+    v = layer.view()
+    for k in ("Y", "Ys", "agg"):
+        eq(k, v[k], f[k])
+    eq("logits", logits, f["logits"])
+    for k in ("Gs", "aggb", "dY"):
+        eq(k, v[k], bo[k])
+    eq("db", db, bo["db"])
+    eq("dX", dX, bo["dX"])
+    eq("dW", dW, bo["dW"])
+
+
+@pytest.mark.parametrize("gspec,F,hid,layers,C,chunk", [((2708, 5278, 3), 1433, 128, 2, 7, 256),
+                                                       ((400, 1500, 4), 64, 32, 3, 5, 5)])
+def test_gcn_model_step_parity(T, orc, gspec, F, hid, layers, C, chunk):
+    from paper_2308_00890_b200.model import GCNModel
+    n, d, s = gspec
+    gr = inputs.random_graph(n, d, seed=s)
+    X = inputs.features(gr.n, F, seed=s + 1)
+    hidden, out = inputs.gcn_model_params(F, hid, layers, C, bias_scale=0.1, seed=s + 2)
+    lab = inputs.labels(gr.n, C, train_frac=0.5, seed=s + 3)
+    n_lab = int((lab >= 0).sum())
+    r = orc.gcn_model_step(gr, X, hidden, out, lab, lr=0.2, bits=8, step=3, chunk=chunk)
+    dev = lambda p: {k: cu(v) for k, v in p.items()}
+    hid_d, out_d = [dev(p) for p in hidden], dev(out)
+    model = GCNModel(T.DeviceGraph(gr, chunk=chunk), hid_d, out_d, bits=8)
+    loss = model.step(cu(X), cu(lab), n_lab, 0.2, step=3)
+    torch.cuda.synchronize()
+    model.check_status()
+    assert abs(loss.item() - r["loss"]) <= 1e-6 * abs(r["loss"])
+    eq("logits", model.logits, r["logits"])
+    for l in range(layers - 1):
+        eq(f"act{l}", model.act[l], r["hs"][l + 1])
+        eq(f"dW{l}", model.grads[l]["W"], r["grads"][l]["W"])
+        eq(f"db{l}", model.grads[l]["b"], r["grads"][l]["b"])
+        eq(f"W{l} updated", hid_d[l]["W"], r["hidden"][l]["W"])
+    eq("out dW", model.out_grads["W"], r["out_grads"]["W"])
+    eq("out W updated", out_d["W"], r["out"]["W"])
+    eq("out b updated", out_d["b"], r["out"]["b"])
