@@ -122,6 +122,183 @@ __global__ void __launch_bounds__(256) k_sgemm(const float* __restrict__ A, int6
   }
 }
 
+// Large-tile variant: BM = 128 rows x BN (128 or 160) columns per block, BK = 8, 256 threads as
+// 16 x 16 with 8 x (BN/16) outputs each; double-buffered shared memory (one barrier per k-tile),
+// 16-B global loads where the operand is aligned and the tile in bounds.  Same per-output chain.
+constexpr int SG2_BM = 128, SG2_BK = 8;
+
+template <bool TA, bool TB, int BN>
+__global__ void __launch_bounds__(256, 2) k_sgemm2(const float* __restrict__ A, int64_t lda, const float* __restrict__ B,
+                                                   int64_t ldb, int64_t M, int64_t N, int64_t K,
+                                                   float* __restrict__ C) {
+  constexpr int BM = SG2_BM, BK = SG2_BK, TN = BN / 16, TM = BM / 16;
+  constexpr int A4 = BM * BK / 4, B4 = BN * BK / 4;          // float4 slots per tile
+  __shared__ __align__(16) float As[2][BK][BM];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+  const int t = threadIdx.x;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t kbeg = (int64_t)blockIdx.z * kCK;
+  const int64_t kend = min(K, kbeg + kCK);
+  float* Cz = C + (int64_t)blockIdx.z * M * N;
+  const bool avec = ((lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  const bool bvec = ((ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+
+  float4 ra[(A4 + 255) / 256], rb[(B4 + 255) / 256];
+  // slot i of A: TA (A[k][m]): k = i / (BM/4), m4 = i % (BM/4);  !TA (A[m][k]): m = i / (BK/4), k4 = i % (BK/4)
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int r = 0; r < (A4 + 255) / 256; ++r) {
+      const int i = t + 256 * r;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < A4) {
+        if (TA) {
+          const int kk = i / (BM / 4), mm = (i % (BM / 4)) * 4;
+          const int64_t gk = k0 + kk, gm = m0 + mm;
+          if (gk < kend) {
+            const float* p = A + gk * lda + gm;
+            if (avec && gm + 3 < M) v = __ldg(reinterpret_cast<const float4*>(p));
+            else {
+              v.x = gm < M ? __ldg(p) : 0.f; v.y = gm + 1 < M ? __ldg(p + 1) : 0.f;
+              v.z = gm + 2 < M ? __ldg(p + 2) : 0.f; v.w = gm + 3 < M ? __ldg(p + 3) : 0.f;
+            }
+          }
+        } else {
+          const int mm = i / (BK / 4), kk = (i % (BK / 4)) * 4;
+          const int64_t gm = m0 + mm, gk = k0 + kk;
+          if (gm < M) {
+            const float* p = A + gm * lda + gk;
+            if (avec && gk + 3 < kend) v = __ldg(reinterpret_cast<const float4*>(p));
+            else {
+              v.x = gk < kend ? __ldg(p) : 0.f; v.y = gk + 1 < kend ? __ldg(p + 1) : 0.f;
+              v.z = gk + 2 < kend ? __ldg(p + 2) : 0.f; v.w = gk + 3 < kend ? __ldg(p + 3) : 0.f;
+            }
+          }
+        }
+      }
+      ra[r] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < (B4 + 255) / 256; ++r) {
+      const int i = t + 256 * r;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < B4) {
+        if (!TB) {   // B[k][n]
+          const int kk = i / (BN / 4), nn = (i % (BN / 4)) * 4;
+          const int64_t gk = k0 + kk, gn = n0 + nn;
+          if (gk < kend) {
+            const float* p = B + gk * ldb + gn;
+            if (bvec && gn + 3 < N) v = __ldg(reinterpret_cast<const float4*>(p));
+            else {
+              v.x = gn < N ? __ldg(p) : 0.f; v.y = gn + 1 < N ? __ldg(p + 1) : 0.f;
+              v.z = gn + 2 < N ? __ldg(p + 2) : 0.f; v.w = gn + 3 < N ? __ldg(p + 3) : 0.f;
+            }
+          }
+        } else {     // B[n][k]
+          const int nn = i / (BK / 4), kk = (i % (BK / 4)) * 4;
+          const int64_t gn = n0 + nn, gk = k0 + kk;
+          if (gn < N) {
+            const float* p = B + gn * ldb + gk;
+            if (bvec && gk + 3 < kend) v = __ldg(reinterpret_cast<const float4*>(p));
+            else {
+              v.x = gk < kend ? __ldg(p) : 0.f; v.y = gk + 1 < kend ? __ldg(p + 1) : 0.f;
+              v.z = gk + 2 < kend ? __ldg(p + 2) : 0.f; v.w = gk + 3 < kend ? __ldg(p + 3) : 0.f;
+            }
+          }
+        }
+      }
+      rb[r] = v;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < (A4 + 255) / 256; ++r) {
+      const int i = t + 256 * r;
+      if (i >= A4) continue;
+      if (TA) {
+        const int kk = i / (BM / 4), mm = (i % (BM / 4)) * 4;
+        *reinterpret_cast<float4*>(&As[buf][kk][mm]) = ra[r];
+      } else {
+        const int mm = i / (BK / 4), kk = (i % (BK / 4)) * 4;
+        As[buf][kk][mm] = ra[r].x; As[buf][kk + 1][mm] = ra[r].y;
+        As[buf][kk + 2][mm] = ra[r].z; As[buf][kk + 3][mm] = ra[r].w;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < (B4 + 255) / 256; ++r) {
+      const int i = t + 256 * r;
+      if (i >= B4) continue;
+      if (!TB) {
+        const int kk = i / (BN / 4), nn = (i % (BN / 4)) * 4;
+        *reinterpret_cast<float4*>(&Bs[buf][kk][nn]) = rb[r];
+      } else {
+        const int nn = i / (BK / 4), kk = (i % (BK / 4)) * 4;
+        Bs[buf][kk][nn] = rb[r].x; Bs[buf][kk + 1][nn] = rb[r].y;
+        Bs[buf][kk + 2][nn] = rb[r].z; Bs[buf][kk + 3][nn] = rb[r].w;
+      }
+    }
+  };
+
+  const int ty = t / 16, tx = t % 16;
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+
+  int buf = 0;
+  if (kbeg < kend) {
+    load(kbeg);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
+    const bool more = k0 + BK < kend;
+    if (more) load(k0 + BK);
+    const int kmax = (kend - k0 < BK) ? (int)(kend - k0) : BK;
+    if (kmax == BK) {
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        float a[TM], b[TN];
+#pragma unroll
+        for (int i = 0; i < TM; i += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + i]);
+          a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
+        }
+#pragma unroll
+        for (int j = 0; j < TN; j += 2) {
+          const float2 v = *reinterpret_cast<const float2*>(&Bs[buf][kk][tx * TN + j]);
+          b[j] = v.x; b[j + 1] = v.y;
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+      }
+    } else {
+      for (int kk = 0; kk < kmax; ++kk) {
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j)
+            acc[i][j] = __fmaf_rn(As[buf][kk][ty * TM + i], Bs[buf][kk][tx * TN + j], acc[i][j]);
+      }
+    }
+    if (more) store(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t gm = m0 + ty * TM + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t gn = n0 + tx * TN + j;
+      if (gn < N) Cz[gm * N + gn] = acc[i][j];
+    }
+  }
+}
+
 // Left-to-right fold of chunk partials (R14/R33): out[i] = ((p0 + p1) + p2) + ...
 __global__ void k_fold(const float* __restrict__ ws, int64_t count, int nchunks, float* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
@@ -143,13 +320,28 @@ static cudaError_t launch_sgemm(const float* A, int64_t lda, bool ta, const floa
   if (M == 0 || N == 0) return cudaSuccess;
   const int64_t nc = nchunks_of(K);
   float* dst = nc > 1 ? ws : C;
-  dim3 grid((unsigned)((N + SG_BN - 1) / SG_BN), (unsigned)((M + SG_BM - 1) / SG_BM), (unsigned)nc);
-  {
+  if (M < 64) {
+    dim3 grid((unsigned)((N + SG_BN - 1) / SG_BN), (unsigned)((M + SG_BM - 1) / SG_BM), (unsigned)nc);
     ProfScope ps("sgemm", st);
     if (!ta && !tb) k_sgemm<false, false><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, dst);
     else if (ta && !tb) k_sgemm<true, false><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, dst);
     else if (!ta && tb) k_sgemm<false, true><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, dst);
     else k_sgemm<true, true><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, dst);
+  } else {
+    // 160-wide column tiles when they cover N with less waste than 128-wide ones
+    const int64_t w128 = (N + 127) / 128 * 128, w160 = (N + 159) / 160 * 160;
+    const bool n160 = w160 < w128;
+    const int bn = n160 ? 160 : 128;
+    dim3 grid((unsigned)((N + bn - 1) / bn), (unsigned)((M + SG2_BM - 1) / SG2_BM), (unsigned)nc);
+    ProfScope ps("sgemm", st);
+#define SG2(TA_, TB_)                                                                              \
+    if (n160) k_sgemm2<TA_, TB_, 160><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, dst);         \
+    else k_sgemm2<TA_, TB_, 128><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, dst);
+    if (!ta && !tb) { SG2(false, false) }
+    else if (ta && !tb) { SG2(true, false) }
+    else if (!ta && tb) { SG2(false, true) }
+    else { SG2(true, true) }
+#undef SG2
   }
   if (nc > 1) {
     ProfScope ps("sgemm_fold", st);
@@ -850,7 +1042,7 @@ tango_status tango_sgemm(const float* A, int64_t lda, int32_t a_layout, const fl
   if (!C || (K > 0 && (!A || !B))) return TANGO_ERR_INVALID_ARG;
   const bool ta = a_layout == TANGO_MN_MAJOR, tb = b_layout == TANGO_K_MAJOR;
   if (lda < (ta ? M : K) || ldb < (tb ? K : N)) return TANGO_ERR_SHAPE;
-  if ((M + SG_BM - 1) / SG_BM > 65535 || nchunks_of(K) > 65535) return TANGO_ERR_UNSUPPORTED;
+  if ((M + SG_BM - 1) / SG_BM > 65535 || nchunks_of(K) > 65535) return TANGO_ERR_UNSUPPORTED;   // grid y / z
   const size_t need = sgemm_ws_bytes(M, N, K);
   if (need > 0 && (!workspace || ws_bytes < need)) return TANGO_ERR_INVALID_ARG;
   M_TRY_CUDA(launch_sgemm(A, lda, ta, B, ldb, tb, M, N, K, C, static_cast<float*>(workspace), stream));

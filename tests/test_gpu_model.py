@@ -29,7 +29,8 @@ def _rand(shape, seed, scale=1.0):
 
 
 @pytest.mark.parametrize("M,N,K", [(100, 70, 2500), (1, 1, 1), (65, 63, 1024), (130, 17, 1025), (64, 64, 0),
-                                   (3000, 160, 512)])
+                                   (3000, 160, 512), (301, 512, 160), (512, 160, 5000), (257, 161, 13),
+                                   (40, 300, 7)])
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
 def test_sgemm_parity(T, orc, M, N, K, ta, tb):
     A = _rand((M, K), 1)
