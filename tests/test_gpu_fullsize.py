@@ -79,3 +79,40 @@ def test_gat_layer_arxiv_full_size(T, orc):
         assert np.all(err <= bound * absum + 1e-7), (name, float(np.max(err / (absum + 1e-30))))
     # the hub rows (max in-degree ~8K, > 31 canonical chunks) are inside this comparison
     assert int(np.diff(g.in_ptr).max()) > 30 * 256
+
+
+def test_gat_train_step_arxiv_full_size(T, orc):
+    """NEXT-1 at full size: one training step of the 3-layer arxiv GAT exactly as bench.py's train_step
+    builds it (same seeded graph, features, parameters, labels, lr), against oracle.gat_model_step."""
+    from paper_2308_00890_b200.model import GATModel
+    from test_gpu_layer import da_ok
+    kw, F, H, D = inputs.WORKLOADS["arxiv"]
+    g = inputs.workload_graph("arxiv")
+    C = inputs.ARXIV_CLASSES
+    hidden, out = inputs.gat_model_params(F, H, D, 3, C)
+    X = inputs.features(g.n, F)
+    lab = inputs.labels(g.n, C, train_frac=inputs.ARXIV_TRAIN_FRAC)
+    n_lab = int((lab >= 0).sum())
+    lr, step = 0.01, 2
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    dev = lambda p: {k: (cu(v) if isinstance(v, np.ndarray) else v) for k, v in p.items()}
+    hid_d, out_d = [dev(p) for p in hidden], dev(out)
+    model = GATModel(T.DeviceGraph(g), hid_d, out_d, slope=0.2, bits=8)
+    loss = model.step(cu(X), cu(lab), n_lab, lr, step=step)
+    torch.cuda.synchronize()
+    model.check_status()
+    r = orc.gat_model_step(g, X, hidden, out, lab, lr=lr, bits=8, step=step, chunk=256)
+    assert abs(loss.item() - r["loss"]) <= 1e-6 * abs(r["loss"])
+    eq("logits", model.logits, r["logits"])
+    for l in range(2):
+        eq(f"act{l}", model.act[l], r["hs"][l + 1])
+        eq(f"dW{l}", model.grads[l]["W"], r["grads"][l]["W"])
+        eq(f"db{l}", model.grads[l]["b"], r["grads"][l]["b"])
+        da_ok(model.grads[l]["a_src"], r["grads"][l]["a_src"], r["grads"][l]["da_src_abs"])
+        eq(f"W{l} updated", hid_d[l]["W"], r["hidden"][l]["W"])
+    og = r["out_grads"]
+    eq("out dW", model.out_grads["W"], og["W"])
+    eq("out db", model.out_grads["b"], og["b"])
+    da_ok(model.out_grads["a_src"], og["a_src"], og["da_src_abs"])
+    da_ok(model.out_grads["a_dst"], og["a_dst"], og["da_dst_abs"])
+    eq("out W updated", out_d["W"], r["out"]["W"])
