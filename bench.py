@@ -246,6 +246,61 @@ def train_step_gcn_bench(T, torch, args, l2_flush):
             "timing": "CUDA-graph replay per step, L2 flushed between steps"}
 
 
+def sddmm_bits_bench(T, torch, dg, g, args, l2_flush, peaks):
+    """NEXT-4 (Fig.18a): SDDMM-dot and SDDMM-add on int8 vs packed int4 node features at the
+    paper's SDDMM shape, heads x D = 4 x 64, on the arxiv-shaped graph; warp-per-row kernels
+    (tango_sddmm_qn), device time per call (CUDA events, L2 flushed before each call), algorithmic GB/s
+    with each gathered row counted once per edge."""
+    H, D = 4, 64
+    cols = H * D
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    A, B = cu(inputs.features(g.n, cols, seed=61)), cu(inputs.features(g.n, cols, seed=62))
+    npad = g.n + (g.n & 1)          # packed int4 [n][4] as one flat run of 8-code groups
+    S = cu(inputs.features(npad, H, seed=63))
+    Dm = cu(inputs.features(npad, H, seed=64))
+    res = {"shape": f"heads x D = {H} x {D} (P:1218), arxiv-shaped graph E={dg.e_in}"}
+    E = dg.e_in
+    out0 = torch.empty((E, H), device="cuda")
+    out1 = torch.empty((E, H), device="cuda")
+    for bits in (8, 4):
+        if bits == 8:
+            qa, sa, _ = T.quantize(A, bits=8, ld=cols)
+            qb, sb, _ = T.quantize(B, bits=8, ld=cols)
+            qs, ss, _ = T.quantize(S, bits=8, ld=H)
+            qd, sd, _ = T.quantize(Dm, bits=8, ld=H)
+        else:
+            qa, sa, _ = T.quantize_int4(A)
+            qb, sb, _ = T.quantize_int4(B)
+            qs, ss, _ = T.quantize_int4(S.reshape(-1, 8), ld_bytes=4)
+            qd, sd, _ = T.quantize_int4(Dm.reshape(-1, 8), ld_bytes=4)
+            qs, qd = qs.reshape(npad, H // 2), qd.reshape(npad, H // 2)
+        row = cols * bits // 8
+        for op, name in ((T.TANGO_SDDMM_DOT, "dot"), (T.TANGO_SDDMM_ADD, "add")):
+            call = (lambda: T.sddmm_qn(dg, op, bits, qb, sb, qa, sa, H, cols, out0=out0)) if name == "dot" else \
+                   (lambda: T.sddmm_qn(dg, op, bits, qs, ss, qd, sd, H, H, out0=out0, out1=out1))
+            for _ in range(3):
+                call()
+            ts = []
+            for _ in range(max(5, args.steps)):
+                l2_flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                call()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms = statistics.median(ts)
+            if name == "dot":
+                byts = E * (4 + row + 4 * H) + g.n * (8 + row)
+            else:
+                byts = E * (4 + H * bits // 8 + 8 * H) + g.n * (8 + H * bits // 8)
+            res[f"{name}_int{bits}_ms"] = round(ms, 4)
+            res[f"{name}_int{bits}_gbs"] = round(byts / (ms / 1e3) / 1e9, 1)
+    res["hbm_peak_gbs"] = peaks["hbm_gbs"]
+    res["dot_speedup_int4_vs_int8"] = round(res["dot_int8_ms"] / res["dot_int4_ms"], 3)
+    return res
+
+
 # ------------------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     if rank != 0:
@@ -529,6 +584,9 @@ def main():
     if world == 1 and args.workload == "arxiv" and not args.no_train_step:
         train = train_step_bench(T, torch, dg, g, F, H, D, args, l2_flush)
         train["gcn_cora"] = train_step_gcn_bench(T, torch, args, l2_flush)
+    sddmm_bits = None
+    if world == 1 and args.workload == "arxiv":
+        sddmm_bits = sddmm_bits_bench(T, torch, dg, g, args, l2_flush, peaks)
 
     # ---------------- CPU baseline: the oracle as it stands, rank 0 at N = 1 only
     cpu = None
@@ -560,7 +618,7 @@ def main():
                                 "(copy stream, double-buffered inputs)",
                         "d2h_bytes_per_step": d2h},
                 "gpu_launches": int(launches_t.item()), "clocks": clk, "kernel_ms": breakdown, "kernel_ms_per_step": per_step,
-                "train_step": train,
+                "train_step": train, "sddmm_bits": sddmm_bits,
                 "timing": "value: CUDA-graph replay of fwd+bwd per step (events per step, L2 flushed between "
                           "steps); kernel_ms/roofline: eager pass, side-stream work serialised, events around every launch "
                           f"(sum of kernel times {eager_ms:.3f} ms/step)"}

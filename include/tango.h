@@ -181,6 +181,32 @@ tango_status tango_edge_sum(const tango_graph* G, int32_t dir, int32_t heads, co
                             cudaStream_t stream);
 
 /* ------------------------------------------------------------------------- */
+/* NEXT-4: 4-bit node features for the SDDMM primitives     */
+/* (§4.4, Fig.18a).  Packed layout: element 2i of a row in the low */
+/* nibble of byte i, element 2i+1 in the high nibble, 4-bit two's complement, */
+/* codes in [−7, 7] (qmax = 2^(4−1) − 1).                                     */
+/* ------------------------------------------------------------------------- */
+/* SR quantization to packed 4-bit codes: the same scale rule, Philox stream and
+ * element index g = (global_row0 + i)·cols + j as tango_quantize with bits = 4.
+ * cols % 8 == 0; q: [rows][ld_bytes] (ld_bytes % 4 == 0, >= cols/2); x 16-B and q
+ * 4-B aligned.  scale_out, amax_out: device scalars (amax_out doubles as the amax
+ * slot; amax_hint, if given, is copied into it). */
+tango_status tango_quantize_int4(const float* x, int64_t rows, int64_t cols, int64_t global_row0,
+                                 const float* amax_hint, tango_rng rng, uint8_t* q, int64_t ld_bytes, float* scale_out,
+                                 float* amax_out, int32_t* dev_status, cudaStream_t stream);
+/* SDDMM on bits-bit codes (bits = 8: int8 bytes, bits = 4: packed nibbles), one warp per
+ * destination row, the same values as tango_sddmm_q:
+ *  TANGO_SDDMM_DOT: out0[e,h] = i2f(Σ_d qA[v,h,d]·qB[u,h,d])·(s_dst·s_src), Xdst = A (rows of the
+ *    owned destinations, global row index), Xsrc = B (global rows); cols = heads·D codes per row,
+ *    row words (32/bits codes per 32-bit word) <= 32, words per head a power of two, ld % 4 == 0.
+ *  TANGO_SDDMM_ADD: cols == heads; e_pre = qS[u,h]·s_src + qD[v,h]·s_dst -> out0 (nullable),
+ *    LeakyReLU -> out1 (nullable).
+ * ld_src / ld_dst in bytes.  Edge outputs [e_in][heads] in in-CSR order. */
+tango_status tango_sddmm_qn(const tango_graph* G, int32_t op, int32_t bits, const void* Xsrc, int64_t ld_src,
+                            const float* s_src, const void* Xdst, int64_t ld_dst, const float* s_dst, int32_t heads,
+                            int32_t cols, float slope, float* out0, float* out1, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------- */
 /* Bit-width derivation (§3.2 Eq.4, Fig.5).  */
 /* ------------------------------------------------------------------------- */
 /* Error_X of codes q (with their scale) against x: the mean over the rows x cols

@@ -107,7 +107,8 @@ EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tan
            "tango_sgemm_workspace_bytes", "tango_sgemm", "tango_colsum_workspace_bytes", "tango_colsum",
            "tango_bias_act_fwd", "tango_bias_act_bwd", "tango_cross_entropy", "tango_sgd_update",
            "tango_gat_out_ctx_bytes", "tango_gat_out_fwd", "tango_gat_out_bwd", "tango_gat_out_ctx_get_view",
-           "tango_gcn_out_ctx_bytes", "tango_gcn_out_fwd", "tango_gcn_out_bwd", "tango_gcn_out_ctx_get_view"]
+           "tango_gcn_out_ctx_bytes", "tango_gcn_out_fwd", "tango_gcn_out_bwd", "tango_gcn_out_ctx_get_view",
+           "tango_quantize_int4", "tango_sddmm_qn"]
 
 
 def load(path: str = LIB_PATH):
@@ -176,6 +177,8 @@ def load(path: str = LIB_PATH):
     L.tango_gat_out_fwd.argtypes = [PG, PO, _P, _P, sz, _P, _P]
     L.tango_gat_out_bwd.argtypes = [PG, PO, _P, sz, _P, _P, _P, _P, _P, _P, _P, _P]
     L.tango_gat_out_ctx_get_view.argtypes = [PG, PO, _P, C.POINTER(GatOutCtxView)]
+    L.tango_quantize_int4.argtypes = [_P, i64, i64, i64, _P, Rng, _P, i64, _P, _P, _P, _P]
+    L.tango_sddmm_qn.argtypes = [PG, i32, i32, _P, i64, _P, _P, i64, _P, i32, i32, f32, _P, _P, _P]
     PGO = C.POINTER(GcnOutParams)
     L.tango_gcn_out_ctx_bytes.restype = sz
     L.tango_gcn_out_ctx_bytes.argtypes = [PG, PGO]
@@ -768,3 +771,29 @@ class GCNOutLayer:
             off = getattr(v, f) - base
             out[f] = self.ctx[off:off + 4 * n * Cc].view(torch.float32).reshape(n, Cc).clone()
         return out
+
+
+# ---------------------------------------------------------------------------------------- NEXT-4
+def quantize_int4(x, seed=0, step=0, tag=0, global_row0=0, amax_hint=None, ld_bytes=None, status=None):
+    """tango_quantize_int4: (packed uint8 [rows, ld_bytes], scale (1,), amax (1,))."""
+    x = x.contiguous()
+    rows, cols = x.shape
+    ld_bytes = ld_bytes if ld_bytes is not None else (cols // 2 + 3) // 4 * 4
+    q = torch.zeros((rows, ld_bytes), dtype=torch.uint8, device=x.device)
+    s = torch.empty(1, dtype=torch.float32, device=x.device)
+    amax = torch.empty(1, dtype=torch.float32, device=x.device)
+    _check(load().tango_quantize_int4(_ptr(x), rows, cols, global_row0, _ptr(amax_hint), Rng(seed, step, tag), _ptr(q),
+                                      ld_bytes, _ptr(s), _ptr(amax), _ptr(status), _stream()), "tango_quantize_int4")
+    return q, s, amax
+
+
+def sddmm_qn(graph: DeviceGraph, op, bits, Xsrc, s_src, Xdst, s_dst, heads, cols, slope=0.2, out0=None, out1=None):
+    """tango_sddmm_qn on int8 (bits 8) or packed int4 (bits 4) rows; returns (out0, out1)."""
+    E = graph.e_in
+    out0 = out0 if out0 is not None else torch.empty((E, heads), dtype=torch.float32, device="cuda")
+    if op == TANGO_SDDMM_ADD and out1 is None:
+        out1 = torch.empty((E, heads), dtype=torch.float32, device="cuda")
+    _check(load().tango_sddmm_qn(graph.ref(), op, bits, _ptr(Xsrc), Xsrc.shape[1] * Xsrc.element_size(), _ptr(s_src),
+                                 _ptr(Xdst), Xdst.shape[1] * Xdst.element_size(), _ptr(s_dst), heads, cols, slope,
+                                 _ptr(out0), _ptr(out1), _stream()), "tango_sddmm_qn")
+    return out0, out1
