@@ -340,11 +340,31 @@ def run_reference(args, rank, world):
                        "head_dim": D},
             "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------------------------- main arm
+_JSON_OUT = None
+
+
+def _claim_stdout():
+    """Route the process's fd 1 to stderr (NCCL prints its version banner on stdout at communicator
+    init) and keep a private handle on the real stdout for the one JSON line."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -353,6 +373,7 @@ def main():
     ap.add_argument("--impl", default="tango", choices=["tango", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train-step", action="store_true")
+    ap.add_argument("--nccl-single", action="store_true", help="N = 1 through a 1-rank NCCL communicator")
     ap.add_argument("--ref-sample", type=float, default=1.0)
     ap.add_argument("--profile-breakdown", action="store_true", help="print per-kernel times to stderr")
     args = ap.parse_args()
@@ -383,6 +404,8 @@ def main():
         uid = [T.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = T.Comm(world, rank, uid[0], starts)
+    elif args.nccl_single:    # the N > 1 code path (NCCL collectives, partition plumbing) on one rank
+        comm = T.Comm(1, 0, T.Comm.unique_id(), starts)
     dg = T.DeviceGraph(g, row_begin=r0, row_end=r1)
     W, a_s, a_d = inputs.gat_params(F, H, D)
     Hx = inputs.features(g.n, F)[r0:r1]
@@ -622,7 +645,7 @@ def main():
                 "timing": "value: CUDA-graph replay of fwd+bwd per step (events per step, L2 flushed between "
                           "steps); kernel_ms/roofline: eager pass, side-stream work serialised, events around every launch "
                           f"(sum of kernel times {eager_ms:.3f} ms/step)"}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if comm is not None:
         comm.close()
     if world > 1:

@@ -134,3 +134,42 @@ def test_gcn_partitioned_local_comm(T, orc, P):
     assert np.array_equal(np.concatenate([r[1] for r in res]), b["dX"])
     for r in range(P):
         assert np.array_equal(res[r][2], b["dW"]), r
+
+
+def test_nccl_single_rank_comm(T, orc):
+    """The NCCL transport itself (tango_comm_init over a real ncclComm, nranks = 1): every collective of
+    the GAT and GCN layers goes through NCCL on the caller's stream; the results must equal the
+    oracle bit for bit (∂a within the bound).  gpurun provides one GPU, so this is the NCCL path's
+    only on-device check; the multi-rank dataflow is covered by the loopback and gloo tests."""
+    from test_gpu_layer import da_ok, eq
+    gr = inputs.random_graph(1200, 6000, seed=31)
+    F, heads, hd = 64, 4, 32
+    X = inputs.features(gr.n, F, seed=32)
+    W, a_s, a_d = inputs.gat_params(F, heads, hd, seed=33)
+    dY = inputs.grad_out(gr.n, heads * hd, seed=34)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    comm = T.Comm(1, 0, T.Comm.unique_id(), [0, gr.n])
+    try:
+        dg = T.DeviceGraph(gr, chunk=16, row_begin=0, row_end=gr.n)
+        layer = T.GATLayer(dg, cu(W), cu(a_s), cu(a_d), heads, hd, slope=0.2, bits=8, comm=comm)
+        Hout, _ = layer.forward(cu(X), step=3, layer_id=1)
+        dX, dW, das, dad = layer.backward(cu(dY), step=3, layer_id=1)
+        Wg = inputs.gcn_params(F, 48, seed=35)
+        gl = T.GCNLayer(dg, cu(Wg), bits=8, comm=comm)
+        gout, _ = gl.forward(cu(X), step=3, layer_id=2)
+        gdX, gdW = gl.backward(cu(dY[:, :48]), step=3, layer_id=2)
+        torch.cuda.synchronize()
+        layer.check_status()
+    finally:
+        comm.close()
+    f = orc.gat_fwd(gr, X, W, a_s, a_d, heads, hd, slope=0.2, bits=8, step=3, layer_id=1, chunk=16)
+    b = orc.gat_bwd(gr, f, X, W, a_s, a_d, dY)
+    eq("H_out", Hout, f["Hout"])
+    eq("dH", dX, b["dH"])
+    eq("dW", dW, b["dW"])
+    da_ok(das, b["da_src"], b["da_src_abs"])
+    gf = orc.gcn_fwd(gr, X, Wg, bits=8, step=3, layer_id=2, chunk=16)
+    gb = orc.gcn_bwd(gr, gf, X, Wg, dY[:, :48])
+    eq("gcn out", gout, gf["out"])
+    eq("gcn dX", gdX, gb["dX"])
+    eq("gcn dW", gdW, gb["dW"])
