@@ -433,11 +433,31 @@ __global__ void __launch_bounds__(256) k_bias_relu_fwd(const float* __restrict__
                                                        unsigned* amax) {
   float mx = 0.0f;
   const int64_t n = rows * cols;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = __fadd_rn(__ldg(x + i), __ldg(b + i % cols));
-    const float a = v > 0.0f ? v : 0.0f;
-    y[i] = a;
-    mx = fmaxf(mx, a);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if ((cols & 3) == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0) {
+    // 16-B path: 4 consecutive columns of one row per step, streaming loads / stores
+    const int64_t n4 = n >> 2;
+    for (int64_t i = tid; i < n4; i += stride) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(x) + i);
+      const int64_t j = (i << 2) % cols;
+      float4 a;
+      a.x = __fadd_rn(v.x, __ldg(b + j));
+      a.y = __fadd_rn(v.y, __ldg(b + j + 1));
+      a.z = __fadd_rn(v.z, __ldg(b + j + 2));
+      a.w = __fadd_rn(v.w, __ldg(b + j + 3));
+      a.x = a.x > 0.0f ? a.x : 0.0f; a.y = a.y > 0.0f ? a.y : 0.0f;
+      a.z = a.z > 0.0f ? a.z : 0.0f; a.w = a.w > 0.0f ? a.w : 0.0f;
+      reinterpret_cast<float4*>(y)[i] = a;
+      mx = fmaxf(mx, fmaxf(fmaxf(a.x, a.y), fmaxf(a.z, a.w)));
+    }
+  } else {
+    for (int64_t i = tid; i < n; i += stride) {
+      const float v = __fadd_rn(__ldg(x + i), __ldg(b + i % cols));
+      const float a = v > 0.0f ? v : 0.0f;
+      y[i] = a;
+      mx = fmaxf(mx, a);
+    }
   }
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
@@ -807,8 +827,19 @@ __global__ void k_out_dalpha(int64_t e_in, int heads, int C, const int32_t* __re
     const float* gv = G + (int64_t)in_dst[e] * C;
     const float* hu = Hp + (int64_t)in_src[e] * HC + (int64_t)h * C;
     float acc = 0.0f;
-#pragma unroll 8
-    for (int c = 0; c < C; ++c) acc = __fmaf_rn(gv[c], hu[c], acc);
+    int c = 0;
+    if ((C & 3) == 0) {   // rows 16-B aligned: 4 terms per load, still one sequential chain over c
+#pragma unroll 2
+      for (; c < C; c += 4) {
+        const float4 gq = __ldg(reinterpret_cast<const float4*>(gv + c));
+        const float4 hq = __ldg(reinterpret_cast<const float4*>(hu + c));
+        acc = __fmaf_rn(gq.x, hq.x, acc);
+        acc = __fmaf_rn(gq.y, hq.y, acc);
+        acc = __fmaf_rn(gq.z, hq.z, acc);
+        acc = __fmaf_rn(gq.w, hq.w, acc);
+      }
+    }
+    for (; c < C; ++c) acc = __fmaf_rn(gv[c], hu[c], acc);
     dalpha[i] = acc;
   }
 }
