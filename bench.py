@@ -372,7 +372,8 @@ def main():
     ap.add_argument("--workload", default="arxiv", choices=sorted(inputs.WORKLOADS))
     ap.add_argument("--impl", default="tango", choices=["tango", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-train-step", action="store_true")
+    ap.add_argument("--no-train-step", "--layer-only", dest="no_train_step", action="store_true",
+                    help="skip the extras (train_step, sddmm_bits): the layer step only")
     ap.add_argument("--nccl-single", action="store_true", help="N = 1 through a 1-rank NCCL communicator")
     ap.add_argument("--ref-sample", type=float, default=1.0)
     ap.add_argument("--profile-breakdown", action="store_true", help="print per-kernel times to stderr")
@@ -608,7 +609,7 @@ def main():
         train = train_step_bench(T, torch, dg, g, F, H, D, args, l2_flush)
         train["gcn_cora"] = train_step_gcn_bench(T, torch, args, l2_flush)
     sddmm_bits = None
-    if world == 1 and args.workload == "arxiv":
+    if world == 1 and args.workload == "arxiv" and not args.no_train_step:
         sddmm_bits = sddmm_bits_bench(T, torch, dg, g, args, l2_flush, peaks)
 
     # ---------------- CPU baseline: the oracle as it stands, rank 0 at N = 1 only
