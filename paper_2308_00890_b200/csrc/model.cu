@@ -125,9 +125,9 @@ __global__ void __launch_bounds__(256) k_sgemm(const float* __restrict__ A, int6
 // Large-tile variant: BM = 128 rows x BN (128 or 160) columns per block, BK = 8, 256 threads as
 // 16 x 16 with 8 x (BN/16) outputs each; double-buffered shared memory (one barrier per k-tile),
 // 16-B global loads where the operand is aligned and the tile in bounds.  Same per-output chain.
-constexpr int SG2_BM = 128, SG2_BK = 8;
+constexpr int SG2_BM = 128;
 
-template <bool TA, bool TB, int BN>
+template <bool TA, bool TB, int BN, int SG2_BK = (BN == 128 ? 16 : 8)>
 __global__ void __launch_bounds__(256, 2) k_sgemm2(const float* __restrict__ A, int64_t lda, const float* __restrict__ B,
                                                    int64_t ldb, int64_t M, int64_t N, int64_t K,
                                                    float* __restrict__ C) {
