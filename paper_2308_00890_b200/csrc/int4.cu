@@ -110,6 +110,37 @@ __global__ void __launch_bounds__(256) k_sddmm_dot_e(GraphDev g, int heads, int 
           wb[k][c] = ok ? __ldg(brow + w) : 0u;
         }
       }
+      if constexpr (GSZ >= DOT_GRP && GSZ <= 32) {
+        // transposed reduction: the DOT_GRP partial dots of a lane are reduce-scattered over the GSZ
+        // lanes of its head (halving exchanges), so a group of edges costs ~DOT_GRP shuffles per
+        // 32-word chunk instead of DOT_GRP·log2(GSZ); lane bit o of each halving step selects
+        // which half (which edges) the lane keeps.
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          int val[DOT_GRP];
+#pragma unroll
+          for (int k = 0; k < DOT_GRP; ++k) val[k] = word_dot<BITS>(wa[k][c], wb[k][c]);
+          int kidx = 0;
+#pragma unroll
+          for (int n = DOT_GRP, o = GSZ / 2; n > 1; n >>= 1, o >>= 1) {
+            const bool upper = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < n / 2; ++i) {
+              const int send = upper ? val[i] : val[i + n / 2];
+              const int keep = upper ? val[i + n / 2] : val[i];
+              val[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+            kidx = kidx * 2 + (upper ? 1 : 0);
+          }
+#pragma unroll
+          for (int o = GSZ / (2 * DOT_GRP); o >= 1; o >>= 1) val[0] += __shfl_xor_sync(0xffffffffu, val[0], o);
+          const int w = c * 32 + lane;
+          const int64_t e = eb + kidx;
+          if (w < words && (lane & (GSZ / DOT_GRP - 1)) == 0 && e < e1)
+            out[e * heads + w / GSZ] = __fmul_rn(__int2float_rn(BITS == 8 ? val[0] : val[0] / 256), s);
+        }
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < DOT_GRP; ++k) {
         const int64_t e = eb + k;
