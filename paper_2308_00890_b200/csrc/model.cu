@@ -695,7 +695,7 @@ struct GatherRow {
 };
 
 // light rows: warp per row, NC columns per lane (j = lane + 32 t)
-template <bool OUT, int NC>
+template <bool OUT, bool WGT, int NC>
 __global__ void __launch_bounds__(256) k_out_gather_light(GatherRow<OUT> R, int64_t n, int chunk,
                                                           float* __restrict__ out) {
   const int lane = threadIdx.x & 31;
@@ -715,14 +715,42 @@ __global__ void __launch_bounds__(256) k_out_gather_light(GatherRow<OUT> R, int6
     float acc[NC];
 #pragma unroll
     for (int t = 0; t < NC; ++t) acc[t] = 0.0f;
-#pragma unroll 4
-    for (int64_t p = b; p < e1; ++p) {
+    // two list entries per step, all loads of both issued before either is accumulated
+    int64_t p = b;
+    for (; p + 1 < e1; p += 2) {
+      const int64_t ea = R.edge(p), eb = R.edge(p + 1);
+      const float* xa = R.X + (int64_t)__ldg(R.idx + p) * R.ldx;
+      const float* xb = R.X + (int64_t)__ldg(R.idx + p + 1) * R.ldx;
+      float va[NC], vb[NC], wa[NC], wb[NC];
+#pragma unroll
+      for (int t = 0; t < NC; ++t) {
+        va[t] = ok[t] ? __ldg(xa + c[t]) : 0.0f;
+        vb[t] = ok[t] ? __ldg(xb + c[t]) : 0.0f;
+        if constexpr (WGT) {
+          wa[t] = ok[t] ? __ldg(R.alpha + ea * R.heads + h[t]) : 0.0f;
+          wb[t] = ok[t] ? __ldg(R.alpha + eb * R.heads + h[t]) : 0.0f;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < NC; ++t) {
+        if constexpr (WGT) {
+          acc[t] = __fmaf_rn(wa[t], va[t], acc[t]);
+          acc[t] = __fmaf_rn(wb[t], vb[t], acc[t]);
+        } else {
+          acc[t] = __fadd_rn(acc[t], va[t]);
+          acc[t] = __fadd_rn(acc[t], vb[t]);
+        }
+      }
+    }
+    if (p < e1) {
       const int64_t e = R.edge(p);
-      const float* xr = R.X + (int64_t)R.idx[p] * R.ldx;
+      const float* xr = R.X + (int64_t)__ldg(R.idx + p) * R.ldx;
 #pragma unroll
       for (int t = 0; t < NC; ++t)
-        if (ok[t]) acc[t] = R.alpha ? __fmaf_rn(R.alpha[e * R.heads + h[t]], xr[c[t]], acc[t])
-                                    : __fadd_rn(acc[t], xr[c[t]]);
+        if (ok[t]) {
+          if constexpr (WGT) acc[t] = __fmaf_rn(__ldg(R.alpha + e * R.heads + h[t]), __ldg(xr + c[t]), acc[t]);
+          else acc[t] = __fadd_rn(acc[t], __ldg(xr + c[t]));
+        }
     }
 #pragma unroll
     for (int t = 0; t < NC; ++t)
@@ -777,17 +805,21 @@ static cudaError_t launch_gather(const GatherRow<OUT>& R, int64_t n, int chunk, 
   const int grid = grid_1d(n, 8);
   {
     ProfScope ps(light_name ? light_name : (OUT ? "out_dhp_light" : "out_agg_light"), st);
+#define GL(NC_)                                                                                   \
+    if (R.alpha) k_out_gather_light<OUT, true, NC_><<<grid, 256, 0, st>>>(R, n, chunk, out);       \
+    else k_out_gather_light<OUT, false, NC_><<<grid, 256, 0, st>>>(R, n, chunk, out);
     switch (nc) {
-      case 1: k_out_gather_light<OUT, 1><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
-      case 2: k_out_gather_light<OUT, 2><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
-      case 3: k_out_gather_light<OUT, 3><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
-      case 4: k_out_gather_light<OUT, 4><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
-      case 5: k_out_gather_light<OUT, 5><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
-      case 6: k_out_gather_light<OUT, 6><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
-      case 7: k_out_gather_light<OUT, 7><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
-      case 8: k_out_gather_light<OUT, 8><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
-      default: k_out_gather_light<OUT, 32><<<grid, 256, 0, st>>>(R, n, chunk, out); break;
+      case 1: GL(1) break;
+      case 2: GL(2) break;
+      case 3: GL(3) break;
+      case 4: GL(4) break;
+      case 5: GL(5) break;
+      case 6: GL(6) break;
+      case 7: GL(7) break;
+      case 8: GL(8) break;
+      default: GL(32) break;
     }
+#undef GL
   }
   {
     ProfScope ps(heavy_name ? heavy_name : (OUT ? "out_dhp_heavy" : "out_agg_heavy"), st);
