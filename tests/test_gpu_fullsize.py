@@ -116,3 +116,29 @@ def test_gat_train_step_arxiv_full_size(T, orc):
     da_ok(model.out_grads["a_src"], og["a_src"], og["da_src_abs"])
     da_ok(model.out_grads["a_dst"], og["a_dst"], og["da_dst_abs"])
     eq("out W updated", out_d["W"], r["out"]["W"])
+
+
+@pytest.mark.skipif(not __import__("os").environ.get("TANGO_FULL_PRODUCTS"),
+                    reason="set TANGO_FULL_PRODUCTS=1 (about 10 min: graph build + oracle on 123 M edges)")
+def test_gat_layer_products_full_size(T, orc):
+    """BASELINE.json configs[4] on one GPU (products-shaped: N = 2.45 M, E = 123 M, F = 100, 4 x 128,
+    tables 10x the L2): every output of the layer against the full oracle."""
+    kw, F, H, D = inputs.WORKLOADS["products"]
+    g = inputs.workload_graph("products")
+    W, a_s, a_d = inputs.gat_params(F, H, D)
+    X = inputs.features(g.n, F)
+    dY = inputs.grad_out(g.n, H * D)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    layer = T.GATLayer(T.DeviceGraph(g), cu(W), cu(a_s), cu(a_d), H, D, slope=0.2, bits=8)
+    Hout, _ = layer.forward(cu(X), step=1, layer_id=0)
+    dX, dW, das, dad = layer.backward(cu(dY), step=1, layer_id=0)
+    torch.cuda.synchronize()
+    layer.check_status()
+    f = orc.gat_fwd(g, X, W, a_s, a_d, H, D, slope=0.2, bits=8, step=1, layer_id=0, chunk=256)
+    eq("H_out", Hout, f["Hout"])
+    b = orc.gat_bwd(g, f, X, W, a_s, a_d, dY)
+    eq("dH", dX, b["dH"])
+    eq("dW", dW, b["dW"])
+    bound = 4096 * 2.0 ** -24
+    err = np.abs(das.cpu().numpy().astype(np.float64) - b["da_src"])
+    assert np.all(err <= bound * b["da_src_abs"] + 1e-7)
