@@ -314,7 +314,12 @@ def run_reference(args, rank, world):
     dH = inputs.grad_out(g.n, HD)
     cores = O.num_threads()
     # each step: the oracle (as it stands) on a bounded row sample of the same workload, scaled by edges
-    frac = min(1.0, args.ref_sample)
+    # bounded sample: by default sized so that the K + W oracle steps take about a minute in total
+    # (one full arxiv-shaped step is ~4 s on 16 host cores); --ref-sample fixes the fraction
+    if args.ref_sample is None:
+        frac = min(1.0, max(0.05, 60.0 / (4.0 * (args.steps + args.warmup))))
+    else:
+        frac = min(1.0, args.ref_sample)
     if frac < 1.0:
         gs = inputs.chung_lu_graph(**{**inputs.WORKLOADS[args.workload][0],
                                       "n": int(g.n * frac), "m": int(inputs.WORKLOADS[args.workload][0]["m"] * frac)})
@@ -375,7 +380,8 @@ def main():
     ap.add_argument("--no-train-step", "--layer-only", dest="no_train_step", action="store_true",
                     help="skip the extras (train_step, sddmm_bits): the layer step only")
     ap.add_argument("--nccl-single", action="store_true", help="N = 1 through a 1-rank NCCL communicator")
-    ap.add_argument("--ref-sample", type=float, default=1.0)
+    ap.add_argument("--ref-sample", type=float, default=None,
+                    help="fraction of the workload per oracle step (default: ~1 min for all K + W steps)")
     ap.add_argument("--profile-breakdown", action="store_true", help="print per-kernel times to stderr")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
