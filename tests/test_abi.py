@@ -78,3 +78,32 @@ def test_no_cpu_fallback(tmp_path):
             tango.load(str(tmp_path / "missing.so"))
     finally:
         tango._lib = saved
+
+
+def test_next_entry_points_validate_without_gpu(lib):
+    """Host-side argument validation of the NEXT-1 / NEXT-4 entry points returns before any CUDA call."""
+    from paper_2308_00890_b200 import tango as T
+    # tango_sgemm: bad layout -> INVALID_ARG, negative size -> SHAPE, missing workspace for K > 1024 -> INVALID_ARG
+    assert lib.tango_sgemm(1, 4, 7, 1, 4, 0, 4, 4, 4, 1, None, 0, None) == 1
+    assert lib.tango_sgemm(1, 4, 0, 1, 4, 0, -1, 4, 4, 1, None, 0, None) == 2
+    assert lib.tango_sgemm_workspace_bytes(64, 64, 1024) == 0
+    assert lib.tango_sgemm_workspace_bytes(64, 64, 1025) == 2 * 64 * 64 * 4
+    assert lib.tango_sgemm(1, 2048, 0, 1, 64, 1, 64, 64, 2048, 1, None, 0, None) == 1
+    # cross-entropy: classes > 1024 -> UNSUPPORTED, n_labeled > rows -> SHAPE
+    assert lib.tango_cross_entropy(1, 1, 10, 2000, 5, 1, 1, None, None) == 6
+    assert lib.tango_cross_entropy(1, 1, 10, 7, 11, 1, 1, None, None) == 2
+    # sgd: more than 32 tensors -> UNSUPPORTED
+    assert lib.tango_sgd_update(None, 33, 0.1, None) == 6
+    # FP32 final layers are one-GPU only: a partitioned graph view has no ctx size
+    g = T.Graph(100, 0, 50, 1, 1, 10, 1, 1, 1, 10, 256)
+    p = T.GatOutParams(1, 1, 1, 1, 16, 4, 40, 0.2)
+    assert lib.tango_gat_out_ctx_bytes(C.byref(g), C.byref(p)) == 0
+    g.row_end = 100
+    assert lib.tango_gat_out_ctx_bytes(C.byref(g), C.byref(p)) > 0
+    p.heads, p.classes = 8, 200                                   # H*C > 1024
+    assert lib.tango_gat_out_ctx_bytes(C.byref(g), C.byref(p)) == 0
+    gp = T.GcnOutParams(1, 1, 16, 7)
+    assert lib.tango_gcn_out_ctx_bytes(C.byref(g), C.byref(gp)) > 0
+    # INT4: cols not a multiple of 8 -> SHAPE; bits other than 4 / 8 -> BITS
+    assert lib.tango_quantize_int4(1, 4, 12, 0, None, T.Rng(0, 0, 0), 16, 8, 1, 1, None, None) == 2
+    assert lib.tango_sddmm_qn(C.byref(g), 1, 5, 16, 16, 16, 16, 16, 16, 4, 64, 0.2, 16, None, None) == 3
