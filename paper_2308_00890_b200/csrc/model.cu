@@ -145,7 +145,27 @@ __global__ void __launch_bounds__(256, 2) k_sgemm2(const float* __restrict__ A, 
 
   float4 ra[(A4 + 255) / 256], rb[(B4 + 255) / 256];
   // slot i of A: TA (A[k][m]): k = i / (BM/4), m4 = i % (BM/4);  !TA (A[m][k]): m = i / (BK/4), k4 = i % (BK/4)
+  const bool mn_in = avec && bvec && m0 + BM <= M && n0 + BN <= N;
   auto load = [&](int64_t k0) {
+    if (mn_in && k0 + BK <= kend) {   // interior tile: unpredicated 16-B loads
+#pragma unroll
+      for (int r = 0; r < (A4 + 255) / 256; ++r) {
+        const int i = t + 256 * r;
+        if (i < A4) {
+          if (TA) ra[r] = __ldg(reinterpret_cast<const float4*>(A + (k0 + i / (BM / 4)) * lda + m0 + (i % (BM / 4)) * 4));
+          else ra[r] = __ldg(reinterpret_cast<const float4*>(A + (m0 + i / (BK / 4)) * lda + k0 + (i % (BK / 4)) * 4));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < (B4 + 255) / 256; ++r) {
+        const int i = t + 256 * r;
+        if (i < B4) {
+          if (!TB) rb[r] = __ldg(reinterpret_cast<const float4*>(B + (k0 + i / (BN / 4)) * ldb + n0 + (i % (BN / 4)) * 4));
+          else rb[r] = __ldg(reinterpret_cast<const float4*>(B + (n0 + i / (BK / 4)) * ldb + k0 + (i % (BK / 4)) * 4));
+        }
+      }
+      return;
+    }
 #pragma unroll
     for (int r = 0; r < (A4 + 255) / 256; ++r) {
       const int i = t + 256 * r;
@@ -269,10 +289,22 @@ __global__ void __launch_bounds__(256, 2) k_sgemm2(const float* __restrict__ A, 
           const float2 v = *reinterpret_cast<const float2*>(&Bs[buf][kk][tx * TN + j]);
           b[j] = v.x; b[j + 1] = v.y;
         }
+        // packed FFMA2 (fma.rn.f32x2: two IEEE fmas per instruction, the 3-register FFMA issues at
+        // half rate): acc[i][j..j+1] = fma({a_i, a_i}, {b_j, b_j+1}, acc[i][j..j+1]) — the same
+        // per-output chain as the scalar form
 #pragma unroll
-        for (int i = 0; i < TM; ++i)
+        for (int i = 0; i < TM; ++i) {
+          uint64_t a2;
+          asm("mov.b64 %0, {%1, %1};" : "=l"(a2) : "f"(a[i]));
 #pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < TN; j += 2) {
+            uint64_t b2, c2;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(b2) : "f"(b[j]), "f"(b[j + 1]));
+            asm("mov.b64 %0, {%1, %2};" : "=l"(c2) : "f"(acc[i][j]), "f"(acc[i][j + 1]));
+            asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c2) : "l"(a2), "l"(b2));
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[i][j]), "=f"(acc[i][j + 1]) : "l"(c2));
+          }
+        }
       }
     } else {
       for (int kk = 0; kk < kmax; ++kk) {
