@@ -873,6 +873,21 @@ __global__ void k_out_logits(const float* __restrict__ agg, int64_t n, int heads
   }
 }
 
+// Wt[j][f] = W[f][j] (so that ∂H = ∂H′·Wᵀ reads its B operand row-major: 16-B shared stores)
+__global__ void k_transpose(const float* __restrict__ W, int64_t rows, int64_t cols, float* __restrict__ Wt) {
+  __shared__ float tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = W[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) Wt[c * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
 // G = ∂logits / heads (the gradient reaching every head's aggregation)
 __global__ void k_out_g(const float* __restrict__ dz, int64_t count, float heads, float* __restrict__ G) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
@@ -1057,7 +1072,7 @@ namespace {
 struct OutLayout {
   int64_t n, e, F, H, C, HC;
   size_t off_Hp, off_S, off_D, off_epre, off_el, off_alpha, off_m, off_den, off_G, off_dalpha, off_dEp, off_P,
-      off_dD, off_dS, off_dHp, off_agg, off_indst, off_hin, off_hout, off_cnt, off_ws, total;
+      off_dD, off_dS, off_dHp, off_agg, off_indst, off_hin, off_hout, off_cnt, off_Wt, off_ws, total;
 };
 inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 bool out_layout(const tango_graph* G, const tango_gat_out_params* p, OutLayout* L) {
@@ -1089,6 +1104,7 @@ bool out_layout(const tango_graph* G, const tango_gat_out_params* p, OutLayout* 
   L->off_hin = take(4 * n);
   L->off_hout = take(4 * n);
   L->off_cnt = take(4 * 8);
+  L->off_Wt = take(4 * F * HC);
   size_t ws = sgemm_ws_bytes(F, HC, n);
   ws = std::max(ws, sgemm_ws_bytes(n, F, HC));
   ws = std::max(ws, colsum_ws_bytes(n, L->C));
@@ -1373,7 +1389,15 @@ tango_status tango_gat_out_bwd(const tango_graph* G, const tango_gat_out_params*
     k_out_da<<<num_sms() * 2, 256, 0, stream>>>(Hp, L.n, H_, C_, dS, dD, da_src, da_dst);
   }
   // ①′ ∂H = ∂H′·Wᵀ (K = H·C), ∂W = Hᵀ·∂H′ (K = n, chunked) (R33)
-  if (dH) M_TRY_CUDA(launch_sgemm(dHp, L.HC, false, p->W, L.HC, true, L.n, L.F, L.HC, dH, ws, stream));
+  if (dH) {
+    float* Wt = reinterpret_cast<float*>(c + L.off_Wt);
+    {
+      ProfScope ps("transpose", stream);
+      k_transpose<<<dim3((unsigned)((L.HC + 31) / 32), (unsigned)((L.F + 31) / 32)), dim3(32, 8), 0, stream>>>(
+          p->W, L.F, L.HC, Wt);
+    }
+    M_TRY_CUDA(launch_sgemm(dHp, L.HC, false, Wt, L.F, false, L.n, L.F, L.HC, dH, ws, stream));
+  }
   M_TRY_CUDA(launch_sgemm(H, L.F, true, dHp, L.HC, false, L.F, L.HC, L.n, dW, ws, stream));
   return TANGO_OK;
 }
