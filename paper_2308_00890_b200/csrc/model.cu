@@ -634,6 +634,7 @@ __device__ void heavy_row_sums(int64_t len, int chunk, int heads, Op op, float* 
       const int h = (int)(it % heads);
       const int64_t i0 = c * chunk, i1 = min(len, i0 + chunk);
       float acc = 0.0f;
+#pragma unroll 8
       for (int64_t i = i0; i < i1; ++i) acc = op(acc, i, h);
       part[it] = acc;
     }
