@@ -238,3 +238,23 @@ def test_gcn_model_step_parity(T, orc, gspec, F, hid, layers, C, chunk):
     eq("out dW", model.out_grads["W"], r["out_grads"]["W"])
     eq("out W updated", out_d["W"], r["out"]["W"])
     eq("out b updated", out_d["b"], r["out"]["b"])
+
+
+def test_cross_entropy_no_labels_and_empty(T, orc):
+    # no labelled row: zero loss and zero gradient on both sides
+    z = _rand((50, 7), 71)
+    lab = np.full(50, -1, np.int32)
+    loss_w, dz_w, _ = orc.cross_entropy(z, lab, n_lab=0)
+    loss, dz = T.cross_entropy(cu(z), cu(lab), 0)
+    torch.cuda.synchronize()
+    eq("dlogits", dz, dz_w)
+    assert loss.item() == 0.0 and loss_w == 0.0
+
+
+def test_bias_act_and_sgd_zero_sizes(T):
+    x = torch.empty((0, 16), device="cuda")
+    y, am = T.bias_act_fwd(x, torch.zeros(16, device="cuda"))
+    dx, db, amd = T.bias_act_bwd(y, x)
+    torch.cuda.synchronize()
+    assert am.item() == 0.0 and amd.item() == 0.0 and torch.all(db == 0)
+    T.sgd_update([], 0.1)
