@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(256) k_bias_relu_fwd(const float* __restrict__
 // Warp per row; the exps of a row are staged in shared memory and summed by lane 0 in class order.
 constexpr int XE_MAXC = 1024;
 __global__ void __launch_bounds__(128) k_xent(const float* __restrict__ z, const int32_t* __restrict__ labels,
-                                              int64_t rows, int C, float inv_dummy, float n_lab,
+                                              int64_t rows, int C, float n_lab,
                                               float* __restrict__ dz, double* loss_acc, int32_t* status) {
   extern __shared__ float sh[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1215,7 +1215,7 @@ tango_status tango_cross_entropy(const float* logits, const int32_t* labels, int
   {
     ProfScope ps("cross_entropy", stream);
     const size_t smem = 4 * sizeof(float) * (size_t)classes;
-    k_xent<<<grid_1d(rows, 4), 128, smem, stream>>>(logits, labels, rows, classes, 0.0f,
+    k_xent<<<grid_1d(rows, 4), 128, smem, stream>>>(logits, labels, rows, classes,
                                                     n_labeled > 0 ? (float)n_labeled : 1.0f, dlogits, loss_out,
                                                     dev_status);
   }
