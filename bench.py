@@ -91,6 +91,18 @@ PASSES = {
     "gat_bwd_src": ["gat_bwd_src", "gat_bwd_src_hub", "gat_bwd_src_combine"],
 }
 
+def pass_profile(prof):
+    """{kernel: (total ms, launches)} -> the same with each gather pass's launches merged under the
+    pass name (time = sum of the member launches, launches = those of the light launch)."""
+    rprof = dict(prof)
+    for pname, members in PASSES.items():
+        if pname in rprof:
+            rprof[pname] = (sum(prof[m][0] for m in members if m in prof), prof[pname][1])
+            for m in members[1:]:
+                rprof.pop(m, None)
+    return rprof
+
+
 def kernel_model(name, g_e, n, F, H, HD, peaks, clock_mhz):
     """Algorithmic bytes and ALU lane-ops per launch of a kernel, or per gather PASS (all E edges; see
     PASSES) for the three gather passes.
@@ -550,12 +562,7 @@ def main():
     # A gather pass is split into launches (light sub-tiles; hub segments + folds on the side stream):
     # its bytes model covers all E edges, so the roofline unit is the PASS, timed as the sum of its
     # launches' serialised device times (one pass per step; launches counted by the light kernel).
-    rprof = dict(prof)
-    for pname, members in PASSES.items():
-        if pname in rprof:
-            rprof[pname] = (sum(prof[m][0] for m in members if m in prof), prof[pname][1])
-            for m in members[1:]:
-                rprof.pop(m, None)
+    rprof = pass_profile(prof)
     ranked = sorted(rprof.items(), key=lambda kv: -kv[1][0])
     dom, (dom_ms, dom_cnt) = ranked[0]
     skipped = []

@@ -1,0 +1,23 @@
+"""CPU checks of bench.py's measurement bookkeeping (no GPU): gather passes are timed as the sum of
+their launches, and every pass / kernel the roofline can pick has a bytes model."""
+import bench
+
+
+def test_pass_profile_merges_launches():
+    prof = {"gat_bwd_src": (2.0, 10), "gat_bwd_src_hub": (1.0, 10), "gat_bwd_src_combine": (0.25, 10),
+            "quantize": (2.5, 60), "gat_fwd_agg": (1.5, 10)}
+    r = bench.pass_profile(prof)
+    assert r["gat_bwd_src"] == (3.25, 10)
+    assert "gat_bwd_src_hub" not in r and "gat_bwd_src_combine" not in r
+    assert r["quantize"] == (2.5, 60) and r["gat_fwd_agg"] == (1.5, 10)
+
+
+def test_models_cover_the_roofline_candidates():
+    for name in list(bench.PASSES) + ["quantize", "absmax"]:
+        m = bench.kernel_model(name, 1000, 100, 128, 4, 512, {}, 1965.0)
+        assert m is not None and m[0] > 0 and m[1] > 0
+    assert bench.kernel_model("gat_bwd_src_hub", 1000, 100, 128, 4, 512, {}, 1965.0) is None
+    # the pass model counts every edge: bytes grow with E at the per-edge rate
+    b1 = bench.kernel_model("gat_bwd_src", 1000, 100, 128, 4, 512, {}, 1965.0)[0]
+    b2 = bench.kernel_model("gat_bwd_src", 2000, 100, 128, 4, 512, {}, 1965.0)[0]
+    assert b2 - b1 == 1000 * (8 + 8 * 4 + 512)
