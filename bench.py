@@ -39,9 +39,9 @@ def load_peaks():
         return PEAKS_FALLBACK, "fallback"
 
 
-def workload(name):
+def workload(name, order="random"):
     kw, F, H, D = inputs.WORKLOADS[name]
-    g = inputs.workload_graph(name)
+    g = inputs.workload_graph(name, order)
     return g, F, H, D
 
 
@@ -442,6 +442,8 @@ def main():
     ap.add_argument("--no-train-step", "--layer-only", dest="no_train_step", action="store_true",
                     help="skip the extras (train_step, sddmm_bits): the layer step only")
     ap.add_argument("--nccl-single", action="store_true", help="N = 1 through a 1-rank NCCL communicator")
+    ap.add_argument("--order", default="random", choices=["random", "degree"],
+                    help="node numbering: the recipe's random relabelling or by descending degree (NEXT-3)")
     ap.add_argument("--ref-sample", type=float, default=None,
                     help="fraction of the workload per oracle step (default: ~1 min for all K + W steps)")
     ap.add_argument("--profile-breakdown", action="store_true", help="print per-kernel times to stderr")
@@ -464,7 +466,7 @@ def main():
     T.load()
     peaks, peak_kind = load_peaks()
 
-    g, F, H, D = workload(args.workload)
+    g, F, H, D = workload(args.workload, args.order)
     HD = H * D
     starts = partition_rows(g, world)
     r0, r1 = starts[rank], starts[rank + 1]
@@ -705,7 +707,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
                 "vs_baseline": None, "dtype": "int8 (tcgen05 kind::i8, IDP4A) + fp32 accumulate/softmax",
                 "data": "synthetic (seeded Chung-Lu power-law graph, N(0,1) features, Glorot weights)",
-                "config": {"workload": f"{args.workload}-shaped GAT layer 1 (fwd+bwd)", "N": g.n, "E": g.e,
+                "config": {"workload": f"{args.workload}-shaped GAT layer 1 (fwd+bwd)" + (", degree-ordered ids" if args.order == "degree" else ""), "N": g.n, "E": g.e,
                            "F": F, "heads": H, "head_dim": D, "bits": 8, "chunk_edges": 256,
                            "parallelism": f"dst-row partition x{world}" if world > 1 else "1 GPU",
                            "l2": "flushed between timed steps (256 MB write)",

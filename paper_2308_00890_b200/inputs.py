@@ -148,9 +148,23 @@ WORKLOADS = {
 }
 
 
-def workload_graph(name: str) -> Graph:
+def workload_graph(name: str, order: str = "random") -> Graph:
+    """order "random": the seeded random relabelling of the recipe; "degree": the same graph with
+    nodes renumbered by descending in-degree (a locality relabelling)."""
     kw, _, _, _ = WORKLOADS[name]
-    return chung_lu_graph(**kw)
+    g = chung_lu_graph(**kw)
+    return relabel_by_degree(g) if order == "degree" else g
+
+
+def relabel_by_degree(g: Graph) -> Graph:
+    """Renumber nodes by descending in-degree (stable), keeping the edge set."""
+    deg = np.diff(g.in_ptr)
+    perm = np.argsort(-deg, kind="stable")          # new id i <- old id perm[i]
+    new_of = np.empty(g.n, dtype=np.int64)
+    new_of[perm] = np.arange(g.n, dtype=np.int64)
+    src = new_of[g.in_src.astype(np.int64)]
+    dst = new_of[g.in_dst().astype(np.int64)]
+    return build_csr(g.n, src, dst)
 
 
 def features(n: int, f: int, seed: int = SEED_FEAT) -> np.ndarray:
