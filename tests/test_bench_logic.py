@@ -21,3 +21,18 @@ def test_models_cover_the_roofline_candidates():
     b1 = bench.kernel_model("gat_bwd_src", 1000, 100, 128, 4, 512, {}, 1965.0)[0]
     b2 = bench.kernel_model("gat_bwd_src", 2000, 100, 128, 4, 512, {}, 1965.0)[0]
     assert b2 - b1 == 1000 * (8 + 8 * 4 + 512)
+
+
+def test_relabel_by_degree_is_a_permutation():
+    import numpy as np
+    from paper_2308_00890_b200 import inputs
+    g = inputs.random_graph(300, 1500, seed=9)
+    h = inputs.relabel_by_degree(g)
+    dg, dh = np.diff(g.in_ptr), np.diff(h.in_ptr)
+    assert h.e == g.e and np.all(np.diff(dh) <= 0)                      # degrees now descending
+    assert np.array_equal(np.sort(dg), np.sort(dh))                      # same degree multiset
+    assert np.array_equal(np.sort(np.diff(g.out_ptr)), np.sort(np.diff(h.out_ptr)))
+    # CSR invariants of the relabelled graph: sources ascending within each row
+    for v in range(h.n):
+        row = h.in_src[h.in_ptr[v]:h.in_ptr[v + 1]]
+        assert np.all(np.diff(row) > 0)
