@@ -276,19 +276,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               for (int i = 0; i < 8; ++i)
                 dst[i] = make_float4(deq(r[4 * i], sAB, has_rs, rs), deq(r[4 * i + 1], sAB, has_rs, rs),
                                      deq(r[4 * i + 2], sAB, has_rs, rs), deq(r[4 * i + 3], sAB, has_rs, rs));
-            } else {
-              for (int i = 0; i < 32 && col0 + i < p.N; ++i) Cf[row * p.ldc + col0 + i] = deq(r[i], sAB, has_rs, rs);
+            } else if (full_chunk && ((p.ldc & 1) == 0)) {   // 8-B aligned rows (e.g. F = 602)
+              float2* dst = reinterpret_cast<float2*>(Cf + row * p.ldc + col0);
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                dst[i] = make_float2(deq(r[2 * i], sAB, has_rs, rs), deq(r[2 * i + 1], sAB, has_rs, rs));
+            } else {   // unrolled with a predicate: r[] stays in registers
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (col0 + i < p.N) Cf[row * p.ldc + col0 + i] = deq(r[i], sAB, has_rs, rs);
             }
           }
         } else if constexpr (MODE == EPI_I32) {
           int32_t* Ci = reinterpret_cast<int32_t*>(p.C);
-          if (row_ok)
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i) Ci[row * p.ldc + col0 + i] = (int32_t)r[i];
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < p.N) Ci[row * p.ldc + col0 + i] = (int32_t)r[i];
+          }
         } else {  // EPI_ATOMIC64
           unsigned long long* C64 = reinterpret_cast<unsigned long long*>(p.C);
-          if (row_ok)
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i)
-              if (r[i] != 0u) atomicAdd(C64 + row * p.ldc + col0 + i, (unsigned long long)(long long)(int32_t)r[i]);
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < p.N && r[i] != 0u)
+                atomicAdd(C64 + row * p.ldc + col0 + i, (unsigned long long)(long long)(int32_t)r[i]);
+          }
         }
       }
       tc_fence_before();
