@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include <mutex>
@@ -817,10 +818,19 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   {
     const int64_t tiles = ((L.F + 127) / 128) * ((L.HD + 255) / 256);
     const int64_t kb = (L.n + 127) / 128;
-    int64_t splits = (num_sms() + tiles - 1) / tiles;
+    // CTAs per SM for the split-K ∂W GEMM: its cost is the int64 atomics of the split partials
+    // (splits x F x HD), not the MMAs; measured on arxiv (splitk 62 / 50 / 58 / 82 us at 1 / 0.5 /
+    // 0.25 / 0.125 CTAs per SM) -> default 0.5; TANGO_DW_CTAS_PER_SM overrides.
+    static const double per_sm = [] {
+      const char* e = getenv("TANGO_DW_CTAS_PER_SM");
+      const double v = e ? atof(e) : 0.5;
+      return v > 0 ? v : 0.5;
+    }();
+    int64_t splits = (int64_t)((num_sms() * per_sm + tiles - 1) / tiles);
     const int64_t min_splits = (L.n + 131071) / 131072;
     if (splits < min_splits) splits = min_splits;
     if (splits > kb) splits = kb > 0 ? kb : 1;
+    if (splits < 1) splits = 1;
     gw.splits = (int)splits;
   }
   gw.mode = EPI_ATOMIC64; gw.C = dW64; gw.ldc = L.HD;
