@@ -81,6 +81,11 @@ typedef struct {
   const int32_t* out_eid;
   int64_t e_out;
   int32_t chunk_edges;     /* C_E of the canonical chunked sums (reading R14); 0 => 256 */
+  /* Caller-chosen identity of this graph's CONTENTS for the static-plan cache (segment plans,
+   * in-CSR -> out-CSR map) kept in a layer ctx: two calls with the same ctx and the same nonzero
+   * graph_id reuse the plans built by the first; 0 rebuilds them on every call.  A caller that modifies
+   * the graph arrays in place must give the new contents a new id. */
+  uint64_t graph_id;
 } tango_graph;
 
 /* Quantized tensor (DS6): int8 codes [rows][ld] + DEVICE fp32 scale s,
@@ -269,9 +274,13 @@ typedef struct {
   int8_t *qH, *qW, *qWt, *qHp, *qS, *qD, *qG, *qdHp;
   int64_t ldF, ldHD, ldFt;
   float *S, *D, *m, *den, *P, *dD, *dHp, *dalpha;   /* dalpha: [e_in][H] ∂α */
-  float *alpha_pack;       /* [e_in][2H]: α (sign bit = LeakyReLU branch of e_pre) | ∂E_pre */
+  float *alpha_pack;       /* dataflow 1: [e_in][2H] α (sign bit = LeakyReLU branch of e_pre) | ∂E_pre;
+                              dataflow 2: [e_out][H] ∂α in out-CSR order (α, ∂E_pre are recomputed) */
   float *scalars;          /* see DESIGN.md §4 "ctx scalars" for the slot map */
   int32_t codes_biased;    /* 1: qHp and qG hold excess-128 codes (bit pattern q ^ 0x80) */
+  float *dS;               /* [n_global][H] ∂S (③′) of the owned rows */
+  int32_t dataflow;        /* 1: round-1 kernels (α stored); 2: v6 (single GPU, α recomputed, one
+                              row-gather pass in the backward) */
 } tango_gat_ctx_view;
 tango_status tango_gat_ctx_get_view(const tango_graph* G, const tango_gat_params* p, void* ctx,
                                     tango_gat_ctx_view* view);
@@ -443,6 +452,7 @@ void tango_profile_reset(void);
  * reduction) in order on the caller's stream instead, so that per-launch event times measure each
  * kernel alone (bench.py's per-kernel pass).  Results are identical either way.  Process-wide. */
 void tango_profile_serialize(int32_t on);
+
 
 #ifdef __cplusplus
 }

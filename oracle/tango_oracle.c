@@ -27,6 +27,9 @@
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
+
+/* chunk of the row/K-chunked FP32 sums of readings R33 and R39 (global rows) */
+#define ORC_CK 1024
 #endif
 
 #define ORC_OK 0
@@ -683,17 +686,25 @@ int orc_gat_bwd(const orc_graph* g, const orc_gat_cfg* c, const float* W, const 
       float t3 = o->dD[u * heads + h] * a_dst[j];
       o->dHp[u * HD + j] = t2 + t3;
     }
+  /* ∂a in the pinned order of reading R39 (= R33's row-chunked Σᶜ, chunk ORC_CK global rows):
+   * ∂a_src[j] = Σᶜ_u fmaf(∂S[u,h], deq(q_H′)[u,j], ·), deq = i2f(q)·s_H′ (one rounding) */
   for (int64_t j = 0; j < HD; ++j) {
     int64_t h = j / hd;
-    double as = 0.0, ad = 0.0, as_abs = 0.0, ad_abs = 0.0;
+    float as = 0.0f, ad = 0.0f, ps = 0.0f, pd = 0.0f;
+    double as_abs = 0.0, ad_abs = 0.0;
     for (int64_t u = 0; u < n; ++u) {
       float hp = QV(rHp, u * HD + j) * rHp.s;
-      double ts = (double)o->dS[u * heads + h] * (double)hp;
-      double td = (double)o->dD[u * heads + h] * (double)hp;
-      as += ts; ad += td; as_abs += fabs(ts); ad_abs += fabs(td);
+      ps = fmaf(o->dS[u * heads + h], hp, ps);
+      pd = fmaf(o->dD[u * heads + h], hp, pd);
+      as_abs += fabs((double)o->dS[u * heads + h] * (double)hp);
+      ad_abs += fabs((double)o->dD[u * heads + h] * (double)hp);
+      if ((u + 1) % ORC_CK == 0 || u + 1 == n) {   /* close the chunk, fold left to right */
+        if (u < ORC_CK) { as = ps; ad = pd; } else { as = as + ps; ad = ad + pd; }
+        ps = 0.0f; pd = 0.0f;
+      }
     }
-    o->da_src[j] = (float)as;
-    o->da_dst[j] = (float)ad;
+    o->da_src[j] = as;
+    o->da_dst[j] = ad;
     if (o->da_src_abs) o->da_src_abs[j] = (float)as_abs;
     if (o->da_dst_abs) o->da_dst_abs[j] = (float)ad_abs;
   }
@@ -828,7 +839,6 @@ void orc_set_threads(int t) {
  * Σᶜ of R14 with chunk ORC_CK = 1024 and FMA terms:
  *   C[m][n] = Σᶜ_k fmaf(A(m,k), B(k,n), ·)
  * A(m,k) = transA ? A[k*lda + m] : A[m*lda + k];  B(k,n) = transB ? B[n*ldb + k] : B[k*ldb + n]. */
-#define ORC_CK 1024
 void orc_sgemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, int transA, const float* B,
                int64_t ldb, int transB, float* C) {
 #pragma omp parallel for schedule(static)
@@ -983,16 +993,22 @@ int orc_gat_out_bwd(const orc_graph* g, const orc_out_cfg* c, const float* H, co
       float t3 = o->dD[u * heads + h] * a_dst[j];
       o->dHp[u * HC + j] = t2 + t3;
     }
-  for (int64_t j = 0; j < HC; ++j) {
+  for (int64_t j = 0; j < HC; ++j) {   /* ∂a in the pinned order of reading R39 (row-chunked Σᶜ) */
     int64_t h = j / C;
-    double as = 0.0, ad = 0.0, as_abs = 0.0, ad_abs = 0.0;
+    float as = 0.0f, ad = 0.0f, ps = 0.0f, pd = 0.0f;
+    double as_abs = 0.0, ad_abs = 0.0;
     for (int64_t u = 0; u < n; ++u) {
-      double ts = (double)o->dS[u * heads + h] * (double)f->Hp[u * HC + j];
-      double td = (double)o->dD[u * heads + h] * (double)f->Hp[u * HC + j];
-      as += ts; ad += td; as_abs += fabs(ts); ad_abs += fabs(td);
+      ps = fmaf(o->dS[u * heads + h], f->Hp[u * HC + j], ps);
+      pd = fmaf(o->dD[u * heads + h], f->Hp[u * HC + j], pd);
+      as_abs += fabs((double)o->dS[u * heads + h] * (double)f->Hp[u * HC + j]);
+      ad_abs += fabs((double)o->dD[u * heads + h] * (double)f->Hp[u * HC + j]);
+      if ((u + 1) % ORC_CK == 0 || u + 1 == n) {
+        if (u < ORC_CK) { as = ps; ad = pd; } else { as = as + ps; ad = ad + pd; }
+        ps = 0.0f; pd = 0.0f;
+      }
     }
-    o->da_src[j] = (float)as;
-    o->da_dst[j] = (float)ad;
+    o->da_src[j] = as;
+    o->da_dst[j] = ad;
     if (o->da_src_abs) o->da_src_abs[j] = (float)as_abs;
     if (o->da_dst_abs) o->da_dst_abs[j] = (float)ad_abs;
   }

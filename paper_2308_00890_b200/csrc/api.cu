@@ -123,6 +123,7 @@ int tango_abi_version(void) { return TANGO_ABI_VERSION; }
 
 void tango_profile_serialize(int32_t on) { g_serialize.store(on ? 1 : 0, std::memory_order_relaxed); }
 
+
 tango_status tango_status_poll(const int32_t* dev_status, cudaStream_t stream, tango_status* out) {
   if (!dev_status || !out) return TANGO_ERR_INVALID_ARG;
   int32_t v = 0;
@@ -489,6 +490,8 @@ struct GatLayout {
   // segment plans (gat.cu) and heavy-segment scratch
   size_t off_pin_hbase, off_pin_hseg, off_pin_hrow, off_pin_cnt, off_pout_hbase, off_pout_hseg, off_pout_hrow,
       off_pout_cnt, off_h1, off_h2, off_hdS, off_hagg, off_work, off_dS, off_alpha, off_pin_tiles, off_pout_tiles;
+  size_t off_hcnt, off_dapart;   // v6 dataflow: finished-segment counters [n], ∂a chunk partials
+  size_t off_nrec;               // packed per-node record [N][nrs] (the v6 in-CSR -> out-CSR map reuses off_dal)
   int64_t tcap;
 };
 GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
@@ -542,6 +545,9 @@ GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   L.tcap = L.n + L.n / 32 + 1;
   L.off_pin_tiles = take((size_t)L.tcap * 4);
   L.off_pout_tiles = take((size_t)L.tcap * 4);
+  L.off_hcnt = take((size_t)L.n * 4);
+  L.off_dapart = take((size_t)((L.n + 1023) / 1024 + 1) * 2 * L.HD * 4);
+  L.off_nrec = take((size_t)L.N * gat2_nrec_stride((int)L.H) * 4);
   L.total = o;
   return L;
 }
@@ -551,6 +557,79 @@ PlanDev plan_of(char* c, size_t hb, size_t hs, size_t hr, size_t cn, int64_t cap
   p.counts = (int32_t*)(c + cn); p.cap = cap;
   p.tiles = (int32_t*)(c + tl); p.tcap = tcap;
   return p;
+}
+// Static-graph plan cache: the segment plans (k_plan / k_plan_tiles of the in- and out-CSR) and the v6
+// in-CSR -> out-CSR map depend only on the graph, so a ctx keeps them across calls.  Keyed on the ctx,
+// the caller's graph_id (0 disables the cache) and the graph's device arrays and sizes.
+struct PlanKey {
+  const void* ctx; const int64_t* in_ptr; const int64_t* out_ptr; const int32_t* out_eid;
+  int64_t n, row_begin, e_in, e_out; int32_t chunk; uint64_t id;
+  bool operator==(const PlanKey& o) const {
+    return ctx == o.ctx && in_ptr == o.in_ptr && out_ptr == o.out_ptr && out_eid == o.out_eid && n == o.n &&
+           row_begin == o.row_begin && e_in == o.e_in && e_out == o.e_out && chunk == o.chunk && id == o.id;
+  }
+};
+struct PlanState { PlanKey key; bool in_done, out_done; };
+std::mutex g_plan_mu;
+std::vector<PlanState> g_plans;
+PlanKey plan_key(const void* ctx, const tango_graph* G) {
+  return PlanKey{ctx, G->in_ptr, G->out_ptr, G->out_eid, G->row_end - G->row_begin, G->row_begin, G->e_in, G->e_out,
+                 G->chunk_edges, G->graph_id};
+}
+// returns true if the plan `which` (0 = in-CSR, 1 = out-CSR) of this ctx/graph still has to be built, and
+// records it as built (the caller enqueues the build on the stream before any use)
+bool plan_needed(const void* ctx, const tango_graph* G, int which) {
+  if (G->graph_id == 0) return true;
+  const PlanKey k = plan_key(ctx, G);
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  for (auto& p : g_plans)
+    if (p.key.ctx == ctx) {
+      if (!(p.key == k)) { p.key = k; p.in_done = p.out_done = false; }
+      bool& done = which ? p.out_done : p.in_done;
+      const bool need = !done;
+      done = true;
+      return need;
+    }
+  g_plans.push_back(PlanState{k, which == 0, which == 1});
+  return true;
+}
+
+// v6 dataflow (gat2.cu) for single-GPU graphs with the edge-id map; TANGO_DATAFLOW=1 selects the
+// round-1 kernels (gat.cu) for A/B measurements.
+bool use_gat2(const GraphDev& g, const tango_gat_params* p, tango_comm* comm) {
+  static const int forced = [] {
+    const char* e = getenv("TANGO_DATAFLOW");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 1 || comm) return false;
+  const int HD = p->heads * p->head_dim;
+  return gat_codes_biased(p->heads, HD) && gat2_supported(g, p->heads, HD);
+}
+G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_params* p) {
+  G2Args a{};
+  unsigned* sc = reinterpret_cast<unsigned*>(c + L.off_scal);
+  a.g = g; a.d = {p->heads, p->head_dim, (int)L.HD}; a.slope = p->neg_slope; a.bits = p->bits;
+  a.qS = (int8_t*)(c + L.off_qS); a.amax_S = sc + SL_AMAX_S;
+  a.qD = (int8_t*)(c + L.off_qD); a.amax_D = sc + SL_AMAX_D;
+  a.qHp = (int8_t*)(c + L.off_qHp); a.ldHp = L.ldHD; a.amax_Hp = sc + SL_AMAX_HP;
+  a.qG = (int8_t*)(c + L.off_qG); a.ldG = L.ldHD; a.amax_G = sc + SL_AMAX_G;
+  a.m = (float*)(c + L.off_m); a.den = (float*)(c + L.off_den);
+  a.P = (float*)(c + L.off_P); a.dD = (float*)(c + L.off_dD); a.dS = (float*)(c + L.off_dS);
+  a.dal_out = (float*)(c + L.off_alpha);
+  a.a_src = p->a_src; a.a_dst = p->a_dst;
+  a.dHp = (float*)(c + L.off_dHp); a.amax_dHp = sc + SL_AMAX_DHP;
+  a.pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in, L.off_pin_tiles, L.tcap);
+  a.pout = plan_of(c, L.off_pout_hbase, L.off_pout_hseg, L.off_pout_hrow, L.off_pout_cnt, L.cap_out, L.off_pout_tiles,
+                   L.tcap);
+  a.hagg = (float*)(c + L.off_hagg);
+  a.h1 = (float*)(c + L.off_h1); a.h2 = (float*)(c + L.off_h2); a.hs = (float*)(c + L.off_hdS);
+  a.hcnt = (int32_t*)(c + L.off_hcnt);
+  a.work = (int32_t*)(c + L.off_work);
+  a.da_part = (float*)(c + L.off_dapart);
+  a.nrec = (float*)(c + L.off_nrec); a.nrs = gat2_nrec_stride(p->heads);
+  a.in2out = (const int32_t*)(c + L.off_dal);
+  a.codes_biased = 1;
+  return a;
 }
 tango_status check_gat(const tango_graph* G, const tango_gat_params* p) {
   TRY(check_graph(G, true));
@@ -592,6 +671,8 @@ tango_status tango_gat_ctx_get_view(const tango_graph* G, const tango_gat_params
   v->den = (float*)(c + L.off_den); v->P = (float*)(c + L.off_P); v->dD = (float*)(c + L.off_dD);
   v->dHp = (float*)(c + L.off_dHp); v->dalpha = (float*)(c + L.off_dal);
   v->alpha_pack = (float*)(c + L.off_alpha);
+  v->dS = (float*)(c + L.off_dS);
+  v->dataflow = use_gat2(dev_graph(G), p, nullptr) ? 2 : 1;
   v->scalars = (float*)(c + L.off_scal);
   v->codes_biased = gat_codes_biased(p->heads, (int)L.HD) ? 1 : 0;
   return TANGO_OK;
@@ -633,9 +714,11 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   TRY(launch_status(launch_quantize(p->W, L.F, L.HD, nullptr, 0, sc + SL_AMAX_W, p->bits, rng.seed, rng.step,
                                     tag_of(layer_id, R_W), qW, L.ldHD, qWt, L.ldFt, scf + SL_S_W, dev_status, aux->s)));
   TRY_CUDA(cudaEventRecord(aux->ev[1], aux->s));
-  TRY_CUDA(cudaMemsetAsync(pin.counts, 0, 16, aux->s));
-  TRY(launch_status(launch_plan(G->in_ptr, L.n, g.chunk, pin, aux->s)));
-  TRY(launch_status(launch_plan_tiles(G->in_ptr, L.n, pin, aux->s)));
+  if (plan_needed(ctx, G, 0)) {
+    TRY_CUDA(cudaMemsetAsync(pin.counts, 0, 16, aux->s));
+    TRY(launch_status(launch_plan(G->in_ptr, L.n, g.chunk, pin, aux->s)));
+    TRY(launch_status(launch_plan_tiles(G->in_ptr, L.n, pin, aux->s)));
+  }
   TRY_CUDA(cudaEventRecord(aux->ev[2], aux->s));
   // F1: amax(H) over all ranks (R28), Q(H)
   if (amax_H_hint) {
@@ -695,7 +778,12 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
   fa.alpha = (float*)(c + L.off_alpha);
   fa.codes_biased = biased;
   TRY_CUDA(cudaMemsetAsync(fa.work, 0, 64, st));
-  {
+  if (use_gat2(g, p, comm)) {
+    G2Args a2 = g2_args(L, c, g, p);
+    a2.Hout = H_out; a2.amax_out = reinterpret_cast<unsigned*>(amax_out);
+    TRY_CUDA(cudaMemsetAsync(a2.hcnt, 0, (size_t)L.n * 4, st));
+    TRY(launch_status(launch_gat2_fwd(a2, st)));
+  } else {
     const SideStream side = aux->side(4);
     TRY(launch_status(launch_gat_fwd(fa, st, &side)));
   }
@@ -744,9 +832,13 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
     const PlanDev pout = plan_of(c, L.off_pout_hbase, L.off_pout_hseg, L.off_pout_hrow, L.off_pout_cnt, L.cap_out,
                                  L.off_pout_tiles, L.tcap);
     TRY_CUDA(stream_after(aux->s, st, aux->ev[0]));
-    TRY_CUDA(cudaMemsetAsync(pout.counts, 0, 16, aux->s));
-    TRY(launch_status(launch_plan(G->out_ptr, L.n, g.chunk, pout, aux->s)));
-    TRY(launch_status(launch_plan_tiles(G->out_ptr, L.n, pout, aux->s)));
+    if (plan_needed(ctx, G, 1)) {
+      TRY_CUDA(cudaMemsetAsync(pout.counts, 0, 16, aux->s));
+      TRY(launch_status(launch_plan(G->out_ptr, L.n, g.chunk, pout, aux->s)));
+      TRY(launch_status(launch_plan_tiles(G->out_ptr, L.n, pout, aux->s)));
+      if (use_gat2(g, p, comm))
+        TRY(launch_status(launch_gat2_in2out(G->out_eid, L.E, (int32_t*)(c + L.off_dal), aux->s)));
+    }
     TRY_CUDA(cudaEventRecord(aux->ev[1], aux->s));
   }
   // B1: Q(∂H_out), shared by ⑤′ and ⑤″
@@ -782,15 +874,29 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
   ba.alpha_dE = (float*)(c + L.off_alpha);
   ba.codes_biased = biased;
   TRY_CUDA(cudaMemsetAsync(ba.work, 0, 64, st));
-  const SideStream side_d = aux->side(4), side_s = aux->side(6);
-  TRY(launch_status(launch_gat_bwd_dst(ba, st, &side_d)));
-  TRY(comm_gather_rows(comm, P, (size_t)L.H * 4, st));
-  TRY_CUDA(cudaStreamWaitEvent(st, aux->ev[1], 0));   // out-CSR plan done
-  TRY(launch_status(launch_gat_bwd_src(ba, st, &side_s)));
-  // ∂a (needs ∂S, ∂D) on the side stream, beside B8/B9
-  TRY_CUDA(stream_after(aux->s, st, aux->ev[2]));
-  TRY(launch_status(launch_gat_attn_grad(ba, aux->s)));
-  TRY_CUDA(cudaEventRecord(aux->ev[3], aux->s));
+  const bool v6 = use_gat2(g, p, comm);
+  if (v6) {
+    // P1 (⑤′ + ⑤″ on source rows), P2 (④′ + ③″ on destination rows), P3 (③′ + ②′ on source rows)
+    G2Args a2 = g2_args(L, c, g, p);
+    a2.da_src = da_src; a2.da_dst = da_dst;
+    TRY_CUDA(cudaMemsetAsync(a2.hcnt, 0, (size_t)L.n * 4, st));
+    TRY_CUDA(cudaStreamWaitEvent(st, aux->ev[1], 0));   // out-CSR plan and in-CSR -> out-CSR map done
+    TRY(launch_status(launch_gat2_bwd(a2, st)));
+    // ∂a (needs ∂S, ∂D; deterministic chunk order, R39) on the side stream, beside B8/B9
+    TRY_CUDA(stream_after(aux->s, st, aux->ev[2]));
+    TRY(launch_status(launch_gat2_attn_grad(a2, aux->s)));
+    TRY_CUDA(cudaEventRecord(aux->ev[3], aux->s));
+  } else {
+    const SideStream side_d = aux->side(4), side_s = aux->side(6);
+    TRY(launch_status(launch_gat_bwd_dst(ba, st, &side_d)));
+    TRY(comm_gather_rows(comm, P, (size_t)L.H * 4, st));
+    TRY_CUDA(cudaStreamWaitEvent(st, aux->ev[1], 0));   // out-CSR plan done
+    TRY(launch_status(launch_gat_bwd_src(ba, st, &side_s)));
+    // ∂a (needs ∂S, ∂D) on the side stream, beside B8/B9
+    TRY_CUDA(stream_after(aux->s, st, aux->ev[2]));
+    TRY(launch_status(launch_gat_attn_grad(ba, aux->s)));
+    TRY_CUDA(cudaEventRecord(aux->ev[3], aux->s));
+  }
   TRY(comm_max(comm, sc + SL_AMAX_DHP, 1, st));
   // B8: Q(∂H′)
   TRY(launch_status(launch_quantize(dHp, L.n, L.HD, nullptr, r0 * L.HD, sc + SL_AMAX_DHP, p->bits, rng.seed,

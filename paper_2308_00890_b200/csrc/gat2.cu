@@ -1,0 +1,1414 @@
+// gat2.cu — the single-GPU sparse half of the quantized GAT layer, v6 dataflow.
+//
+// Paper: ③ SDDMM-add + LeakyReLU, ④ edge softmax (FP32 per P:604-615),
+// ⑤ SPMM, ⑤′ SPMM on the reversed graph, ⑤″ SDDMM-dot on codes (P:252-255,
+// P:875-876), ④′ softmax backward, ③′/③″ incidence SPMM, ②′ (R23).
+//
+// Values are exactly those of the oracle (canonical chunked sums Σᶜ of reading R14, pinned fp32 ops);
+// only WHERE each value is computed differs from the round-1 kernels (gat.cu):
+//   * No edge-sized α array: every pass recomputes α[e,h] = exp_p(lrelu(e_pre) − m[v,h]) / den[v,h]
+//     from the int8 q_S, q_D rows and the per-node m, den — bit-identical to the stored value.
+//   * Forward = two kernels: F-stats (m, den per destination; hub rows by a whole CTA, light rows by
+//     warp tiles) and F-agg (⑤ with α recomputed; hub segments folded by the last finishing warp).
+//   * Backward = ONE row-gather pass instead of two: the SOURCE pass P1 gathers q_G[v] along out-edges
+//     of u and computes both ⑤′ (α·q_G[v] into ∂H′_agg[u]) and ⑤″ (∂α[e] = q_G[v]·q_H′[u] on codes, u's
+//     row held in registers), writing ∂α in out-CSR order (coalesced).  P2 (destination rows, no row
+//     gather; ∂α through the in-CSR -> out-CSR position map) folds P = Σᶜ fmaf(∂α, α) and
+//     ∂D = Σᶜ ∂E_pre; P3 (source rows, no row gather) folds ∂S = Σᶜ ∂E_pre and finalizes
+//     ∂H′ = (∂H′_agg + ∂S·a_src) + ∂D·a_dst.  For the Reddit-shaped layer this removes one 58.8 GB
+//     pass of int8 row gathers (the former destination-side SDDMM-dot).
+#include "gat_common.cuh"
+
+namespace tango {
+
+namespace {
+
+// ------------------------------------------------------------------ small helpers
+template <int H>
+__device__ __forceinline__ void ld_h(const float* __restrict__ p, float (&o)[H]) {
+  if constexpr (H == 4) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  } else if constexpr (H == 8) {
+    const float4 v = *reinterpret_cast<const float4*>(p), w = *reinterpret_cast<const float4*>(p + 4);
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; o[4] = w.x; o[5] = w.y; o[6] = w.z; o[7] = w.w;
+  } else if constexpr (H == 2) {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    o[0] = v.x; o[1] = v.y;
+  } else {
+#pragma unroll
+    for (int h = 0; h < H; ++h) o[h] = p[h];
+  }
+}
+template <int H>
+__device__ __forceinline__ void st_h(float* __restrict__ p, const float (&o)[H]) {
+  if constexpr (H == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+  } else if constexpr (H == 8) {
+    *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(o[4], o[5], o[6], o[7]);
+  } else if constexpr (H == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(o[0], o[1]);
+  } else {
+#pragma unroll
+    for (int h = 0; h < H; ++h) p[h] = o[h];
+  }
+}
+
+// per-destination data of the edge softmax: q_D row, m, den
+template <int H>
+struct DstSm {
+  int8_t qd[H];
+  float m[H], den[H];
+};
+template <int H>
+__device__ __forceinline__ DstSm<H> load_dst(const G2Args& a, int64_t vg) {
+  DstSm<H> d;
+  load_qh<H>(a.qD + vg * H, d.qd);
+  ld_h<H>(a.m + vg * H, d.m);
+  ld_h<H>(a.den + vg * H, d.den);
+  return d;
+}
+// the same from the packed per-node record (one 64-B block at H = 4: m, den in the first sector, P and q_D
+// in the second), for gathers of another node's data
+template <int H>
+__device__ __forceinline__ DstSm<H> load_rec(const G2Args& a, int64_t v) {
+  DstSm<H> d;
+  const float* r = a.nrec + v * a.nrs;
+  ld_h<H>(r, d.m);
+  ld_h<H>(r + H, d.den);
+  load_qh<H>(reinterpret_cast<const int8_t*>(r + 3 * H), d.qd);
+  return d;
+}
+template <int H>
+__device__ __forceinline__ void rec_put(const G2Args& a, int64_t v, int field, const float (&x)[H]) {
+  st_h<H>(a.nrec + v * a.nrs + field * H, x);
+}
+__device__ __forceinline__ void rec_put1(const G2Args& a, int64_t v, int field, int h, float x) {
+  a.nrec[v * a.nrs + field * a.d.heads + h] = x;
+}
+template <int H>
+__device__ __forceinline__ void rec_put_qd(const G2Args& a, int64_t v) {
+  int8_t* r = reinterpret_cast<int8_t*>(a.nrec + v * a.nrs + 3 * H);
+#pragma unroll
+  for (int h = 0; h < H; ++h) r[h] = a.qD[v * H + h];
+}
+
+// e_pre (③, two rn multiplies + one rn add) and α (④: exp_p(el − m) / den), all heads
+template <int H>
+__device__ __forceinline__ void alpha_rec(const int8_t (&qs)[H], const DstSm<H>& d, float sS, float sD, float slope,
+                                          float (&ep)[H], float (&al)[H]) {
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    ep[h] = sddmm_add1(qs[h], sS, d.qd[h], sD);
+    al[h] = __fdiv_rn(exp_p(__fsub_rn(lrelu(ep[h], slope), d.m[h])), d.den[h]);
+  }
+}
+
+template <int H>
+__host__ __device__ constexpr int hbatch() { return H >= 8 ? 32 : 64; }   // edges per staged batch of a hub chunk
+
+// ------------------------------------------------------------------ light tiles: segmented sums
+// A light sub-tile's rows form one edge stream t = 0..T-1 (TileLane).  For each 32-position batch every
+// lane computes the per-head values of its position; the row's owner lane then adds its row's part
+// of the batch sequentially (a light row is a single chunk of the canonical sum, reading R14).
+struct TileCtx {
+  TileLane L;
+  int T;
+  int64_t r0;
+};
+__device__ __forceinline__ int64_t tile_edge(const TileCtx& t, int pos, int& row) {
+  row = tile_row(pos < t.T ? pos : t.T - 1, t.L.end);
+  return __shfl_sync(0xffffffffu, t.L.eb, row) + (pos - __shfl_sync(0xffffffffu, t.L.off, row));
+}
+
+// sequential per-row fold of a staged 32-position batch: plain adds (FMA = false) of x, or fmaf(x, y, ·)
+template <int H, bool FMA>
+__device__ __forceinline__ void tile_fold(const TileCtx& t, int base, const float (*sx)[H], const float (*sy)[H],
+                                          float (&acc)[H]) {
+  const int cnt = t.T - base < 32 ? t.T - base : 32;
+  const int lo = (t.L.off > base ? t.L.off : base) - base;
+  const int hi = (t.L.end < base + cnt ? t.L.end : base + cnt) - base;
+  for (int i = lo; i < hi; ++i)
+#pragma unroll
+    for (int h = 0; h < H; ++h) acc[h] = FMA ? __fmaf_rn(sx[i][h], sy[i][h], acc[h]) : __fadd_rn(acc[h], sx[i][h]);
+}
+
+// ------------------------------------------------------------------ hub rows: per-segment partials
+// A hub row (degree > C_E) is cut into its canonical chunks ("segments", reading R14), each an
+// independent warp work item.  A segment's per-edge values are computed lane-parallel, two edges per
+// lane per batch of 64 (both edges' loads issued before either is used), staged in the warp's buffer,
+// and lane h < H adds head h's values of the batch in edge order: the chunk partial of Σᶜ.  The warp
+// whose segment completes the row last (atomic count per row) folds the row's partials in chunk order
+// (total = p_0, total = total + p_c) — bit-identical to the oracle's left-to-right fold.
+constexpr int SB = 64;   // edges per staged batch
+template <int H, bool FMA, typename LD, typename CV>
+__device__ __forceinline__ float seg_partial(int64_t eb, int64_t ee, float (*bx)[H], float (*by)[H], LD&& ld,
+                                             CV&& cv) {
+  const int lane = threadIdx.x & 31;
+  float acc = 0.0f;   // lane h < H: head h
+  const int cnt = (int)(ee - eb);
+  for (int b0 = 0; b0 < cnt; b0 += SB) {
+    const int bc = cnt - b0 < SB ? cnt - b0 : SB;
+    const bool v0 = lane < bc, v1 = lane + 32 < bc;
+    const auto l0 = ld(eb + b0 + (v0 ? lane : 0));
+    const auto l1 = ld(eb + b0 + (v1 ? lane + 32 : 0));
+    float x[H], y[H];
+    if (v0) {
+      cv(l0, x, y);
+#pragma unroll
+      for (int h = 0; h < H; ++h) { bx[lane][h] = x[h]; if (FMA) by[lane][h] = y[h]; }
+    }
+    if (v1) {
+      cv(l1, x, y);
+#pragma unroll
+      for (int h = 0; h < H; ++h) { bx[lane + 32][h] = x[h]; if (FMA) by[lane + 32][h] = y[h]; }
+    }
+    __syncwarp();
+    if (lane < H) {
+      int i = 0;
+      for (; i + 4 <= bc; i += 4) {
+        const float x0 = bx[i][lane], x1 = bx[i + 1][lane], x2 = bx[i + 2][lane], x3 = bx[i + 3][lane];
+        if (FMA) {
+          const float y0 = by[i][lane], y1 = by[i + 1][lane], y2 = by[i + 2][lane], y3 = by[i + 3][lane];
+          acc = __fmaf_rn(x0, y0, acc); acc = __fmaf_rn(x1, y1, acc);
+          acc = __fmaf_rn(x2, y2, acc); acc = __fmaf_rn(x3, y3, acc);
+        } else {
+          acc = __fadd_rn(acc, x0); acc = __fadd_rn(acc, x1); acc = __fadd_rn(acc, x2); acc = __fadd_rn(acc, x3);
+        }
+      }
+      for (; i < bc; ++i) acc = FMA ? __fmaf_rn(bx[i][lane], by[i][lane], acc) : __fadd_rn(acc, bx[i][lane]);
+    }
+    __syncwarp();
+  }
+  return acc;
+}
+// true (whole warp) for the warp that finished the row's last segment; resets the row's counter
+__device__ __forceinline__ bool seg_last(int32_t* cnt, int64_t row, int nseg) {
+  if (nseg == 1) return true;
+  __threadfence();
+  int d = 0;
+  if ((threadIdx.x & 31) == 0) d = atomicAdd(cnt + row, 1);
+  d = __shfl_sync(0xffffffffu, d, 0);
+  if (d != nseg - 1) return false;
+  __threadfence();
+  if ((threadIdx.x & 31) == 0) cnt[row] = 0;
+  return true;
+}
+// chunk-order fold of a row's per-segment partials [slot][H] (L2 reads: written by other SMs); lane h < H
+// returns head h's total
+template <int H>
+__device__ __forceinline__ float seg_fold(const float* part, int base, int nseg) {
+  const int lane = threadIdx.x & 31;
+  float tot = 0.0f;
+  for (int j0 = 0; j0 < nseg; j0 += 32 / H) {
+    // lanes load 32/H segments x H heads at once: lane = jj * H + h
+    const int jj = lane / H, h = lane % H, j = j0 + jj;
+    const float v = j < nseg ? __ldcg(part + (int64_t)(base + j) * H + h) : 0.0f;
+    const int cnt = nseg - j0 < 32 / H ? nseg - j0 : 32 / H;
+    for (int k = 0; k < cnt; ++k) {
+      const float y = __shfl_sync(0xffffffffu, v, k * H + (lane % H));
+      tot = (j0 + k == 0) ? y : __fadd_rn(tot, y);
+    }
+  }
+  return tot;   // valid in every lane for head lane % H
+}
+template <int H>
+__device__ __forceinline__ float seg_fold_max(const float* part, int base, int nseg) {
+  const int lane = threadIdx.x & 31;
+  float m = -INFINITY;
+  for (int j = lane / H; j < nseg; j += 32 / H) m = fmaxf(m, __ldcg(part + (int64_t)(base + j) * H + lane % H));
+#pragma unroll
+  for (int o = 16; o >= H; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  return m;   // every lane: max for head lane % H
+}
+
+}  // namespace
+
+// ================================================================== F-stats: m, den per destination
+// FS1 (hub segments): segment max of el = lrelu(e_pre); the row's last segment writes m = max over them.
+// FS2 (hub segments, then light sub-tiles): segment Σ exp_p(el − m) partial, folded in chunk order by the
+// row's last segment into den; a light sub-tile computes m and den of its rows in two lane-parallel passes
+// (per-row max by a segmented lane scan, Σ by the row's owner lane in edge order).
+template <int H>
+__global__ void __launch_bounds__(256, 4) k2_fstats1(const G2Args a) {
+  const int lane = threadIdx.x & 31;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t hc = load_count(a.pin.counts);
+  FOR_ITEMS(si, a.work + 0, hc) {
+    Seg s;
+    decode_item(si, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
+    const int64_t vg = a.g.row_begin + s.vl;
+    int8_t qd[H];
+    load_qh<H>(a.qD + vg * H, qd);
+    float mx[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) mx[h] = -INFINITY;
+    for (int64_t b = s.eb; b < s.ee; b += 128) {
+      int u[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) u[k] = b + 32 * k + lane < s.ee ? a.g.in_src[b + 32 * k + lane] : -1;
+      int8_t qs[4][H];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (u[k] >= 0) load_qh<H>(a.qS + (int64_t)u[k] * H, qs[k]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (u[k] >= 0)
+#pragma unroll
+          for (int h = 0; h < H; ++h) mx[h] = fmaxf(mx[h], lrelu(sddmm_add1(qs[k][h], scS.s, qd[h], scD.s), a.slope));
+    }
+#pragma unroll
+    for (int h = 0; h < H; ++h) mx[h] = warp_max(mx[h]);
+    if (lane < H) __stcg(a.h1 + (int64_t)s.slot * H + lane, head_pick<H>(mx, lane));
+    if (!seg_last(a.hcnt, s.vl, s.nseg)) continue;
+    const float m = seg_fold_max<H>(a.h1, s.base, s.nseg);
+    if (lane < H) {
+      a.m[vg * H + lane] = m;
+      rec_put1(a, vg, 0, lane, m);
+    }
+  }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256, 4) k2_fstats2(const G2Args a) {
+  __shared__ float sbx[8][SB][H];
+  __shared__ float tmx[8][32][H];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t n = a.g.n_local, hc = load_count(a.pin.counts), nitems = hc + load_count(a.pin.counts + 2);
+  FOR_ITEMS(item, a.work + 3, nitems) {
+    if (item < hc) {   // ---- hub segment
+      Seg s;
+      decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
+      const int64_t vg = a.g.row_begin + s.vl;
+      int8_t qd[H];
+      load_qh<H>(a.qD + vg * H, qd);
+      float m[H];
+      ld_h<H>(a.m + vg * H, m);
+      struct L { int8_t qs[H]; };
+      const float part = seg_partial<H, false>(
+          s.eb, s.ee, sbx[w], nullptr,
+          [&](int64_t e) { L l; load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs); return l; },
+          [&](const L& l, float (&x)[H], float (&)[H]) {
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+              x[h] = exp_p(__fsub_rn(lrelu(sddmm_add1(l.qs[h], scS.s, qd[h], scD.s), a.slope), m[h]));
+          });
+      if (lane < H) __stcg(a.h2 + (int64_t)s.slot * H + lane, part);
+      if (!seg_last(a.hcnt, s.vl, s.nseg)) continue;
+      const float den = seg_fold<H>(a.h2, s.base, s.nseg);
+      if (lane < H) {
+        a.den[vg * H + lane] = den;
+        rec_put1(a, vg, 1, lane, den);
+      }
+      if (lane == 0) rec_put_qd<H>(a, vg);
+      continue;
+    }
+    // ---- light sub-tile
+    const int32_t code = a.pin.tiles[item - hc];
+    TileCtx t;
+    t.r0 = (int64_t)(code >> 10) * TILE;
+    t.L = tile_setup(a.g.in_ptr, a.pin.hbase, t.r0, n, t.T, (code >> 5) & 31, (code & 31) + 1);
+    const int64_t vgl = a.g.row_begin + t.L.r;
+    float (*tbuf)[H] = reinterpret_cast<float (*)[H]>(&sbx[w][0][0]);
+    int qdj[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      qdj[h] = t.L.light ? (int)a.qD[vgl * H + h] : 0;
+      tmx[w][lane][h] = -INFINITY;
+    }
+    __syncwarp();
+    auto el_at = [&](int pos, float (&el)[H], int& row) {
+      const int64_t e = tile_edge(t, pos, row);
+      int qdr[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) qdr[h] = __shfl_sync(0xffffffffu, qdj[h], row);
+      if (pos < t.T) {
+        int8_t qs[H];
+        load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, qs);
+#pragma unroll
+        for (int h = 0; h < H; ++h) el[h] = lrelu(sddmm_add1(qs[h], scS.s, (int8_t)qdr[h], scD.s), a.slope);
+      } else {
+#pragma unroll
+        for (int h = 0; h < H; ++h) el[h] = -INFINITY;
+      }
+    };
+    for (int base = 0; base < t.T; base += 32) {   // pass A: per-row max (segmented lane scan)
+      float el[H];
+      int row;
+      el_at(base + lane, el, row);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ro = __shfl_up_sync(0xffffffffu, row, o);
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const float y = __shfl_up_sync(0xffffffffu, el[h], o);
+          if (lane >= o && ro == row) el[h] = fmaxf(el[h], y);
+        }
+      }
+      const int rn = __shfl_down_sync(0xffffffffu, row, 1);
+      if (base + lane < t.T && (lane == 31 || rn != row || base + lane + 1 >= t.T))
+#pragma unroll
+        for (int h = 0; h < H; ++h) tmx[w][row][h] = fmaxf(tmx[w][row][h], el[h]);
+      __syncwarp();
+    }
+    float mown[H], den[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      mown[h] = (t.L.light && t.L.deg > 0) ? tmx[w][lane][h] : 0.0f;
+      den[h] = 0.0f;
+    }
+    for (int base = 0; base < t.T; base += 32) {   // pass B: Σ exp_p(el − m) by the row owner
+      float el[H];
+      int row;
+      el_at(base + lane, el, row);
+      float mr[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) mr[h] = __shfl_sync(0xffffffffu, mown[h], row);
+      if (base + lane < t.T)
+#pragma unroll
+        for (int h = 0; h < H; ++h) tbuf[lane][h] = exp_p(__fsub_rn(el[h], mr[h]));
+      __syncwarp();
+      tile_fold<H, false>(t, base, tbuf, nullptr, den);
+      __syncwarp();
+    }
+    if (t.L.light) {
+      st_h<H>(a.m + vgl * H, mown);
+      st_h<H>(a.den + vgl * H, den);
+      rec_put<H>(a, vgl, 0, mown);
+      rec_put<H>(a, vgl, 1, den);
+      rec_put_qd<H>(a, vgl);
+    }
+  }
+}
+
+// ================================================================== gather engine (v8: cp.async, 8-edge groups)
+// One warp streams a heavy segment (one row, ≤ C_E edges) or a light sub-tile (≤ 32 rows).  Each lane
+// copies its own 16-B (VPL-byte) slice of every gathered row into a per-warp ring of RING = 16 rows
+// (two groups of GR = 8 edges) with cp.async (L2 only, evict_last: the gathered table is the one
+// structure worth keeping in L2), waits for the group with cp.async.wait_group and reads back only its
+// own bytes (no cross-lane synchronisation).  A group is always 8 edges: positions past the end of the
+// stream gather row 0 with α = +0, exact no-ops (fmaf(+0, q, acc) == acc; acc is never −0), so the hot
+// loop has no per-edge predicates; every group (possibly empty past the end) is committed, so
+// wait_group<1> always means "the current group has landed".  Per-edge attributes (gather row, α per
+// head, tile row, ...) are computed lane-parallel for 32-edge chunks: gather rows two chunks ahead,
+// attributes one chunk ahead, stashed in per-warp shared memory ([head][edge] for α).
+constexpr int GR = 8;       // edges per group
+constexpr int RING = 16;    // ring rows per warp (two groups)
+
+template <int VPL>
+__host__ __device__ constexpr int g8_ring_bytes() { return RING * 32 * VPL; }
+
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+template <int VPL>
+__device__ __forceinline__ void cp_slice_hint(uint32_t saddr, const int8_t* g, uint64_t pol) {
+  if constexpr (VPL == 16)
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "l"(pol) : "memory");
+  else if constexpr (VPL == 8)
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(saddr), "l"(g), "l"(pol) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(saddr), "l"(g), "l"(pol) : "memory");
+}
+// issue group g (rows sidx[8g .. 8g+7] of the chunk double buffer) into ring half g & 1, then commit
+template <int VPL>
+__device__ __forceinline__ void g8_fill(uint32_t ring_lane, const int8_t* lane_base, uint32_t ld, const int* sidx, int g,
+                                        bool any, uint64_t pol) {
+  if (any) {
+    const int* ix = sidx + (((8 * g) >> 5) & 1) * 32 + ((8 * g) & 31);
+    const int4 x0 = *reinterpret_cast<const int4*>(ix), x1 = *reinterpret_cast<const int4*>(ix + 4);
+    const int iv[GR] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    const uint32_t s0 = ring_lane + (uint32_t)(g & 1) * (GR * 32 * VPL);
+#pragma unroll
+    for (int j = 0; j < GR; ++j) cp_slice_hint<VPL>(s0 + j * 32 * VPL, lane_base + (uint32_t)iv[j] * ld, pol);
+  }
+  cp_commit();
+}
+template <int VPL>
+__device__ __forceinline__ void g8_rows(uint32_t ring_lane, int g, Row<VPL> (&r)[GR]) {
+  const uint32_t s0 = ring_lane + (uint32_t)(g & 1) * (GR * 32 * VPL);
+#pragma unroll
+  for (int j = 0; j < GR; ++j) r[j] = lds_row_slice<VPL>(s0 + j * 32 * VPL);
+}
+
+// ================================================================== F-agg: ⑤ with α recomputed
+// H_out[v] = (Σᶜ fmaf(α[e], q_H′[u]))·s_H′ over v's in-edges; α = exp_p(lrelu(e_pre) − m[v]) / den[v].
+template <int H, int VPL>
+__host__ __device__ constexpr int fa_warp_smem() {   // ring | α [2][H][32] | rows [2][32] | tile rows [2][32]
+  return g8_ring_bytes<VPL>() + 2 * H * 32 * 4 + 2 * 32 * 4 + 2 * 32;
+}
+template <int H, int VPL>
+__global__ void __launch_bounds__(256, 3) k2_fagg(const G2Args a) {
+  constexpr int HD = 32 * VPL, WS = fa_warp_smem<H, VPL>();
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int myh = lane / (32 / H);
+  uint8_t* wsm = dsm + w * ((WS + 15) & ~15);
+  float* sa = reinterpret_cast<float*>(wsm + g8_ring_bytes<VPL>());   // [2][H][32]
+  int* sidx = reinterpret_cast<int*>(sa + 2 * H * 32);                // [2][32]
+  uint8_t* srow = reinterpret_cast<uint8_t*>(sidx + 64);             // [2][32]
+  const uint32_t ring_lane = smem_u32(wsm) + lane * VPL;
+  const int8_t* lane_base = a.qHp + lane * VPL;
+  const uint32_t ld32 = (uint32_t)a.ldHp;
+  const uint64_t pol = l2_evict_last();
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t n = a.g.n_local, hc = load_count(a.pin.counts);
+  const int64_t nitems = hc + load_count(a.pin.counts + 2);
+  float amax_loc = 0.0f;
+  FOR_ITEMS(item, a.work + 1, nitems) {
+    const bool tile = item >= hc;
+    Seg s;
+    s.eb = 0; s.vl = 0; s.slot = -1; s.nseg = 1;
+    TileCtx t;
+    t.r0 = 0;
+    if (!tile) {
+      decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
+      t.T = (int)(s.ee - s.eb);
+      t.L.eb = 0; t.L.off = 0; t.L.end = 0;
+    } else {
+      const int32_t code = a.pin.tiles[item - hc];
+      t.r0 = (int64_t)(code >> 10) * TILE;
+      t.L = tile_setup(a.g.in_ptr, a.pin.hbase, t.r0, n, t.T, (code >> 5) & 31, (code & 31) + 1);
+      unsigned zm = __ballot_sync(0xffffffffu, t.L.light && t.L.deg == 0);
+      while (zm) {   // light rows without in-edges: H_out = 0
+        const int j = __ffs(zm) - 1;
+        zm &= zm - 1;
+        float4* dst = reinterpret_cast<float4*>(a.Hout + (t.r0 + j) * HD + lane * VPL);
+#pragma unroll
+        for (int k = 0; k < VPL / 4; ++k) __stcs(dst + k, make_float4(0.0f, 0.0f, 0.0f, 0.0f));
+      }
+    }
+    const int T = t.T;
+    if (T == 0) continue;
+    DstSm<H> dseg;
+    if (!tile) dseg = load_dst<H>(a, a.g.row_begin + s.vl);
+    // stream position -> (edge, tile row); gather row u (0 past the end)
+    auto pos_of = [&](int c, int& row) -> int64_t {
+      const int pos = c * 32 + lane;
+      if (tile) return tile_edge(t, pos, row);
+      row = 0;
+      return s.eb + (pos < T ? pos : T - 1);
+    };
+    auto alpha_of = [&](int c, int u, int row, float (&al)[H]) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) al[h] = 0.0f;
+      if (c * 32 + lane < T) {
+        const DstSm<H> d = tile ? load_dst<H>(a, a.g.row_begin + t.r0 + row) : dseg;
+        int8_t qs[H];
+        load_qh<H>(a.qS + (int64_t)u * H, qs);
+        float ep[H];
+        alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+      }
+    };
+    auto stash = [&](int c, int row, const float (&al)[H]) {
+      const int b = c & 1;
+#pragma unroll
+      for (int h = 0; h < H; ++h) sa[(b * H + h) * 32 + lane] = al[h];
+      srow[b * 32 + lane] = (uint8_t)row;
+    };
+    const int nch = (T + 31) >> 5, ng = (T + GR - 1) / GR;
+    // prologue: chunk 0 attributes, chunk 1 gather rows, first two groups
+    int row1, u1 = 0;
+    {
+      int row0;
+      const int64_t e0 = pos_of(0, row0);
+      const int u0 = lane < T ? __ldcs(a.g.in_src + e0) : 0;
+      float al0[H];
+      alpha_of(0, u0, row0, al0);
+      stash(0, row0, al0);
+      sidx[lane] = u0;
+      const int64_t e1 = pos_of(1, row1);
+      if (32 + lane < T) u1 = __ldcs(a.g.in_src + e1);
+      sidx[32 + lane] = u1;
+    }
+    __syncwarp();
+    g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, 0, true, pol);
+    g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, 1, 1 < ng, pol);
+    float2 acc[VPL / 2];
+#pragma unroll
+    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
+    auto flush = [&](int j) {   // tile row j done: H_out = acc · s_H′
+      float4* dst = reinterpret_cast<float4*>(a.Hout + (t.r0 + j) * HD + lane * VPL);
+      const float2 sH2 = make_float2(scH.s, scH.s);
+#pragma unroll
+      for (int k = 0; k < VPL / 4; ++k) {
+        const float2 o01 = __fmul2_rn(acc[2 * k], sH2), o23 = __fmul2_rn(acc[2 * k + 1], sH2);
+        amax_loc = fmaxf(amax_loc, fmaxf(fmaxf(fabsf(o01.x), fabsf(o01.y)), fmaxf(fabsf(o23.x), fabsf(o23.y))));
+        __stcs(dst + k, make_float4(o01.x, o01.y, o23.x, o23.y));
+        acc[2 * k] = make_float2(0.0f, 0.0f);
+        acc[2 * k + 1] = make_float2(0.0f, 0.0f);
+      }
+    };
+    int cur = tile ? -1 : 0;
+    for (int c = 0; c < nch; ++c) {
+      // loads for chunk c + 2's gather rows and chunk c + 1's attributes, used after this chunk's groups
+      int row2;
+      const int64_t e2 = pos_of(c + 2, row2);
+      const int u2 = (c + 2) * 32 + lane < T ? __ldcs(a.g.in_src + e2) : 0;
+      int8_t qs1[H];
+      int row1x = 0;
+      (void)pos_of(c + 1, row1x);
+      DstSm<H> d1 = dseg;
+      if ((c + 1) * 32 + lane < T) {
+        load_qh<H>(a.qS + (int64_t)u1 * H, qs1);
+        if (tile) d1 = load_dst<H>(a, a.g.row_begin + t.r0 + row1x);
+      }
+      const int b = c & 1;
+      const float* sac = sa + (b * H + myh) * 32;
+      for (int i0 = 0; i0 < 32; i0 += GR) {
+        const int t0 = c * 32 + i0;
+        if (t0 >= T) break;
+        const int g = t0 / GR;
+        cp_wait<1>();
+        const uint32_t s0 = ring_lane + (uint32_t)(g & 1) * (GR * 32 * VPL);
+        const float4 a4 = *reinterpret_cast<const float4*>(sac + i0);
+        const float4 b4 = *reinterpret_cast<const float4*>(sac + i0 + 4);
+        const float al[GR] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
+        bool same = true;
+        uint32_t rw0 = 0, rw1 = 0;
+        if (tile) {
+          rw0 = *reinterpret_cast<const uint32_t*>(srow + b * 32 + i0);
+          rw1 = *reinterpret_cast<const uint32_t*>(srow + b * 32 + i0 + 4);
+          same = (int)(rw0 & 0xffu) == cur && (int)(rw1 >> 24) == cur;
+        }
+        if (same) {
+#pragma unroll
+          for (int j = 0; j < GR; ++j) {
+            const Row<VPL> rj = lds_row_slice<VPL>(s0 + j * 32 * VPL);
+            const float2 al2 = make_float2(al[j], al[j]);
+#pragma unroll
+            for (int q = 0; q < VPL / 4; ++q) fma4_biased(rj.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < GR; ++j) {
+            const int rowj = (int)(((j < 4 ? rw0 : rw1) >> (8 * (j & 3))) & 0xffu);
+            if (rowj != cur) {
+              if (cur >= 0) flush(cur);
+              cur = rowj;
+            }
+            const Row<VPL> rj = lds_row_slice<VPL>(s0 + j * 32 * VPL);
+            const float2 al2 = make_float2(al[j], al[j]);
+#pragma unroll
+            for (int q = 0; q < VPL / 4; ++q) fma4_biased(rj.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+          }
+        }
+        g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, g + 2, g + 2 < ng, pol);
+      }
+      // attributes of chunk c + 1 (buffer (c+1)&1, last read by chunk c − 1) and rows of chunk c + 2
+      // (buffer c&1: chunk c's rows were last read by the refill after its first group)
+      __syncwarp();
+      if (c + 1 < nch) {
+        float al1[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) al1[h] = 0.0f;
+        if ((c + 1) * 32 + lane < T) {
+          float ep[H];
+          alpha_rec<H>(qs1, d1, scS.s, scD.s, a.slope, ep, al1);
+        }
+        stash(c + 1, row1x, al1);
+        sidx[b * 32 + lane] = u2;
+      }
+      __syncwarp();
+      u1 = u2;
+      (void)row2;
+    }
+    if (tile) {
+      if (cur >= 0) flush(cur);
+      continue;
+    }
+    // heavy segment: partial -> scratch; the row's last segment folds the partials in chunk order
+    {
+      float4* dst = reinterpret_cast<float4*>(a.hagg + (int64_t)s.slot * HD + lane * VPL);
+#pragma unroll
+      for (int k = 0; k < VPL / 4; ++k)
+        __stcg(dst + k, make_float4(acc[2 * k].x, acc[2 * k].y, acc[2 * k + 1].x, acc[2 * k + 1].y));
+    }
+    if (!seg_last(a.hcnt, s.vl, s.nseg)) continue;
+    float tot[VPL];
+    {
+      const float* p0 = a.hagg + (int64_t)s.base * HD + lane * VPL;
+#pragma unroll
+      for (int k = 0; k < VPL / 4; ++k) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(p0) + k);
+        tot[4 * k] = v.x; tot[4 * k + 1] = v.y; tot[4 * k + 2] = v.z; tot[4 * k + 3] = v.w;
+      }
+      for (int j = 1; j < s.nseg; ++j) {
+        const float4* pj = reinterpret_cast<const float4*>(p0 + (int64_t)j * HD);
+#pragma unroll
+        for (int k = 0; k < VPL / 4; ++k) {
+          const float4 v = __ldcg(pj + k);
+          tot[4 * k] = __fadd_rn(tot[4 * k], v.x); tot[4 * k + 1] = __fadd_rn(tot[4 * k + 1], v.y);
+          tot[4 * k + 2] = __fadd_rn(tot[4 * k + 2], v.z); tot[4 * k + 3] = __fadd_rn(tot[4 * k + 3], v.w);
+        }
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(a.Hout + s.vl * HD + lane * VPL);
+#pragma unroll
+    for (int k = 0; k < VPL / 4; ++k) {
+      float o[4];
+#pragma unroll
+      for (int z = 0; z < 4; ++z) {
+        o[z] = __fmul_rn(tot[4 * k + z], scH.s);
+        amax_loc = fmaxf(amax_loc, fabsf(o[z]));
+      }
+      __stcs(dst + k, make_float4(o[0], o[1], o[2], o[3]));
+    }
+  }
+  amax_flush(a.amax_out, amax_loc);
+}
+
+// ================================================================== P1: source rows, ⑤′ + ⑤″
+// Per out-edge e' = (u → v): gather q_G[v] (excess-128 codes); ∂α[e'] = i2f(q_G[v]·q_H′[u])·s_G s_H′ (u's
+// row in registers as plain codes, exact IDP4A dot + 4-edge transposed reduction); acc += α·q_G[v] with α
+// recomputed.  ∂α is written in out-CSR order (dal_out, coalesced; the destination pass P2 reads it through
+// the in-CSR -> out-CSR position map).  Rows: ∂H′_agg = acc·s_G into dHp (finalized by P3).
+template <int H, int VPL>
+__host__ __device__ constexpr int bs_warp_smem() {
+  // ring | α [2][H][32] | rows [2][32] | in-CSR slots [2][32] | out-CSR slots [2][32] | ∂α [H][32] | tile rows
+  return g8_ring_bytes<VPL>() + 2 * H * 32 * 4 + 3 * 2 * 32 * 4 + H * 32 * 4 + 2 * 32;
+}
+template <int H, int VPL, int NW>
+__global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
+  constexpr int HD = 32 * VPL, LPH = 32 / H, WS = bs_warp_smem<H, VPL>();
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int myh = lane / LPH;
+  uint8_t* wsm = dsm + w * ((WS + 15) & ~15);
+  float* sa = reinterpret_cast<float*>(wsm + g8_ring_bytes<VPL>());   // [2][H][32] α
+  int* sidx = reinterpret_cast<int*>(sa + 2 * H * 32);                // [2][32] gather rows (v)
+  int* seid = sidx + 64;                                              // [2][32] in-CSR position
+  int* seo = seid + 64;                                               // [2][32] out-CSR position
+  float* sd = reinterpret_cast<float*>(seo + 64);                     // [H][32] ∂α of the chunk
+  uint8_t* srow = reinterpret_cast<uint8_t*>(sd + H * 32);           // [2][32]
+  const uint32_t ring_lane = smem_u32(wsm) + lane * VPL;
+  const int8_t* lane_base = a.qG + lane * VPL;
+  const uint32_t ld32 = (uint32_t)a.ldG;
+  const uint64_t pol = l2_evict_last();
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const float sGH = __fmul_rn(scG.s, scH.s);
+  const int64_t n = a.g.n_local, hc = load_count(a.pout.counts);
+  const int64_t nitems = hc + load_count(a.pout.counts + 2);
+  const int8_t* obase = a.qHp + lane * VPL;      // own: q_H′[u] (excess-128 -> flipped to plain)
+  FOR_ITEMS(item, a.work + 2, nitems) {
+    const bool tile = item >= hc;
+    Seg s;
+    s.eb = 0; s.vl = 0; s.slot = -1; s.nseg = 1;
+    TileCtx t;
+    t.r0 = 0;
+    if (!tile) {
+      decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
+      t.T = (int)(s.ee - s.eb);
+      t.L.eb = 0; t.L.off = 0; t.L.end = 0; t.L.deg = 0; t.L.light = false;
+      t.r0 = s.vl;
+    } else {
+      const int32_t code = a.pout.tiles[item - hc];
+      t.r0 = (int64_t)(code >> 10) * TILE;
+      t.L = tile_setup(a.g.out_ptr, a.pout.hbase, t.r0, n, t.T, (code >> 5) & 31, (code & 31) + 1);
+      unsigned zm = __ballot_sync(0xffffffffu, t.L.light && t.L.deg == 0);
+      while (zm) {   // light rows without out-edges: ∂H′_agg = 0
+        const int j = __ffs(zm) - 1;
+        zm &= zm - 1;
+        float4* dst = reinterpret_cast<float4*>(a.dHp + (t.r0 + j) * HD + lane * VPL);
+#pragma unroll
+        for (int k = 0; k < VPL / 4; ++k) dst[k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
+    }
+    const int T = t.T;
+    if (T == 0) continue;
+    const int64_t ug0 = a.g.row_begin + t.r0;
+    int qsj[H];   // own row's q_S (tile lane j: row j; segment: the row)
+    {
+      const int64_t ugl = tile ? ug0 + lane : ug0;
+      const bool ok = tile ? t.L.light : true;
+#pragma unroll
+      for (int h = 0; h < H; ++h) qsj[h] = ok ? (int)a.qS[ugl * H + h] : 0;
+    }
+    auto pos_of = [&](int c, int& row) -> int64_t {
+      const int pos = c * 32 + lane;
+      if (tile) return tile_edge(t, pos, row);
+      row = 0;
+      return s.eb + (pos < T ? pos : T - 1);
+    };
+    // attributes of a chunk: α (needs v's softmax data), in-CSR slot, out-CSR slot, tile row
+    struct AttrIn { DstSm<H> d; int eid; };
+    auto attr_load = [&](int c, int v, int64_t e) {
+      AttrIn x;
+      x.eid = 0;
+      if (c * 32 + lane < T) {
+        x.eid = __ldcs(a.g.out_eid + e);
+        x.d = load_rec<H>(a, v);
+      }
+      return x;
+    };
+    auto attrs = [&](int c, int row, const AttrIn& x, float (&al)[H]) {
+      int8_t qs[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) qs[h] = (int8_t)(tile ? __shfl_sync(0xffffffffu, qsj[h], row) : qsj[h]);
+#pragma unroll
+      for (int h = 0; h < H; ++h) al[h] = 0.0f;
+      if (c * 32 + lane < T) {
+        float ep[H];
+        alpha_rec<H>(qs, x.d, scS.s, scD.s, a.slope, ep, al);
+      }
+    };
+    auto stash = [&](int c, int row, int eid, int64_t e, const float (&al)[H]) {
+      const int b = c & 1;
+#pragma unroll
+      for (int h = 0; h < H; ++h) sa[(b * H + h) * 32 + lane] = al[h];
+      srow[b * 32 + lane] = (uint8_t)row;
+      seid[b * 32 + lane] = eid;
+      seo[b * 32 + lane] = (int)e;
+    };
+    const int nch = (T + 31) >> 5, ng = (T + GR - 1) / GR;
+    int row1, v1 = 0;
+    int64_t e1;
+    {
+      int row0;
+      const int64_t e0 = pos_of(0, row0);
+      const int v0 = lane < T ? __ldcs(a.g.out_dst + e0) : 0;
+      float al0[H];
+      const AttrIn x0 = attr_load(0, v0, e0);
+      attrs(0, row0, x0, al0);
+      stash(0, row0, x0.eid, e0, al0);
+      sidx[lane] = v0;
+      e1 = pos_of(1, row1);
+      if (32 + lane < T) v1 = __ldcs(a.g.out_dst + e1);
+      sidx[32 + lane] = v1;
+    }
+    __syncwarp();
+    g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, 0, true, pol);
+    g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, 1, 1 < ng, pol);
+    // own q_H′[u] slice per row (plain codes + their sum for the excess-128 dot), prefetched a row ahead
+    const unsigned act = tile ? __ballot_sync(0xffffffffu, t.L.deg > 0) : 1u;
+    int nxt = act ? __ffs(act) - 1 : -1;
+    Row<VPL> ow{}, ow_nxt{};
+    int osum = 0;
+    if (nxt >= 0) ow_nxt = load_row<VPL>(obase + (ug0 + nxt) * a.ldHp);
+    int cur = -1;
+    if (!tile) {
+      cur = 0;
+      ow = ow_nxt;
+      osum = row_sum_plain<VPL>(ow, true);
+    }
+    float2 acc[VPL / 2];
+#pragma unroll
+    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
+    auto flush = [&](int j) {   // tile row j done: ∂H′_agg = acc · s_G
+      float4* dst = reinterpret_cast<float4*>(a.dHp + (t.r0 + j) * HD + lane * VPL);
+      const float2 s2 = make_float2(scG.s, scG.s);
+#pragma unroll
+      for (int k = 0; k < VPL / 4; ++k) {
+        const float2 o01 = __fmul2_rn(acc[2 * k], s2), o23 = __fmul2_rn(acc[2 * k + 1], s2);
+        dst[k] = make_float4(o01.x, o01.y, o23.x, o23.y);
+        acc[2 * k] = make_float2(0.0f, 0.0f);
+        acc[2 * k + 1] = make_float2(0.0f, 0.0f);
+      }
+    };
+    auto row_change = [&](int rj) {
+      if (cur >= 0) flush(cur);
+      cur = rj;
+      ow = ow_nxt;
+      osum = row_sum_plain<VPL>(ow, true);
+      nxt = tile_next(act, cur);
+      if (nxt >= 0) ow_nxt = load_row<VPL>(obase + (ug0 + nxt) * a.ldHp);
+    };
+    for (int c = 0; c < nch; ++c) {
+      int row2;
+      const int64_t e2 = pos_of(c + 2, row2);
+      const int v2 = (c + 2) * 32 + lane < T ? __ldcs(a.g.out_dst + e2) : 0;
+      const AttrIn x1 = attr_load(c + 1, v1, e1);
+      const int b = c & 1;
+      const float* sac = sa + (b * H + myh) * 32;
+      for (int i0 = 0; i0 < 32; i0 += GR) {
+        const int t0 = c * 32 + i0;
+        if (t0 >= T) break;
+        const int g = t0 / GR;
+        cp_wait<1>();
+        const uint32_t s0 = ring_lane + (uint32_t)(g & 1) * (GR * 32 * VPL);
+        const float4 a4 = *reinterpret_cast<const float4*>(sac + i0);
+        const float4 b4 = *reinterpret_cast<const float4*>(sac + i0 + 4);
+        const float al[GR] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
+        int d[GR];
+        bool same = true;
+        uint32_t rw0 = 0, rw1 = 0;
+        if (tile) {
+          rw0 = *reinterpret_cast<const uint32_t*>(srow + b * 32 + i0);
+          rw1 = *reinterpret_cast<const uint32_t*>(srow + b * 32 + i0 + 4);
+          same = (int)(rw0 & 0xffu) == cur && (int)(rw1 >> 24) == cur;
+        }
+        if (same) {
+#pragma unroll
+          for (int j = 0; j < GR; ++j) {
+            const Row<VPL> rj = lds_row_slice<VPL>(s0 + j * 32 * VPL);
+            d[j] = row_dot_biased<VPL>(rj, ow, osum);
+            const float2 al2 = make_float2(al[j], al[j]);
+#pragma unroll
+            for (int q = 0; q < VPL / 4; ++q) fma4_biased(rj.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < GR; ++j) {
+            const int rowj = (int)(((j < 4 ? rw0 : rw1) >> (8 * (j & 3))) & 0xffu);
+            if (rowj != cur) row_change(rowj);
+            const Row<VPL> rj = lds_row_slice<VPL>(s0 + j * 32 * VPL);
+            d[j] = row_dot_biased<VPL>(rj, ow, osum);
+            const float2 al2 = make_float2(al[j], al[j]);
+#pragma unroll
+            for (int q = 0; q < VPL / 4; ++q) fma4_biased(rj.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+          }
+        }
+        {
+          int k;
+          const int d0[4] = {d[0], d[1], d[2], d[3]}, d1[4] = {d[4], d[5], d[6], d[7]};
+          const int x0 = group_dot_reduce<LPH>(d0, k);
+          const int x1 = group_dot_reduce<LPH>(d1, k);
+          sd[myh * 32 + i0 + k] = __fmul_rn(__int2float_rn(x0), sGH);
+          sd[myh * 32 + i0 + 4 + k] = __fmul_rn(__int2float_rn(x1), sGH);
+        }
+        g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, g + 2, g + 2 < ng, pol);
+      }
+      __syncwarp();
+      if (c * 32 + lane < T) {   // ∂α of this chunk: out-CSR order (coalesced) and the edge's in-CSR slot
+        float o[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) o[h] = sd[h * 32 + lane];
+        st_h<H>(a.dal_out + (int64_t)seo[b * 32 + lane] * H, o);
+
+      }
+      __syncwarp();
+      if (c + 1 < nch) {
+        float al1[H];
+        attrs(c + 1, row1, x1, al1);
+        stash(c + 1, row1, x1.eid, e1, al1);
+        sidx[b * 32 + lane] = v2;
+      }
+      __syncwarp();
+      v1 = v2; e1 = e2; row1 = row2;
+    }
+    if (tile) {
+      if (cur >= 0) flush(cur);
+      continue;
+    }
+    {
+      float4* dst = reinterpret_cast<float4*>(a.hagg + (int64_t)s.slot * HD + lane * VPL);
+#pragma unroll
+      for (int k = 0; k < VPL / 4; ++k)
+        __stcg(dst + k, make_float4(acc[2 * k].x, acc[2 * k].y, acc[2 * k + 1].x, acc[2 * k + 1].y));
+    }
+    if (!seg_last(a.hcnt, s.vl, s.nseg)) continue;
+    float tot[VPL];
+    {
+      const float* p0 = a.hagg + (int64_t)s.base * HD + lane * VPL;
+#pragma unroll
+      for (int k = 0; k < VPL / 4; ++k) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(p0) + k);
+        tot[4 * k] = v.x; tot[4 * k + 1] = v.y; tot[4 * k + 2] = v.z; tot[4 * k + 3] = v.w;
+      }
+      for (int j = 1; j < s.nseg; ++j) {
+        const float4* pj = reinterpret_cast<const float4*>(p0 + (int64_t)j * HD);
+#pragma unroll
+        for (int k = 0; k < VPL / 4; ++k) {
+          const float4 v = __ldcg(pj + k);
+          tot[4 * k] = __fadd_rn(tot[4 * k], v.x); tot[4 * k + 1] = __fadd_rn(tot[4 * k + 1], v.y);
+          tot[4 * k + 2] = __fadd_rn(tot[4 * k + 2], v.z); tot[4 * k + 3] = __fadd_rn(tot[4 * k + 3], v.w);
+        }
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(a.dHp + s.vl * HD + lane * VPL);
+#pragma unroll
+    for (int k = 0; k < VPL / 4; ++k)
+      dst[k] = make_float4(__fmul_rn(tot[4 * k], scG.s), __fmul_rn(tot[4 * k + 1], scG.s),
+                           __fmul_rn(tot[4 * k + 2], scG.s), __fmul_rn(tot[4 * k + 3], scG.s));
+  }
+}
+
+// ================================================================== P2: destination rows, ④′ + ③″
+// P[v] = Σᶜ fmaf(∂α, α) over in-edges (in-CSR order), ∂E = α(∂α − P[v]), ∂E_pre = e_pre > 0 ? ∂E : ∂E·slope,
+// ∂D[v] = Σᶜ ∂E_pre.  ∂α = dal_out[in2out[e]] (written by P1), α recomputed.
+// P2a: hub segments (P partials, folded by the row's last segment) and light sub-tiles (P and ∂D);
+// P2b: hub segments (∂D partials with the row's P, folded likewise).
+template <int H>
+struct EdgeIn { int8_t qs[H]; float da[H]; };
+
+template <int H>
+__global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
+  __shared__ float sbx[8][SB][H];
+  __shared__ float sby[8][SB][H];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t n = a.g.n_local, hc = load_count(a.pin.counts), nitems = hc + load_count(a.pin.counts + 2);
+  FOR_ITEMS(item, a.work + 3, nitems) {
+    if (item < hc) {   // ---- hub segment: P partial
+      Seg s;
+      decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
+      const int64_t vg = a.g.row_begin + s.vl;
+      const DstSm<H> d = load_dst<H>(a, vg);
+      const float part = seg_partial<H, true>(
+          s.eb, s.ee, sbx[w], sby[w],
+          [&](int64_t e) {
+            EdgeIn<H> l;
+            load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs);
+            ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, l.da);
+            return l;
+          },
+          [&](const EdgeIn<H>& l, float (&x)[H], float (&y)[H]) {
+            float ep[H];
+            alpha_rec<H>(l.qs, d, scS.s, scD.s, a.slope, ep, y);
+#pragma unroll
+            for (int h = 0; h < H; ++h) x[h] = l.da[h];
+          });
+      if (lane < H) __stcg(a.h1 + (int64_t)s.slot * H + lane, part);
+      if (!seg_last(a.hcnt, s.vl, s.nseg)) continue;
+      const float P = seg_fold<H>(a.h1, s.base, s.nseg);
+      if (lane < H) {
+        a.P[vg * H + lane] = P;
+        rec_put1(a, vg, 2, lane, P);
+      }
+      continue;
+    }
+    // ---- light sub-tile: P and ∂D of its rows
+    const int32_t code = a.pin.tiles[item - hc];
+    TileCtx t;
+    t.r0 = (int64_t)(code >> 10) * TILE;
+    t.L = tile_setup(a.g.in_ptr, a.pin.hbase, t.r0, n, t.T, (code >> 5) & 31, (code & 31) + 1);
+    const int64_t vgl = a.g.row_begin + t.L.r;
+    float (*tbx)[H] = reinterpret_cast<float (*)[H]>(&sbx[w][0][0]);
+    float (*tby)[H] = reinterpret_cast<float (*)[H]>(&sby[w][0][0]);
+    DstSm<H> dj;
+    if (t.L.light) dj = load_dst<H>(a, vgl);
+    else {
+#pragma unroll
+      for (int h = 0; h < H; ++h) { dj.qd[h] = 0; dj.m[h] = 0.0f; dj.den[h] = 1.0f; }
+    }
+    auto edge_vals = [&](int pos, float (&da)[H], float (&al)[H], float (&ep)[H], int& row) {
+      const int64_t e = tile_edge(t, pos, row);
+      DstSm<H> d;
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        d.qd[h] = (int8_t)__shfl_sync(0xffffffffu, (int)dj.qd[h], row);
+        d.m[h] = __shfl_sync(0xffffffffu, dj.m[h], row);
+        d.den[h] = __shfl_sync(0xffffffffu, dj.den[h], row);
+      }
+      if (pos < t.T) {
+        int8_t qs[H];
+        load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, qs);
+        ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, da);
+        alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+      }
+    };
+    float P[H], dD[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) { P[h] = 0.0f; dD[h] = 0.0f; }
+    for (int base = 0; base < t.T; base += 32) {
+      float da[H], al[H], ep[H];
+      int row;
+      edge_vals(base + lane, da, al, ep, row);
+      if (base + lane < t.T)
+#pragma unroll
+        for (int h = 0; h < H; ++h) { tbx[lane][h] = da[h]; tby[lane][h] = al[h]; }
+      __syncwarp();
+      tile_fold<H, true>(t, base, tbx, tby, P);
+      __syncwarp();
+    }
+    for (int base = 0; base < t.T; base += 32) {
+      float da[H], al[H], ep[H];
+      int row;
+      edge_vals(base + lane, da, al, ep, row);
+      float Pr[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) Pr[h] = __shfl_sync(0xffffffffu, P[h], row);
+      if (base + lane < t.T)
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const float dE = __fmul_rn(al[h], __fsub_rn(da[h], Pr[h]));
+          tbx[lane][h] = ep[h] > 0.0f ? dE : __fmul_rn(dE, a.slope);
+        }
+      __syncwarp();
+      tile_fold<H, false>(t, base, tbx, nullptr, dD);
+      __syncwarp();
+    }
+    if (t.L.light) {
+      st_h<H>(a.P + vgl * H, P);
+      st_h<H>(a.dD + vgl * H, dD);
+      rec_put<H>(a, vgl, 2, P);
+    }
+  }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256, 4) k2_bdst_b(const G2Args a) {
+  __shared__ float sbx[8][SB][H];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t hc = load_count(a.pin.counts);
+  FOR_ITEMS(si, a.work + 4, hc) {
+    Seg s;
+    decode_item(si, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
+    const int64_t vg = a.g.row_begin + s.vl;
+    const DstSm<H> d = load_dst<H>(a, vg);
+    float P[H];
+    ld_h<H>(a.P + vg * H, P);
+    const float part = seg_partial<H, false>(
+        s.eb, s.ee, sbx[w], nullptr,
+        [&](int64_t e) {
+          EdgeIn<H> l;
+          load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs);
+          ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, l.da);
+          return l;
+        },
+        [&](const EdgeIn<H>& l, float (&x)[H], float (&)[H]) {
+          float ep[H], al[H];
+          alpha_rec<H>(l.qs, d, scS.s, scD.s, a.slope, ep, al);
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            const float dE = __fmul_rn(al[h], __fsub_rn(l.da[h], P[h]));
+            x[h] = ep[h] > 0.0f ? dE : __fmul_rn(dE, a.slope);
+          }
+        });
+    if (lane < H) __stcg(a.h2 + (int64_t)s.slot * H + lane, part);
+    if (!seg_last(a.hcnt, s.vl, s.nseg)) continue;
+    const float dD = seg_fold<H>(a.h2, s.base, s.nseg);
+    if (lane < H) a.dD[vg * H + lane] = dD;
+  }
+}
+
+// ================================================================== P3: source rows, ③′ + ②′
+// ∂S[u] = Σᶜ ∂E_pre over out-edges (out-CSR order), ∂E_pre recomputed from ∂α (dal_out), α, P[v]; then
+// ∂H′[u] = (∂H′_agg[u] + ∂S·a_src) + ∂D[u]·a_dst in place over dHp (one warp per row), amax(∂H′).
+template <int H, int VPL>
+__device__ __forceinline__ void src_finalize_row(const G2Args& a, int64_t ul, const float (&dS)[H], float& amax_loc) {
+  constexpr int HD = 32 * VPL, LPH = 32 / H;
+  const int lane = threadIdx.x & 31;
+  const int64_t ug = a.g.row_begin + ul;
+  const int myh = lane / LPH;
+  const float dSh = head_pick<H>(dS, myh);
+  const float dD = a.dD[ug * H + myh];
+  const int c0 = lane * VPL;
+  float4* p = reinterpret_cast<float4*>(a.dHp + ul * HD + c0);
+  const float4* as = reinterpret_cast<const float4*>(a.a_src + c0);
+  const float4* ad = reinterpret_cast<const float4*>(a.a_dst + c0);
+#pragma unroll
+  for (int k = 0; k < VPL / 4; ++k) {
+    const float4 g4 = p[k], s4 = __ldg(as + k), d4 = __ldg(ad + k);
+    const float v[4] = {g4.x, g4.y, g4.z, g4.w}, sv[4] = {s4.x, s4.y, s4.z, s4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+    float o[4];
+#pragma unroll
+    for (int z = 0; z < 4; ++z) {
+      const float t2 = __fadd_rn(v[z], __fmul_rn(dSh, sv[z]));
+      o[z] = __fadd_rn(t2, __fmul_rn(dD, dv[z]));
+      amax_loc = fmaxf(amax_loc, fabsf(o[z]));
+    }
+    p[k] = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+template <int H>
+struct EdgeOut { int v; float da[H]; };
+
+template <int H, int VPL>
+__global__ void __launch_bounds__(256, 3) k2_bsrc2(const G2Args a) {
+  __shared__ float sbx[8][SB][H];
+  __shared__ float tS[8][32][H];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t n = a.g.n_local, hc = load_count(a.pout.counts), nitems = hc + load_count(a.pout.counts + 2);
+  float amax_loc = 0.0f;
+  // ∂E_pre of out-edge e' = (u → v) with u's q_S
+  auto dEp = [&](int v, const float (&da)[H], const int8_t (&qs)[H], float (&x)[H]) {
+    const DstSm<H> d = load_rec<H>(a, v);
+    float ep[H], al[H], Pv[H];
+    ld_h<H>(a.nrec + (int64_t)v * a.nrs + 2 * H, Pv);
+    alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const float dE = __fmul_rn(al[h], __fsub_rn(da[h], Pv[h]));
+      x[h] = ep[h] > 0.0f ? dE : __fmul_rn(dE, a.slope);
+    }
+  };
+  FOR_ITEMS(item, a.work + 6, nitems) {
+    if (item < hc) {   // ---- hub segment: ∂S partial; the row's last segment folds and finalizes
+      Seg s;
+      decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
+      const int64_t ug = a.g.row_begin + s.vl;
+      int8_t qs[H];
+      load_qh<H>(a.qS + ug * H, qs);
+      const float part = seg_partial<H, false>(
+          s.eb, s.ee, sbx[w], nullptr,
+          [&](int64_t e) {
+            EdgeOut<H> l;
+            l.v = a.g.out_dst[e];
+            ld_h<H>(a.dal_out + e * H, l.da);
+            return l;
+          },
+          [&](const EdgeOut<H>& l, float (&x)[H], float (&)[H]) { dEp(l.v, l.da, qs, x); });
+      if (lane < H) __stcg(a.hs + (int64_t)s.slot * H + lane, part);
+      if (!seg_last(a.hcnt, s.vl, s.nseg)) continue;
+      const float tot = seg_fold<H>(a.hs, s.base, s.nseg);
+      float dS[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) dS[h] = __shfl_sync(0xffffffffu, tot, h);
+      if (lane < H) a.dS[ug * H + lane] = tot;
+      src_finalize_row<H, VPL>(a, s.vl, dS, amax_loc);
+      continue;
+    }
+    // ---- light sub-tile
+    const int32_t code = a.pout.tiles[item - hc];
+    TileCtx t;
+    t.r0 = (int64_t)(code >> 10) * TILE;
+    t.L = tile_setup(a.g.out_ptr, a.pout.hbase, t.r0, n, t.T, (code >> 5) & 31, (code & 31) + 1);
+    const int64_t ugl = a.g.row_begin + t.L.r;
+    float (*tbx)[H] = reinterpret_cast<float (*)[H]>(&sbx[w][0][0]);
+    int qsj[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) qsj[h] = t.L.light ? (int)a.qS[ugl * H + h] : 0;
+    float dS[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) dS[h] = 0.0f;
+    for (int base = 0; base < t.T; base += 32) {
+      int row;
+      const int64_t e = tile_edge(t, base + lane, row);
+      int8_t qs[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) qs[h] = (int8_t)__shfl_sync(0xffffffffu, qsj[h], row);
+      if (base + lane < t.T) {
+        float da[H], x[H];
+        ld_h<H>(a.dal_out + e * H, da);
+        dEp(a.g.out_dst[e], da, qs, x);
+#pragma unroll
+        for (int h = 0; h < H; ++h) tbx[lane][h] = x[h];
+      }
+      __syncwarp();
+      tile_fold<H, false>(t, base, tbx, nullptr, dS);
+      __syncwarp();
+    }
+    if (t.L.light) st_h<H>(a.dS + ugl * H, dS);
+#pragma unroll
+    for (int h = 0; h < H; ++h) tS[w][lane][h] = dS[h];
+    __syncwarp();
+    const unsigned lm = __ballot_sync(0xffffffffu, t.L.light);   // finalize the light rows, a warp per row
+    for (unsigned mm = lm; mm; mm &= mm - 1) {
+      const int j = __ffs(mm) - 1;
+      float dSj[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) dSj[h] = tS[w][j][h];
+      src_finalize_row<H, VPL>(a, t.r0 + j, dSj, amax_loc);
+    }
+    __syncwarp();
+  }
+  amax_flush(a.amax_dHp, amax_loc);
+}
+
+// ================================================================== ∂a, deterministic (reading R39)
+// ∂a_src[j] = Σᶜ_u fmaf(∂S[u,h], deq(q_H′)[u,j], ·) with chunks of DA_CHUNK global rows folded left to
+// right (R33's order); block b computes chunk b's partials for all 2·HD outputs (one sequential fmaf chain
+// per output and thread), the last block to finish folds the partials in chunk order.
+constexpr int DA_CHUNK = 1024;
+template <int H, int VPL>
+__global__ void __launch_bounds__(256) k2_attn_grad(const G2Args a) {
+  constexpr int HD = 32 * VPL;
+  constexpr int CW = HD > 256 ? HD / 256 : 1;   // columns per thread (the same columns in both halves)
+  constexpr int TR = 16;                        // rows per staged tile
+  constexpr int NT = 4;                         // tiles in flight (cp.async ring)
+  __shared__ __align__(16) int8_t sq[NT][TR][HD];
+  __shared__ float ssd[NT][TR][2 * H];
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const uint32_t flip = a.codes_biased ? 0x80808080u : 0u;   // stored excess-128 -> plain codes
+  const int64_t nch = (a.g.n_local + DA_CHUNK - 1) / DA_CHUNK;
+  const int tid = threadIdx.x;
+  const int j0 = tid * CW;
+  const bool act = j0 < HD;
+  const int h = (act ? j0 : 0) / (HD / H);
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    const int64_t u0 = ch * DA_CHUNK, u1 = u0 + DA_CHUNK < a.g.n_local ? u0 + DA_CHUNK : a.g.n_local;
+    const int ntile = (int)((u1 - u0 + TR - 1) / TR);
+    // tile k: rows u0 + k*TR ..; each thread copies 16-B pieces of the q_H′ rows and the ∂S|∂D words
+    auto issue = [&](int k) {
+      const int64_t r0 = u0 + (int64_t)k * TR;
+      const int rows = u1 - r0 < TR ? (int)(u1 - r0) : TR;
+      for (int i = tid; i < rows * (HD / 16); i += 256) {
+        const int r = i / (HD / 16), c = i % (HD / 16);
+        const int64_t ug = a.g.row_begin + r0 + r;
+        cp_async_bytes16(smem_u32(&sq[k % NT][r][c * 16]), a.qHp + ug * a.ldHp + c * 16);
+      }
+      for (int i = tid; i < rows * 2 * H; i += 256) {
+        const int r = i / (2 * H), c = i % (2 * H);
+        const int64_t ug = a.g.row_begin + r0 + r;
+        ssd[k % NT][r][c] = c < H ? a.dS[ug * H + c] : a.dD[ug * H + c - H];
+      }
+      cp_commit();
+    };
+    float ps[CW], pd[CW];
+#pragma unroll
+    for (int k = 0; k < CW; ++k) { ps[k] = 0.0f; pd[k] = 0.0f; }
+#pragma unroll
+    for (int k = 0; k < NT - 1; ++k) {
+      if (k < ntile) issue(k);
+      else cp_commit();
+    }
+    for (int k = 0; k < ntile; ++k) {
+      if (k + NT - 1 < ntile) issue(k + NT - 1);
+      else cp_commit();
+      cp_wait<NT - 1>();
+      __syncthreads();
+      const int rows = u1 - (u0 + (int64_t)k * TR) < TR ? (int)(u1 - (u0 + (int64_t)k * TR)) : TR;
+      if (act) {
+        for (int r = 0; r < rows; ++r) {
+          uint32_t x;
+          if constexpr (CW == 2) x = *reinterpret_cast<const uint16_t*>(&sq[k % NT][r][j0]);
+          else x = *reinterpret_cast<const uint8_t*>(&sq[k % NT][r][j0]);
+          x ^= flip;
+          const float s = ssd[k % NT][r][h], d = ssd[k % NT][r][H + h];
+#pragma unroll
+          for (int c = 0; c < CW; ++c) {
+            const float hp = __fmul_rn(__int2float_rn((int)(int8_t)(x >> (8 * c))), scH.s);
+            ps[c] = __fmaf_rn(s, hp, ps[c]);
+            pd[c] = __fmaf_rn(d, hp, pd[c]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    cp_wait<0>();
+    if (act)
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        __stcg(a.da_part + ch * 2 * HD + j0 + c, ps[c]);
+        __stcg(a.da_part + ch * 2 * HD + HD + j0 + c, pd[c]);
+      }
+  }
+  // the last block to finish folds the chunk partials left to right
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(a.work + 5, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int j = tid; j < 2 * HD; j += blockDim.x) {
+    float tot = 0.0f;
+    for (int64_t c0 = 0; c0 < nch; c0 += 8) {
+      float p[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) p[k] = c0 + k < nch ? __ldcg(a.da_part + (c0 + k) * 2 * HD + j) : 0.0f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (c0 + k < nch) tot = (c0 + k == 0) ? p[k] : __fadd_rn(tot, p[k]);
+    }
+    (j < HD ? a.da_src : a.da_dst)[j % HD] = tot;
+  }
+  if (tid == 0) a.work[5] = 0;
+}
+
+// ================================================================== in-CSR -> out-CSR position map
+__global__ void k2_in2out(const int32_t* __restrict__ out_eid, int64_t e, int32_t* __restrict__ in2out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x)
+    in2out[out_eid[i]] = (int32_t)i;
+}
+cudaError_t launch_gat2_in2out(const int32_t* out_eid, int64_t e, int32_t* in2out, cudaStream_t st) {
+  if (e == 0) return cudaSuccess;
+  ProfScope p("plan_in2out", st);
+  const int64_t blocks = (e + 255) / 256;
+  k2_in2out<<<(unsigned)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16), 256, 0, st>>>(out_eid, e,
+                                                                                                          in2out);
+  return cudaGetLastError();
+}
+
+// ================================================================== launchers
+static int grid_items(int64_t items, int per_sm) {
+  int64_t g = items;
+  const int64_t cap = (int64_t)num_sms() * per_sm;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+bool gat2_supported(const GraphDev& g, int heads, int hd) {
+  const int vpl = hd / 32;
+  return g.out_eid && g.row_begin == 0 && g.n_local == g.n_global && g.chunk <= 256 &&
+         (vpl == 4 || vpl == 8 || vpl == 16) && (heads == 1 || heads == 2 || heads == 4 || heads == 8) &&
+         hd % heads == 0 && (hd / heads) % (vpl) == 0 && 32 % heads == 0;
+}
+
+#define G2_CASES(X) X(1, 4) X(1, 8) X(1, 16) X(2, 4) X(2, 8) X(2, 16) X(4, 4) X(4, 8) X(4, 16) X(8, 4) X(8, 8) X(8, 16)
+
+cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st) {
+  const int hv = a.d.heads * 100 + a.d.hd / 32;
+  bool ok = false;
+  cudaError_t e = cudaSuccess;
+#define X(H_, V_)                                                                                    \
+  if (hv == H_ * 100 + V_) {                                                                         \
+    ok = true;                                                                                       \
+    constexpr int smem = 8 * ((fa_warp_smem<H_, V_>() + 15) & ~15);                                   \
+    static bool attr = false;                                                                        \
+    if (!attr) {                                                                                     \
+      cudaFuncSetAttribute(k2_fagg<H_, V_>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);      \
+      attr = true;                                                                                   \
+    }                                                                                                \
+    { ProfScope p("gat_fwd_stats1", st); k2_fstats1<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
+    { ProfScope p("gat_fwd_stats", st); k2_fstats2<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
+    { ProfScope p("gat_fwd_agg", st); k2_fagg<H_, V_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 3), 256, smem, st>>>(a); } \
+  }
+  G2_CASES(X)
+#undef X
+  if (!ok) return cudaErrorInvalidValue;
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st) {
+  const int hv = a.d.heads * 100 + a.d.hd / 32;
+  bool ok = false;
+  cudaError_t e = cudaSuccess;
+#define X(H_, V_)                                                                                    \
+  if (hv == H_ * 100 + V_) {                                                                         \
+    ok = true;                                                                                       \
+    constexpr int NW = 4, smem = NW * ((bs_warp_smem<H_, V_>() + 15) & ~15);                          \
+    static bool attr = false;                                                                        \
+    if (!attr) {                                                                                     \
+      cudaFuncSetAttribute(k2_bsrc1<H_, V_, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      attr = true;                                                                                   \
+    }                                                                                                \
+    { ProfScope p("gat_bwd_src", st); k2_bsrc1<H_, V_, NW><<<grid_items((a.pout.cap + a.pout.tcap + NW - 1) / NW, 20 / NW), NW * 32, smem, st>>>(a); } \
+    { ProfScope p("gat_bwd_dst", st); k2_bdst_a<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
+    { ProfScope p("gat_bwd_dst2", st); k2_bdst_b<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
+    { ProfScope p("gat_bwd_src2", st); k2_bsrc2<H_, V_><<<grid_items((a.pout.cap + a.pout.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
+  }
+  G2_CASES(X)
+#undef X
+  if (!ok) return cudaErrorInvalidValue;
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gat2_attn_grad(const G2Args& a, cudaStream_t st) {
+  const int hv = a.d.heads * 100 + a.d.hd / 32;
+  const int64_t nch = (a.g.n_local + DA_CHUNK - 1) / DA_CHUNK;
+  const int grid = (int)(nch < 1 ? 1 : (nch < 4 * num_sms() ? nch : 4 * num_sms()));
+  bool ok = false;
+#define X(H_, V_)                                                                                    \
+  if (hv == H_ * 100 + V_) {                                                                         \
+    ok = true;                                                                                       \
+    ProfScope p("gat_bwd_attn_grad", st);                                                            \
+    k2_attn_grad<H_, V_><<<grid, 256, 0, st>>>(a);                                                   \
+  }
+  G2_CASES(X)
+#undef X
+  if (!ok) return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+}  // namespace tango

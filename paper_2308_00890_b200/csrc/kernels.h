@@ -8,6 +8,7 @@ namespace tango {
 
 int num_sms();
 
+
 // Every kernel launch is wrapped in a ProfScope (prof.cu): launch counter + optional event timing.
 class ProfScope {
  public:
@@ -140,6 +141,38 @@ struct GatBwdArgs {
 cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st, const SideStream* aux = nullptr);
 cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st, const SideStream* aux = nullptr);
 cudaError_t launch_gat_attn_grad(const GatBwdArgs& a, cudaStream_t st);
+
+// ---- gat2.cu : v6 single-GPU dataflow (α recomputed, one row-gather pass in the backward)
+struct G2Args {
+  GraphDev g; GatDims d; float slope; int bits;
+  const int8_t* qS; const unsigned* amax_S;                  // [N][H]
+  const int8_t* qD; const unsigned* amax_D;                  // [N][H]
+  const int8_t* qHp; int64_t ldHp; const unsigned* amax_Hp;  // [N][ldHp] excess-128 codes
+  const int8_t* qG; int64_t ldG; const unsigned* amax_G;     // [N][ldG] excess-128 codes
+  float* m; float* den;                                      // [N][H]
+  float* Hout; unsigned* amax_out;                           // forward output [n][HD]
+  float* P; float* dD; float* dS;                            // [N][H]
+  float* dal_out;                                            // [E][H] ∂α in out-CSR order
+  const float* a_src; const float* a_dst;
+  float* dHp; unsigned* amax_dHp;                            // [n][HD]: ∂H′_agg (P1) -> ∂H′ (P3)
+  PlanDev pin, pout;
+  float* hagg;                                               // [cap][HD] heavy-segment partials
+  float* h1; float* h2;                                      // [pin.cap][H] segment partials (max, Σ, P, ∂D)
+  float* hs;                                                 // [pout.cap][H] segment partials (∂S)
+  int32_t* hcnt;                                             // [n] finished-segment counters (zeroed)
+  int32_t* work;                                             // [8] work-queue counters (zeroed)
+  float* da_part;                                            // [ceil(n/1024)][2 HD] ∂a chunk partials
+  float* nrec; int nrs;                                      // [N][nrs] packed per-node record: m | den | P | q_D
+  const int32_t* in2out;                                     // [E] out-CSR position of each in-CSR edge
+  float* da_src; float* da_dst;                              // [HD]
+  int codes_biased;
+};
+bool gat2_supported(const GraphDev& g, int heads, int hd);
+constexpr int gat2_nrec_stride(int heads) { return heads <= 1 ? 4 : heads <= 2 ? 8 : heads <= 4 ? 16 : 32; }
+cudaError_t launch_gat2_in2out(const int32_t* out_eid, int64_t e, int32_t* in2out, cudaStream_t st);
+cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st);
+cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st);
+cudaError_t launch_gat2_attn_grad(const G2Args& a, cudaStream_t st);
 
 // standalone primitives (unfused; used by the primitive C-ABI entry points)
 cudaError_t launch_sddmm_add(const GraphDev& g, int heads, const int8_t* qS, const float* sS, const int8_t* qD,

@@ -37,7 +37,7 @@ _P = C.c_void_p
 class Graph(C.Structure):
     _fields_ = [("n_global", C.c_int64), ("row_begin", C.c_int64), ("row_end", C.c_int64), ("in_ptr", _P),
                 ("in_src", _P), ("e_in", C.c_int64), ("out_ptr", _P), ("out_dst", _P), ("out_eid", _P),
-                ("e_out", C.c_int64), ("chunk_edges", C.c_int32)]
+                ("e_out", C.c_int64), ("chunk_edges", C.c_int32), ("graph_id", C.c_uint64)]
 
 
 class QTensor(C.Structure):
@@ -58,7 +58,7 @@ class GatCtxView(C.Structure):
     _fields_ = [(f, _P) for f in ("qH", "qW", "qWt", "qHp", "qS", "qD", "qG", "qdHp")] + \
                [(f, C.c_int64) for f in ("ldF", "ldHD", "ldFt")] + \
                [(f, _P) for f in ("S", "D", "m", "den", "P", "dD", "dHp", "dalpha", "alpha_pack", "scalars")] + \
-               [("codes_biased", C.c_int32)]
+               [("codes_biased", C.c_int32), ("dS", _P), ("dataflow", C.c_int32)]
 
 
 class GcnParams(C.Structure):
@@ -248,6 +248,8 @@ class DeviceGraph:
     the in/out CSR arrays are then sliced to the owned rows.
     """
 
+    _next_id = 0
+
     def __init__(self, g, device="cuda", chunk=256, row_begin=0, row_end=None, keep_eid=None):
         lg = local_graph(g, row_begin, row_end, keep_eid)
         t = lambda a: torch.from_numpy(a).to(device)
@@ -258,10 +260,11 @@ class DeviceGraph:
         self.n_local = lg.n
         self.e_in, self.e_out = lg.e, lg.e_out
         self.chunk = chunk
+        DeviceGraph._next_id += 1   # a process-unique id per device graph: the layers' static-plan cache key
         self.struct = Graph(g.n, lg.row_begin, lg.row_end, _ptr(self.in_ptr), _ptr(self.in_src) if self.e_in else None,
                             self.e_in, _ptr(self.out_ptr), _ptr(self.out_dst) if self.e_out else None,
                             _ptr(self.out_eid) if self.out_eid is not None and self.e_out else None, self.e_out,
-                            chunk)
+                            chunk, DeviceGraph._next_id)
 
     def ref(self):
         return C.byref(self.struct)
@@ -520,10 +523,15 @@ class GATLayer:
             out["qHp"] = torch.bitwise_xor(out["qHp"], flip)
             out["qG"] = torch.bitwise_xor(out["qG"], flip)
         out["codes_biased"] = bool(v.codes_biased)
-        pack = sl(v.alpha_pack, E * 2 * H * 4, f4, (E, 2 * H))
-        out["alpha"] = pack[:, :H].abs()
-        out["e_pre_pos"] = ~torch.signbit(pack[:, :H])
-        out["dE_pre"] = pack[:, H:]
+        out["dS"] = sl(v.dS, N * H * 4, f4, (N, H))
+        out["dataflow"] = int(v.dataflow)
+        if v.dataflow == 1:
+            pack = sl(v.alpha_pack, E * 2 * H * 4, f4, (E, 2 * H))
+            out["alpha"] = pack[:, :H].abs()
+            out["e_pre_pos"] = ~torch.signbit(pack[:, :H])
+            out["dE_pre"] = pack[:, H:]
+        else:
+            out["dalpha_out"] = sl(v.alpha_pack, self.graph.e_out * H * 4, f4, (self.graph.e_out, H))
         return out
 
     def check_status(self):

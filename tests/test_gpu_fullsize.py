@@ -60,23 +60,32 @@ def test_gat_layer_arxiv_full_size(T, orc):
     eq("D", fv["D"], f["Dd"])
     eq("m", fv["m"], f["m"])
     eq("den", fv["den"], f["den"])
-    eq("alpha", fv["alpha"], f["alpha"])
+    if fv["dataflow"] == 1:
+        eq("alpha", fv["alpha"], f["alpha"])
     eq("H_out", Hout, f["Hout"])
     eq("amax_out", amax_out, f["amax_out"])
     eq("qG", bv["qG"], b["qG"])
-    eq("dalpha", bv["dalpha"], b["dalpha"])
-    eq("dE_pre", bv["dE_pre"], b["dE_pre"])
+    if bv["dataflow"] == 1:
+        eq("dalpha", bv["dalpha"], b["dalpha"])
+        eq("dE_pre", bv["dE_pre"], b["dE_pre"])
+    else:
+        eq("dalpha_out", bv["dalpha_out"], b["dalpha"][g.out_eid])
+        eq("dS", bv["dS"], b["dS"])
     eq("P", bv["P"], b["P"])
     eq("dD", bv["dD"], b["dD"])
     eq("dHp", bv["dHp"], b["dHp"])
     eq("qdHp", bv["qdHp"], b["qdHp"])
     eq("dH", dX, b["dH"])
     eq("dW", dW, b["dW"])
-    bound = 4096 * 2.0 ** -24
-    for name, got, want, absum in (("da_src", das, b["da_src"], b["da_src_abs"]),
-                                   ("da_dst", dad, b["da_dst"], b["da_dst_abs"])):
-        err = np.abs(got.cpu().numpy().astype(np.float64) - want)
-        assert np.all(err <= bound * absum + 1e-7), (name, float(np.max(err / (absum + 1e-30))))
+    if bv["dataflow"] == 2:   # deterministic chunk order (reading R39): bit-exact
+        eq("da_src", das, b["da_src"])
+        eq("da_dst", dad, b["da_dst"])
+    else:
+        bound = 4096 * 2.0 ** -24
+        for name, got, want, absum in (("da_src", das, b["da_src"], b["da_src_abs"]),
+                                       ("da_dst", dad, b["da_dst"], b["da_dst_abs"])):
+            err = np.abs(got.cpu().numpy().astype(np.float64) - want)
+            assert np.all(err <= bound * absum + 1e-7), (name, float(np.max(err / (absum + 1e-30))))
     # the hub rows (max in-degree ~8K, > 31 canonical chunks) are inside this comparison
     assert int(np.diff(g.in_ptr).max()) > 30 * 256
 
