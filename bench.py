@@ -2,7 +2,10 @@
 """Benchmark of the hot path: one quantized GAT layer forward + backward (Tango, arXiv 2308.00890)
 through libtango.so on synthetic inputs shaped like the paper's datasets.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload arxiv] [--impl tango|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload reddit] [--impl tango|reference]
+
+Default workload: the Reddit-shaped layer of BASELINE.json configs[3] (the metric's 1-8 GPU config);
+the arxiv-shaped layer (configs[2]) is measured too and reported under "extra_workloads".
 
 N > 1 is launched by torchrun: destination-row partitioning of ONE graph over N GPUs with NCCL
 (all-gather of int8 node rows, all-reduce of amax / ∂W / ∂a inside libtango) -> strong scaling.
@@ -83,17 +86,23 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------- roofline model
-# The three gather passes of the layer and the launches each is split into (gat.cu: light sub-tiles on
-# the main stream; hub-row segments, their statistics and folds on the side stream).
+# Passes of the layer and the launches each is split into.  v6 dataflow (gat2.cu, one GPU): F-stats = stats1
+# (hub segment maxima) + stats (sums), P2 = bwd_dst (P) + bwd_dst2 (∂D).  Round-1 dataflow (gat.cu:
+# partitioned graphs, HD < 128): light sub-tiles + hub segments + folds.
 PASSES = {
+    "gat_fwd_stats": ["gat_fwd_stats", "gat_fwd_stats1"],
+    "gat_bwd_dst": ["gat_bwd_dst", "gat_bwd_dst2"],
     "gat_fwd_agg": ["gat_fwd_agg", "gat_fwd_agg_hub", "gat_fwd_combine"],
     "gat_bwd_dst1": ["gat_bwd_dst1", "gat_bwd_dst1_hub", "gat_bwd_dst2", "gat_bwd_dst3"],
     "gat_bwd_src": ["gat_bwd_src", "gat_bwd_src_hub", "gat_bwd_src_combine"],
 }
+GATHER_PASSES = ("gat_fwd_agg", "gat_bwd_src", "gat_bwd_dst1")   # int8 row gathers (E x HD elements)
+L2_BYTES = 126.5e6    # B200 L2 (cudaDevAttrL2CacheSize 132,644,864 B measured on the box)
+
 
 def pass_profile(prof):
-    """{kernel: (total ms, launches)} -> the same with each gather pass's launches merged under the
-    pass name (time = sum of the member launches, launches = those of the light launch)."""
+    """{kernel: (total ms, launches)} -> the same with each pass's launches merged under the pass name
+    (time = sum of the member launches, launches = those of the named launch)."""
     rprof = dict(prof)
     for pname, members in PASSES.items():
         if pname in rprof:
@@ -103,24 +112,41 @@ def pass_profile(prof):
     return rprof
 
 
-def kernel_model(name, g_e, n, F, H, HD, peaks, clock_mhz):
-    """Algorithmic bytes and ALU lane-ops per launch of a kernel, or per gather PASS (all E edges; see
-    PASSES) for the three gather passes.
+def alu_peak(clock_mhz):
+    """Lane-instruction issue peak: 148 SMs x 4 SMSPs x 32 lanes x 1 instruction / cycle (B200_PROFILING.md
+    unit counts) at the given SM clock; the FMA and ALU pipes each take one instruction per 2 cycles."""
+    return 148 * 128 * clock_mhz * 1e6
 
-    Bytes count each gathered int8 row once per edge (no cache reuse assumed), every per-edge
-    attribute and every per-row output once.  ALU ops count 2 lane-ops per gathered element for the
-    exact int8->fp32 convert + FMA (aggregations) and 1/4 per element for the IDP4A dots.
-    """
+
+def kernel_model(name, g_e, n, F, H, HD, peaks, clock_mhz, dataflow=2):
+    """Algorithmic bytes and lane-ops per launch of a kernel, or per PASS for the passes of PASSES
+    (SURVEY.md §8(d)).  Bytes count each gathered int8 row once per edge (no cache reuse)
+    and every per-edge / per-row input and output once; lane-ops count 2 per gathered element for the
+    exact int8 -> fp32 conversion + FMA (PRMT, half an FADD2, half an FFMA2) and 1/4 per element for
+    the IDP4A dots."""
     E = g_e
-    if name == "gat_fwd_agg":        # ⑤: index + stored α + q_H′[u] row per edge; H_out row per node
-        byts = E * (4 + 4 * H + HD) + n * (8 + 4 * HD)
+    if name == "gat_fwd_agg":        # ⑤: index + q_S[u] + q_H′[u] row per edge; H_out row + softmax data per row
+        byts = E * (4 + H + HD) + n * (4 * HD + 9 * H) if dataflow == 2 else E * (4 + 4 * H + HD) + n * (8 + 4 * HD)
         ops = 2 * E * HD
-    elif name == "gat_bwd_dst1":     # ⑤″+④′: index + α + q_H′[u] row + ∂α/∂E_pre scratch; q_G[v] row, P, ∂D
+    elif name == "gat_bwd_src":      # v6 P1 ⑤′+⑤″: dst index + q_G[v] row + v's record + ∂α out; own rows
+        if dataflow == 2:
+            byts = E * (4 + HD + 9 * H + 4 * H) + n * (5 * HD + H)
+            ops = 2 * E * HD + E * HD // 4
+        else:                        # round 1 ⑤′+③′+②′: dst index + eid + α + ∂E_pre + q_G[v] row
+            byts = E * (8 + 8 * H + HD) + n * (8 + 4 * HD + 8 * H)
+            ops = 2 * E * HD
+    elif name == "gat_bwd_dst1":     # round 1 ⑤″+④′: index + α + q_H′[u] row + ∂α/∂E_pre scratch
         byts = E * (4 + 4 * H + HD + 12 * H) + n * (8 + HD + 8 * H)
         ops = E * HD // 4
-    elif name == "gat_bwd_src":      # ⑤′+③′+②′: dst index + eid + α + ∂E_pre + q_G[v] row; ∂H′ row per node
-        byts = E * (8 + 8 * H + HD) + n * (8 + 4 * HD + 8 * H)
-        ops = 2 * E * HD
+    elif name == "gat_bwd_dst":      # v6 P2 (two sweeps): src index, position map, q_S[u], ∂α per edge
+        byts = 2 * E * (8 + 5 * H) + n * 12 * H
+        ops = 2 * E * H * 40
+    elif name == "gat_bwd_src2":     # v6 P3: dst index, ∂α, v's record (m, den, P, q_D) per edge; ∂H′ rows
+        byts = E * (4 + 4 * H + 13 * H) + n * (8 * HD + 8 * H)
+        ops = E * H * 40
+    elif name == "gat_fwd_stats":    # v6 F-stats (max sweep + Σ sweep): src index, q_S[u] per edge
+        byts = 2 * E * (4 + H) + n * 9 * H
+        ops = E * H * 25
     elif name == "quantize":         # SR quantize: 4 B read + 1 B code written per element.  Per step:
         # Q(W) F*HD, Q(H) n*F, Q(S) and Q(D) n*H each, Q(dH_out) and Q(dH') n*HD each = 6 launches;
         # returned per launch (average), like the per-launch time it is divided by.
@@ -132,8 +158,26 @@ def kernel_model(name, g_e, n, F, H, HD, peaks, clock_mhz):
         ops = 2 * (n * F + n * HD) / 2
     else:
         return None
-    alu_peak = 148 * 128 * clock_mhz * 1e6   # FP32 lanes x clock (lane-ops/s)
-    return byts, ops, alu_peak
+    return byts, ops, alu_peak(clock_mhz)
+
+
+def pass_bound(name, table_bytes):
+    """The roofline that governs a pass: the int8 row gathers are issue-bound on the conversion + FMA
+    when the gathered table fits in L2 (its rows are served from L2, not HBM) and HBM-bound when it does
+    not; the per-edge softmax / incidence passes stream their inputs (HBM)."""
+    if name in GATHER_PASSES:
+        return "alu" if table_bytes <= L2_BYTES else "hbm"
+    return "hbm"
+
+
+def ncu_traffic(workload, kernel):
+    """DRAM bytes per launch of `kernel` on `workload` from the committed ncu --set full captures
+    (profiles/ncu_traffic.json, keyed by workload), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(workload, {}).get(kernel)
+    except Exception:
+        return None
 
 
 def gemm_microbench(T, torch, int8_peak, size=8192, reps=10):
@@ -364,48 +408,64 @@ def spmm_sweep_bench(T, torch, dg, g, F, args, l2_flush, peaks):
 
 
 # ------------------------------------------------------------------------------------- reference arm
+def sample_graph(name, frac):
+    """The workload's recipe (same degree law, cap, seeds) at a fraction of its nodes and draws."""
+    kw = dict(inputs.WORKLOADS[name][0])
+    kw["n"], kw["m"] = max(64, int(kw["n"] * frac)), max(64, int(kw["m"] * frac))
+    return inputs.chung_lu_graph(**kw)
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_layer_ms(O, g, F, H, D, step=0):
+    """One oracle fwd + bwd of the layer on graph g (the oracle as it stands), wall-clock ms."""
+    X = inputs.features(g.n, F)
+    W, a_s, a_d = inputs.gat_params(F, H, D)
+    dY = inputs.grad_out(g.n, H * D)
+    t0 = time.perf_counter()
+    f = O.gat_fwd(g, X, W, a_s, a_d, H, D, step=step)
+    O.gat_bwd(g, f, X, W, a_s, a_d, dY)
+    return (time.perf_counter() - t0) * 1e3
+
+
 def run_reference(args, rank, world):
+    """--impl reference: the oracle (the only reference there is; the paper ships no code) timed on the
+    box's host cores, each step a bounded sample of the workload: the workload's own graph recipe at a
+    fraction of its nodes and draws, sized so the K + W steps end within a few minutes.  ms_per_step is
+    the measured time of one sampled step (nothing extrapolated); the estimate for the full workload is
+    reported beside it, labelled as such."""
     if rank != 0:
         return
     from oracle import oracle as O
     O.build()
-    g, F, H, D = workload(args.workload)
-    HD = H * D
-    Hx = inputs.features(g.n, F)
-    W, a_s, a_d = inputs.gat_params(F, H, D)
-    dH = inputs.grad_out(g.n, HD)
+    kw, F, H, D = inputs.WORKLOADS[args.workload]
     cores = O.num_threads()
-    # each step: the oracle (as it stands) on a bounded row sample of the same workload, scaled by edges
-    # bounded sample: by default sized so that the K + W oracle steps take about a minute in total
-    # (one full arxiv-shaped step is ~4 s on 16 host cores); --ref-sample fixes the fraction
-    if args.ref_sample is None:
-        frac = min(1.0, max(0.05, 60.0 / (4.0 * (args.steps + args.warmup))))
-    else:
-        frac = min(1.0, args.ref_sample)
-    if frac < 1.0:
-        gs = inputs.chung_lu_graph(**{**inputs.WORKLOADS[args.workload][0],
-                                      "n": int(g.n * frac), "m": int(inputs.WORKLOADS[args.workload][0]["m"] * frac)})
-    else:
-        gs = g
-    Hs, dHs = Hx[:gs.n], dH[:gs.n]
-    times = []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        f = O.gat_fwd(gs, Hs, W, a_s, a_d, H, D, step=i)
-        O.gat_bwd(gs, f, Hs, W, a_s, a_d, dHs)
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            times.append(dt)
-    scale = (g.e + g.n) / (gs.e + gs.n)
-    ms = 1e3 * statistics.mean(times) * scale
-    sample = (f"oracle gat_fwd+gat_bwd on {'the full graph' if gs is g else f'a {frac:.3f}-scale Chung-Lu sample'} "
-              f"(N={gs.n}, E={gs.e}), scaled by (E+N) ratio {scale:.3f}")
+    # full-size oracle step on 16 host cores: reddit ~52 s, arxiv ~4 s; budget ~90 s over the K + W steps
+    full_est_s = {"reddit": 52.0, "arxiv": 4.0, "products": 60.0}.get(args.workload, 10.0) * 16.0 / max(cores, 1)
+    frac = args.ref_sample if args.ref_sample is not None else min(1.0, 90.0 / (full_est_s * (args.steps + args.warmup)))
+    gs = inputs.workload_graph(args.workload) if frac >= 1.0 else sample_graph(args.workload, frac)
+    times = [oracle_layer_ms(O, gs, F, H, D, step=i) for i in range(args.warmup + args.steps)][args.warmup:]
+    ms = statistics.mean(times)
+    e_full = inputs.WORKLOADS[args.workload][0]["m"] * 2 + kw["n"]
+    sample = (f"oracle gat_fwd + gat_bwd (all {cores} host threads) on the {args.workload} recipe at "
+              f"{frac:.4f} of its nodes and draws (N={gs.n}, E={gs.e}); value = measured time per sampled step")
     line = {"impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "int8 codes / fp32 (CPU)", "data": "synthetic",
-            "config": {"workload": f"{args.workload}-shaped GAT layer 1", "N": g.n, "E": g.e, "F": F, "heads": H,
-                       "head_dim": D},
-            "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample},
+            "config": {"workload": f"{args.workload}-shaped GAT layer 1 (fwd+bwd)", "N": kw["n"], "F": F, "heads": H,
+                       "head_dim": D, "sample": {"fraction": frac, "N": gs.n, "E": gs.e}},
+            "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
+            "full_workload_estimate_ms": ms * e_full / max(gs.e + gs.n, 1),
             "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
@@ -430,43 +490,11 @@ def emit(line):
     out.flush()
 
 
-def main():
-    _claim_stdout()
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="arxiv", choices=sorted(inputs.WORKLOADS))
-    ap.add_argument("--impl", default="tango", choices=["tango", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-train-step", "--layer-only", dest="no_train_step", action="store_true",
-                    help="skip the extras (train_step, sddmm_bits): the layer step only")
-    ap.add_argument("--nccl-single", action="store_true", help="N = 1 through a 1-rank NCCL communicator")
-    ap.add_argument("--order", default="random", choices=["random", "degree"],
-                    help="node numbering: the recipe's random relabelling or by descending degree (NEXT-3)")
-    ap.add_argument("--ref-sample", type=float, default=None,
-                    help="fraction of the workload per oracle step (default: ~1 min for all K + W steps)")
-    ap.add_argument("--profile-breakdown", action="store_true", help="print per-kernel times to stderr")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-        return
-
-    import torch
-    import torch.distributed as dist
-    from paper_2308_00890_b200 import tango as T
-
-    torch.cuda.set_device(local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    T.load()
-    peaks, peak_kind = load_peaks()
-
-    g, F, H, D = workload(args.workload, args.order)
+def measure_layer(T, torch, dist, wname, args, rank, world, local_rank, peaks, peak_kind, l2_flush, timed=True):
+    """One workload: build the layer, K eager steps with per-launch events (kernel times, roofline),
+    then K CUDA-graph replays timed with events (the value), then the e2e pass with host buffers.
+    Returns (result dict, extras for the caller)."""
+    g, F, H, D = workload(wname, args.order)
     HD = H * D
     starts = partition_rows(g, world)
     r0, r1 = starts[rank], starts[rank + 1]
@@ -489,7 +517,6 @@ def main():
             torch.empty(HD, device="cuda"), torch.empty(HD, device="cuda"))
     Hout = torch.empty((n, HD), device="cuda")
     amax = torch.empty(1, device="cuda")
-    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
 
     def step(i):
         layer.forward(Hd, step=i, out=Hout, amax_out=amax)
@@ -499,12 +526,12 @@ def main():
         step(i)
     torch.cuda.synchronize()
     layer.check_status()
+    dataflow = layer.view_dataflow()
 
     # ---------------- per-kernel pass: K eager steps with CUDA events around every library launch
-    # (ProfScope, on the launching stream); gives the per-kernel times, the dominant kernel's
-    # roofline and the launch count per step.  L2 flushed before every step.
+    # (on the launching stream), side-stream work serialised so each launch is timed alone
     T.profile_enable(True)
-    T.profile_serialize(True)     # per-kernel pass: side-stream work in order, each launch timed alone
+    T.profile_serialize(True)
     T.profile_read(reset=True)
     torch.cuda.synchronize()
     launches0 = T.launch_count()
@@ -517,13 +544,13 @@ def main():
     T.profile_enable(False)
     T.profile_serialize(False)
 
-    # ---------------- timed region: K steps replayed from one CUDA graph (fwd + bwd of the layer,
-    # captured once: no host launch gaps), L2 flushed between steps, CUDA events per step
+    # ---------------- timed region: K steps replayed from one CUDA graph (fwd + bwd), L2 flushed between
+    # steps, CUDA events per step, repeated until >= 0.5 s so the clock sampler sees the load
     graph = torch.cuda.CUDAGraph()
     cap_stream = torch.cuda.Stream()
     cap_stream.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(cap_stream):
-        step(args.warmup)   # warm the capture stream
+        step(args.warmup)
         torch.cuda.synchronize()
         with torch.cuda.graph(graph, stream=cap_stream):
             step(args.warmup + 1)
@@ -532,11 +559,11 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local_rank)
-    time.sleep(0.2)   # let the sampler start before the timed region
+    clocks = ClockSampler(local_rank) if timed else None
+    time.sleep(0.2 if timed else 0.0)
     reps = 0
     t_start = time.perf_counter()
-    while True:   # repeat the K-step timed region until >= 0.5 s so the clock sampler sees it
+    while True:
         for i in range(args.steps):
             l2_flush.zero_()
             evs[i][0].record()
@@ -548,8 +575,7 @@ def main():
             break
     if world > 1:
         dist.barrier()
-    clk = clocks.stop()
-    launches = int(round(launches_per_step * args.steps))
+    clk = clocks.stop() if clocks else None
     layer.check_status()
     ms_rank = sum(a.elapsed_time(b) for a, b in evs) / args.steps   # the last repetition's K steps
     ms_t = torch.tensor([ms_rank], dtype=torch.float64, device="cuda")
@@ -558,68 +584,53 @@ def main():
     ms = float(ms_t.item())
     eager_ms = sum(v[0] for v in prof.values()) / args.steps
 
-    # ---------------- dominant kernel roofline (live CUDA-event time over the timed region)
-    # dominant = largest device time per step; a kernel without a bytes/ops model falls through to
-    # the next one (and is named in "skipped")
-    # A gather pass is split into launches (light sub-tiles; hub segments + folds on the side stream):
-    # its bytes model covers all E edges, so the roofline unit is the PASS, timed as the sum of its
-    # launches' serialised device times (one pass per step; launches counted by the light kernel).
+    # ---------------- roofline of every pass and of the dominant one (live event times, per pass)
+    clock = (clk or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    table_bytes = g.n * ((HD + 31) // 32 * 32)
     rprof = pass_profile(prof)
-    ranked = sorted(rprof.items(), key=lambda kv: -kv[1][0])
-    dom, (dom_ms, dom_cnt) = ranked[0]
-    skipped = []
-    for kname, kv in ranked:
-        if kernel_model(kname, dg.e_in, n, F, H, HD, peaks, 1965.0) is not None:
-            dom, (dom_ms, dom_cnt) = kname, kv
-            break
-        skipped.append(kname)
-    clock = clk["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
-    model = kernel_model(dom, dg.e_in, n, F, H, HD, peaks, clock)
-    per_launch_s = dom_ms / dom_cnt / 1e3
-    roof = None
-    if model is not None:
-        byts, ops, alu_peak = model
-        t_hbm = byts / (peaks["hbm_gbs"] * 1e9)
-        t_alu = ops / alu_peak
-        if t_hbm >= t_alu:
-            roof = {"bound": "hbm", "achieved": byts / per_launch_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
-        else:
-            roof = {"bound": "alu", "achieved": ops / per_launch_s / 1e12, "peak": alu_peak / 1e12,
-                    "unit": "Tlane-op/s"}
-        roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = None
-        try:   # DRAM bytes of this kernel per launch from the committed ncu --set full capture
-            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                tr = json.load(f).get(dom)
-            if tr:
-                roof["traffic"] = tr["dram_bytes_per_launch"]
-                roof["traffic_source"] = tr["source"]
-        except Exception:
-            pass
-        roof["algorithmic_bytes"] = byts
-        roof["kernel"] = dom
-        if dom in PASSES:
-            roof["pass_launches"] = [m for m in PASSES[dom] if m in prof]
-        roof["kernel_ms"] = per_launch_s * 1e3
-        roof["launches_per_step"] = dom_cnt / args.steps
-        roof["share_of_step"] = dom_ms / args.steps / ms
-        if skipped:
-            roof["unmodelled_larger_kernels"] = skipped
-        roof["peak_kind"] = peak_kind
-    breakdown = {k: round(v[0] / v[1], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
-    per_step = {k: round(v[0] / args.steps, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
-    # per-kernel rooflines of SURVEY.md §8(d): sparse kernels vs HBM (algorithmic bytes) and the
-    # ALU, GEMMs as int8 TOPS vs the int8 tensor peak (measured bf16 x the nominal int8:bf16 ratio 2)
-    int8_peak = 2.0 * peaks["bf16_tflops"]
-    kroof = {}
-    for kname in ("gat_fwd_agg", "gat_bwd_dst1", "gat_bwd_src"):
-        if kname not in rprof:
+    kroof, dom = {}, None
+    for kname, (kms, kcnt) in sorted(rprof.items(), key=lambda kv: -kv[1][0]):
+        km = kernel_model(kname, dg.e_in, n, F, H, HD, peaks, clock, dataflow)
+        if km is None:
             continue
-        km = kernel_model(kname, dg.e_in, n, F, H, HD, peaks, clock)
-        t_s = rprof[kname][0] / rprof[kname][1] / 1e3
-        kroof[kname] = {"ms": round(t_s * 1e3, 4), "hbm_gbs": round(km[0] / t_s / 1e9, 1),
-                        "hbm_frac": round(km[0] / t_s / 1e9 / peaks["hbm_gbs"], 3),
-                        "alu_frac": round(km[1] / t_s / km[2], 3)}
+        byts, ops, apk = km
+        t_s = kms / kcnt / 1e3
+        ent = {"ms": round(t_s * 1e3, 4), "launches_per_step": kcnt / args.steps,
+               "share_of_step": round(kms / args.steps / ms, 3), "bound": pass_bound(kname, table_bytes),
+               "alg_bytes": byts, "alg_gbs": round(byts / t_s / 1e9, 1),
+               "alg_hbm_frac": round(byts / t_s / 1e9 / peaks["hbm_gbs"], 3),
+               "lane_ops": ops, "alu_frac": round(ops / t_s / apk, 3)}
+        tr = ncu_traffic(wname, kname)
+        if tr:
+            ent["dram_bytes"] = tr["dram_bytes_per_launch"]
+            ent["dram_frac"] = round(tr["dram_bytes_per_launch"] / t_s / 1e9 / peaks["hbm_gbs"], 3)
+            if tr.get("l2_bytes_per_launch"):
+                ent["l2_bytes"] = tr["l2_bytes_per_launch"]
+            ent["traffic_source"] = tr["source"]
+        if kname in PASSES:
+            ent["launches"] = [m for m in PASSES[kname] if m in prof]
+        kroof[kname] = ent
+        if dom is None and kname in GATHER_PASSES + ("gat_bwd_dst", "gat_bwd_src2", "gat_fwd_stats", "quantize"):
+            dom = kname
+    roof = None
+    if dom is not None:
+        e = kroof[dom]
+        t_s = e["ms"] / 1e3
+        if e["bound"] == "alu":
+            roof = {"bound": "alu", "achieved": e["lane_ops"] / t_s / 1e12, "peak": alu_peak(clock) / 1e12,
+                    "unit": "Tlane-op/s"}
+        else:
+            roof = {"bound": "hbm", "achieved": e["alg_bytes"] / t_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = e.get("dram_bytes")
+        roof.update({"kernel": dom, "kernel_ms": e["ms"], "share_of_step": e["share_of_step"],
+                     "alg_bytes": e["alg_bytes"], "alg_hbm_frac": e["alg_hbm_frac"], "alu_frac": e["alu_frac"],
+                     "dram_frac": e.get("dram_frac"), "l2_bytes": e.get("l2_bytes"), "peak_kind": peak_kind,
+                     "clock_mhz": clock, "gathered_table_bytes": table_bytes,
+                     "regime": ("gathered int8 table (%.0f MB) fits the %.0f MB L2: rows come from L2, the "
+                                "conversion + FMA issue rate bounds the pass" % (table_bytes / 1e6, L2_BYTES / 1e6))
+                     if e["bound"] == "alu" else "table exceeds L2 or streaming pass: HBM bytes bound it"})
+    int8_peak = 2.0 * peaks["bf16_tflops"]
     gemm_ops = {"gemm_amax": 2 * n * F * HD, "gemm_quant": 2 * n * F * HD, "gemm_store": 2 * n * HD * F,
                 "gemm_splitk_i64": 2 * n * F * HD}
     for kname, ops in gemm_ops.items():
@@ -627,24 +638,35 @@ def main():
             t_s = prof[kname][0] / prof[kname][1] / 1e3
             kroof[kname] = {"ms": round(t_s * 1e3, 4), "tops": round(ops / t_s / 1e12, 1),
                             "tensor_frac": round(ops / t_s / 1e12 / int8_peak, 3)}
-    tensor = gemm_microbench(T, torch, int8_peak) if (rank == 0 and world == 1) else None
+    per_step = {k: round(v[0] / args.steps, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     if args.profile_breakdown and rank == 0:
-        print(json.dumps({"per_launch_ms": breakdown, "launches_per_kernel": {k: v[1] for k, v in prof.items()}}),
-              file=sys.stderr)
+        print(json.dumps({"workload": wname, "per_launch_ms": {k: round(v[0] / v[1], 4) for k, v in prof.items()},
+                          "launches_per_kernel": {k: v[1] for k, v in prof.items()}}), file=sys.stderr)
 
-    # ---------------- e2e: through the public API with host buffers (pinned), copies in the timed region.
-    # Every step copies its inputs H and ∂H_out host->device and reads the step's result (the layer's
-    # parameter gradients ∂W, ∂a_src, ∂a_dst and the amax of H_out) device->host.  The input copies
-    # of step i+1 run on a copy stream into the other of two device buffers while step i computes.
-    H_host = torch.from_numpy(np.ascontiguousarray(Hx)).pin_memory()
-    dH_host = torch.from_numpy(np.ascontiguousarray(dH)).pin_memory()
+    res = {"ms": ms, "N": g.n, "E": g.e, "F": F, "heads": H, "head_dim": D, "degree": g.degree_stats(),
+           "dataflow": dataflow, "roofline": roof, "kernel_roofline": kroof, "kernel_ms_per_step": per_step,
+           "eager_kernel_ms_per_step": round(eager_ms, 4), "gpu_launches_per_step": launches_per_step,
+           "clocks": clk}
+    extra = dict(g=g, dg=dg, F=F, H=H, D=D, layer=layer, Hx=Hx, dH=dH, Hd=Hd, dHd=dHd, outs=outs, Hout=Hout,
+                 amax=amax, comm=comm, W=W, a_s=a_s, a_d=a_d, n=n)
+    return res, extra
+
+
+def measure_e2e(T, torch, dist, x, world):
+    """The same metric end to end through the public API with host buffers (pinned): every step copies
+    its inputs H and ∂H_out host->device and reads the layer's parameter gradients and amax(H_out) back;
+    the input copies of step i+1 run on a copy stream into the other of two device buffers while step i
+    computes."""
+    layer, Hd, dHd, outs, Hout, amax = x["layer"], x["Hd"], x["dHd"], x["outs"], x["Hout"], x["amax"]
+    H_host = torch.from_numpy(np.ascontiguousarray(x["Hx"])).pin_memory()
+    dH_host = torch.from_numpy(np.ascontiguousarray(x["dH"])).pin_memory()
     res_dev = (outs[1], outs[2], outs[3], amax)
     res_host = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in res_dev]
     Hbuf, dHbuf = [Hd, torch.empty_like(Hd)], [dHd, torch.empty_like(dHd)]
     s_copy, s_comp = torch.cuda.Stream(), torch.cuda.Stream()
     ev_in = [torch.cuda.Event(), torch.cuda.Event()]
     ev_free = [torch.cuda.Event(), torch.cuda.Event()]
-    e2e_steps = max(4, min(args.steps, 20))
+    e2e_steps = 8
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -674,52 +696,123 @@ def main():
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     h2d = (H_host.numel() + dH_host.numel()) * 4
     d2h = sum(t.numel() * t.element_size() for t in res_host)
+    return {"value": float(e2e_t.item()), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "what": "per step: H2D of H and dH_out (pinned), fwd+bwd through GATLayer (C ABI), D2H of dW, "
+                    "da_src, da_dst, amax(H_out); input copies of step i+1 overlap step i (copy stream, "
+                    "double-buffered inputs)"}
 
-    launches_t = torch.tensor([launches], dtype=torch.int64, device="cuda")
+
+def main():
+    _claim_stdout()
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="reddit", choices=sorted(inputs.WORKLOADS))
+    ap.add_argument("--extras", default="arxiv",
+                    help="comma list of extra measurements at N = 1: arxiv, products (layer), train (NEXT-1 "
+                         "steps), sddmm (NEXT-4), or none")
+    ap.add_argument("--impl", default="tango", choices=["tango", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train-step", "--layer-only", dest="no_train_step", action="store_true",
+                    help="the headline layer only (no extras)")
+    ap.add_argument("--nccl-single", action="store_true", help="N = 1 through a 1-rank NCCL communicator")
+    ap.add_argument("--order", default="random", choices=["random", "degree"],
+                    help="node numbering: the recipe's random relabelling or by descending degree (NEXT-3)")
+    ap.add_argument("--ref-sample", type=float, default=None,
+                    help="fraction of the workload per oracle step in --impl reference (default: ~90 s total)")
+    ap.add_argument("--profile-breakdown", action="store_true", help="print per-kernel times to stderr")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2308_00890_b200 import tango as T
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    T.load()
+    peaks, peak_kind = load_peaks()
+    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
+
+    res, x = measure_layer(T, torch, dist, args.workload, args, rank, world, local_rank, peaks, peak_kind, l2_flush)
+    e2e = measure_e2e(T, torch, dist, x, world)
+    launches_t = torch.tensor([int(round(res["gpu_launches_per_step"] * args.steps))], dtype=torch.int64, device="cuda")
     if world > 1:
         dist.all_reduce(launches_t)
+    g, F, H, D = x["g"], x["F"], x["H"], x["D"]
+    W, a_s, a_d = x["W"], x["a_s"], x["a_d"]
+    if x["comm"] is not None:
+        x["comm"].close()
+    del x
+    torch.cuda.empty_cache()
 
-    # ---------------- NEXT-1: the training step around the layer (one GPU, arxiv workload)
-    train = None
-    if world == 1 and args.workload == "arxiv" and not args.no_train_step:
-        train = train_step_bench(T, torch, dg, g, F, H, D, args, l2_flush)
-        train["gcn_cora"] = train_step_gcn_bench(T, torch, args, l2_flush)
-    sddmm_bits = None
-    if world == 1 and args.workload == "arxiv" and not args.no_train_step:
-        sddmm_bits = sddmm_bits_bench(T, torch, dg, g, args, l2_flush, peaks)
-        sddmm_bits["spmm_sweep"] = spmm_sweep_bench(T, torch, dg, g, F, args, l2_flush, peaks)
+    extras = [] if args.no_train_step or args.extras == "none" else [e for e in args.extras.split(",") if e]
+    extra_out = {}
+    if world == 1:
+        for wname in extras:
+            if wname in inputs.WORKLOADS and wname != args.workload:
+                r2, x2 = measure_layer(T, torch, dist, wname, args, rank, world, local_rank, peaks, peak_kind,
+                                       l2_flush, timed=False)
+                extra_out[wname] = {k: r2[k] for k in ("ms", "N", "E", "F", "heads", "head_dim", "dataflow",
+                                                        "roofline", "kernel_ms_per_step")}
+                if wname == "arxiv" and ("train" in extras or "sddmm" in extras):
+                    gA, dgA = x2["g"], x2["dg"]
+                    if "train" in extras:
+                        tr = train_step_bench(T, torch, dgA, gA, x2["F"], x2["H"], x2["D"], args, l2_flush)
+                        tr["gcn_cora"] = train_step_gcn_bench(T, torch, args, l2_flush)
+                        extra_out["train_step"] = tr
+                    if "sddmm" in extras:
+                        sb = sddmm_bits_bench(T, torch, dgA, gA, args, l2_flush, peaks)
+                        sb["spmm_sweep"] = spmm_sweep_bench(T, torch, dgA, gA, x2["F"], args, l2_flush, peaks)
+                        extra_out["sddmm_bits"] = sb
+                del x2
+                torch.cuda.empty_cache()
+        if "gemm" in extras or args.workload in ("reddit", "products"):
+            extra_out["tensor"] = gemm_microbench(T, torch, 2.0 * peaks["bf16_tflops"])
 
-    # ---------------- CPU baseline: the oracle as it stands, rank 0 at N = 1 only
+    # ---------------- CPU baseline: the oracle as it stands, rank 0 at N = 1 only: the full workload with all
+    # host threads, and one thread on a bounded sample of the same recipe
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
         O.build()
-        t0 = time.perf_counter()
-        f = O.gat_fwd(g, Hx, W, a_s, a_d, H, D, step=0)
-        O.gat_bwd(g, f, Hx, W, a_s, a_d, dH)
-        cpu_ms = (time.perf_counter() - t0) * 1e3
-        cpu = {"value": cpu_ms, "unit": "ms", "cores": O.num_threads(), "kind": "oracle",
-               "sample": f"one full fwd+bwd of the same {args.workload}-shaped layer (N={g.n}, E={g.e}), "
-                         "OpenMP rows, bit-identical to single-threaded"}
+        cores = O.num_threads()
+        full_ms = oracle_layer_ms(O, g, F, H, D)
+        frac1 = {"reddit": 0.02, "products": 0.02}.get(args.workload, 0.1)
+        gs = sample_graph(args.workload, frac1)
+        O.set_threads(1)
+        one_ms = oracle_layer_ms(O, gs, F, H, D)
+        O.set_threads(cores)
+        cpu = {"value": full_ms, "unit": "ms", "cores": cores, "kind": "oracle",
+               "sample": f"one full fwd+bwd of the same {args.workload}-shaped layer (N={g.n}, E={g.e}) with all "
+                         f"{cores} host threads (OpenMP rows, bit-identical to one thread)",
+               "cpu_model": cpu_model(),
+               "single_thread": {"value": one_ms, "unit": "ms", "cores": 1,
+                                 "sample": f"the {args.workload} recipe at {frac1} of its nodes and draws "
+                                           f"(N={gs.n}, E={gs.e}), one thread"}}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        wl = f"{args.workload}-shaped GAT layer 1 (fwd+bwd)" + (", degree-ordered ids" if args.order == "degree" else "")
+        line = {"metric": METRIC, "value": res["ms"], "unit": "ms", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": False, "scaling": "strong",
                 "vs_baseline": None, "dtype": "int8 (tcgen05 kind::i8, IDP4A) + fp32 accumulate/softmax",
-                "data": "synthetic (seeded Chung-Lu power-law graph, N(0,1) features, Glorot weights)",
-                "config": {"workload": f"{args.workload}-shaped GAT layer 1 (fwd+bwd)" + (", degree-ordered ids" if args.order == "degree" else ""), "N": g.n, "E": g.e,
-                           "F": F, "heads": H, "head_dim": D, "bits": 8, "chunk_edges": 256,
+                "data": "synthetic (seeded Chung-Lu graph with the workload's degree law, N(0,1) features, Glorot weights)",
+                "config": {"workload": wl, "N": res["N"], "E": res["E"], "F": res["F"], "heads": res["heads"],
+                           "head_dim": res["head_dim"], "bits": 8, "chunk_edges": 256,
                            "parallelism": f"dst-row partition x{world}" if world > 1 else "1 GPU",
-                           "l2": "flushed between timed steps (256 MB write)",
-                           "degree": g.degree_stats()},
-                "roofline": roof, "kernel_roofline": kroof, "tensor": tensor, "cpu_baseline": cpu,
-                "e2e": {"value": float(e2e_t.item()), "unit": "ms", "h2d_bytes_per_step": h2d,
-                        "what": "per step: H2D of H and dH_out (pinned), fwd+bwd through GATLayer (C ABI), D2H of "
-                                "dW, da_src, da_dst, amax(H_out); input copies of step i+1 overlap step i "
-                                "(copy stream, double-buffered inputs)",
-                        "d2h_bytes_per_step": d2h},
-                "gpu_launches": int(launches_t.item()), "clocks": clk, "kernel_ms": breakdown, "kernel_ms_per_step": per_step,
-                "train_step": train, "sddmm_bits": sddmm_bits,
+                           "dataflow": "v6 (gat2.cu)" if res["dataflow"] == 2 else "round-1 (gat.cu)",
+                           "l2": "flushed between timed steps (256 MB write)", "degree": res["degree"]},
+                "roofline": res["roofline"], "kernel_roofline": res["kernel_roofline"], "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": int(launches_t.item()), "clocks": res["clocks"],
+                "kernel_ms_per_step": res["kernel_ms_per_step"], "extra_workloads": extra_out,
                 "paper_context": {
                     "note": "the paper's own numbers (BASELINE.md), other hardware: context, not targets; it "
                             "publishes no absolute layer or primitive times",
@@ -730,11 +823,9 @@ def main():
                     "int4_sddmm_add_dot_vs_fp32_dgl": "3.3x / 1.8x (GPU unstated, P:1245-1246)",
                     "qgemm_int8_tc_vs_cublas_fp16": "1.9x (D=256), 1.8x (D=512) (A100, P:1101-1103)"},
                 "timing": "value: CUDA-graph replay of fwd+bwd per step (events per step, L2 flushed between "
-                          "steps); kernel_ms/roofline: eager pass, side-stream work serialised, events around every launch "
-                          f"(sum of kernel times {eager_ms:.3f} ms/step)"}
+                          "steps); kernel_ms/roofline: eager pass, side-stream work serialised, events around every "
+                          f"launch (sum of kernel times {res['eager_kernel_ms_per_step']:.3f} ms/step)"}
         emit(line)
-    if comm is not None:
-        comm.close()
     if world > 1:
         dist.destroy_process_group()
 

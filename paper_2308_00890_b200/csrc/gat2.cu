@@ -411,10 +411,10 @@ template <int VPL>
 __device__ __forceinline__ void cp_slice_hint(uint32_t saddr, const int8_t* g, uint64_t pol) {
   if constexpr (VPL == 16)
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "l"(pol) : "memory");
-  else if constexpr (VPL == 8)
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(saddr), "l"(g), "l"(pol) : "memory");
+  else if constexpr (VPL == 8)   // (the cache-hint form of the 8- and 4-byte copies faults on sm_100a)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(g) : "memory");
   else
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(saddr), "l"(g), "l"(pol) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
 }
 // issue group g (rows sidx[8g .. 8g+7] of the chunk double buffer) into ring half g & 1, then commit
 template <int VPL>
@@ -463,8 +463,9 @@ __global__ void __launch_bounds__(256, 3) k2_fagg(const G2Args a) {
   const int64_t n = a.g.n_local, hc = load_count(a.pin.counts);
   const int64_t nitems = hc + load_count(a.pin.counts + 2);
   float amax_loc = 0.0f;
-  FOR_ITEMS(item, a.work + 1, nitems) {
-    const bool tile = item >= hc;
+  FOR_ITEMS(it, a.work + 2, nitems - hc) {   // light sub-tiles (hub rows: k2_fagg_seg)
+    const int64_t item = hc + it;
+    constexpr bool tile = true;
     Seg s;
     s.eb = 0; s.vl = 0; s.slot = -1; s.nseg = 1;
     TileCtx t;
@@ -666,6 +667,202 @@ __global__ void __launch_bounds__(256, 3) k2_fagg(const G2Args a) {
   amax_flush(a.amax_out, amax_loc);
 }
 
+// ================================================================== F-agg, hub rows: segment pieces
+// A hub row (degree > C_E) is cut into its canonical chunks.  A warp takes the row's first SPIECE chunks as
+// one piece and folds their partials itself in registers (total = p_0, total = total + p_c), so rows of
+// up to SPIECE chunks (the common hub on Reddit-like graphs) write no partials at all; each further chunk
+// is its own item whose partial goes to scratch, and the row's last finishing item continues the fold
+// from piece 0's running total in chunk order — the same left-to-right fold as the oracle's Σᶜ.
+constexpr int SPIECE = 4;
+
+// groups of one piece: 8 edges; a chunk boundary can only fall on a group start when C_E % 8 == 0 (the
+// FAST form); other C_E (parity tests use 3, 7, 64 ...) check every edge
+template <int VPL>
+struct PieceFold {
+  float tot[VPL];
+  int nfold;
+  __device__ __forceinline__ void fold(float2 (&acc)[VPL / 2]) {
+#pragma unroll
+    for (int k = 0; k < VPL / 2; ++k) {
+      tot[2 * k] = nfold == 0 ? acc[k].x : __fadd_rn(tot[2 * k], acc[k].x);
+      tot[2 * k + 1] = nfold == 0 ? acc[k].y : __fadd_rn(tot[2 * k + 1], acc[k].y);
+      acc[k] = make_float2(0.0f, 0.0f);
+    }
+    ++nfold;
+  }
+};
+
+template <int H, int VPL>
+__host__ __device__ constexpr int fs_warp_smem_seg() {   // ring | α [2][H][32] | gather offsets [2][32]
+  return g8_ring_bytes<VPL>() + 2 * H * 32 * 4 + 2 * 32 * 4;
+}
+
+// last item of a split hub row: fold piece 0's running total (slot base) with the partials of chunks
+// SPIECE .. nseg-1 (slots base + c), in chunk order; every lane its VPL columns
+template <int VPL>
+__device__ __forceinline__ void fold_tail(const float* hagg, int64_t base, int nseg, float (&tot)[VPL]) {
+  constexpr int HD = 32 * VPL;
+  const float* p0 = hagg + base * HD + (threadIdx.x & 31) * VPL;
+#pragma unroll
+  for (int k = 0; k < VPL / 4; ++k) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(p0) + k);
+    tot[4 * k] = v.x; tot[4 * k + 1] = v.y; tot[4 * k + 2] = v.z; tot[4 * k + 3] = v.w;
+  }
+  for (int j = SPIECE; j < nseg; ++j) {
+    const float4* pj = reinterpret_cast<const float4*>(p0 + (int64_t)j * HD);
+#pragma unroll
+    for (int k = 0; k < VPL / 4; ++k) {
+      const float4 v = __ldcg(pj + k);
+      tot[4 * k] = __fadd_rn(tot[4 * k], v.x); tot[4 * k + 1] = __fadd_rn(tot[4 * k + 1], v.y);
+      tot[4 * k + 2] = __fadd_rn(tot[4 * k + 2], v.z); tot[4 * k + 3] = __fadd_rn(tot[4 * k + 3], v.w);
+    }
+  }
+}
+template <int VPL>
+__device__ __forceinline__ void store_partial(float* dst_row, const float* x) {
+  float4* d = reinterpret_cast<float4*>(dst_row + (threadIdx.x & 31) * VPL);
+#pragma unroll
+  for (int k = 0; k < VPL / 4; ++k) __stcg(d + k, make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]));
+}
+// true for the warp whose item completes the row (count of items = 1 + nseg - SPIECE)
+__device__ __forceinline__ bool piece_last(int32_t* cnt, int64_t row, int nseg) {
+  return seg_last(cnt, row, 1 + nseg - SPIECE);
+}
+
+template <int H, int VPL>
+__global__ void __launch_bounds__(256, 3) k2_fagg_seg(const G2Args a) {
+  constexpr int HD = 32 * VPL, WS = fs_warp_smem_seg<H, VPL>();
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int myh = lane / (32 / H);
+  uint8_t* wsm = dsm + w * ((WS + 15) & ~15);
+  float* sa = reinterpret_cast<float*>(wsm + g8_ring_bytes<VPL>());   // [2][H][32]
+  int* sidx = reinterpret_cast<int*>(sa + 2 * H * 32);                // [2][32]
+  const uint32_t ring_lane = smem_u32(wsm) + lane * VPL;
+  const int8_t* lane_base = a.qHp + lane * VPL;
+  const uint32_t ld32 = (uint32_t)a.ldHp;
+  const uint64_t pol = l2_evict_last();
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t hc = load_count(a.pin.counts);
+  const int C = a.g.chunk;
+  const bool fast = (C % GR) == 0;
+  float amax_loc = 0.0f;
+  FOR_ITEMS(si, a.work + 1, hc) {
+    Seg s;
+    decode_item(si, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
+    if (s.c > 0 && s.c < SPIECE) continue;            // part of the row's piece 0
+    const int kseg = s.c == 0 ? (s.nseg < SPIECE ? s.nseg : SPIECE) : 1;
+    const int64_t rend = a.g.in_ptr[s.vl + 1];
+    const int64_t eb = s.eb, ee = eb + (int64_t)kseg * C < rend ? eb + (int64_t)kseg * C : rend;
+    const int T = (int)(ee - eb);
+    const DstSm<H> d = load_dst<H>(a, a.g.row_begin + s.vl);
+    auto alpha_of = [&](int c, const int8_t (&qs)[H], float (&al)[H]) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) al[h] = 0.0f;
+      if (c * 32 + lane < T) {
+        float ep[H];
+        alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+      }
+    };
+    auto stash = [&](int c, const float (&al)[H]) {
+      const int b = c & 1;
+#pragma unroll
+      for (int h = 0; h < H; ++h) sa[(b * H + h) * 32 + lane] = al[h];
+    };
+    auto edge_u = [&](int c) -> int { return c * 32 + lane < T ? __ldcs(a.g.in_src + eb + c * 32 + lane) : 0; };
+    const int nch = (T + 31) >> 5, ng = (T + GR - 1) / GR;
+    int u1;
+    {
+      const int u0 = edge_u(0);
+      int8_t qs0[H];
+      load_qh<H>(a.qS + (int64_t)u0 * H, qs0);
+      float al0[H];
+      alpha_of(0, qs0, al0);
+      stash(0, al0);
+      sidx[lane] = u0;
+      u1 = edge_u(1);
+      sidx[32 + lane] = u1;
+    }
+    __syncwarp();
+    g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, 0, true, pol);
+    g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, 1, 1 < ng, pol);
+    float2 acc[VPL / 2];
+#pragma unroll
+    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
+    PieceFold<VPL> pf;
+    pf.nfold = 0;
+    for (int c = 0; c < nch; ++c) {
+      const int u2 = edge_u(c + 2);
+      int8_t qs1[H];
+      load_qh<H>(a.qS + (int64_t)u1 * H, qs1);
+      const float* sac = sa + ((c & 1) * H + myh) * 32;
+      for (int i0 = 0; i0 < 32; i0 += GR) {
+        const int t0 = c * 32 + i0;
+        if (t0 >= T) break;
+        const int g = t0 / GR;
+        cp_wait<1>();
+        const uint32_t s0 = ring_lane + (uint32_t)(g & 1) * (GR * 32 * VPL);
+        const float4 a4 = *reinterpret_cast<const float4*>(sac + i0);
+        const float4 b4 = *reinterpret_cast<const float4*>(sac + i0 + 4);
+        const float al[GR] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
+        if (fast) {
+          if (t0 > 0 && t0 % C == 0) pf.fold(acc);
+#pragma unroll
+          for (int j = 0; j < GR; ++j) {
+            const Row<VPL> rj = lds_row_slice<VPL>(s0 + j * 32 * VPL);
+            const float2 al2 = make_float2(al[j], al[j]);
+#pragma unroll
+            for (int q = 0; q < VPL / 4; ++q) fma4_biased(rj.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < GR; ++j) {
+            if (t0 + j > 0 && t0 + j < T && (t0 + j) % C == 0) pf.fold(acc);
+            const Row<VPL> rj = lds_row_slice<VPL>(s0 + j * 32 * VPL);
+            const float2 al2 = make_float2(al[j], al[j]);
+#pragma unroll
+            for (int q = 0; q < VPL / 4; ++q) fma4_biased(rj.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+          }
+        }
+        g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, g + 2, g + 2 < ng, pol);
+      }
+      __syncwarp();
+      if (c + 1 < nch) {
+        float al1[H];
+        alpha_of(c + 1, qs1, al1);
+        stash(c + 1, al1);
+        sidx[(c & 1) * 32 + lane] = u2;
+      }
+      __syncwarp();
+      u1 = u2;
+    }
+    pf.fold(acc);   // the last chunk's partial
+    float* out_row = nullptr;
+    if (s.nseg <= SPIECE) {
+      out_row = a.Hout + s.vl * HD;   // the whole row in this piece
+    } else {
+      store_partial<VPL>(a.hagg + (int64_t)(s.c == 0 ? s.base : s.base + s.c) * HD, pf.tot);
+      if (!piece_last(a.hcnt, s.vl, s.nseg)) continue;
+      fold_tail<VPL>(a.hagg, s.base, s.nseg, pf.tot);
+      out_row = a.Hout + s.vl * HD;
+    }
+    float4* dst = reinterpret_cast<float4*>(out_row + lane * VPL);
+#pragma unroll
+    for (int k = 0; k < VPL / 4; ++k) {
+      float o[4];
+#pragma unroll
+      for (int z = 0; z < 4; ++z) {
+        o[z] = __fmul_rn(pf.tot[4 * k + z], scH.s);
+        amax_loc = fmaxf(amax_loc, fabsf(o[z]));
+      }
+      __stcs(dst + k, make_float4(o[0], o[1], o[2], o[3]));
+    }
+  }
+  amax_flush(a.amax_out, amax_loc);
+}
+
 // ================================================================== P1: source rows, ⑤′ + ⑤″
 // Per out-edge e' = (u → v): gather q_G[v] (excess-128 codes); ∂α[e'] = i2f(q_G[v]·q_H′[u])·s_G s_H′ (u's
 // row in registers as plain codes, exact IDP4A dot + 4-edge transposed reduction); acc += α·q_G[v] with α
@@ -673,8 +870,8 @@ __global__ void __launch_bounds__(256, 3) k2_fagg(const G2Args a) {
 // the in-CSR -> out-CSR position map).  Rows: ∂H′_agg = acc·s_G into dHp (finalized by P3).
 template <int H, int VPL>
 __host__ __device__ constexpr int bs_warp_smem() {
-  // ring | α [2][H][32] | rows [2][32] | in-CSR slots [2][32] | out-CSR slots [2][32] | ∂α [H][32] | tile rows
-  return g8_ring_bytes<VPL>() + 2 * H * 32 * 4 + 3 * 2 * 32 * 4 + H * 32 * 4 + 2 * 32;
+  // ring | α [2][H][32] | rows [2][32] | out-CSR slots [2][32] | ∂α [H][32] | tile rows
+  return g8_ring_bytes<VPL>() + 2 * H * 32 * 4 + 2 * 2 * 32 * 4 + H * 32 * 4 + 2 * 32;
 }
 template <int H, int VPL, int NW>
 __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
@@ -685,8 +882,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
   uint8_t* wsm = dsm + w * ((WS + 15) & ~15);
   float* sa = reinterpret_cast<float*>(wsm + g8_ring_bytes<VPL>());   // [2][H][32] α
   int* sidx = reinterpret_cast<int*>(sa + 2 * H * 32);                // [2][32] gather rows (v)
-  int* seid = sidx + 64;                                              // [2][32] in-CSR position
-  int* seo = seid + 64;                                               // [2][32] out-CSR position
+  int* seo = sidx + 64;                                               // [2][32] out-CSR position
   float* sd = reinterpret_cast<float*>(seo + 64);                     // [H][32] ∂α of the chunk
   uint8_t* srow = reinterpret_cast<uint8_t*>(sd + H * 32);           // [2][32]
   const uint32_t ring_lane = smem_u32(wsm) + lane * VPL;
@@ -701,8 +897,9 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
   const int64_t n = a.g.n_local, hc = load_count(a.pout.counts);
   const int64_t nitems = hc + load_count(a.pout.counts + 2);
   const int8_t* obase = a.qHp + lane * VPL;      // own: q_H′[u] (excess-128 -> flipped to plain)
-  FOR_ITEMS(item, a.work + 2, nitems) {
-    const bool tile = item >= hc;
+  FOR_ITEMS(it, a.work + 7, nitems - hc) {   // light sub-tiles (hub rows: k2_bsrc1_seg)
+    const int64_t item = hc + it;
+    constexpr bool tile = true;
     Seg s;
     s.eb = 0; s.vl = 0; s.slot = -1; s.nseg = 1;
     TileCtx t;
@@ -742,14 +939,11 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
       return s.eb + (pos < T ? pos : T - 1);
     };
     // attributes of a chunk: α (needs v's softmax data), in-CSR slot, out-CSR slot, tile row
-    struct AttrIn { DstSm<H> d; int eid; };
+    struct AttrIn { DstSm<H> d; };
     auto attr_load = [&](int c, int v, int64_t e) {
       AttrIn x;
-      x.eid = 0;
-      if (c * 32 + lane < T) {
-        x.eid = __ldcs(a.g.out_eid + e);
-        x.d = load_rec<H>(a, v);
-      }
+      (void)e;
+      if (c * 32 + lane < T) x.d = load_rec<H>(a, v);
       return x;
     };
     auto attrs = [&](int c, int row, const AttrIn& x, float (&al)[H]) {
@@ -763,12 +957,11 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
         alpha_rec<H>(qs, x.d, scS.s, scD.s, a.slope, ep, al);
       }
     };
-    auto stash = [&](int c, int row, int eid, int64_t e, const float (&al)[H]) {
+    auto stash = [&](int c, int row, int64_t e, const float (&al)[H]) {
       const int b = c & 1;
 #pragma unroll
       for (int h = 0; h < H; ++h) sa[(b * H + h) * 32 + lane] = al[h];
       srow[b * 32 + lane] = (uint8_t)row;
-      seid[b * 32 + lane] = eid;
       seo[b * 32 + lane] = (int)e;
     };
     const int nch = (T + 31) >> 5, ng = (T + GR - 1) / GR;
@@ -781,7 +974,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
       float al0[H];
       const AttrIn x0 = attr_load(0, v0, e0);
       attrs(0, row0, x0, al0);
-      stash(0, row0, x0.eid, e0, al0);
+      stash(0, row0, e0, al0);
       sidx[lane] = v0;
       e1 = pos_of(1, row1);
       if (32 + lane < T) v1 = __ldcs(a.g.out_dst + e1);
@@ -891,7 +1084,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
       if (c + 1 < nch) {
         float al1[H];
         attrs(c + 1, row1, x1, al1);
-        stash(c + 1, row1, x1.eid, e1, al1);
+        stash(c + 1, row1, e1, al1);
         sidx[b * 32 + lane] = v2;
       }
       __syncwarp();
@@ -931,6 +1124,156 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
     for (int k = 0; k < VPL / 4; ++k)
       dst[k] = make_float4(__fmul_rn(tot[4 * k], scG.s), __fmul_rn(tot[4 * k + 1], scG.s),
                            __fmul_rn(tot[4 * k + 2], scG.s), __fmul_rn(tot[4 * k + 3], scG.s));
+  }
+}
+
+// ================================================================== P1, hub rows: segment pieces
+// As k2_fagg_seg for the source pass: piece 0 folds the row's first SPIECE out-CSR chunks in registers,
+// further chunks write partials folded by the row's last item; u's own q_H′ row (the ⑤″ dot operand) is
+// fixed for the whole piece, and the piece's ∂α are written coalesced at their out-CSR positions.
+template <int H, int VPL>
+__host__ __device__ constexpr int bs_warp_smem_seg() {   // ring | α [2][H][32] | rows [2][32] | ∂α [H][32]
+  return g8_ring_bytes<VPL>() + 2 * H * 32 * 4 + 2 * 32 * 4 + H * 32 * 4;
+}
+template <int H, int VPL, int NW>
+__global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a) {
+  constexpr int HD = 32 * VPL, LPH = 32 / H, WS = bs_warp_smem_seg<H, VPL>();
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int myh = lane / LPH;
+  uint8_t* wsm = dsm + w * ((WS + 15) & ~15);
+  float* sa = reinterpret_cast<float*>(wsm + g8_ring_bytes<VPL>());   // [2][H][32] α
+  int* sidx = reinterpret_cast<int*>(sa + 2 * H * 32);                // [2][32] gather rows (v)
+  float* sd = reinterpret_cast<float*>(sidx + 64);                    // [H][32] ∂α of the chunk
+  const uint32_t ring_lane = smem_u32(wsm) + lane * VPL;
+  const int8_t* lane_base = a.qG + lane * VPL;
+  const uint32_t ld32 = (uint32_t)a.ldG;
+  const uint64_t pol = l2_evict_last();
+  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
+  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const float sGH = __fmul_rn(scG.s, scH.s);
+  const int64_t hc = load_count(a.pout.counts);
+  const int C = a.g.chunk;
+  const bool fast = (C % GR) == 0;
+  FOR_ITEMS(si, a.work + 2, hc) {
+    Seg s;
+    decode_item(si, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
+    if (s.c > 0 && s.c < SPIECE) continue;
+    const int kseg = s.c == 0 ? (s.nseg < SPIECE ? s.nseg : SPIECE) : 1;
+    const int64_t rend = a.g.out_ptr[s.vl + 1];
+    const int64_t eb = s.eb, ee = eb + (int64_t)kseg * C < rend ? eb + (int64_t)kseg * C : rend;
+    const int T = (int)(ee - eb);
+    const int64_t ug = a.g.row_begin + s.vl;
+    int8_t qs[H];
+    load_qh<H>(a.qS + ug * H, qs);
+    Row<VPL> ow = load_row<VPL>(a.qHp + ug * a.ldHp + lane * VPL);
+    const int osum = row_sum_plain<VPL>(ow, true);
+    auto edge_v = [&](int c) -> int { return c * 32 + lane < T ? __ldcs(a.g.out_dst + eb + c * 32 + lane) : 0; };
+    auto alpha_of = [&](int c, const DstSm<H>& d, float (&al)[H]) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) al[h] = 0.0f;
+      if (c * 32 + lane < T) {
+        float ep[H];
+        alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+      }
+    };
+    auto stash = [&](int c, const float (&al)[H]) {
+      const int b = c & 1;
+#pragma unroll
+      for (int h = 0; h < H; ++h) sa[(b * H + h) * 32 + lane] = al[h];
+    };
+    const int nch = (T + 31) >> 5, ng = (T + GR - 1) / GR;
+    int v1;
+    {
+      const int v0 = edge_v(0);
+      DstSm<H> d0;
+      if (lane < T) d0 = load_rec<H>(a, v0);
+      float al0[H];
+      alpha_of(0, d0, al0);
+      stash(0, al0);
+      sidx[lane] = v0;
+      v1 = edge_v(1);
+      sidx[32 + lane] = v1;
+    }
+    __syncwarp();
+    g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, 0, true, pol);
+    g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, 1, 1 < ng, pol);
+    float2 acc[VPL / 2];
+#pragma unroll
+    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
+    PieceFold<VPL> pf;
+    pf.nfold = 0;
+    for (int c = 0; c < nch; ++c) {
+      const int v2 = edge_v(c + 2);
+      DstSm<H> d1;
+      if ((c + 1) * 32 + lane < T) d1 = load_rec<H>(a, v1);
+      const float* sac = sa + ((c & 1) * H + myh) * 32;
+      for (int i0 = 0; i0 < 32; i0 += GR) {
+        const int t0 = c * 32 + i0;
+        if (t0 >= T) break;
+        const int g = t0 / GR;
+        cp_wait<1>();
+        const uint32_t s0 = ring_lane + (uint32_t)(g & 1) * (GR * 32 * VPL);
+        const float4 a4 = *reinterpret_cast<const float4*>(sac + i0);
+        const float4 b4 = *reinterpret_cast<const float4*>(sac + i0 + 4);
+        const float al[GR] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
+        int dd[GR];
+        if (fast && t0 > 0 && t0 % C == 0) pf.fold(acc);
+#pragma unroll
+        for (int j = 0; j < GR; ++j) {
+          if (!fast && t0 + j > 0 && t0 + j < T && (t0 + j) % C == 0) pf.fold(acc);
+          const Row<VPL> rj = lds_row_slice<VPL>(s0 + j * 32 * VPL);
+          dd[j] = row_dot_biased<VPL>(rj, ow, osum);
+          const float2 al2 = make_float2(al[j], al[j]);
+#pragma unroll
+          for (int q = 0; q < VPL / 4; ++q) fma4_biased(rj.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+        }
+        {
+          int k;
+          const int d0[4] = {dd[0], dd[1], dd[2], dd[3]}, d1x[4] = {dd[4], dd[5], dd[6], dd[7]};
+          const int x0 = group_dot_reduce<LPH>(d0, k);
+          const int x1 = group_dot_reduce<LPH>(d1x, k);
+          sd[myh * 32 + i0 + k] = __fmul_rn(__int2float_rn(x0), sGH);
+          sd[myh * 32 + i0 + 4 + k] = __fmul_rn(__int2float_rn(x1), sGH);
+        }
+        g8_fill<VPL>(ring_lane, lane_base, ld32, sidx, g + 2, g + 2 < ng, pol);
+      }
+      __syncwarp();
+      if (c * 32 + lane < T) {   // ∂α of this chunk at its out-CSR positions (coalesced)
+        float o[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) o[h] = sd[h * 32 + lane];
+        float4 o4;
+        if constexpr (H == 4) {
+          o4 = make_float4(o[0], o[1], o[2], o[3]);
+          __stcs(reinterpret_cast<float4*>(a.dal_out + (eb + c * 32 + lane) * H), o4);
+        } else {
+          st_h<H>(a.dal_out + (eb + c * 32 + lane) * H, o);
+        }
+      }
+      __syncwarp();
+      if (c + 1 < nch) {
+        float al1[H];
+        alpha_of(c + 1, d1, al1);
+        stash(c + 1, al1);
+        sidx[(c & 1) * 32 + lane] = v2;
+      }
+      __syncwarp();
+      v1 = v2;
+    }
+    pf.fold(acc);
+    if (s.nseg > SPIECE) {
+      store_partial<VPL>(a.hagg + (int64_t)(s.c == 0 ? s.base : s.base + s.c) * HD, pf.tot);
+      if (!piece_last(a.hcnt, s.vl, s.nseg)) continue;
+      fold_tail<VPL>(a.hagg, s.base, s.nseg, pf.tot);
+    }
+    float4* dst = reinterpret_cast<float4*>(a.dHp + s.vl * HD + lane * VPL);
+#pragma unroll
+    for (int k = 0; k < VPL / 4; ++k)
+      dst[k] = make_float4(__fmul_rn(pf.tot[4 * k], scG.s), __fmul_rn(pf.tot[4 * k + 1], scG.s),
+                           __fmul_rn(pf.tot[4 * k + 2], scG.s), __fmul_rn(pf.tot[4 * k + 3], scG.s));
   }
 }
 
@@ -1353,14 +1696,17 @@ cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st) {
   if (hv == H_ * 100 + V_) {                                                                         \
     ok = true;                                                                                       \
     constexpr int smem = 8 * ((fa_warp_smem<H_, V_>() + 15) & ~15);                                   \
+    constexpr int smem_s = 8 * ((fs_warp_smem_seg<H_, V_>() + 15) & ~15);                             \
     static bool attr = false;                                                                        \
     if (!attr) {                                                                                     \
       cudaFuncSetAttribute(k2_fagg<H_, V_>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);      \
+      cudaFuncSetAttribute(k2_fagg_seg<H_, V_>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s); \
       attr = true;                                                                                   \
     }                                                                                                \
     { ProfScope p("gat_fwd_stats1", st); k2_fstats1<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
     { ProfScope p("gat_fwd_stats", st); k2_fstats2<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
-    { ProfScope p("gat_fwd_agg", st); k2_fagg<H_, V_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 3), 256, smem, st>>>(a); } \
+    { ProfScope p("gat_fwd_agg_hub", st); k2_fagg_seg<H_, V_><<<grid_items((a.pin.cap + 7) / 8, 3), 256, smem_s, st>>>(a); } \
+    { ProfScope p("gat_fwd_agg", st); k2_fagg<H_, V_><<<grid_items((a.pin.tcap + 7) / 8, 3), 256, smem, st>>>(a); } \
   }
   G2_CASES(X)
 #undef X
@@ -1377,12 +1723,15 @@ cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st) {
   if (hv == H_ * 100 + V_) {                                                                         \
     ok = true;                                                                                       \
     constexpr int NW = 4, smem = NW * ((bs_warp_smem<H_, V_>() + 15) & ~15);                          \
+    constexpr int smem_s = NW * ((bs_warp_smem_seg<H_, V_>() + 15) & ~15);                           \
     static bool attr = false;                                                                        \
     if (!attr) {                                                                                     \
       cudaFuncSetAttribute(k2_bsrc1<H_, V_, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      cudaFuncSetAttribute(k2_bsrc1_seg<H_, V_, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s); \
       attr = true;                                                                                   \
     }                                                                                                \
-    { ProfScope p("gat_bwd_src", st); k2_bsrc1<H_, V_, NW><<<grid_items((a.pout.cap + a.pout.tcap + NW - 1) / NW, 20 / NW), NW * 32, smem, st>>>(a); } \
+    { ProfScope p("gat_bwd_src_hub", st); k2_bsrc1_seg<H_, V_, NW><<<grid_items((a.pout.cap + NW - 1) / NW, 20 / NW), NW * 32, smem_s, st>>>(a); } \
+    { ProfScope p("gat_bwd_src", st); k2_bsrc1<H_, V_, NW><<<grid_items((a.pout.tcap + NW - 1) / NW, 20 / NW), NW * 32, smem, st>>>(a); } \
     { ProfScope p("gat_bwd_dst", st); k2_bdst_a<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
     { ProfScope p("gat_bwd_dst2", st); k2_bdst_b<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
     { ProfScope p("gat_bwd_src2", st); k2_bsrc2<H_, V_><<<grid_items((a.pout.cap + a.pout.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \

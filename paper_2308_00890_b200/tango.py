@@ -493,6 +493,13 @@ class GATLayer:
                "tango_gat_layer_bwd")
         return dH, dW, da_s, da_d
 
+    def view_dataflow(self) -> int:
+        """1: round-1 kernels (gat.cu), 2: v6 single-GPU dataflow (gat2.cu)."""
+        v = GatCtxView()
+        _check(load().tango_gat_ctx_get_view(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), C.byref(v)),
+               "tango_gat_ctx_get_view")
+        return int(v.dataflow)
+
     def view(self):
         """Device tensors inside ctx (copies), for parity tests."""
         L = load()

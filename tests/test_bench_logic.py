@@ -17,10 +17,24 @@ def test_models_cover_the_roofline_candidates():
         m = bench.kernel_model(name, 1000, 100, 128, 4, 512, {}, 1965.0)
         assert m is not None and m[0] > 0 and m[1] > 0
     assert bench.kernel_model("gat_bwd_src_hub", 1000, 100, 128, 4, 512, {}, 1965.0) is None
-    # the pass model counts every edge: bytes grow with E at the per-edge rate
-    b1 = bench.kernel_model("gat_bwd_src", 1000, 100, 128, 4, 512, {}, 1965.0)[0]
-    b2 = bench.kernel_model("gat_bwd_src", 2000, 100, 128, 4, 512, {}, 1965.0)[0]
-    assert b2 - b1 == 1000 * (8 + 8 * 4 + 512)
+    # the pass model counts every edge: bytes grow with E at the per-edge rate of each dataflow
+    for df, per_edge in ((1, 8 + 8 * 4 + 512), (2, 4 + 512 + 13 * 4)):
+        b1 = bench.kernel_model("gat_bwd_src", 1000, 100, 128, 4, 512, {}, 1965.0, df)[0]
+        b2 = bench.kernel_model("gat_bwd_src", 2000, 100, 128, 4, 512, {}, 1965.0, df)[0]
+        assert b2 - b1 == 1000 * per_edge
+    # v6 passes merge their launches; the ALU peak follows the unit counts (148 SMs x 128 lanes x clock)
+    r = bench.pass_profile({"gat_bwd_dst": (1.0, 5), "gat_bwd_dst2": (0.5, 5), "gat_fwd_stats": (0.2, 5),
+                            "gat_fwd_stats1": (0.1, 5)})
+    assert r == {"gat_bwd_dst": (1.5, 5), "gat_fwd_stats": (0.30000000000000004, 5)}
+    assert abs(bench.alu_peak(1965.0) - 148 * 128 * 1.965e9) < 1
+
+
+def test_pass_bound_follows_the_l2():
+    # gather passes are issue-bound while the gathered int8 table fits in L2 (Reddit: 233 K x 512 B)
+    assert bench.pass_bound("gat_fwd_agg", 232_965 * 512) == "alu"
+    assert bench.pass_bound("gat_bwd_src", 2_449_029 * 512) == "hbm"     # products: 1.25 GB table
+    assert bench.pass_bound("gat_bwd_dst", 1000) == "hbm"
+    assert bench.ncu_traffic("no-such-workload", "gat_bwd_src") is None
 
 
 def test_relabel_by_degree_is_a_permutation():
