@@ -739,6 +739,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     T.load()
+    if os.environ.get("TANGO_L2_FETCH"):
+        prev = T.set_l2_fetch_granularity(int(os.environ["TANGO_L2_FETCH"]))
+        print(f"L2 fetch granularity {prev} -> {os.environ['TANGO_L2_FETCH']}", file=sys.stderr)
     peaks, peak_kind = load_peaks()
     l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
 

@@ -453,6 +453,12 @@ void tango_profile_reset(void);
  * kernel alone (bench.py's per-kernel pass).  Results are identical either way.  Process-wide. */
 void tango_profile_serialize(int32_t on);
 
+/* L2 fetch granularity for the calling thread's device (cudaLimitMaxL2FetchGranularity, bytes in
+ * {0, 32, 64, 128}): the v6 passes gather 16-B per-edge records at random positions (∂α through the
+ * in-CSR -> out-CSR map) and 4-B node codes, where a 128-B L2 fill multiplies the DRAM traffic.
+ * Process-wide device setting, not a stream operation; *before (nullable) receives the previous value. */
+tango_status tango_set_l2_fetch_granularity(int32_t bytes, int32_t* before);
+
 
 #ifdef __cplusplus
 }

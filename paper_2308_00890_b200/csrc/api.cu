@@ -123,6 +123,15 @@ int tango_abi_version(void) { return TANGO_ABI_VERSION; }
 
 void tango_profile_serialize(int32_t on) { g_serialize.store(on ? 1 : 0, std::memory_order_relaxed); }
 
+tango_status tango_set_l2_fetch_granularity(int32_t bytes, int32_t* before) {
+  if (!(bytes == 0 || bytes == 32 || bytes == 64 || bytes == 128)) return TANGO_ERR_INVALID_ARG;
+  size_t prev = 0;
+  TRY_CUDA(cudaDeviceGetLimit(&prev, cudaLimitMaxL2FetchGranularity));
+  if (before) *before = (int32_t)prev;
+  TRY_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes));
+  return TANGO_OK;
+}
+
 
 tango_status tango_status_poll(const int32_t* dev_status, cudaStream_t stream, tango_status* out) {
   if (!dev_status || !out) return TANGO_ERR_INVALID_ARG;
@@ -616,6 +625,7 @@ G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_p
   a.m = (float*)(c + L.off_m); a.den = (float*)(c + L.off_den);
   a.P = (float*)(c + L.off_P); a.dD = (float*)(c + L.off_dD); a.dS = (float*)(c + L.off_dS);
   a.dal_out = (float*)(c + L.off_alpha);
+  a.dal_in = (float*)(c + L.off_alpha) + L.E * L.H;
   a.a_src = p->a_src; a.a_dst = p->a_dst;
   a.dHp = (float*)(c + L.off_dHp); a.amax_dHp = sc + SL_AMAX_DHP;
   a.pin = plan_of(c, L.off_pin_hbase, L.off_pin_hseg, L.off_pin_hrow, L.off_pin_cnt, L.cap_in, L.off_pin_tiles, L.tcap);
@@ -782,7 +792,9 @@ tango_status tango_gat_layer_fwd(const tango_graph* G, const tango_gat_params* p
     G2Args a2 = g2_args(L, c, g, p);
     a2.Hout = H_out; a2.amax_out = reinterpret_cast<unsigned*>(amax_out);
     TRY_CUDA(cudaMemsetAsync(a2.hcnt, 0, (size_t)L.n * 4, st));
-    TRY(launch_status(launch_gat2_fwd(a2, st)));
+    TRY_CUDA(cudaMemsetAsync(a2.nrec, 0, (size_t)L.N * a2.nrs * 4, st));   // m keys of hub rows start below all
+    const SideStream side = aux->side(4);
+    TRY(launch_status(launch_gat2_fwd(a2, st, &side)));
   } else {
     const SideStream side = aux->side(4);
     TRY(launch_status(launch_gat_fwd(fa, st, &side)));
@@ -881,7 +893,8 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
     a2.da_src = da_src; a2.da_dst = da_dst;
     TRY_CUDA(cudaMemsetAsync(a2.hcnt, 0, (size_t)L.n * 4, st));
     TRY_CUDA(cudaStreamWaitEvent(st, aux->ev[1], 0));   // out-CSR plan and in-CSR -> out-CSR map done
-    TRY(launch_status(launch_gat2_bwd(a2, st)));
+    const SideStream side = aux->side(4);
+    TRY(launch_status(launch_gat2_bwd(a2, st, &side)));
     // ∂a (needs ∂S, ∂D; deterministic chunk order, R39) on the side stream, beside B8/B9
     TRY_CUDA(stream_after(aux->s, st, aux->ev[2]));
     TRY(launch_status(launch_gat2_attn_grad(a2, aux->s)));

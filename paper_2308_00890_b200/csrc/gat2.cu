@@ -55,6 +55,16 @@ __device__ __forceinline__ void st_h(float* __restrict__ p, const float (&o)[H])
   }
 }
 
+// order-preserving unsigned key of a float (never −0 or NaN here: el = lrelu(e_pre) and e_pre is a sum
+// of two products of finite values, which is never −0)
+__device__ __forceinline__ unsigned fkey(float x) {
+  const unsigned b = __float_as_uint(x);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_dec(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
 // per-destination data of the edge softmax: q_D row, m, den
 template <int H>
 struct DstSm {
@@ -148,11 +158,12 @@ __device__ __forceinline__ float seg_partial(int64_t eb, int64_t ee, float (*bx)
   const int lane = threadIdx.x & 31;
   float acc = 0.0f;   // lane h < H: head h
   const int cnt = (int)(ee - eb);
+  // the next batch's loads are issued before this batch's sequential sums (latency overlap)
+  auto l0 = ld(eb + (lane < cnt ? lane : 0));
+  auto l1 = ld(eb + (lane + 32 < cnt ? lane + 32 : 0));
   for (int b0 = 0; b0 < cnt; b0 += SB) {
     const int bc = cnt - b0 < SB ? cnt - b0 : SB;
     const bool v0 = lane < bc, v1 = lane + 32 < bc;
-    const auto l0 = ld(eb + b0 + (v0 ? lane : 0));
-    const auto l1 = ld(eb + b0 + (v1 ? lane + 32 : 0));
     float x[H], y[H];
     if (v0) {
       cv(l0, x, y);
@@ -165,6 +176,11 @@ __device__ __forceinline__ float seg_partial(int64_t eb, int64_t ee, float (*bx)
       for (int h = 0; h < H; ++h) { bx[lane + 32][h] = x[h]; if (FMA) by[lane + 32][h] = y[h]; }
     }
     __syncwarp();
+    const int nb = b0 + SB;
+    if (nb < cnt) {
+      l0 = ld(eb + nb + (nb + lane < cnt ? lane : 0));
+      l1 = ld(eb + nb + (nb + lane + 32 < cnt ? lane + 32 : 0));
+    }
     if (lane < H) {
       int i = 0;
       for (; i + 4 <= bc; i += 4) {
@@ -226,7 +242,8 @@ __device__ __forceinline__ float seg_fold_max(const float* part, int base, int n
 }  // namespace
 
 // ================================================================== F-stats: m, den per destination
-// FS1 (hub segments): segment max of el = lrelu(e_pre); the row's last segment writes m = max over them.
+// FS1 (hub segments): segment max of el = lrelu(e_pre), folded into the row's m by an atomic max on
+// order-preserving keys (max is order-free: no partials, no fold).
 // FS2 (hub segments, then light sub-tiles): segment Σ exp_p(el − m) partial, folded in chunk order by the
 // row's last segment into den; a light sub-tile computes m and den of its rows in two lane-parallel passes
 // (per-row max by a segmented lane scan, Σ by the row's owner lane in edge order).
@@ -261,13 +278,9 @@ __global__ void __launch_bounds__(256, 4) k2_fstats1(const G2Args a) {
     }
 #pragma unroll
     for (int h = 0; h < H; ++h) mx[h] = warp_max(mx[h]);
-    if (lane < H) __stcg(a.h1 + (int64_t)s.slot * H + lane, head_pick<H>(mx, lane));
-    if (!seg_last(a.hcnt, s.vl, s.nseg)) continue;
-    const float m = seg_fold_max<H>(a.h1, s.base, s.nseg);
-    if (lane < H) {
-      a.m[vg * H + lane] = m;
-      rec_put1(a, vg, 0, lane, m);
-    }
+    // max is order-free: every segment folds its maximum into the row's m field of the node record
+    // (order-preserving unsigned keys; the record is zeroed at the start of the forward, below any key)
+    if (lane < H) atomicMax(reinterpret_cast<unsigned*>(a.nrec + vg * a.nrs) + lane, fkey(head_pick<H>(mx, lane)));
   }
 }
 
@@ -287,7 +300,8 @@ __global__ void __launch_bounds__(256, 4) k2_fstats2(const G2Args a) {
       int8_t qd[H];
       load_qh<H>(a.qD + vg * H, qd);
       float m[H];
-      ld_h<H>(a.m + vg * H, m);
+#pragma unroll
+      for (int h = 0; h < H; ++h) m[h] = fkey_dec(reinterpret_cast<const unsigned*>(a.nrec + vg * a.nrs)[h]);
       struct L { int8_t qs[H]; };
       const float part = seg_partial<H, false>(
           s.eb, s.ee, sbx[w], nullptr,
@@ -300,7 +314,9 @@ __global__ void __launch_bounds__(256, 4) k2_fstats2(const G2Args a) {
       if (lane < H) __stcg(a.h2 + (int64_t)s.slot * H + lane, part);
       if (!seg_last(a.hcnt, s.vl, s.nseg)) continue;
       const float den = seg_fold<H>(a.h2, s.base, s.nseg);
-      if (lane < H) {
+      if (lane < H) {   // the row's m (as a float) and den; every segment of the row has read the keys
+        a.m[vg * H + lane] = head_pick<H>(m, lane);
+        rec_put1(a, vg, 0, lane, head_pick<H>(m, lane));
         a.den[vg * H + lane] = den;
         rec_put1(a, vg, 1, lane, den);
       }
@@ -668,11 +684,11 @@ __global__ void __launch_bounds__(256, 3) k2_fagg(const G2Args a) {
 }
 
 // ================================================================== F-agg, hub rows: segment pieces
-// A hub row (degree > C_E) is cut into its canonical chunks.  A warp takes the row's first SPIECE chunks as
-// one piece and folds their partials itself in registers (total = p_0, total = total + p_c), so rows of
-// up to SPIECE chunks (the common hub on Reddit-like graphs) write no partials at all; each further chunk
-// is its own item whose partial goes to scratch, and the row's last finishing item continues the fold
-// from piece 0's running total in chunk order — the same left-to-right fold as the oracle's Σᶜ.
+// A hub row (degree > C_E) is cut into its canonical chunks.  A row of at most SPIECE chunks (the common hub
+// on Reddit-like graphs) is one warp item that folds its chunk partials itself in registers (total = p_0,
+// total = total + p_c) and writes no partials; a longer row is spread chunk by chunk over warps whose
+// partials go to scratch, and the row's last finishing item folds them in chunk order — the same
+// left-to-right fold as the oracle's Σᶜ.
 constexpr int SPIECE = 4;
 
 // groups of one piece: 8 edges; a chunk boundary can only fall on a group start when C_E % 8 == 0 (the
@@ -697,8 +713,12 @@ __host__ __device__ constexpr int fs_warp_smem_seg() {   // ring | α [2][H][32]
   return g8_ring_bytes<VPL>() + 2 * H * 32 * 4 + 2 * 32 * 4;
 }
 
-// last item of a split hub row: fold piece 0's running total (slot base) with the partials of chunks
-// SPIECE .. nseg-1 (slots base + c), in chunk order; every lane its VPL columns
+// chunks in a row's piece 0: the whole row when it has at most SPIECE chunks (folded in registers, no
+// partials), else the first chunk only (long rows stay spread over many warps)
+__device__ __forceinline__ int piece0(int nseg) { return nseg <= SPIECE ? nseg : 1; }
+
+// last item of a split hub row: fold piece 0's partial (slot base) with the partials of chunks
+// 1 .. nseg-1 (slots base + c), in chunk order; every lane its VPL columns
 template <int VPL>
 __device__ __forceinline__ void fold_tail(const float* hagg, int64_t base, int nseg, float (&tot)[VPL]) {
   constexpr int HD = 32 * VPL;
@@ -708,7 +728,7 @@ __device__ __forceinline__ void fold_tail(const float* hagg, int64_t base, int n
     const float4 v = __ldcg(reinterpret_cast<const float4*>(p0) + k);
     tot[4 * k] = v.x; tot[4 * k + 1] = v.y; tot[4 * k + 2] = v.z; tot[4 * k + 3] = v.w;
   }
-  for (int j = SPIECE; j < nseg; ++j) {
+  for (int j = 1; j < nseg; ++j) {
     const float4* pj = reinterpret_cast<const float4*>(p0 + (int64_t)j * HD);
 #pragma unroll
     for (int k = 0; k < VPL / 4; ++k) {
@@ -724,10 +744,8 @@ __device__ __forceinline__ void store_partial(float* dst_row, const float* x) {
 #pragma unroll
   for (int k = 0; k < VPL / 4; ++k) __stcg(d + k, make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]));
 }
-// true for the warp whose item completes the row (count of items = 1 + nseg - SPIECE)
-__device__ __forceinline__ bool piece_last(int32_t* cnt, int64_t row, int nseg) {
-  return seg_last(cnt, row, 1 + nseg - SPIECE);
-}
+// true for the warp whose item completes a split row (nseg > SPIECE: one item per chunk)
+__device__ __forceinline__ bool piece_last(int32_t* cnt, int64_t row, int nseg) { return seg_last(cnt, row, nseg); }
 
 template <int H, int VPL>
 __global__ void __launch_bounds__(256, 3) k2_fagg_seg(const G2Args a) {
@@ -752,8 +770,9 @@ __global__ void __launch_bounds__(256, 3) k2_fagg_seg(const G2Args a) {
   FOR_ITEMS(si, a.work + 1, hc) {
     Seg s;
     decode_item(si, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
-    if (s.c > 0 && s.c < SPIECE) continue;            // part of the row's piece 0
-    const int kseg = s.c == 0 ? (s.nseg < SPIECE ? s.nseg : SPIECE) : 1;
+    const int k0 = piece0(s.nseg);
+    if (s.c > 0 && s.c < k0) continue;                // part of the row's piece 0
+    const int kseg = s.c == 0 ? k0 : 1;
     const int64_t rend = a.g.in_ptr[s.vl + 1];
     const int64_t eb = s.eb, ee = eb + (int64_t)kseg * C < rend ? eb + (int64_t)kseg * C : rend;
     const int T = (int)(ee - eb);
@@ -1160,8 +1179,9 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
   FOR_ITEMS(si, a.work + 2, hc) {
     Seg s;
     decode_item(si, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
-    if (s.c > 0 && s.c < SPIECE) continue;
-    const int kseg = s.c == 0 ? (s.nseg < SPIECE ? s.nseg : SPIECE) : 1;
+    const int k0 = piece0(s.nseg);
+    if (s.c > 0 && s.c < k0) continue;
+    const int kseg = s.c == 0 ? k0 : 1;
     const int64_t rend = a.g.out_ptr[s.vl + 1];
     const int64_t eb = s.eb, ee = eb + (int64_t)kseg * C < rend ? eb + (int64_t)kseg * C : rend;
     const int T = (int)(ee - eb);
@@ -1279,7 +1299,8 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
 
 // ================================================================== P2: destination rows, ④′ + ③″
 // P[v] = Σᶜ fmaf(∂α, α) over in-edges (in-CSR order), ∂E = α(∂α − P[v]), ∂E_pre = e_pre > 0 ? ∂E : ∂E·slope,
-// ∂D[v] = Σᶜ ∂E_pre.  ∂α = dal_out[in2out[e]] (written by P1), α recomputed.
+// ∂D[v] = Σᶜ ∂E_pre.  ∂α = dal_out[in2out[e]] (written by P1), α recomputed; P2a also stores the gathered ∂α
+// of hub rows in in-CSR order (dal_in), so that P2b reads it coalesced.
 // P2a: hub segments (P partials, folded by the row's last segment) and light sub-tiles (P and ∂D);
 // P2b: hub segments (∂D partials with the row's P, folded likewise).
 template <int H>
@@ -1305,6 +1326,7 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
             EdgeIn<H> l;
             load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs);
             ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, l.da);
+            st_h<H>(a.dal_in + e * H, l.da);   // ∂α in in-CSR order for P2b (coalesced)
             return l;
           },
           [&](const EdgeIn<H>& l, float (&x)[H], float (&y)[H]) {
@@ -1410,7 +1432,7 @@ __global__ void __launch_bounds__(256, 4) k2_bdst_b(const G2Args a) {
         [&](int64_t e) {
           EdgeIn<H> l;
           load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs);
-          ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, l.da);
+          ld_h<H>(a.dal_in + e * H, l.da);
           return l;
         },
         [&](const EdgeIn<H>& l, float (&x)[H], float (&)[H]) {
@@ -1688,7 +1710,20 @@ bool gat2_supported(const GraphDev& g, int heads, int hd) {
 
 #define G2_CASES(X) X(1, 4) X(1, 8) X(1, 16) X(2, 4) X(2, 8) X(2, 16) X(4, 4) X(4, 8) X(4, 16) X(8, 4) X(8, 8) X(8, 16)
 
-cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st) {
+static cudaError_t fork2(cudaStream_t st, const SideStream* x) {
+  if (!x || x->s == st) return cudaSuccess;
+  cudaError_t e = cudaEventRecord(x->fork, st);
+  return e == cudaSuccess ? cudaStreamWaitEvent(x->s, x->fork, 0) : e;
+}
+static cudaError_t join2(cudaStream_t st, const SideStream* x) {
+  if (!x || x->s == st) return cudaSuccess;
+  cudaError_t e = cudaEventRecord(x->join, x->s);
+  return e == cudaSuccess ? cudaStreamWaitEvent(st, x->join, 0) : e;
+}
+
+// hub-row pieces on the side stream (when given) beside the light sub-tiles on st
+cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st, const SideStream* x) {
+  cudaStream_t sh = (x && x->s) ? x->s : st;
   const int hv = a.d.heads * 100 + a.d.hd / 32;
   bool ok = false;
   cudaError_t e = cudaSuccess;
@@ -1705,8 +1740,10 @@ cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st) {
     }                                                                                                \
     { ProfScope p("gat_fwd_stats1", st); k2_fstats1<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
     { ProfScope p("gat_fwd_stats", st); k2_fstats2<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
-    { ProfScope p("gat_fwd_agg_hub", st); k2_fagg_seg<H_, V_><<<grid_items((a.pin.cap + 7) / 8, 3), 256, smem_s, st>>>(a); } \
+    e = fork2(st, x);                                                                                \
+    { ProfScope p("gat_fwd_agg_hub", sh); k2_fagg_seg<H_, V_><<<grid_items((a.pin.cap + 7) / 8, 3), 256, smem_s, sh>>>(a); } \
     { ProfScope p("gat_fwd_agg", st); k2_fagg<H_, V_><<<grid_items((a.pin.tcap + 7) / 8, 3), 256, smem, st>>>(a); } \
+    if (e == cudaSuccess) e = join2(st, x);                                                          \
   }
   G2_CASES(X)
 #undef X
@@ -1715,7 +1752,8 @@ cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st) {
+cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st, const SideStream* x) {
+  cudaStream_t sh = (x && x->s) ? x->s : st;
   const int hv = a.d.heads * 100 + a.d.hd / 32;
   bool ok = false;
   cudaError_t e = cudaSuccess;
@@ -1730,8 +1768,10 @@ cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st) {
       cudaFuncSetAttribute(k2_bsrc1_seg<H_, V_, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s); \
       attr = true;                                                                                   \
     }                                                                                                \
-    { ProfScope p("gat_bwd_src_hub", st); k2_bsrc1_seg<H_, V_, NW><<<grid_items((a.pout.cap + NW - 1) / NW, 20 / NW), NW * 32, smem_s, st>>>(a); } \
+    e = fork2(st, x);                                                                                \
+    { ProfScope p("gat_bwd_src_hub", sh); k2_bsrc1_seg<H_, V_, NW><<<grid_items((a.pout.cap + NW - 1) / NW, 20 / NW), NW * 32, smem_s, sh>>>(a); } \
     { ProfScope p("gat_bwd_src", st); k2_bsrc1<H_, V_, NW><<<grid_items((a.pout.tcap + NW - 1) / NW, 20 / NW), NW * 32, smem, st>>>(a); } \
+    if (e == cudaSuccess) e = join2(st, x);                                                          \
     { ProfScope p("gat_bwd_dst", st); k2_bdst_a<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
     { ProfScope p("gat_bwd_dst2", st); k2_bdst_b<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
     { ProfScope p("gat_bwd_src2", st); k2_bsrc2<H_, V_><<<grid_items((a.pout.cap + a.pout.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \

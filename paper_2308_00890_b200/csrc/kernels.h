@@ -153,6 +153,7 @@ struct G2Args {
   float* Hout; unsigned* amax_out;                           // forward output [n][HD]
   float* P; float* dD; float* dS;                            // [N][H]
   float* dal_out;                                            // [E][H] ∂α in out-CSR order
+  float* dal_in;                                             // [E][H] ∂α of hub rows in in-CSR order (P2a -> P2b)
   const float* a_src; const float* a_dst;
   float* dHp; unsigned* amax_dHp;                            // [n][HD]: ∂H′_agg (P1) -> ∂H′ (P3)
   PlanDev pin, pout;
@@ -170,8 +171,9 @@ struct G2Args {
 bool gat2_supported(const GraphDev& g, int heads, int hd);
 constexpr int gat2_nrec_stride(int heads) { return heads <= 1 ? 4 : heads <= 2 ? 8 : heads <= 4 ? 16 : 32; }
 cudaError_t launch_gat2_in2out(const int32_t* out_eid, int64_t e, int32_t* in2out, cudaStream_t st);
-cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st);
-cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st);
+struct SideStream;
+cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st, const SideStream* aux = nullptr);
+cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st, const SideStream* aux = nullptr);
 cudaError_t launch_gat2_attn_grad(const G2Args& a, cudaStream_t st);
 
 // standalone primitives (unfused; used by the primitive C-ABI entry points)

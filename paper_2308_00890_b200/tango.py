@@ -132,6 +132,7 @@ def load(path: str = LIB_PATH):
     L.tango_softmax_bwd.argtypes = [PG, i32, _P, _P, _P, f32, _P, _P, _P]
     L.tango_spmm_q.argtypes = [PG, i32, _P, PQ, i32, _P, _P, _P]
     L.tango_edge_sum.argtypes = [PG, i32, i32, _P, _P, _P]
+    L.tango_set_l2_fetch_granularity.argtypes = [i32, _P]
     L.tango_gat_ctx_bytes.restype = sz
     L.tango_gat_ctx_bytes.argtypes = [PG, C.POINTER(GatParams)]
     L.tango_gat_ctx_get_view.argtypes = [PG, C.POINTER(GatParams), _P, C.POINTER(GatCtxView)]
@@ -218,6 +219,14 @@ def profile_enable(on: bool = True):
 def profile_serialize(on: bool = True):
     """Side-stream work in order on the caller's stream (per-kernel event times without overlap)."""
     load().tango_profile_serialize(1 if on else 0)
+
+
+def set_l2_fetch_granularity(nbytes: int) -> int:
+    """cudaLimitMaxL2FetchGranularity for the current device (tango_set_l2_fetch_granularity); returns the
+    previous value."""
+    prev = C.c_int32(0)
+    _check(load().tango_set_l2_fetch_granularity(int(nbytes), C.byref(prev)), "tango_set_l2_fetch_granularity")
+    return int(prev.value)
 
 
 def launch_count() -> int:
