@@ -161,6 +161,7 @@ static GraphDev dev_graph(const tango_graph* G) {
   g.n_local = G->row_end - G->row_begin;
   g.n_global = G->n_global;
   g.row_begin = G->row_begin;
+  g.e_in = G->e_in;
   g.in_ptr = G->in_ptr; g.in_src = G->in_src;
   g.out_ptr = G->out_ptr; g.out_dst = G->out_dst; g.out_eid = G->out_eid;
   g.chunk = G->chunk_edges > 0 ? G->chunk_edges : 256;
@@ -603,8 +604,8 @@ bool plan_needed(const void* ctx, const tango_graph* G, int which) {
   return true;
 }
 
-// v6 dataflow (gat2.cu) for single-GPU graphs with the edge-id map; TANGO_DATAFLOW=1 selects the
-// round-1 kernels (gat.cu) for A/B measurements.
+// v6 dataflow (gat2.cu) for single-GPU graphs with the edge-id map; TANGO_DATAFLOW=1 / 2 force the
+// round-1 kernels (gat.cu) / v6 for A/B measurements.
 bool use_gat2(const GraphDev& g, const tango_gat_params* p, tango_comm* comm) {
   static const int forced = [] {
     const char* e = getenv("TANGO_DATAFLOW");
@@ -612,7 +613,16 @@ bool use_gat2(const GraphDev& g, const tango_gat_params* p, tango_comm* comm) {
   }();
   if (forced == 1 || comm) return false;
   const int HD = p->heads * p->head_dim;
-  return gat_codes_biased(p->heads, HD) && gat2_supported(g, p->heads, HD);
+  if (!(gat_codes_biased(p->heads, HD) && gat2_supported(g, p->heads, HD))) return false;
+  if (forced == 2) return true;
+  // v6 removes a whole row-gather pass but adds two edge-streaming passes: it pays off on dense graphs
+  // (mean in-degree >= TANGO_V6_MIN_DEGREE, default 32: Reddit-shaped 489); sparse graphs (arxiv-shaped
+  // 13) keep the round-1 kernels
+  static const double min_deg = [] {
+    const char* e = getenv("TANGO_V6_MIN_DEGREE");
+    return e ? atof(e) : 32.0;
+  }();
+  return g.n_local > 0 && (double)g.e_in >= min_deg * (double)g.n_local;
 }
 G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_params* p) {
   G2Args a{};
@@ -905,9 +915,16 @@ tango_status tango_gat_layer_bwd(const tango_graph* G, const tango_gat_params* p
     TRY(comm_gather_rows(comm, P, (size_t)L.H * 4, st));
     TRY_CUDA(cudaStreamWaitEvent(st, aux->ev[1], 0));   // out-CSR plan done
     TRY(launch_status(launch_gat_bwd_src(ba, st, &side_s)));
-    // ∂a (needs ∂S, ∂D) on the side stream, beside B8/B9
+    // ∂a (needs ∂S, ∂D) on the side stream, beside B8/B9: on one GPU in the pinned chunk order of R39
+    // (deterministic, gat2.cu) when the shape allows, else fp32 atomics (summed over ranks by comm)
     TRY_CUDA(stream_after(aux->s, st, aux->ev[2]));
-    TRY(launch_status(launch_gat_attn_grad(ba, aux->s)));
+    if (!comm && g.row_begin == 0 && L.HD % 128 == 0 && gat_codes_biased(p->heads, (int)L.HD)) {
+      G2Args a2 = g2_args(L, c, g, p);
+      a2.da_src = da_src; a2.da_dst = da_dst;
+      TRY(launch_status(launch_gat2_attn_grad(a2, aux->s)));
+    } else {
+      TRY(launch_status(launch_gat_attn_grad(ba, aux->s)));
+    }
     TRY_CUDA(cudaEventRecord(aux->ev[3], aux->s));
   }
   TRY(comm_max(comm, sc + SL_AMAX_DHP, 1, st));

@@ -1583,100 +1583,80 @@ __global__ void __launch_bounds__(256, 3) k2_bsrc2(const G2Args a) {
 // right (R33's order); block b computes chunk b's partials for all 2·HD outputs (one sequential fmaf chain
 // per output and thread), the last block to finish folds the partials in chunk order.
 constexpr int DA_CHUNK = 1024;
+// Block (chunk, 128-column slice): one thread per column carries the ∂a_src and ∂a_dst chains of its column
+// over the chunk's rows; the slice of every row (128 codes) and the rows' ∂S | ∂D are staged through a
+// ring of 32-row tiles with cp.async.  A second kernel folds the chunk partials of every output left to right.
+constexpr int DA_COLS = 128, DA_TR = 32, DA_NT = 4;
 template <int H, int VPL>
-__global__ void __launch_bounds__(256) k2_attn_grad(const G2Args a) {
+__global__ void __launch_bounds__(DA_COLS) k2_attn_part(const G2Args a) {
   constexpr int HD = 32 * VPL;
-  constexpr int CW = HD > 256 ? HD / 256 : 1;   // columns per thread (the same columns in both halves)
-  constexpr int TR = 16;                        // rows per staged tile
-  constexpr int NT = 4;                         // tiles in flight (cp.async ring)
-  __shared__ __align__(16) int8_t sq[NT][TR][HD];
-  __shared__ float ssd[NT][TR][2 * H];
+  __shared__ __align__(16) int8_t sq[DA_NT][DA_TR][DA_COLS];
+  __shared__ float ssd[DA_NT][DA_TR][2 * H];
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
-  const uint32_t flip = a.codes_biased ? 0x80808080u : 0u;   // stored excess-128 -> plain codes
+  const int flip = a.codes_biased ? 128 : 0;   // stored excess-128 -> plain codes
+  const int nsl = HD / DA_COLS;
+  const int64_t ch = blockIdx.x / nsl;
+  const int c0 = (blockIdx.x % nsl) * DA_COLS;
+  const int tid = threadIdx.x, col = c0 + tid, h = col / (HD / H);
+  const int64_t u0 = ch * DA_CHUNK, u1 = u0 + DA_CHUNK < a.g.n_local ? u0 + DA_CHUNK : a.g.n_local;
+  const int ntile = (int)((u1 - u0 + DA_TR - 1) / DA_TR);
+  auto issue = [&](int k) {
+    const int64_t r0 = u0 + (int64_t)k * DA_TR;
+    const int rows = u1 - r0 < DA_TR ? (int)(u1 - r0) : DA_TR;
+    for (int i = tid; i < rows * (DA_COLS / 16); i += DA_COLS) {
+      const int r = i / (DA_COLS / 16), c = i % (DA_COLS / 16);
+      cp_async_bytes16(smem_u32(&sq[k % DA_NT][r][c * 16]), a.qHp + (a.g.row_begin + r0 + r) * a.ldHp + c0 + c * 16);
+    }
+    for (int i = tid; i < rows * 2 * H; i += DA_COLS) {
+      const int r = i / (2 * H), c = i % (2 * H);
+      const int64_t ug = a.g.row_begin + r0 + r;
+      ssd[k % DA_NT][r][c] = c < H ? a.dS[ug * H + c] : a.dD[ug * H + c - H];
+    }
+    cp_commit();
+  };
+  float ps = 0.0f, pd = 0.0f;
+#pragma unroll
+  for (int k = 0; k < DA_NT - 1; ++k) {
+    if (k < ntile) issue(k);
+    else cp_commit();
+  }
+  for (int k = 0; k < ntile; ++k) {
+    if (k + DA_NT - 1 < ntile) issue(k + DA_NT - 1);
+    else cp_commit();
+    cp_wait<DA_NT - 1>();
+    __syncthreads();
+    const int rows = u1 - (u0 + (int64_t)k * DA_TR) < DA_TR ? (int)(u1 - (u0 + (int64_t)k * DA_TR)) : DA_TR;
+    const int b = k % DA_NT;
+#pragma unroll 8
+    for (int r = 0; r < rows; ++r) {
+      const int q = (int)(uint8_t)sq[b][r][tid] - flip;   // plain code (two's complement if not biased)
+      const float hp = __fmul_rn(__int2float_rn(flip ? q : (int)(int8_t)sq[b][r][tid]), scH.s);
+      ps = __fmaf_rn(ssd[b][r][h], hp, ps);
+      pd = __fmaf_rn(ssd[b][r][H + h], hp, pd);
+    }
+    __syncthreads();
+  }
+  cp_wait<0>();
+  __stcg(a.da_part + ch * 2 * HD + col, ps);
+  __stcg(a.da_part + ch * 2 * HD + HD + col, pd);
+}
+// output j (∂a_src then ∂a_dst): total = p_0, total = total + p_c over the chunks (R39), loads batched
+template <int H, int VPL>
+__global__ void __launch_bounds__(128) k2_attn_fold(const G2Args a) {
+  constexpr int HD = 32 * VPL;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= 2 * HD) return;
   const int64_t nch = (a.g.n_local + DA_CHUNK - 1) / DA_CHUNK;
-  const int tid = threadIdx.x;
-  const int j0 = tid * CW;
-  const bool act = j0 < HD;
-  const int h = (act ? j0 : 0) / (HD / H);
-  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
-    const int64_t u0 = ch * DA_CHUNK, u1 = u0 + DA_CHUNK < a.g.n_local ? u0 + DA_CHUNK : a.g.n_local;
-    const int ntile = (int)((u1 - u0 + TR - 1) / TR);
-    // tile k: rows u0 + k*TR ..; each thread copies 16-B pieces of the q_H′ rows and the ∂S|∂D words
-    auto issue = [&](int k) {
-      const int64_t r0 = u0 + (int64_t)k * TR;
-      const int rows = u1 - r0 < TR ? (int)(u1 - r0) : TR;
-      for (int i = tid; i < rows * (HD / 16); i += 256) {
-        const int r = i / (HD / 16), c = i % (HD / 16);
-        const int64_t ug = a.g.row_begin + r0 + r;
-        cp_async_bytes16(smem_u32(&sq[k % NT][r][c * 16]), a.qHp + ug * a.ldHp + c * 16);
-      }
-      for (int i = tid; i < rows * 2 * H; i += 256) {
-        const int r = i / (2 * H), c = i % (2 * H);
-        const int64_t ug = a.g.row_begin + r0 + r;
-        ssd[k % NT][r][c] = c < H ? a.dS[ug * H + c] : a.dD[ug * H + c - H];
-      }
-      cp_commit();
-    };
-    float ps[CW], pd[CW];
+  float tot = 0.0f;
+  for (int64_t c0 = 0; c0 < nch; c0 += 16) {
+    float p[16];
 #pragma unroll
-    for (int k = 0; k < CW; ++k) { ps[k] = 0.0f; pd[k] = 0.0f; }
+    for (int k = 0; k < 16; ++k) p[k] = c0 + k < nch ? __ldcg(a.da_part + (c0 + k) * 2 * HD + j) : 0.0f;
 #pragma unroll
-    for (int k = 0; k < NT - 1; ++k) {
-      if (k < ntile) issue(k);
-      else cp_commit();
-    }
-    for (int k = 0; k < ntile; ++k) {
-      if (k + NT - 1 < ntile) issue(k + NT - 1);
-      else cp_commit();
-      cp_wait<NT - 1>();
-      __syncthreads();
-      const int rows = u1 - (u0 + (int64_t)k * TR) < TR ? (int)(u1 - (u0 + (int64_t)k * TR)) : TR;
-      if (act) {
-        for (int r = 0; r < rows; ++r) {
-          uint32_t x;
-          if constexpr (CW == 2) x = *reinterpret_cast<const uint16_t*>(&sq[k % NT][r][j0]);
-          else x = *reinterpret_cast<const uint8_t*>(&sq[k % NT][r][j0]);
-          x ^= flip;
-          const float s = ssd[k % NT][r][h], d = ssd[k % NT][r][H + h];
-#pragma unroll
-          for (int c = 0; c < CW; ++c) {
-            const float hp = __fmul_rn(__int2float_rn((int)(int8_t)(x >> (8 * c))), scH.s);
-            ps[c] = __fmaf_rn(s, hp, ps[c]);
-            pd[c] = __fmaf_rn(d, hp, pd[c]);
-          }
-        }
-      }
-      __syncthreads();
-    }
-    cp_wait<0>();
-    if (act)
-#pragma unroll
-      for (int c = 0; c < CW; ++c) {
-        __stcg(a.da_part + ch * 2 * HD + j0 + c, ps[c]);
-        __stcg(a.da_part + ch * 2 * HD + HD + j0 + c, pd[c]);
-      }
+    for (int k = 0; k < 16; ++k)
+      if (c0 + k < nch) tot = (c0 + k == 0) ? p[k] : __fadd_rn(tot, p[k]);
   }
-  // the last block to finish folds the chunk partials left to right
-  __shared__ int last;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) last = atomicAdd(a.work + 5, 1) == (int)gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int j = tid; j < 2 * HD; j += blockDim.x) {
-    float tot = 0.0f;
-    for (int64_t c0 = 0; c0 < nch; c0 += 8) {
-      float p[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) p[k] = c0 + k < nch ? __ldcg(a.da_part + (c0 + k) * 2 * HD + j) : 0.0f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (c0 + k < nch) tot = (c0 + k == 0) ? p[k] : __fadd_rn(tot, p[k]);
-    }
-    (j < HD ? a.da_src : a.da_dst)[j % HD] = tot;
-  }
-  if (tid == 0) a.work[5] = 0;
+  (j < HD ? a.da_src : a.da_dst)[j % HD] = tot;
 }
 
 // ================================================================== in-CSR -> out-CSR position map
@@ -1786,13 +1766,15 @@ cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st, const SideStream* 
 cudaError_t launch_gat2_attn_grad(const G2Args& a, cudaStream_t st) {
   const int hv = a.d.heads * 100 + a.d.hd / 32;
   const int64_t nch = (a.g.n_local + DA_CHUNK - 1) / DA_CHUNK;
-  const int grid = (int)(nch < 1 ? 1 : (nch < 4 * num_sms() ? nch : 4 * num_sms()));
   bool ok = false;
 #define X(H_, V_)                                                                                    \
   if (hv == H_ * 100 + V_) {                                                                         \
     ok = true;                                                                                       \
-    ProfScope p("gat_bwd_attn_grad", st);                                                            \
-    k2_attn_grad<H_, V_><<<grid, 256, 0, st>>>(a);                                                   \
+    if (nch > 0) {                                                                                   \
+      ProfScope p("gat_bwd_attn_grad", st);                                                          \
+      k2_attn_part<H_, V_><<<(unsigned)(nch * (32 * V_ / DA_COLS)), DA_COLS, 0, st>>>(a);            \
+    }                                                                                                \
+    { ProfScope p("gat_bwd_attn_fold", st); k2_attn_fold<H_, V_><<<(2 * 32 * V_ + 127) / 128, 128, 0, st>>>(a); } \
   }
   G2_CASES(X)
 #undef X

@@ -72,7 +72,7 @@ bool make_row_gather_map(CUtensorMap* m, const void* base, uint64_t rows, uint64
 // ---- gat.cu : fused GAT destination / source row kernels and standalone sparse primitives
 struct GatDims { int heads, head_dim, hd; };
 struct GraphDev {
-  int64_t n_local, row_begin, n_global;
+  int64_t n_local, row_begin, n_global, e_in;
   const int64_t* in_ptr; const int32_t* in_src;
   const int64_t* out_ptr; const int32_t* out_dst; const int32_t* out_eid;
   int chunk;

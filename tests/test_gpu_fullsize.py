@@ -77,7 +77,7 @@ def test_gat_layer_arxiv_full_size(T, orc):
     eq("qdHp", bv["qdHp"], b["qdHp"])
     eq("dH", dX, b["dH"])
     eq("dW", dW, b["dW"])
-    if bv["dataflow"] == 2:   # deterministic chunk order (reading R39): bit-exact
+    if True:   # one GPU, HD = 512: the pinned chunk order of R39 on either dataflow, bit-exact
         eq("da_src", das, b["da_src"])
         eq("da_dst", dad, b["da_dst"])
     else:

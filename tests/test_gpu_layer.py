@@ -125,7 +125,7 @@ def _gat_parity(T, orc, case, keep_eid):
     eq("qdHp", bv["qdHp"], b["qdHp"])
     eq("dH", dHg, b["dH"])
     eq("dW", dWg, b["dW"])
-    if bv["dataflow"] == 2:   # deterministic chunk order (reading R39): bit-exact
+    if bv["dataflow"] == 2 or HD % 128 == 0:   # one GPU: the pinned chunk order of R39, bit-exact
         eq("da_src", das, b["da_src"])
         eq("da_dst", dad, b["da_dst"])
     else:
