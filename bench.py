@@ -502,9 +502,9 @@ def measure_layer(T, torch, dist, wname, args, rank, world, local_rank, peaks, p
     if world > 1:
         uid = [T.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        comm = T.Comm(world, rank, uid[0], starts)
+        comm = T.Comm(world, rank, uid[0], starts, reserve_row_bytes=(HD + 31) // 32 * 32)
     elif args.nccl_single:    # the N > 1 code path (NCCL collectives, partition plumbing) on one rank
-        comm = T.Comm(1, 0, T.Comm.unique_id(), starts)
+        comm = T.Comm(1, 0, T.Comm.unique_id(), starts, always=True, reserve_row_bytes=(HD + 31) // 32 * 32)
     dg = T.DeviceGraph(g, row_begin=r0, row_end=r1)
     W, a_s, a_d = inputs.gat_params(F, H, D)
     Hx = inputs.features(g.n, F)[r0:r1]

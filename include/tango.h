@@ -436,6 +436,16 @@ tango_status tango_comm_init_local(struct tango_comm** out, struct tango_local_g
 /* Row partition of the node set: rank r owns [row_starts[r], row_starts[r+1]).
  * Must be called (identically on every rank) before a layer call with this comm. */
 tango_status tango_comm_set_partition(struct tango_comm* comm, const int64_t* row_starts /* nranks+1, host */);
+/* always != 0: a one-rank NCCL communicator still enqueues every collective (identities on one rank),
+ * so the NCCL data plane executes on one GPU exactly as with N ranks (tests, bench --nccl-single). */
+tango_status tango_comm_set_options(struct tango_comm* comm, int32_t always);
+/* Allocates (outside any graph capture) the staging buffer of the padded all-gather: nranks x largest
+ * row block x max_row_bytes device bytes, owned by the comm and freed by tango_comm_destroy.  Without
+ * it, node-row all-gathers run as grouped in-place broadcasts.  Call after tango_comm_set_partition. */
+tango_status tango_comm_reserve(struct tango_comm* comm, size_t max_row_bytes);
+/* Number of NCCL collectives this comm has enqueued (an all-gather counts once, a broadcast group once
+ * per broadcast); -1 for NULL. */
+int64_t tango_comm_nccl_calls(const struct tango_comm* comm);
 
 /* ------------------------------------------------------------------------- */
 /* Tracing: every kernel launch increments a counter; with profiling enabled  */

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+#include <algorithm>
 #include <mutex>
 #include <condition_variable>
 #include <atomic>
@@ -78,6 +79,11 @@ struct tango_comm {
   tango_local_group* local = nullptr;
   int nranks = 1, rank = 0;
   std::vector<int64_t> starts;  // nranks + 1
+  int64_t max_rows = 0;         // largest row block
+  bool always = false;          // run the NCCL collectives even with one rank (tango_comm_set_options)
+  void* stage = nullptr;        // padded all-gather staging, nranks x max_rows x stage_row_bytes (tango_comm_reserve)
+  size_t stage_row_bytes = 0;
+  int64_t nccl_calls = 0;       // collectives enqueued (tango_comm_nccl_calls)
 };
 
 #define TRY_CUDA(x)                                  \
@@ -288,28 +294,38 @@ static tango_status local_reduce(tango_comm* c, void* buf, size_t count, size_t 
 }
 
 // ------------------------------------------------------------------ collectives (caller stream)
+// A one-rank communicator skips its collectives (identities) unless set to `always` (tests / bench
+// --nccl-single: the NCCL calls then execute on the device with the same arguments as with N ranks).
+static bool comm_skip(const tango_comm* c, size_t count) {
+  return !c || count == 0 || (c->nranks == 1 && !(c->always && c->nccl));
+}
 static tango_status comm_max(tango_comm* c, void* buf, size_t count, cudaStream_t st) {
-  if (!c || c->nranks == 1 || count == 0) return TANGO_OK;
+  if (comm_skip(c, count)) return TANGO_OK;
   if (c->local) return local_reduce(c, buf, count, 4, 0, st);
   TRY_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclMax, c->nccl, st));
+  ++c->nccl_calls;
   return TANGO_OK;
 }
 static tango_status comm_sum_f32(tango_comm* c, float* buf, size_t count, cudaStream_t st) {
-  if (!c || c->nranks == 1 || count == 0) return TANGO_OK;
+  if (comm_skip(c, count)) return TANGO_OK;
   if (c->local) return local_reduce(c, buf, count, 4, 1, st);
   TRY_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, c->nccl, st));
+  ++c->nccl_calls;
   return TANGO_OK;
 }
 static tango_status comm_sum_i64(tango_comm* c, int64_t* buf, size_t count, cudaStream_t st) {
-  if (!c || c->nranks == 1 || count == 0) return TANGO_OK;
+  if (comm_skip(c, count)) return TANGO_OK;
   if (c->local) return local_reduce(c, buf, count, 8, 1, st);
   TRY_NCCL(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, c->nccl, st));
+  ++c->nccl_calls;
   return TANGO_OK;
 }
-// All-gather of node-row blocks of `row_bytes` bytes: rank r's block [starts[r], starts[r+1]) is
-// broadcast in place to every rank (grouped broadcasts: partitions have different sizes).
+// All-gather of node-row blocks of `row_bytes` bytes (rank r owns rows [starts[r], starts[r+1])).  With a
+// reserved staging buffer: one padded ncclAllGather (every block padded to max_rows rows; own block
+// copied into its staging slot, in-place all-gather, the other blocks copied into place).  Without one:
+// grouped in-place broadcasts of the blocks.
 static tango_status comm_gather_rows(tango_comm* c, void* base, size_t row_bytes, cudaStream_t st) {
-  if (!c || c->nranks == 1) return TANGO_OK;
+  if (comm_skip(c, 1)) return TANGO_OK;
   if (c->local) {
     TRY(local_begin(c, base, st));
     for (int k = 0; k < c->nranks; ++k) {
@@ -321,6 +337,22 @@ static tango_status comm_gather_rows(tango_comm* c, void* base, size_t row_bytes
     }
     return local_end(c, st);
   }
+  if (c->stage && row_bytes <= c->stage_row_bytes && c->max_rows > 0) {
+    const size_t slot = (size_t)c->max_rows * row_bytes;
+    char* stg = static_cast<char*>(c->stage);
+    char* b = static_cast<char*>(base);
+    const size_t own = (size_t)(c->starts[c->rank + 1] - c->starts[c->rank]) * row_bytes;
+    if (own) TRY_CUDA(cudaMemcpyAsync(stg + c->rank * slot, b + (size_t)c->starts[c->rank] * row_bytes, own,
+                                      cudaMemcpyDeviceToDevice, st));
+    TRY_NCCL(ncclAllGather(stg + c->rank * slot, stg, slot, ncclInt8, c->nccl, st));
+    ++c->nccl_calls;
+    for (int r = 0; r < c->nranks; ++r) {
+      const size_t cnt = (size_t)(c->starts[r + 1] - c->starts[r]) * row_bytes;
+      if (r == c->rank || cnt == 0) continue;
+      TRY_CUDA(cudaMemcpyAsync(b + (size_t)c->starts[r] * row_bytes, stg + r * slot, cnt, cudaMemcpyDeviceToDevice, st));
+    }
+    return TANGO_OK;
+  }
   TRY_NCCL(ncclGroupStart());
   for (int r = 0; r < c->nranks; ++r) {
     const size_t off = (size_t)c->starts[r] * row_bytes;
@@ -328,6 +360,7 @@ static tango_status comm_gather_rows(tango_comm* c, void* base, size_t row_bytes
     if (cnt == 0) continue;
     char* p = static_cast<char*>(base) + off;
     TRY_NCCL(ncclBroadcast(p, p, cnt, ncclInt8, r, c->nccl, st));
+    ++c->nccl_calls;
   }
   TRY_NCCL(ncclGroupEnd());
   return TANGO_OK;
@@ -1216,14 +1249,39 @@ tango_status tango_comm_init(tango_comm** out, const void* unique_id, int32_t nr
 tango_status tango_comm_set_partition(tango_comm* c, const int64_t* row_starts) {
   if (!c || !row_starts) return TANGO_ERR_INVALID_ARG;
   c->starts.assign(row_starts, row_starts + c->nranks + 1);
-  for (int r = 0; r < c->nranks; ++r)
+  c->max_rows = 0;
+  for (int r = 0; r < c->nranks; ++r) {
     if (c->starts[r] > c->starts[r + 1]) return TANGO_ERR_SHAPE;
+    c->max_rows = std::max<int64_t>(c->max_rows, c->starts[r + 1] - c->starts[r]);
+  }
   return TANGO_OK;
 }
+
+tango_status tango_comm_set_options(tango_comm* c, int32_t always) {
+  if (!c) return TANGO_ERR_INVALID_ARG;
+  c->always = always != 0;
+  return TANGO_OK;
+}
+
+tango_status tango_comm_reserve(tango_comm* c, size_t max_row_bytes) {
+  if (!c || c->starts.empty()) return TANGO_ERR_INVALID_ARG;
+  if (c->local || max_row_bytes <= c->stage_row_bytes) return TANGO_OK;
+  if (c->stage) TRY_CUDA(cudaFree(c->stage));
+  c->stage = nullptr;
+  c->stage_row_bytes = 0;
+  const size_t bytes = (size_t)c->nranks * (size_t)c->max_rows * max_row_bytes;
+  if (bytes == 0) return TANGO_OK;
+  TRY_CUDA(cudaMalloc(&c->stage, bytes));
+  c->stage_row_bytes = max_row_bytes;
+  return TANGO_OK;
+}
+
+int64_t tango_comm_nccl_calls(const tango_comm* c) { return c ? c->nccl_calls : -1; }
 
 tango_status tango_comm_destroy(tango_comm* c) {
   if (!c) return TANGO_ERR_INVALID_ARG;
   if (c->nccl) ncclCommDestroy(c->nccl);
+  if (c->stage) cudaFree(c->stage);
   delete c;
   return TANGO_OK;
 }

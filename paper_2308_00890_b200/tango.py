@@ -108,7 +108,8 @@ EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tan
            "tango_bias_act_fwd", "tango_bias_act_bwd", "tango_cross_entropy", "tango_sgd_update",
            "tango_gat_out_ctx_bytes", "tango_gat_out_fwd", "tango_gat_out_bwd", "tango_gat_out_ctx_get_view",
            "tango_gcn_out_ctx_bytes", "tango_gcn_out_fwd", "tango_gcn_out_bwd", "tango_gcn_out_ctx_get_view",
-           "tango_quantize_int4", "tango_sddmm_qn"]
+           "tango_quantize_int4", "tango_sddmm_qn", "tango_set_l2_fetch_granularity", "tango_comm_set_options",
+           "tango_comm_reserve", "tango_comm_nccl_calls"]
 
 
 def load(path: str = LIB_PATH):
@@ -133,6 +134,10 @@ def load(path: str = LIB_PATH):
     L.tango_spmm_q.argtypes = [PG, i32, _P, PQ, i32, _P, _P, _P]
     L.tango_edge_sum.argtypes = [PG, i32, i32, _P, _P, _P]
     L.tango_set_l2_fetch_granularity.argtypes = [i32, _P]
+    L.tango_comm_set_options.argtypes = [_P, i32]
+    L.tango_comm_reserve.argtypes = [_P, sz]
+    L.tango_comm_nccl_calls.argtypes = [_P]
+    L.tango_comm_nccl_calls.restype = C.c_int64
     L.tango_gat_ctx_bytes.restype = sz
     L.tango_gat_ctx_bytes.argtypes = [PG, C.POINTER(GatParams)]
     L.tango_gat_ctx_get_view.argtypes = [PG, C.POINTER(GatParams), _P, C.POINTER(GatCtxView)]
@@ -386,13 +391,24 @@ class Comm:
     """NCCL communicator (tango_comm) for destination-row partitioning; the unique id is
     broadcast by the caller (torch.distributed)."""
 
-    def __init__(self, nranks, rank, unique_id: bytes, row_starts):
+    def __init__(self, nranks, rank, unique_id: bytes, row_starts, always=False, reserve_row_bytes=0):
         L = load()
         self.handle = C.c_void_p()
         buf = C.create_string_buffer(unique_id, len(unique_id))
         _check(L.tango_comm_init(C.byref(self.handle), buf, nranks, rank), "tango_comm_init")
         starts = np.ascontiguousarray(row_starts, dtype=np.int64)
         _check(L.tango_comm_set_partition(self.handle, starts.ctypes.data), "tango_comm_set_partition")
+        if always:
+            _check(L.tango_comm_set_options(self.handle, 1), "tango_comm_set_options")
+        if reserve_row_bytes:
+            self.reserve(reserve_row_bytes)
+
+    def reserve(self, max_row_bytes: int):
+        """Staging of the padded ncclAllGather for node rows of up to max_row_bytes bytes."""
+        _check(load().tango_comm_reserve(self.handle, int(max_row_bytes)), "tango_comm_reserve")
+
+    def nccl_calls(self) -> int:
+        return int(load().tango_comm_nccl_calls(self.handle))
 
     @classmethod
     def local(cls, group: "LocalGroup", rank, row_starts):

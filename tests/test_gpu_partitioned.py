@@ -136,11 +136,14 @@ def test_gcn_partitioned_local_comm(T, orc, P):
         assert np.array_equal(res[r][2], b["dW"]), r
 
 
-def test_nccl_single_rank_comm(T, orc):
-    """The NCCL transport itself (tango_comm_init over a real ncclComm, nranks = 1): every collective of
-    the GAT and GCN layers goes through NCCL on the caller's stream; the results must equal the
-    oracle bit for bit (∂a within the bound).  gpurun provides one GPU, so this is the NCCL path's
-    only on-device check; the multi-rank dataflow is covered by the loopback and gloo tests."""
+@pytest.mark.parametrize("staged", [True, False], ids=["padded_allgather", "grouped_broadcast"])
+def test_nccl_single_rank_comm(T, orc, staged):
+    """The NCCL transport itself (tango_comm_init over a real ncclComm, nranks = 1, set to always run its
+    collectives): every collective of the GAT and GCN layers is enqueued through NCCL on the caller's
+    stream (counted by tango_comm_nccl_calls), node-row all-gathers as one padded ncclAllGather through
+    the reserved staging buffer or as grouped broadcasts; the results must equal the oracle bit for bit
+    (∂a within the bound).  gpurun provides one GPU, so this is the NCCL path's only on-device check; the
+    multi-rank dataflow is covered by the loopback and gloo tests."""
     from test_gpu_layer import da_ok, eq
     gr = inputs.random_graph(1200, 6000, seed=31)
     F, heads, hd = 64, 4, 32
@@ -148,7 +151,7 @@ def test_nccl_single_rank_comm(T, orc):
     W, a_s, a_d = inputs.gat_params(F, heads, hd, seed=33)
     dY = inputs.grad_out(gr.n, heads * hd, seed=34)
     cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    comm = T.Comm(1, 0, T.Comm.unique_id(), [0, gr.n])
+    comm = T.Comm(1, 0, T.Comm.unique_id(), [0, gr.n], always=True, reserve_row_bytes=512 if staged else 0)
     try:
         dg = T.DeviceGraph(gr, chunk=16, row_begin=0, row_end=gr.n)
         layer = T.GATLayer(dg, cu(W), cu(a_s), cu(a_d), heads, hd, slope=0.2, bits=8, comm=comm)
@@ -160,8 +163,12 @@ def test_nccl_single_rank_comm(T, orc):
         gdX, gdW = gl.backward(cu(dY[:, :48]), step=3, layer_id=2)
         torch.cuda.synchronize()
         layer.check_status()
+        calls = comm.nccl_calls()
     finally:
         comm.close()
+    # GAT fwd: amax(H), {amax H', S, D}, q_H', q_S, q_D, amax(out), m, den; bwd: amax(dH_out), q_G, P,
+    # amax(dH'), dW, da_src, da_dst (+ amax(dH)); GCN adds its own: all of them must have executed
+    assert calls >= 20, calls
     f = orc.gat_fwd(gr, X, W, a_s, a_d, heads, hd, slope=0.2, bits=8, step=3, layer_id=1, chunk=16)
     b = orc.gat_bwd(gr, f, X, W, a_s, a_d, dY)
     eq("H_out", Hout, f["Hout"])
