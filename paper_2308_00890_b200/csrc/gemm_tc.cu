@@ -28,7 +28,8 @@ constexpr int B_BYTES_MAX = 256 * BKB;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES_MAX;
 constexpr int EPI_WARPS = 8;       // two per TMEM sub-partition, each owning a column group of the N tile
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4096 + 1024;
+constexpr int TR_LD = 17;          // EPI_STORE transpose tile: 32 rows x 16 columns (+1 pad) per epilogue warp
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4096 + 1024 + EPI_WARPS * 32 * TR_LD * 4 + 1024;   // + alignment slack
 
 struct KParams {
   int64_t M, N, K;
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* sm_asrc = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024);
   float* sm_adst = sm_asrc + 256;
+  float* sm_tr = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 4096 + 1024);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -268,24 +270,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
           }
         } else if constexpr (MODE == EPI_STORE) {
+          // lane = row: transpose the 32 x 32 chunk through shared memory in two 16-column halves so that
+          // every store instruction writes two rows' 16 consecutive columns (64 contiguous bytes per row,
+          // whole sectors) instead of one 16-B piece of 32 different rows; any ldc / C alignment works
           float* Cf = reinterpret_cast<float*>(p.C);
-          if (row_ok) {
-            if (full_chunk && ((p.ldc & 3) == 0)) {
-              float4* dst = reinterpret_cast<float4*>(Cf + row * p.ldc + col0);
+          float* tr = sm_tr + ew * (32 * TR_LD);
+          const int64_t rowbase = (int64_t)mt * BM + sub * 32;
+          const int cl = lane & 15, rh = lane >> 4;
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                dst[i] = make_float4(deq(r[4 * i], sAB, has_rs, rs), deq(r[4 * i + 1], sAB, has_rs, rs),
-                                     deq(r[4 * i + 2], sAB, has_rs, rs), deq(r[4 * i + 3], sAB, has_rs, rs));
-            } else if (full_chunk && ((p.ldc & 1) == 0)) {   // 8-B aligned rows (e.g. F = 602)
-              float2* dst = reinterpret_cast<float2*>(Cf + row * p.ldc + col0);
+          for (int hf = 0; hf < 2; ++hf) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i)
-                dst[i] = make_float2(deq(r[2 * i], sAB, has_rs, rs), deq(r[2 * i + 1], sAB, has_rs, rs));
-            } else {   // unrolled with a predicate: r[] stays in registers
+            for (int i = 0; i < 16; ++i) tr[lane * TR_LD + i] = deq(r[hf * 16 + i], sAB, has_rs, rs);
+            __syncwarp();
+            const int64_t col = col0 + hf * 16 + cl;
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (col0 + i < p.N) Cf[row * p.ldc + col0 + i] = deq(r[i], sAB, has_rs, rs);
+            for (int j = 0; j < 32; j += 2) {
+              const int64_t rr = rowbase + j + rh;
+              if (rr < p.M && col < p.N) Cf[rr * p.ldc + col] = tr[(j + rh) * TR_LD + cl];
             }
+            __syncwarp();
           }
         } else if constexpr (MODE == EPI_I32) {
           int32_t* Ci = reinterpret_cast<int32_t*>(p.C);
