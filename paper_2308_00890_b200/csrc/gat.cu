@@ -247,35 +247,6 @@ __device__ __forceinline__ float bx2f(uint32_t wx, int k) {
   return __fsub_rn(__uint_as_float(__byte_perm(wx, 0x4B000000u, 0x7440u | (uint32_t)k)), 8388736.0f);
 }
 
-// part[k] += α[e] * q_X[w_e][lane*VPL + k] over the segment's 32-edge batch (α staged in abuf[i][myh]),
-// rows gathered 8 deep.  `idx` holds the other endpoint of edge (base + lane).
-template <int VPL>
-__device__ __forceinline__ void gather_fma_batch(const int8_t* __restrict__ xbase, int64_t ldx, int idx, int cnt,
-                                                 const float* __restrict__ acol /* &abuf[0][myh] */, int astride,
-                                                 float (&part)[VPL]) {
-  for (int i0 = 0; i0 < cnt; i0 += UNR) {
-    Row<VPL> r[UNR];
-#pragma unroll
-    for (int j = 0; j < UNR; ++j) {
-      const int w = __shfl_sync(0xffffffffu, idx, (i0 + j) & 31);
-      if (i0 + j < cnt) r[j] = load_row<VPL>(xbase + (int64_t)w * ldx);
-    }
-#pragma unroll
-    for (int j = 0; j < UNR; ++j) {
-      if (i0 + j < cnt) {
-        const float al = acol[(i0 + j) * astride];
-#pragma unroll
-        for (int q = 0; q < (VPL + 3) / 4; ++q) {
-          const uint32_t wx = r[j].w[q] ^ 0x80808080u;
-#pragma unroll
-          for (int k = 0; k < 4 && q * 4 + k < VPL; ++k) part[q * 4 + k] = __fmaf_rn(al, bx2f(wx, k), part[q * 4 + k]);
-        }
-      }
-    }
-  }
-}
-
-
 // ================================================================== forward
 
 // FS (tiles): heavy segments -> segment max (hmax); light sub-tiles -> m, den and α for every edge.
@@ -558,174 +529,7 @@ struct CGCfg {
   static constexpr int UNRC = WORDS == 1 ? 16 : (WORDS == 2 ? 8 : 4);
 };
 
-// fwd: α for the group's heads of one edge batch; lane l holds the edge's source u
-template <int HPW>
-__device__ __forceinline__ void cg_alpha_fwd(const GatFwdArgs& a, int H, int h0, int u, const int (&qdr)[HPW],
-                                             const float (&mr)[HPW], const float (&dr)[HPW], float sS, float sD,
-                                             float (*buf)[HPW]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < HPW; ++k)
-    buf[lane][k] = __fdiv_rn(
-        exp_p(__fsub_rn(lrelu(sddmm_add1(a.qS[(int64_t)u * H + h0 + k], sS, (int8_t)qdr[k], sD), a.slope), mr[k])),
-        dr[k]);
-}
-
-// part += α(edge i) * q_X[w_i][cols of this lane] over a staged batch, 16-deep gather pipeline.
-// If rb != nullptr, rows change inside the batch: `on_row(ri)` is called before the first edge of a row.
-template <int VPL, int HPW, typename F>
-__device__ __forceinline__ void cg_gather_fma(const int8_t* __restrict__ xbase, int64_t ldx, int idx, int cnt,
-                                              float (*buf)[HPW], const int* rb, int& cur, float (&part)[VPL],
-                                              F&& on_row) {
-  constexpr int UNRC = CGCfg<VPL>::UNRC;
-  const int lh = (threadIdx.x & 31) / (32 / HPW);
-  for (int i0 = 0; i0 < cnt; i0 += UNRC) {
-    Row<VPL> rr[UNRC];
-#pragma unroll
-    for (int j = 0; j < UNRC; ++j) {
-      const int wv = __shfl_sync(0xffffffffu, idx, (i0 + j) & 31);
-      if (i0 + j < cnt) rr[j] = load_row<VPL>(xbase + (int64_t)wv * ldx);
-    }
-#pragma unroll
-    for (int j = 0; j < UNRC; ++j) {
-      if (i0 + j < cnt) {
-        if (rb) {
-          const int ri = rb[i0 + j];
-          if (ri != cur) { on_row(ri); cur = ri; }
-        }
-        const float al = buf[i0 + j][lh];
-#pragma unroll
-        for (int q = 0; q < CGCfg<VPL>::WORDS; ++q) {
-          const uint32_t wx = rr[j].w[q] ^ 0x80808080u;
-#pragma unroll
-          for (int k = 0; k < 4 && q * 4 + k < VPL; ++k) part[q * 4 + k] = __fmaf_rn(al, bx2f(wx, k), part[q * 4 + k]);
-        }
-      }
-    }
-  }
-}
-
 // ---- FA: aggregation ⑤ per (tile | heavy segment, head group)
-template <int VPL, int HPW>
-__global__ void __launch_bounds__(256) k_fwd_agg_cg(const GatFwdArgs a) {
-  constexpr int WC = 32 * VPL;
-  __shared__ float sh_a[WPB][32][HPW];
-  __shared__ int sh_rb[WPB][32];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int H = a.d.heads, HD = a.d.hd, NG = HD / WC;
-  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
-  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
-  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
-  const int64_t n = a.g.n_local, hc = load_count(a.plan.counts);
-  const int64_t nitems = (hc + (n + TILE - 1) / TILE) * NG;
-  float amax_loc = 0.0f;
-  FOR_ITEMS(item, a.work + 2, nitems) {
-    const int64_t wi = item / NG;
-    const int g = (int)(item - wi * NG), h0 = g * HPW;
-    const int8_t* xbase = a.qHp + g * WC + lane * VPL;
-    float part[VPL];
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) part[k] = 0.0f;
-    if (wi < hc) {   // ----------------------------------------------- heavy segment
-      Seg s;
-      decode_item(wi, hc, a.g.in_ptr, a.plan, a.g.chunk, s);
-      const int64_t vg = a.g.row_begin + s.vl;
-      float mr[HPW], dr[HPW];
-      int qdr[HPW];
-#pragma unroll
-      for (int k = 0; k < HPW; ++k) {
-        float mx = -INFINITY;
-        for (int j = lane; j < s.nseg; j += 32) mx = fmaxf(mx, a.hmax[(int64_t)(s.base + j) * H + h0 + k]);
-        mr[k] = warp_max(mx);
-        float tot = 0.0f;
-        if (lane == 0) {
-          tot = a.hden[(int64_t)s.base * H + h0 + k];
-          for (int j = 1; j < s.nseg; ++j) tot = __fadd_rn(tot, a.hden[(int64_t)(s.base + j) * H + h0 + k]);
-        }
-        dr[k] = __shfl_sync(0xffffffffu, tot, 0);
-        qdr[k] = (int)a.qD[vg * H + h0 + k];
-      }
-      int cur = 0;
-      for (int64_t base = s.eb; base < s.ee; base += 32) {
-        const int cnt = (int)(s.ee - base < 32 ? s.ee - base : 32);
-        int u = 0;
-        if (lane < cnt) {
-          u = a.g.in_src[base + lane];
-          cg_alpha_fwd<HPW>(a, H, h0, u, qdr, mr, dr, scS.s, scD.s, sh_a[w]);
-        }
-        __syncwarp();
-        cg_gather_fma<VPL, HPW>(xbase, a.ldHp, u, cnt, sh_a[w], nullptr, cur, part, [](int) {});
-        __syncwarp();
-      }
-      float* dst = a.hagg + (int64_t)s.slot * HD + g * WC + lane * VPL;
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) dst[k] = part[k];
-      continue;
-    }
-    // ------------------------------------------------------------- tile of light rows
-    const int64_t r0 = (wi - hc) * TILE;
-    int T;
-    const TileLane L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, n, T);
-    const int64_t vg = a.g.row_begin + L.r;
-    float mj[HPW], dj[HPW];
-    int qdj[HPW];
-#pragma unroll
-    for (int k = 0; k < HPW; ++k) {
-      mj[k] = L.deg > 0 ? a.m[vg * H + h0 + k] : 0.0f;
-      dj[k] = L.deg > 0 ? a.den[vg * H + h0 + k] : 0.0f;
-      qdj[k] = L.deg > 0 ? (int)a.qD[vg * H + h0 + k] : 0;
-    }
-    unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
-    while (zm) {   // light rows without in-edges: H_out = 0
-      const int j = __ffs(zm) - 1;
-      zm &= zm - 1;
-      float* dst = a.Hout + (r0 + j) * HD + g * WC + lane * VPL;
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) dst[k] = 0.0f;
-    }
-    int cur = -1;
-    auto flush = [&](int j) {
-      float* dst = a.Hout + (r0 + j) * HD + g * WC + lane * VPL;
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) {
-        const float o = __fmul_rn(part[k], scH.s);
-        amax_loc = fmaxf(amax_loc, fabsf(o));
-        dst[k] = o;
-        part[k] = 0.0f;
-      }
-    };
-    for (int base = 0; base < T; base += 32) {
-      const int cnt = T - base < 32 ? T - base : 32;
-      const int t = base + lane;
-      const int row = tile_row(t, L.end);
-      const int64_t ebr = __shfl_sync(0xffffffffu, L.eb, row);
-      const int offr = __shfl_sync(0xffffffffu, L.off, row);
-      float mr[HPW], dr[HPW];
-      int qdr[HPW];
-#pragma unroll
-      for (int k = 0; k < HPW; ++k) {
-        mr[k] = __shfl_sync(0xffffffffu, mj[k], row);
-        dr[k] = __shfl_sync(0xffffffffu, dj[k], row);
-        qdr[k] = __shfl_sync(0xffffffffu, qdj[k], row);
-      }
-      int u = 0;
-      if (lane < cnt) {
-        u = a.g.in_src[ebr + (t - offr)];
-        cg_alpha_fwd<HPW>(a, H, h0, u, qdr, mr, dr, scS.s, scD.s, sh_a[w]);
-        sh_rb[w][lane] = row;
-      }
-      __syncwarp();
-      cg_gather_fma<VPL, HPW>(xbase, a.ldHp, u, cnt, sh_a[w], sh_rb[w], cur, part, [&](int ri) {
-        if (cur >= 0) flush(cur);
-      });
-      __syncwarp();
-    }
-    if (cur >= 0) flush(cur);
-  }
-  amax_flush(a.amax_out, amax_loc);
-}
-
-
 // Streamed aggregation of one 32-edge chunk: rows q_X[w_i] gathered through a rolling ring of RING
 // loads in flight; edge i of the chunk uses weight sa[i][myh] and (if rb) belongs to row rb[i].
 template <int H, int VPL, int RING, typename F>
@@ -863,162 +667,8 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg2(const GatFwdArgs a) {
 }
 
 
-template <int H, int VPL>
-__host__ __device__ constexpr int agg3_warp_smem() { return AGG_RING * 32 * VPL + 2 * 32 * H * 4 + 2 * 32 * 4; }
 
 // FA (VPL >= 4): ⑤ H_out = (Σ fmaf(α, q_H′[u])) * s_H′ over (heavy segment | light sub-tile)
-template <int H, int VPL>
-__global__ void __launch_bounds__(256, 3) k_fwd_agg3(const GatFwdArgs a) {
-  constexpr int HD = 32 * VPL, R = AGG_RING, RB = 32 * VPL;
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int myh = lane / (32 / H);
-  uint8_t* wsm = dsm + w * agg3_warp_smem<H, VPL>();
-  float (*sa)[32][H] = reinterpret_cast<float (*)[32][H]>(wsm + R * RB);
-  int (*srb)[32] = reinterpret_cast<int (*)[32]>(wsm + R * RB + 2 * 32 * H * 4);
-  const uint32_t ring_s = smem_u32(wsm) + lane * VPL;
-  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
-  const int64_t n = a.g.n_local, hc = load_count(a.plan.counts);
-  const int64_t nitems = hc + load_count(a.plan.counts + 2);
-  const int8_t* xbase = a.qHp + lane * VPL;
-  const uint32_t ld32 = (uint32_t)a.ldHp;
-  float amax_loc = 0.0f;
-  FOR_ITEMS(item, a.work + 2, nitems) {
-    // ---- stream set-up: a heavy segment (one row) or a light sub-tile (rows change)
-    const bool tile = item >= hc;
-    Seg s;
-    TileLane L;
-    int64_t r0 = 0;
-    int T;
-    if (!tile) {
-      decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s);
-      T = (int)(s.ee - s.eb);
-      L.eb = 0; L.off = 0; L.end = 0;
-    } else {
-      const int32_t code = a.plan.tiles[item - hc];
-      r0 = (int64_t)(code >> 10) * TILE;
-      L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
-      unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
-      while (zm) {   // light rows without in-edges: H_out = 0
-        const int j = __ffs(zm) - 1;
-        zm &= zm - 1;
-        float* dst = a.Hout + (r0 + j) * HD + lane * VPL;
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) __stcs(dst + k, 0.0f);
-      }
-    }
-    auto attrs = [&](int c, int& u, float (&al)[H], int& row) {
-      const int t = c * 32 + lane;
-      int64_t e;
-      if (tile) {
-        row = tile_row(t, L.end);
-        e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
-      } else {
-        row = 0;
-        e = s.eb + t;
-      }
-      u = 0;
-#pragma unroll
-      for (int h = 0; h < H; ++h) al[h] = 0.0f;
-      if (t < T) {
-        u = a.g.in_src[e];
-        if constexpr (H == 4) {
-          const float4 v = *reinterpret_cast<const float4*>(a.alpha + e * 8);
-          al[0] = fabsf(v.x); al[1] = fabsf(v.y); al[2] = fabsf(v.z); al[3] = fabsf(v.w);
-        } else {
-#pragma unroll
-          for (int h = 0; h < H; ++h) al[h] = fabsf(a.alpha[e * 2 * H + h]);
-        }
-      }
-    };
-    int uA, rowA;
-    float alA[H];
-    attrs(0, uA, alA, rowA);
-#pragma unroll
-    for (int h = 0; h < H; ++h) sa[0][lane][h] = alA[h];
-    srb[0][lane] = rowA;
-#pragma unroll
-    for (int j = 0; j < R; ++j) {   // ring prologue: edges 0 .. R-1, one commit group per 4 edges
-      const int uu = __shfl_sync(0xffffffffu, uA, j);
-      if (j < T) cp_row_slice<VPL>(ring_s + j * RB, xbase + (uint32_t)uu * ld32);
-      if ((j & 3) == 3) cp_commit();
-    }
-    float2 acc[VPL / 2];
-#pragma unroll
-    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
-    int cur = -1;
-    auto flush = [&](int j) {
-      float* dst = a.Hout + (r0 + j) * HD + lane * VPL;
-#pragma unroll
-      for (int k = 0; k < VPL / 2; ++k) {
-        const float x = __fmul_rn(acc[k].x, scH.s), y = __fmul_rn(acc[k].y, scH.s);
-        amax_loc = fmaxf(amax_loc, fmaxf(fabsf(x), fabsf(y)));
-        __stcs(dst + 2 * k, x);
-        __stcs(dst + 2 * k + 1, y);
-        acc[k] = make_float2(0.0f, 0.0f);
-      }
-    };
-    const int nch = (T + 31) >> 5;
-    for (int c = 0; c < nch; ++c) {
-      int uB, rowB;
-      float alB[H];
-      attrs(c + 1, uB, alB, rowB);   // next chunk, in flight while this chunk streams
-      __syncwarp();
-      const int cb = c & 1;
-      for (int i0 = 0; i0 < 32; i0 += 4) {
-        const int t0 = c * 32 + i0;
-        if (t0 >= T) break;
-        cp_wait<R / 4 - 1>();        // the 4 rows of this group have landed
-        const uint32_t slot0 = ring_s + (uint32_t)(t0 & (R - 1)) * RB;
-        Row<VPL> r[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) r[j] = lds_row_slice<VPL>(slot0 + j * RB);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (t0 + j < T) {
-            if (tile) {
-              const int ri = srb[cb][i0 + j];
-              if (ri != cur) {
-                if (cur >= 0) flush(cur);
-                cur = ri;
-              }
-            }
-            const float al = sa[cb][i0 + j][myh];
-            const float2 al2 = make_float2(al, al);
-#pragma unroll
-            for (int q = 0; q < VPL / 4; ++q) fma4_codes(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {   // refill the 4 consumed slots with edges t0+R .. t0+R+3
-          const int tn = t0 + R + j;
-          const int ua = __shfl_sync(0xffffffffu, uA, tn & 31);
-          const int ub = __shfl_sync(0xffffffffu, uB, tn & 31);
-          const uint32_t un = (uint32_t)(tn < (c + 1) * 32 ? ua : ub);
-          if (tn < T) cp_row_slice<VPL>(slot0 + j * RB, xbase + un * ld32);   // 32-bit offset (N*ld < 2^32)
-        }
-        cp_commit();
-      }
-      __syncwarp();
-#pragma unroll
-      for (int h = 0; h < H; ++h) sa[cb ^ 1][lane][h] = alB[h];
-      srb[cb ^ 1][lane] = rowB;
-      uA = uB;
-    }
-    cp_wait<0>();
-    __syncwarp();
-    if (tile) {
-      if (cur >= 0) flush(cur);
-    } else {
-      float* dst = a.hagg + (int64_t)s.slot * HD + lane * VPL;
-#pragma unroll
-      for (int k = 0; k < VPL / 2; ++k) { dst[2 * k] = acc[k].x; dst[2 * k + 1] = acc[k].y; }
-    }
-  }
-  amax_flush(a.amax_out, amax_loc);
-}
-
-
 // ================================================================== gather engine v4
 // One warp streams a heavy segment or a light sub-tile: the 32-edge chunk attributes (gather index,
 // tile row, |α| per head, optional per-edge addend x per head) are loaded one chunk ahead into
@@ -1239,251 +889,9 @@ __global__ void __launch_bounds__(256, 3) k_fwd_agg4(const GatFwdArgs a) {
 // cp.async.bulk.tensor.2d.tile::gather4 per group of 4 edges (4 rows of HD bytes land contiguously in
 // a ring slot, completion on the slot's mbarrier), so consumer lanes spend no issue slots on
 // addresses.  Ring: G slots of 4 rows per warp; slot/phase follow a per-warp running group counter.
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int r0, int r1,
-                                            int r2, int r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx_u32(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
 
-constexpr int G5_SLOTS = 4;   // ring slots (4 rows each) per warp
-template <int H, bool HAS_X, int EXTRA>
-__host__ __device__ constexpr int g5_small_bytes() {   // per-warp attribute arrays + mbarriers
-  return 2 * H * 32 * 4 * (HAS_X ? 2 : 1) + 2 * 32 * 4 + 2 * 32 + EXTRA + 8 * G5_SLOTS;
-}
-template <int H, int VPL, bool HAS_X, int EXTRA>
-__host__ __device__ constexpr int g5_block_smem(int nw) {
-  return 128 + nw * (G5_SLOTS * 4 * 32 * VPL) + nw * g5_small_bytes<H, HAS_X, EXTRA>();
-}
-
-struct G5Warp {
-  uint32_t ring;     // shared address of this warp's ring (128-B aligned)
-  uint8_t* small;    // attribute arrays
-  uint32_t bars;     // shared address of G5_SLOTS mbarriers
-  uint32_t gi;       // groups consumed so far by this warp
-};
-template <int H, int VPL, bool HAS_X, int EXTRA>
-__device__ __forceinline__ G5Warp g5_setup(uint8_t* dsm, int nw) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t base = (smem_u32(dsm) + 127u) & ~127u;
-  uint8_t* gbase = dsm + (base - smem_u32(dsm));
-  G5Warp W;
-  W.ring = base + w * (G5_SLOTS * 4 * 32 * VPL);
-  W.small = gbase + nw * (G5_SLOTS * 4 * 32 * VPL) + w * g5_small_bytes<H, HAS_X, EXTRA>();
-  W.bars = smem_u32(W.small) + g5_small_bytes<H, HAS_X, EXTRA>() - 8 * G5_SLOTS;
-  W.gi = 0;
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < G5_SLOTS; ++k)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(W.bars + 8 * k) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  return W;
-}
-
-template <int H, int VPL, bool HAS_X, typename AttrF, typename RowF>
-__device__ __forceinline__ int g5_stream(G5Warp& W, const CUtensorMap* tmap, bool tile, int64_t seg_eb,
-                                         const TileLane& L, int T, AttrF&& attr, RowF&& on_row,
-                                         float2 (&acc)[VPL / 2], float& xs) {
-  constexpr int RB = 32 * VPL, GB = 4 * RB, S = G5_SLOTS;
-  const int lane = threadIdx.x & 31, myh = lane / (32 / H);
-  float* sa = reinterpret_cast<float*>(W.small);                         // [2][H][32] |α|
-  float* sx = sa + 2 * H * 32;                                           // [2][H][32] x (HAS_X)
-  int* sidx = reinterpret_cast<int*>(W.small + 2 * H * 32 * 4 * (HAS_X ? 2 : 1));   // [2][32] rows
-  uint8_t* srow = reinterpret_cast<uint8_t*>(sidx + 64);                // [2][32]
-  const uint32_t lane_off = lane * VPL;
-  const int tlast = T - 1;
-  const int ngroups = (T + 3) >> 2;
-  const uint32_t gi0 = W.gi;
-  auto load = [&](int c, int& idx, int& row, float (&al)[H], float (&x)[H]) {
-    const int t = c * 32 + lane;
-    int64_t e;
-    if (tile) {
-      row = tile_row(t < T ? t : tlast, L.end);
-      e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
-    } else {
-      row = 0;
-      e = seg_eb + t;
-    }
-    idx = 0;   // padding rows gather row 0 (always valid); their weight is +0
-#pragma unroll
-    for (int h = 0; h < H; ++h) { al[h] = 0.0f; x[h] = 0.0f; }
-    if (t < T) attr(e, idx, al, x);
-  };
-  auto stash = [&](int b, int row, const float (&al)[H], const float (&x)[H]) {
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      sa[(b * H + h) * 32 + lane] = al[h];
-      if constexpr (HAS_X) sx[(b * H + h) * 32 + lane] = x[h];
-    }
-    srow[b * 32 + lane] = (uint8_t)row;
-  };
-  auto issue = [&](int g) {   // stream group g -> ring slot (gi0 + g) % S
-    if (lane == 0) {
-      const uint32_t k = (gi0 + (uint32_t)g) % S;
-      const int4 nx = *reinterpret_cast<const int4*>(sidx + (((4 * g) >> 5) & 1) * 32 + ((4 * g) & 31));
-      mbar_expect_tx_u32(W.bars + 8 * k, GB);
-      tma_gather4(W.ring + k * GB, tmap, W.bars + 8 * k, 0, nx.x, nx.y, nx.z, nx.w);
-    }
-  };
-  auto group = [&](const Row<VPL> (&r)[4], float4 a4, float4 x4, uint32_t rw, int& cur) {
-    const float al[4] = {a4.x, a4.y, a4.z, a4.w};
-    const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
-    if ((int)(rw >> 24) == cur) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 al2 = make_float2(al[j], al[j]);
-#pragma unroll
-        for (int q = 0; q < VPL / 4; ++q) fma4_codes(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
-        if constexpr (HAS_X) xs = __fadd_rn(xs, xv[j]);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int rj = (int)((rw >> (8 * j)) & 0xffu);
-        if (rj != cur) {
-          if (cur >= 0) on_row(cur);
-          cur = rj;
-        }
-        const float2 al2 = make_float2(al[j], al[j]);
-#pragma unroll
-        for (int q = 0; q < VPL / 4; ++q) fma4_codes(r[j].w[q], al2, acc[2 * q], acc[2 * q + 1]);
-        if constexpr (HAS_X) xs = __fadd_rn(xs, xv[j]);
-      }
-    }
-  };
-  {
-    int idxA, rowA;
-    float alA[H], xA[H];
-    load(0, idxA, rowA, alA, xA);
-    stash(0, rowA, alA, xA);
-    sidx[lane] = idxA;
-  }
-  __syncwarp();
-#pragma unroll
-  for (int g = 0; g < S; ++g)
-    if (g < ngroups) issue(g);
-  int cur = tile ? -1 : 0;
-  const int nch = (T + 31) >> 5;
-  for (int c = 0; c < nch; ++c) {
-    int idxB, rowB;
-    float alB[H], xB[H];
-    load(c + 1, idxB, rowB, alB, xB);
-    const int cb = c & 1;
-    const float* sac = sa + (cb * H + myh) * 32;
-    const float* sxc = sx + (cb * H + myh) * 32;
-    const uint8_t* src_ = srow + cb * 32;
-    for (int i0 = 0; i0 < 32; i0 += 4) {
-      const int t0 = c * 32 + i0;
-      if (t0 >= T) break;
-      if (i0 == 12) {   // groups issued from here on read the next chunk's rows
-        sidx[(cb ^ 1) * 32 + lane] = idxB;
-        __syncwarp();
-      }
-      const int g = t0 >> 2;
-      const uint32_t gq = gi0 + (uint32_t)g, k = gq % S;
-      mbar_wait_addr(W.bars + 8 * k, (gq / S) & 1u);
-      const uint32_t slot0 = W.ring + k * GB + lane_off;
-      Row<VPL> r[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) r[j] = lds_row_slice<VPL>(slot0 + j * RB);
-      const float4 a4 = *reinterpret_cast<const float4*>(sac + i0);
-      float4 x4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      if constexpr (HAS_X) x4 = *reinterpret_cast<const float4*>(sxc + i0);
-      const uint32_t rw = *reinterpret_cast<const uint32_t*>(src_ + i0);
-      group(r, a4, x4, rw, cur);
-      __syncwarp();
-      if (g + S < ngroups) issue(g + S);   // refill the consumed slot (its reads are complete)
-    }
-    __syncwarp();
-    stash(cb ^ 1, rowB, alB, xB);
-    __syncwarp();
-  }
-  W.gi = gi0 + (uint32_t)ngroups;
-  return cur;
-}
 
 // FA (VPL >= 4, TMA gather): ⑤ H_out = (Σ fmaf(α, q_H′[u])) * s_H′ over (heavy segment | light sub-tile)
-template <int H, int VPL>
-__global__ void __launch_bounds__(256, 3) k_fwd_agg5(const __grid_constant__ GatFwdArgs a,
-                                                    const __grid_constant__ CUtensorMap tmap) {
-  constexpr int HD = 32 * VPL;
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int lane = threadIdx.x & 31;
-  G5Warp W = g5_setup<H, VPL, false, 0>(dsm, 8);
-  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
-  const int64_t n = a.g.n_local, hc = load_count(a.plan.counts);
-  const int64_t nitems = hc + load_count(a.plan.counts + 2);
-  float amax_loc = 0.0f;
-  FOR_ITEMS(item, a.work + 2, nitems) {
-    const bool tile = item >= hc;
-    Seg s;
-    s.eb = 0;
-    TileLane L;
-    int64_t r0 = 0;
-    int T;
-    if (!tile) {
-      decode_item(item, hc, a.g.in_ptr, a.plan, a.g.chunk, s);
-      T = (int)(s.ee - s.eb);
-      L.eb = 0; L.off = 0; L.end = 0;
-    } else {
-      const int32_t code = a.plan.tiles[item - hc];
-      r0 = (int64_t)(code >> 10) * TILE;
-      L = tile_setup(a.g.in_ptr, a.plan.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
-      unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
-      while (zm) {
-        const int j = __ffs(zm) - 1;
-        zm &= zm - 1;
-        float4* dst = reinterpret_cast<float4*>(a.Hout + (r0 + j) * HD + lane * VPL);
-#pragma unroll
-        for (int k = 0; k < VPL / 4; ++k) __stcs(dst + k, make_float4(0.0f, 0.0f, 0.0f, 0.0f));
-      }
-    }
-    float2 acc[VPL / 2];
-#pragma unroll
-    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
-    float xs = 0.0f;
-    auto flush = [&](int j) {
-      float4* dst = reinterpret_cast<float4*>(a.Hout + (r0 + j) * HD + lane * VPL);
-#pragma unroll
-      for (int k = 0; k < VPL / 4; ++k) {
-        const float4 o = make_float4(__fmul_rn(acc[2 * k].x, scH.s), __fmul_rn(acc[2 * k].y, scH.s),
-                                     __fmul_rn(acc[2 * k + 1].x, scH.s), __fmul_rn(acc[2 * k + 1].y, scH.s));
-        amax_loc = fmaxf(amax_loc, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
-        __stcs(dst + k, o);
-        acc[2 * k] = make_float2(0.0f, 0.0f);
-        acc[2 * k + 1] = make_float2(0.0f, 0.0f);
-      }
-    };
-    auto attr = [&](int64_t e, int& u, float (&al)[H], float (&)[H]) {
-      u = a.g.in_src[e];
-      if constexpr (H == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(a.alpha + e * 8);
-        al[0] = fabsf(v.x); al[1] = fabsf(v.y); al[2] = fabsf(v.z); al[3] = fabsf(v.w);
-      } else {
-#pragma unroll
-        for (int h = 0; h < H; ++h) al[h] = fabsf(a.alpha[e * 2 * H + h]);
-      }
-    };
-    const int cur = g5_stream<H, VPL, false>(W, &tmap, tile, s.eb, L, T, attr, flush, acc, xs);
-    if (tile) {
-      if (cur >= 0) flush(cur);
-    } else {
-      float4* dst = reinterpret_cast<float4*>(a.hagg + (int64_t)s.slot * HD + lane * VPL);
-#pragma unroll
-      for (int k = 0; k < VPL / 4; ++k)
-        dst[k] = make_float4(acc[2 * k].x, acc[2 * k].y, acc[2 * k + 1].x, acc[2 * k + 1].y);
-    }
-  }
-  amax_flush(a.amax_out, amax_loc);
-}
-
 // ================================================================== backward gather kernels (cp.async engine)
 template <int H, int VPL>
 __host__ __device__ constexpr int bwd3_warp_smem() {
@@ -1502,190 +910,6 @@ __device__ __forceinline__ int head_dot(const Row<VPL>& x, const Row<VPL>& y) {
 
 // BD1: ⑤″ ∂α = i2f(q_G[v]·q_H′[u]) (s_G s_H′) (IDP4A on codes), ④′ P = Σ fmaf(∂α, α) per
 // destination row (heavy segments: P partials), then for light rows ∂E_pre and ∂D.
-template <int H, int VPL>
-__global__ void __launch_bounds__(256, 2) k_bwd_dst1_v3(const GatBwdArgs a) {
-  constexpr int HD = 32 * VPL, R = AGG_RING, RB = 32 * VPL, LPH = 32 / H;
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int myh = lane / LPH;
-  const bool leader = (lane % LPH) == 0;
-  uint8_t* wsm = dsm + w * bwd3_warp_smem<H, VPL>();
-  float (*sa)[32][H] = reinterpret_cast<float (*)[32][H]>(wsm + R * RB);
-  float (*sd)[32][H] = reinterpret_cast<float (*)[32][H]>(wsm + R * RB + 2 * 32 * H * 4);
-  int (*srb)[32] = reinterpret_cast<int (*)[32]>(wsm + R * RB + 4 * 32 * H * 4);
-  int (*sed)[32] = reinterpret_cast<int (*)[32]>(wsm + R * RB + 4 * 32 * H * 4 + 2 * 32 * 4);
-  float (*pt)[H] = reinterpret_cast<float (*)[H]>(wsm + R * RB + 4 * 32 * H * 4 + 4 * 32 * 4);
-  const uint32_t ring_s = smem_u32(wsm) + lane * VPL;
-  const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
-  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
-  const float sGH = __fmul_rn(scG.s, scH.s);
-  const int64_t n = a.g.n_local, hc = load_count(a.pin.counts);
-  const int64_t nitems = hc + load_count(a.pin.counts + 2);
-  const int8_t* xbase = a.qHp + lane * VPL;
-  const int8_t* gbase = a.qG + lane * VPL;
-  const uint32_t ld32 = (uint32_t)a.ldHp;
-  FOR_ITEMS(item, a.work + 0, nitems) {
-    const bool tile = item >= hc;
-    Seg s;
-    TileLane L;
-    int64_t r0 = 0;
-    int T;
-    if (!tile) {
-      decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
-      T = (int)(s.ee - s.eb);
-      L.eb = 0; L.off = 0; L.end = 0; L.deg = 0; L.light = false;
-    } else {
-      const int32_t code = a.pin.tiles[item - hc];
-      r0 = (int64_t)(code >> 10) * TILE;
-      L = tile_setup(a.g.in_ptr, a.pin.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
-      if (L.light && L.deg == 0) {
-        const int64_t vg = a.g.row_begin + L.r;
-#pragma unroll
-        for (int h = 0; h < H; ++h) { a.P[vg * H + h] = 0.0f; a.dD[vg * H + h] = 0.0f; }
-      }
-    }
-    auto attrs = [&](int c, int& u, float (&al)[H], int& row, int& e32) {
-      const int t = c * 32 + lane;
-      int64_t e;
-      if (tile) {
-        row = tile_row(t, L.end);
-        e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
-      } else {
-        row = 0;
-        e = s.eb + t;
-      }
-      u = 0;
-      e32 = (int)e;
-#pragma unroll
-      for (int h = 0; h < H; ++h) al[h] = 0.0f;
-      if (t < T) {
-        u = a.g.in_src[e];
-#pragma unroll
-        for (int h = 0; h < H; ++h) al[h] = fabsf(a.alpha[e * 2 * H + h]);
-      }
-    };
-    // own q_G[v] slice per row (prefetched one row ahead)
-    const unsigned act = tile ? __ballot_sync(0xffffffffu, L.deg > 0) : 1u;
-    const int64_t vg0 = tile ? a.g.row_begin + r0 : a.g.row_begin + s.vl;
-    int nxt = act ? __ffs(act) - 1 : -1;
-    Row<VPL> gw{}, gw_nxt{};
-    if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
-    int uA, rowA, eA;
-    float alA[H];
-    attrs(0, uA, alA, rowA, eA);
-#pragma unroll
-    for (int h = 0; h < H; ++h) sa[0][lane][h] = alA[h];
-    srb[0][lane] = rowA;
-    sed[0][lane] = eA;
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const int uu = __shfl_sync(0xffffffffu, uA, j);
-      if (j < T) cp_row_slice<VPL>(ring_s + j * RB, xbase + (uint32_t)uu * ld32);
-      if ((j & 3) == 3) cp_commit();
-    }
-    float P = 0.0f;
-    int cur = -1;
-    const int nch = (T + 31) >> 5;
-    for (int c = 0; c < nch; ++c) {
-      int uB, rowB, eB;
-      float alB[H];
-      attrs(c + 1, uB, alB, rowB, eB);
-      __syncwarp();
-      const int cb = c & 1;
-      for (int i0 = 0; i0 < 32; i0 += 4) {
-        const int t0 = c * 32 + i0;
-        if (t0 >= T) break;
-        cp_wait<R / 4 - 1>();
-        const uint32_t slot0 = ring_s + (uint32_t)(t0 & (R - 1)) * RB;
-        Row<VPL> r[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) r[j] = lds_row_slice<VPL>(slot0 + j * RB);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (t0 + j < T) {
-            const int ri = tile ? srb[cb][i0 + j] : 0;
-            if (ri != cur) {
-              if (cur >= 0 && leader) pt[cur][myh] = P;
-              P = 0.0f;
-              cur = ri;
-              gw = gw_nxt;
-              nxt = tile ? tile_next(act, cur) : -1;
-              if (nxt >= 0) gw_nxt = load_row<VPL>(gbase + (vg0 + nxt) * a.ldG);
-            }
-            const int dot = head_dot<VPL, LPH>(gw, r[j]);
-            if (leader) {
-              const float dal = __fmul_rn(__int2float_rn(dot), sGH);
-              P = __fmaf_rn(dal, sa[cb][i0 + j][myh], P);
-              sd[cb][i0 + j][myh] = dal;
-            }
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int tn = t0 + R + j;
-          const int ua = __shfl_sync(0xffffffffu, uA, tn & 31);
-          const int ub = __shfl_sync(0xffffffffu, uB, tn & 31);
-          const uint32_t un = (uint32_t)(tn < (c + 1) * 32 ? ua : ub);
-          if (tn < T) cp_row_slice<VPL>(slot0 + j * RB, xbase + un * ld32);
-        }
-        cp_commit();
-      }
-      __syncwarp();
-      if (c * 32 + lane < T) {   // ∂α of this chunk -> scratch (edge-major, coalesced per edge)
-#pragma unroll
-        for (int h = 0; h < H; ++h) a.dalpha[(int64_t)sed[cb][lane] * H + h] = sd[cb][lane][h];
-      }
-#pragma unroll
-      for (int h = 0; h < H; ++h) sa[cb ^ 1][lane][h] = alB[h];
-      srb[cb ^ 1][lane] = rowB;
-      sed[cb ^ 1][lane] = eB;
-      uA = uB;
-      __syncwarp();
-    }
-    cp_wait<0>();
-    __syncwarp();
-    if (!tile) {
-      if (leader) a.hP[(int64_t)s.slot * H + myh] = P;
-      continue;
-    }
-    if (cur >= 0 && leader) pt[cur][myh] = P;
-    __syncwarp();
-    // ---- pass 2 (light rows): ∂E = α(∂α − P[v]), ∂E_pre, ∂D = Σ ∂E_pre (lane j sums row j)
-    float dDp[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) dDp[h] = 0.0f;
-    for (int base = 0; base < T; base += 32) {
-      const int cnt = T - base < 32 ? T - base : 32;
-      const int t = base + lane;
-      const int row = tile_row(t, L.end);
-      const int64_t e = __shfl_sync(0xffffffffu, L.eb, row) + (t - __shfl_sync(0xffffffffu, L.off, row));
-      if (lane < cnt) {
-#pragma unroll
-        for (int h = 0; h < H; ++h) {
-          const float x = a.alpha[e * 2 * H + h];
-          const float dE = __fmul_rn(fabsf(x), __fsub_rn(a.dalpha[e * H + h], pt[row][h]));
-          const float dEp = signbit(x) ? __fmul_rn(dE, a.slope) : dE;
-          sd[0][lane][h] = dEp;
-          a.alpha_dE[e * 2 * H + H + h] = dEp;   // ∂E_pre beside α (one sector per edge for the source pass)
-        }
-      }
-      __syncwarp();
-      const int lo = (L.off > base ? L.off : base) - base;
-      const int hi = (L.end < base + cnt ? L.end : base + cnt) - base;
-      for (int i = lo; i < hi; ++i)
-#pragma unroll
-        for (int h = 0; h < H; ++h) dDp[h] = __fadd_rn(dDp[h], sd[0][i][h]);
-      __syncwarp();
-    }
-    if (L.deg > 0) {
-      const int64_t vg = a.g.row_begin + L.r;
-#pragma unroll
-      for (int h = 0; h < H; ++h) { a.P[vg * H + h] = pt[lane][h]; a.dD[vg * H + h] = dDp[h]; }
-    }
-    __syncwarp();
-  }
-}
-
 // ②′ finalize of source row u (full row): ∂H′ = (agg·s_G + ∂S·a_src) + ∂D·a_dst ; ∂S stored
 template <int VPL>
 __device__ __forceinline__ void src_finalize_full(const GatBwdArgs& a, int64_t ul, int64_t ug, int myh, int H,
@@ -2281,78 +1505,6 @@ __global__ void __maxnreg__(96) k_bwd_src4(const GatBwdArgs a) {
 }
 
 // BS (one GPU, out_eid present, TMA gather): ⑤′ ∂H′_agg, ③′ ∂S over out-edges, ②′ finalize
-template <int H, int VPL, int NW>
-__global__ void __launch_bounds__(NW * 32, 3) k_bwd_src5(const __grid_constant__ GatBwdArgs a,
-                                                        const __grid_constant__ CUtensorMap tmap) {
-  constexpr int HD = 32 * VPL;
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int lane = threadIdx.x & 31;
-  const int myh = lane / (32 / H);
-  const bool leader = (lane % (32 / H)) == 0;
-  G5Warp W = g5_setup<H, VPL, true, 0>(dsm, NW);
-  const Scale scG = scale_from_amax(amax_load(a.amax_G), a.bits);
-  const int64_t n = a.g.n_local, hc = load_count(a.pout.counts);
-  const int64_t nitems = hc + load_count(a.pout.counts + 2);
-  float amax_loc = 0.0f;
-  FOR_ITEMS(item, a.work + 2, nitems) {
-    const bool tile = item >= hc;
-    Seg s;
-    s.eb = 0;
-    TileLane L;
-    int64_t r0 = 0;
-    int T;
-    float2 acc[VPL / 2];
-#pragma unroll
-    for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
-    if (!tile) {
-      decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
-      T = (int)(s.ee - s.eb);
-      L.eb = 0; L.off = 0; L.end = 0;
-      r0 = s.vl;
-    } else {
-      const int32_t code = a.pout.tiles[item - hc];
-      r0 = (int64_t)(code >> 10) * TILE;
-      L = tile_setup(a.g.out_ptr, a.pout.hbase, r0, n, T, (code >> 5) & 31, (code & 31) + 1);
-      unsigned zm = __ballot_sync(0xffffffffu, L.light && L.deg == 0);
-      while (zm) {
-        const int j = __ffs(zm) - 1;
-        zm &= zm - 1;
-        src_finalize4<H, VPL>(a, r0 + j, a.g.row_begin + r0 + j, myh, leader, 0.0f, acc, scG.s, amax_loc);
-      }
-    }
-    const int64_t ug0 = a.g.row_begin + r0;
-    float dS = 0.0f;
-    auto flush = [&](int j) {
-      src_finalize4<H, VPL>(a, r0 + j, ug0 + j, myh, leader, dS, acc, scG.s, amax_loc);
-      dS = 0.0f;
-    };
-    auto attr = [&](int64_t e, int& v, float (&al)[H], float (&x)[H]) {
-      v = a.g.out_dst[e];
-      const int64_t eid = a.g.out_eid[e];
-      if constexpr (H == 4) {
-        const float4 p = *reinterpret_cast<const float4*>(a.alpha + eid * 8);
-        const float4 q = *reinterpret_cast<const float4*>(a.alpha + eid * 8 + 4);
-        al[0] = fabsf(p.x); al[1] = fabsf(p.y); al[2] = fabsf(p.z); al[3] = fabsf(p.w);
-        x[0] = q.x; x[1] = q.y; x[2] = q.z; x[3] = q.w;
-      } else {
-#pragma unroll
-        for (int h = 0; h < H; ++h) { al[h] = fabsf(a.alpha[eid * 2 * H + h]); x[h] = a.alpha[eid * 2 * H + H + h]; }
-      }
-    };
-    const int cur = g5_stream<H, VPL, true>(W, &tmap, tile, s.eb, L, T, attr, flush, acc, dS);
-    if (tile) {
-      if (cur >= 0) flush(cur);
-    } else {
-      if (leader) a.hdS[(int64_t)s.slot * H + myh] = dS;
-      float4* dst = reinterpret_cast<float4*>(a.hagg + (int64_t)s.slot * HD + lane * VPL);
-#pragma unroll
-      for (int k = 0; k < VPL / 4; ++k)
-        dst[k] = make_float4(acc[2 * k].x, acc[2 * k].y, acc[2 * k + 1].x, acc[2 * k + 1].y);
-    }
-  }
-  amax_flush(a.amax_dHp, amax_loc);
-}
-
 // ---- BD1: ⑤″ ∂α (IDP4A on codes) + ④′ P (+ ∂E_pre, ∂D for light rows) per (tile | segment, group)
 template <int VPL, int HPW>
 __device__ __forceinline__ int cg_dot(const Row<VPL>& x, const Row<VPL>& y) {
@@ -2742,7 +1894,7 @@ template <int H, int VPL>
 __global__ void __launch_bounds__(256) k_fwd_combine(const GatFwdArgs a) {
   constexpr int HD = 32 * VPL;
   __shared__ unsigned sh_amax;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) sh_amax = 0u;
   __syncthreads();
   const Scale scH = scale_from_amax(amax_load(a.amax_Hp), a.bits);
@@ -2945,16 +2097,6 @@ __global__ void __launch_bounds__(256) k_bwd_attn_grad(const GatBwdArgs a) {
 }
 
 // ------------------------------------------------------------------ dispatch
-// Gather engine: cp.async (v4) by default; TMA gather4 (v5) with TANGO_GATHER=tma.  Measured on the
-// arxiv layer (r1): v5 fwd_agg 0.233 ms vs v4 0.220 ms, bwd_src 0.465 vs 0.338 ms, so v4 stays default.
-static bool gather_tma() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TANGO_GATHER");
-    v = (e && strcmp(e, "tma") == 0) ? 1 : 0;
-  }
-  return v == 1;
-}
 static int item_grid(int64_t items) {
   int64_t g = (items + WPB - 1) / WPB;
   const int64_t cap = (int64_t)num_sms() * 8;     // >= resident blocks; the work queue balances
@@ -2978,7 +2120,7 @@ static int heavy_grid(int64_t cap) {
   return g < c ? g : c;
 }
 
-bool gat_codes_biased(int heads, int hd) { return hd / 32 >= 4 && heads <= 8 && !gather_tma(); }
+bool gat_codes_biased(int heads, int hd) { return hd / 32 >= 4 && heads <= 8; }
 
 // (H, HD/32) for the row-wide kernels, (VPL, HPW) head-group shape for the gather kernels
 #define TANGO_HV_CASES(X) X(1, 2) X(1, 4) X(1, 8) X(1, 16) X(2, 2) X(2, 4) X(2, 8) X(2, 16) \
@@ -3111,7 +2253,7 @@ static cudaError_t launch_gat_bwd_src_split(const GatBwdArgs& a, cudaStream_t st
 
 cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st, const SideStream* aux) {
   if (a.g.n_local == 0) return cudaSuccess;
-  if (aux && a.d.hd / 32 >= 4 && !gather_tma()) return launch_gat_fwd_split(a, st, *aux);
+  if (aux && a.d.hd / 32 >= 4) return launch_gat_fwd_split(a, st, *aux);
   const int hv = a.d.heads * 100 + a.d.hd / 32;
   int vpl, hpw;
   if (!cg_shape(a.d.head_dim, vpl, hpw)) return cudaErrorInvalidValue;
@@ -3148,21 +2290,7 @@ cudaError_t launch_gat_fwd(const GatFwdArgs& a, cudaStream_t st, const SideStrea
                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                 \
           attr_set = true;                                                                         \
         }                                                                                          \
-        if (gather_tma()) {                                                                        \
-          constexpr int smem5 = g5_block_smem<H_, (V_ >= 4 ? V_ : 4), false, 0>(8);                \
-          static bool attr5_set = false;                                                           \
-          if (!attr5_set) {                                                                        \
-            cudaFuncSetAttribute(k_fwd_agg5<H_, (V_ >= 4 ? V_ : 4)>,                               \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem5);              \
-            attr5_set = true;                                                                      \
-          }                                                                                        \
-          CUtensorMap tm;                                                                          \
-          if (!make_row_gather_map(&tm, a.qHp, (uint64_t)a.g.n_global, (uint64_t)a.d.hd, (uint64_t)a.ldHp)) \
-            return cudaErrorInvalidValue;                                                          \
-          k_fwd_agg5<H_, (V_ >= 4 ? V_ : 4)><<<item_grid(a.plan.cap + a.plan.tcap), 256, smem5, st>>>(a, tm); \
-        } else {                                                                                   \
-          k_fwd_agg4<H_, (V_ >= 4 ? V_ : 4)><<<item_grid(a.plan.cap + a.plan.tcap), 256, smem, st>>>(a); \
-        }                                                                                          \
+        k_fwd_agg4<H_, (V_ >= 4 ? V_ : 4)><<<item_grid(a.plan.cap + a.plan.tcap), 256, smem, st>>>(a); \
       } else {                                                                                     \
         k_fwd_agg2<H_, V_><<<item_grid(a.plan.cap + a.plan.tcap), 256, 0, st>>>(a);               \
       } }                                                                                          \
@@ -3187,12 +2315,6 @@ cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st, const SideS
     if (hv == H_ * 100 + V_ && V_ >= 4) {                                                          \
       ok = true;                                                                                   \
       constexpr int VV = V_ >= 4 ? V_ : 4;                                                          \
-      constexpr int smem = 8 * bwd3_warp_smem<H_, VV>();                                           \
-      static bool attr_set = false;                                                                \
-      if (!attr_set) {                                                                             \
-        cudaFuncSetAttribute(k_bwd_dst1_v3<H_, VV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-        attr_set = true;                                                                           \
-      }                                                                                            \
       ProfScope p("gat_bwd_dst1", st);                                                             \
       if (H_ <= 8) {                                                                               \
         constexpr int NW = 7, smem4 = NW * dst4_warp_smem<H_, VV>();                               \
@@ -3202,8 +2324,6 @@ cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st, const SideS
           attr4_set = true;                                                                        \
         }                                                                                          \
         if (a.codes_biased) k_bwd_dst1_v4<H_, VV, NW, true><<<item_grid(a.pin.cap + a.pin.tcap), NW * 32, smem4, st>>>(a); else k_bwd_dst1_v4<H_, VV, NW, false><<<item_grid(a.pin.cap + a.pin.tcap), NW * 32, smem4, st>>>(a);   \
-      } else {                                                                                     \
-        k_bwd_dst1_v3<H_, VV><<<item_grid(a.pin.cap + a.pin.tcap), 256, smem, st>>>(a);            \
       }                                                                                            \
     }
     TANGO_HV_CASES(X)
@@ -3235,7 +2355,7 @@ cudaError_t launch_gat_bwd_dst(const GatBwdArgs& a, cudaStream_t st, const SideS
 
 cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st, const SideStream* aux) {
   if (a.g.n_local == 0) return cudaSuccess;
-  if (aux && a.d.hd / 32 >= 4 && a.g.out_eid && !gather_tma()) return launch_gat_bwd_src_split(a, st, *aux);
+  if (aux && a.d.hd / 32 >= 4 && a.g.out_eid) return launch_gat_bwd_src_split(a, st, *aux);
   int vpl, hpw;
   if (!cg_shape(a.d.head_dim, vpl, hpw)) return cudaErrorInvalidValue;
   const int64_t cg_items = (a.pout.cap + (a.g.n_local + TILE - 1) / TILE) * (a.d.hd / (32 * vpl));
@@ -3261,20 +2381,7 @@ cudaError_t launch_gat_bwd_src(const GatBwdArgs& a, cudaStream_t st, const SideS
           cudaFuncSetAttribute(k_bwd_src4<H_, VV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4); \
           attr4_set = true;                                                                        \
         }                                                                                          \
-        if (gather_tma()) {                                                                        \
-          constexpr int smem5 = g5_block_smem<H_, VV, true, 0>(NW);                                \
-          static bool attr5_set = false;                                                           \
-          if (!attr5_set) {                                                                        \
-            cudaFuncSetAttribute(k_bwd_src5<H_, VV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem5); \
-            attr5_set = true;                                                                      \
-          }                                                                                        \
-          CUtensorMap tm;                                                                          \
-          if (!make_row_gather_map(&tm, a.qG, (uint64_t)a.g.n_global, (uint64_t)a.d.hd, (uint64_t)a.ldG)) \
-            return cudaErrorInvalidValue;                                                          \
-          k_bwd_src5<H_, VV, NW><<<item_grid(a.pout.cap + a.pout.tcap), NW * 32, smem5, st>>>(a, tm); \
-        } else {                                                                                   \
-          k_bwd_src4<H_, VV, NW><<<item_grid(a.pout.cap + a.pout.tcap), NW * 32, smem4, st>>>(a);  \
-        }                                                                                          \
+        k_bwd_src4<H_, VV, NW><<<item_grid(a.pout.cap + a.pout.tcap), NW * 32, smem4, st>>>(a);  \
       } else {                                                                                     \
         if (a.codes_biased) k_bwd_src_v3<H_, VV, true><<<item_grid(a.pout.cap + a.pout.tcap), 256, smem, st>>>(a); \
         else k_bwd_src_v3<H_, VV, false><<<item_grid(a.pout.cap + a.pout.tcap), 256, smem, st>>>(a);  \

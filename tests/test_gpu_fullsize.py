@@ -151,3 +151,40 @@ def test_gat_layer_products_full_size(T, orc):
     bound = 4096 * 2.0 ** -24
     err = np.abs(das.cpu().numpy().astype(np.float64) - b["da_src"])
     assert np.all(err <= bound * b["da_src_abs"] + 1e-7)
+
+
+@pytest.mark.skipif(not __import__("os").environ.get("TANGO_FULL_REDDIT"),
+                    reason="set TANGO_FULL_REDDIT=1 (about 4 min: graph build + oracle on 114 M edges)")
+def test_gat_layer_reddit_full_size(T, orc):
+    """BASELINE.json configs[3] on one GPU, exactly as bench.py times it (Reddit-shaped: N = 233 K,
+    E = 114 M, mean in-degree 489, F = 602, 4 x 128, the v6 dataflow): every output of the layer
+    against the full oracle, bit for bit (∂a included: the pinned chunk order of R39)."""
+    kw, F, H, D = inputs.WORKLOADS["reddit"]
+    g = inputs.workload_graph("reddit")
+    W, a_s, a_d = inputs.gat_params(F, H, D)
+    X = inputs.features(g.n, F)
+    dY = inputs.grad_out(g.n, H * D)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    layer = T.GATLayer(T.DeviceGraph(g), cu(W), cu(a_s), cu(a_d), H, D, slope=0.2, bits=8)
+    Hout, amax_out = layer.forward(cu(X), step=0, layer_id=0)
+    fv = layer.view()
+    dX, dW, das, dad = layer.backward(cu(dY), step=0, layer_id=0)
+    bv = layer.view()
+    torch.cuda.synchronize()
+    layer.check_status()
+    assert fv["dataflow"] == 2
+    f = orc.gat_fwd(g, X, W, a_s, a_d, H, D, slope=0.2, bits=8, step=0, layer_id=0, chunk=256)
+    for name, key in (("qH", "qH"), ("qHp", "qHp"), ("S", "S"), ("qS", "qS"), ("qD", "qD"), ("m", "m"),
+                      ("den", "den")):
+        eq(name, fv[name], f[key])
+    eq("H_out", Hout, f["Hout"])
+    eq("amax_out", amax_out, f["amax_out"])
+    b = orc.gat_bwd(g, f, X, W, a_s, a_d, dY)
+    eq("qG", bv["qG"], b["qG"])
+    eq("dalpha_out", bv["dalpha_out"], b["dalpha"][g.out_eid])
+    for name in ("P", "dD", "dS", "dHp", "qdHp"):
+        eq(name, bv[name], b[name])
+    eq("dH", dX, b["dH"])
+    eq("dW", dW, b["dW"])
+    eq("da_src", das, b["da_src"])
+    eq("da_dst", dad, b["da_dst"])
