@@ -290,12 +290,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
             __syncwarp();
           }
-        } else if constexpr (MODE == EPI_I32) {
+        } else if constexpr (MODE == EPI_I32) {   // transposed through shared memory as EPI_STORE
           int32_t* Ci = reinterpret_cast<int32_t*>(p.C);
-          if (row_ok) {
+          int32_t* tr = reinterpret_cast<int32_t*>(sm_tr) + ew * (32 * TR_LD);
+          const int64_t rowbase = (int64_t)mt * BM + sub * 32;
+          const int cl = lane & 15, rh = lane >> 4;
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i < p.N) Ci[row * p.ldc + col0 + i] = (int32_t)r[i];
+          for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) tr[lane * TR_LD + i] = (int32_t)r[hf * 16 + i];
+            __syncwarp();
+            const int64_t col = col0 + hf * 16 + cl;
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const int64_t rr = rowbase + j + rh;
+              if (rr < p.M && col < p.N) Ci[rr * p.ldc + col] = tr[(j + rh) * TR_LD + cl];
+            }
+            __syncwarp();
           }
         } else {  // EPI_ATOMIC64
           unsigned long long* C64 = reinterpret_cast<unsigned long long*>(p.C);
