@@ -438,6 +438,37 @@ def spmm_sweep_bench(T, torch, dg, g, F, args, l2_flush, peaks):
     return res
 
 
+def incidence_spmm_bench(T, torch, dg, g, wname, args, l2_flush, peaks, widths=(4, 8, 12, 16, 20)):
+    """SURVEY.md §8(d) μ row (Fig.16a, Table 2): the incidence-matrix SPMM ③″ (out[v] = Σᶜ of
+    the edge-feature rows of v's contiguous in-edges, tango_edge_sum dir IN) and its reversed form ③′
+    (out-edges, rows gathered through out_eid) at edge-feature widths 4-20 (headline 16).  Device time per
+    call (CUDA events on the launching stream, L2 flushed before each call, median of >= 5); algorithmic
+    bytes = E·F·4 edge records + n·F·4 output + (n + 1)·8 CSR pointers (+ E·4 out_eid for ③′)."""
+    res = {"graph": f"{wname}-shaped (N={g.n}, E={dg.e_in})", "hbm_peak_gbs": peaks["hbm_gbs"]}
+    E, n = dg.e_in, g.n
+    for F in widths:
+        x = torch.randn((E, F), device="cuda", generator=torch.Generator(device="cuda").manual_seed(F))
+        for direction, name in ((0, "in"), (1, "out")):
+            out = T.edge_sum(dg, direction, F, x)
+            ts = []
+            for _ in range(max(5, args.steps)):
+                l2_flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                T.edge_sum(dg, direction, F, x, out=out)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms = statistics.median(ts)
+            byts = E * F * 4 + n * F * 4 + (n + 1) * 8 + (E * 4 if direction else 0)
+            gbs = byts / (ms / 1e3) / 1e9
+            res[f"F{F}_{name}"] = {"ms": round(ms, 4), "gbs": round(gbs, 1),
+                                   "hbm_frac": round(gbs / peaks["hbm_gbs"], 3)}
+        del x
+    res["paper_table2_gbs_F16"] = {"arxiv": 344.06, "products": 491.72, "gpu": "V100S (P:1150-1163)"}
+    return res
+
+
 # ------------------------------------------------------------------------------------- reference arm
 def sample_graph(name, frac):
     """The workload's recipe (same degree law, cap, seeds) at a fraction of its nodes and draws."""
@@ -797,6 +828,9 @@ def main():
                                        l2_flush, timed=False)
                 extra_out[wname] = {k: r2[k] for k in ("ms", "N", "E", "F", "heads", "head_dim", "dataflow",
                                                         "roofline", "kernel_ms_per_step")}
+                if wname in ("arxiv", "products"):   # Table 2's datasets
+                    extra_out[f"incidence_spmm_{wname}"] = incidence_spmm_bench(T, torch, x2["dg"], x2["g"], wname,
+                                                                               args, l2_flush, peaks)
                 if wname == "arxiv" and ("train" in extras or "sddmm" in extras):
                     gA, dgA = x2["g"], x2["dg"]
                     if "train" in extras:

@@ -174,11 +174,17 @@ tango_status tango_softmax_bwd(const tango_graph* G, int32_t heads, const float*
 /*     dir TANGO_OUT sums out-edges (w_e = destination, weight w[out_eid[e]]).*/
 /*  edge_w == NULL: out_i32[v,j] = Σ q_X[w_e,j] (exact int32, order-free);     */
 /*     out (nullable) = (float)out_i32 * s_X.                                  */
+/*  row_scale (nullable, device [n_local]): out[v,j] = out[v,j] * row_scale[v] */
+/*     (one more rn multiply; the GCN normalisation nd / ns, reading R26).     */
+/*  amax_out (nullable, device fp32 scalar, pre-set by the caller, e.g. 0):    */
+/*     atomically raised to max |out| (the next layer's quantization scale,   */
+/*     P:736-739), order-free.                                                 */
 /* X: [n_global][X->ld] codes with X->cols = heads*D.  out [n_local][cols].    */
 /* ------------------------------------------------------------------------- */
 enum { TANGO_IN = 0, TANGO_OUT = 1 };
 tango_status tango_spmm_q(const tango_graph* G, int32_t dir, const float* edge_w, const tango_qtensor* X,
-                          int32_t heads, float* out, int32_t* out_i32, cudaStream_t stream);
+                          int32_t heads, const float* row_scale, float* out, int32_t* out_i32, float* amax_out,
+                          cudaStream_t stream);
 
 /* Incidence-matrix SPMM for edge features (③″/③′):        */
 /* out[v,h] = Σᶜ x[e,h] over the in-edges (dir IN) or out-edges (dir OUT).    */

@@ -383,13 +383,9 @@ tango_status tango_quantize(const float* x, int64_t rows, int64_t cols, int64_t 
   TRY(check_q(out));
   if (!x && rows * cols > 0) return TANGO_ERR_INVALID_ARG;
   if (out->rows != rows || out->cols != cols || global_row0 < 0) return TANGO_ERR_SHAPE;
-  // the amax lives in amax_out if given, otherwise in a small stream-ordered scratch
-  float* slot = amax_out;
-  float* scratch = nullptr;
-  if (!slot) {
-    TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(float), stream));
-    slot = scratch;
-  }
+  // the amax lives in amax_out if given; otherwise the scale word holds it until the codes are written and
+  // is then converted in place (no allocation inside the call)
+  float* slot = amax_out ? amax_out : out->scale;
   if (amax_hint) {
     TRY_CUDA(cudaMemcpyAsync(slot, amax_hint, sizeof(float), cudaMemcpyDeviceToDevice, stream));
   } else {
@@ -397,9 +393,9 @@ tango_status tango_quantize(const float* x, int64_t rows, int64_t cols, int64_t 
     TRY(launch_status(launch_absmax(x, rows, cols, nullptr, reinterpret_cast<unsigned*>(slot), stream)));
   }
   TRY(launch_status(launch_quantize(x, rows, cols, nullptr, global_row0 * cols, reinterpret_cast<unsigned*>(slot),
-                                    out->bits, rng.seed, rng.step, rng.tag, out->q, out->ld, nullptr, 0, out->scale,
-                                    dev_status, stream)));
-  if (scratch) TRY_CUDA(cudaFreeAsync(scratch, stream));
+                                    out->bits, rng.seed, rng.step, rng.tag, out->q, out->ld, nullptr, 0,
+                                    amax_out ? out->scale : nullptr, dev_status, stream)));
+  if (!amax_out) TRY(launch_status(launch_amax_to_scale(out->scale, out->bits, stream)));
   return TANGO_OK;
 }
 
@@ -496,20 +492,24 @@ tango_status tango_softmax_bwd(const tango_graph* G, int32_t heads, const float*
 }
 
 tango_status tango_spmm_q(const tango_graph* G, int32_t dir, const float* edge_w, const tango_qtensor* X,
-                          int32_t heads, float* out, int32_t* out_i32, cudaStream_t stream) {
+                          int32_t heads, const float* row_scale, float* out, int32_t* out_i32, float* amax_out,
+                          cudaStream_t stream) {
   TRY(check_graph(G, dir == TANGO_OUT));
   TRY(check_q(X));
   if (dir != TANGO_IN && dir != TANGO_OUT) return TANGO_ERR_INVALID_ARG;
   if (heads <= 0 || X->cols % heads || X->rows != G->n_global) return TANGO_ERR_SHAPE;
+  if ((row_scale || amax_out) && !out) return TANGO_ERR_INVALID_ARG;
   const GraphDev g = dev_graph(G);
+  unsigned* amax = reinterpret_cast<unsigned*>(amax_out);
   if (edge_w) {
     if (!out) return TANGO_ERR_INVALID_ARG;
     if (dir == TANGO_OUT && G->e_out > 0 && !G->out_eid) return TANGO_ERR_INVALID_ARG;
-    return launch_status(launch_spmm_w(g, dir, heads, (int)X->cols, edge_w, X->q, X->ld, X->scale, out, stream));
+    return launch_status(launch_spmm_w(g, dir, heads, (int)X->cols, edge_w, X->q, X->ld, X->scale, row_scale, out,
+                                       amax, dir == TANGO_OUT ? G->e_out : G->e_in, stream));
   }
   if (!out && !out_i32) return TANGO_ERR_INVALID_ARG;
   return launch_status(
-      launch_spmm_sum(g, dir, (int)X->cols, X->q, X->ld, X->scale, nullptr, out, out_i32, nullptr, stream));
+      launch_spmm_sum(g, dir, (int)X->cols, X->q, X->ld, X->scale, row_scale, out, out_i32, amax, stream));
 }
 
 tango_status tango_edge_sum(const tango_graph* G, int32_t dir, int32_t heads, const float* x, float* out,
@@ -519,7 +519,7 @@ tango_status tango_edge_sum(const tango_graph* G, int32_t dir, int32_t heads, co
   if (dir == TANGO_OUT && G->e_out > 0 && !G->out_eid) return TANGO_ERR_INVALID_ARG;
   if (heads <= 0) return TANGO_ERR_SHAPE;
   if (!out) return TANGO_ERR_INVALID_ARG;
-  return launch_status(launch_edge_sum(dev_graph(G), dir, heads, x, out, stream));
+  return launch_status(launch_edge_sum(dev_graph(G), dir, heads, x, out, dir == TANGO_OUT ? G->e_out : G->e_in, stream));
 }
 
 }  // extern "C"

@@ -28,6 +28,7 @@ cudaError_t launch_quantize(const float* x, int64_t rows, int64_t cols, const fl
                             const unsigned* amax_slot, int bits, uint64_t seed, uint32_t step, uint32_t tag,
                             int8_t* q, int64_t ld, int8_t* qt, int64_t ldt, float* scale_out, int32_t* status,
                             cudaStream_t st, uint32_t code_xor = 0u);
+cudaError_t launch_amax_to_scale(float* slot, int bits, cudaStream_t st);
 
 cudaError_t launch_error_x(const float* x, int64_t rows, int64_t cols, const int8_t* q, int64_t ld, const float* s,
                            double* err, cudaStream_t st);
@@ -186,9 +187,11 @@ cudaError_t launch_edge_softmax(const GraphDev& g, int heads, const float* el, f
                                 cudaStream_t st);
 cudaError_t launch_softmax_bwd(const GraphDev& g, int heads, const float* alpha, const float* dalpha,
                                const float* e_pre, float slope, float* P, float* dEp, cudaStream_t st);
-cudaError_t launch_edge_sum(const GraphDev& g, int dir, int heads, const float* x, float* out, cudaStream_t st);
+cudaError_t launch_edge_sum(const GraphDev& g, int dir, int heads, const float* x, float* out, int64_t e_list,
+                            cudaStream_t st);
 cudaError_t launch_spmm_w(const GraphDev& g, int dir, int heads, int cols, const float* w, const int8_t* qX,
-                          int64_t ldx, const float* sX, float* out, cudaStream_t st);
+                          int64_t ldx, const float* sX, const float* rowscale, float* out, unsigned* amax_out,
+                          int64_t e_list, cudaStream_t st);
 cudaError_t launch_spmm_sum(const GraphDev& g, int dir, int cols, const int8_t* qX, int64_t ldx, const float* sX,
                             const float* rowscale, float* out, int32_t* out_i32, unsigned* amax_out,
                             cudaStream_t st);

@@ -1,7 +1,8 @@
 // prims.cu — the unfused sparse primitives of the C ABI (tango_sddmm_q, tango_edge_softmax,
-// tango_softmax_bwd, tango_edge_sum, tango_spmm_q) and the GCN helpers.  One thread per
-// (row, head) or (row, column), sequential over the row's edges in canonical order: the same
-// arithmetic as the fused kernels of gat.cu, laid out for clarity rather than speed.
+// tango_softmax_bwd, tango_edge_sum, tango_spmm_q) and the GCN helpers.  tango_edge_sum (the paper's
+// incidence SPMM, Table 2) is a bandwidth kernel (edge-window blocks, chunk items); the others run one
+// thread per (row, head) or (row, column), sequential over the row's edges in canonical order: the
+// same arithmetic as the fused kernels of gat.cu / gat2.cu, laid out for clarity rather than speed.
 // Paper: ③ P:204-209, ④ P:212-217, ⑤/⑤′ P:224-251, ⑤″ P:252-255, ④′ P:258-264,
 // ③′/③″ P:276 and P:821-832, GCN P:347-348.
 #include "rowops.cuh"
@@ -88,43 +89,338 @@ __global__ void k_softmax_bwd(GraphDev g, int heads, const float* alpha, const f
   }
 }
 
-__global__ void k_edge_sum(GraphDev g, int dir, int heads, const float* x, float* out) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (tid >= g.n_local * heads) return;
-  const int64_t vl = tid / heads;
-  const int h = (int)(tid % heads);
-  const int64_t* ptr = dir ? g.out_ptr : g.in_ptr;
-  const int64_t b = ptr[vl], e1 = ptr[vl + 1];
-  CSum cs; cs.init();
-  int left = g.chunk;
-  for (int64_t p = b; p < e1; ++p) {
-    const int64_t eid = dir ? (int64_t)g.out_eid[p] : p;
-    if (left == 0) { cs.fold(); left = g.chunk; }
-    cs.part = __fadd_rn(cs.part, x[eid * heads + h]);
-    --left;
-  }
-  out[vl * heads + h] = cs.finish(e1 - b);
+// ---------------------------------------------------------------------------- incidence SPMM (③′ / ③″)
+// out[v,h] = Σᶜ x[e,h] over v's in-edges (dir 0, contiguous in-CSR edge records: a streaming read) or
+// out-edges (dir 1, records out_eid[p]: a gather of F-float rows), reading R14.
+// Edge-window blocks: block b owns the rows whose edge list starts in [b·EPB, (b+1)·EPB) (a binary
+// search of the CSR pointer, no plan); its rows are cut into canonical chunks ("items", ≤ C_E edges).  A
+// group of GW = min(F, 32) lanes sums one (item, 32-column block) sequentially — F consecutive floats per
+// edge, so a group's load is one contiguous 4F-byte run; a row with one chunk is written directly, a hub
+// row's chunk partials go to shared memory and are folded left to right (total = p_0, total += p_c)
+// after a barrier.  Rows are taken in batches of at most ES_ROWS rows and ES_SLOTS(F) items; a row with
+// more chunks than one batch holds is folded window by window (the running total kept in registers of
+// the folding threads — the same left-to-right order).
+constexpr int ES_THREADS = 256, ES_ROWS = 256;
+
+__host__ __device__ inline int es_slots(int F) {
+  const int s = 4096 / F;
+  return s > 1024 ? 1024 : (s < 8 ? 8 : s);
 }
 
-__global__ void k_spmm_w(GraphDev g, int dir, int heads, int cols, const float* w, const int8_t* qX, int64_t ldx,
-                         const float* sX, float* out) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (tid >= g.n_local * cols) return;
-  const int64_t vl = tid / cols;
-  const int j = (int)(tid % cols);
-  const int h = j / (cols / heads);
-  const int64_t* ptr = dir ? g.out_ptr : g.in_ptr;
-  const int64_t b = ptr[vl], e1 = ptr[vl + 1];
-  CSum cs; cs.init();
-  int left = g.chunk;
-  for (int64_t p = b; p < e1; ++p) {
-    const int64_t eid = dir ? (int64_t)g.out_eid[p] : p;
-    const int64_t other = dir ? (int64_t)g.out_dst[p] : (int64_t)g.in_src[p];
-    if (left == 0) { cs.fold(); left = g.chunk; }
-    cs.part = __fmaf_rn(w[eid * heads + h], i8f(qX[other * ldx + j]), cs.part);
-    --left;
+template <int DIR>
+__global__ void __launch_bounds__(ES_THREADS) k_edge_sum_w(GraphDev g, int F, int64_t epb, int64_t E,
+                                                          const float* __restrict__ x, float* __restrict__ out) {
+  extern __shared__ __align__(16) float es_part[];               // [slots + 1][F]
+  __shared__ int s_pre[ES_ROWS];                                 // inclusive prefix of chunk counts
+  __shared__ int s_cnt;
+  const int64_t* __restrict__ ptr = DIR ? g.out_ptr : g.in_ptr;
+  const int32_t* __restrict__ eid = g.out_eid;
+  const int64_t n = g.n_local, C = g.chunk;
+  const int slots = es_slots(F);
+  // rows of this block: starts in [lo, hi)
+  auto lower = [&](int64_t key) {   // first row r in [0, n] with ptr[r] >= key (ptr[n] = E)
+    int64_t a = 0, b = n;
+    while (a < b) {
+      const int64_t m = (a + b) >> 1;
+      if (ptr[m] < key) a = m + 1; else b = m;
+    }
+    return a;
+  };
+  const int64_t lo = (int64_t)blockIdx.x * epb, hi = lo + epb;
+  int64_t r0 = lower(lo), r1 = (hi > E) ? n : lower(hi);
+  if (lo > E) return;
+  if (hi > E) r1 = n;   // the last block also owns the trailing rows that start at E
+  const int GW = F < 32 ? F : 32, GPW = 32 / GW, ncb = (F + 31) / 32;
+  const int lane = threadIdx.x & 31, grp = (threadIdx.x >> 5) * GPW + lane / GW, gl = lane % GW;
+  const bool lane_ok = lane / GW < GPW;
+  const int ngroups = (ES_THREADS / 32) * GPW;
+  auto chunks = [&](int64_t r) -> int64_t {
+    const int64_t d = ptr[r + 1] - ptr[r];
+    return d <= C ? 1 : (d + C - 1) / C;
+  };
+  // sequential sum of list positions [pb, pe) of column h (pe - pb <= C)
+  auto chunk_sum = [&](int64_t pb, int64_t pe, int h) -> float {
+    float acc = 0.0f;
+    for (int64_t p = pb; p < pe; p += 8) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[j] = 0.0f;
+        if (p + j < pe) {
+          const int64_t e = DIR ? (int64_t)__ldg(eid + p + j) : p + j;
+          v[j] = __ldg(x + e * F + h);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (p + j < pe) acc = __fadd_rn(acc, v[j]);
+    }
+    return acc;
+  };
+  int64_t row = r0;
+  while (row < r1) {
+    const int64_t rr = row + threadIdx.x;
+    const int64_t c = (threadIdx.x < ES_ROWS && rr < r1) ? chunks(rr) : 0;
+    // block inclusive scan of the chunk counts (saturated at slots + 1: only the batch cut matters)
+    int v = (int)(c > slots ? slots + 1 : c);
+    if (threadIdx.x < ES_ROWS) s_pre[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < ES_ROWS; off <<= 1) {
+      int add = 0;
+      if (threadIdx.x < ES_ROWS && threadIdx.x >= off) add = s_pre[threadIdx.x - off];
+      __syncthreads();
+      if (threadIdx.x < ES_ROWS) { v += add; s_pre[threadIdx.x] = v; }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      int k = 0;
+      const int lim = (int)((r1 - row) < ES_ROWS ? (r1 - row) : ES_ROWS);
+      while (k < lim && s_pre[k] <= slots) ++k;
+      s_cnt = k;
+    }
+    __syncthreads();
+    const int nb = s_cnt;
+    if (nb == 0) {
+      // one row with more chunks than a batch: windows of `slots` chunks, folded in order
+      const int64_t pb0 = ptr[row], pe0 = ptr[row + 1], nch = (pe0 - pb0 + C - 1) / C;
+      for (int64_t w0 = 0; w0 < nch; w0 += slots) {
+        const int wn = (int)(nch - w0 < slots ? nch - w0 : slots);
+        for (int u = grp; u < wn * ncb; u += ngroups) {
+          const int it = u / ncb, h = (u % ncb) * 32 + gl;
+          if (!lane_ok || h >= F) continue;
+          const int64_t pb = pb0 + (w0 + it) * C, pe = pb + C < pe0 ? pb + C : pe0;
+          es_part[it * F + h] = chunk_sum(pb, pe, h);
+        }
+        __syncthreads();
+        float* tot = es_part + (int64_t)slots * F;   // running totals of the row [F]
+        for (int h = threadIdx.x; h < F; h += ES_THREADS) {
+          float t = w0 == 0 ? es_part[h] : __fadd_rn(tot[h], es_part[h]);
+          for (int it = 1; it < wn; ++it) t = __fadd_rn(t, es_part[it * F + h]);
+          tot[h] = t;
+          if (w0 + wn == nch) out[row * F + h] = t;
+        }
+        __syncthreads();
+      }
+      row += 1;
+      continue;
+    }
+    const int nitems = s_pre[nb - 1];
+    // items of the batch: (row j, chunk k) with s_pre[j-1] <= item < s_pre[j]
+    for (int u = grp; u < nitems * ncb; u += ngroups) {
+      const int it = u / ncb, h = (u % ncb) * 32 + gl;
+      int a = 0, b = nb - 1;   // first j with s_pre[j] > it
+      while (a < b) {
+        const int m = (a + b) >> 1;
+        if (s_pre[m] > it) b = m; else a = m + 1;
+      }
+      const int j = a, k = it - (j ? s_pre[j - 1] : 0);
+      const int64_t r = row + j, pb0 = ptr[r], pe0 = ptr[r + 1];
+      const int64_t pb = pb0 + (int64_t)k * C, pe = pb + C < pe0 ? pb + C : pe0;
+      if (!lane_ok || h >= F) continue;
+      const float s = chunk_sum(pb, pe, h);
+      if (pe0 - pb0 <= C) out[r * F + h] = s;   // single-chunk row (also the empty row: 0)
+      else es_part[it * F + h] = s;
+    }
+    __syncthreads();
+    // fold the multi-chunk rows of the batch
+    for (int t = threadIdx.x; t < nb * F; t += ES_THREADS) {
+      const int j = t / F, h = t % F;
+      const int i0 = j ? s_pre[j - 1] : 0, i1 = s_pre[j];
+      if (i1 - i0 < 2) continue;
+      float tot = es_part[i0 * F + h];
+      for (int it = i0 + 1; it < i1; ++it) tot = __fadd_rn(tot, es_part[it * F + h]);
+      out[(row + j) * F + h] = tot;
+    }
+    __syncthreads();
+    row += nb;
   }
-  out[vl * cols + j] = __fmul_rn(cs.finish(e1 - b), *sX);
+}
+
+// ---------------------------------------------------------------------------- weighted SPMM ⑤ / ⑤′
+// out[v,j] = ((Σᶜ fmaf(w[e,h(j)], i2f(q_X[u_e,j]))) · s_X) [· row_scale[v]] over v's in-edges (dir 0, u_e =
+// source) or out-edges (dir 1, u_e = destination, weight w[out_eid[p]]), R14.  The
+// same edge-window blocks and chunk items as tango_edge_sum; a WARP sums one (item, 128-column pass): per
+// 32-edge batch the lanes load the batch's gather rows and weights in parallel into per-warp shared memory,
+// then every lane streams its 4 columns (one 32-bit word) of each gathered row, 8 rows in flight, fp32
+// fmaf in edge order.  Multi-chunk rows fold their chunk partials left to right after a barrier.
+constexpr int SW_COLS = 128;
+
+__host__ __device__ inline int sw_slots() { return 64; }
+
+template <int DIR, bool WORD>
+__global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int heads, int cols, int64_t epb, int64_t E,
+                                                           const float* __restrict__ w, const int8_t* __restrict__ qX,
+                                                           int64_t ldx, const float* __restrict__ sX,
+                                                           const float* __restrict__ rowscale, float* __restrict__ out,
+                                                           unsigned* amax_out) {
+  extern __shared__ __align__(16) float sw_dyn[];
+  float* part = sw_dyn;                                            // [slots][SW_COLS]
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* su = reinterpret_cast<int*>(part + sw_slots() * SW_COLS) + wid * 32 * (1 + heads);   // [32] rows
+  float* swt = reinterpret_cast<float*>(su + 32);                                           // [32][heads]
+  __shared__ int s_pre[ES_ROWS];
+  __shared__ int s_cnt;
+  const int64_t* __restrict__ ptr = DIR ? g.out_ptr : g.in_ptr;
+  const int32_t* __restrict__ nbr = DIR ? g.out_dst : g.in_src;
+  const int64_t n = g.n_local, C = g.chunk;
+  const int slots = sw_slots();
+  const int D = cols / heads, npass = (cols + SW_COLS - 1) / SW_COLS;
+  const float s = *sX;
+  float amax_loc = 0.0f;
+  auto lower = [&](int64_t key) {
+    int64_t a = 0, b = n;
+    while (a < b) {
+      const int64_t m = (a + b) >> 1;
+      if (ptr[m] < key) a = m + 1; else b = m;
+    }
+    return a;
+  };
+  const int64_t lo = (int64_t)blockIdx.x * epb, hi = lo + epb;
+  if (lo > E) return;
+  const int64_t r0 = lower(lo), r1 = hi > E ? n : lower(hi);
+  auto chunks = [&](int64_t r) -> int64_t {
+    const int64_t d = ptr[r + 1] - ptr[r];
+    return d <= C ? 1 : (d + C - 1) / C;
+  };
+  auto finish = [&](int64_t r, int j, float acc) {   // (Σᶜ)·s_X [· row_scale] -> out, amax
+    float v = __fmul_rn(acc, s);
+    if (rowscale) v = __fmul_rn(v, rowscale[r]);
+    out[r * cols + j] = v;
+    amax_loc = fmaxf(amax_loc, fabsf(v));
+  };
+  // chunk sum of list positions [pb, pe) for the lane's columns j0 .. j0+3 of pass cp -> acc[4]
+  auto chunk_sum = [&](int64_t pb, int64_t pe, int j0, float (&acc)[4]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c] = 0.0f;
+    int hc[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) hc[c] = (j0 + c < cols) ? (j0 + c) / D : 0;
+    for (int64_t b0 = pb; b0 < pe; b0 += 32) {
+      const int nb = (int)(pe - b0 < 32 ? pe - b0 : 32);
+      __syncwarp();
+      if (lane < nb) {
+        const int64_t p = b0 + lane;
+        const int64_t e = DIR ? (int64_t)g.out_eid[p] : p;
+        su[lane] = nbr[p];
+        for (int h = 0; h < heads; ++h) swt[lane * heads + h] = w[e * heads + h];
+      }
+      __syncwarp();
+      for (int i0 = 0; i0 < nb; i0 += 8) {
+        uint32_t word[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          word[i] = 0u;
+          if (i0 + i < nb) {
+            const int8_t* row = qX + (int64_t)su[i0 + i] * ldx;
+            if (WORD) {
+              if (j0 < cols) word[i] = __ldg(reinterpret_cast<const unsigned*>(row + j0));
+            } else {
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                if (j0 + c < cols) word[i] |= (uint32_t)(uint8_t)__ldg(row + j0 + c) << (8 * c);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i0 + i < nb) {
+            const float* wr = swt + (i0 + i) * heads;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              acc[c] = __fmaf_rn(wr[hc[c]], __int2float_rn((int)(int8_t)(word[i] >> (8 * c))), acc[c]);
+          }
+        }
+      }
+    }
+  };
+  int64_t row = r0;
+  while (row < r1) {
+    const int64_t rr = row + threadIdx.x;
+    const int64_t c = (threadIdx.x < ES_ROWS && rr < r1) ? chunks(rr) : 0;
+    int v = (int)(c > slots ? slots + 1 : c);
+    s_pre[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < ES_ROWS; off <<= 1) {
+      const int add = threadIdx.x >= off ? s_pre[threadIdx.x - off] : 0;
+      __syncthreads();
+      v += add;
+      s_pre[threadIdx.x] = v;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      int k = 0;
+      const int lim = (int)((r1 - row) < ES_ROWS ? (r1 - row) : ES_ROWS);
+      while (k < lim && s_pre[k] <= slots) ++k;
+      s_cnt = k;
+    }
+    __syncthreads();
+    const int nb = s_cnt;
+    if (nb == 0) {   // one row with more chunks than the partial slots: windows, folded in order
+      const int64_t pb0 = ptr[row], pe0 = ptr[row + 1], nch = (pe0 - pb0 + C - 1) / C;
+      for (int cp = 0; cp < npass; ++cp) {
+        float tot = 0.0f;   // thread t < SW_COLS: column cp*128 + t
+        for (int64_t w0 = 0; w0 < nch; w0 += slots) {
+          const int wn = (int)(nch - w0 < slots ? nch - w0 : slots);
+          for (int it = wid; it < wn; it += ES_THREADS / 32) {
+            const int64_t pb = pb0 + (w0 + it) * C, pe = pb + C < pe0 ? pb + C : pe0;
+            float acc[4];
+            chunk_sum(pb, pe, cp * SW_COLS + lane * 4, acc);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) part[it * SW_COLS + lane * 4 + q] = acc[q];
+          }
+          __syncthreads();
+          if (threadIdx.x < SW_COLS) {
+            for (int it = 0; it < wn; ++it)
+              tot = (w0 == 0 && it == 0) ? part[threadIdx.x] : __fadd_rn(tot, part[it * SW_COLS + threadIdx.x]);
+          }
+          __syncthreads();
+        }
+        const int j = cp * SW_COLS + threadIdx.x;
+        if (threadIdx.x < SW_COLS && j < cols) finish(row, j, tot);
+      }
+      row += 1;
+      continue;
+    }
+    const int nitems = s_pre[nb - 1];
+    for (int cp = 0; cp < npass; ++cp) {
+      for (int it = wid; it < nitems; it += ES_THREADS / 32) {
+        int a = 0, b = nb - 1;
+        while (a < b) {
+          const int m = (a + b) >> 1;
+          if (s_pre[m] > it) b = m; else a = m + 1;
+        }
+        const int j = a, k = it - (j ? s_pre[j - 1] : 0);
+        const int64_t r = row + j, pb0 = ptr[r], pe0 = ptr[r + 1];
+        const int64_t pb = pb0 + (int64_t)k * C, pe = pb + C < pe0 ? pb + C : pe0;
+        const int j0 = cp * SW_COLS + lane * 4;
+        float acc[4];
+        chunk_sum(pb, pe, j0, acc);
+        if (pe0 - pb0 <= C) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (j0 + q < cols) finish(r, j0 + q, acc[q]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) part[it * SW_COLS + lane * 4 + q] = acc[q];
+        }
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < nb * SW_COLS; t += ES_THREADS) {
+        const int jr = t / SW_COLS, col = cp * SW_COLS + t % SW_COLS;
+        const int i0 = jr ? s_pre[jr - 1] : 0, i1 = s_pre[jr];
+        if (i1 - i0 < 2 || col >= cols) continue;
+        float tot = part[i0 * SW_COLS + t % SW_COLS];
+        for (int it = i0 + 1; it < i1; ++it) tot = __fadd_rn(tot, part[it * SW_COLS + t % SW_COLS]);
+        finish(row + jr, col, tot);
+      }
+      __syncthreads();
+    }
+    row += nb;
+  }
+  if (amax_out) {
+    amax_loc = warp_max(amax_loc);
+    if (lane == 0) atomicMax(amax_out, __float_as_uint(amax_loc));
+  }
 }
 
 // Unweighted int32 SPMM (GCN; exact, order-free).  Warp per row, lanes over columns (coalesced rows).
@@ -206,17 +502,43 @@ cudaError_t launch_softmax_bwd(const GraphDev& g, int heads, const float* alpha,
   k_softmax_bwd<<<flat_grid(g.n_local * heads), 256, 0, st>>>(g, heads, alpha, dalpha, e_pre, slope, P, dEp);
   return cudaGetLastError();
 }
-cudaError_t launch_edge_sum(const GraphDev& g, int dir, int heads, const float* x, float* out, cudaStream_t st) {
+cudaError_t launch_edge_sum(const GraphDev& g, int dir, int heads, const float* x, float* out, int64_t e_list,
+                            cudaStream_t st) {
   if (g.n_local == 0) return cudaSuccess;
   ProfScope ps("edge_sum", st);
-  k_edge_sum<<<flat_grid(g.n_local * heads), 256, 0, st>>>(g, dir, heads, x, out);
+  // edges per block: about 8 blocks per SM, at least 256, at most 16 Ki edges
+  const int64_t e = e_list > 0 ? e_list : 1;
+  int64_t epb = e / ((int64_t)num_sms() * 8);
+  epb = epb < 256 ? 256 : (epb > 16384 ? 16384 : epb);
+  const int64_t blocks = e_list / epb + 1;   // list positions [0, e_list]: the last block owns rows starting at e_list
+  const size_t smem = (size_t)(es_slots(heads) + 1) * heads * 4;
+  if (smem > 48 * 1024) {
+    auto f = dir ? k_edge_sum_w<1> : k_edge_sum_w<0>;
+    const cudaError_t err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+  }
+  if (dir) k_edge_sum_w<1><<<(unsigned)blocks, ES_THREADS, smem, st>>>(g, heads, epb, e_list, x, out);
+  else k_edge_sum_w<0><<<(unsigned)blocks, ES_THREADS, smem, st>>>(g, heads, epb, e_list, x, out);
   return cudaGetLastError();
 }
 cudaError_t launch_spmm_w(const GraphDev& g, int dir, int heads, int cols, const float* w, const int8_t* qX,
-                          int64_t ldx, const float* sX, float* out, cudaStream_t st) {
+                          int64_t ldx, const float* sX, const float* rowscale, float* out, unsigned* amax_out,
+                          int64_t e_list, cudaStream_t st) {
   if (g.n_local == 0) return cudaSuccess;
   ProfScope ps("spmm_w", st);
-  k_spmm_w<<<flat_grid(g.n_local * cols), 256, 0, st>>>(g, dir, heads, cols, w, qX, ldx, sX, out);
+  const int64_t e = e_list > 0 ? e_list : 1;
+  int64_t epb = e / ((int64_t)num_sms() * 4);
+  epb = epb < 256 ? 256 : (epb > 16384 ? 16384 : epb);
+  const int64_t blocks = e_list / epb + 1;
+  const size_t smem = (size_t)sw_slots() * SW_COLS * 4 + (size_t)(ES_THREADS / 32) * 32 * (1 + heads) * 4;
+  const bool word = (ldx % 4 == 0) && ((uintptr_t)qX % 4 == 0);
+  auto f = dir ? (word ? k_spmm_w_fast<1, true> : k_spmm_w_fast<1, false>)
+               : (word ? k_spmm_w_fast<0, true> : k_spmm_w_fast<0, false>);
+  if (smem > 48 * 1024) {
+    const cudaError_t err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+  }
+  f<<<(unsigned)blocks, ES_THREADS, smem, st>>>(g, heads, cols, epb, e_list, w, qX, ldx, sX, rowscale, out, amax_out);
   return cudaGetLastError();
 }
 cudaError_t launch_spmm_sum(const GraphDev& g, int dir, int cols, const int8_t* qX, int64_t ldx, const float* sX,

@@ -189,6 +189,17 @@ cudaError_t launch_quantize(const float* x, int64_t rows, int64_t cols, const fl
   return cudaGetLastError();
 }
 
+// in place: the amax held (as float bits) in `slot` -> its scale s = amax/qmax (reading R1/R7); used when a
+// caller of tango_quantize gives no amax slot, so the scale word doubles as the amax scratch
+__global__ void k_amax_to_scale(float* slot, int bits) {
+  *slot = scale_from_amax(amax_load(reinterpret_cast<const unsigned*>(slot)), bits).s;
+}
+cudaError_t launch_amax_to_scale(float* slot, int bits, cudaStream_t st) {
+  ProfScope ps("amax_to_scale", st);
+  k_amax_to_scale<<<1, 1, 0, st>>>(slot, bits);
+  return cudaGetLastError();
+}
+
 }  // namespace tango
 
 // ================================================================== Error_X and bit selection (NEXT-2)

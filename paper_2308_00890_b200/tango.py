@@ -131,7 +131,7 @@ def load(path: str = LIB_PATH):
     L.tango_sddmm_q.argtypes = [PG, i32, PQ, PQ, i32, f32, _P, _P, _P, _P]
     L.tango_edge_softmax.argtypes = [PG, i32, _P, _P, _P, _P, _P]
     L.tango_softmax_bwd.argtypes = [PG, i32, _P, _P, _P, f32, _P, _P, _P]
-    L.tango_spmm_q.argtypes = [PG, i32, _P, PQ, i32, _P, _P, _P]
+    L.tango_spmm_q.argtypes = [PG, i32, _P, PQ, i32, _P, _P, _P, _P, _P]
     L.tango_edge_sum.argtypes = [PG, i32, i32, _P, _P, _P]
     L.tango_set_l2_fetch_granularity.argtypes = [i32, _P]
     L.tango_comm_set_options.argtypes = [_P, i32]
@@ -289,15 +289,15 @@ def qtensor(q, scale, rows, cols, bits=8):
 
 
 # ---------------------------------------------------------------------------------------- primitives
-def quantize(x, bits=8, seed=0, step=0, tag=0, global_row0=0, amax_hint=None, ld=None, status=None):
-    """tango_quantize: returns (q int8 [rows, ld], scale f32 (1,), amax f32 (1,))."""
+def quantize(x, bits=8, seed=0, step=0, tag=0, global_row0=0, amax_hint=None, ld=None, status=None, want_amax=True):
+    """tango_quantize: returns (q int8 [rows, ld], scale f32 (1,), amax f32 (1,) or None)."""
     L = load()
     x = x.contiguous()
     rows, cols = x.shape
     ld = ld if ld is not None else ld32(cols)
     q = torch.empty((rows, ld), dtype=torch.int8, device=x.device)
     s = torch.empty(1, dtype=torch.float32, device=x.device)
-    amax = torch.empty(1, dtype=torch.float32, device=x.device)
+    amax = torch.empty(1, dtype=torch.float32, device=x.device) if want_amax else None
     qt = QTensor(_ptr(q), _ptr(s), rows, cols, ld, bits)
     _check(L.tango_quantize(_ptr(x), rows, cols, global_row0, _ptr(amax_hint), Rng(seed, step, tag), C.byref(qt),
                             _ptr(amax), _ptr(status), _stream()), "tango_quantize")
@@ -368,19 +368,22 @@ def softmax_bwd(graph: DeviceGraph, heads, alpha, dalpha, e_pre, slope):
     return P, dEp
 
 
-def spmm(graph: DeviceGraph, direction, qX, sX, cols, heads, edge_w=None):
+def spmm(graph: DeviceGraph, direction, qX, sX, cols, heads, edge_w=None, row_scale=None, amax_out=None,
+         out=None):
+    """tango_spmm_q: weighted (edge_w [E][heads] fp32, Σᶜ fmaf) or unweighted (exact int32) aggregation of
+    int8 rows; optional per-row scale and amax(|out|) (amax_out is raised, not reset)."""
     L = load()
     x = QTensor(_ptr(qX), _ptr(sX), qX.shape[0], cols, qX.shape[1], 8)
-    out = torch.empty((graph.n_local, cols), dtype=torch.float32, device="cuda")
+    out = out if out is not None else torch.empty((graph.n_local, cols), dtype=torch.float32, device="cuda")
     oi = None if edge_w is not None else torch.empty((graph.n_local, cols), dtype=torch.int32, device="cuda")
-    _check(L.tango_spmm_q(graph.ref(), direction, _ptr(edge_w), C.byref(x), heads, _ptr(out), _ptr(oi), _stream()),
-           "tango_spmm_q")
+    _check(L.tango_spmm_q(graph.ref(), direction, _ptr(edge_w), C.byref(x), heads, _ptr(row_scale), _ptr(out),
+                          _ptr(oi), _ptr(amax_out), _stream()), "tango_spmm_q")
     return out, oi
 
 
-def edge_sum(graph: DeviceGraph, direction, heads, x):
+def edge_sum(graph: DeviceGraph, direction, heads, x, out=None):
     L = load()
-    out = torch.empty((graph.n_local, heads), dtype=torch.float32, device="cuda")
+    out = out if out is not None else torch.empty((graph.n_local, heads), dtype=torch.float32, device="cuda")
     _check(L.tango_edge_sum(graph.ref(), direction, heads, _ptr(x.contiguous()), _ptr(out), _stream()),
            "tango_edge_sum")
     return out

@@ -169,3 +169,81 @@ def test_sparse_primitives_parity(T, orc, spec, chunk):
     for direction in (0, 1):
         s = T.edge_sum(dg, direction, H, dEp)
         assert np.array_equal(s.cpu().numpy(), orc.edge_sum(gr, direction, H, odEp, chunk=chunk))
+
+
+# Incidence SPMM ③′/③″ at the paper's edge-feature widths 4-20, plus widths
+# past one warp (33, 300) and chunk sizes that cut hub rows into many canonical chunks; C_E = 1 with F = 300
+# (13 partial slots per batch) forces the window-by-window fold of a row with more chunks than a batch.
+ES_GRAPHS = [("toy", None), ("noself", (200, 500, 3)), ("hub", None)]
+
+
+def _es_graph(name):
+    if name == "hub":   # power-law with hub rows of several hundred edges, plus empty rows
+        return inputs.chung_lu_graph(3000, 40000, 2.1, seed=11, dmax=900, self_loops=False)
+    return make_graph((name, dict(ES_GRAPHS)[name]))
+
+
+@pytest.mark.parametrize("name", [g[0] for g in ES_GRAPHS])
+@pytest.mark.parametrize("F,chunk", [(4, 256), (7, 3), (12, 64), (16, 256), (16, 5), (20, 256), (33, 7),
+                                     (300, 1), (300, 256)])
+def test_edge_sum_parity(T, orc, name, F, chunk):
+    gr = _es_graph(name)
+    dg = T.DeviceGraph(gr, chunk=chunk)
+    x = np.random.default_rng(F * 1000 + chunk).standard_normal((gr.e, F)).astype(np.float32)
+    xd = cu(x)
+    for direction in (0, 1):
+        s = T.edge_sum(dg, direction, F, xd)
+        assert np.array_equal(s.cpu().numpy(), orc.edge_sum(gr, direction, F, x, chunk=chunk)), (direction, F, chunk)
+
+
+# Weighted SPMM ⑤ / ⑤′ as a standalone primitive (tango_spmm_q with edge weights):
+# multi-head shapes of P:1186-1189, ragged column passes, D not a multiple of 4, byte-strided rows (ld % 4 != 0),
+# plus the optional per-row scale and amax(|out|) of §8(b).
+@pytest.mark.parametrize("name", ["noself", "hub"])
+@pytest.mark.parametrize("H,D,ld,chunk", [(4, 128, 512, 256), (2, 48, 96, 7), (2, 300, 608, 64), (1, 37, 37, 3),
+                                          (3, 5, 16, 256), (2, 128, 256, 1)])
+def test_spmm_weighted_parity(T, orc, name, H, D, ld, chunk):
+    gr = _es_graph(name)
+    dg = T.DeviceGraph(gr, chunk=chunk)
+    rng = np.random.default_rng(H * 100 + D)
+    cols = H * D
+    qX = _rand_i8(rng, (gr.n, ld))
+    sX = np.float32(0.0173)
+    w = rng.random((gr.e, H)).astype(np.float32)
+    rs = rng.random(gr.n).astype(np.float32) + np.float32(0.5)
+    for direction in (0, 1):
+        ref = orc.spmm_alpha(gr, direction, H, cols, w, orc.qref(q=qX[:, :cols], s=sX), chunk=chunk)
+        out, _ = T.spmm(dg, direction, cu(qX), cu(np.array([sX])), cols, H, edge_w=cu(w))
+        assert np.array_equal(out.cpu().numpy(), ref), direction
+        amax = torch.zeros(1, device="cuda")
+        out2, _ = T.spmm(dg, direction, cu(qX), cu(np.array([sX])), cols, H, edge_w=cu(w), row_scale=cu(rs),
+                         amax_out=amax)
+        ref2 = ref * rs[:, None]            # one more fp32 rn multiply per element
+        assert np.array_equal(out2.cpu().numpy(), ref2), direction
+        assert amax.item() == np.abs(ref2).max()
+
+
+def test_spmm_unweighted_rowscale_amax(T, orc):
+    gr = _es_graph("hub")
+    dg = T.DeviceGraph(gr)
+    rng = np.random.default_rng(5)
+    cols = 64
+    qX = _rand_i8(rng, (gr.n, cols))
+    sX = np.float32(0.02)
+    rs = rng.random(gr.n).astype(np.float32)
+    for direction in (0, 1):
+        ri, rf = orc.spmm_sum(gr, direction, cols, orc.qref(q=qX, s=sX))
+        amax = torch.zeros(1, device="cuda")
+        out, oi = T.spmm(dg, direction, cu(qX), cu(np.array([sX])), cols, 1, row_scale=cu(rs), amax_out=amax)
+        assert np.array_equal(oi.cpu().numpy(), ri)
+        ref = rf * rs[:, None]
+        assert np.array_equal(out.cpu().numpy(), ref)
+        assert amax.item() == np.abs(ref).max()
+
+
+def test_quantize_without_amax_slot(T, orc):
+    """tango_quantize with amax_out = NULL: the scale word doubles as the amax scratch (no allocation)."""
+    x = inputs.features(333, 100, seed=9)
+    q, s, _ = T.quantize(cu(x), bits=8, ld=128, want_amax=False)
+    oq, os_, _ = orc.quantize(x, bits=8)
+    assert np.array_equal(q.cpu().numpy()[:, :100], oq) and s.item() == os_
