@@ -681,6 +681,12 @@ G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_p
   a.da_part = (float*)(c + L.off_dapart);
   a.nrec = (float*)(c + L.off_nrec); a.nrs = gat2_nrec_stride(p->heads);
   a.in2out = (const int32_t*)(c + L.off_dal);
+  // P2's ∂α in in-CSR order: scattered by P1 (default) or gathered by P2 through the in2out map
+  static const int scatter = [] {
+    const char* e = getenv("TANGO_P2_GATHER");
+    return (e && atoi(e)) ? 0 : 1;
+  }();
+  a.scatter_in = scatter;
   a.codes_biased = 1;
   return a;
 }

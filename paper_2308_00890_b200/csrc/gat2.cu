@@ -442,7 +442,9 @@ __device__ __forceinline__ void g8_fill(uint32_t ring_lane, const int8_t* lane_b
     const int iv[GR] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
     const uint32_t s0 = ring_lane + (uint32_t)(g & 1) * (GR * 32 * VPL);
 #pragma unroll
-    for (int j = 0; j < GR; ++j) cp_slice_hint<VPL>(s0 + j * 32 * VPL, lane_base + (uint32_t)iv[j] * ld, pol);
+    for (int j = 0; j < GR; ++j)   // base + row * ld as one 32 x 32 -> 64-bit IMAD.WIDE.U32
+      cp_slice_hint<VPL>(s0 + j * 32 * VPL,
+                         reinterpret_cast<const int8_t*>((uint64_t)lane_base + (uint64_t)(uint32_t)iv[j] * ld), pol);
   }
   cp_commit();
 }
@@ -812,6 +814,7 @@ __global__ void __launch_bounds__(256, 3) k2_fagg_seg(const G2Args a) {
     for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
     PieceFold<VPL> pf;
     pf.nfold = 0;
+    int nextf = C;   // next chunk boundary of the piece (FAST form: group starts only)
     for (int c = 0; c < nch; ++c) {
       const int u2 = edge_u(c + 2);
       int8_t qs1[H];
@@ -827,7 +830,10 @@ __global__ void __launch_bounds__(256, 3) k2_fagg_seg(const G2Args a) {
         const float4 b4 = *reinterpret_cast<const float4*>(sac + i0 + 4);
         const float al[GR] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
         if (fast) {
-          if (t0 > 0 && t0 % C == 0) pf.fold(acc);
+          if (t0 == nextf) {
+            pf.fold(acc);
+            nextf += C;
+          }
 #pragma unroll
           for (int j = 0; j < GR; ++j) {
             const Row<VPL> rj = lds_row_slice<VPL>(s0 + j * 32 * VPL);
@@ -1097,6 +1103,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
 #pragma unroll
         for (int h = 0; h < H; ++h) o[h] = sd[h * 32 + lane];
         st_h<H>(a.dal_out + (int64_t)seo[b * 32 + lane] * H, o);
+        if (a.scatter_in) st_h<H>(a.dal_in + (int64_t)__ldcs(a.g.out_eid + seo[b * 32 + lane]) * H, o);
 
       }
       __syncwarp();
@@ -1225,6 +1232,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
     for (int k = 0; k < VPL / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
     PieceFold<VPL> pf;
     pf.nfold = 0;
+    int nextf = C;   // next chunk boundary of the piece (FAST form: group starts only)
     for (int c = 0; c < nch; ++c) {
       const int v2 = edge_v(c + 2);
       DstSm<H> d1;
@@ -1240,7 +1248,10 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
         const float4 b4 = *reinterpret_cast<const float4*>(sac + i0 + 4);
         const float al[GR] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
         int dd[GR];
-        if (fast && t0 > 0 && t0 % C == 0) pf.fold(acc);
+        if (fast && t0 == nextf) {
+          pf.fold(acc);
+          nextf += C;
+        }
 #pragma unroll
         for (int j = 0; j < GR; ++j) {
           if (!fast && t0 + j > 0 && t0 + j < T && (t0 + j) % C == 0) pf.fold(acc);
@@ -1272,6 +1283,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
         } else {
           st_h<H>(a.dal_out + (eb + c * 32 + lane) * H, o);
         }
+        if (a.scatter_in) st_h<H>(a.dal_in + (int64_t)__ldcs(a.g.out_eid + eb + c * 32 + lane) * H, o);
       }
       __syncwarp();
       if (c + 1 < nch) {
@@ -1325,8 +1337,12 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
           [&](int64_t e) {
             EdgeIn<H> l;
             load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs);
-            ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, l.da);
-            st_h<H>(a.dal_in + e * H, l.da);   // ∂α in in-CSR order for P2b (coalesced)
+            if (a.scatter_in) {
+              ld_h<H>(a.dal_in + e * H, l.da);   // scattered into in-CSR order by P1
+            } else {
+              ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, l.da);
+              st_h<H>(a.dal_in + e * H, l.da);   // ∂α in in-CSR order for P2b (coalesced)
+            }
             return l;
           },
           [&](const EdgeIn<H>& l, float (&x)[H], float (&y)[H]) {
@@ -1370,7 +1386,8 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
       if (pos < t.T) {
         int8_t qs[H];
         load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, qs);
-        ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, da);
+        if (a.scatter_in) ld_h<H>(a.dal_in + e * H, da);
+        else ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, da);
         alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
       }
     };

@@ -94,12 +94,13 @@ __global__ void k_softmax_bwd(GraphDev g, int heads, const float* alpha, const f
 // out-edges (dir 1, records out_eid[p]: a gather of F-float rows), reading R14.
 // Edge-window blocks: block b owns the rows whose edge list starts in [b·EPB, (b+1)·EPB) (a binary
 // search of the CSR pointer, no plan); its rows are cut into canonical chunks ("items", ≤ C_E edges).  A
-// group of GW = min(F, 32) lanes sums one (item, 32-column block) sequentially — F consecutive floats per
-// edge, so a group's load is one contiguous 4F-byte run; a row with one chunk is written directly, a hub
-// row's chunk partials go to shared memory and are folded left to right (total = p_0, total += p_c)
-// after a barrier.  Rows are taken in batches of at most ES_ROWS rows and ES_SLOTS(F) items; a row with
-// more chunks than one batch holds is folded window by window (the running total kept in registers of
-// the folding threads — the same left-to-right order).
+// group of GW = ceil(F / VW) lanes sums one item sequentially, each lane VW consecutive columns (float4 /
+// float2 / float loads), so a group's load of one edge record is one contiguous 4F-byte run; 16 floats
+// per lane are in flight (16 / VW records) and the blocks run at 4 per SM (32 warps).  A
+// row with one chunk is written directly, a hub row's chunk partials go to shared memory and are folded
+// left to right (total = p_0, total += p_c) after a barrier.  Rows are taken in batches of at most
+// ES_ROWS rows and es_slots(F) items; a row with more chunks than one batch holds is folded window by
+// window (running totals in shared memory — the same left-to-right order).
 constexpr int ES_THREADS = 256, ES_ROWS = 256;
 
 __host__ __device__ inline int es_slots(int F) {
@@ -107,18 +108,33 @@ __host__ __device__ inline int es_slots(int F) {
   return s > 1024 ? 1024 : (s < 8 ? 8 : s);
 }
 
-template <int DIR>
-__global__ void __launch_bounds__(ES_THREADS) k_edge_sum_w(GraphDev g, int F, int64_t epb, int64_t E,
+template <int VW> struct VecF;
+template <> struct VecF<1> { using T = float; };
+template <> struct VecF<2> { using T = float2; };
+template <> struct VecF<4> { using T = float4; };
+template <int VW>
+__device__ __forceinline__ void vadd(float (&acc)[VW], const typename VecF<VW>::T& v) {
+  if constexpr (VW == 1) {
+    acc[0] = __fadd_rn(acc[0], v);
+  } else if constexpr (VW == 2) {
+    acc[0] = __fadd_rn(acc[0], v.x); acc[1] = __fadd_rn(acc[1], v.y);
+  } else {
+    acc[0] = __fadd_rn(acc[0], v.x); acc[1] = __fadd_rn(acc[1], v.y);
+    acc[2] = __fadd_rn(acc[2], v.z); acc[3] = __fadd_rn(acc[3], v.w);
+  }
+}
+
+template <int DIR, int VW>
+__global__ void __launch_bounds__(ES_THREADS, 4) k_edge_sum_w(GraphDev g, int F, int64_t epb, int64_t E,
                                                           const float* __restrict__ x, float* __restrict__ out) {
+  using V = typename VecF<VW>::T;
   extern __shared__ __align__(16) float es_part[];               // [slots + 1][F]
   __shared__ int s_pre[ES_ROWS];                                 // inclusive prefix of chunk counts
-  __shared__ int s_cnt;
   const int64_t* __restrict__ ptr = DIR ? g.out_ptr : g.in_ptr;
   const int32_t* __restrict__ eid = g.out_eid;
   const int64_t n = g.n_local, C = g.chunk;
   const int slots = es_slots(F);
-  // rows of this block: starts in [lo, hi)
-  auto lower = [&](int64_t key) {   // first row r in [0, n] with ptr[r] >= key (ptr[n] = E)
+  auto lower = [&](int64_t key) {   // first row r in [0, n] with ptr[r] >= key
     int64_t a = 0, b = n;
     while (a < b) {
       const int64_t m = (a + b) >> 1;
@@ -127,72 +143,74 @@ __global__ void __launch_bounds__(ES_THREADS) k_edge_sum_w(GraphDev g, int F, in
     return a;
   };
   const int64_t lo = (int64_t)blockIdx.x * epb, hi = lo + epb;
-  int64_t r0 = lower(lo), r1 = (hi > E) ? n : lower(hi);
   if (lo > E) return;
-  if (hi > E) r1 = n;   // the last block also owns the trailing rows that start at E
-  const int GW = F < 32 ? F : 32, GPW = 32 / GW, ncb = (F + 31) / 32;
+  const int64_t r0 = lower(lo), r1 = hi > E ? n : lower(hi);
+  const int nv = (F + VW - 1) / VW;                 // vectors per record
+  const int GW = nv < 32 ? nv : 32, GPW = 32 / GW, ncb = (nv + 31) / 32;
   const int lane = threadIdx.x & 31, grp = (threadIdx.x >> 5) * GPW + lane / GW, gl = lane % GW;
   const bool lane_ok = lane / GW < GPW;
   const int ngroups = (ES_THREADS / 32) * GPW;
+  const V* __restrict__ xv = reinterpret_cast<const V*>(x);
   auto chunks = [&](int64_t r) -> int64_t {
     const int64_t d = ptr[r + 1] - ptr[r];
     return d <= C ? 1 : (d + C - 1) / C;
   };
-  // sequential sum of list positions [pb, pe) of column h (pe - pb <= C)
-  auto chunk_sum = [&](int64_t pb, int64_t pe, int h) -> float {
-    float acc = 0.0f;
-    for (int64_t p = pb; p < pe; p += 8) {
-      float v[8];
+  // sequential sum of list positions [pb, pe) (pe - pb <= C) for the lane's vector vi (columns VW·vi ..):
+  // 16 floats per lane in flight (U = 16 / VW records), then added in order
+  auto chunk_sum = [&](int64_t pb, int64_t pe, int vi, float (&acc)[VW]) {
+    constexpr int U = 16 / VW;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        v[j] = 0.0f;
+    for (int k = 0; k < VW; ++k) acc[k] = 0.0f;
+    for (int64_t p = pb; p < pe; p += U) {
+      V v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
         if (p + j < pe) {
           const int64_t e = DIR ? (int64_t)__ldg(eid + p + j) : p + j;
-          v[j] = __ldg(x + e * F + h);
+          v[j] = __ldg(xv + e * nv + vi);
         }
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (p + j < pe) acc = __fadd_rn(acc, v[j]);
+      for (int j = 0; j < U; ++j)
+        if (p + j < pe) vadd<VW>(acc, v[j]);
     }
-    return acc;
+  };
+  auto put = [&](float* dst, int vi, const float (&acc)[VW]) {   // columns VW·vi .. of one row (F floats)
+#pragma unroll
+    for (int k = 0; k < VW; ++k)
+      if (vi * VW + k < F) dst[vi * VW + k] = acc[k];
   };
   int64_t row = r0;
   while (row < r1) {
     const int64_t rr = row + threadIdx.x;
     const int64_t c = (threadIdx.x < ES_ROWS && rr < r1) ? chunks(rr) : 0;
-    // block inclusive scan of the chunk counts (saturated at slots + 1: only the batch cut matters)
-    int v = (int)(c > slots ? slots + 1 : c);
-    if (threadIdx.x < ES_ROWS) s_pre[threadIdx.x] = v;
+    int v = (int)(c > slots ? slots + 1 : c);   // saturated: only the batch cut matters
+    s_pre[threadIdx.x] = v;
     __syncthreads();
     for (int off = 1; off < ES_ROWS; off <<= 1) {
-      int add = 0;
-      if (threadIdx.x < ES_ROWS && threadIdx.x >= off) add = s_pre[threadIdx.x - off];
+      const int add = threadIdx.x >= off ? s_pre[threadIdx.x - off] : 0;
       __syncthreads();
-      if (threadIdx.x < ES_ROWS) { v += add; s_pre[threadIdx.x] = v; }
+      v += add;
+      s_pre[threadIdx.x] = v;
       __syncthreads();
     }
-    if (threadIdx.x == 0) {
-      int k = 0;
-      const int lim = (int)((r1 - row) < ES_ROWS ? (r1 - row) : ES_ROWS);
-      while (k < lim && s_pre[k] <= slots) ++k;
-      s_cnt = k;
-    }
-    __syncthreads();
-    const int nb = s_cnt;
+    // rows of the batch: the prefix is non-decreasing, so the cut is a count
+    const int nb = __syncthreads_count(rr < r1 && v <= slots);
     if (nb == 0) {
       // one row with more chunks than a batch: windows of `slots` chunks, folded in order
       const int64_t pb0 = ptr[row], pe0 = ptr[row + 1], nch = (pe0 - pb0 + C - 1) / C;
+      float* tot = es_part + (int64_t)slots * F;   // running totals of the row [F]
       for (int64_t w0 = 0; w0 < nch; w0 += slots) {
         const int wn = (int)(nch - w0 < slots ? nch - w0 : slots);
         for (int u = grp; u < wn * ncb; u += ngroups) {
-          const int it = u / ncb, h = (u % ncb) * 32 + gl;
-          if (!lane_ok || h >= F) continue;
+          const int it = u / ncb, vi = (u % ncb) * 32 + gl;
+          if (!lane_ok || vi >= nv) continue;
           const int64_t pb = pb0 + (w0 + it) * C, pe = pb + C < pe0 ? pb + C : pe0;
-          es_part[it * F + h] = chunk_sum(pb, pe, h);
+          float acc[VW];
+          chunk_sum(pb, pe, vi, acc);
+          put(es_part + it * F, vi, acc);
         }
         __syncthreads();
-        float* tot = es_part + (int64_t)slots * F;   // running totals of the row [F]
         for (int h = threadIdx.x; h < F; h += ES_THREADS) {
           float t = w0 == 0 ? es_part[h] : __fadd_rn(tot[h], es_part[h]);
           for (int it = 1; it < wn; ++it) t = __fadd_rn(t, es_part[it * F + h]);
@@ -205,9 +223,8 @@ __global__ void __launch_bounds__(ES_THREADS) k_edge_sum_w(GraphDev g, int F, in
       continue;
     }
     const int nitems = s_pre[nb - 1];
-    // items of the batch: (row j, chunk k) with s_pre[j-1] <= item < s_pre[j]
     for (int u = grp; u < nitems * ncb; u += ngroups) {
-      const int it = u / ncb, h = (u % ncb) * 32 + gl;
+      const int it = u / ncb, vi = (u % ncb) * 32 + gl;
       int a = 0, b = nb - 1;   // first j with s_pre[j] > it
       while (a < b) {
         const int m = (a + b) >> 1;
@@ -216,10 +233,10 @@ __global__ void __launch_bounds__(ES_THREADS) k_edge_sum_w(GraphDev g, int F, in
       const int j = a, k = it - (j ? s_pre[j - 1] : 0);
       const int64_t r = row + j, pb0 = ptr[r], pe0 = ptr[r + 1];
       const int64_t pb = pb0 + (int64_t)k * C, pe = pb + C < pe0 ? pb + C : pe0;
-      if (!lane_ok || h >= F) continue;
-      const float s = chunk_sum(pb, pe, h);
-      if (pe0 - pb0 <= C) out[r * F + h] = s;   // single-chunk row (also the empty row: 0)
-      else es_part[it * F + h] = s;
+      if (!lane_ok || vi >= nv) continue;
+      float acc[VW];
+      chunk_sum(pb, pe, vi, acc);
+      put(pe0 - pb0 <= C ? out + r * F : es_part + it * F, vi, acc);   // single-chunk row: direct
     }
     __syncthreads();
     // fold the multi-chunk rows of the batch
@@ -512,13 +529,16 @@ cudaError_t launch_edge_sum(const GraphDev& g, int dir, int heads, const float* 
   epb = epb < 256 ? 256 : (epb > 16384 ? 16384 : epb);
   const int64_t blocks = e_list / epb + 1;   // list positions [0, e_list]: the last block owns rows starting at e_list
   const size_t smem = (size_t)(es_slots(heads) + 1) * heads * 4;
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(x);
+  const int vw = (heads % 4 == 0 && xa % 16 == 0) ? 4 : (heads % 2 == 0 && xa % 8 == 0) ? 2 : 1;
+  void (*f)(GraphDev, int, int64_t, int64_t, const float*, float*) =
+      dir ? (vw == 4 ? k_edge_sum_w<1, 4> : vw == 2 ? k_edge_sum_w<1, 2> : k_edge_sum_w<1, 1>)
+          : (vw == 4 ? k_edge_sum_w<0, 4> : vw == 2 ? k_edge_sum_w<0, 2> : k_edge_sum_w<0, 1>);
   if (smem > 48 * 1024) {
-    auto f = dir ? k_edge_sum_w<1> : k_edge_sum_w<0>;
     const cudaError_t err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
   }
-  if (dir) k_edge_sum_w<1><<<(unsigned)blocks, ES_THREADS, smem, st>>>(g, heads, epb, e_list, x, out);
-  else k_edge_sum_w<0><<<(unsigned)blocks, ES_THREADS, smem, st>>>(g, heads, epb, e_list, x, out);
+  f<<<(unsigned)blocks, ES_THREADS, smem, st>>>(g, heads, epb, e_list, x, out);
   return cudaGetLastError();
 }
 cudaError_t launch_spmm_w(const GraphDev& g, int dir, int heads, int cols, const float* w, const int8_t* qX,

@@ -76,6 +76,46 @@ __global__ void __launch_bounds__(256) k_quantize(const float* __restrict__ x, i
                        ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && ((reinterpret_cast<uintptr_t>(q) & 7) == 0);
   const bool fast = aligned && ((cols & 7) == 0);
   const bool dense = ld == cols;   // q[i*ld + j] = q[e]: no division in the fast loop
+  const bool aligned_x = (rowscale == nullptr) && (qt == nullptr) && ((g0 & 7) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  if (aligned_x && !dense && (cols & 7) != 0) {
+    // padded output rows whose width is not a multiple of 8 (e.g. F = 602 -> ld 608): stream x as one flat
+    // run of 8-element groups (the same Philox groups) and scatter each group's codes to (i, j); the row
+    // coordinates of the thread's group advance by a fixed (si, sj) per grid stride, no division in the loop
+    const int64_t full1 = blk0 + (count >> 3);
+    const int64_t e0 = tid << 3, stride = nthr << 3;
+    int64_t ci = e0 / cols, cj = e0 - ci * cols;
+    const int64_t si = stride / cols, sj = stride - si * cols;
+    for (int64_t blk = blk0 + tid; blk < full1; blk += nthr) {
+      const int64_t e = (blk << 3) - g0;
+      const float4* src = reinterpret_cast<const float4*>(x + e);
+      const float4 a = __ldcs(src), b = __ldcs(src + 1);
+      const SR8 rnd = sr_draw8((uint64_t)blk, tag, step, key);
+      const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint2 pk = sr_quant8(v, sc.r, rnd, qmax);
+      pk.x ^= code_xor; pk.y ^= code_xor;
+      const uint32_t w2[2] = {pk.x, pk.y};
+      int64_t i = ci, j = cj;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (j == cols) { j = 0; ++i; }
+        q[i * ld + j] = (int8_t)(w2[k >> 2] >> (8 * (k & 3)));
+        ++j;
+      }
+      cj += sj; ci += si;
+      if (cj >= cols) { cj -= cols; ++ci; }
+    }
+    if ((count & 7) && tid == nthr - 1) {   // the partial last group, element by element
+      const SR8 rnd = sr_draw8((uint64_t)full1, tag, step, key);
+      for (int k = 0; k < (int)(count & 7); ++k) {
+        const int64_t e = ((full1 << 3) - g0) + k;
+        const int64_t i = e / cols, j = e - i * cols;
+        const int qq = sr_quant(x[e], sc.r, sr_half(rnd, k), qmax);
+        q[i * ld + j] = (int8_t)(qq ^ (int)(code_xor & 0xFFu));
+      }
+    }
+    return;
+  }
   if (aligned && dense) {
     // streaming path over the whole groups (any cols: the tensor is one flat run of codes); the
     // next group's 32 bytes are loaded before this one is rounded.  A partial last group (count

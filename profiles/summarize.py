@@ -33,17 +33,14 @@ def launches(path, tag):
                 u = d["Metric Unit"]
                 us = v / 1000 if u == "ns" else (v * 1000 if u == "ms" else v)
                 out.append((re.sub(r"\(.*", "", d["Kernel Name"]).replace("void ", "").replace("tango::", ""), us))
-    # the last step = everything after the last L2-flush fill kernel that precedes a quantize of H
-    # (simple and robust: take the launches after the midpoint of the list's library kernels)
-    # the extras bench.py runs after the layer step (train step, sddmm_bits) are not part of it
-    for i, (n, _) in enumerate(out):
-        if n.startswith(("k_sddmm_dot_e", "k_sddmm_add_e", "k_quantize_pack4", "k_sgemm", "k_out_")):
-            out = out[:i]
-            break
-    lib = [i for i, (n, _) in enumerate(out) if n.startswith("k_")]
-    first_gemm = [i for i in lib if out[i][0].startswith("k_gemm_i8<0")]
-    start = first_gemm[-1] - 3 if len(first_gemm) >= 2 else 0
-    step = [x for x in out[start:] if x[0].startswith("k_")]
+    # one layer step = the library launches from a step's Q(W) absmax to its ∂W finalize (k_finalize_dw, the
+    # last launch of the backward); take the last complete step (the GEMM microbenchmarks and other extras
+    # bench.py runs afterwards have no finalize)
+    ends = [i for i, (n, _) in enumerate(out) if n.startswith("k_finalize_dw")]
+    if len(ends) >= 2:
+        step = [x for x in out[ends[-2] + 1:ends[-1] + 1] if x[0].startswith(("k_", "k2_"))]
+    else:
+        step = [x for x in out if x[0].startswith(("k_", "k2_"))]
     agg = OrderedDict()
     for n, us in step:
         a = agg.setdefault(n, [0.0, 0])
@@ -51,8 +48,8 @@ def launches(path, tag):
         a[1] += 1
     tot = sum(v[0] for v in agg.values())
     lines = [f"# {tag} ncu launch list (gpu__time_duration.sum, --clock-control none, cold-cache serialised)", "",
-             f"Source: `{os.path.basename(path)}` — one step (the last) of `bench.py --steps 2 --warmup 3` "
-             "(arxiv-shaped GAT layer fwd+bwd); bench.py's L2-flush fills excluded.", "",
+             f"Source: `{os.path.basename(path)}` — the last complete layer step (fwd+bwd, Q(W) .. ∂W finalize) of "
+             "a `bench.py --layer-only` run under ncu; bench.py's L2-flush fills excluded.", "",
              "| kernel | us / step | launches | share |", "|---|---|---|---|"]
     for n, (us, c) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
         lines.append(f"| {n} | {us:.1f} | {c} | {100 * us / tot:.1f}% |")

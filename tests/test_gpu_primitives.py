@@ -236,7 +236,7 @@ def test_spmm_unweighted_rowscale_amax(T, orc):
         amax = torch.zeros(1, device="cuda")
         out, oi = T.spmm(dg, direction, cu(qX), cu(np.array([sX])), cols, 1, row_scale=cu(rs), amax_out=amax)
         assert np.array_equal(oi.cpu().numpy(), ri)
-        ref = rf * rs[:, None]
+        ref = (rf * sX) * rs[:, None]       # orc_spmm_sum's float output is (float)Σ, before the scale
         assert np.array_equal(out.cpu().numpy(), ref)
         assert amax.item() == np.abs(ref).max()
 

@@ -10,11 +10,11 @@ import os
 import subprocess
 import sys
 
-PASS_OF = {"k2_fagg": "gat_fwd_agg", "k2_bsrc1": "gat_bwd_src", "k2_bdst_a": "gat_bwd_dst", "k2_bdst_b": "gat_bwd_dst",
+PASS_OF = {"k2_fagg": "gat_fwd_agg", "k2_fagg_seg": "gat_fwd_agg", "k2_bsrc1": "gat_bwd_src", "k2_bsrc1_seg": "gat_bwd_src", "k2_bdst_a": "gat_bwd_dst", "k2_bdst_b": "gat_bwd_dst",
            "k2_bsrc2": "gat_bwd_src2", "k2_fstats1": "gat_fwd_stats", "k2_fstats2": "gat_fwd_stats",
            "k_quantize": "quantize"}
-METRICS = "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum"
-UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+METRICS = "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors.sum"
+UNIT = {"sector": 32, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def main(rep, workload, tag=None):
@@ -32,7 +32,7 @@ def main(rep, workload, tag=None):
             continue
         a = acc.setdefault(p, {"dram": 0.0, "l2": 0.0, "launches": 0, "kernels": set()})
         a["dram"] += sum(float(d[m]) * UNIT[u[m]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-        a["l2"] += float(d["lts__t_bytes.sum"]) * UNIT[u["lts__t_bytes.sum"]]
+        a["l2"] += float(d["lts__t_sectors.sum"]) * 32.0   # sectors of 32 B
         a["launches"] += 1
         a["kernels"].add(kname)
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
