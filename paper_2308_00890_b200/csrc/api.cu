@@ -687,6 +687,11 @@ G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_p
     return (e && atoi(e)) ? 0 : 1;
   }();
   a.scatter_in = scatter;
+  static const int staged = [] {
+    const char* e = getenv("TANGO_HUB_STAGED");
+    return (e && atoi(e)) ? 1 : 0;
+  }();
+  a.lane_hubs = !staged;
   a.codes_biased = 1;
   return a;
 }

@@ -292,8 +292,8 @@ __global__ void __launch_bounds__(256, 4) k2_fstats2(const G2Args a) {
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t n = a.g.n_local, hc = load_count(a.pin.counts), nitems = hc + load_count(a.pin.counts + 2);
-  FOR_ITEMS(item, a.work + 3, nitems) {
-    if (item < hc) {   // ---- hub segment
+  FOR_ITEMS_FROM(item, a.work + 3, a.lane_hubs ? hc : 0, nitems) {
+    if (item < hc) {   // ---- hub segment (staged form; k2_fstats2_hub when lane_hubs)
       Seg s;
       decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
       const int64_t vg = a.g.row_begin + s.vl;
@@ -1326,8 +1326,8 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t n = a.g.n_local, hc = load_count(a.pin.counts), nitems = hc + load_count(a.pin.counts + 2);
-  FOR_ITEMS(item, a.work + 3, nitems) {
-    if (item < hc) {   // ---- hub segment: P partial
+  FOR_ITEMS_FROM(item, a.work + 3, a.lane_hubs ? hc : 0, nitems) {
+    if (item < hc) {   // ---- hub segment: P partial (staged form; k2_bdst_a_hub when lane_hubs)
       Seg s;
       decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
       const int64_t vg = a.g.row_begin + s.vl;
@@ -1522,8 +1522,8 @@ __global__ void __launch_bounds__(256, 3) k2_bsrc2(const G2Args a) {
       x[h] = ep[h] > 0.0f ? dE : __fmul_rn(dE, a.slope);
     }
   };
-  FOR_ITEMS(item, a.work + 6, nitems) {
-    if (item < hc) {   // ---- hub segment: ∂S partial; the row's last segment folds and finalizes
+  FOR_ITEMS_FROM(item, a.work + 6, a.lane_hubs ? hc : 0, nitems) {
+    if (item < hc) {   // ---- hub segment: ∂S partial; the row's last segment folds and finalizes (staged form)
       Seg s;
       decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
       const int64_t ug = a.g.row_begin + s.vl;
@@ -1591,6 +1591,276 @@ __global__ void __launch_bounds__(256, 3) k2_bsrc2(const G2Args a) {
       src_finalize_row<H, VPL>(a, t.r0 + j, dSj, amax_loc);
     }
     __syncwarp();
+  }
+  amax_flush(a.amax_dHp, amax_loc);
+}
+
+// ================================================================== hub segments, one lane per (segment, head)
+// The per-edge scalar passes over hub rows (F-stats Σ, P2's P and ∂D, P3's ∂S) as lane-parallel chunk sums: a
+// warp claims SPW = 32/H consecutive hub segments (canonical chunks of C_E edges, reading R14) and lane
+// L = k·H + h computes segment k's partial of head h sequentially in edge order, all 32 lanes busy (the
+// staged form, seg_partial, sums on H lanes only).  Each group of H lanes stores its segment's partials
+// (coalesced), and the group that completes a row (atomic count per row) folds the row's partials in chunk
+// order (total = p_0, total = total + p_c) — the oracle's left-to-right Σᶜ.
+struct LaneSeg {
+  int64_t slot, row, eb, ee;
+  int base, nseg;
+  bool ok;
+};
+template <int H>
+__device__ __forceinline__ LaneSeg lane_seg(int64_t first, int64_t hc, const int64_t* __restrict__ ptr,
+                                            const PlanDev& p, int C) {
+  LaneSeg s;
+  s.slot = first + (threadIdx.x & 31) / H;
+  s.ok = s.slot < hc;
+  s.row = 0; s.eb = 0; s.ee = 0; s.base = 0; s.nseg = 1;
+  if (s.ok) {
+    s.row = p.hseg_row[s.slot];
+    s.base = p.hbase[s.row];
+    const int64_t beg = ptr[s.row], end = ptr[s.row + 1];
+    s.nseg = (int)((end - beg + C - 1) / C);
+    s.eb = beg + (s.slot - s.base) * (int64_t)C;
+    s.ee = s.eb + C < end ? s.eb + C : end;
+  }
+  return s;
+}
+// after the group's partials are stored: true for the (whole) group whose segment completed its row; the
+// row's counter is reset for the next pass.  Every lane of the warp must call it.
+template <int H>
+__device__ __forceinline__ bool lane_seg_last(int32_t* cnt, const LaneSeg& s) {
+  const int lane = threadIdx.x & 31;
+  __threadfence();
+  int d = -1;
+  if (s.ok && (lane % H) == 0) d = atomicAdd(cnt + s.row, 1);
+  d = __shfl_sync(0xffffffffu, d, lane & ~(H - 1));
+  const bool last = s.ok && d == s.nseg - 1;
+  if (last) {
+    __threadfence();
+    if ((lane % H) == 0) cnt[s.row] = 0;
+  }
+  return last;
+}
+// chunk-order fold of the row's partials part[(base + j)·H + h], j = 0 .. nseg-1 (L2 reads)
+template <int H>
+__device__ __forceinline__ float lane_seg_fold(const float* part, const LaneSeg& s) {
+  const int h = (threadIdx.x & 31) % H;
+  const float* p = part + (int64_t)s.base * H + h;
+  float tot = __ldcg(p);
+  int j = 1;
+  for (; j + 4 <= s.nseg; j += 4) {
+    const float x0 = __ldcg(p + (int64_t)j * H), x1 = __ldcg(p + (int64_t)(j + 1) * H);
+    const float x2 = __ldcg(p + (int64_t)(j + 2) * H), x3 = __ldcg(p + (int64_t)(j + 3) * H);
+    tot = __fadd_rn(tot, x0); tot = __fadd_rn(tot, x1); tot = __fadd_rn(tot, x2); tot = __fadd_rn(tot, x3);
+  }
+  for (; j < s.nseg; ++j) tot = __fadd_rn(tot, __ldcg(p + (int64_t)j * H));
+  return tot;
+}
+constexpr int LSU = 8;   // edges in flight per lane
+
+// claim SPW segments per warp; the loop body sees `first` (the warp's first slot)
+#define FOR_LANE_SEGS(first, counter, hc, SPW)                                                     \
+  for (int64_t first = claim_n(counter, SPW); first < (hc); first = claim_n(counter, SPW))
+
+__device__ __forceinline__ int64_t claim_n(int32_t* counter, int n) {
+  int it = 0;
+  if ((threadIdx.x & 31) == 0) it = atomicAdd(counter, n);
+  return (int64_t)__shfl_sync(0xffffffffu, it, 0);
+}
+
+// ---- F-stats Σ over hub segments: den partial Σ exp_p(el − m), m from FS1's keys in the node record
+template <int H>
+__global__ void __launch_bounds__(256, 4) k2_fstats2_hub(const G2Args a) {
+  constexpr int SPW = 32 / H;
+  const int h = (threadIdx.x & 31) % H;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t hc = load_count(a.pin.counts);
+  FOR_LANE_SEGS(first, a.work + 8, hc, SPW) {
+    const LaneSeg s = lane_seg<H>(first, hc, a.g.in_ptr, a.pin, a.g.chunk);
+    const int64_t vg = a.g.row_begin + s.row;
+    float m = 0.0f, acc = 0.0f;
+    int qd = 0;
+    if (s.ok) {
+      m = fkey_dec(reinterpret_cast<const unsigned*>(a.nrec + vg * a.nrs)[h]);
+      qd = a.qD[vg * H + h];
+      for (int64_t e0 = s.eb; e0 < s.ee; e0 += LSU) {
+        int qs[LSU];
+#pragma unroll
+        for (int j = 0; j < LSU; ++j) {
+          const int u = e0 + j < s.ee ? __ldg(a.g.in_src + e0 + j) : 0;
+          qs[j] = a.qS[(int64_t)u * H + h];
+        }
+#pragma unroll
+        for (int j = 0; j < LSU; ++j)
+          if (e0 + j < s.ee)
+            acc = __fadd_rn(acc, exp_p(__fsub_rn(lrelu(sddmm_add1((int8_t)qs[j], scS.s, (int8_t)qd, scD.s), a.slope), m)));
+      }
+      __stcg(a.h2 + s.slot * H + h, acc);
+    }
+    if (lane_seg_last<H>(a.hcnt, s)) {   // the row's m (as a float) and den; every segment has read the keys
+      const float den = lane_seg_fold<H>(a.h2, s);
+      a.m[vg * H + h] = m;
+      rec_put1(a, vg, 0, h, m);
+      a.den[vg * H + h] = den;
+      rec_put1(a, vg, 1, h, den);
+      reinterpret_cast<int8_t*>(a.nrec + vg * a.nrs + 3 * H)[h] = (int8_t)qd;
+    }
+  }
+}
+
+// α of one in-edge for head h: e_pre (③) and exp_p(lrelu(e_pre) − m) / den (④)
+__device__ __forceinline__ float alpha1(int qs, int qd, float sS, float sD, float slope, float m, float den, float& ep) {
+  ep = sddmm_add1((int8_t)qs, sS, (int8_t)qd, sD);
+  return __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, slope), m)), den);
+}
+
+// ---- P2a over hub segments: P partial Σ fmaf(∂α, α); ∂α in in-CSR order (scattered there by P1), or gathered
+// through the in2out map and stored in in-CSR order for P2b
+template <int H>
+__global__ void __launch_bounds__(256, 4) k2_bdst_a_hub(const G2Args a) {
+  constexpr int SPW = 32 / H;
+  const int h = (threadIdx.x & 31) % H;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t hc = load_count(a.pin.counts);
+  FOR_LANE_SEGS(first, a.work + 9, hc, SPW) {
+    const LaneSeg s = lane_seg<H>(first, hc, a.g.in_ptr, a.pin, a.g.chunk);
+    const int64_t vg = a.g.row_begin + s.row;
+    if (s.ok) {
+      const float m = a.m[vg * H + h], den = a.den[vg * H + h];
+      const int qd = a.qD[vg * H + h];
+      float acc = 0.0f;
+      for (int64_t e0 = s.eb; e0 < s.ee; e0 += LSU) {
+        int qs[LSU];
+        float da[LSU];
+#pragma unroll
+        for (int j = 0; j < LSU; ++j) {
+          const bool in = e0 + j < s.ee;
+          const int u = in ? __ldg(a.g.in_src + e0 + j) : 0;
+          if (a.scatter_in) da[j] = in ? __ldcs(a.dal_in + (e0 + j) * H + h) : 0.0f;
+          else da[j] = in ? a.dal_out[(int64_t)__ldg(a.in2out + e0 + j) * H + h] : 0.0f;
+          qs[j] = a.qS[(int64_t)u * H + h];
+        }
+        if (!a.scatter_in)
+#pragma unroll
+          for (int j = 0; j < LSU; ++j)
+            if (e0 + j < s.ee) a.dal_in[(e0 + j) * H + h] = da[j];   // for P2b (coalesced)
+#pragma unroll
+        for (int j = 0; j < LSU; ++j)
+          if (e0 + j < s.ee) {
+            float ep;
+            acc = __fmaf_rn(da[j], alpha1(qs[j], qd, scS.s, scD.s, a.slope, m, den, ep), acc);
+          }
+      }
+      __stcg(a.h1 + s.slot * H + h, acc);
+    }
+    if (lane_seg_last<H>(a.hcnt, s)) {
+      const float P = lane_seg_fold<H>(a.h1, s);
+      a.P[vg * H + h] = P;
+      rec_put1(a, vg, 2, h, P);
+    }
+  }
+}
+
+// ---- P2b over hub segments: ∂D partial Σ ∂E_pre, ∂E_pre = α(∂α − P[v]) · lrelu′(e_pre)
+template <int H>
+__global__ void __launch_bounds__(256, 4) k2_bdst_b_hub(const G2Args a) {
+  constexpr int SPW = 32 / H;
+  const int h = (threadIdx.x & 31) % H;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t hc = load_count(a.pin.counts);
+  FOR_LANE_SEGS(first, a.work + 10, hc, SPW) {
+    const LaneSeg s = lane_seg<H>(first, hc, a.g.in_ptr, a.pin, a.g.chunk);
+    const int64_t vg = a.g.row_begin + s.row;
+    if (s.ok) {
+      const float m = a.m[vg * H + h], den = a.den[vg * H + h], P = a.P[vg * H + h];
+      const int qd = a.qD[vg * H + h];
+      float acc = 0.0f;
+      for (int64_t e0 = s.eb; e0 < s.ee; e0 += LSU) {
+        int qs[LSU];
+        float da[LSU];
+#pragma unroll
+        for (int j = 0; j < LSU; ++j) {
+          const bool in = e0 + j < s.ee;
+          const int u = in ? __ldg(a.g.in_src + e0 + j) : 0;
+          da[j] = in ? __ldcs(a.dal_in + (e0 + j) * H + h) : 0.0f;
+          qs[j] = a.qS[(int64_t)u * H + h];
+        }
+#pragma unroll
+        for (int j = 0; j < LSU; ++j)
+          if (e0 + j < s.ee) {
+            float ep;
+            const float al = alpha1(qs[j], qd, scS.s, scD.s, a.slope, m, den, ep);
+            const float dE = __fmul_rn(al, __fsub_rn(da[j], P));
+            acc = __fadd_rn(acc, ep > 0.0f ? dE : __fmul_rn(dE, a.slope));
+          }
+      }
+      __stcg(a.h2 + s.slot * H + h, acc);
+    }
+    if (lane_seg_last<H>(a.hcnt, s)) a.dD[vg * H + h] = lane_seg_fold<H>(a.h2, s);
+  }
+}
+
+// ---- P3 over hub segments (out-CSR): ∂S partial Σ ∂E_pre over u's out-edges, v's m, den, P, q_D from the
+// node record; the group that completes u's row writes ∂S[u], then the warp finalizes the completed rows'
+// ∂H′ = (∂H′_agg + ∂S·a_src) + ∂D·a_dst (one warp per row)
+template <int H, int VPL>
+__global__ void __launch_bounds__(256, 3) k2_bsrc2_hub(const G2Args a) {
+  constexpr int SPW = 32 / H;
+  const int lane = threadIdx.x & 31, h = lane % H;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t hc = load_count(a.pout.counts);
+  float amax_loc = 0.0f;
+  FOR_LANE_SEGS(first, a.work + 11, hc, SPW) {
+    const LaneSeg s = lane_seg<H>(first, hc, a.g.out_ptr, a.pout, a.g.chunk);
+    const int64_t ug = a.g.row_begin + s.row;
+    if (s.ok) {
+      const int qs = a.qS[ug * H + h];
+      float acc = 0.0f;
+      for (int64_t e0 = s.eb; e0 < s.ee; e0 += LSU) {
+        float da[LSU], mv[LSU], dv[LSU], pv[LSU];
+        int qd[LSU];
+#pragma unroll
+        for (int j = 0; j < LSU; ++j) {
+          const bool in = e0 + j < s.ee;
+          const int v = in ? __ldg(a.g.out_dst + e0 + j) : 0;
+          da[j] = in ? __ldcs(a.dal_out + (e0 + j) * H + h) : 0.0f;
+          const float* r = a.nrec + (int64_t)v * a.nrs;
+          mv[j] = r[h];
+          dv[j] = r[H + h];
+          pv[j] = r[2 * H + h];
+          qd[j] = reinterpret_cast<const int8_t*>(r + 3 * H)[h];
+        }
+#pragma unroll
+        for (int j = 0; j < LSU; ++j)
+          if (e0 + j < s.ee) {
+            float ep;
+            const float al = alpha1(qs, qd[j], scS.s, scD.s, a.slope, mv[j], dv[j], ep);
+            const float dE = __fmul_rn(al, __fsub_rn(da[j], pv[j]));
+            acc = __fadd_rn(acc, ep > 0.0f ? dE : __fmul_rn(dE, a.slope));
+          }
+      }
+      __stcg(a.hs + s.slot * H + h, acc);
+    }
+    const bool last = lane_seg_last<H>(a.hcnt, s);
+    float dS = 0.0f;
+    if (last) {
+      dS = lane_seg_fold<H>(a.hs, s);
+      a.dS[ug * H + h] = dS;
+    }
+    // finalize the rows completed by this warp's groups, the whole warp per row
+    unsigned done = __ballot_sync(0xffffffffu, last && h == 0);
+    while (done) {
+      const int g0 = __ffs(done) - 1;
+      done &= done - 1;
+      float dSr[H];
+#pragma unroll
+      for (int k = 0; k < H; ++k) dSr[k] = __shfl_sync(0xffffffffu, dS, g0 + k);
+      const int64_t rl = __shfl_sync(0xffffffffu, s.row, g0);
+      src_finalize_row<H, VPL>(a, rl, dSr, amax_loc);
+    }
   }
   amax_flush(a.amax_dHp, amax_loc);
 }
@@ -1736,6 +2006,7 @@ cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st, const SideStream* 
       attr = true;                                                                                   \
     }                                                                                                \
     { ProfScope p("gat_fwd_stats1", st); k2_fstats1<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
+    if (a.lane_hubs) { ProfScope p("gat_fwd_stats_hub", st); k2_fstats2_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
     { ProfScope p("gat_fwd_stats", st); k2_fstats2<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
     e = fork2(st, x);                                                                                \
     { ProfScope p("gat_fwd_agg_hub", sh); k2_fagg_seg<H_, V_><<<grid_items((a.pin.cap + 7) / 8, 3), 256, smem_s, sh>>>(a); } \
@@ -1769,8 +2040,11 @@ cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st, const SideStream* 
     { ProfScope p("gat_bwd_src_hub", sh); k2_bsrc1_seg<H_, V_, NW><<<grid_items((a.pout.cap + NW - 1) / NW, 20 / NW), NW * 32, smem_s, sh>>>(a); } \
     { ProfScope p("gat_bwd_src", st); k2_bsrc1<H_, V_, NW><<<grid_items((a.pout.tcap + NW - 1) / NW, 20 / NW), NW * 32, smem, st>>>(a); } \
     if (e == cudaSuccess) e = join2(st, x);                                                          \
+    if (a.lane_hubs) { ProfScope p("gat_bwd_dst_hub", st); k2_bdst_a_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
     { ProfScope p("gat_bwd_dst", st); k2_bdst_a<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
-    { ProfScope p("gat_bwd_dst2", st); k2_bdst_b<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
+    if (a.lane_hubs) { ProfScope p("gat_bwd_dst2", st); k2_bdst_b_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
+    else { ProfScope p("gat_bwd_dst2", st); k2_bdst_b<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
+    if (a.lane_hubs) { ProfScope p("gat_bwd_src2_hub", st); k2_bsrc2_hub<H_, V_><<<grid_items((a.pout.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
     { ProfScope p("gat_bwd_src2", st); k2_bsrc2<H_, V_><<<grid_items((a.pout.cap + a.pout.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
   }
   G2_CASES(X)

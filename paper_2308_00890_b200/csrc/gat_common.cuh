@@ -47,6 +47,8 @@ __device__ __forceinline__ int64_t claim(int32_t* counter) {
   return (int64_t)__shfl_sync(0xffffffffu, it, 0);
 }
 #define FOR_ITEMS(item, counter, nitems) for (int64_t item = claim(counter); item < (nitems); item = claim(counter))
+#define FOR_ITEMS_FROM(item, counter, start, nitems) \
+  for (int64_t item = (start) + claim(counter); item < (nitems); item = (start) + claim(counter))
 
 template <int H>
 __device__ __forceinline__ float head_pick(const float (&x)[H], int h) {

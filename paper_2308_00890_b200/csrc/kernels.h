@@ -167,6 +167,7 @@ struct G2Args {
   float* nrec; int nrs;                                      // [N][nrs] packed per-node record: m | den | P | q_D
   const int32_t* in2out;                                     // [E] out-CSR position of each in-CSR edge
   int scatter_in;                                            // P1 also writes ∂α at its in-CSR slot (dal_in)
+  int lane_hubs;                                             // hub segments of F-stats / P2 / P3: lane per (segment, head)
   float* da_src; float* da_dst;                              // [HD]
   int codes_biased;
 };

@@ -205,7 +205,24 @@ def _ptr(t):
         return None
     if not t.is_cuda:
         raise TypeError("libtango takes CUDA tensors only")
+    if not t.is_contiguous():
+        raise ValueError("libtango takes contiguous tensors only (row strides are passed explicitly)")
     return t.data_ptr()
+
+
+def _arg(t, name, shape, dtype=torch.float32, optional=False):
+    """Pointer of a layer argument after checking what the C ABI assumes of it: a contiguous CUDA tensor
+    of the given dtype and shape (a transposed, sliced or mistyped tensor would be read with the wrong
+    layout without an error)."""
+    if t is None:
+        if optional:
+            return None
+        raise ValueError(f"{name}: required")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return _ptr(t)
 
 
 def _stream():
@@ -499,9 +516,10 @@ class GATLayer:
         n = self.graph.n_local
         out = out if out is not None else torch.empty((n, self.HD), dtype=torch.float32, device="cuda")
         amax_out = amax_out if amax_out is not None else torch.empty(1, dtype=torch.float32, device="cuda")
-        _check(L.tango_gat_layer_fwd(self.graph.ref(), C.byref(self.params), _ptr(H), _ptr(amax_hint),
-                                     Rng(seed, step, 0), layer_id, _ptr(self.ctx), self.ctx.numel(), _ptr(out),
-                                     _ptr(amax_out), self._comm(), _ptr(self.status), _stream()),
+        _check(L.tango_gat_layer_fwd(self.graph.ref(), C.byref(self.params), _arg(H, "H", (n, self.F)),
+                                     _arg(amax_hint, "amax_hint", (1,), optional=True), Rng(seed, step, 0), layer_id,
+                                     _ptr(self.ctx), self.ctx.numel(), _arg(out, "out", (n, self.HD)),
+                                     _arg(amax_out, "amax_out", (1,)), self._comm(), _ptr(self.status), _stream()),
                "tango_gat_layer_fwd")
         return out, amax_out
 
@@ -516,8 +534,11 @@ class GATLayer:
         else:
             dH, dW, da_s, da_d = outs
         _check(L.tango_gat_layer_bwd(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), self.ctx.numel(),
-                                     _ptr(dH_out), _ptr(amax_hint), Rng(seed, step, 0), layer_id, _ptr(dH), _ptr(dW),
-                                     _ptr(da_s), _ptr(da_d), None, self._comm(), _ptr(self.status), _stream()),
+                                     _arg(dH_out, "dH_out", (n, self.HD)),
+                                     _arg(amax_hint, "amax_hint", (1,), optional=True), Rng(seed, step, 0), layer_id,
+                                     _arg(dH, "dH", (n, self.F), optional=True), _arg(dW, "dW", (self.F, self.HD)),
+                                     _arg(da_s, "da_src", (self.HD,)), _arg(da_d, "da_dst", (self.HD,)), None,
+                                     self._comm(), _ptr(self.status), _stream()),
                "tango_gat_layer_bwd")
         return dH, dW, da_s, da_d
 
@@ -596,10 +617,12 @@ class GCNLayer:
         out = out if out is not None else torch.empty((self.graph.n_local, self.O), dtype=torch.float32,
                                                       device="cuda")
         amax_out = amax_out if amax_out is not None else torch.empty(1, dtype=torch.float32, device="cuda")
-        _check(L.tango_gcn_layer_fwd(self.graph.ref(), C.byref(self.params), _ptr(X), _ptr(amax_hint),
-                                     Rng(seed, step, 0), layer_id, _ptr(self.ctx), self.ctx.numel(), _ptr(out),
-                                     _ptr(amax_out), self.comm.handle if self.comm else None, _ptr(self.status),
-                                     _stream()), "tango_gcn_layer_fwd")
+        n = self.graph.n_local
+        _check(L.tango_gcn_layer_fwd(self.graph.ref(), C.byref(self.params), _arg(X, "X", (n, self.F)),
+                                     _arg(amax_hint, "amax_hint", (1,), optional=True), Rng(seed, step, 0), layer_id,
+                                     _ptr(self.ctx), self.ctx.numel(), _arg(out, "out", (n, self.O)),
+                                     _arg(amax_out, "amax_out", (1,)), self.comm.handle if self.comm else None,
+                                     _ptr(self.status), _stream()), "tango_gcn_layer_fwd")
         return out, amax_out
 
     def backward(self, dout, seed=0x7A4E60, step=0, layer_id=0, want_dX=True, outs=None):
@@ -609,8 +632,10 @@ class GCNLayer:
             dW = torch.empty((self.F, self.O), dtype=torch.float32, device="cuda")
         else:
             dX, dW = outs
+        n = self.graph.n_local
         _check(L.tango_gcn_layer_bwd(self.graph.ref(), C.byref(self.params), _ptr(self.ctx), self.ctx.numel(),
-                                     _ptr(dout), Rng(seed, step, 0), layer_id, _ptr(dX), _ptr(dW),
+                                     _arg(dout, "dout", (n, self.O)), Rng(seed, step, 0), layer_id,
+                                     _arg(dX, "dX", (n, self.F), optional=True), _arg(dW, "dW", (self.F, self.O)),
                                      self.comm.handle if self.comm else None, _ptr(self.status), _stream()),
                "tango_gcn_layer_bwd")
         return dX, dW

@@ -52,6 +52,14 @@ CASES = [
     ("noself", ("noself", 500, 900, 5), 48, 1, 64, 256),
     ("hd512", ("rand", 2000, 20000, 6), 128, 4, 128, 256),
     ("f602", ("rand", 700, 5000, 8), 602, 4, 128, 64),
+    # mean in-degree >= 32: the v6 dataflow (gat2.cu) with hub rows (degree > C_E) — split into many
+    # canonical chunks at C_E = 7 / 16 / 64 (rows beyond SPIECE chunks fold scratch partials)
+    ("v6_h4", ("rand", 800, 30000, 21), 64, 4, 128, 256),
+    ("v6_h4_c7", ("rand", 800, 30000, 21), 64, 4, 128, 7),
+    ("v6_h2_c64", ("rand", 500, 12000, 22), 32, 2, 64, 64),
+    ("v6_h8_c16", ("rand", 400, 10000, 23), 40, 8, 32, 16),
+    ("v6_h1", ("rand", 400, 10000, 23), 40, 1, 128, 256),
+    ("v6_noself_c64", ("noself", 600, 20000, 24), 48, 4, 64, 64),
 ]
 
 
@@ -106,6 +114,8 @@ def _gat_parity(T, orc, case, keep_eid):
     eq("qD", fv["qD"], f["qD"])
     eq("m", fv["m"], f["m"])
     eq("den", fv["den"], f["den"])
+    if keep_eid is None:
+        assert fv["dataflow"] == (2 if name.startswith("v6") else 1), (name, fv["dataflow"])
     if fv["dataflow"] == 1:   # round-1 kernels store α (sign = LeakyReLU branch); v6 recomputes it
         eq("alpha", fv["alpha"], f["alpha"])
         assert np.array_equal(fv["e_pre_pos"].cpu().numpy(), f["e_pre"] > 0)
