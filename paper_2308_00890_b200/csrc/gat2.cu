@@ -90,6 +90,39 @@ __device__ __forceinline__ DstSm<H> load_rec(const G2Args& a, int64_t v) {
   load_qh<H>(reinterpret_cast<const int8_t*>(r + 3 * H), d.qd);
   return d;
 }
+// the record's fields as loaded (q_D still packed), unpacked where α is computed, so that a gather issued a
+// chunk ahead is not consumed (byte extraction) right after it is issued
+template <int H>
+struct RecRaw {
+  float m[H], den[H];
+  uint32_t qw[(H + 3) / 4];
+};
+template <int H>
+__device__ __forceinline__ RecRaw<H> load_rec_raw(const G2Args& a, int64_t v) {
+  RecRaw<H> r;
+  const float* p = a.nrec + v * a.nrs;
+  ld_h<H>(p, r.m);
+  ld_h<H>(p + H, r.den);
+  const uint32_t* q = reinterpret_cast<const uint32_t*>(p + 3 * H);
+  if constexpr (H == 1) r.qw[0] = *reinterpret_cast<const uint8_t*>(q);
+  else if constexpr (H == 2) r.qw[0] = *reinterpret_cast<const uint16_t*>(q);
+  else {
+#pragma unroll
+    for (int k = 0; k < (H + 3) / 4; ++k) r.qw[k] = q[k];
+  }
+  return r;
+}
+template <int H>
+__device__ __forceinline__ DstSm<H> rec_unpack(const RecRaw<H>& r) {
+  DstSm<H> d;
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    d.m[h] = r.m[h];
+    d.den[h] = r.den[h];
+    d.qd[h] = (int8_t)(r.qw[h >> 2] >> (8 * (h & 3)));
+  }
+  return d;
+}
 template <int H>
 __device__ __forceinline__ void rec_put(const G2Args& a, int64_t v, int field, const float (&x)[H]) {
   st_h<H>(a.nrec + v * a.nrs + field * H, x);
@@ -964,11 +997,11 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
       return s.eb + (pos < T ? pos : T - 1);
     };
     // attributes of a chunk: α (needs v's softmax data), in-CSR slot, out-CSR slot, tile row
-    struct AttrIn { DstSm<H> d; };
+    struct AttrIn { RecRaw<H> r; };
     auto attr_load = [&](int c, int v, int64_t e) {
       AttrIn x;
       (void)e;
-      if (c * 32 + lane < T) x.d = load_rec<H>(a, v);
+      if (c * 32 + lane < T) x.r = load_rec_raw<H>(a, v);
       return x;
     };
     auto attrs = [&](int c, int row, const AttrIn& x, float (&al)[H]) {
@@ -979,7 +1012,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
       for (int h = 0; h < H; ++h) al[h] = 0.0f;
       if (c * 32 + lane < T) {
         float ep[H];
-        alpha_rec<H>(qs, x.d, scS.s, scD.s, a.slope, ep, al);
+        alpha_rec<H>(qs, rec_unpack<H>(x.r), scS.s, scD.s, a.slope, ep, al);
       }
     };
     auto stash = [&](int c, int row, int64_t e, const float (&al)[H]) {
@@ -1196,7 +1229,9 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
     int8_t qs[H];
     load_qh<H>(a.qS + ug * H, qs);
     Row<VPL> ow = load_row<VPL>(a.qHp + ug * a.ldHp + lane * VPL);
-    const int osum = row_sum_plain<VPL>(ow, true);
+    int osum_h = row_sum_plain<VPL>(ow, true);   // -> Σ of the head's plain own codes (all its lanes)
+#pragma unroll
+    for (int o = LPH / 2; o > 0; o >>= 1) osum_h += __shfl_xor_sync(0xffffffffu, osum_h, o);
     auto edge_v = [&](int c) -> int { return c * 32 + lane < T ? __ldcs(a.g.out_dst + eb + c * 32 + lane) : 0; };
     auto alpha_of = [&](int c, const DstSm<H>& d, float (&al)[H]) {
 #pragma unroll
@@ -1235,8 +1270,8 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
     int nextf = C;   // next chunk boundary of the piece (FAST form: group starts only)
     for (int c = 0; c < nch; ++c) {
       const int v2 = edge_v(c + 2);
-      DstSm<H> d1;
-      if ((c + 1) * 32 + lane < T) d1 = load_rec<H>(a, v1);
+      RecRaw<H> r1;
+      if ((c + 1) * 32 + lane < T) r1 = load_rec_raw<H>(a, v1);
       const float* sac = sa + ((c & 1) * H + myh) * 32;
       for (int i0 = 0; i0 < 32; i0 += GR) {
         const int t0 = c * 32 + i0;
@@ -1248,24 +1283,37 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
         const float4 b4 = *reinterpret_cast<const float4*>(sac + i0 + 4);
         const float al[GR] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
         int dd[GR];
-        if (fast && t0 == nextf) {
-          pf.fold(acc);
-          nextf += C;
-        }
+        // per edge: the lane's raw IDP4A sum on excess-128 codes; the −128·Σq_H′ correction is applied once
+        // per edge after the reduction over the head's lanes (osum_h: the head's Σ of plain own codes)
+        if (fast) {
+          if (t0 == nextf) {
+            pf.fold(acc);
+            nextf += C;
+          }
 #pragma unroll
-        for (int j = 0; j < GR; ++j) {
-          if (!fast && t0 + j > 0 && t0 + j < T && (t0 + j) % C == 0) pf.fold(acc);
-          const Row<VPL> rj = lds_row_slice<VPL>(s0 + j * 32 * VPL);
-          dd[j] = row_dot_biased<VPL>(rj, ow, osum);
-          const float2 al2 = make_float2(al[j], al[j]);
+          for (int j = 0; j < GR; ++j) {
+            const Row<VPL> rj = lds_row_slice<VPL>(s0 + j * 32 * VPL);
+            dd[j] = row_dot_raw<VPL>(rj, ow);
+            const float2 al2 = make_float2(al[j], al[j]);
 #pragma unroll
-          for (int q = 0; q < VPL / 4; ++q) fma4_biased(rj.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+            for (int q = 0; q < VPL / 4; ++q) fma4_biased(rj.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < GR; ++j) {
+            if (t0 + j > 0 && t0 + j < T && (t0 + j) % C == 0) pf.fold(acc);
+            const Row<VPL> rj = lds_row_slice<VPL>(s0 + j * 32 * VPL);
+            dd[j] = row_dot_raw<VPL>(rj, ow);
+            const float2 al2 = make_float2(al[j], al[j]);
+#pragma unroll
+            for (int q = 0; q < VPL / 4; ++q) fma4_biased(rj.w[q], al2, acc[2 * q], acc[2 * q + 1]);
+          }
         }
         {
           int k;
           const int d0[4] = {dd[0], dd[1], dd[2], dd[3]}, d1x[4] = {dd[4], dd[5], dd[6], dd[7]};
-          const int x0 = group_dot_reduce<LPH>(d0, k);
-          const int x1 = group_dot_reduce<LPH>(d1x, k);
+          const int x0 = group_dot_reduce<LPH>(d0, k) - 128 * osum_h;
+          const int x1 = group_dot_reduce<LPH>(d1x, k) - 128 * osum_h;
           sd[myh * 32 + i0 + k] = __fmul_rn(__int2float_rn(x0), sGH);
           sd[myh * 32 + i0 + 4 + k] = __fmul_rn(__int2float_rn(x1), sGH);
         }
@@ -1288,6 +1336,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
       __syncwarp();
       if (c + 1 < nch) {
         float al1[H];
+        const DstSm<H> d1 = rec_unpack<H>(r1);
         alpha_of(c + 1, d1, al1);
         stash(c + 1, al1);
         sidx[(c & 1) * 32 + lane] = v2;
@@ -1655,7 +1704,39 @@ __device__ __forceinline__ float lane_seg_fold(const float* part, const LaneSeg&
   for (; j < s.nseg; ++j) tot = __fadd_rn(tot, __ldcg(p + (int64_t)j * H));
   return tot;
 }
-constexpr int LSU = 8;   // edges in flight per lane
+// Software pipeline over a lane's segment: the index loads of batch k+2 and the dependent loads of batch k+1
+// are issued before batch k is used (in edge order), so both load latencies overlap the arithmetic.
+// fi(e) -> I (independent loads of edge e), fd(I, e) -> D (loads that need I), fu(D) (the sequential use).
+template <int U, typename I, typename D, typename FI, typename FD, typename FU>
+__device__ __forceinline__ void lane_pipe(int64_t eb, int64_t ee, FI&& fi, FD&& fd, FU&& fu) {
+  I ia[U], ib[U];
+  D dc[U], dn[U];
+#pragma unroll
+  for (int j = 0; j < U; ++j)
+    if (eb + j < ee) ia[j] = fi(eb + j);
+#pragma unroll
+  for (int j = 0; j < U; ++j)
+    if (eb + j < ee) dc[j] = fd(ia[j], eb + j);
+#pragma unroll
+  for (int j = 0; j < U; ++j)
+    if (eb + U + j < ee) ia[j] = fi(eb + U + j);
+  for (int64_t e0 = eb; e0 < ee; e0 += U) {
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (e0 + 2 * U + j < ee) ib[j] = fi(e0 + 2 * U + j);
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (e0 + U + j < ee) dn[j] = fd(ia[j], e0 + U + j);
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (e0 + j < ee) fu(dc[j]);
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      dc[j] = dn[j];
+      ia[j] = ib[j];
+    }
+  }
+}
 
 // claim SPW segments per warp; the loop body sees `first` (the warp's first slot)
 #define FOR_LANE_SEGS(first, counter, hc, SPW)                                                     \
@@ -1669,7 +1750,7 @@ __device__ __forceinline__ int64_t claim_n(int32_t* counter, int n) {
 
 // ---- F-stats Σ over hub segments: den partial Σ exp_p(el − m), m from FS1's keys in the node record
 template <int H>
-__global__ void __launch_bounds__(256, 4) k2_fstats2_hub(const G2Args a) {
+__global__ void __launch_bounds__(256, 3) k2_fstats2_hub(const G2Args a) {
   constexpr int SPW = 32 / H;
   const int h = (threadIdx.x & 31) % H;
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
@@ -1683,18 +1764,12 @@ __global__ void __launch_bounds__(256, 4) k2_fstats2_hub(const G2Args a) {
     if (s.ok) {
       m = fkey_dec(reinterpret_cast<const unsigned*>(a.nrec + vg * a.nrs)[h]);
       qd = a.qD[vg * H + h];
-      for (int64_t e0 = s.eb; e0 < s.ee; e0 += LSU) {
-        int qs[LSU];
-#pragma unroll
-        for (int j = 0; j < LSU; ++j) {
-          const int u = e0 + j < s.ee ? __ldg(a.g.in_src + e0 + j) : 0;
-          qs[j] = a.qS[(int64_t)u * H + h];
-        }
-#pragma unroll
-        for (int j = 0; j < LSU; ++j)
-          if (e0 + j < s.ee)
-            acc = __fadd_rn(acc, exp_p(__fsub_rn(lrelu(sddmm_add1((int8_t)qs[j], scS.s, (int8_t)qd, scD.s), a.slope), m)));
-      }
+      lane_pipe<8, int, int>(
+          s.eb, s.ee, [&](int64_t e) { return (int)__ldg(a.g.in_src + e); },
+          [&](int u, int64_t) { return (int)a.qS[(int64_t)u * H + h]; },
+          [&](int qs) {
+            acc = __fadd_rn(acc, exp_p(__fsub_rn(lrelu(sddmm_add1((int8_t)qs, scS.s, (int8_t)qd, scD.s), a.slope), m)));
+          });
       __stcg(a.h2 + s.slot * H + h, acc);
     }
     if (lane_seg_last<H>(a.hcnt, s)) {   // the row's m (as a float) and den; every segment has read the keys
@@ -1713,11 +1788,13 @@ __device__ __forceinline__ float alpha1(int qs, int qd, float sS, float sD, floa
   ep = sddmm_add1((int8_t)qs, sS, (int8_t)qd, sD);
   return __fdiv_rn(exp_p(__fsub_rn(lrelu(ep, slope), m)), den);
 }
+struct UDa { int u; float da; };
+struct QDa { int qs; float da; };
 
 // ---- P2a over hub segments: P partial Σ fmaf(∂α, α); ∂α in in-CSR order (scattered there by P1), or gathered
 // through the in2out map and stored in in-CSR order for P2b
 template <int H>
-__global__ void __launch_bounds__(256, 4) k2_bdst_a_hub(const G2Args a) {
+__global__ void __launch_bounds__(256, 3) k2_bdst_a_hub(const G2Args a) {
   constexpr int SPW = 32 / H;
   const int h = (threadIdx.x & 31) % H;
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
@@ -1730,28 +1807,24 @@ __global__ void __launch_bounds__(256, 4) k2_bdst_a_hub(const G2Args a) {
       const float m = a.m[vg * H + h], den = a.den[vg * H + h];
       const int qd = a.qD[vg * H + h];
       float acc = 0.0f;
-      for (int64_t e0 = s.eb; e0 < s.ee; e0 += LSU) {
-        int qs[LSU];
-        float da[LSU];
-#pragma unroll
-        for (int j = 0; j < LSU; ++j) {
-          const bool in = e0 + j < s.ee;
-          const int u = in ? __ldg(a.g.in_src + e0 + j) : 0;
-          if (a.scatter_in) da[j] = in ? __ldcs(a.dal_in + (e0 + j) * H + h) : 0.0f;
-          else da[j] = in ? a.dal_out[(int64_t)__ldg(a.in2out + e0 + j) * H + h] : 0.0f;
-          qs[j] = a.qS[(int64_t)u * H + h];
-        }
-        if (!a.scatter_in)
-#pragma unroll
-          for (int j = 0; j < LSU; ++j)
-            if (e0 + j < s.ee) a.dal_in[(e0 + j) * H + h] = da[j];   // for P2b (coalesced)
-#pragma unroll
-        for (int j = 0; j < LSU; ++j)
-          if (e0 + j < s.ee) {
+      lane_pipe<4, UDa, QDa>(
+          s.eb, s.ee,
+          [&](int64_t e) {
+            UDa x;
+            x.u = __ldg(a.g.in_src + e);
+            if (a.scatter_in) {
+              x.da = __ldcs(a.dal_in + e * H + h);
+            } else {
+              x.da = a.dal_out[(int64_t)__ldg(a.in2out + e) * H + h];
+              a.dal_in[e * H + h] = x.da;   // for P2b (coalesced)
+            }
+            return x;
+          },
+          [&](const UDa& x, int64_t) { return QDa{(int)a.qS[(int64_t)x.u * H + h], x.da}; },
+          [&](const QDa& y) {
             float ep;
-            acc = __fmaf_rn(da[j], alpha1(qs[j], qd, scS.s, scD.s, a.slope, m, den, ep), acc);
-          }
-      }
+            acc = __fmaf_rn(y.da, alpha1(y.qs, qd, scS.s, scD.s, a.slope, m, den, ep), acc);
+          });
       __stcg(a.h1 + s.slot * H + h, acc);
     }
     if (lane_seg_last<H>(a.hcnt, s)) {
@@ -1764,7 +1837,7 @@ __global__ void __launch_bounds__(256, 4) k2_bdst_a_hub(const G2Args a) {
 
 // ---- P2b over hub segments: ∂D partial Σ ∂E_pre, ∂E_pre = α(∂α − P[v]) · lrelu′(e_pre)
 template <int H>
-__global__ void __launch_bounds__(256, 4) k2_bdst_b_hub(const G2Args a) {
+__global__ void __launch_bounds__(256, 3) k2_bdst_b_hub(const G2Args a) {
   constexpr int SPW = 32 / H;
   const int h = (threadIdx.x & 31) % H;
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
@@ -1777,25 +1850,16 @@ __global__ void __launch_bounds__(256, 4) k2_bdst_b_hub(const G2Args a) {
       const float m = a.m[vg * H + h], den = a.den[vg * H + h], P = a.P[vg * H + h];
       const int qd = a.qD[vg * H + h];
       float acc = 0.0f;
-      for (int64_t e0 = s.eb; e0 < s.ee; e0 += LSU) {
-        int qs[LSU];
-        float da[LSU];
-#pragma unroll
-        for (int j = 0; j < LSU; ++j) {
-          const bool in = e0 + j < s.ee;
-          const int u = in ? __ldg(a.g.in_src + e0 + j) : 0;
-          da[j] = in ? __ldcs(a.dal_in + (e0 + j) * H + h) : 0.0f;
-          qs[j] = a.qS[(int64_t)u * H + h];
-        }
-#pragma unroll
-        for (int j = 0; j < LSU; ++j)
-          if (e0 + j < s.ee) {
+      lane_pipe<4, UDa, QDa>(
+          s.eb, s.ee,
+          [&](int64_t e) { return UDa{(int)__ldg(a.g.in_src + e), __ldcs(a.dal_in + e * H + h)}; },
+          [&](const UDa& x, int64_t) { return QDa{(int)a.qS[(int64_t)x.u * H + h], x.da}; },
+          [&](const QDa& y) {
             float ep;
-            const float al = alpha1(qs[j], qd, scS.s, scD.s, a.slope, m, den, ep);
-            const float dE = __fmul_rn(al, __fsub_rn(da[j], P));
+            const float al = alpha1(y.qs, qd, scS.s, scD.s, a.slope, m, den, ep);
+            const float dE = __fmul_rn(al, __fsub_rn(y.da, P));
             acc = __fadd_rn(acc, ep > 0.0f ? dE : __fmul_rn(dE, a.slope));
-          }
-      }
+          });
       __stcg(a.h2 + s.slot * H + h, acc);
     }
     if (lane_seg_last<H>(a.hcnt, s)) a.dD[vg * H + h] = lane_seg_fold<H>(a.h2, s);
@@ -1805,8 +1869,10 @@ __global__ void __launch_bounds__(256, 4) k2_bdst_b_hub(const G2Args a) {
 // ---- P3 over hub segments (out-CSR): ∂S partial Σ ∂E_pre over u's out-edges, v's m, den, P, q_D from the
 // node record; the group that completes u's row writes ∂S[u], then the warp finalizes the completed rows'
 // ∂H′ = (∂H′_agg + ∂S·a_src) + ∂D·a_dst (one warp per row)
+struct VDa { int v; float da; };
+struct RecH { float m, den, P, da; int qd; };
 template <int H, int VPL>
-__global__ void __launch_bounds__(256, 3) k2_bsrc2_hub(const G2Args a) {
+__global__ void __launch_bounds__(256, 2) k2_bsrc2_hub(const G2Args a) {
   constexpr int SPW = 32 / H;
   const int lane = threadIdx.x & 31, h = lane % H;
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
@@ -1819,29 +1885,18 @@ __global__ void __launch_bounds__(256, 3) k2_bsrc2_hub(const G2Args a) {
     if (s.ok) {
       const int qs = a.qS[ug * H + h];
       float acc = 0.0f;
-      for (int64_t e0 = s.eb; e0 < s.ee; e0 += LSU) {
-        float da[LSU], mv[LSU], dv[LSU], pv[LSU];
-        int qd[LSU];
-#pragma unroll
-        for (int j = 0; j < LSU; ++j) {
-          const bool in = e0 + j < s.ee;
-          const int v = in ? __ldg(a.g.out_dst + e0 + j) : 0;
-          da[j] = in ? __ldcs(a.dal_out + (e0 + j) * H + h) : 0.0f;
-          const float* r = a.nrec + (int64_t)v * a.nrs;
-          mv[j] = r[h];
-          dv[j] = r[H + h];
-          pv[j] = r[2 * H + h];
-          qd[j] = reinterpret_cast<const int8_t*>(r + 3 * H)[h];
-        }
-#pragma unroll
-        for (int j = 0; j < LSU; ++j)
-          if (e0 + j < s.ee) {
+      lane_pipe<4, VDa, RecH>(
+          s.eb, s.ee, [&](int64_t e) { return VDa{(int)__ldg(a.g.out_dst + e), __ldcs(a.dal_out + e * H + h)}; },
+          [&](const VDa& x, int64_t) {
+            const float* r = a.nrec + (int64_t)x.v * a.nrs;
+            return RecH{r[h], r[H + h], r[2 * H + h], x.da, (int)reinterpret_cast<const int8_t*>(r + 3 * H)[h]};
+          },
+          [&](const RecH& y) {
             float ep;
-            const float al = alpha1(qs, qd[j], scS.s, scD.s, a.slope, mv[j], dv[j], ep);
-            const float dE = __fmul_rn(al, __fsub_rn(da[j], pv[j]));
+            const float al = alpha1(qs, y.qd, scS.s, scD.s, a.slope, y.m, y.den, ep);
+            const float dE = __fmul_rn(al, __fsub_rn(y.da, y.P));
             acc = __fadd_rn(acc, ep > 0.0f ? dE : __fmul_rn(dE, a.slope));
-          }
-      }
+          });
       __stcg(a.hs + s.slot * H + h, acc);
     }
     const bool last = lane_seg_last<H>(a.hcnt, s);

@@ -174,6 +174,14 @@ __device__ __forceinline__ int row_dot_biased(const Row<VPL>& x, const Row<VPL>&
   for (int i = 0; i < VPL / 4; ++i) acc = dp4a_us(x.w[i], y.w[i], acc);
   return acc - 128 * ysum;
 }
+// Σ (q_x + 128)·q_y of this lane's slice without the correction (applied after a cross-lane reduction)
+template <int VPL>
+__device__ __forceinline__ int row_dot_raw(const Row<VPL>& x, const Row<VPL>& y) {
+  int acc = 0;
+#pragma unroll
+  for (int i = 0; i < VPL / 4; ++i) acc = dp4a_us(x.w[i], y.w[i], acc);
+  return acc;
+}
 // Σ of this lane's plain codes (for the correction above); flips excess-128 codes to plain first
 template <int VPL>
 __device__ __forceinline__ int row_sum_plain(Row<VPL>& y, bool flip) {
