@@ -149,6 +149,14 @@ __device__ __forceinline__ void alpha_rec(const int8_t (&qs)[H], const DstSm<H>&
 }
 
 template <int H>
+__device__ __forceinline__ int8_t head_pick_i8(const int8_t (&x)[H], int h) {
+  int8_t r = 0;
+#pragma unroll
+  for (int k = 0; k < H; ++k) if (k == h) r = x[k];
+  return r;
+}
+
+template <int H>
 __host__ __device__ constexpr int hbatch() { return H >= 8 ? 32 : 64; }   // edges per staged batch of a hub chunk
 
 // ------------------------------------------------------------------ light tiles: segmented sums
@@ -292,6 +300,43 @@ __global__ void __launch_bounds__(256, 4) k2_fstats1(const G2Args a) {
     const int64_t vg = a.g.row_begin + s.vl;
     int8_t qd[H];
     load_qh<H>(a.qD + vg * H, qd);
+    if (a.slope > 0.0f) {
+      // e_pre (two rn products and one rn add, sS > 0) and LeakyReLU (slope > 0) are monotone
+      // non-decreasing in q_S[u], so max over the edges of el = lrelu(e_pre(max q_S)): the max is taken on
+      // the int8 codes (SIMD byte max over all heads at once) and converted once — the same value as the
+      // oracle's max of the el (no ±0 ties: el = −0 needs slope 0)
+      constexpr int NW = (H + 3) / 4;
+      uint32_t mw[NW];
+#pragma unroll
+      for (int k = 0; k < NW; ++k) mw[k] = 0x80808080u;
+      for (int64_t b = s.eb; b < s.ee; b += 128) {
+        int u[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u[k] = b + 32 * k + lane < s.ee ? __ldg(a.g.in_src + b + 32 * k + lane) : -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (u[k] >= 0) {
+            const int8_t* q = a.qS + (int64_t)u[k] * H;
+            if constexpr (H == 1) mw[0] = __vmaxs4(mw[0], 0x80808000u | (uint32_t)(uint8_t)__ldg(q));
+            else if constexpr (H == 2)
+              mw[0] = __vmaxs4(mw[0], 0x80800000u | (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(q)));
+            else {
+#pragma unroll
+              for (int w = 0; w < NW; ++w) mw[w] = __vmaxs4(mw[w], __ldg(reinterpret_cast<const unsigned*>(q) + w));
+            }
+          }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int w = 0; w < NW; ++w) mw[w] = __vmaxs4(mw[w], __shfl_xor_sync(0xffffffffu, mw[w], o));
+      if (lane < H) {
+        const int code = (int8_t)(mw[lane >> 2] >> (8 * (lane & 3)));
+        const float m = lrelu(sddmm_add1((int8_t)code, scS.s, head_pick_i8<H>(qd, lane), scD.s), a.slope);
+        atomicMax(reinterpret_cast<unsigned*>(a.nrec + vg * a.nrs) + lane, fkey(m));
+      }
+      continue;
+    }
     float mx[H];
 #pragma unroll
     for (int h = 0; h < H; ++h) mx[h] = -INFINITY;
@@ -2061,9 +2106,13 @@ cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st, const SideStream* 
       attr = true;                                                                                   \
     }                                                                                                \
     { ProfScope p("gat_fwd_stats1", st); k2_fstats1<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
-    if (a.lane_hubs) { ProfScope p("gat_fwd_stats_hub", st); k2_fstats2_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
-    { ProfScope p("gat_fwd_stats", st); k2_fstats2<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
-    e = fork2(st, x);                                                                                \
+    if (a.lane_hubs) { /* hub segments on the side stream beside the light sub-tiles */                \
+      e = fork2(st, x);                                                                              \
+      { ProfScope p("gat_fwd_stats_hub", sh); k2_fstats2_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
+      { ProfScope p("gat_fwd_stats", st); k2_fstats2<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
+      if (e == cudaSuccess) e = join2(st, x);                                                        \
+    } else { ProfScope p("gat_fwd_stats", st); k2_fstats2<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
+    if (e == cudaSuccess) e = fork2(st, x);                                                          \
     { ProfScope p("gat_fwd_agg_hub", sh); k2_fagg_seg<H_, V_><<<grid_items((a.pin.cap + 7) / 8, 3), 256, smem_s, sh>>>(a); } \
     { ProfScope p("gat_fwd_agg", st); k2_fagg<H_, V_><<<grid_items((a.pin.tcap + 7) / 8, 3), 256, smem, st>>>(a); } \
     if (e == cudaSuccess) e = join2(st, x);                                                          \
@@ -2095,12 +2144,21 @@ cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st, const SideStream* 
     { ProfScope p("gat_bwd_src_hub", sh); k2_bsrc1_seg<H_, V_, NW><<<grid_items((a.pout.cap + NW - 1) / NW, 20 / NW), NW * 32, smem_s, sh>>>(a); } \
     { ProfScope p("gat_bwd_src", st); k2_bsrc1<H_, V_, NW><<<grid_items((a.pout.tcap + NW - 1) / NW, 20 / NW), NW * 32, smem, st>>>(a); } \
     if (e == cudaSuccess) e = join2(st, x);                                                          \
-    if (a.lane_hubs) { ProfScope p("gat_bwd_dst_hub", st); k2_bdst_a_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
-    { ProfScope p("gat_bwd_dst", st); k2_bdst_a<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
-    if (a.lane_hubs) { ProfScope p("gat_bwd_dst2", st); k2_bdst_b_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
-    else { ProfScope p("gat_bwd_dst2", st); k2_bdst_b<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
-    if (a.lane_hubs) { ProfScope p("gat_bwd_src2_hub", st); k2_bsrc2_hub<H_, V_><<<grid_items((a.pout.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
-    { ProfScope p("gat_bwd_src2", st); k2_bsrc2<H_, V_><<<grid_items((a.pout.cap + a.pout.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
+    if (a.lane_hubs) { /* hub segments on the side stream beside the light sub-tiles (P2a, P3) */        \
+      if (e == cudaSuccess) e = fork2(st, x);                                                        \
+      { ProfScope p("gat_bwd_dst_hub", sh); k2_bdst_a_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
+      { ProfScope p("gat_bwd_dst", st); k2_bdst_a<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
+      if (e == cudaSuccess) e = join2(st, x);                                                        \
+      { ProfScope p("gat_bwd_dst2", st); k2_bdst_b_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
+      if (e == cudaSuccess) e = fork2(st, x);                                                        \
+      { ProfScope p("gat_bwd_src2_hub", sh); k2_bsrc2_hub<H_, V_><<<grid_items((a.pout.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
+      { ProfScope p("gat_bwd_src2", st); k2_bsrc2<H_, V_><<<grid_items((a.pout.cap + a.pout.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
+      if (e == cudaSuccess) e = join2(st, x);                                                        \
+    } else {                                                                                         \
+      { ProfScope p("gat_bwd_dst", st); k2_bdst_a<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
+      { ProfScope p("gat_bwd_dst2", st); k2_bdst_b<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
+      { ProfScope p("gat_bwd_src2", st); k2_bsrc2<H_, V_><<<grid_items((a.pout.cap + a.pout.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
+    }                                                                                                \
   }
   G2_CASES(X)
 #undef X
