@@ -435,6 +435,32 @@ def spmm_sweep_bench(T, torch, dg, g, F, args, l2_flush, peaks):
         del layer
         torch.cuda.empty_cache()
     res["note"] = "fused ⑤ aggregation of the layer forward; int8 rows, fp32 accumulation; arxiv graph"
+    # the same shapes through the standalone primitive tango_spmm_q (edge weights [E][H] fp32, int8 rows,
+    # canonical fp32 chunk sums), which has no HD <= 512 limit: the paper's (4 x 256) shape included
+    prim = {}
+    g_ = torch.Generator(device="cuda").manual_seed(7)
+    for H, D in ((2, 128), (4, 128), (2, 256), (4, 256)):
+        HD = H * D
+        qX = torch.randint(-127, 128, (g.n, HD), dtype=torch.int8, device="cuda", generator=g_)
+        sX = torch.full((1,), 0.01, device="cuda")
+        w = torch.rand((dg.e_in, H), device="cuda", generator=g_)
+        out = torch.empty((g.n, HD), device="cuda")
+        for _ in range(3):
+            T.spmm(dg, 0, qX, sX, HD, H, edge_w=w, out=out)
+        ts = []
+        for _ in range(max(5, args.steps)):
+            l2_flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            T.spmm(dg, 0, qX, sX, HD, H, edge_w=w, out=out)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        byts = dg.e_in * (4 + 4 * H + HD) + g.n * 4 * HD
+        prim[f"{H}x{D}"] = {"ms": round(ms, 4), "gbs": round(byts / (ms / 1e3) / 1e9, 1)}
+        del qX, w, out
+    res["primitive_tango_spmm_q"] = prim
     return res
 
 

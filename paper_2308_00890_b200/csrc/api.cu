@@ -681,17 +681,20 @@ G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_p
   a.da_part = (float*)(c + L.off_dapart);
   a.nrec = (float*)(c + L.off_nrec); a.nrs = gat2_nrec_stride(p->heads);
   a.in2out = (const int32_t*)(c + L.off_dal);
-  // P2's ∂α in in-CSR order: scattered by P1 (default) or gathered by P2 through the in2out map
+  // P2's ∂α in in-CSR order: gathered by P2 through the in2out map (default) or scattered there by P1
+  // (TANGO_P2_SCATTER=1: P2 reads coalesced, P1 pays the random 16-B stores — measured a wash on Reddit,
+  // profiles/r2x_*); hub segments of F-stats / P2 / P3: staged warp sums (default) or lane-parallel chunk
+  // sums (TANGO_HUB_LANE=1: latency-bound, no faster) — both variants stay parity-tested
   static const int scatter = [] {
-    const char* e = getenv("TANGO_P2_GATHER");
-    return (e && atoi(e)) ? 0 : 1;
-  }();
-  a.scatter_in = scatter;
-  static const int staged = [] {
-    const char* e = getenv("TANGO_HUB_STAGED");
+    const char* e = getenv("TANGO_P2_SCATTER");
     return (e && atoi(e)) ? 1 : 0;
   }();
-  a.lane_hubs = !staged;
+  a.scatter_in = scatter;
+  static const int lane = [] {
+    const char* e = getenv("TANGO_HUB_LANE");
+    return (e && atoi(e)) ? 1 : 0;
+  }();
+  a.lane_hubs = lane;
   a.codes_biased = 1;
   return a;
 }

@@ -1317,6 +1317,8 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
       const int v2 = edge_v(c + 2);
       RecRaw<H> r1;
       if ((c + 1) * 32 + lane < T) r1 = load_rec_raw<H>(a, v1);
+      // in-CSR slot of this chunk's edge (scatter of ∂α), loaded here so the store at the chunk end does not wait
+      const int ein = (a.scatter_in && c * 32 + lane < T) ? __ldcs(a.g.out_eid + eb + c * 32 + lane) : 0;
       const float* sac = sa + ((c & 1) * H + myh) * 32;
       for (int i0 = 0; i0 < 32; i0 += GR) {
         const int t0 = c * 32 + i0;
@@ -1376,7 +1378,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
         } else {
           st_h<H>(a.dal_out + (eb + c * 32 + lane) * H, o);
         }
-        if (a.scatter_in) st_h<H>(a.dal_in + (int64_t)__ldcs(a.g.out_eid + eb + c * 32 + lane) * H, o);
+        if (a.scatter_in) st_h<H>(a.dal_in + (int64_t)ein * H, o);
       }
       __syncwarp();
       if (c + 1 < nch) {
