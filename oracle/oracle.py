@@ -121,6 +121,7 @@ def lib():
         L.orc_softmax_bwd.argtypes = [C.POINTER(Graph), C.c_int, _P, _P, _P, C.c_float, _P, _P, _P]
         L.orc_edge_sum.argtypes = [C.POINTER(Graph), C.c_int, C.c_int, _P, _P]
         L.orc_spmm_sum.argtypes = [C.POINTER(Graph), C.c_int, C.c_int, QRef, _P, _P]
+        L.orc_spmm_q8.argtypes = [C.POINTER(Graph), C.c_int, C.c_int, C.c_int, _P, C.c_float, _P, C.c_float, _P, _P]
         L.orc_gemm.argtypes = [C.c_int64, C.c_int64, C.c_int64, QRef, C.c_int64, C.c_int, QRef, C.c_int64, C.c_int,
                                _P, _P]
         L.orc_gat_fwd.argtypes = [C.POINTER(Graph), C.POINTER(Cfg), _P, _P, _P, _P, C.POINTER(FwdOut)]
@@ -292,6 +293,18 @@ def edge_sum(g, direction, heads, x, chunk=256):
     out = np.zeros((g.n, heads), np.float32)
     _check(lib().orc_edge_sum(C.byref(gs), direction, heads, _p(x), _p(out)))
     return out
+
+
+def spmm_q8(g, direction, heads, cols, qa, sa, qx, sx):
+    """NEXT-4 int8-α SPMM (orc_spmm_q8): exact int32 sums of q_α·q_X and (float)acc · fl(s_α·s_X)."""
+    gs = graph_struct(g, 256)
+    qa = _c(qa, np.int8)
+    qx = _c(qx, np.int8)
+    oi = np.zeros((g.n, cols), np.int32)
+    of = np.zeros((g.n, cols), np.float32)
+    _check(lib().orc_spmm_q8(C.byref(gs), direction, heads, cols, _p(qa), C.c_float(sa), _p(qx), C.c_float(sx),
+                             _p(oi), _p(of)))
+    return oi, of
 
 
 def spmm_sum(g, direction, cols, X: QRef, chunk=256):

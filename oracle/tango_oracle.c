@@ -464,6 +464,38 @@ int orc_edge_sum(const orc_graph* g, int dir, int heads, const float* x, float* 
 /* dir 0: w = sources of in-edges of v;  dir 1: w = destinations of v's      */
 /* out-edges.  Bypass: double accumulation.  Output as float (exact int).    */
 /* ------------------------------------------------------------------------- */
+/* NEXT-4 int8-α SPMM (the edge-feature quantization of P:900-902 applied to the attention
+ * coefficients): with α quantized to int8 codes q_α [e][heads] (scale s_α, the same SR quantizer as every
+ * other tensor), the aggregation is an exact integer sum, order-free:
+ *   acc[v][j] = Σ_{e→v} q_α[e][h(j)] · q_X[w_e][j]   (int64 here; |acc| < 2^31 for deg < 133,144)
+ *   out[v][j] = (float)acc · fl(s_α · s_X)            (one i2f, one rn multiply)
+ * dir 0: in-edges of v (w_e = source, α in in-CSR order); dir 1: out-edges (w_e = destination, α of the
+ * edge's in-CSR slot).  Pinned by the brute-force dense product in tests/test_oracle_dense.py. */
+int orc_spmm_q8(const orc_graph* g, int dir, int heads, int cols, const int8_t* qa, float sa, const int8_t* qx,
+                float sx, int32_t* out_i32, float* out_f) {
+  orc_rev rv = {0};
+  if (dir == 1 && orc_build_rev(g, &rv)) return ORC_ERR_ALLOC;
+  const int hd = cols / heads;
+  const float s = sa * sx;
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t v = 0; v < g->n; ++v) {
+    const int64_t* ptr = dir ? rv.ptr : g->in_ptr;
+    int64_t b = ptr[v], len = ptr[v + 1] - b;
+    for (int j = 0; j < cols; ++j) {
+      int64_t acc = 0;
+      for (int64_t i = 0; i < len; ++i) {
+        int64_t eid = dir ? rv.eid[b + i] : (b + i);
+        int64_t w = dir ? rv.dst[b + i] : g->in_src[b + i];
+        acc += (int64_t)qa[eid * heads + j / hd] * (int64_t)qx[w * cols + j];
+      }
+      if (out_i32) out_i32[v * cols + j] = (int32_t)acc;
+      if (out_f) out_f[v * cols + j] = (float)acc * s;
+    }
+  }
+  if (dir == 1) orc_free_rev(&rv);
+  return ORC_OK;
+}
+
 int orc_spmm_sum(const orc_graph* g, int dir, int cols, orc_qref X, int32_t* out_i32, float* out_f) {
   orc_rev rv = {0};
   if (dir == 1 && orc_build_rev(g, &rv)) return ORC_ERR_ALLOC;

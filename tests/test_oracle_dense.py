@@ -140,3 +140,28 @@ def test_chunking_changes_only_rounding(orc):
     _, den2, a2 = orc.edge_softmax(gr, 2, el, chunk=3)
     assert np.allclose(den1, den2, rtol=1e-6)
     assert np.allclose(a1, a2, rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("heads,hd", [(1, 5), (2, 4), (4, 3)])
+def test_spmm_q8_dense(orc, case, heads, hd):
+    """NEXT-4 int8-α SPMM vs the dense product: out_i32 = (G ⊙ q_α)·q_X per head (int64 brute force, exact), in
+    both directions (dir 1 = the reversed graph, α taken at each edge's in-CSR slot), and the float output
+    = (float)acc · fl(s_α·s_X)."""
+    gr, rng = case
+    cols = heads * hd
+    qa = rng.integers(-127, 128, size=(gr.e, heads)).astype(np.int8)
+    qx = rng.integers(-127, 128, size=(gr.n, cols)).astype(np.int8)
+    sa, sx = np.float32(0.0071), np.float32(0.013)
+    dst, src = gr.in_dst(), gr.in_src
+    for direction in (0, 1):
+        ref = np.zeros((gr.n, cols), np.int64)
+        for h in range(heads):
+            A = np.zeros((gr.n, gr.n), np.int64)          # A[row, other endpoint] = q_α of the edge
+            if direction == 0:
+                A[dst, src] = qa[:, h]
+            else:
+                A[src, dst] = qa[:, h]
+            ref[:, h * hd:(h + 1) * hd] = A @ qx[:, h * hd:(h + 1) * hd].astype(np.int64)
+        oi, of = orc.spmm_q8(gr, direction, heads, cols, qa, sa, qx, sx)
+        assert np.array_equal(oi.astype(np.int64), ref)
+        assert np.array_equal(of, ref.astype(np.float32) * np.float32(sa * sx))
