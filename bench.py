@@ -458,8 +458,26 @@ def spmm_sweep_bench(T, torch, dg, g, F, args, l2_flush, peaks):
             ts.append(e0.elapsed_time(e1))
         ms = statistics.median(ts)
         byts = dg.e_in * (4 + 4 * H + HD) + g.n * 4 * HD
-        prim[f"{H}x{D}"] = {"ms": round(ms, 4), "gbs": round(byts / (ms / 1e3) / 1e9, 1)}
-        del qX, w, out
+        ent = {"ms": round(ms, 4), "gbs": round(byts / (ms / 1e3) / 1e9, 1)}
+        # NEXT-4 int8-α variant (tango_spmm_q8): α quantized to int8, exact int32 sums (IDP4A on transposed codes)
+        qa, sa, _ = T.quantize(w, bits=8, ld=H, tag=0x55)
+        oi = torch.empty((g.n, HD), dtype=torch.int32, device="cuda")
+        for _ in range(3):
+            T.spmm_q8(dg, 0, qa, sa, qX, sX, HD, H, out=out, out_i32=oi)
+        ts = []
+        for _ in range(max(5, args.steps)):
+            l2_flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            T.spmm_q8(dg, 0, qa, sa, qX, sX, HD, H, out=out, out_i32=oi)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms8 = statistics.median(ts)
+        ent["int8_alpha_ms"] = round(ms8, 4)
+        ent["int8_alpha_speedup"] = round(ms / ms8, 3)
+        prim[f"{H}x{D}"] = ent
+        del qX, w, out, qa, oi
     res["primitive_tango_spmm_q"] = prim
     return res
 

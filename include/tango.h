@@ -186,6 +186,18 @@ tango_status tango_spmm_q(const tango_graph* G, int32_t dir, const float* edge_w
                           int32_t heads, const float* row_scale, float* out, int32_t* out_i32, float* amax_out,
                           cudaStream_t stream);
 
+/* NEXT-4 int8-α SPMM (edge-feature quantization P:900-902 applied to α): the edge weights
+ * are int8 codes Aq (rows = e_in or e_out edges in in-CSR slot order, cols = heads, ld = heads, scale
+ * Aq->scale, e.g. from tango_quantize of α), so the aggregation is an exact, order-free int32 sum:
+ *   out_i32[v,j] = Σ_e Aq[e,h(j)]·q_X[w_e,j]   (dir TANGO_IN: in-edges, w_e = source, Aq in in-CSR order;
+ *                                            dir TANGO_OUT: out-edges, w_e = destination, Aq[out_eid[e]])
+ *   out[v,j] (nullable) = i2f(out_i32[v,j]) · fl(s_α·s_X)
+ * out_i32 [n_local][cols] is required (it is also the accumulator; zeroed by the call), 16-B aligned.
+ * Requires cols = heads·D with D % 4 == 0, X->ld % 4 == 0 and X->q 4-B aligned: TANGO_ERR_UNSUPPORTED
+ * otherwise.  Exactness needs deg·127² < 2³¹ (deg < 133,144): TANGO_ERR_OVERFLOW is not checked per row. */
+tango_status tango_spmm_q8(const tango_graph* G, int32_t dir, const tango_qtensor* Aq, const tango_qtensor* X,
+                           int32_t heads, int32_t* out_i32, float* out, cudaStream_t stream);
+
 /* Incidence-matrix SPMM for edge features (③″/③′):        */
 /* out[v,h] = Σᶜ x[e,h] over the in-edges (dir IN) or out-edges (dir OUT).    */
 tango_status tango_edge_sum(const tango_graph* G, int32_t dir, int32_t heads, const float* x, float* out,

@@ -512,6 +512,23 @@ tango_status tango_spmm_q(const tango_graph* G, int32_t dir, const float* edge_w
       launch_spmm_sum(g, dir, (int)X->cols, X->q, X->ld, X->scale, row_scale, out, out_i32, amax, stream));
 }
 
+tango_status tango_spmm_q8(const tango_graph* G, int32_t dir, const tango_qtensor* Aq, const tango_qtensor* X,
+                           int32_t heads, int32_t* out_i32, float* out, cudaStream_t stream) {
+  TRY(check_graph(G, dir == TANGO_OUT));
+  TRY(check_q(Aq));
+  TRY(check_q(X));
+  if (dir != TANGO_IN && dir != TANGO_OUT) return TANGO_ERR_INVALID_ARG;
+  if (!out_i32) return TANGO_ERR_INVALID_ARG;
+  if (dir == TANGO_OUT && G->e_out > 0 && !G->out_eid) return TANGO_ERR_INVALID_ARG;
+  if (heads <= 0 || X->cols % heads || X->rows != G->n_global) return TANGO_ERR_SHAPE;
+  if (Aq->cols != heads || Aq->ld != heads || Aq->rows != G->e_in) return TANGO_ERR_SHAPE;
+  const int64_t D = X->cols / heads;
+  if (D % 4 || X->ld % 4 || (reinterpret_cast<uintptr_t>(X->q) & 3) || (reinterpret_cast<uintptr_t>(out_i32) & 15))
+    return TANGO_ERR_UNSUPPORTED;
+  return launch_status(launch_spmm_q8(dev_graph(G), dir, heads, (int)X->cols, Aq->q, Aq->scale, X->q, X->ld,
+                                      X->scale, out_i32, out, dir == TANGO_OUT ? G->e_out : G->e_in, stream));
+}
+
 tango_status tango_edge_sum(const tango_graph* G, int32_t dir, int32_t heads, const float* x, float* out,
                             cudaStream_t stream) {
   TRY(check_graph(G, dir == TANGO_OUT));

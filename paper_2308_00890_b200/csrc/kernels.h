@@ -194,6 +194,9 @@ cudaError_t launch_edge_sum(const GraphDev& g, int dir, int heads, const float* 
 cudaError_t launch_spmm_w(const GraphDev& g, int dir, int heads, int cols, const float* w, const int8_t* qX,
                           int64_t ldx, const float* sX, const float* rowscale, float* out, unsigned* amax_out,
                           int64_t e_list, cudaStream_t st);
+cudaError_t launch_spmm_q8(const GraphDev& g, int dir, int heads, int cols, const int8_t* qa, const float* sa,
+                           const int8_t* qX, int64_t ldx, const float* sX, int32_t* out_i32, float* out,
+                           int64_t e_list, cudaStream_t st);
 cudaError_t launch_spmm_sum(const GraphDev& g, int dir, int cols, const int8_t* qX, int64_t ldx, const float* sX,
                             const float* rowscale, float* out, int32_t* out_i32, unsigned* amax_out,
                             cudaStream_t st);

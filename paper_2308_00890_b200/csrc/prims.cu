@@ -440,6 +440,130 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int head
   }
 }
 
+// ---------------------------------------------------------------------------- int8-α SPMM (NEXT-4)
+// acc[v,j] = Σ q_α[e,h(j)]·q_X[w_e,j] (exact int32, order-free), out = i2f(acc)·fl(s_α·s_X) (orc_spmm_q8).
+// The same edge-window blocks and chunk items as tango_spmm_q; a warp sums one (item, 128-column pass): per
+// 32-edge batch the lanes stage the batch's gather rows and α codes ([head][edge] bytes) in shared memory;
+// every lane then takes its 4 columns (one 32-bit word) of 4 gathered rows at a time, transposes the 4x4
+// bytes (8 PRMT) and adds 4 IDP4A dots against the 4 edges' α codes of its head — 16 products in 12
+// instructions instead of the fp32 path's 2 per product.  Integer sums are order-free, so a multi-chunk row
+// adds its chunks with int32 atomics (out_i32 zeroed first); a second pass writes the fp32 output.
+__device__ __forceinline__ void transpose4(uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3, uint32_t (&t)[4]) {
+  const uint32_t a = __byte_perm(r0, r1, 0x5140), b = __byte_perm(r2, r3, 0x5140);
+  const uint32_t c = __byte_perm(r0, r1, 0x7362), d = __byte_perm(r2, r3, 0x7362);
+  t[0] = __byte_perm(a, b, 0x5410); t[1] = __byte_perm(a, b, 0x7632);
+  t[2] = __byte_perm(c, d, 0x5410); t[3] = __byte_perm(c, d, 0x7632);
+}
+
+template <int DIR>
+__global__ void __launch_bounds__(ES_THREADS) k_spmm_q8(GraphDev g, int heads, int cols, int64_t epb, int64_t E,
+                                                       const int8_t* __restrict__ qa, const int8_t* __restrict__ qX,
+                                                       int64_t ldx, int32_t* __restrict__ out_i32) {
+  extern __shared__ __align__(16) uint8_t q8_dyn[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* su = reinterpret_cast<int*>(q8_dyn) + wid * 32;                                    // [32] rows
+  uint8_t* sa = q8_dyn + (ES_THREADS / 32) * 32 * 4 + wid * 32 * heads;                  // [heads][32]
+  __shared__ int s_pre[ES_ROWS];
+  const int64_t* __restrict__ ptr = DIR ? g.out_ptr : g.in_ptr;
+  const int32_t* __restrict__ nbr = DIR ? g.out_dst : g.in_src;
+  const int64_t n = g.n_local, C = g.chunk;
+  const int D = cols / heads, npass = (cols + SW_COLS - 1) / SW_COLS;
+  auto lower = [&](int64_t key) {
+    int64_t a = 0, b = n;
+    while (a < b) {
+      const int64_t m = (a + b) >> 1;
+      if (ptr[m] < key) a = m + 1; else b = m;
+    }
+    return a;
+  };
+  const int64_t lo = (int64_t)blockIdx.x * epb, hi = lo + epb;
+  if (lo > E) return;
+  const int64_t r0 = lower(lo), r1 = hi > E ? n : lower(hi);
+  auto chunks = [&](int64_t r) -> int64_t {
+    const int64_t d = ptr[r + 1] - ptr[r];
+    return d <= C ? 1 : (d + C - 1) / C;
+  };
+  // integer dot sums of list positions [pb, pe) for the lane's 4 columns j0 .. j0+3 (one head: D % 4 == 0)
+  auto chunk_dot = [&](int64_t pb, int64_t pe, int j0, int (&acc)[4]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c] = 0;
+    const int h = j0 < cols ? j0 / D : 0;
+    for (int64_t b0 = pb; b0 < pe; b0 += 32) {
+      const int nb = (int)(pe - b0 < 32 ? pe - b0 : 32);
+      __syncwarp();
+      {
+        const int64_t p = b0 + lane;
+        const bool in = lane < nb;
+        const int64_t e = in ? (DIR ? (int64_t)g.out_eid[p] : p) : 0;
+        su[lane] = in ? nbr[p] : 0;
+        for (int k = 0; k < heads; ++k) sa[k * 32 + lane] = in ? (uint8_t)qa[e * heads + k] : 0;   // pad: α code 0
+      }
+      __syncwarp();
+      for (int i0 = 0; i0 < nb; i0 += 4) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          w[i] = j0 < cols ? __ldg(reinterpret_cast<const unsigned*>(qX + (int64_t)su[i0 + i] * ldx + j0)) : 0u;
+        uint32_t t[4];
+        transpose4(w[0], w[1], w[2], w[3], t);
+        const int wa = *reinterpret_cast<const int*>(sa + h * 32 + i0);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c] = __dp4a((int)t[c], wa, acc[c]);
+      }
+    }
+  };
+  int64_t row = r0;
+  while (row < r1) {
+    const int64_t rr = row + threadIdx.x;
+    // rows per batch: up to ES_ROWS, no item cap (multi-chunk rows add their chunks atomically)
+    const int64_t c = (threadIdx.x < ES_ROWS && rr < r1) ? chunks(rr) : 0;
+    int v = (int)(c > (1 << 20) ? (1 << 20) : c);
+    s_pre[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < ES_ROWS; off <<= 1) {
+      const int add = threadIdx.x >= off ? s_pre[threadIdx.x - off] : 0;
+      __syncthreads();
+      v += add;
+      s_pre[threadIdx.x] = v;
+      __syncthreads();
+    }
+    const int nb = (int)((r1 - row) < ES_ROWS ? (r1 - row) : ES_ROWS);
+    const int nitems = s_pre[nb - 1];
+    for (int cp = 0; cp < npass; ++cp) {
+      for (int it = wid; it < nitems; it += ES_THREADS / 32) {
+        int a = 0, b = nb - 1;
+        while (a < b) {
+          const int m = (a + b) >> 1;
+          if (s_pre[m] > it) b = m; else a = m + 1;
+        }
+        const int j = a, k = it - (j ? s_pre[j - 1] : 0);
+        const int64_t r = row + j, pb0 = ptr[r], pe0 = ptr[r + 1];
+        const int64_t pb = pb0 + (int64_t)k * C, pe = pb + C < pe0 ? pb + C : pe0;
+        const int j0 = cp * SW_COLS + lane * 4;
+        int acc[4];
+        chunk_dot(pb, pe, j0, acc);
+        if (j0 < cols) {
+          if (pe0 - pb0 <= C) {
+            *reinterpret_cast<int4*>(out_i32 + r * cols + j0) = make_int4(acc[0], acc[1], acc[2], acc[3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) atomicAdd(out_i32 + r * cols + j0 + q, acc[q]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    row += nb;
+  }
+}
+
+__global__ void k_i32_to_f32(const int32_t* __restrict__ acc, int64_t count, const float* sa, const float* sx,
+                             float* __restrict__ out) {
+  const float s = __fmul_rn(*sa, *sx);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __fmul_rn(__int2float_rn(acc[i]), s);
+}
+
 // Unweighted int32 SPMM (GCN; exact, order-free).  Warp per row, lanes over columns (coalesced rows).
 // out = ((float)sum * s_X) * rowscale[row] (optional), amax over |out| (optional).
 __global__ void __launch_bounds__(256) k_spmm_sum(GraphDev g, int dir, int cols, const int8_t* qX, int64_t ldx,
@@ -560,6 +684,38 @@ cudaError_t launch_spmm_w(const GraphDev& g, int dir, int heads, int cols, const
   }
   f<<<(unsigned)blocks, ES_THREADS, smem, st>>>(g, heads, cols, epb, e_list, w, qX, ldx, sX, rowscale, out, amax_out);
   return cudaGetLastError();
+}
+cudaError_t launch_spmm_q8(const GraphDev& g, int dir, int heads, int cols, const int8_t* qa, const float* sa,
+                           const int8_t* qX, int64_t ldx, const float* sX, int32_t* out_i32, float* out,
+                           int64_t e_list, cudaStream_t st) {
+  if (g.n_local == 0) return cudaSuccess;
+  cudaError_t err = cudaMemsetAsync(out_i32, 0, (size_t)g.n_local * cols * 4, st);
+  if (err != cudaSuccess) return err;
+  {
+    ProfScope ps("spmm_q8", st);
+    const int64_t e = e_list > 0 ? e_list : 1;
+    int64_t epb = e / ((int64_t)num_sms() * 4);
+    epb = epb < 256 ? 256 : (epb > 16384 ? 16384 : epb);
+    const int64_t blocks = e_list / epb + 1;
+    const size_t smem = (size_t)(ES_THREADS / 32) * 32 * (4 + heads);
+    auto f = dir ? k_spmm_q8<1> : k_spmm_q8<0>;
+    if (smem > 48 * 1024) {
+      err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (err != cudaSuccess) return err;
+    }
+    f<<<(unsigned)blocks, ES_THREADS, smem, st>>>(g, heads, cols, epb, e_list, qa, qX, ldx, out_i32);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+  }
+  if (out) {
+    ProfScope ps("spmm_q8_out", st);
+    const int64_t count = g.n_local * (int64_t)cols;
+    int64_t gr = (count + 255) / 256;
+    if (gr > (int64_t)num_sms() * 8) gr = (int64_t)num_sms() * 8;
+    k_i32_to_f32<<<(unsigned)gr, 256, 0, st>>>(out_i32, count, sa, sX, out);
+    err = cudaGetLastError();
+  }
+  return err;
 }
 cudaError_t launch_spmm_sum(const GraphDev& g, int dir, int cols, const int8_t* qX, int64_t ldx, const float* sX,
                             const float* rowscale, float* out, int32_t* out_i32, unsigned* amax_out,

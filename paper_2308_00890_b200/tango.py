@@ -109,7 +109,7 @@ EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tan
            "tango_gat_out_ctx_bytes", "tango_gat_out_fwd", "tango_gat_out_bwd", "tango_gat_out_ctx_get_view",
            "tango_gcn_out_ctx_bytes", "tango_gcn_out_fwd", "tango_gcn_out_bwd", "tango_gcn_out_ctx_get_view",
            "tango_quantize_int4", "tango_sddmm_qn", "tango_set_l2_fetch_granularity", "tango_comm_set_options",
-           "tango_comm_reserve", "tango_comm_nccl_calls"]
+           "tango_comm_reserve", "tango_comm_nccl_calls", "tango_spmm_q8"]
 
 
 def load(path: str = LIB_PATH):
@@ -137,6 +137,7 @@ def load(path: str = LIB_PATH):
     L.tango_comm_set_options.argtypes = [_P, i32]
     L.tango_comm_reserve.argtypes = [_P, sz]
     L.tango_comm_nccl_calls.argtypes = [_P]
+    L.tango_spmm_q8.argtypes = [PG, i32, PQ, PQ, i32, _P, _P, _P]
     L.tango_comm_nccl_calls.restype = C.c_int64
     L.tango_gat_ctx_bytes.restype = sz
     L.tango_gat_ctx_bytes.argtypes = [PG, C.POINTER(GatParams)]
@@ -396,6 +397,20 @@ def spmm(graph: DeviceGraph, direction, qX, sX, cols, heads, edge_w=None, row_sc
     _check(L.tango_spmm_q(graph.ref(), direction, _ptr(edge_w), C.byref(x), heads, _ptr(row_scale), _ptr(out),
                           _ptr(oi), _ptr(amax_out), _stream()), "tango_spmm_q")
     return out, oi
+
+
+def spmm_q8(graph: DeviceGraph, direction, qa, sa, qX, sX, cols, heads, out=None, out_i32=None, want_f32=True):
+    """tango_spmm_q8 (NEXT-4 int8-α SPMM): qa int8 [e_in, heads] edge codes (in-CSR slot order) with scale sa,
+    qX int8 [N, ld] node codes; returns (out f32 or None, out_i32)."""
+    L = load()
+    a = QTensor(_ptr(qa), _ptr(sa), qa.shape[0], heads, heads, 8)
+    x = QTensor(_ptr(qX), _ptr(sX), qX.shape[0], cols, qX.shape[1], 8)
+    out_i32 = out_i32 if out_i32 is not None else torch.empty((graph.n_local, cols), dtype=torch.int32, device="cuda")
+    if want_f32 and out is None:
+        out = torch.empty((graph.n_local, cols), dtype=torch.float32, device="cuda")
+    _check(L.tango_spmm_q8(graph.ref(), direction, C.byref(a), C.byref(x), heads, _ptr(out_i32),
+                           _ptr(out) if want_f32 else None, _stream()), "tango_spmm_q8")
+    return (out if want_f32 else None), out_i32
 
 
 def edge_sum(graph: DeviceGraph, direction, heads, x, out=None):

@@ -247,3 +247,35 @@ def test_quantize_without_amax_slot(T, orc):
     q, s, _ = T.quantize(cu(x), bits=8, ld=128, want_amax=False)
     oq, os_, _ = orc.quantize(x, bits=8)
     assert np.array_equal(q.cpu().numpy()[:, :100], oq) and s.item() == os_
+
+
+# NEXT-4 int8-α SPMM (tango_spmm_q8): α codes from the SR quantizer, exact int32 sums — bit-exact vs
+# orc_spmm_q8, both directions, ragged column passes (cols not a multiple of 128), hub rows split into
+# chunks that add atomically (C_E = 7), heads 1/2/4.
+@pytest.mark.parametrize("name", ["noself", "hub"])
+@pytest.mark.parametrize("H,D,ld,chunk", [(4, 128, 512, 256), (2, 48, 96, 7), (1, 36, 40, 64), (4, 64, 256, 1)])
+def test_spmm_q8_parity(T, orc, name, H, D, ld, chunk):
+    gr = _es_graph(name)
+    dg = T.DeviceGraph(gr, chunk=chunk)
+    rng = np.random.default_rng(H * 7 + D)
+    cols = H * D
+    qX = _rand_i8(rng, (gr.n, ld))
+    sX = np.float32(0.0173)
+    alpha = rng.random((gr.e, H)).astype(np.float32)
+    qa, sa, _ = T.quantize(cu(alpha), bits=8, ld=H, tag=0x55)
+    qa_np, sa_np = qa.cpu().numpy(), np.float32(sa.item())
+    for direction in (0, 1):
+        ri, rf = orc.spmm_q8(gr, direction, H, cols, qa_np, sa_np, qX[:, :cols], sX)
+        out, oi = T.spmm_q8(dg, direction, qa, sa, cu(qX), cu(np.array([sX])), cols, H)
+        assert np.array_equal(oi.cpu().numpy(), ri), direction
+        assert np.array_equal(out.cpu().numpy(), rf), direction
+
+
+def test_spmm_q8_validation(T):
+    gr = _es_graph("noself")
+    dg = T.DeviceGraph(gr)
+    qa = torch.zeros((gr.e, 2), dtype=torch.int8, device="cuda")
+    s = torch.ones(1, device="cuda")
+    qX = torch.zeros((gr.n, 12), dtype=torch.int8, device="cuda")
+    with pytest.raises(T.TangoError):          # D = 6: a lane's 4 columns would straddle two heads
+        T.spmm_q8(dg, 0, qa, s, qX, s, 12, 2)
