@@ -398,43 +398,12 @@ def sddmm_bits_bench(T, torch, dg, g, args, l2_flush, peaks):
 
 
 def spmm_sweep_bench(T, torch, dg, g, F, args, l2_flush, peaks):
-    """NEXT-4 shape sweep of the multi-head SPMM ⑤ (node features H x D, edge features
-    H x 1, shapes (2,128) (4,128) (2,256) (4,256)) on the arxiv-shaped graph: the fused aggregation of
-    the layer forward (light sub-tiles + hub segments + hub combine), eager with the side-stream work
-    serialised, L2 flushed before each forward; algorithmic GB/s with each gathered row counted once
-    per edge."""
-    res = {}
-    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    X = cu(inputs.features(g.n, F))
-    for H, D in ((2, 128), (4, 128), (2, 256), (4, 256)):
-        key = f"{H}x{D}"
-        try:
-            W, a_s, a_d = inputs.gat_params(F, H, D)
-            layer = T.GATLayer(dg, cu(W), cu(a_s), cu(a_d), H, D, slope=0.2, bits=8)
-        except T.TangoError as e:
-            res[key] = {"unsupported": str(e)}
-            continue
-        out = torch.empty((g.n, H * D), device="cuda")
-        for i in range(3):
-            layer.forward(X, step=i, out=out)
-        torch.cuda.synchronize()
-        T.profile_enable(True)
-        T.profile_serialize(True)
-        T.profile_read(reset=True)
-        for i in range(args.steps):
-            l2_flush.zero_()
-            layer.forward(X, step=3 + i, out=out)
-        torch.cuda.synchronize()
-        prof = T.profile_read(reset=True)
-        T.profile_enable(False)
-        T.profile_serialize(False)
-        ms = sum(prof[k][0] for k in ("gat_fwd_agg", "gat_fwd_agg_hub", "gat_fwd_combine") if k in prof) / args.steps
-        HD = H * D
-        byts = dg.e_in * (4 + 4 * H + HD) + g.n * 4 * HD
-        res[key] = {"ms": round(ms, 4), "gbs": round(byts / (ms / 1e3) / 1e9, 1)}
-        del layer
-        torch.cuda.empty_cache()
-    res["note"] = "fused ⑤ aggregation of the layer forward; int8 rows, fp32 accumulation; arxiv graph"
+    """NEXT-4 shape sweep of the multi-head SPMM ⑤ (node features H x D, edge features H x 1,
+    shapes (2,128) (4,128) (2,256) (4,256)) on the arxiv-shaped graph through the standalone primitive
+    tango_spmm_q (fp32 edge weights, int8 rows, canonical fp32 chunk sums) and its int8-α variant
+    tango_spmm_q8; device time per call, L2 flushed before each call, algorithmic GB/s with each gathered
+    row counted once per edge.  (The layer's own fused ⑤ is timed per pass in the main line.)"""
+    res = {"note": "standalone ⑤ primitive (tango_spmm_q) and its int8-α variant (tango_spmm_q8); arxiv graph"}
     # the same shapes through the standalone primitive tango_spmm_q (edge weights [E][H] fp32, int8 rows,
     # canonical fp32 chunk sums), which has no HD <= 512 limit: the paper's (4 x 256) shape included
     prim = {}

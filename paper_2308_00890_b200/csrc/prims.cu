@@ -1,11 +1,11 @@
 // prims.cu — the unfused sparse primitives of the C ABI (tango_sddmm_q, tango_edge_softmax,
 // tango_softmax_bwd, tango_edge_sum, tango_spmm_q) and the GCN helpers.  tango_edge_sum (the paper's
-// incidence SPMM, Table 2) is a bandwidth kernel (edge-window blocks, chunk items); the others run one
+// incidence SPMM, Table 2), tango_spmm_q and tango_spmm_q8 are row-block kernels with chunk items; the others run one
 // thread per (row, head) or (row, column), sequential over the row's edges in canonical order: the
 // same arithmetic as the fused kernels of gat.cu / gat2.cu, laid out for clarity rather than speed.
 // Paper: ③ P:204-209, ④ P:212-217, ⑤/⑤′ P:224-251, ⑤″ P:252-255, ④′ P:258-264,
 // ③′/③″ P:276 and P:821-832, GCN P:347-348.
-#include "rowops.cuh"
+#include "gat_common.cuh"
 
 namespace tango {
 // One thread per (row, head) or (row, column), sequential over the row's edges in canonical order:
@@ -92,8 +92,8 @@ __global__ void k_softmax_bwd(GraphDev g, int heads, const float* alpha, const f
 // ---------------------------------------------------------------------------- incidence SPMM (③′ / ③″)
 // out[v,h] = Σᶜ x[e,h] over v's in-edges (dir 0, contiguous in-CSR edge records: a streaming read) or
 // out-edges (dir 1, records out_eid[p]: a gather of F-float rows), reading R14.
-// Edge-window blocks: block b owns the rows whose edge list starts in [b·EPB, (b+1)·EPB) (a binary
-// search of the CSR pointer, no plan); its rows are cut into canonical chunks ("items", ≤ C_E edges).  A
+// Row blocks: block b owns rows [256·b, 256·b + 256) (no plan, no search); its rows are cut into canonical
+// chunks ("items", ≤ C_E edges), so a hub row's chunks are spread over the block's 8 warps.  A
 // group of GW = ceil(F / VW) lanes sums one item sequentially, each lane VW consecutive columns (float4 /
 // float2 / float loads), so a group's load of one edge record is one contiguous 4F-byte run; 16 floats
 // per lane are in flight (16 / VW records) and the blocks run at 4 per SM (32 warps).  A
@@ -134,17 +134,8 @@ __global__ void __launch_bounds__(ES_THREADS, 4) k_edge_sum_w(GraphDev g, int F,
   const int32_t* __restrict__ eid = g.out_eid;
   const int64_t n = g.n_local, C = g.chunk;
   const int slots = es_slots(F);
-  auto lower = [&](int64_t key) {   // first row r in [0, n] with ptr[r] >= key
-    int64_t a = 0, b = n;
-    while (a < b) {
-      const int64_t m = (a + b) >> 1;
-      if (ptr[m] < key) a = m + 1; else b = m;
-    }
-    return a;
-  };
-  const int64_t lo = (int64_t)blockIdx.x * epb, hi = lo + epb;
-  if (lo > E) return;
-  const int64_t r0 = lower(lo), r1 = hi > E ? n : lower(hi);
+  (void)epb; (void)E;
+  const int64_t r0 = (int64_t)blockIdx.x * ES_ROWS, r1 = r0 + ES_ROWS < n ? r0 + ES_ROWS : n;   // the block's rows
   const int nv = (F + VW - 1) / VW;                 // vectors per record
   const int GW = nv < 32 ? nv : 32, GPW = 32 / GW, ncb = (nv + 31) / 32;
   const int lane = threadIdx.x & 31, grp = (threadIdx.x >> 5) * GPW + lane / GW, gl = lane % GW;
@@ -256,45 +247,39 @@ __global__ void __launch_bounds__(ES_THREADS, 4) k_edge_sum_w(GraphDev g, int F,
 // ---------------------------------------------------------------------------- weighted SPMM ⑤ / ⑤′
 // out[v,j] = ((Σᶜ fmaf(w[e,h(j)], i2f(q_X[u_e,j]))) · s_X) [· row_scale[v]] over v's in-edges (dir 0, u_e =
 // source) or out-edges (dir 1, u_e = destination, weight w[out_eid[p]]), R14.  The
-// same edge-window blocks and chunk items as tango_edge_sum; a WARP sums one (item, 128-column pass): per
-// 32-edge batch the lanes load the batch's gather rows and weights in parallel into per-warp shared memory,
-// then every lane streams its 4 columns (one 32-bit word) of each gathered row, 8 rows in flight, fp32
-// fmaf in edge order.  Multi-chunk rows fold their chunk partials left to right after a barrier.
-constexpr int SW_COLS = 128;
+// same row blocks and chunk items as tango_edge_sum; a WARP sums one (item, 32·V-column pass): per 32-edge
+// batch the lanes load the batch's gather rows and weights in parallel into per-warp shared memory, then
+// every lane streams its V columns (V = 16: one 16-B load, 4: one word, 1: bytes) of each gathered row, 8
+// rows in flight, with the exact int8 -> fp32 conversion (PRMT + FADD2) and packed FFMA2 in edge order
+// (bit-identical to fmaf).  Multi-chunk rows fold their chunk partials left to right after a barrier.
+template <int V>
+__host__ __device__ constexpr int sw_cols() { return 32 * V; }
+template <int V>
+__host__ __device__ constexpr int sw_slots() { return V == 16 ? 16 : 64; }
 
-__host__ __device__ inline int sw_slots() { return 64; }
-
-template <int DIR, bool WORD>
+template <int DIR, int V>
 __global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int heads, int cols, int64_t epb, int64_t E,
                                                            const float* __restrict__ w, const int8_t* __restrict__ qX,
                                                            int64_t ldx, const float* __restrict__ sX,
                                                            const float* __restrict__ rowscale, float* __restrict__ out,
                                                            unsigned* amax_out) {
   extern __shared__ __align__(16) float sw_dyn[];
+  constexpr int SW_COLS = sw_cols<V>();
   float* part = sw_dyn;                                            // [slots][SW_COLS]
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int* su = reinterpret_cast<int*>(part + sw_slots() * SW_COLS) + wid * 32 * (1 + heads);   // [32] rows
+  int* su = reinterpret_cast<int*>(part + (sw_slots<V>() + 1) * SW_COLS) + wid * 32 * (1 + heads);   // [32] rows
   float* swt = reinterpret_cast<float*>(su + 32);                                           // [32][heads]
   __shared__ int s_pre[ES_ROWS];
   __shared__ int s_cnt;
   const int64_t* __restrict__ ptr = DIR ? g.out_ptr : g.in_ptr;
   const int32_t* __restrict__ nbr = DIR ? g.out_dst : g.in_src;
   const int64_t n = g.n_local, C = g.chunk;
-  const int slots = sw_slots();
+  const int slots = sw_slots<V>();
   const int D = cols / heads, npass = (cols + SW_COLS - 1) / SW_COLS;
   const float s = *sX;
   float amax_loc = 0.0f;
-  auto lower = [&](int64_t key) {
-    int64_t a = 0, b = n;
-    while (a < b) {
-      const int64_t m = (a + b) >> 1;
-      if (ptr[m] < key) a = m + 1; else b = m;
-    }
-    return a;
-  };
-  const int64_t lo = (int64_t)blockIdx.x * epb, hi = lo + epb;
-  if (lo > E) return;
-  const int64_t r0 = lower(lo), r1 = hi > E ? n : lower(hi);
+  (void)epb; (void)E;
+  const int64_t r0 = (int64_t)blockIdx.x * ES_ROWS, r1 = r0 + ES_ROWS < n ? r0 + ES_ROWS : n;   // the block's rows
   auto chunks = [&](int64_t r) -> int64_t {
     const int64_t d = ptr[r + 1] - ptr[r];
     return d <= C ? 1 : (d + C - 1) / C;
@@ -305,13 +290,13 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int head
     out[r * cols + j] = v;
     amax_loc = fmaxf(amax_loc, fabsf(v));
   };
-  // chunk sum of list positions [pb, pe) for the lane's columns j0 .. j0+3 of pass cp -> acc[4]
-  auto chunk_sum = [&](int64_t pb, int64_t pe, int j0, float (&acc)[4]) {
+  // chunk sum of list positions [pb, pe) for the lane's columns j0 .. j0+V-1 of pass cp -> acc[V]
+  auto chunk_sum = [&](int64_t pb, int64_t pe, int j0, float (&acc)[V]) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[c] = 0.0f;
-    int hc[4];
+    for (int c = 0; c < V; ++c) acc[c] = 0.0f;
+    int hc[V];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) hc[c] = (j0 + c < cols) ? (j0 + c) / D : 0;
+    for (int c = 0; c < V; ++c) hc[c] = (j0 + c < cols) ? (j0 + c) / D : 0;
     for (int64_t b0 = pb; b0 < pe; b0 += 32) {
       const int nb = (int)(pe - b0 < 32 ? pe - b0 : 32);
       __syncwarp();
@@ -323,18 +308,22 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int head
       }
       __syncwarp();
       for (int i0 = 0; i0 < nb; i0 += 8) {
-        uint32_t word[8];
+        uint32_t word[8][(V + 3) / 4];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          word[i] = 0u;
+#pragma unroll
+          for (int k = 0; k < (V + 3) / 4; ++k) word[i][k] = 0u;
           if (i0 + i < nb) {
             const int8_t* row = qX + (int64_t)su[i0 + i] * ldx;
-            if (WORD) {
-              if (j0 < cols) word[i] = __ldg(reinterpret_cast<const unsigned*>(row + j0));
+            if constexpr (V == 16) {
+              if (j0 < cols) {
+                const uint4 x = __ldg(reinterpret_cast<const uint4*>(row + j0));
+                word[i][0] = x.x; word[i][1] = x.y; word[i][2] = x.z; word[i][3] = x.w;
+              }
+            } else if constexpr (V == 4) {
+              if (j0 < cols) word[i][0] = __ldg(reinterpret_cast<const unsigned*>(row + j0));
             } else {
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                if (j0 + c < cols) word[i] |= (uint32_t)(uint8_t)__ldg(row + j0 + c) << (8 * c);
+              if (j0 < cols) word[i][0] = (uint32_t)(uint8_t)__ldg(row + j0);
             }
           }
         }
@@ -342,9 +331,17 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int head
         for (int i = 0; i < 8; ++i) {
           if (i0 + i < nb) {
             const float* wr = swt + (i0 + i) * heads;
+            if constexpr (V >= 4) {   // D % 4 == 0: a word's 4 columns share one head
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-              acc[c] = __fmaf_rn(wr[hc[c]], __int2float_rn((int)(int8_t)(word[i] >> (8 * c))), acc[c]);
+              for (int k = 0; k < V / 4; ++k) {
+                const float wk = wr[hc[4 * k]];
+                float2 a01 = make_float2(acc[4 * k], acc[4 * k + 1]), a23 = make_float2(acc[4 * k + 2], acc[4 * k + 3]);
+                fma4_codes(word[i][k], make_float2(wk, wk), a01, a23);
+                acc[4 * k] = a01.x; acc[4 * k + 1] = a01.y; acc[4 * k + 2] = a23.x; acc[4 * k + 3] = a23.y;
+              }
+            } else {
+              acc[0] = __fmaf_rn(wr[hc[0]], __int2float_rn((int)(int8_t)word[i][0]), acc[0]);
+            }
           }
         }
       }
@@ -374,26 +371,28 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int head
     const int nb = s_cnt;
     if (nb == 0) {   // one row with more chunks than the partial slots: windows, folded in order
       const int64_t pb0 = ptr[row], pe0 = ptr[row + 1], nch = (pe0 - pb0 + C - 1) / C;
+      float* wtot = part + (int64_t)slots * SW_COLS;   // running totals of the pass's columns
       for (int cp = 0; cp < npass; ++cp) {
-        float tot = 0.0f;   // thread t < SW_COLS: column cp*128 + t
         for (int64_t w0 = 0; w0 < nch; w0 += slots) {
           const int wn = (int)(nch - w0 < slots ? nch - w0 : slots);
           for (int it = wid; it < wn; it += ES_THREADS / 32) {
             const int64_t pb = pb0 + (w0 + it) * C, pe = pb + C < pe0 ? pb + C : pe0;
-            float acc[4];
-            chunk_sum(pb, pe, cp * SW_COLS + lane * 4, acc);
+            float acc[V];
+            chunk_sum(pb, pe, cp * SW_COLS + lane * V, acc);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) part[it * SW_COLS + lane * 4 + q] = acc[q];
+            for (int q = 0; q < V; ++q) part[it * SW_COLS + lane * V + q] = acc[q];
           }
           __syncthreads();
-          if (threadIdx.x < SW_COLS) {
-            for (int it = 0; it < wn; ++it)
-              tot = (w0 == 0 && it == 0) ? part[threadIdx.x] : __fadd_rn(tot, part[it * SW_COLS + threadIdx.x]);
+          for (int t = threadIdx.x; t < SW_COLS; t += ES_THREADS) {
+            float tot = w0 == 0 ? part[t] : __fadd_rn(wtot[t], part[t]);
+            for (int it = 1; it < wn; ++it) tot = __fadd_rn(tot, part[it * SW_COLS + t]);
+            wtot[t] = tot;
           }
           __syncthreads();
         }
-        const int j = cp * SW_COLS + threadIdx.x;
-        if (threadIdx.x < SW_COLS && j < cols) finish(row, j, tot);
+        for (int t = threadIdx.x; t < SW_COLS; t += ES_THREADS)
+          if (cp * SW_COLS + t < cols) finish(row, cp * SW_COLS + t, wtot[t]);
+        __syncthreads();
       }
       row += 1;
       continue;
@@ -409,16 +408,16 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int head
         const int j = a, k = it - (j ? s_pre[j - 1] : 0);
         const int64_t r = row + j, pb0 = ptr[r], pe0 = ptr[r + 1];
         const int64_t pb = pb0 + (int64_t)k * C, pe = pb + C < pe0 ? pb + C : pe0;
-        const int j0 = cp * SW_COLS + lane * 4;
-        float acc[4];
+        const int j0 = cp * SW_COLS + lane * V;
+        float acc[V];
         chunk_sum(pb, pe, j0, acc);
         if (pe0 - pb0 <= C) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < V; ++q)
             if (j0 + q < cols) finish(r, j0 + q, acc[q]);
         } else {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) part[it * SW_COLS + lane * 4 + q] = acc[q];
+          for (int q = 0; q < V; ++q) part[it * SW_COLS + lane * V + q] = acc[q];
         }
       }
       __syncthreads();
@@ -442,12 +441,14 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int head
 
 // ---------------------------------------------------------------------------- int8-α SPMM (NEXT-4)
 // acc[v,j] = Σ q_α[e,h(j)]·q_X[w_e,j] (exact int32, order-free), out = i2f(acc)·fl(s_α·s_X) (orc_spmm_q8).
-// The same edge-window blocks and chunk items as tango_spmm_q; a warp sums one (item, 128-column pass): per
+// The same row blocks and chunk items as tango_spmm_q; a warp sums one (item, 128-column pass): per
 // 32-edge batch the lanes stage the batch's gather rows and α codes ([head][edge] bytes) in shared memory;
 // every lane then takes its 4 columns (one 32-bit word) of 4 gathered rows at a time, transposes the 4x4
 // bytes (8 PRMT) and adds 4 IDP4A dots against the 4 edges' α codes of its head — 16 products in 12
 // instructions instead of the fp32 path's 2 per product.  Integer sums are order-free, so a multi-chunk row
 // adds its chunks with int32 atomics (out_i32 zeroed first); a second pass writes the fp32 output.
+constexpr int Q8_COLS = 128;   // 4 columns per lane
+
 __device__ __forceinline__ void transpose4(uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3, uint32_t (&t)[4]) {
   const uint32_t a = __byte_perm(r0, r1, 0x5140), b = __byte_perm(r2, r3, 0x5140);
   const uint32_t c = __byte_perm(r0, r1, 0x7362), d = __byte_perm(r2, r3, 0x7362);
@@ -467,18 +468,9 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_q8(GraphDev g, int heads, i
   const int64_t* __restrict__ ptr = DIR ? g.out_ptr : g.in_ptr;
   const int32_t* __restrict__ nbr = DIR ? g.out_dst : g.in_src;
   const int64_t n = g.n_local, C = g.chunk;
-  const int D = cols / heads, npass = (cols + SW_COLS - 1) / SW_COLS;
-  auto lower = [&](int64_t key) {
-    int64_t a = 0, b = n;
-    while (a < b) {
-      const int64_t m = (a + b) >> 1;
-      if (ptr[m] < key) a = m + 1; else b = m;
-    }
-    return a;
-  };
-  const int64_t lo = (int64_t)blockIdx.x * epb, hi = lo + epb;
-  if (lo > E) return;
-  const int64_t r0 = lower(lo), r1 = hi > E ? n : lower(hi);
+  const int D = cols / heads, npass = (cols + Q8_COLS - 1) / Q8_COLS;
+  (void)epb; (void)E;
+  const int64_t r0 = (int64_t)blockIdx.x * ES_ROWS, r1 = r0 + ES_ROWS < n ? r0 + ES_ROWS : n;   // the block's rows
   auto chunks = [&](int64_t r) -> int64_t {
     const int64_t d = ptr[r + 1] - ptr[r];
     return d <= C ? 1 : (d + C - 1) / C;
@@ -539,7 +531,7 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_q8(GraphDev g, int heads, i
         const int j = a, k = it - (j ? s_pre[j - 1] : 0);
         const int64_t r = row + j, pb0 = ptr[r], pe0 = ptr[r + 1];
         const int64_t pb = pb0 + (int64_t)k * C, pe = pb + C < pe0 ? pb + C : pe0;
-        const int j0 = cp * SW_COLS + lane * 4;
+        const int j0 = cp * Q8_COLS + lane * 4;
         int acc[4];
         chunk_dot(pb, pe, j0, acc);
         if (j0 < cols) {
@@ -651,7 +643,7 @@ cudaError_t launch_edge_sum(const GraphDev& g, int dir, int heads, const float* 
   const int64_t e = e_list > 0 ? e_list : 1;
   int64_t epb = e / ((int64_t)num_sms() * 8);
   epb = epb < 256 ? 256 : (epb > 16384 ? 16384 : epb);
-  const int64_t blocks = e_list / epb + 1;   // list positions [0, e_list]: the last block owns rows starting at e_list
+  const int64_t blocks = (g.n_local + ES_ROWS - 1) / ES_ROWS;   // row blocks
   const size_t smem = (size_t)(es_slots(heads) + 1) * heads * 4;
   const uintptr_t xa = reinterpret_cast<uintptr_t>(x);
   const int vw = (heads % 4 == 0 && xa % 16 == 0) ? 4 : (heads % 2 == 0 && xa % 8 == 0) ? 2 : 1;
@@ -670,19 +662,23 @@ cudaError_t launch_spmm_w(const GraphDev& g, int dir, int heads, int cols, const
                           int64_t e_list, cudaStream_t st) {
   if (g.n_local == 0) return cudaSuccess;
   ProfScope ps("spmm_w", st);
-  const int64_t e = e_list > 0 ? e_list : 1;
-  int64_t epb = e / ((int64_t)num_sms() * 4);
-  epb = epb < 256 ? 256 : (epb > 16384 ? 16384 : epb);
-  const int64_t blocks = e_list / epb + 1;
-  const size_t smem = (size_t)sw_slots() * SW_COLS * 4 + (size_t)(ES_THREADS / 32) * 32 * (1 + heads) * 4;
-  const bool word = (ldx % 4 == 0) && ((uintptr_t)qX % 4 == 0);
-  auto f = dir ? (word ? k_spmm_w_fast<1, true> : k_spmm_w_fast<1, false>)
-               : (word ? k_spmm_w_fast<0, true> : k_spmm_w_fast<0, false>);
+  const int64_t blocks = (g.n_local + ES_ROWS - 1) / ES_ROWS;   // row blocks
+  const int D = cols / heads;
+  const uintptr_t qa = reinterpret_cast<uintptr_t>(qX);
+  const int v = (D % 16 == 0 && ldx % 16 == 0 && qa % 16 == 0) ? 16 : (D % 4 == 0 && ldx % 4 == 0 && qa % 4 == 0) ? 4 : 1;
+  void (*f)(GraphDev, int, int, int64_t, int64_t, const float*, const int8_t*, int64_t, const float*, const float*,
+            float*, unsigned*);
+  size_t cols_pass;
+  int slots;
+  if (v == 16) { f = dir ? k_spmm_w_fast<1, 16> : k_spmm_w_fast<0, 16>; cols_pass = sw_cols<16>(); slots = sw_slots<16>(); }
+  else if (v == 4) { f = dir ? k_spmm_w_fast<1, 4> : k_spmm_w_fast<0, 4>; cols_pass = sw_cols<4>(); slots = sw_slots<4>(); }
+  else { f = dir ? k_spmm_w_fast<1, 1> : k_spmm_w_fast<0, 1>; cols_pass = sw_cols<1>(); slots = sw_slots<1>(); }
+  const size_t smem = (size_t)(slots + 1) * cols_pass * 4 + (size_t)(ES_THREADS / 32) * 32 * (1 + heads) * 4;
   if (smem > 48 * 1024) {
     const cudaError_t err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
   }
-  f<<<(unsigned)blocks, ES_THREADS, smem, st>>>(g, heads, cols, epb, e_list, w, qX, ldx, sX, rowscale, out, amax_out);
+  f<<<(unsigned)blocks, ES_THREADS, smem, st>>>(g, heads, cols, 0, e_list, w, qX, ldx, sX, rowscale, out, amax_out);
   return cudaGetLastError();
 }
 cudaError_t launch_spmm_q8(const GraphDev& g, int dir, int heads, int cols, const int8_t* qa, const float* sa,
@@ -696,7 +692,7 @@ cudaError_t launch_spmm_q8(const GraphDev& g, int dir, int heads, int cols, cons
     const int64_t e = e_list > 0 ? e_list : 1;
     int64_t epb = e / ((int64_t)num_sms() * 4);
     epb = epb < 256 ? 256 : (epb > 16384 ? 16384 : epb);
-    const int64_t blocks = e_list / epb + 1;
+    const int64_t blocks = (g.n_local + ES_ROWS - 1) / ES_ROWS;   // row blocks
     const size_t smem = (size_t)(ES_THREADS / 32) * 32 * (4 + heads);
     auto f = dir ? k_spmm_q8<1> : k_spmm_q8<0>;
     if (smem > 48 * 1024) {
