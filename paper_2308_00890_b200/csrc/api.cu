@@ -552,6 +552,7 @@ struct GatLayout {
       off_pout_cnt, off_h1, off_h2, off_hdS, off_hagg, off_work, off_dS, off_alpha, off_pin_tiles, off_pout_tiles;
   size_t off_hcnt, off_dapart;   // v6 dataflow: finished-segment counters [n], ∂a chunk partials
   size_t off_nrec;               // packed per-node record [N][nrs] (the v6 in-CSR -> out-CSR map reuses off_dal)
+  size_t off_ast;                // v6: α stored by F-agg for P2 [E][H] (sign = LeakyReLU branch)
   int64_t tcap;
 };
 GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
@@ -608,6 +609,7 @@ GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   L.off_hcnt = take((size_t)L.n * 4);
   L.off_dapart = take((size_t)((L.n + 1023) / 1024 + 1) * 2 * L.HD * 4);
   L.off_nrec = take((size_t)L.N * gat2_nrec_stride((int)L.H) * 4);
+  L.off_ast = take((size_t)L.E * L.H * 4);
   L.total = o;
   return L;
 }
@@ -712,6 +714,12 @@ G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_p
     return (e && atoi(e)) ? 1 : 0;
   }();
   a.lane_hubs = lane;
+  // α stored by F-agg and read by P2 (default), or recomputed by P2 (TANGO_ALPHA_RECOMPUTE=1)
+  static const int recompute = [] {
+    const char* e = getenv("TANGO_ALPHA_RECOMPUTE");
+    return (e && atoi(e)) ? 1 : 0;
+  }();
+  a.alpha_st = recompute ? nullptr : (float*)(c + L.off_ast);
   a.codes_biased = 1;
   return a;
 }

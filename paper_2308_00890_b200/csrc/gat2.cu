@@ -156,6 +156,16 @@ __device__ __forceinline__ int8_t head_pick_i8(const int8_t (&x)[H], int h) {
   return r;
 }
 
+// α with the LeakyReLU branch in its sign bit (negative: e_pre <= 0), stored by F-agg for the destination
+// pass P2 (which then neither gathers q_S nor recomputes α); α >= 0, so |stored| = α exactly
+template <int H>
+__device__ __forceinline__ void store_alpha(float* dst, const float (&al)[H], const float (&ep)[H]) {
+  float o[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) o[h] = ep[h] > 0.0f ? al[h] : -al[h];
+  st_h<H>(dst, o);
+}
+
 template <int H>
 __host__ __device__ constexpr int hbatch() { return H >= 8 ? 32 : 64; }   // edges per staged batch of a hub chunk
 
@@ -594,7 +604,7 @@ __global__ void __launch_bounds__(256, 3) k2_fagg(const G2Args a) {
       row = 0;
       return s.eb + (pos < T ? pos : T - 1);
     };
-    auto alpha_of = [&](int c, int u, int row, float (&al)[H]) {
+    auto alpha_of = [&](int c, int u, int row, int64_t e, float (&al)[H]) {
 #pragma unroll
       for (int h = 0; h < H; ++h) al[h] = 0.0f;
       if (c * 32 + lane < T) {
@@ -603,6 +613,7 @@ __global__ void __launch_bounds__(256, 3) k2_fagg(const G2Args a) {
         load_qh<H>(a.qS + (int64_t)u * H, qs);
         float ep[H];
         alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+        if (a.alpha_st) store_alpha<H>(a.alpha_st + e * H, al, ep);
       }
     };
     auto stash = [&](int c, int row, const float (&al)[H]) {
@@ -619,7 +630,7 @@ __global__ void __launch_bounds__(256, 3) k2_fagg(const G2Args a) {
       const int64_t e0 = pos_of(0, row0);
       const int u0 = lane < T ? __ldcs(a.g.in_src + e0) : 0;
       float al0[H];
-      alpha_of(0, u0, row0, al0);
+      alpha_of(0, u0, row0, e0, al0);
       stash(0, row0, al0);
       sidx[lane] = u0;
       const int64_t e1 = pos_of(1, row1);
@@ -652,7 +663,7 @@ __global__ void __launch_bounds__(256, 3) k2_fagg(const G2Args a) {
       const int u2 = (c + 2) * 32 + lane < T ? __ldcs(a.g.in_src + e2) : 0;
       int8_t qs1[H];
       int row1x = 0;
-      (void)pos_of(c + 1, row1x);
+      const int64_t e1x = pos_of(c + 1, row1x);
       DstSm<H> d1 = dseg;
       if ((c + 1) * 32 + lane < T) {
         load_qh<H>(a.qS + (int64_t)u1 * H, qs1);
@@ -710,6 +721,7 @@ __global__ void __launch_bounds__(256, 3) k2_fagg(const G2Args a) {
         if ((c + 1) * 32 + lane < T) {
           float ep[H];
           alpha_rec<H>(qs1, d1, scS.s, scD.s, a.slope, ep, al1);
+          if (a.alpha_st) store_alpha<H>(a.alpha_st + e1x * H, al1, ep);
         }
         stash(c + 1, row1x, al1);
         sidx[b * 32 + lane] = u2;
@@ -863,6 +875,7 @@ __global__ void __launch_bounds__(256, 3) k2_fagg_seg(const G2Args a) {
       if (c * 32 + lane < T) {
         float ep[H];
         alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+        if (a.alpha_st) store_alpha<H>(a.alpha_st + (eb + c * 32 + lane) * H, al, ep);
       }
     };
     auto stash = [&](int c, const float (&al)[H]) {
@@ -1412,7 +1425,17 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
 // P2a: hub segments (P partials, folded by the row's last segment) and light sub-tiles (P and ∂D);
 // P2b: hub segments (∂D partials with the row's P, folded likewise).
 template <int H>
-struct EdgeIn { int8_t qs[H]; float da[H]; };
+struct EdgeIn { int8_t qs[H]; float da[H], st[H]; };   // st: α stored by F-agg (sign = LeakyReLU branch)
+
+// α and the branch from F-agg's stored signed α
+template <int H>
+__device__ __forceinline__ void alpha_from_st(const float (&st)[H], float (&ep)[H], float (&al)[H]) {
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    al[h] = fabsf(st[h]);
+    ep[h] = signbit(st[h]) ? -1.0f : 1.0f;
+  }
+}
 
 template <int H>
 __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
@@ -1432,7 +1455,8 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
           s.eb, s.ee, sbx[w], sby[w],
           [&](int64_t e) {
             EdgeIn<H> l;
-            load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs);
+            if (a.alpha_st) ld_h<H>(a.alpha_st + e * H, l.st);
+            else load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs);
             if (a.scatter_in) {
               ld_h<H>(a.dal_in + e * H, l.da);   // scattered into in-CSR order by P1
             } else {
@@ -1443,7 +1467,8 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
           },
           [&](const EdgeIn<H>& l, float (&x)[H], float (&y)[H]) {
             float ep[H];
-            alpha_rec<H>(l.qs, d, scS.s, scD.s, a.slope, ep, y);
+            if (a.alpha_st) alpha_from_st<H>(l.st, ep, y);
+            else alpha_rec<H>(l.qs, d, scS.s, scD.s, a.slope, ep, y);
 #pragma unroll
             for (int h = 0; h < H; ++h) x[h] = l.da[h];
           });
@@ -1480,11 +1505,17 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
         d.den[h] = __shfl_sync(0xffffffffu, dj.den[h], row);
       }
       if (pos < t.T) {
-        int8_t qs[H];
-        load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, qs);
         if (a.scatter_in) ld_h<H>(a.dal_in + e * H, da);
         else ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, da);
-        alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+        if (a.alpha_st) {
+          float st[H];
+          ld_h<H>(a.alpha_st + e * H, st);
+          alpha_from_st<H>(st, ep, al);
+        } else {
+          int8_t qs[H];
+          load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, qs);
+          alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+        }
       }
     };
     float P[H], dD[H];
@@ -1544,13 +1575,15 @@ __global__ void __launch_bounds__(256, 4) k2_bdst_b(const G2Args a) {
         s.eb, s.ee, sbx[w], nullptr,
         [&](int64_t e) {
           EdgeIn<H> l;
-          load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs);
+          if (a.alpha_st) ld_h<H>(a.alpha_st + e * H, l.st);
+          else load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs);
           ld_h<H>(a.dal_in + e * H, l.da);
           return l;
         },
         [&](const EdgeIn<H>& l, float (&x)[H], float (&)[H]) {
           float ep[H], al[H];
-          alpha_rec<H>(l.qs, d, scS.s, scD.s, a.slope, ep, al);
+          if (a.alpha_st) alpha_from_st<H>(l.st, ep, al);
+          else alpha_rec<H>(l.qs, d, scS.s, scD.s, a.slope, ep, al);
 #pragma unroll
           for (int h = 0; h < H; ++h) {
             const float dE = __fmul_rn(al[h], __fsub_rn(l.da[h], P[h]));

@@ -168,6 +168,7 @@ struct G2Args {
   const int32_t* in2out;                                     // [E] out-CSR position of each in-CSR edge
   int scatter_in;                                            // P1 also writes ∂α at its in-CSR slot (dal_in)
   int lane_hubs;                                             // hub segments of F-stats / P2 / P3: lane per (segment, head)
+  float* alpha_st;                                           // [E][H] α from F-agg, sign = LeakyReLU branch (nullable)
   float* da_src; float* da_dst;                              // [HD]
   int codes_biased;
 };
