@@ -711,9 +711,9 @@ G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_p
   a.scatter_in = scatter;
   static const int lane = [] {
     const char* e = getenv("TANGO_HUB_LANE");
-    return (e && atoi(e)) ? 1 : 0;
+    return e ? atoi(e) : 0;
   }();
-  a.lane_hubs = lane;
+  a.lane_hubs = lane;   // 0: staged warp sums, 1: lane-pipelined, 2: multi-segment staged
   // α stored by F-agg and read by P2 (default), or recomputed by P2 (TANGO_ALPHA_RECOMPUTE=1)
   static const int recompute = [] {
     const char* e = getenv("TANGO_ALPHA_RECOMPUTE");

@@ -2000,6 +2000,219 @@ __global__ void __launch_bounds__(256, 2) k2_bsrc2_hub(const G2Args a) {
   amax_flush(a.amax_dHp, amax_loc);
 }
 
+// ================================================================== hub segments, multi-segment staged sums
+// The per-edge scalar passes over hub rows with all 32 lanes busy in BOTH halves of the staged form: a warp
+// claims SPW = 32/H consecutive hub segments (canonical chunks); per batch of 32 positions lane L computes
+// position L of every one of the SPW segments (coalesced loads per segment) and stages the per-head values
+// in shared memory [seg][pos][H]; then lane L = k·H + h adds segment k's staged values of head h in edge
+// order (the chunk partial of Σᶜ).  Partials, the row's last-finisher fold and the P3 finalize are those of
+// the lane form above.
+template <int H, bool FMA, typename CV>
+__device__ __forceinline__ float seg_multi(const LaneSeg& s, float* __restrict__ bx, float* __restrict__ by, CV&& cv) {
+  constexpr int SPW = 32 / H;
+  const int lane = threadIdx.x & 31, k = lane / H, h = lane % H;
+  const int mylen = s.ok ? (int)(s.ee - s.eb) : 0;
+  int maxlen = mylen;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+  float acc = 0.0f;
+  for (int b0 = 0; b0 < maxlen; b0 += 32) {
+#pragma unroll 2
+    for (int t = 0; t < SPW; ++t) {   // segment t: its start, length and row from its group leader
+      const int ebt = __shfl_sync(0xffffffffu, (int)s.eb, t * H);
+      const int lent = __shfl_sync(0xffffffffu, mylen, t * H);
+      const int rowt = __shfl_sync(0xffffffffu, (int)s.row, t * H);
+      if (b0 + lane < lent) {
+        float x[H], y[H];
+        cv(rowt, (int64_t)ebt + b0 + lane, x, y);
+#pragma unroll
+        for (int hh = 0; hh < H; ++hh) {
+          bx[(t * 32 + lane) * H + hh] = x[hh];
+          if (FMA) by[(t * 32 + lane) * H + hh] = y[hh];
+        }
+      }
+    }
+    __syncwarp();
+    const int cnt = mylen - b0 < 32 ? mylen - b0 : 32;
+    const float* px = bx + (k * 32) * H + h;
+    const float* py = by + (k * 32) * H + h;
+    int i = 0;
+    for (; i + 4 <= cnt; i += 4) {
+      const float x0 = px[i * H], x1 = px[(i + 1) * H], x2 = px[(i + 2) * H], x3 = px[(i + 3) * H];
+      if (FMA) {
+        const float y0 = py[i * H], y1 = py[(i + 1) * H], y2 = py[(i + 2) * H], y3 = py[(i + 3) * H];
+        acc = __fmaf_rn(x0, y0, acc); acc = __fmaf_rn(x1, y1, acc);
+        acc = __fmaf_rn(x2, y2, acc); acc = __fmaf_rn(x3, y3, acc);
+      } else {
+        acc = __fadd_rn(acc, x0); acc = __fadd_rn(acc, x1); acc = __fadd_rn(acc, x2); acc = __fadd_rn(acc, x3);
+      }
+    }
+    for (; i < cnt; ++i) acc = FMA ? __fmaf_rn(px[i * H], py[i * H], acc) : __fadd_rn(acc, px[i * H]);
+    __syncwarp();
+  }
+  return acc;
+}
+
+template <int H>
+__global__ void __launch_bounds__(256, 3) k2_fstats2_hubm(const G2Args a) {
+  constexpr int SPW = 32 / H;
+  __shared__ float sbx[8][SPW * 32 * H];
+  const int w = threadIdx.x >> 5, h = (threadIdx.x & 31) % H;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t hc = load_count(a.pin.counts);
+  FOR_LANE_SEGS(first, a.work + 8, hc, SPW) {
+    const LaneSeg s = lane_seg<H>(first, hc, a.g.in_ptr, a.pin, a.g.chunk);
+    const int64_t vg = a.g.row_begin + s.row;
+    const float acc = seg_multi<H, false>(s, sbx[w], nullptr, [&](int rowt, int64_t e, float (&x)[H], float (&)[H]) {
+      const int64_t rg = a.g.row_begin + rowt;
+      int8_t qd[H], qs[H];
+      load_qh<H>(a.qD + rg * H, qd);
+      load_qh<H>(a.qS + (int64_t)__ldg(a.g.in_src + e) * H, qs);
+      const unsigned* mk = reinterpret_cast<const unsigned*>(a.nrec + rg * a.nrs);
+#pragma unroll
+      for (int hh = 0; hh < H; ++hh)
+        x[hh] = exp_p(__fsub_rn(lrelu(sddmm_add1(qs[hh], scS.s, qd[hh], scD.s), a.slope), fkey_dec(mk[hh])));
+    });
+    float m = 0.0f;
+    if (s.ok) {
+      m = fkey_dec(reinterpret_cast<const unsigned*>(a.nrec + vg * a.nrs)[h]);
+      __stcg(a.h2 + s.slot * H + h, acc);
+    }
+    if (lane_seg_last<H>(a.hcnt, s)) {
+      const float den = lane_seg_fold<H>(a.h2, s);
+      a.m[vg * H + h] = m;
+      rec_put1(a, vg, 0, h, m);
+      a.den[vg * H + h] = den;
+      rec_put1(a, vg, 1, h, den);
+      reinterpret_cast<int8_t*>(a.nrec + vg * a.nrs + 3 * H)[h] = a.qD[vg * H + h];
+    }
+  }
+}
+
+template <int H>
+__global__ void __launch_bounds__(128, 6) k2_bdst_a_hubm(const G2Args a) {   // 4-warp blocks (x and y staged)
+  constexpr int SPW = 32 / H;
+  __shared__ float sbx[4][SPW * 32 * H];
+  __shared__ float sby[4][SPW * 32 * H];
+  const int w = threadIdx.x >> 5, h = (threadIdx.x & 31) % H;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t hc = load_count(a.pin.counts);
+  FOR_LANE_SEGS(first, a.work + 9, hc, SPW) {
+    const LaneSeg s = lane_seg<H>(first, hc, a.g.in_ptr, a.pin, a.g.chunk);
+    const int64_t vg = a.g.row_begin + s.row;
+    const float acc = seg_multi<H, true>(s, sbx[w], sby[w], [&](int rowt, int64_t e, float (&x)[H], float (&y)[H]) {
+      if (a.scatter_in) {
+        ld_h<H>(a.dal_in + e * H, x);
+      } else {
+        ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, x);
+        st_h<H>(a.dal_in + e * H, x);   // for P2b (coalesced)
+      }
+      float ep[H];
+      if (a.alpha_st) {
+        float st[H];
+        ld_h<H>(a.alpha_st + e * H, st);
+        alpha_from_st<H>(st, ep, y);
+      } else {
+        int8_t qs[H];
+        load_qh<H>(a.qS + (int64_t)__ldg(a.g.in_src + e) * H, qs);
+        alpha_rec<H>(qs, load_dst<H>(a, a.g.row_begin + rowt), scS.s, scD.s, a.slope, ep, y);
+      }
+    });
+    if (s.ok) __stcg(a.h1 + s.slot * H + h, acc);
+    if (lane_seg_last<H>(a.hcnt, s)) {
+      const float P = lane_seg_fold<H>(a.h1, s);
+      a.P[vg * H + h] = P;
+      rec_put1(a, vg, 2, h, P);
+    }
+  }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256, 3) k2_bdst_b_hubm(const G2Args a) {
+  constexpr int SPW = 32 / H;
+  __shared__ float sbx[8][SPW * 32 * H];
+  const int w = threadIdx.x >> 5, h = (threadIdx.x & 31) % H;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t hc = load_count(a.pin.counts);
+  FOR_LANE_SEGS(first, a.work + 10, hc, SPW) {
+    const LaneSeg s = lane_seg<H>(first, hc, a.g.in_ptr, a.pin, a.g.chunk);
+    const int64_t vg = a.g.row_begin + s.row;
+    const float acc = seg_multi<H, false>(s, sbx[w], nullptr, [&](int rowt, int64_t e, float (&x)[H], float (&)[H]) {
+      const int64_t rg = a.g.row_begin + rowt;
+      float da[H], P[H], ep[H], al[H];
+      ld_h<H>(a.dal_in + e * H, da);
+      ld_h<H>(a.P + rg * H, P);
+      if (a.alpha_st) {
+        float st[H];
+        ld_h<H>(a.alpha_st + e * H, st);
+        alpha_from_st<H>(st, ep, al);
+      } else {
+        int8_t qs[H];
+        load_qh<H>(a.qS + (int64_t)__ldg(a.g.in_src + e) * H, qs);
+        alpha_rec<H>(qs, load_dst<H>(a, rg), scS.s, scD.s, a.slope, ep, al);
+      }
+#pragma unroll
+      for (int hh = 0; hh < H; ++hh) {
+        const float dE = __fmul_rn(al[hh], __fsub_rn(da[hh], P[hh]));
+        x[hh] = ep[hh] > 0.0f ? dE : __fmul_rn(dE, a.slope);
+      }
+    });
+    if (s.ok) __stcg(a.h2 + s.slot * H + h, acc);
+    if (lane_seg_last<H>(a.hcnt, s)) a.dD[vg * H + h] = lane_seg_fold<H>(a.h2, s);
+  }
+}
+
+template <int H, int VPL>
+__global__ void __launch_bounds__(256, 3) k2_bsrc2_hubm(const G2Args a) {
+  constexpr int SPW = 32 / H;
+  __shared__ float sbx[8][SPW * 32 * H];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane % H;
+  const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
+  const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
+  const int64_t hc = load_count(a.pout.counts);
+  float amax_loc = 0.0f;
+  FOR_LANE_SEGS(first, a.work + 11, hc, SPW) {
+    const LaneSeg s = lane_seg<H>(first, hc, a.g.out_ptr, a.pout, a.g.chunk);
+    const int64_t ug = a.g.row_begin + s.row;
+    const float acc = seg_multi<H, false>(s, sbx[w], nullptr, [&](int rowt, int64_t e, float (&x)[H], float (&)[H]) {
+      int8_t qs[H];
+      load_qh<H>(a.qS + (a.g.row_begin + rowt) * H, qs);
+      const int v = __ldg(a.g.out_dst + e);
+      float da[H], Pv[H], ep[H], al[H];
+      ld_h<H>(a.dal_out + e * H, da);
+      const DstSm<H> d = load_rec<H>(a, v);
+      ld_h<H>(a.nrec + (int64_t)v * a.nrs + 2 * H, Pv);
+      alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+#pragma unroll
+      for (int hh = 0; hh < H; ++hh) {
+        const float dE = __fmul_rn(al[hh], __fsub_rn(da[hh], Pv[hh]));
+        x[hh] = ep[hh] > 0.0f ? dE : __fmul_rn(dE, a.slope);
+      }
+    });
+    if (s.ok) __stcg(a.hs + s.slot * H + h, acc);
+    const bool last = lane_seg_last<H>(a.hcnt, s);
+    float dS = 0.0f;
+    if (last) {
+      dS = lane_seg_fold<H>(a.hs, s);
+      a.dS[ug * H + h] = dS;
+    }
+    unsigned done = __ballot_sync(0xffffffffu, last && h == 0);
+    while (done) {
+      const int g0 = __ffs(done) - 1;
+      done &= done - 1;
+      float dSr[H];
+#pragma unroll
+      for (int k2 = 0; k2 < H; ++k2) dSr[k2] = __shfl_sync(0xffffffffu, dS, g0 + k2);
+      const int64_t rl = __shfl_sync(0xffffffffu, s.row, g0);
+      src_finalize_row<H, VPL>(a, rl, dSr, amax_loc);
+    }
+  }
+  amax_flush(a.amax_dHp, amax_loc);
+}
+
 // ================================================================== ∂a, deterministic (reading R39)
 // ∂a_src[j] = Σᶜ_u fmaf(∂S[u,h], deq(q_H′)[u,j], ·) with chunks of DA_CHUNK global rows folded left to
 // right (R33's order); block b computes chunk b's partials for all 2·HD outputs (one sequential fmaf chain
@@ -2143,7 +2356,7 @@ cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st, const SideStream* 
     { ProfScope p("gat_fwd_stats1", st); k2_fstats1<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
     if (a.lane_hubs) { /* hub segments on the side stream beside the light sub-tiles */                \
       e = fork2(st, x);                                                                              \
-      { ProfScope p("gat_fwd_stats_hub", sh); k2_fstats2_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
+      { ProfScope p("gat_fwd_stats_hub", sh); if (a.lane_hubs == 2) k2_fstats2_hubm<H_><<<grid_items((a.pin.cap + 63) / 64, 3), 256, 0, sh>>>(a); else k2_fstats2_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
       { ProfScope p("gat_fwd_stats", st); k2_fstats2<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
       if (e == cudaSuccess) e = join2(st, x);                                                        \
     } else { ProfScope p("gat_fwd_stats", st); k2_fstats2<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
@@ -2181,12 +2394,12 @@ cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st, const SideStream* 
     if (e == cudaSuccess) e = join2(st, x);                                                          \
     if (a.lane_hubs) { /* hub segments on the side stream beside the light sub-tiles (P2a, P3) */        \
       if (e == cudaSuccess) e = fork2(st, x);                                                        \
-      { ProfScope p("gat_bwd_dst_hub", sh); k2_bdst_a_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
+      { ProfScope p("gat_bwd_dst_hub", sh); if (a.lane_hubs == 2) k2_bdst_a_hubm<H_><<<grid_items((a.pin.cap + 31) / 32, 6), 128, 0, sh>>>(a); else k2_bdst_a_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
       { ProfScope p("gat_bwd_dst", st); k2_bdst_a<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
       if (e == cudaSuccess) e = join2(st, x);                                                        \
-      { ProfScope p("gat_bwd_dst2", st); k2_bdst_b_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
+      { ProfScope p("gat_bwd_dst2", st); if (a.lane_hubs == 2) k2_bdst_b_hubm<H_><<<grid_items((a.pin.cap + 63) / 64, 3), 256, 0, st>>>(a); else k2_bdst_b_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
       if (e == cudaSuccess) e = fork2(st, x);                                                        \
-      { ProfScope p("gat_bwd_src2_hub", sh); k2_bsrc2_hub<H_, V_><<<grid_items((a.pout.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
+      { ProfScope p("gat_bwd_src2_hub", sh); if (a.lane_hubs == 2) k2_bsrc2_hubm<H_, V_><<<grid_items((a.pout.cap + 63) / 64, 3), 256, 0, sh>>>(a); else k2_bsrc2_hub<H_, V_><<<grid_items((a.pout.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
       { ProfScope p("gat_bwd_src2", st); k2_bsrc2<H_, V_><<<grid_items((a.pout.cap + a.pout.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
       if (e == cudaSuccess) e = join2(st, x);                                                        \
     } else {                                                                                         \
