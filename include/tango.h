@@ -471,6 +471,9 @@ int64_t tango_comm_nccl_calls(const struct tango_comm* comm);
 /* accumulated per kernel name (host-side state, process-wide, thread-safe).  */
 /* ------------------------------------------------------------------------- */
 void tango_profile_enable(int32_t on);
+/* NVTX ranges (one per kernel launch, named after the kernel) for timeline tools; default from the
+ * environment variable TANGO_NVTX (off). */
+void tango_nvtx_enable(int32_t on);
 int64_t tango_launch_count(void);
 tango_status tango_profile_collect(void);          /* waits for the recorded events */
 int32_t tango_profile_num_entries(void);

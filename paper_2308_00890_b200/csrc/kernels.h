@@ -17,6 +17,7 @@ class ProfScope {
  private:
   cudaStream_t st_;
   bool on_ = false;
+  bool nvtx_ = false;
   int entry_ = -1;
   cudaEvent_t a_ = nullptr, b_ = nullptr;
 };

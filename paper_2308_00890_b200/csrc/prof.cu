@@ -4,8 +4,11 @@
 // counter (tango_launch_count) and, when profiling is enabled, brackets the launch with two CUDA
 // events on the launching stream.  tango_profile_collect() waits for the recorded events and
 // accumulates per-kernel device time; bench.py reads it to compute the live roofline fraction of
-// the dominant kernel over the timed region.
+// the dominant kernel over the timed region.  With tango_nvtx_enable(1) (or TANGO_NVTX=1) every launch is
+// also an NVTX range named after the kernel (header-only NVTX v3), for timeline tools.
 #include <atomic>
+#include <cstdlib>
+#include <nvtx3/nvToolsExt.h>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -23,6 +26,16 @@ std::vector<Entry> g_entries;
 std::vector<Pending> g_pending;
 std::vector<cudaEvent_t> g_pool;
 std::atomic<bool> g_enabled{false};
+std::atomic<int> g_nvtx{-1};   // -1: not yet read from the environment
+bool nvtx_on() {
+  int v = g_nvtx.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("TANGO_NVTX");
+    v = (e && atoi(e)) ? 1 : 0;
+    g_nvtx.store(v);
+  }
+  return v != 0;
+}
 std::atomic<int64_t> g_launches{0};
 
 cudaEvent_t take_event() {
@@ -41,6 +54,8 @@ int entry_of(const char* name) {
 
 ProfScope::ProfScope(const char* name, cudaStream_t st) : st_(st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  nvtx_ = nvtx_on();
+  if (nvtx_) nvtxRangePushA(name);
   on_ = g_enabled.load(std::memory_order_relaxed);
   if (on_) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -51,6 +66,7 @@ ProfScope::ProfScope(const char* name, cudaStream_t st) : st_(st) {
   }
 }
 ProfScope::~ProfScope() {
+  if (nvtx_) nvtxRangePop();
   if (on_) {
     cudaEventRecord(b_, st_);
     std::lock_guard<std::mutex> lk(g_mu);
@@ -65,6 +81,8 @@ using namespace tango;
 extern "C" {
 
 void tango_profile_enable(int32_t on) { g_enabled.store(on != 0); }
+
+void tango_nvtx_enable(int32_t on) { g_nvtx.store(on != 0 ? 1 : 0); }
 
 int64_t tango_launch_count(void) { return g_launches.load(); }
 

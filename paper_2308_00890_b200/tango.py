@@ -109,7 +109,7 @@ EXPORTS = ["tango_status_string", "tango_abi_version", "tango_status_poll", "tan
            "tango_gat_out_ctx_bytes", "tango_gat_out_fwd", "tango_gat_out_bwd", "tango_gat_out_ctx_get_view",
            "tango_gcn_out_ctx_bytes", "tango_gcn_out_fwd", "tango_gcn_out_bwd", "tango_gcn_out_ctx_get_view",
            "tango_quantize_int4", "tango_sddmm_qn", "tango_set_l2_fetch_granularity", "tango_comm_set_options",
-           "tango_comm_reserve", "tango_comm_nccl_calls", "tango_spmm_q8"]
+           "tango_comm_reserve", "tango_comm_nccl_calls", "tango_spmm_q8", "tango_nvtx_enable"]
 
 
 def load(path: str = LIB_PATH):
@@ -138,6 +138,8 @@ def load(path: str = LIB_PATH):
     L.tango_comm_reserve.argtypes = [_P, sz]
     L.tango_comm_nccl_calls.argtypes = [_P]
     L.tango_spmm_q8.argtypes = [PG, i32, PQ, PQ, i32, _P, _P, _P]
+    L.tango_nvtx_enable.argtypes = [i32]
+    L.tango_nvtx_enable.restype = None
     L.tango_comm_nccl_calls.restype = C.c_int64
     L.tango_gat_ctx_bytes.restype = sz
     L.tango_gat_ctx_bytes.argtypes = [PG, C.POINTER(GatParams)]
@@ -237,6 +239,11 @@ def ld32(cols: int) -> int:
 # ---------------------------------------------------------------------------------------- tracing
 def profile_enable(on: bool = True):
     load().tango_profile_enable(1 if on else 0)
+
+
+def nvtx_enable(on: bool = True):
+    """NVTX range per library kernel launch (timeline tools); also TANGO_NVTX=1."""
+    load().tango_nvtx_enable(1 if on else 0)
 
 
 def profile_serialize(on: bool = True):

@@ -279,3 +279,15 @@ def test_spmm_q8_validation(T):
     qX = torch.zeros((gr.n, 12), dtype=torch.int8, device="cuda")
     with pytest.raises(T.TangoError):          # D = 6: a lane's 4 columns would straddle two heads
         T.spmm_q8(dg, 0, qa, s, qX, s, 12, 2)
+
+
+def test_nvtx_ranges_do_not_change_results(T, orc):
+    """Tracing: with NVTX ranges on (one per library launch) the kernels run unchanged."""
+    x = inputs.features(100, 64, seed=4)
+    T.nvtx_enable(True)
+    try:
+        q, s, _ = T.quantize(cu(x), bits=8, ld=64)
+    finally:
+        T.nvtx_enable(False)
+    oq, os_, _ = orc.quantize(x, bits=8)
+    assert np.array_equal(q.cpu().numpy(), oq) and s.item() == os_
