@@ -609,7 +609,7 @@ GatLayout gat_layout(const tango_graph* G, const tango_gat_params* p) {
   L.off_hcnt = take((size_t)L.n * 4);
   L.off_dapart = take((size_t)((L.n + 1023) / 1024 + 1) * 2 * L.HD * 4);
   L.off_nrec = take((size_t)L.N * gat2_nrec_stride((int)L.H) * 4);
-  L.off_ast = take((size_t)L.E * L.H * 4);
+  L.off_ast = take((size_t)L.E * L.H * 8);     // v6: F-agg's α [E][H], or P1's records [E][2H]
   L.total = o;
   return L;
 }
@@ -720,6 +720,17 @@ G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_p
     return (e && atoi(e)) ? 1 : 0;
   }();
   a.alpha_st = recompute ? nullptr : (float*)(c + L.off_ast);
+  // P1 writes a full-sector record {∂α, signed α} per edge at its in-CSR slot and P2 reads it coalesced
+  // (default for H = 4 / 8: 2H floats = whole 32-B sectors; TANGO_P2_REC=0 keeps the gather of ∂α)
+  static const int use_rec = [] {
+    const char* e = getenv("TANGO_P2_REC");
+    return e ? atoi(e) : 1;
+  }();
+  a.rec = nullptr;
+  if (use_rec && (p->heads == 4 || p->heads == 8) && !a.scatter_in) {
+    a.rec = (float*)(c + L.off_ast);
+    a.alpha_st = nullptr;
+  }
   a.codes_biased = 1;
   return a;
 }

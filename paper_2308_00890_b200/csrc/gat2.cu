@@ -156,6 +156,28 @@ __device__ __forceinline__ int8_t head_pick_i8(const int8_t (&x)[H], int h) {
   return r;
 }
 
+// P1's record of an edge at its in-CSR slot for P2: {∂α[H], α[H] with the LeakyReLU branch in its sign bit},
+// 2H floats = one full 32-B sector at H = 4 (no partial-sector read-modify-write in L2 / DRAM)
+template <int H>
+__device__ __forceinline__ void put_rec(float* rec, int64_t slot, const float (&dal)[H], const float* sa_lane,
+                                        uint32_t sg) {
+  float al[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    const float x = sa_lane[h * 32];
+    al[h] = (sg >> h) & 1u ? x : -x;
+  }
+  st_h<H>(rec + slot * 2 * H, dal);
+  st_h<H>(rec + slot * 2 * H + H, al);
+}
+template <int H>
+__device__ __forceinline__ uint32_t ep_sign_bits(const float (&ep)[H]) {
+  uint32_t sg = 0;
+#pragma unroll
+  for (int h = 0; h < H; ++h) sg |= (ep[h] > 0.0f ? 1u : 0u) << h;
+  return sg;
+}
+
 // α with the LeakyReLU branch in its sign bit (negative: e_pre <= 0), stored by F-agg for the destination
 // pass P2 (which then neither gathers q_S nor recomputes α); α >= 0, so |stored| = α exactly
 template <int H>
@@ -1062,15 +1084,17 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
       if (c * 32 + lane < T) x.r = load_rec_raw<H>(a, v);
       return x;
     };
-    auto attrs = [&](int c, int row, const AttrIn& x, float (&al)[H]) {
+    auto attrs = [&](int c, int row, const AttrIn& x, float (&al)[H], uint32_t& sg) {
       int8_t qs[H];
 #pragma unroll
       for (int h = 0; h < H; ++h) qs[h] = (int8_t)(tile ? __shfl_sync(0xffffffffu, qsj[h], row) : qsj[h]);
 #pragma unroll
       for (int h = 0; h < H; ++h) al[h] = 0.0f;
+      sg = 0;
       if (c * 32 + lane < T) {
         float ep[H];
         alpha_rec<H>(qs, rec_unpack<H>(x.r), scS.s, scD.s, a.slope, ep, al);
+        sg = ep_sign_bits<H>(ep);
       }
     };
     auto stash = [&](int c, int row, int64_t e, const float (&al)[H]) {
@@ -1082,6 +1106,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
     };
     const int nch = (T + 31) >> 5, ng = (T + GR - 1) / GR;
     int row1, v1 = 0;
+    uint32_t sg_cur = 0, sg_nxt = 0;   // LeakyReLU branch bits of the lane's edge of chunk c / c + 1
     int64_t e1;
     {
       int row0;
@@ -1089,7 +1114,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
       const int v0 = lane < T ? __ldcs(a.g.out_dst + e0) : 0;
       float al0[H];
       const AttrIn x0 = attr_load(0, v0, e0);
-      attrs(0, row0, x0, al0);
+      attrs(0, row0, x0, al0, sg_cur);
       stash(0, row0, e0, al0);
       sidx[lane] = v0;
       e1 = pos_of(1, row1);
@@ -1139,6 +1164,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
       const int v2 = (c + 2) * 32 + lane < T ? __ldcs(a.g.out_dst + e2) : 0;
       const AttrIn x1 = attr_load(c + 1, v1, e1);
       const int b = c & 1;
+      const int ein = (a.rec && c * 32 + lane < T) ? __ldcs(a.g.out_eid + seo[b * 32 + lane]) : 0;
       const float* sac = sa + (b * H + myh) * 32;
       for (int i0 = 0; i0 < 32; i0 += GR) {
         const int t0 = c * 32 + i0;
@@ -1195,12 +1221,14 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
         for (int h = 0; h < H; ++h) o[h] = sd[h * 32 + lane];
         st_h<H>(a.dal_out + (int64_t)seo[b * 32 + lane] * H, o);
         if (a.scatter_in) st_h<H>(a.dal_in + (int64_t)__ldcs(a.g.out_eid + seo[b * 32 + lane]) * H, o);
+        if (a.rec) put_rec<H>(a.rec, ein, o, sa + b * H * 32 + lane, sg_cur);
 
       }
       __syncwarp();
       if (c + 1 < nch) {
         float al1[H];
-        attrs(c + 1, row1, x1, al1);
+        attrs(c + 1, row1, x1, al1, sg_nxt);
+        sg_cur = sg_nxt;
         stash(c + 1, row1, e1, al1);
         sidx[b * 32 + lane] = v2;
       }
@@ -1291,12 +1319,14 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
 #pragma unroll
     for (int o = LPH / 2; o > 0; o >>= 1) osum_h += __shfl_xor_sync(0xffffffffu, osum_h, o);
     auto edge_v = [&](int c) -> int { return c * 32 + lane < T ? __ldcs(a.g.out_dst + eb + c * 32 + lane) : 0; };
-    auto alpha_of = [&](int c, const DstSm<H>& d, float (&al)[H]) {
+    auto alpha_of = [&](int c, const DstSm<H>& d, float (&al)[H], uint32_t& sg) {
 #pragma unroll
       for (int h = 0; h < H; ++h) al[h] = 0.0f;
+      sg = 0;
       if (c * 32 + lane < T) {
         float ep[H];
         alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+        sg = ep_sign_bits<H>(ep);
       }
     };
     auto stash = [&](int c, const float (&al)[H]) {
@@ -1306,12 +1336,13 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
     };
     const int nch = (T + 31) >> 5, ng = (T + GR - 1) / GR;
     int v1;
+    uint32_t sg_cur = 0, sg_nxt = 0;   // LeakyReLU branch bits of the lane's edge of chunk c / c + 1
     {
       const int v0 = edge_v(0);
       DstSm<H> d0;
       if (lane < T) d0 = load_rec<H>(a, v0);
       float al0[H];
-      alpha_of(0, d0, al0);
+      alpha_of(0, d0, al0, sg_cur);
       stash(0, al0);
       sidx[lane] = v0;
       v1 = edge_v(1);
@@ -1331,7 +1362,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
       RecRaw<H> r1;
       if ((c + 1) * 32 + lane < T) r1 = load_rec_raw<H>(a, v1);
       // in-CSR slot of this chunk's edge (scatter of ∂α), loaded here so the store at the chunk end does not wait
-      const int ein = (a.scatter_in && c * 32 + lane < T) ? __ldcs(a.g.out_eid + eb + c * 32 + lane) : 0;
+      const int ein = ((a.scatter_in || a.rec) && c * 32 + lane < T) ? __ldcs(a.g.out_eid + eb + c * 32 + lane) : 0;
       const float* sac = sa + ((c & 1) * H + myh) * 32;
       for (int i0 = 0; i0 < 32; i0 += GR) {
         const int t0 = c * 32 + i0;
@@ -1392,12 +1423,14 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
           st_h<H>(a.dal_out + (eb + c * 32 + lane) * H, o);
         }
         if (a.scatter_in) st_h<H>(a.dal_in + (int64_t)ein * H, o);
+        if (a.rec) put_rec<H>(a.rec, ein, o, sa + (c & 1) * H * 32 + lane, sg_cur);
       }
       __syncwarp();
       if (c + 1 < nch) {
         float al1[H];
         const DstSm<H> d1 = rec_unpack<H>(r1);
-        alpha_of(c + 1, d1, al1);
+        alpha_of(c + 1, d1, al1, sg_nxt);
+        sg_cur = sg_nxt;
         stash(c + 1, al1);
         sidx[(c & 1) * 32 + lane] = v2;
       }
@@ -1455,6 +1488,11 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
           s.eb, s.ee, sbx[w], sby[w],
           [&](int64_t e) {
             EdgeIn<H> l;
+            if (a.rec) {   // P1's record: ∂α and signed α at the in-CSR slot
+              ld_h<H>(a.rec + e * 2 * H, l.da);
+              ld_h<H>(a.rec + e * 2 * H + H, l.st);
+              return l;
+            }
             if (a.alpha_st) ld_h<H>(a.alpha_st + e * H, l.st);
             else load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs);
             if (a.scatter_in) {
@@ -1467,7 +1505,7 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
           },
           [&](const EdgeIn<H>& l, float (&x)[H], float (&y)[H]) {
             float ep[H];
-            if (a.alpha_st) alpha_from_st<H>(l.st, ep, y);
+            if (a.alpha_st || a.rec) alpha_from_st<H>(l.st, ep, y);
             else alpha_rec<H>(l.qs, d, scS.s, scD.s, a.slope, ep, y);
 #pragma unroll
             for (int h = 0; h < H; ++h) x[h] = l.da[h];
@@ -1504,7 +1542,12 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
         d.m[h] = __shfl_sync(0xffffffffu, dj.m[h], row);
         d.den[h] = __shfl_sync(0xffffffffu, dj.den[h], row);
       }
-      if (pos < t.T) {
+      if (pos < t.T && a.rec) {
+        float st[H];
+        ld_h<H>(a.rec + e * 2 * H, da);
+        ld_h<H>(a.rec + e * 2 * H + H, st);
+        alpha_from_st<H>(st, ep, al);
+      } else if (pos < t.T) {
         if (a.scatter_in) ld_h<H>(a.dal_in + e * H, da);
         else ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, da);
         if (a.alpha_st) {
@@ -1575,6 +1618,11 @@ __global__ void __launch_bounds__(256, 4) k2_bdst_b(const G2Args a) {
         s.eb, s.ee, sbx[w], nullptr,
         [&](int64_t e) {
           EdgeIn<H> l;
+          if (a.rec) {
+            ld_h<H>(a.rec + e * 2 * H, l.da);
+            ld_h<H>(a.rec + e * 2 * H + H, l.st);
+            return l;
+          }
           if (a.alpha_st) ld_h<H>(a.alpha_st + e * H, l.st);
           else load_qh<H>(a.qS + (int64_t)a.g.in_src[e] * H, l.qs);
           ld_h<H>(a.dal_in + e * H, l.da);
@@ -1582,7 +1630,7 @@ __global__ void __launch_bounds__(256, 4) k2_bdst_b(const G2Args a) {
         },
         [&](const EdgeIn<H>& l, float (&x)[H], float (&)[H]) {
           float ep[H], al[H];
-          if (a.alpha_st) alpha_from_st<H>(l.st, ep, al);
+          if (a.alpha_st || a.rec) alpha_from_st<H>(l.st, ep, al);
           else alpha_rec<H>(l.qs, d, scS.s, scD.s, a.slope, ep, al);
 #pragma unroll
           for (int h = 0; h < H; ++h) {
@@ -2103,13 +2151,20 @@ __global__ void __launch_bounds__(128, 6) k2_bdst_a_hubm(const G2Args a) {   // 
     const LaneSeg s = lane_seg<H>(first, hc, a.g.in_ptr, a.pin, a.g.chunk);
     const int64_t vg = a.g.row_begin + s.row;
     const float acc = seg_multi<H, true>(s, sbx[w], sby[w], [&](int rowt, int64_t e, float (&x)[H], float (&y)[H]) {
+      float ep[H];
+      if (a.rec) {
+        float st[H];
+        ld_h<H>(a.rec + e * 2 * H, x);
+        ld_h<H>(a.rec + e * 2 * H + H, st);
+        alpha_from_st<H>(st, ep, y);
+        return;
+      }
       if (a.scatter_in) {
         ld_h<H>(a.dal_in + e * H, x);
       } else {
         ld_h<H>(a.dal_out + (int64_t)__ldcs(a.in2out + e) * H, x);
         st_h<H>(a.dal_in + e * H, x);   // for P2b (coalesced)
       }
-      float ep[H];
       if (a.alpha_st) {
         float st[H];
         ld_h<H>(a.alpha_st + e * H, st);
@@ -2143,13 +2198,19 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_b_hubm(const G2Args a) {
     const float acc = seg_multi<H, false>(s, sbx[w], nullptr, [&](int rowt, int64_t e, float (&x)[H], float (&)[H]) {
       const int64_t rg = a.g.row_begin + rowt;
       float da[H], P[H], ep[H], al[H];
-      ld_h<H>(a.dal_in + e * H, da);
       ld_h<H>(a.P + rg * H, P);
-      if (a.alpha_st) {
+      if (a.rec) {
+        float st[H];
+        ld_h<H>(a.rec + e * 2 * H, da);
+        ld_h<H>(a.rec + e * 2 * H + H, st);
+        alpha_from_st<H>(st, ep, al);
+      } else if (a.alpha_st) {
+        ld_h<H>(a.dal_in + e * H, da);
         float st[H];
         ld_h<H>(a.alpha_st + e * H, st);
         alpha_from_st<H>(st, ep, al);
       } else {
+        ld_h<H>(a.dal_in + e * H, da);
         int8_t qs[H];
         load_qh<H>(a.qS + (int64_t)__ldg(a.g.in_src + e) * H, qs);
         alpha_rec<H>(qs, load_dst<H>(a, rg), scS.s, scD.s, a.slope, ep, al);

@@ -205,16 +205,18 @@ def test_layer_validation(T):
 
 def test_v6_variants_subprocess():
     """The v6 alternatives kept behind environment switches (read once per process): P1 scattering ∂α into
-    in-CSR order (TANGO_P2_SCATTER), the lane-parallel hub-segment kernels (TANGO_HUB_LANE) and P2
-    recomputing α instead of reading F-agg's stored α (TANGO_ALPHA_RECOMPUTE) — the dense v6 parity cases
-    in a fresh process per setting."""
+    in-CSR order (TANGO_P2_SCATTER), the lane-parallel / multi-segment hub kernels (TANGO_HUB_LANE 1 / 2),
+    P2 recomputing α instead of reading F-agg's stored α (TANGO_ALPHA_RECOMPUTE), and P2 gathering ∂α
+    instead of reading P1's {∂α, α} records (TANGO_P2_REC=0) — the dense v6 parity cases in a fresh
+    process per setting."""
     import os
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     for env in ({"TANGO_P2_SCATTER": "1", "TANGO_HUB_LANE": "1"}, {"TANGO_HUB_LANE": "1"}, {"TANGO_P2_SCATTER": "1"},
                 {"TANGO_ALPHA_RECOMPUTE": "1"}, {"TANGO_HUB_LANE": "2"}, {"TANGO_HUB_LANE": "2", "TANGO_P2_SCATTER": "1"},
-                {"TANGO_HUB_LANE": "2", "TANGO_ALPHA_RECOMPUTE": "1"}):
+                {"TANGO_HUB_LANE": "2", "TANGO_ALPHA_RECOMPUTE": "1"}, {"TANGO_P2_REC": "0"},
+                {"TANGO_P2_REC": "0", "TANGO_HUB_LANE": "2"}):
         r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_layer.py"), "-x", "-q",
                             "-k", "v6 and not variants"], env=dict(os.environ, **env), capture_output=True, text=True,
                            timeout=900)
