@@ -727,9 +727,11 @@ G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_p
     return e ? atoi(e) : 1;
   }();
   a.rec = nullptr;
+  a.al_out = nullptr;
   if (use_rec && (p->heads == 4 || p->heads == 8) && !a.scatter_in) {
     a.rec = (float*)(c + L.off_ast);
     a.alpha_st = nullptr;
+    a.al_out = a.dal_in;   // P1 also leaves its signed α in out-CSR order for P3 (dal_in is unused here)
   }
   a.codes_biased = 1;
   return a;

@@ -170,6 +170,17 @@ __device__ __forceinline__ void put_rec(float* rec, int64_t slot, const float (&
   st_h<H>(rec + slot * 2 * H, dal);
   st_h<H>(rec + slot * 2 * H + H, al);
 }
+// P1's signed α of an out-edge at its out-CSR position (for P3, coalesced)
+template <int H>
+__device__ __forceinline__ void put_alpha(float* dst, const float* sa_lane, uint32_t sg) {
+  float al[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    const float x = sa_lane[h * 32];
+    al[h] = (sg >> h) & 1u ? x : -x;
+  }
+  st_h<H>(dst, al);
+}
 template <int H>
 __device__ __forceinline__ uint32_t ep_sign_bits(const float (&ep)[H]) {
   uint32_t sg = 0;
@@ -1222,6 +1233,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
         st_h<H>(a.dal_out + (int64_t)seo[b * 32 + lane] * H, o);
         if (a.scatter_in) st_h<H>(a.dal_in + (int64_t)__ldcs(a.g.out_eid + seo[b * 32 + lane]) * H, o);
         if (a.rec) put_rec<H>(a.rec, ein, o, sa + b * H * 32 + lane, sg_cur);
+        if (a.al_out) put_alpha<H>(a.al_out + (int64_t)seo[b * 32 + lane] * H, sa + b * H * 32 + lane, sg_cur);
 
       }
       __syncwarp();
@@ -1424,6 +1436,7 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1_seg(const G2Args a)
         }
         if (a.scatter_in) st_h<H>(a.dal_in + (int64_t)ein * H, o);
         if (a.rec) put_rec<H>(a.rec, ein, o, sa + (c & 1) * H * 32 + lane, sg_cur);
+        if (a.al_out) put_alpha<H>(a.al_out + (eb + c * 32 + lane) * H, sa + (c & 1) * H * 32 + lane, sg_cur);
       }
       __syncwarp();
       if (c + 1 < nch) {
@@ -1676,7 +1689,7 @@ __device__ __forceinline__ void src_finalize_row(const G2Args& a, int64_t ul, co
 }
 
 template <int H>
-struct EdgeOut { int v; float da[H]; };
+struct EdgeOut { int64_t e; int v; float da[H]; };
 
 template <int H, int VPL>
 __global__ void __launch_bounds__(256, 3) k2_bsrc2(const G2Args a) {
@@ -1687,12 +1700,18 @@ __global__ void __launch_bounds__(256, 3) k2_bsrc2(const G2Args a) {
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t n = a.g.n_local, hc = load_count(a.pout.counts), nitems = hc + load_count(a.pout.counts + 2);
   float amax_loc = 0.0f;
-  // ∂E_pre of out-edge e' = (u → v) with u's q_S
-  auto dEp = [&](int v, const float (&da)[H], const int8_t (&qs)[H], float (&x)[H]) {
-    const DstSm<H> d = load_rec<H>(a, v);
+  // ∂E_pre of out-edge e' = (u → v) with u's q_S; α from P1's out-CSR copy (al_out, signed) when present
+  auto dEp = [&](int64_t e, int v, const float (&da)[H], const int8_t (&qs)[H], float (&x)[H]) {
     float ep[H], al[H], Pv[H];
     ld_h<H>(a.nrec + (int64_t)v * a.nrs + 2 * H, Pv);
-    alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+    if (a.al_out) {
+      float st[H];
+      ld_h<H>(a.al_out + e * H, st);
+      alpha_from_st<H>(st, ep, al);
+    } else {
+      const DstSm<H> d = load_rec<H>(a, v);
+      alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+    }
 #pragma unroll
     for (int h = 0; h < H; ++h) {
       const float dE = __fmul_rn(al[h], __fsub_rn(da[h], Pv[h]));
@@ -1710,11 +1729,12 @@ __global__ void __launch_bounds__(256, 3) k2_bsrc2(const G2Args a) {
           s.eb, s.ee, sbx[w], nullptr,
           [&](int64_t e) {
             EdgeOut<H> l;
+            l.e = e;
             l.v = a.g.out_dst[e];
             ld_h<H>(a.dal_out + e * H, l.da);
             return l;
           },
-          [&](const EdgeOut<H>& l, float (&x)[H], float (&)[H]) { dEp(l.v, l.da, qs, x); });
+          [&](const EdgeOut<H>& l, float (&x)[H], float (&)[H]) { dEp(l.e, l.v, l.da, qs, x); });
       if (lane < H) __stcg(a.hs + (int64_t)s.slot * H + lane, part);
       if (!seg_last(a.hcnt, s.vl, s.nseg)) continue;
       const float tot = seg_fold<H>(a.hs, s.base, s.nseg);
@@ -1747,7 +1767,7 @@ __global__ void __launch_bounds__(256, 3) k2_bsrc2(const G2Args a) {
       if (base + lane < t.T) {
         float da[H], x[H];
         ld_h<H>(a.dal_out + e * H, da);
-        dEp(a.g.out_dst[e], da, qs, x);
+        dEp(e, a.g.out_dst[e], da, qs, x);
 #pragma unroll
         for (int h = 0; h < H; ++h) tbx[lane][h] = x[h];
       }
@@ -1940,7 +1960,9 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a_hub(const G2Args a) {
           [&](int64_t e) {
             UDa x;
             x.u = __ldg(a.g.in_src + e);
-            if (a.scatter_in) {
+            if (a.rec) {
+              x.da = __ldcs(a.rec + e * 2 * H + h);
+            } else if (a.scatter_in) {
               x.da = __ldcs(a.dal_in + e * H + h);
             } else {
               x.da = a.dal_out[(int64_t)__ldg(a.in2out + e) * H + h];
@@ -1980,7 +2002,9 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_b_hub(const G2Args a) {
       float acc = 0.0f;
       lane_pipe<4, UDa, QDa>(
           s.eb, s.ee,
-          [&](int64_t e) { return UDa{(int)__ldg(a.g.in_src + e), __ldcs(a.dal_in + e * H + h)}; },
+          [&](int64_t e) {
+            return UDa{(int)__ldg(a.g.in_src + e), a.rec ? __ldcs(a.rec + e * 2 * H + h) : __ldcs(a.dal_in + e * H + h)};
+          },
           [&](const UDa& x, int64_t) { return QDa{(int)a.qS[(int64_t)x.u * H + h], x.da}; },
           [&](const QDa& y) {
             float ep;

@@ -171,6 +171,7 @@ struct G2Args {
   int lane_hubs;                                             // hub segments of F-stats / P2 / P3: lane per (segment, head)
   float* alpha_st;                                           // [E][H] α from F-agg, sign = LeakyReLU branch (nullable)
   float* rec;                                                // [E][2H] P1's {∂α, signed α} at in-CSR slots (nullable)
+  float* al_out;                                             // [E][H] P1's signed α in out-CSR order, for P3 (nullable)
   float* da_src; float* da_dst;                              // [HD]
   int codes_biased;
 };
