@@ -713,7 +713,13 @@ G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_p
     const char* e = getenv("TANGO_HUB_LANE");
     return e ? atoi(e) : 0;
   }();
-  a.lane_hubs = lane;   // 0: staged warp sums, 1: lane-pipelined, 2: multi-segment staged
+  static const int lane_p2 = [] {   // per-pass override for P2 (TANGO_HUB_P2)
+    const char* e = getenv("TANGO_HUB_P2");
+    return e ? atoi(e) : -1;
+  }();
+  a.hub_fs = lane;   // 0: staged warp sums, 1: lane-pipelined, 2: multi-segment staged
+  a.hub_p2 = lane_p2 >= 0 ? lane_p2 : lane;
+  a.hub_p3 = lane;
   // α stored by F-agg and read by P2 (default), or recomputed by P2 (TANGO_ALPHA_RECOMPUTE=1)
   static const int recompute = [] {
     const char* e = getenv("TANGO_ALPHA_RECOMPUTE");

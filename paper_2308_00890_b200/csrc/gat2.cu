@@ -167,8 +167,14 @@ __device__ __forceinline__ void put_rec(float* rec, int64_t slot, const float (&
     const float x = sa_lane[h * 32];
     al[h] = (sg >> h) & 1u ? x : -x;
   }
-  st_h<H>(rec + slot * 2 * H, dal);
-  st_h<H>(rec + slot * 2 * H + H, al);
+  if constexpr (H == 4) {   // one 256-bit store: the whole sector in one L2 write (no partial-sector fill)
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(rec + slot * 8), "f"(dal[0]), "f"(dal[1]),
+                 "f"(dal[2]), "f"(dal[3]), "f"(al[0]), "f"(al[1]), "f"(al[2]), "f"(al[3])
+                 : "memory");
+  } else {
+    st_h<H>(rec + slot * 2 * H, dal);
+    st_h<H>(rec + slot * 2 * H + H, al);
+  }
 }
 // P1's signed α of an out-edge at its out-CSR position (for P3, coalesced)
 template <int H>
@@ -413,8 +419,8 @@ __global__ void __launch_bounds__(256, 4) k2_fstats2(const G2Args a) {
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t n = a.g.n_local, hc = load_count(a.pin.counts), nitems = hc + load_count(a.pin.counts + 2);
-  FOR_ITEMS_FROM(item, a.work + 3, a.lane_hubs ? hc : 0, nitems) {
-    if (item < hc) {   // ---- hub segment (staged form; k2_fstats2_hub when lane_hubs)
+  FOR_ITEMS_FROM(item, a.work + 3, a.hub_fs ? hc : 0, nitems) {
+    if (item < hc) {   // ---- hub segment (staged form; k2_fstats2_hub(m) when hub_fs)
       Seg s;
       decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
       const int64_t vg = a.g.row_begin + s.vl;
@@ -1491,8 +1497,8 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t n = a.g.n_local, hc = load_count(a.pin.counts), nitems = hc + load_count(a.pin.counts + 2);
-  FOR_ITEMS_FROM(item, a.work + 3, a.lane_hubs ? hc : 0, nitems) {
-    if (item < hc) {   // ---- hub segment: P partial (staged form; k2_bdst_a_hub when lane_hubs)
+  FOR_ITEMS_FROM(item, a.work + 3, a.hub_p2 ? hc : 0, nitems) {
+    if (item < hc) {   // ---- hub segment: P partial (staged form; k2_bdst_a_hub(m) when hub_p2)
       Seg s;
       decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
       const int64_t vg = a.g.row_begin + s.vl;
@@ -1718,7 +1724,7 @@ __global__ void __launch_bounds__(256, 3) k2_bsrc2(const G2Args a) {
       x[h] = ep[h] > 0.0f ? dE : __fmul_rn(dE, a.slope);
     }
   };
-  FOR_ITEMS_FROM(item, a.work + 6, a.lane_hubs ? hc : 0, nitems) {
+  FOR_ITEMS_FROM(item, a.work + 6, a.hub_p3 ? hc : 0, nitems) {
     if (item < hc) {   // ---- hub segment: ∂S partial; the row's last segment folds and finalizes (staged form)
       Seg s;
       decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s);
@@ -2439,9 +2445,9 @@ cudaError_t launch_gat2_fwd(const G2Args& a, cudaStream_t st, const SideStream* 
       attr = true;                                                                                   \
     }                                                                                                \
     { ProfScope p("gat_fwd_stats1", st); k2_fstats1<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
-    if (a.lane_hubs) { /* hub segments on the side stream beside the light sub-tiles */                \
+    if (a.hub_fs) { /* hub segments on the side stream beside the light sub-tiles */                   \
       e = fork2(st, x);                                                                              \
-      { ProfScope p("gat_fwd_stats_hub", sh); if (a.lane_hubs == 2) k2_fstats2_hubm<H_><<<grid_items((a.pin.cap + 63) / 64, 3), 256, 0, sh>>>(a); else k2_fstats2_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
+      { ProfScope p("gat_fwd_stats_hub", sh); if (a.hub_fs == 2) k2_fstats2_hubm<H_><<<grid_items((a.pin.cap + 63) / 64, 3), 256, 0, sh>>>(a); else k2_fstats2_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
       { ProfScope p("gat_fwd_stats", st); k2_fstats2<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
       if (e == cudaSuccess) e = join2(st, x);                                                        \
     } else { ProfScope p("gat_fwd_stats", st); k2_fstats2<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
@@ -2477,19 +2483,22 @@ cudaError_t launch_gat2_bwd(const G2Args& a, cudaStream_t st, const SideStream* 
     { ProfScope p("gat_bwd_src_hub", sh); k2_bsrc1_seg<H_, V_, NW><<<grid_items((a.pout.cap + NW - 1) / NW, 20 / NW), NW * 32, smem_s, sh>>>(a); } \
     { ProfScope p("gat_bwd_src", st); k2_bsrc1<H_, V_, NW><<<grid_items((a.pout.tcap + NW - 1) / NW, 20 / NW), NW * 32, smem, st>>>(a); } \
     if (e == cudaSuccess) e = join2(st, x);                                                          \
-    if (a.lane_hubs) { /* hub segments on the side stream beside the light sub-tiles (P2a, P3) */        \
+    if (a.hub_p2) { /* P2 hub segments on the side stream beside the light sub-tiles */                \
       if (e == cudaSuccess) e = fork2(st, x);                                                        \
-      { ProfScope p("gat_bwd_dst_hub", sh); if (a.lane_hubs == 2) k2_bdst_a_hubm<H_><<<grid_items((a.pin.cap + 31) / 32, 6), 128, 0, sh>>>(a); else k2_bdst_a_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
+      { ProfScope p("gat_bwd_dst_hub", sh); if (a.hub_p2 == 2) k2_bdst_a_hubm<H_><<<grid_items((a.pin.cap + 31) / 32, 6), 128, 0, sh>>>(a); else k2_bdst_a_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
       { ProfScope p("gat_bwd_dst", st); k2_bdst_a<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
       if (e == cudaSuccess) e = join2(st, x);                                                        \
-      { ProfScope p("gat_bwd_dst2", st); if (a.lane_hubs == 2) k2_bdst_b_hubm<H_><<<grid_items((a.pin.cap + 63) / 64, 3), 256, 0, st>>>(a); else k2_bdst_b_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
-      if (e == cudaSuccess) e = fork2(st, x);                                                        \
-      { ProfScope p("gat_bwd_src2_hub", sh); if (a.lane_hubs == 2) k2_bsrc2_hubm<H_, V_><<<grid_items((a.pout.cap + 63) / 64, 3), 256, 0, sh>>>(a); else k2_bsrc2_hub<H_, V_><<<grid_items((a.pout.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
-      { ProfScope p("gat_bwd_src2", st); k2_bsrc2<H_, V_><<<grid_items((a.pout.cap + a.pout.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
-      if (e == cudaSuccess) e = join2(st, x);                                                        \
+      { ProfScope p("gat_bwd_dst2", st); if (a.hub_p2 == 2) k2_bdst_b_hubm<H_><<<grid_items((a.pin.cap + 63) / 64, 3), 256, 0, st>>>(a); else k2_bdst_b_hub<H_><<<grid_items((a.pin.cap + 63) / 64, 4), 256, 0, st>>>(a); } \
     } else {                                                                                         \
       { ProfScope p("gat_bwd_dst", st); k2_bdst_a<H_><<<grid_items((a.pin.cap + a.pin.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
       { ProfScope p("gat_bwd_dst2", st); k2_bdst_b<H_><<<grid_items((a.pin.cap + 7) / 8, 4), 256, 0, st>>>(a); } \
+    }                                                                                                \
+    if (a.hub_p3) { /* P3 hub segments on the side stream beside the light sub-tiles */                \
+      if (e == cudaSuccess) e = fork2(st, x);                                                        \
+      { ProfScope p("gat_bwd_src2_hub", sh); if (a.hub_p3 == 2) k2_bsrc2_hubm<H_, V_><<<grid_items((a.pout.cap + 63) / 64, 3), 256, 0, sh>>>(a); else k2_bsrc2_hub<H_, V_><<<grid_items((a.pout.cap + 63) / 64, 4), 256, 0, sh>>>(a); } \
+      { ProfScope p("gat_bwd_src2", st); k2_bsrc2<H_, V_><<<grid_items((a.pout.cap + a.pout.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
+      if (e == cudaSuccess) e = join2(st, x);                                                        \
+    } else {                                                                                         \
       { ProfScope p("gat_bwd_src2", st); k2_bsrc2<H_, V_><<<grid_items((a.pout.cap + a.pout.tcap + 7) / 8, 4), 256, 0, st>>>(a); } \
     }                                                                                                \
   }

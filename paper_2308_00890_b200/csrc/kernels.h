@@ -168,7 +168,8 @@ struct G2Args {
   float* nrec; int nrs;                                      // [N][nrs] packed per-node record: m | den | P | q_D
   const int32_t* in2out;                                     // [E] out-CSR position of each in-CSR edge
   int scatter_in;                                            // P1 also writes ∂α at its in-CSR slot (dal_in)
-  int lane_hubs;                                             // hub segments of F-stats / P2 / P3: lane per (segment, head)
+  int hub_fs, hub_p2, hub_p3;                                // hub segments of F-stats / P2 / P3: 0 staged warp sums,
+                                                             // 1 lane per (segment, head), 2 multi-segment staged
   float* alpha_st;                                           // [E][H] α from F-agg, sign = LeakyReLU branch (nullable)
   float* rec;                                                // [E][2H] P1's {∂α, signed α} at in-CSR slots (nullable)
   float* al_out;                                             // [E][H] P1's signed α in out-CSR order, for P3 (nullable)
