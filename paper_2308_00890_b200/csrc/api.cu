@@ -738,6 +738,8 @@ G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_p
     a.rec = (float*)(c + L.off_ast);
     a.alpha_st = nullptr;
     a.al_out = a.dal_in;   // P1 also leaves its signed α in out-CSR order for P3 (dal_in is unused here)
+    // P2 reading coalesced records: the multi-segment staged hub sums are the faster form (profiles/r3e_*)
+    if (lane_p2 < 0 && lane == 0) a.hub_p2 = 2;
   }
   a.codes_biased = 1;
   return a;
