@@ -460,15 +460,27 @@ tango_status tango_sddmm_q(const tango_graph* G, int32_t op, const tango_qtensor
   if (heads <= 0) return TANGO_ERR_SHAPE;
   const GraphDev g = dev_graph(G);
   if (Xsrc->rows != G->n_global || Xdst->rows < G->row_end) return TANGO_ERR_SHAPE;
+  // the warp-per-edge-run kernels of tango_sddmm_qn (int4.cu, bits = 8) compute the same values; the
+  // thread-per-(row, head) kernels remain for the shapes they do not take and for the acc_i32 test hook
   if (op == TANGO_SDDMM_ADD) {
     if (Xsrc->cols != heads || Xdst->cols != heads || Xsrc->ld != heads || Xdst->ld != heads) return TANGO_ERR_SHAPE;
     if (!out0 && !out1) return TANGO_ERR_INVALID_ARG;
+    if (out0 && Xsrc->bits == 8 && Xdst->bits == 8) {
+      const tango_status st = tango_sddmm_qn(G, op, 8, Xsrc->q, Xsrc->ld, Xsrc->scale, Xdst->q, Xdst->ld, Xdst->scale,
+                                             heads, heads, slope, out0, out1, stream);
+      if (st != TANGO_ERR_UNSUPPORTED) return st;
+    }
     return launch_status(launch_sddmm_add(g, heads, Xsrc->q, Xsrc->scale, Xdst->q, Xdst->scale, slope, out0, out1,
                                           stream));
   }
   if (op == TANGO_SDDMM_DOT) {
     if (Xsrc->cols != Xdst->cols || Xsrc->cols % heads) return TANGO_ERR_SHAPE;
     if (!out0 && !acc_i32) return TANGO_ERR_INVALID_ARG;
+    if (out0 && !acc_i32) {
+      const tango_status st = tango_sddmm_qn(G, op, 8, Xsrc->q, Xsrc->ld, Xsrc->scale, Xdst->q, Xdst->ld, Xdst->scale,
+                                             heads, (int32_t)Xsrc->cols, slope, out0, nullptr, stream);
+      if (st != TANGO_ERR_UNSUPPORTED) return st;
+    }
     return launch_status(launch_sddmm_dot(g, heads, (int)Xsrc->cols, Xdst->q, Xdst->ld, Xdst->scale, Xsrc->q,
                                           Xsrc->ld, Xsrc->scale, out0, acc_i32, stream));
   }
