@@ -7,7 +7,9 @@ python tools/ncu_to_traffic.py /tmp/ncu_final.ncu-rep reddit r3_final_reddit > g
 cp profiles/ncu_traffic.json gpurun_out/final/ncu_traffic.json
 python tools/ncu_summary.py /tmp/ncu_final.ncu-rep > gpurun_out/final/ncu_summary.txt 2>&1
 python tools/ncu_stalls.py /tmp/ncu_final.ncu-rep > gpurun_out/final/ncu_stalls.txt 2>&1
-cp /tmp/ncu_final.ncu-rep gpurun_out/final/
+ls -la /tmp/ncu_final.ncu-rep > gpurun_out/final/ncu_rep_size.txt   # the report stays on the box (64 MiB return limit)
+python tools/ncu_hot.py /tmp/ncu_final.ncu-rep k2_bsrc1_seg > gpurun_out/final/hot_bsrc1_seg.txt 2>&1
+python tools/ncu_hot.py /tmp/ncu_final.ncu-rep k2_fagg_seg > gpurun_out/final/hot_fagg_seg.txt 2>&1
 ( time timeout 1500 python bench.py > gpurun_out/final/bench.json 2> gpurun_out/final/bench.err ) 2> gpurun_out/final/bench_time.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1; echo rc=$? >> gpurun_out/final/smoke.log
 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/final/gpu_tests.log 2>&1; echo rc=$? >> gpurun_out/final/gpu_tests.log
