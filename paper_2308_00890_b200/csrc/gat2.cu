@@ -167,8 +167,9 @@ __device__ __forceinline__ void put_rec(float* rec, int64_t slot, const float (&
     const float x = sa_lane[h * 32];
     al[h] = (sg >> h) & 1u ? x : -x;
   }
-  if constexpr (H == 4) {   // one 256-bit store: the whole sector in one L2 write (no partial-sector fill)
-    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(rec + slot * 8), "f"(dal[0]), "f"(dal[1]),
+  if constexpr (H == 4) {   // one 256-bit streaming store: the whole sector in one L2 write (no partial-sector
+                            // fill), evict-first so the write streams do not push the gathered table out of L2
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(rec + slot * 8), "f"(dal[0]), "f"(dal[1]),
                  "f"(dal[2]), "f"(dal[3]), "f"(al[0]), "f"(al[1]), "f"(al[2]), "f"(al[3])
                  : "memory");
   } else {
@@ -176,7 +177,7 @@ __device__ __forceinline__ void put_rec(float* rec, int64_t slot, const float (&
     st_h<H>(rec + slot * 2 * H + H, al);
   }
 }
-// P1's signed α of an out-edge at its out-CSR position (for P3, coalesced)
+// P1's signed α of an out-edge at its out-CSR position (for P3, coalesced, streaming)
 template <int H>
 __device__ __forceinline__ void put_alpha(float* dst, const float* sa_lane, uint32_t sg) {
   float al[H];
@@ -185,7 +186,8 @@ __device__ __forceinline__ void put_alpha(float* dst, const float* sa_lane, uint
     const float x = sa_lane[h * 32];
     al[h] = (sg >> h) & 1u ? x : -x;
   }
-  st_h<H>(dst, al);
+  if constexpr (H == 4) __stcs(reinterpret_cast<float4*>(dst), make_float4(al[0], al[1], al[2], al[3]));
+  else st_h<H>(dst, al);
 }
 template <int H>
 __device__ __forceinline__ uint32_t ep_sign_bits(const float (&ep)[H]) {
@@ -1236,7 +1238,10 @@ __global__ void __launch_bounds__(NW * 32, 20 / NW) k2_bsrc1(const G2Args a) {
         float o[H];
 #pragma unroll
         for (int h = 0; h < H; ++h) o[h] = sd[h * 32 + lane];
-        st_h<H>(a.dal_out + (int64_t)seo[b * 32 + lane] * H, o);
+        if constexpr (H == 4)
+          __stcs(reinterpret_cast<float4*>(a.dal_out + (int64_t)seo[b * 32 + lane] * H), make_float4(o[0], o[1], o[2], o[3]));
+        else
+          st_h<H>(a.dal_out + (int64_t)seo[b * 32 + lane] * H, o);
         if (a.scatter_in) st_h<H>(a.dal_in + (int64_t)__ldcs(a.g.out_eid + seo[b * 32 + lane]) * H, o);
         if (a.rec) put_rec<H>(a.rec, ein, o, sa + b * H * 32 + lane, sg_cur);
         if (a.al_out) put_alpha<H>(a.al_out + (int64_t)seo[b * 32 + lane] * H, sa + b * H * 32 + lane, sg_cur);
