@@ -125,11 +125,12 @@ __device__ __forceinline__ void vadd(float (&acc)[VW], const typename VecF<VW>::
 }
 
 template <int DIR, int VW>
-__global__ void __launch_bounds__(ES_THREADS, 4) k_edge_sum_w(GraphDev g, int F, int64_t epb, int64_t E,
+__global__ void __launch_bounds__(ES_THREADS, 2) k_edge_sum_w(GraphDev g, int F, int64_t epb, int64_t E,
                                                           const float* __restrict__ x, float* __restrict__ out) {
   using V = typename VecF<VW>::T;
   extern __shared__ __align__(16) float es_part[];               // [slots + 1][F]
-  __shared__ int s_pre[ES_ROWS];                                 // inclusive prefix of chunk counts
+  __shared__ int s_pre[ES_ROWS];                                 // inclusive prefix of chunk counts (items)
+  __shared__ int s_slot[ES_ROWS];                                // inclusive prefix of partial slots
   const int64_t* __restrict__ ptr = DIR ? g.out_ptr : g.in_ptr;
   const int32_t* __restrict__ eid = g.out_eid;
   const int64_t n = g.n_local, C = g.chunk;
@@ -147,9 +148,9 @@ __global__ void __launch_bounds__(ES_THREADS, 4) k_edge_sum_w(GraphDev g, int F,
     return d <= C ? 1 : (d + C - 1) / C;
   };
   // sequential sum of list positions [pb, pe) (pe - pb <= C) for the lane's vector vi (columns VW·vi ..):
-  // 16 floats per lane in flight (U = 16 / VW records), then added in order
+  // 32 floats per lane in flight (U = 32 / VW records; 2 blocks per SM at 128 registers), then added in order
   auto chunk_sum = [&](int64_t pb, int64_t pe, int vi, float (&acc)[VW]) {
-    constexpr int U = 16 / VW;
+    constexpr int U = 32 / VW;
 #pragma unroll
     for (int k = 0; k < VW; ++k) acc[k] = 0.0f;
     for (int64_t p = pb; p < pe; p += U) {
@@ -175,18 +176,25 @@ __global__ void __launch_bounds__(ES_THREADS, 4) k_edge_sum_w(GraphDev g, int F,
   while (row < r1) {
     const int64_t rr = row + threadIdx.x;
     const int64_t c = (threadIdx.x < ES_ROWS && rr < r1) ? chunks(rr) : 0;
-    int v = (int)(c > slots ? slots + 1 : c);   // saturated: only the batch cut matters
+    // two prefixes over the batch's rows: items (chunks of every row) and partial slots (chunks of the
+    // multi-chunk rows only: a single-chunk row writes its output directly and needs no slot)
+    int v = (int)(c < (1 << 20) ? c : (1 << 20));
+    int ws = c > 1 ? (int)(c > slots ? slots + 1 : c) : 0;
     s_pre[threadIdx.x] = v;
+    s_slot[threadIdx.x] = ws;
     __syncthreads();
     for (int off = 1; off < ES_ROWS; off <<= 1) {
       const int add = threadIdx.x >= off ? s_pre[threadIdx.x - off] : 0;
+      const int adw = threadIdx.x >= off ? s_slot[threadIdx.x - off] : 0;
       __syncthreads();
       v += add;
+      ws += adw;
       s_pre[threadIdx.x] = v;
+      s_slot[threadIdx.x] = ws;
       __syncthreads();
     }
-    // rows of the batch: the prefix is non-decreasing, so the cut is a count
-    const int nb = __syncthreads_count(rr < r1 && v <= slots);
+    // rows of the batch: the slot prefix is non-decreasing, so the cut is a count
+    const int nb = __syncthreads_count(rr < r1 && ws <= slots);
     if (nb == 0) {
       // one row with more chunks than a batch: windows of `slots` chunks, folded in order
       const int64_t pb0 = ptr[row], pe0 = ptr[row + 1], nch = (pe0 - pb0 + C - 1) / C;
@@ -227,13 +235,14 @@ __global__ void __launch_bounds__(ES_THREADS, 4) k_edge_sum_w(GraphDev g, int F,
       if (!lane_ok || vi >= nv) continue;
       float acc[VW];
       chunk_sum(pb, pe, vi, acc);
-      put(pe0 - pb0 <= C ? out + r * F : es_part + it * F, vi, acc);   // single-chunk row: direct
+      const int slot = (j ? s_slot[j - 1] : 0) + k;
+      put(pe0 - pb0 <= C ? out + r * F : es_part + slot * F, vi, acc);   // single-chunk row: direct
     }
     __syncthreads();
     // fold the multi-chunk rows of the batch
     for (int t = threadIdx.x; t < nb * F; t += ES_THREADS) {
       const int j = t / F, h = t % F;
-      const int i0 = j ? s_pre[j - 1] : 0, i1 = s_pre[j];
+      const int i0 = j ? s_slot[j - 1] : 0, i1 = s_slot[j];
       if (i1 - i0 < 2) continue;
       float tot = es_part[i0 * F + h];
       for (int it = i0 + 1; it < i1; ++it) tot = __fadd_rn(tot, es_part[it * F + h]);
@@ -269,8 +278,8 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int head
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* su = reinterpret_cast<int*>(part + (sw_slots<V>() + 1) * SW_COLS) + wid * 32 * (1 + heads);   // [32] rows
   float* swt = reinterpret_cast<float*>(su + 32);                                           // [32][heads]
-  __shared__ int s_pre[ES_ROWS];
-  __shared__ int s_cnt;
+  __shared__ int s_pre[ES_ROWS];    // inclusive prefix of chunk counts (items)
+  __shared__ int s_slot[ES_ROWS];   // inclusive prefix of partial slots (multi-chunk rows)
   const int64_t* __restrict__ ptr = DIR ? g.out_ptr : g.in_ptr;
   const int32_t* __restrict__ nbr = DIR ? g.out_dst : g.in_src;
   const int64_t n = g.n_local, C = g.chunk;
@@ -351,24 +360,23 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int head
   while (row < r1) {
     const int64_t rr = row + threadIdx.x;
     const int64_t c = (threadIdx.x < ES_ROWS && rr < r1) ? chunks(rr) : 0;
-    int v = (int)(c > slots ? slots + 1 : c);
+    // items of every row, partial slots of the multi-chunk rows only (as in tango_edge_sum)
+    int v = (int)(c < (1 << 20) ? c : (1 << 20));
+    int ws = c > 1 ? (int)(c > slots ? slots + 1 : c) : 0;
     s_pre[threadIdx.x] = v;
+    s_slot[threadIdx.x] = ws;
     __syncthreads();
     for (int off = 1; off < ES_ROWS; off <<= 1) {
       const int add = threadIdx.x >= off ? s_pre[threadIdx.x - off] : 0;
+      const int adw = threadIdx.x >= off ? s_slot[threadIdx.x - off] : 0;
       __syncthreads();
       v += add;
+      ws += adw;
       s_pre[threadIdx.x] = v;
+      s_slot[threadIdx.x] = ws;
       __syncthreads();
     }
-    if (threadIdx.x == 0) {
-      int k = 0;
-      const int lim = (int)((r1 - row) < ES_ROWS ? (r1 - row) : ES_ROWS);
-      while (k < lim && s_pre[k] <= slots) ++k;
-      s_cnt = k;
-    }
-    __syncthreads();
-    const int nb = s_cnt;
+    const int nb = __syncthreads_count(rr < r1 && ws <= slots);
     if (nb == 0) {   // one row with more chunks than the partial slots: windows, folded in order
       const int64_t pb0 = ptr[row], pe0 = ptr[row + 1], nch = (pe0 - pb0 + C - 1) / C;
       float* wtot = part + (int64_t)slots * SW_COLS;   // running totals of the pass's columns
@@ -416,14 +424,15 @@ __global__ void __launch_bounds__(ES_THREADS) k_spmm_w_fast(GraphDev g, int head
           for (int q = 0; q < V; ++q)
             if (j0 + q < cols) finish(r, j0 + q, acc[q]);
         } else {
+          const int slot = (j ? s_slot[j - 1] : 0) + k;
 #pragma unroll
-          for (int q = 0; q < V; ++q) part[it * SW_COLS + lane * V + q] = acc[q];
+          for (int q = 0; q < V; ++q) part[slot * SW_COLS + lane * V + q] = acc[q];
         }
       }
       __syncthreads();
       for (int t = threadIdx.x; t < nb * SW_COLS; t += ES_THREADS) {
         const int jr = t / SW_COLS, col = cp * SW_COLS + t % SW_COLS;
-        const int i0 = jr ? s_pre[jr - 1] : 0, i1 = s_pre[jr];
+        const int i0 = jr ? s_slot[jr - 1] : 0, i1 = s_slot[jr];
         if (i1 - i0 < 2 || col >= cols) continue;
         float tot = part[i0 * SW_COLS + t % SW_COLS];
         for (int it = i0 + 1; it < i1; ++it) tot = __fadd_rn(tot, part[it * SW_COLS + t % SW_COLS]);
