@@ -791,7 +791,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="reddit", choices=sorted(inputs.WORKLOADS))
-    ap.add_argument("--extras", default="arxiv,sddmm,train",
+    ap.add_argument("--extras", default="arxiv,products,sddmm,train",
                     help="comma list of extra measurements at N = 1: arxiv, products (layer), train (NEXT-1 "
                          "steps), sddmm (NEXT-4), or none")
     ap.add_argument("--impl", default="tango", choices=["tango", "reference"])
