@@ -360,12 +360,12 @@ __global__ void __launch_bounds__(256, 4) k2_fstats1(const G2Args a) {
       uint32_t mw[NW];
 #pragma unroll
       for (int k = 0; k < NW; ++k) mw[k] = 0x80808080u;
-      for (int64_t b = s.eb; b < s.ee; b += 128) {
-        int u[4];
+      for (int64_t b = s.eb; b < s.ee; b += 256) {   // a whole C_E = 256 chunk per round trip pair
+        int u[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) u[k] = b + 32 * k + lane < s.ee ? __ldg(a.g.in_src + b + 32 * k + lane) : -1;
+        for (int k = 0; k < 8; ++k) u[k] = b + 32 * k + lane < s.ee ? __ldg(a.g.in_src + b + 32 * k + lane) : -1;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < 8; ++k)
           if (u[k] >= 0) {
             const int8_t* q = a.qS + (int64_t)u[k] * H;
             if constexpr (H == 1) mw[0] = __vmaxs4(mw[0], 0x80808000u | (uint32_t)(uint8_t)__ldg(q));
