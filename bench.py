@@ -5,7 +5,10 @@ through libtango.so on synthetic inputs shaped like the paper's datasets.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload reddit] [--impl tango|reference]
 
 Default workload: the Reddit-shaped layer of BASELINE.json configs[3] (the metric's 1-8 GPU config);
-the arxiv-shaped layer (configs[2]) is measured too and reported under "extra_workloads".
+the arxiv- and products-shaped layers (configs[2], configs[4] on one GPU) and the μ benchmarks of
+SURVEY.md §8(d) (incidence SPMM at edge-feature widths 4-20, int8 GEMM at D = 256/512 and 8192³, INT4
+SDDMM, multi-head SPMM incl. int8-α, training steps) are reported under "extra_workloads"
+(`--extras` selects them; `--layer-only` skips them).
 
 N > 1 is launched by torchrun: destination-row partitioning of ONE graph over N GPUs with NCCL
 (all-gather of int8 node rows, all-reduce of amax / ∂W / ∂a inside libtango) -> strong scaling.
