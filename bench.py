@@ -866,7 +866,7 @@ def main():
                         extra_out["sddmm_bits"] = sb
                 del x2
                 torch.cuda.empty_cache()
-        if "gemm" in extras or args.workload in ("reddit", "products"):
+        if "gemm" in extras or (extras and args.workload in ("reddit", "products")):
             extra_out["tensor"] = gemm_microbench(T, torch, 2.0 * peaks["bf16_tflops"])
 
     # ---------------- CPU baseline: the oracle as it stands, rank 0 at N = 1 only: the full workload with all
