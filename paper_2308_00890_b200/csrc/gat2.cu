@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(256, 4) k2_fstats1(const G2Args a) {
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t hc = load_count(a.pin.counts);
-  FOR_ITEMS(si, a.work + 0, hc) {
+  FOR_ITEMS4(si, a.work + 0, hc) {
     Seg s;
     decode_item(si, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
     const int64_t vg = a.g.row_begin + s.vl;
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(256, 4) k2_fstats2(const G2Args a) {
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t n = a.g.n_local, hc = load_count(a.pin.counts), nitems = hc + load_count(a.pin.counts + 2);
-  FOR_ITEMS_FROM(item, a.work + 3, a.hub_fs ? hc : 0, nitems) {
+  FOR_ITEMS_FROM4(item, a.work + 3, a.hub_fs ? hc : 0, nitems) {
     if (item < hc) {   // ---- hub segment (staged form; k2_fstats2_hub(m) when hub_fs)
       Seg s;
       decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
@@ -1502,7 +1502,7 @@ __global__ void __launch_bounds__(256, 3) k2_bdst_a(const G2Args a) {
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t n = a.g.n_local, hc = load_count(a.pin.counts), nitems = hc + load_count(a.pin.counts + 2);
-  FOR_ITEMS_FROM(item, a.work + 3, a.hub_p2 ? hc : 0, nitems) {
+  FOR_ITEMS_FROM4(item, a.work + 3, a.hub_p2 ? hc : 0, nitems) {
     if (item < hc) {   // ---- hub segment: P partial (staged form; k2_bdst_a_hub(m) when hub_p2)
       Seg s;
       decode_item(item, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
@@ -1631,7 +1631,7 @@ __global__ void __launch_bounds__(256, 4) k2_bdst_b(const G2Args a) {
   const Scale scS = scale_from_amax(amax_load(a.amax_S), a.bits);
   const Scale scD = scale_from_amax(amax_load(a.amax_D), a.bits);
   const int64_t hc = load_count(a.pin.counts);
-  FOR_ITEMS(si, a.work + 4, hc) {
+  FOR_ITEMS4(si, a.work + 4, hc) {
     Seg s;
     decode_item(si, hc, a.g.in_ptr, a.pin, a.g.chunk, s);
     const int64_t vg = a.g.row_begin + s.vl;
@@ -1729,7 +1729,7 @@ __global__ void __launch_bounds__(256, 3) k2_bsrc2(const G2Args a) {
       x[h] = ep[h] > 0.0f ? dE : __fmul_rn(dE, a.slope);
     }
   };
-  FOR_ITEMS_FROM(item, a.work + 6, a.hub_p3 ? hc : 0, nitems) {
+  FOR_ITEMS_FROM4(item, a.work + 6, a.hub_p3 ? hc : 0, nitems) {
     if (item < hc) {   // ---- hub segment: ∂S partial; the row's last segment folds and finalizes (staged form)
       Seg s;
       decode_item(item, hc, a.g.out_ptr, a.pout, a.g.chunk, s);

@@ -46,20 +46,25 @@ __device__ __forceinline__ int64_t claim(int32_t* counter) {
   if ((threadIdx.x & 31) == 0) it = atomicAdd(counter, 1);
   return (int64_t)__shfl_sync(0xffffffffu, it, 0);
 }
-// Items are claimed CLAIM_BATCH at a time: one same-address atomic per batch instead of per item (with
-// ~400 K hub segments per pass on Reddit-shaped graphs a per-item claim serialises on the counter).
+#define FOR_ITEMS(item, counter, nitems) for (int64_t item = claim(counter); item < (nitems); item = claim(counter))
+#define FOR_ITEMS_FROM(item, counter, start, nitems) \
+  for (int64_t item = (start) + claim(counter); item < (nitems); item = (start) + claim(counter))
+// Batched claims for work queues of many small, uniform items (the v6 scalar passes: ~400 K hub segments
+// per pass on Reddit-shaped graphs, where a per-item claim serialises on the counter's address): one
+// same-address atomic per CLAIM_BATCH items.  Queues whose consecutive items belong to one hub row (the
+// gather passes, the round-1 kernels) keep per-item claims so that a row's chunks spread over warps.
 constexpr int CLAIM_BATCH = 4;
 __device__ __forceinline__ int64_t claim_batch(int32_t* counter) {
   int it = 0;
   if ((threadIdx.x & 31) == 0) it = atomicAdd(counter, CLAIM_BATCH);
   return (int64_t)__shfl_sync(0xffffffffu, it, 0);
 }
-#define FOR_ITEMS(item, counter, nitems)                                                                   \
+#define FOR_ITEMS4(item, counter, nitems)                                                                  \
   for (int64_t item##_b = claim_batch(counter); item##_b < (nitems); item##_b = claim_batch(counter))     \
     for (int64_t item = item##_b, item##_e = item##_b + CLAIM_BATCH < (int64_t)(nitems) ? item##_b + CLAIM_BATCH \
                                                                                       : (int64_t)(nitems); \
          item < item##_e; ++item)
-#define FOR_ITEMS_FROM(item, counter, start, nitems)                                                       \
+#define FOR_ITEMS_FROM4(item, counter, start, nitems)                                                      \
   for (int64_t item##_b = (start) + claim_batch(counter); item##_b < (nitems);                            \
        item##_b = (start) + claim_batch(counter))                                                         \
     for (int64_t item = item##_b, item##_e = item##_b + CLAIM_BATCH < (int64_t)(nitems) ? item##_b + CLAIM_BATCH \
