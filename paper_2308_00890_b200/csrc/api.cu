@@ -731,7 +731,11 @@ G2Args g2_args(const GatLayout& L, char* c, const GraphDev& g, const tango_gat_p
   }();
   a.hub_fs = lane;   // 0: staged warp sums, 1: lane-pipelined, 2: multi-segment staged
   a.hub_p2 = lane_p2 >= 0 ? lane_p2 : lane;
-  a.hub_p3 = lane;
+  static const int lane_p3 = [] {   // per-pass override for P3 (TANGO_HUB_P3)
+    const char* e = getenv("TANGO_HUB_P3");
+    return e ? atoi(e) : -1;
+  }();
+  a.hub_p3 = lane_p3 >= 0 ? lane_p3 : lane;
   // α stored by F-agg and read by P2 (default), or recomputed by P2 (TANGO_ALPHA_RECOMPUTE=1)
   static const int recompute = [] {
     const char* e = getenv("TANGO_ALPHA_RECOMPUTE");

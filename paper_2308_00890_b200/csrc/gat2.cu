@@ -2274,14 +2274,19 @@ __global__ void __launch_bounds__(256, 3) k2_bsrc2_hubm(const G2Args a) {
     const LaneSeg s = lane_seg<H>(first, hc, a.g.out_ptr, a.pout, a.g.chunk);
     const int64_t ug = a.g.row_begin + s.row;
     const float acc = seg_multi<H, false>(s, sbx[w], nullptr, [&](int rowt, int64_t e, float (&x)[H], float (&)[H]) {
-      int8_t qs[H];
-      load_qh<H>(a.qS + (a.g.row_begin + rowt) * H, qs);
       const int v = __ldg(a.g.out_dst + e);
       float da[H], Pv[H], ep[H], al[H];
       ld_h<H>(a.dal_out + e * H, da);
-      const DstSm<H> d = load_rec<H>(a, v);
       ld_h<H>(a.nrec + (int64_t)v * a.nrs + 2 * H, Pv);
-      alpha_rec<H>(qs, d, scS.s, scD.s, a.slope, ep, al);
+      if (a.al_out) {   // P1's signed α in out-CSR order
+        float st[H];
+        ld_h<H>(a.al_out + e * H, st);
+        alpha_from_st<H>(st, ep, al);
+      } else {
+        int8_t qs[H];
+        load_qh<H>(a.qS + (a.g.row_begin + rowt) * H, qs);
+        alpha_rec<H>(qs, load_rec<H>(a, v), scS.s, scD.s, a.slope, ep, al);
+      }
 #pragma unroll
       for (int hh = 0; hh < H; ++hh) {
         const float dE = __fmul_rn(al[hh], __fsub_rn(da[hh], Pv[hh]));

@@ -216,7 +216,7 @@ def test_v6_variants_subprocess():
     for env in ({"TANGO_P2_SCATTER": "1", "TANGO_HUB_LANE": "1"}, {"TANGO_HUB_LANE": "1"}, {"TANGO_P2_SCATTER": "1"},
                 {"TANGO_ALPHA_RECOMPUTE": "1"}, {"TANGO_HUB_LANE": "2"}, {"TANGO_HUB_LANE": "2", "TANGO_P2_SCATTER": "1"},
                 {"TANGO_HUB_LANE": "2", "TANGO_ALPHA_RECOMPUTE": "1"}, {"TANGO_P2_REC": "0"},
-                {"TANGO_P2_REC": "0", "TANGO_HUB_LANE": "2"}, {"TANGO_HUB_P2": "0"}):
+                {"TANGO_P2_REC": "0", "TANGO_HUB_LANE": "2"}, {"TANGO_HUB_P2": "0"}, {"TANGO_HUB_P3": "2"}):
         r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_layer.py"), "-x", "-q",
                             "-k", "v6 and not variants"], env=dict(os.environ, **env), capture_output=True, text=True,
                            timeout=900)
