@@ -45,6 +45,7 @@ struct KParams {
   const unsigned* amax_in; int bits; PhiloxKey key; uint32_t step; uint32_t tag; int64_t g_row0;
   int8_t* q_out; int64_t ldq; float* scale_out; int32_t* status;
   void* C; int64_t ldc;
+  int c_pair;   // EPI_STORE: even ldc and 8-B aligned C -> float2 stores
 };
 
 // dequantized epilogue value: v = i2f(acc) * (s_A s_B) [* rowscale]  (two roundings)
@@ -276,17 +277,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           float* Cf = reinterpret_cast<float*>(p.C);
           float* tr = sm_tr + ew * (32 * TR_LD);
           const int64_t rowbase = (int64_t)mt * BM + sub * 32;
-          const int cl = lane & 15, rh = lane >> 4;
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) tr[lane * TR_LD + i] = deq(r[hf * 16 + i], sAB, has_rs, rs);
             __syncwarp();
-            const int64_t col = col0 + hf * 16 + cl;
+            if (p.c_pair) {   // 8-B aligned rows (even ldc, 8-B aligned C): float2 stores, 4 rows x 16 columns each
+              const int c2 = (lane & 7) * 2, rq = lane >> 3;
+              const int64_t col = col0 + hf * 16 + c2;
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              const int64_t rr = rowbase + j + rh;
-              if (rr < p.M && col < p.N) Cf[rr * p.ldc + col] = tr[(j + rh) * TR_LD + cl];
+              for (int j = 0; j < 32; j += 4) {
+                const int64_t rr = rowbase + j + rq;
+                const float x0 = tr[(j + rq) * TR_LD + c2], x1 = tr[(j + rq) * TR_LD + c2 + 1];
+                if (rr < p.M) {
+                  if (col + 1 < p.N) *reinterpret_cast<float2*>(Cf + rr * p.ldc + col) = make_float2(x0, x1);
+                  else if (col < p.N) Cf[rr * p.ldc + col] = x0;
+                }
+              }
+            } else {
+              const int cl = lane & 15, rh = lane >> 4;
+              const int64_t col = col0 + hf * 16 + cl;
+#pragma unroll
+              for (int j = 0; j < 32; j += 2) {
+                const int64_t rr = rowbase + j + rh;
+                if (rr < p.M && col < p.N) Cf[rr * p.ldc + col] = tr[(j + rh) * TR_LD + cl];
+              }
             }
             __syncwarp();
           }
@@ -430,6 +445,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
   p.amax_in = a.amax_in; p.bits = a.bits > 0 ? a.bits : 8; p.key = philox_key(a.seed); p.code_xor = a.code_xor; p.step = a.step; p.tag = a.tag;
   p.g_row0 = a.g_row0; p.q_out = a.q_out; p.ldq = a.ldq; p.scale_out = a.scale_out; p.status = a.status;
   p.C = a.C; p.ldc = a.ldc;
+  p.c_pair = (a.ldc % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.C) & 7) == 0);
 
   CUtensorMap tA, tB;
   bool ok;
